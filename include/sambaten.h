@@ -1,0 +1,227 @@
+/*
+ * sambaten.h -- C-ABI of the B200-native SamBaTen per-batch incremental CP update.
+ *
+ * Paper: Gujral, Pasricha, Papalexakis, "SamBaTen: Sampling-based Batch Incremental Tensor
+ * Decomposition", arXiv 1709.00668.  "P:n" below is line n of the paper's text;
+ * "Rn" is reading n in DESIGN.md section 2 (where the paper is silent or garbled).
+ *
+ * General conventions
+ *  - All functions return a sambaten_status; SAMBATEN_OK == 0.  The message of the last
+ *    failure on the calling thread is available from sambaten_last_error().
+ *  - A dense tensor X of dims (I, J, K) is a float32 array with X(i,j,k) at
+ *    vals[i + I*(j + J*k)]: i fastest, frontal slices X(:,:,k) contiguous.
+ *  - A sparse tensor is COO: int32 idx[0..2][n] (0-based i, j, k) and float32 vals[n].
+ *    Inputs to sambaten_init / sambaten_update must be canonical: sorted by (k, j, i),
+ *    without duplicates or explicit zeros (R28); violations return SAMBATEN_E_INVALID.
+ *  - Factor matrices are float32 row-major [rows][R] (R innermost); lambda is float32[R].
+ *  - Pointers passed to stateless primitives (sambaten_marginals ... sambaten_fit) are
+ *    DEVICE pointers unless stated otherwise; work is enqueued on `stream` (a cudaStream_t,
+ *    NULL = legacy default stream) and the call returns without synchronising.
+ *  - Handle-based calls accept host or device buffers for tensors and factors (the copy
+ *    direction is taken from the pointer; sambaten_tensor.on_device is advisory) and
+ *    synchronise their stream once before returning, so that they can report a status.
+ *  - Only sm_100a (B200) devices are supported.  There is no CPU fallback: without a
+ *    usable CUDA device every compute call returns SAMBATEN_E_CUDA.
+ *  - A handle is not thread-safe; distinct handles may be used from distinct threads.
+ */
+#ifndef SAMBATEN_H_
+#define SAMBATEN_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SAMBATEN_API __attribute__((visibility("default")))
+#else
+#define SAMBATEN_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sambaten_s* sambaten_t; /* opaque; owns the tensor store, model, workspaces */
+
+typedef enum {
+  SAMBATEN_OK = 0,
+  SAMBATEN_E_INVALID = -1,          /* bad argument (NULL, negative size, R > 32, ...)      */
+  SAMBATEN_E_SHAPE = -2,            /* I or J of a batch differs from the state's    */
+  SAMBATEN_E_DEGENERATE = -3,       /* all-zero initial tensor                      */
+  SAMBATEN_E_EMPTY_BATCH = -4,      /* batch with zero slices                       */
+  SAMBATEN_E_INDEX_RANGE = -5,      /* index outside its mode                        */
+  SAMBATEN_E_NUMERICAL = -6,        /* non-finite value in ALS                      */
+  SAMBATEN_E_BATCH_REJECTED = -7,   /* every repetition failed the acceptance test (R26)    */
+  SAMBATEN_E_FIXEDPOINT_RANGE = -8, /* batch value outside the fixed-point range (R7)       */
+  SAMBATEN_E_OOM = -9,              /* device allocation failed / capacity exceeded         */
+  SAMBATEN_E_CUDA = -10             /* CUDA runtime error (message has the CUDA string)     */
+} sambaten_status;
+
+enum { SAMBATEN_DENSE = 0, SAMBATEN_COO = 1 };
+enum { SAMBATEN_MOI_ABS = 0,  /* phi(x) = |x|  (BASELINE north_star, R1)   */
+       SAMBATEN_MOI_SQ = 1 }; /* phi(x) = x^2  (Eq. 1)         */
+
+typedef struct {
+  int fmt;                /* SAMBATEN_DENSE or SAMBATEN_COO                                 */
+  int64_t dims[3];        /* I, J, K (K = number of frontal slices in this tensor / batch)  */
+  const float* vals;      /* dense: I*J*K values (layout above); COO: nnz values            */
+  const int32_t* idx[3];  /* COO only: i, j, k coordinates (k relative to this tensor)      */
+  int64_t nnz;            /* COO only                                                       */
+  int on_device;          /* 1 if vals/idx are device pointers (advisory)                   */
+} sambaten_tensor;
+
+typedef struct {
+  int als_max_iters;      /* ALS iterations per summary (R11); default 30                     */
+  double als_tol;         /* stop when it >= 2 and |fit - fit_prev| < tol; 0 = fixed count   */
+  int moi;                /* SAMBATEN_MOI_ABS (default) or SAMBATEN_MOI_SQ (R1)              */
+  int s_mode[3];          /* per-mode sampling factor; 0 = use the `s` argument      */
+  int merge_policy;       /* 0 = update zero entries only (default); 1 = overwrite    */
+                          /*     the sampled rows (R17)                              */
+  double accept_tau;      /* rep acceptance threshold on min_f S(f, pi f) (R26); default 0.9 */
+  int full_fit;           /* 1: sambaten_update also computes the full relative error (a7)   */
+  int64_t capacity;       /* dense: total K slices to preallocate; COO: total nnz; 0 = 2x X0 */
+  int init_max_iters;     /* sambaten_init: ALS iterations on X0 (default 1000)       */
+  double init_tol;        /* sambaten_init: tolerance (default 1e-6)                         */
+  void* stream;           /* cudaStream_t for all work of this handle; NULL = default       */
+} sambaten_opts;
+
+typedef struct {
+  double fit_summary;          /* mean over repetitions of the summary ALS fit (R21)         */
+  double fit_full;             /* 1 - ||X - model||/||X|| over the whole tensor if full_fit,  */
+                               /* else -1                                         */
+  int als_iters_max;           /* largest ALS iteration count over repetitions               */
+  int64_t k_total;             /* slices (mode-3 extent) after the update                    */
+  uint32_t reps_rejected_mask; /* bit rho set if repetition rho was rejected (R26; r <= 32)  */
+  int scale_exp;               /* fixed-point exponent S of the marginals (R7)                */
+  int kernel_launches;         /* CUDA kernels this update launched (all are this library's) */
+  double step_ms[8];           /* device time of steps a0..a7 (CUDA events)                   */
+} sambaten_info;
+
+/* Fill *opts with the defaults listed above. */
+SAMBATEN_API void sambaten_default_opts(sambaten_opts* opts);
+
+/* ---------------------------------------------------------------------------------------
+ * Handle API: the incremental update of Problem 1 and Alg. 1.
+ * ------------------------------------------------------------------------------------- */
+
+/* Create a handle from the existing tensor X0 (I x J x K0) and decompose it with full
+ * CP-ALS at rank R (the "existing data"; Philox init R10, update_id 0).
+ * s: sampling factor for every mode unless opts->s_mode overrides it;
+ * r: repetitions per batch, 1 <= r <= 32; seed: Philox key (R6); 1 <= R <= 32.
+ * Errors: E_INVALID, E_DEGENERATE (all-zero X0), E_INDEX_RANGE, E_OOM, E_CUDA. On error
+ * *h is set to NULL. */
+SAMBATEN_API sambaten_status sambaten_init(sambaten_t* h, const sambaten_tensor* X0, int R, int s, int r,
+                              uint64_t seed, const sambaten_opts* opts);
+
+/* As sambaten_init, but the model [lambda; A, B, C] (float32, host or device; C has K0
+ * rows) is given instead of computed.  Used for parity tests and the throughput bench. */
+SAMBATEN_API sambaten_status sambaten_init_factors(sambaten_t* h, const sambaten_tensor* X0, int R, int s,
+                                      int r, uint64_t seed, const float* A, const float* B,
+                                      const float* C, const float* lambda,
+                                      const sambaten_opts* opts);
+
+/* One SamBaTen update with the batch X_new (I x J x K_new, K_new >= 1): steps a0..a7 of
+ * DESIGN.md (ingest, marginals, sampling, gather, batched CP-ALS, matching, merge, fit).
+ * On success the model has K_old + K_new rows of C.  If A, B, C, lambda are
+ * non-NULL the updated factors are copied there (host or device; C gets K_old+K_new rows).
+ * info may be NULL.  Strong guarantee: on any error the state is unchanged.
+ * Errors: E_INVALID, E_SHAPE, E_EMPTY_BATCH, E_INDEX_RANGE, E_FIXEDPOINT_RANGE,
+ * E_BATCH_REJECTED, E_NUMERICAL, E_OOM (capacity exceeded), E_CUDA. */
+SAMBATEN_API sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* batch, float* A, float* B,
+                                float* C, float* lambda, sambaten_info* info);
+
+/* Device pointers to the current model (valid until the next mutating call) and dims. */
+SAMBATEN_API sambaten_status sambaten_get_factors(sambaten_t h, const float** A, const float** B,
+                                     const float** C, const float** lambda, int64_t dims[3],
+                                     int* R);
+
+/* Sample sets of the last update, copied to caller (host or device) buffers of
+ * r * n_mode int32 each (rep-major): I_s, J_s, K_s (sorted, R9).  Any pointer may be NULL.
+ * n_out[3] receives n_I, n_J, n_Ks. */
+SAMBATEN_API sambaten_status sambaten_last_samples(sambaten_t h, int32_t* Is, int32_t* Js, int32_t* Ks,
+                                      int64_t n_out[3]);
+
+/* Full relative error ||X - [[lambda; A, B, C]]||_F / ||X||_F of the current model over the
+ * whole retained tensor. */
+SAMBATEN_API sambaten_status sambaten_relative_error(sambaten_t h, double* relerr);
+
+/* In-memory checkpoint of (model, K extent, update counter) and its restore; the tensor
+ * store is append-only, so restore discards slices appended after the checkpoint.
+ * Deterministic resume: Philox counters depend only on (seed, update_id, rep, mode, index). */
+SAMBATEN_API sambaten_status sambaten_checkpoint(sambaten_t h);
+SAMBATEN_API sambaten_status sambaten_restore(sambaten_t h);
+
+SAMBATEN_API void sambaten_destroy(sambaten_t h);
+
+/* ---------------------------------------------------------------------------------------
+ * Stateless primitives (device pointers, enqueue on `stream`, no synchronisation).
+ * ------------------------------------------------------------------------------------- */
+
+/* Fixed-point exponent S = 62 - ceil(log2 cap_entries) - ceil(log2 max_phi) - 8, clamped
+ * to [-60, 120] (R7).  Host-only arithmetic; max_phi must be > 0. */
+SAMBATEN_API int sambaten_fixed_point_scale(int64_t cap_entries, double max_phi);
+
+/* Measure of importance (Eq. 1; R1, R7): with q(x) = RNE(phi(x) * 2^S) in int64,
+ * x1[i] = sum_{j,k} q(X(i,j,k)), x2[j] = sum_{i,k} q, x3[k] = sum_{i,j} q, over the dense or
+ * COO tensor X (device).  x1, x2, x3: device int64 arrays of I, J, K entries, OVERWRITTEN.
+ * Exact and independent of launch configuration (integer sums). */
+SAMBATEN_API sambaten_status sambaten_marginals(const sambaten_tensor* X, int moi, int scale_exp,
+                                   int64_t* x1, int64_t* x2, int64_t* x3, void* stream);
+
+/* Importance sample without replacement (Alg. 1 line 3 P:211; R4-R6): the n_s
+ * smallest (key_i, i), key_i = -ln(u_i)/w[i] (+inf if w[i] == 0), u_i from Philox4x32-10
+ * with key = seed and counter (i, 0, update_id, 1<<24 | rep<<8 | mode), written sorted
+ * ascending to out_idx[0..n_s).  w: device int64[n]; 0 <= n_s <= n. */
+SAMBATEN_API sambaten_status sambaten_sample(const int64_t* w, int64_t n, int64_t n_s, uint64_t seed,
+                                uint32_t update_id, uint32_t rep, uint32_t mode,
+                                int32_t* out_idx, void* stream);
+
+/* Summary gather (Alg. 1 line 4 P:212): Y(p,q,u) = X(Is[p], Js[q], Ks[u]).
+ * Dense X: out_dense is float32 [nK][nJ][nI] (p fastest).  COO X: the entries whose three
+ * coordinates are sampled, relabelled to (p, q, u), in canonical (u, q, p) order, written
+ * to out_idx[0..2] / out_vals (capacity out_cap entries); *out_nnz (device int64) gets the
+ * count.  Index lists: device int32, sorted ascending, distinct. */
+SAMBATEN_API sambaten_status sambaten_gather(const sambaten_tensor* X, const int32_t* Is, int64_t nI,
+                                const int32_t* Js, int64_t nJ, const int32_t* Ks, int64_t nK,
+                                float* out_dense, int32_t* out_idx_i, int32_t* out_idx_j,
+                                int32_t* out_idx_k, float* out_vals, int64_t out_cap,
+                                int64_t* out_nnz, void* stream);
+
+/* MTTKRP: M = X_(mode) (Khatri-Rao product of the other two factors), i.e.
+ * M(i,f) = sum_{j,k} X(i,j,k) U1(j,f) U2(k,f) for mode 0 and likewise for modes 1, 2.
+ * U0, U1, U2: device float32 row-major [dims[m]][R] (the one of `mode` is ignored);
+ * M: device float32 [dims[mode]][R].  1 <= R <= 32.  fp32 products, fp64 partial sums. */
+SAMBATEN_API sambaten_status sambaten_mttkrp(const sambaten_tensor* X, const float* U0, const float* U1,
+                                const float* U2, int R, int mode, float* M, void* stream);
+
+/* CP-ALS on one tensor, starting from U0, U1, U2 (device float32, overwritten by
+ * the column-normalised result); lambda_out: device float64[R].  Iterations as in R11:
+ * modes 0,1,2 each: M = mttkrp, V = Hadamard of the other Grams, U = M V^-1 (Cholesky,
+ * pseudo-inverse fallback R12), lambda = column 2-norms, normalise.  fit_out: device
+ * float64[1], iters_out: device int32[1]. */
+SAMBATEN_API sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, float* U0, float* U1,
+                                float* U2, double* lambda_out, int max_iters, double tol,
+                                double* fit_out, int32_t* iters_out, void* stream);
+
+/* Relative error ||X - [[lambda; A, B, C]]||_F / ||X||_F of a dense or COO
+ * tensor X against a model (device float32); relerr: device float64[1]. */
+SAMBATEN_API sambaten_status sambaten_fit(const sambaten_tensor* X, const float* lambda, const float* A,
+                             const float* B, const float* C, int R, double* relerr,
+                             void* stream);
+
+/* Philox4x32-10 (R6) on device for the cross-check tests: out[4*t..4*t+3] = Philox(counter
+ * (c0 + t, c1, c2, c3), key) for t < n.  out: device uint32[4n]. */
+SAMBATEN_API sambaten_status sambaten_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                uint64_t key, int64_t n, uint32_t* out, void* stream);
+
+/* detlog (R7) on device: out[t] = detlog(u[t]) for u in (0,1). Device float64 arrays. */
+SAMBATEN_API sambaten_status sambaten_detlog(const double* u, int64_t n, double* out, void* stream);
+
+/* Message of the last failure on this thread ("" if none). */
+SAMBATEN_API const char* sambaten_last_error(void);
+
+/* Library version string. */
+SAMBATEN_API const char* sambaten_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SAMBATEN_H_ */

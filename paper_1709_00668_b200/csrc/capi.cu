@@ -1,0 +1,695 @@
+// capi.cu -- the C-ABI (include/sambaten.h) and the per-handle engine that sequences the
+// hot path a0..a7 on one CUDA stream.  Host code here only validates, sizes buffers and
+// launches; every step of the method runs in the kernels of k_*.cu.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/sambaten.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace sbt {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+}  // namespace sbt
+
+using namespace sbt;
+
+#define FAIL(code, msg)        \
+  do {                         \
+    sbt::set_error(msg);       \
+    return (code);             \
+  } while (0)
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess) {                                                  \
+      sbt::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));     \
+      return e_ == cudaErrorMemoryAllocation ? SAMBATEN_E_OOM : SAMBATEN_E_CUDA; \
+    }                                                                         \
+  } while (0)
+
+static int ceil_log2_d(double v) {
+  int e;
+  const double m = frexp(v, &e);
+  return m == 0.5 ? e - 1 : e;
+}
+
+// ---------------------------------------------------------------------------------------
+// device buffer helper
+// ---------------------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct HostStatus {        // pinned; filled by one D2H copy at the end of an update
+  unsigned long long maxphi_bits;
+  int accepted[kMaxReps];
+  int iters[kMaxReps];
+  int flags[kMaxReps];
+  double fit[kMaxReps];
+  double relerr;
+};
+
+struct sambaten_s {
+  int fmt = SAMBATEN_DENSE;
+  int64_t I = 0, J = 0, K = 0, Kcap = 0, pitch = 0;
+  int R = 0, r = 0, s[3] = {1, 1, 1};
+  uint64_t seed = 0;
+  uint32_t update_id = 0;
+  sambaten_opts opts;
+  cudaStream_t st = nullptr;
+  int S = 0, maxphi_log2 = 0;
+  // store and model
+  DevBuf X;
+  DevBuf model[2];          // A | B | C | lam, double-buffered (merge writes the shadow)
+  int cur = 0;
+  DevBuf ck;                // checkpoint of the model
+  int64_t K_ck = -1;
+  uint32_t uid_ck = 0;
+  // workspaces
+  DevBuf marg, samp, summ, fac, als, match, misc, segs;
+  SampleSeg* segs_host = nullptr;   // pinned
+  HostStatus* hs = nullptr;         // pinned
+  cudaEvent_t ev[9] = {};
+  // last sample sizes
+  int64_t last_n[3] = {0, 0, 0};
+  int64_t last_nKp = 0;
+
+  float* A(int b) const { return model[b].as<float>(); }
+  float* B(int b) const { return A(b) + I * R; }
+  float* C(int b) const { return B(b) + J * R; }
+  float* lam(int b) const { return C(b) + Kcap * R; }
+  size_t model_floats() const { return (size_t)(I + J + Kcap + 1) * R; }
+  DenseView view() const { return DenseView{X.as<float>(), I, J, K, pitch}; }
+};
+
+extern "C" {
+
+void sambaten_default_opts(sambaten_opts* o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->als_max_iters = 30;
+  o->als_tol = 1e-6;
+  o->moi = SAMBATEN_MOI_ABS;
+  o->merge_policy = 0;
+  o->accept_tau = 0.9;
+  o->full_fit = 0;
+  o->capacity = 0;
+  o->init_max_iters = 1000;
+  o->init_tol = 1e-6;
+  o->stream = nullptr;
+}
+
+const char* sambaten_last_error(void) { return sbt::g_err.c_str(); }
+const char* sambaten_version(void) { return "sambaten-b200 0.1 (sm_100a)"; }
+
+int sambaten_fixed_point_scale(int64_t cap_entries, double max_phi) {
+  if (!(max_phi > 0.0)) return 0;
+  int S = 62 - ceil_log2_d((double)std::max<int64_t>(cap_entries, 1)) - ceil_log2_d(max_phi) - 8;
+  return std::min(std::max(S, -60), 120);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------------------
+// validation helpers
+// ---------------------------------------------------------------------------------------
+static sambaten_status check_dense(const sambaten_tensor* X, const char* what) {
+  if (!X) FAIL(SAMBATEN_E_INVALID, std::string(what) + ": NULL tensor");
+  if (X->fmt != SAMBATEN_DENSE && X->fmt != SAMBATEN_COO)
+    FAIL(SAMBATEN_E_INVALID, std::string(what) + ": unknown format");
+  for (int m = 0; m < 3; ++m)
+    if (X->dims[m] < 0) FAIL(SAMBATEN_E_INVALID, std::string(what) + ": negative dimension");
+  if (X->fmt == SAMBATEN_DENSE && X->dims[0] * X->dims[1] * X->dims[2] > 0 && !X->vals)
+    FAIL(SAMBATEN_E_INVALID, std::string(what) + ": NULL values");
+  return SAMBATEN_OK;
+}
+
+static cudaStream_t stream_of(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------------------
+// handle creation
+// ---------------------------------------------------------------------------------------
+static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0, int R, int s,
+                                     int r, uint64_t seed, const sambaten_opts* opts) {
+  if (!out) FAIL(SAMBATEN_E_INVALID, "init: NULL handle pointer");
+  *out = nullptr;
+  if (sambaten_status st = check_dense(X0, "init")) return st;
+  if (X0->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "init: COO store not available in this build");
+  if (R < 1 || R > kMaxR) FAIL(SAMBATEN_E_INVALID, "init: R must be in [1, 32]");
+  if (r < 1 || r > kMaxReps) FAIL(SAMBATEN_E_INVALID, "init: r must be in [1, 32]");
+  if (s < 1) FAIL(SAMBATEN_E_INVALID, "init: s must be >= 1");
+  if (X0->dims[0] < 1 || X0->dims[1] < 1 || X0->dims[2] < 1)
+    FAIL(SAMBATEN_E_INVALID, "init: empty initial tensor");
+  int dev = 0;
+  cudaDeviceProp prop;
+  CK(cudaGetDevice(&dev));
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) FAIL(SAMBATEN_E_CUDA, "init: needs an sm_100 (B200) device");
+
+  auto* h = new sambaten_s();
+  if (opts) h->opts = *opts; else sambaten_default_opts(&h->opts);
+  h->fmt = X0->fmt;
+  h->I = X0->dims[0]; h->J = X0->dims[1]; h->K = X0->dims[2];
+  h->R = R; h->r = r; h->seed = seed; h->update_id = 0;
+  for (int m = 0; m < 3; ++m) h->s[m] = h->opts.s_mode[m] > 0 ? h->opts.s_mode[m] : s;
+  h->Kcap = h->opts.capacity > 0 ? h->opts.capacity : 2 * h->K;
+  if (h->Kcap < h->K) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity < K0"); }
+  h->st = stream_of(h->opts.stream);
+  h->pitch = (h->I + 3) & ~int64_t(3);
+  *out = h;
+  return SAMBATEN_OK;
+}
+
+static sambaten_status alloc_store_and_model(sambaten_s* h, const sambaten_tensor* X0) {
+  const size_t store = (size_t)h->Kcap * h->J * h->pitch * sizeof(float);
+  CK(h->X.ensure(store));
+  CK(cudaMemsetAsync(h->X.p, 0, store, h->st));
+  CK(cudaMemcpy2DAsync(h->X.p, h->pitch * sizeof(float), X0->vals, h->I * sizeof(float),
+                       h->I * sizeof(float), h->J * h->K, cudaMemcpyDefault, h->st));
+  for (int b = 0; b < 2; ++b) {
+    CK(h->model[b].ensure(h->model_floats() * sizeof(float)));
+    CK(cudaMemsetAsync(h->model[b].p, 0, h->model_floats() * sizeof(float), h->st));
+  }
+  CK(cudaMallocHost(&h->segs_host, sizeof(SampleSeg) * 3 * kMaxReps));
+  CK(cudaMallocHost(&h->hs, sizeof(HostStatus)));
+  for (int e = 0; e < 9; ++e) CK(cudaEventCreate(&h->ev[e]));
+  // fixed-point scale from X0 (R7)
+  CK(h->misc.ensure(4096));
+  CK(cudaMemsetAsync(h->misc.p, 0, 8, h->st));
+  CK(launch_max_phi_dense(h->view(), 0, h->K, h->opts.moi, h->misc.as<unsigned long long>(), h->st));
+  unsigned long long bits = 0;
+  CK(cudaMemcpyAsync(&bits, h->misc.p, 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  double maxphi;
+  memcpy(&maxphi, &bits, 8);
+  if (!(maxphi > 0.0)) FAIL(SAMBATEN_E_DEGENERATE, "init: all-zero initial tensor");
+  h->S = sambaten_fixed_point_scale(h->I * h->J * h->Kcap, maxphi);
+  h->maxphi_log2 = ceil_log2_d(maxphi);
+  return SAMBATEN_OK;
+}
+
+extern "C" void sambaten_destroy(sambaten_t h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->st);
+  h->X.release();
+  h->model[0].release(); h->model[1].release(); h->ck.release();
+  h->marg.release(); h->samp.release(); h->summ.release(); h->fac.release();
+  h->als.release(); h->match.release(); h->misc.release(); h->segs.release();
+  if (h->segs_host) cudaFreeHost(h->segs_host);
+  if (h->hs) cudaFreeHost(h->hs);
+  for (int e = 0; e < 9; ++e)
+    if (h->ev[e]) cudaEventDestroy(h->ev[e]);
+  delete h;
+}
+
+__global__ static void lam_to_f32_kernel(const double* l, int R, float* out) {
+  if (threadIdx.x < R) out[threadIdx.x] = (float)l[threadIdx.x];
+}
+
+extern "C" sambaten_status sambaten_init(sambaten_t* out, const sambaten_tensor* X0, int R, int s,
+                                         int r, uint64_t seed, const sambaten_opts* opts) {
+  if (sambaten_status e = create_common(out, X0, R, s, r, seed, opts)) return e;
+  sambaten_s* h = *out;
+  if (sambaten_status e = alloc_store_and_model(h, X0)) { sambaten_destroy(h); *out = nullptr; return e; }
+  // full CP-ALS on X0, r = 1, Philox init with update_id 0 (R10)
+  DenseAls a{};
+  a.Y = h->X.as<float>(); a.y_stride = 0; a.pitch = h->pitch;
+  a.nI = (int)h->I; a.nJ = (int)h->J; a.nK = (int)h->K; a.R = R; a.r = 1;
+  a.U[0] = h->A(h->cur); a.U[1] = h->B(h->cur); a.U[2] = h->C(h->cur);
+  a.u_stride[0] = a.u_stride[1] = a.u_stride[2] = 0;
+  a.maxit = h->opts.init_max_iters; a.tol = h->opts.init_tol;
+  DevBuf ws;
+  cudaError_t ce = ws.ensure(dense_als_workspace(&a));
+  if (ce == cudaSuccess) ce = dense_als_bind_workspace(&a, ws.p);
+  if (ce == cudaSuccess) ce = launch_als_init(a, seed, 0, 0, true, h->st);
+  if (ce == cudaSuccess) ce = run_dense_als(a, h->st);
+  if (ce == cudaSuccess) {
+    lam_to_f32_kernel<<<1, 32, 0, h->st>>>(a.lam, R, h->lam(h->cur));
+    ce = cudaStreamSynchronize(h->st);
+  }
+  ws.release();
+  if (ce != cudaSuccess) {
+    set_error(std::string("init ALS: ") + cudaGetErrorString(ce));
+    sambaten_destroy(h); *out = nullptr;
+    return ce == cudaErrorMemoryAllocation ? SAMBATEN_E_OOM : SAMBATEN_E_CUDA;
+  }
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_init_factors(sambaten_t* out, const sambaten_tensor* X0, int R,
+                                                 int s, int r, uint64_t seed, const float* A,
+                                                 const float* B, const float* C,
+                                                 const float* lambda, const sambaten_opts* opts) {
+  if (!A || !B || !C || !lambda) FAIL(SAMBATEN_E_INVALID, "init_factors: NULL factor");
+  if (sambaten_status e = create_common(out, X0, R, s, r, seed, opts)) return e;
+  sambaten_s* h = *out;
+  if (sambaten_status e = alloc_store_and_model(h, X0)) { sambaten_destroy(h); *out = nullptr; return e; }
+  const int b = h->cur;
+  cudaError_t ce = cudaMemcpyAsync(h->A(b), A, sizeof(float) * h->I * R, cudaMemcpyDefault, h->st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(h->B(b), B, sizeof(float) * h->J * R, cudaMemcpyDefault, h->st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(h->C(b), C, sizeof(float) * h->K * R, cudaMemcpyDefault, h->st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(h->lam(b), lambda, sizeof(float) * R, cudaMemcpyDefault, h->st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->st);
+  if (ce != cudaSuccess) {
+    set_error(std::string("init_factors: ") + cudaGetErrorString(ce));
+    sambaten_destroy(h); *out = nullptr;
+    return SAMBATEN_E_CUDA;
+  }
+  return SAMBATEN_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// the update (Alg. 1)
+// ---------------------------------------------------------------------------------------
+static inline int64_t sample_n(int64_t n, int s) { return std::min<int64_t>(n, (n + s - 1) / s); }
+
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* batch, float* Aout,
+                                           float* Bout, float* Cout, float* lamout,
+                                           sambaten_info* info) {
+  if (!h) FAIL(SAMBATEN_E_INVALID, "update: NULL handle");
+  if (sambaten_status e = check_dense(batch, "update")) return e;
+  if (batch->fmt != h->fmt) FAIL(SAMBATEN_E_INVALID, "update: batch format differs from the state's");
+  if (batch->dims[0] != h->I || batch->dims[1] != h->J)
+    FAIL(SAMBATEN_E_SHAPE, "update: batch I x J differs from the state's (S:68)");
+  const int64_t Kn = batch->dims[2];
+  if (Kn < 1) FAIL(SAMBATEN_E_EMPTY_BATCH, "update: empty batch (S:275)");
+  const int64_t Ko = h->K;
+  if (Ko + Kn > h->Kcap) FAIL(SAMBATEN_E_OOM, "update: capacity exceeded (opts.capacity)");
+  cudaStream_t st = h->st;
+  const int R = h->R, r = h->r;
+  const uint32_t uid = h->update_id + 1;
+  const int64_t nI = sample_n(h->I, h->s[0]), nJ = sample_n(h->J, h->s[1]);
+  const int64_t nKs = sample_n(Ko, h->s[2]), nKp = nKs + Kn;
+
+  CK(cudaEventRecord(h->ev[0], st));
+  // ---- a0: ingest into the preallocated capacity (not visible until commit) --------------
+  float* dst = h->X.as<float>() + Ko * h->J * h->pitch;
+  CK(cudaMemcpy2DAsync(dst, h->pitch * sizeof(float), batch->vals, h->I * sizeof(float),
+                       h->I * sizeof(float), h->J * Kn, cudaMemcpyDefault, st));
+  CK(h->misc.ensure(4096));
+  unsigned long long* d_maxphi = h->misc.as<unsigned long long>();
+  double* d_relerr = reinterpret_cast<double*>(h->misc.as<char>() + 64);
+  CK(cudaMemsetAsync(d_maxphi, 0, 8, st));
+  DenseView V = h->view();
+  V.K = Ko + Kn;
+  CK(launch_max_phi_dense(V, Ko, Kn, h->opts.moi, d_maxphi, st));
+  CK(cudaEventRecord(h->ev[1], st));
+  // ---- a1: marginals over X_old U X_new (R2, R3) ----------------------------------------
+  const size_t marg_bytes = sizeof(int64_t) * (h->I + h->J + h->Kcap);
+  CK(h->marg.ensure(marg_bytes));
+  int64_t* x1 = h->marg.as<int64_t>();
+  int64_t* x2 = x1 + h->I;
+  int64_t* x3 = x2 + h->J;
+  CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
+  CK(launch_marginals_dense(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, st));
+  CK(cudaEventRecord(h->ev[2], st));
+  // ---- a2: sampling (R4-R6); K_s from the old slices only, then K' = K_s ++ new ----------
+  const size_t is_b = align256(sizeof(int32_t) * r * nI), js_b = align256(sizeof(int32_t) * r * nJ);
+  const size_t kp_b = align256(sizeof(int32_t) * r * nKp);
+  const size_t li_b = align256(sizeof(int32_t) * r * h->I), lj_b = align256(sizeof(int32_t) * r * h->J);
+  const size_t lk_b = align256(sizeof(int32_t) * r * Ko);
+  const size_t key_b = align256(sizeof(uint64_t) * 3 * r * std::max(h->I, std::max(h->J, Ko)));
+  CK(h->samp.ensure(is_b + js_b + kp_b + li_b + lj_b + lk_b + key_b));
+  char* sp = h->samp.as<char>();
+  int32_t* Is = (int32_t*)sp; sp += is_b;
+  int32_t* Js = (int32_t*)sp; sp += js_b;
+  int32_t* Kp = (int32_t*)sp; sp += kp_b;
+  int32_t* locI = (int32_t*)sp; sp += li_b;
+  int32_t* locJ = (int32_t*)sp; sp += lj_b;
+  int32_t* locK = (int32_t*)sp; sp += lk_b;
+  uint64_t* keys = (uint64_t*)sp;
+  const int64_t kstride = std::max(h->I, std::max(h->J, Ko));
+  for (int rho = 0; rho < r; ++rho) {
+    for (int m = 0; m < 3; ++m) {
+      SampleSeg& g = h->segs_host[rho * 3 + m];
+      g.rep = rho; g.mode = m;
+      g.keys = keys + (int64_t)(rho * 3 + m) * kstride;
+      g.kp_tail = nullptr; g.tail0 = 0; g.ntail = 0;
+      if (m == 0) { g.w = x1; g.n = h->I; g.ns = nI; g.out = Is + rho * nI; g.loc = locI + rho * h->I; }
+      if (m == 1) { g.w = x2; g.n = h->J; g.ns = nJ; g.out = Js + rho * nJ; g.loc = locJ + rho * h->J; }
+      if (m == 2) {
+        g.w = x3; g.n = Ko; g.ns = nKs; g.out = Kp + rho * nKp; g.loc = locK + rho * Ko;
+        g.kp_tail = Kp + rho * nKp + nKs; g.tail0 = Ko; g.ntail = Kn;
+      }
+    }
+  }
+  CK(h->segs.ensure(sizeof(SampleSeg) * 3 * kMaxReps));
+  CK(cudaMemcpyAsync(h->segs.p, h->segs_host, sizeof(SampleSeg) * 3 * r, cudaMemcpyHostToDevice, st));
+  CK(launch_sample(h->segs.as<SampleSeg>(), 3 * r, h->seed, uid, st));
+  CK(cudaEventRecord(h->ev[3], st));
+  // ---- a3: gather the r summaries ------------------------------------------------------
+  const int64_t y_stride = nKp * nJ * nI;
+  CK(h->summ.ensure(sizeof(float) * r * y_stride));
+  float* Y = h->summ.as<float>();
+  CK(launch_gather_dense(V, Is, Js, Kp, (int)nI, (int)nJ, (int)nKp, r, nI, nJ, nKp, Y, y_stride, st));
+  CK(cudaEventRecord(h->ev[4], st));
+  // ---- a4: batched CP-ALS ---------------------------------------------------------------
+  const size_t u0 = align256(sizeof(float) * r * nI * R), u1 = align256(sizeof(float) * r * nJ * R);
+  const size_t u2 = align256(sizeof(float) * r * nKp * R);
+  CK(h->fac.ensure(u0 + u1 + u2));
+  DenseAls a{};
+  a.Y = Y; a.y_stride = y_stride; a.pitch = nI;
+  a.nI = (int)nI; a.nJ = (int)nJ; a.nK = (int)nKp; a.R = R; a.r = r;
+  a.U[0] = h->fac.as<float>();
+  a.U[1] = reinterpret_cast<float*>(h->fac.as<char>() + u0);
+  a.U[2] = reinterpret_cast<float*>(h->fac.as<char>() + u0 + u1);
+  a.u_stride[0] = nI * R; a.u_stride[1] = nJ * R; a.u_stride[2] = nKp * R;
+  a.maxit = h->opts.als_max_iters; a.tol = h->opts.als_tol;
+  CK(h->als.ensure(dense_als_workspace(&a)));
+  CK(dense_als_bind_workspace(&a, h->als.p));
+  CK(launch_als_init(a, h->seed, uid, 0, true, st));
+  CK(run_dense_als(a, st));
+  CK(cudaEventRecord(h->ev[5], st));
+  // ---- a5: match against the batch-start model (R13-R16, R26) ---------------------------
+  const int b = h->cur, nb = 1 - h->cur;
+  CK(h->match.ensure(align256(sizeof(int) * r * R) + align256(sizeof(double) * r * 3 * R) +
+                     align256(sizeof(double) * r * R) + align256(sizeof(double) * r) +
+                     align256(sizeof(int) * r)));
+  char* mp = h->match.as<char>();
+  MatchArgs ma{};
+  ma.A = h->A(b); ma.B = h->B(b); ma.C = h->C(b); ma.R = R; ma.r = r;
+  ma.Is = Is; ma.Js = Js; ma.Ks = Kp;
+  ma.nI = (int)nI; ma.nJ = (int)nJ; ma.nKs = (int)nKs; ma.nK = (int)nKp; ma.ks_stride = nKp;
+  for (int m = 0; m < 3; ++m) { ma.U[m] = a.U[m]; ma.u_stride[m] = a.u_stride[m]; }
+  ma.lamp = a.lam; ma.tau = h->opts.accept_tau;
+  ma.pi = (int*)mp; mp += align256(sizeof(int) * r * R);
+  ma.scale = (double*)mp; mp += align256(sizeof(double) * r * 3 * R);
+  ma.lam_hat = (double*)mp; mp += align256(sizeof(double) * r * R);
+  ma.score_min = (double*)mp; mp += align256(sizeof(double) * r);
+  ma.accepted = (int*)mp;
+  CK(launch_match(ma, st));
+  CK(cudaEventRecord(h->ev[6], st));
+  // ---- a6: merge into the shadow model --------------------------------------
+  CK(cudaMemcpyAsync(h->model[nb].p, h->model[b].p, h->model_floats() * sizeof(float),
+                     cudaMemcpyDeviceToDevice, st));
+  MergeArgs g{};
+  g.A = h->A(b); g.B = h->B(b); g.C = h->C(b); g.lam = h->lam(b);
+  g.An = h->A(nb); g.Bn = h->B(nb); g.Cn = h->C(nb); g.lamn = h->lam(nb);
+  g.I = h->I; g.J = h->J; g.Ko = Ko; g.Kn = Kn; g.R = R; g.r = r;
+  g.loc[0] = locI; g.loc[1] = locJ; g.loc[2] = locK; g.nKs = (int)nKs;
+  for (int m = 0; m < 3; ++m) { g.U[m] = a.U[m]; g.u_stride[m] = a.u_stride[m]; }
+  g.pi = ma.pi; g.scale = ma.scale; g.lam_hat = ma.lam_hat; g.accepted = ma.accepted;
+  g.policy = h->opts.merge_policy;
+  CK(launch_merge(g, st));
+  CK(cudaEventRecord(h->ev[7], st));
+  // ---- a7: full fit of the new model (optional) ------------------------------------------
+  if (h->opts.full_fit) {
+    DevBuf& fw = h->misc;
+    const size_t need = 128 + sizeof(double) * fit_dense_ws_doubles(V);
+    CK(fw.ensure(std::max<size_t>(4096, need)));
+    d_maxphi = fw.as<unsigned long long>();
+    d_relerr = reinterpret_cast<double*>(fw.as<char>() + 64);
+    CK(launch_fit_dense(V, h->lam(nb), h->A(nb), h->B(nb), h->C(nb), R,
+                        reinterpret_cast<double*>(fw.as<char>() + 128), d_relerr, st));
+  }
+  CK(cudaEventRecord(h->ev[8], st));
+  // ---- status readback and commit ------------------------------------------------------
+  HostStatus* hs = h->hs;
+  CK(cudaMemcpyAsync(&hs->maxphi_bits, d_maxphi, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs->accepted, ma.accepted, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs->iters, a.iters, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs->flags, a.flags, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs->fit, a.fit, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
+  if (h->opts.full_fit) CK(cudaMemcpyAsync(&hs->relerr, d_relerr, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double maxphi;
+  memcpy(&maxphi, &hs->maxphi_bits, 8);
+  if (maxphi > ldexp(1.0, h->maxphi_log2 + 8))
+    FAIL(SAMBATEN_E_FIXEDPOINT_RANGE, "update: batch value outside the fixed-point range (R7)");
+  uint32_t rejected = 0;
+  int nacc = 0, itmax = 0;
+  double fsum = 0.0;
+  for (int rho = 0; rho < r; ++rho) {
+    if (hs->accepted[rho]) ++nacc; else rejected |= 1u << rho;
+    itmax = std::max(itmax, hs->iters[rho]);
+    fsum += hs->fit[rho];
+  }
+  if (nacc == 0) FAIL(SAMBATEN_E_BATCH_REJECTED, "update: every repetition was rejected (R26)");
+  // commit
+  h->cur = nb;
+  h->K = Ko + Kn;
+  h->update_id = uid;
+  h->last_n[0] = nI; h->last_n[1] = nJ; h->last_n[2] = nKs; h->last_nKp = nKp;
+  if (info) {
+    info->fit_summary = fsum / r;
+    info->fit_full = h->opts.full_fit ? 1.0 - hs->relerr : -1.0;
+    info->als_iters_max = itmax;
+    info->k_total = h->K;
+    info->reps_rejected_mask = rejected;
+    info->scale_exp = h->S;
+    // max_phi, marginals, sample, gather, als_init + gram + 2 sumsq, 7 per ALS iteration
+    // (all iterations are launched; converged reps exit at once), match, 3 + 1 merge, 2 fit
+    info->kernel_launches = 1 + 1 + 1 + 1 + 4 + 7 * a.maxit + 1 + 4 + (h->opts.full_fit ? 2 : 0);
+    for (int e = 0; e < 8; ++e) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);
+      info->step_ms[e] = ms;
+    }
+  }
+  if (Aout) CK(cudaMemcpyAsync(Aout, h->A(nb), sizeof(float) * h->I * R, cudaMemcpyDefault, st));
+  if (Bout) CK(cudaMemcpyAsync(Bout, h->B(nb), sizeof(float) * h->J * R, cudaMemcpyDefault, st));
+  if (Cout) CK(cudaMemcpyAsync(Cout, h->C(nb), sizeof(float) * h->K * R, cudaMemcpyDefault, st));
+  if (lamout) CK(cudaMemcpyAsync(lamout, h->lam(nb), sizeof(float) * R, cudaMemcpyDefault, st));
+  if (Aout || Bout || Cout || lamout) CK(cudaStreamSynchronize(st));
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_get_factors(sambaten_t h, const float** A, const float** B,
+                                                const float** C, const float** lambda,
+                                                int64_t dims[3], int* R) {
+  if (!h) FAIL(SAMBATEN_E_INVALID, "get_factors: NULL handle");
+  if (A) *A = h->A(h->cur);
+  if (B) *B = h->B(h->cur);
+  if (C) *C = h->C(h->cur);
+  if (lambda) *lambda = h->lam(h->cur);
+  if (dims) { dims[0] = h->I; dims[1] = h->J; dims[2] = h->K; }
+  if (R) *R = h->R;
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_last_samples(sambaten_t h, int32_t* Is, int32_t* Js,
+                                                 int32_t* Ks, int64_t n_out[3]) {
+  if (!h) FAIL(SAMBATEN_E_INVALID, "last_samples: NULL handle");
+  if (h->update_id == 0) FAIL(SAMBATEN_E_INVALID, "last_samples: no update yet");
+  const int64_t nI = h->last_n[0], nJ = h->last_n[1], nKs = h->last_n[2], nKp = h->last_nKp;
+  const int r = h->r;
+  const size_t is_b = align256(sizeof(int32_t) * r * nI), js_b = align256(sizeof(int32_t) * r * nJ);
+  const char* sp = h->samp.as<char>();
+  if (Is) CK(cudaMemcpyAsync(Is, sp, sizeof(int32_t) * r * nI, cudaMemcpyDefault, h->st));
+  if (Js) CK(cudaMemcpyAsync(Js, sp + is_b, sizeof(int32_t) * r * nJ, cudaMemcpyDefault, h->st));
+  if (Ks)
+    CK(cudaMemcpy2DAsync(Ks, sizeof(int32_t) * nKs, sp + is_b + js_b, sizeof(int32_t) * nKp,
+                         sizeof(int32_t) * nKs, r, cudaMemcpyDefault, h->st));
+  if (n_out) { n_out[0] = nI; n_out[1] = nJ; n_out[2] = nKs; }
+  CK(cudaStreamSynchronize(h->st));
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_relative_error(sambaten_t h, double* relerr) {
+  if (!h || !relerr) FAIL(SAMBATEN_E_INVALID, "relative_error: NULL argument");
+  DenseView V = h->view();
+  DevBuf ws;
+  CK(ws.ensure(sizeof(double) * (fit_dense_ws_doubles(V) + 8)));
+  double* d = ws.as<double>();
+  CK(launch_fit_dense(V, h->lam(h->cur), h->A(h->cur), h->B(h->cur), h->C(h->cur), h->R, d + 8, d, h->st));
+  CK(cudaMemcpyAsync(relerr, d, 8, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  ws.release();
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_checkpoint(sambaten_t h) {
+  if (!h) FAIL(SAMBATEN_E_INVALID, "checkpoint: NULL handle");
+  CK(h->ck.ensure(h->model_floats() * sizeof(float)));
+  CK(cudaMemcpyAsync(h->ck.p, h->model[h->cur].p, h->model_floats() * sizeof(float),
+                     cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->K_ck = h->K;
+  h->uid_ck = h->update_id;
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_restore(sambaten_t h) {
+  if (!h) FAIL(SAMBATEN_E_INVALID, "restore: NULL handle");
+  if (h->K_ck < 0) FAIL(SAMBATEN_E_INVALID, "restore: no checkpoint");
+  CK(cudaMemcpyAsync(h->model[h->cur].p, h->ck.p, h->model_floats() * sizeof(float),
+                     cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  h->K = h->K_ck;
+  h->update_id = h->uid_ck;
+  return SAMBATEN_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// stateless primitives
+// ---------------------------------------------------------------------------------------
+static DenseView user_view(const sambaten_tensor* X) {
+  return DenseView{X->vals, X->dims[0], X->dims[1], X->dims[2], X->dims[0]};
+}
+
+extern "C" sambaten_status sambaten_marginals(const sambaten_tensor* X, int moi, int scale_exp,
+                                              int64_t* x1, int64_t* x2, int64_t* x3, void* stream) {
+  if (sambaten_status e = check_dense(X, "marginals")) return e;
+  if (!x1 || !x2 || !x3) FAIL(SAMBATEN_E_INVALID, "marginals: NULL output");
+  if (moi != 0 && moi != 1) FAIL(SAMBATEN_E_INVALID, "marginals: moi must be 0 or 1");
+  cudaStream_t st = stream_of(stream);
+  CK(cudaMemsetAsync(x1, 0, sizeof(int64_t) * X->dims[0], st));
+  CK(cudaMemsetAsync(x2, 0, sizeof(int64_t) * X->dims[1], st));
+  CK(cudaMemsetAsync(x3, 0, sizeof(int64_t) * X->dims[2], st));
+  if (X->fmt == SAMBATEN_DENSE) {
+    if (X->dims[0] > 4096) FAIL(SAMBATEN_E_INVALID, "marginals: dense I > 4096 not supported");
+    CK(launch_marginals_dense(user_view(X), 0, X->dims[2], moi, scale_exp, x1, x2, x3, st));
+  } else {
+    CK(launch_marginals_coo(X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, moi, scale_exp, x1,
+                            x2, x3, st));
+  }
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_sample(const int64_t* w, int64_t n, int64_t n_s, uint64_t seed,
+                                           uint32_t update_id, uint32_t rep, uint32_t mode,
+                                           int32_t* out_idx, void* stream) {
+  if (n < 0 || n_s < 0 || n_s > n) FAIL(SAMBATEN_E_INVALID, "sample: need 0 <= n_s <= n");
+  if (n > 0 && (!w || (n_s > 0 && !out_idx))) FAIL(SAMBATEN_E_INVALID, "sample: NULL pointer");
+  if (n >= (int64_t)1 << 31) FAIL(SAMBATEN_E_INVALID, "sample: n >= 2^31");
+  if (n == 0) return SAMBATEN_OK;
+  cudaStream_t st = stream_of(stream);
+  const size_t bytes = align256(sizeof(SampleSeg)) + sizeof(uint64_t) * n;
+  void* p = nullptr;
+  CK(cudaMallocAsync(&p, bytes, st));
+  SampleSeg g{};
+  g.w = w; g.n = n; g.ns = n_s; g.out = out_idx; g.loc = nullptr;
+  g.keys = reinterpret_cast<uint64_t*>(static_cast<char*>(p) + align256(sizeof(SampleSeg)));
+  g.rep = rep; g.mode = mode; g.kp_tail = nullptr; g.tail0 = 0; g.ntail = 0;
+  CK(cudaMemcpyAsync(p, &g, sizeof(g), cudaMemcpyHostToDevice, st));
+  CK(launch_sample(static_cast<SampleSeg*>(p), 1, seed, update_id, st));
+  CK(cudaStreamSynchronize(st));   // g lives on this stack frame
+  CK(cudaFreeAsync(p, st));
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_gather(const sambaten_tensor* X, const int32_t* Is, int64_t nI,
+                                           const int32_t* Js, int64_t nJ, const int32_t* Ks,
+                                           int64_t nK, float* out_dense, int32_t* oi, int32_t* oj,
+                                           int32_t* ok, float* ov, int64_t out_cap,
+                                           int64_t* out_nnz, void* stream) {
+  if (sambaten_status e = check_dense(X, "gather")) return e;
+  if (nI < 0 || nJ < 0 || nK < 0) FAIL(SAMBATEN_E_INVALID, "gather: negative size");
+  cudaStream_t st = stream_of(stream);
+  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "gather: COO gather not available in this build");
+  if (!out_dense) FAIL(SAMBATEN_E_INVALID, "gather: NULL output");
+  CK(launch_gather_dense(user_view(X), Is, Js, Ks, (int)nI, (int)nJ, (int)nK, 1, nI, nJ, nK,
+                         out_dense, nK * nJ * nI, st));
+  (void)oi; (void)oj; (void)ok; (void)ov; (void)out_cap; (void)out_nnz;
+  return SAMBATEN_OK;
+}
+
+static sambaten_status single_als_setup(const sambaten_tensor* X, int R, float* U0, float* U1,
+                                        float* U2, DenseAls* a) {
+  if (sambaten_status e = check_dense(X, "mttkrp/cp_als")) return e;
+  if (R < 1 || R > kMaxR) FAIL(SAMBATEN_E_INVALID, "R must be in [1, 32]");
+  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "COO MTTKRP not available in this build");
+  *a = DenseAls{};
+  a->Y = X->vals; a->y_stride = 0; a->pitch = X->dims[0];
+  a->nI = (int)X->dims[0]; a->nJ = (int)X->dims[1]; a->nK = (int)X->dims[2]; a->R = R; a->r = 1;
+  a->U[0] = U0; a->U[1] = U1; a->U[2] = U2;
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_mttkrp(const sambaten_tensor* X, const float* U0, const float* U1,
+                                           const float* U2, int R, int mode, float* M, void* stream) {
+  if (mode < 0 || mode > 2) FAIL(SAMBATEN_E_INVALID, "mttkrp: mode must be 0, 1 or 2");
+  if (!M) FAIL(SAMBATEN_E_INVALID, "mttkrp: NULL output");
+  DenseAls a;
+  if (sambaten_status e = single_als_setup(X, R, (float*)U0, (float*)U1, (float*)U2, &a)) return e;
+  cudaStream_t st = stream_of(stream);
+  void* ws = nullptr;
+  CK(cudaMallocAsync(&ws, dense_als_workspace(&a), st));
+  CK(dense_als_bind_workspace(&a, ws));
+  CK(dense_mttkrp_single(a, mode, M, st));
+  CK(cudaFreeAsync(ws, st));
+  return SAMBATEN_OK;
+}
+
+__global__ static void copy_als_out_kernel(const double* lam, const double* fit, const int* iters,
+                                           int R, double* lam_out, double* fit_out, int* iters_out) {
+  if (threadIdx.x < R && lam_out) lam_out[threadIdx.x] = lam[threadIdx.x];
+  if (threadIdx.x == 0) {
+    if (fit_out) *fit_out = *fit;
+    if (iters_out) *iters_out = *iters;
+  }
+}
+
+extern "C" sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, float* U0, float* U1,
+                                           float* U2, double* lambda_out, int max_iters, double tol,
+                                           double* fit_out, int32_t* iters_out, void* stream) {
+  if (max_iters < 1) FAIL(SAMBATEN_E_INVALID, "cp_als: max_iters >= 1");
+  DenseAls a;
+  if (sambaten_status e = single_als_setup(X, R, U0, U1, U2, &a)) return e;
+  a.maxit = max_iters; a.tol = tol;
+  cudaStream_t st = stream_of(stream);
+  void* ws = nullptr;
+  CK(cudaMallocAsync(&ws, dense_als_workspace(&a), st));
+  CK(dense_als_bind_workspace(&a, ws));
+  CK(launch_als_init(a, 0, 0, 0, false, st));
+  CK(run_dense_als(a, st));
+  copy_als_out_kernel<<<1, 32, 0, st>>>(a.lam, a.fit, a.iters, R, lambda_out, fit_out, iters_out);
+  CK(cudaGetLastError());
+  CK(cudaFreeAsync(ws, st));
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_fit(const sambaten_tensor* X, const float* lambda, const float* A,
+                                        const float* B, const float* C, int R, double* relerr,
+                                        void* stream) {
+  if (sambaten_status e = check_dense(X, "fit")) return e;
+  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "fit: COO fit not available in this build");
+  if (R < 1 || R > kMaxR || !relerr) FAIL(SAMBATEN_E_INVALID, "fit: bad argument");
+  cudaStream_t st = stream_of(stream);
+  const DenseView V = user_view(X);
+  void* ws = nullptr;
+  CK(cudaMallocAsync(&ws, sizeof(double) * fit_dense_ws_doubles(V), st));
+  CK(launch_fit_dense(V, lambda, A, B, C, R, static_cast<double*>(ws), relerr, st));
+  CK(cudaFreeAsync(ws, st));
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                           uint64_t key, int64_t n, uint32_t* out, void* stream) {
+  if (n < 0 || (n > 0 && !out)) FAIL(SAMBATEN_E_INVALID, "philox: bad argument");
+  CK(launch_philox(c0, c1, c2, c3, key, n, out, stream_of(stream)));
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_detlog(const double* u, int64_t n, double* out, void* stream) {
+  if (n < 0 || (n > 0 && (!u || !out))) FAIL(SAMBATEN_E_INVALID, "detlog: bad argument");
+  CK(launch_detlog(u, n, out, stream_of(stream)));
+  return SAMBATEN_OK;
+}

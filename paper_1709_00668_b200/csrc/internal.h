@@ -1,0 +1,134 @@
+// internal.h -- launchers shared between the kernel translation units and the engine.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+namespace sbt {
+
+// ---- errors ---------------------------------------------------------------------------
+void set_error(const std::string& msg);
+#define SBT_CUDA(call)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      ::sbt::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));            \
+      return SAMBATEN_E_CUDA;                                                          \
+    }                                                                                  \
+  } while (0)
+
+// ---- dense tensor view: X(i,j,k) at base[(k*J + j)*pitch + i] ---------------------------
+struct DenseView {
+  const float* base;
+  int64_t I, J, K;
+  int64_t pitch;
+};
+
+// a1: marginals over slices [k0, k0+nk) of a dense view; x1/x2/x3 (x3 indexed by absolute
+// k) are accumulated with integer atomics (callers zero them first).
+cudaError_t launch_marginals_dense(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
+                                   int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st);
+cudaError_t launch_marginals_coo(const int32_t* i, const int32_t* j, const int32_t* k,
+                                 const float* v, int64_t nnz, int moi, int S, int64_t* x1,
+                                 int64_t* x2, int64_t* x3, cudaStream_t st);
+// max phi over a dense view (slices [k0,k0+nk)) or COO values; result as double bits in
+// *out (callers zero it; phi >= 0 so the bit pattern is monotone).
+cudaError_t launch_max_phi_dense(const DenseView& X, int64_t k0, int64_t nk, int moi,
+                                 unsigned long long* out, cudaStream_t st);
+cudaError_t launch_max_phi_vals(const float* v, int64_t n, int moi, unsigned long long* out,
+                                cudaStream_t st);
+
+// a2: one block per (rep, mode) segment.
+struct SampleSeg {
+  const int64_t* w;   // weights (device)
+  int64_t n;          // population size
+  int64_t ns;         // sample size
+  int32_t* out;       // sorted sample (device, ns entries)
+  int32_t* loc;       // optional local-index map [n]: position in out or -1 (may be null)
+  uint64_t* keys;     // workspace [n]
+  uint32_t rep, mode;
+  int32_t* kp_tail;   // optional: write kp_tail[t] = tail0 + t after out (t < ntail)
+  int64_t tail0, ntail;
+};
+cudaError_t launch_sample(const SampleSeg* segs_dev, int nseg, uint64_t seed, uint32_t update_id,
+                          cudaStream_t st);
+
+// a3 dense: Y[rep][u][q][p] = X(Is[rep][p], Js[rep][q], Kp[rep][u]) ; Y pitch = nI.
+// ysq_part (optional) [rep][gridDim.x] gets per-block sums of squares (fp64).
+cudaError_t launch_gather_dense(const DenseView& X, const int32_t* Is, const int32_t* Js,
+                                const int32_t* Kp, int nI, int nJ, int nK, int r,
+                                int64_t idx_stride_I, int64_t idx_stride_J, int64_t idx_stride_K,
+                                float* Y, int64_t y_stride, cudaStream_t st);
+
+// ---- dense batched CP-ALS -------------------------------------------------------------
+struct DenseAls {
+  const float* Y;  int64_t y_stride;   // [r][nK][nJ][pitch]
+  int64_t pitch;
+  int nI, nJ, nK, R, r;
+  float* U[3]; int64_t u_stride[3];    // [r][n_m][R]
+  double* G;       // [r][3][R][R]
+  double* lam;     // [r][R]
+  double* ysq;     // [r]
+  double* fit;     // [r]
+  double* fit_prev;// [r]
+  int* iters;      // [r]
+  int* done;       // [r]
+  int* flags;      // [r]: bit0 pinv used, bit1 non-finite
+  double* part0;   int nb0;  int64_t rows_per_block0;   // [r][nb0][nI][R]
+  float* D;                            // [r][nK][nJ][R]
+  double* M;       int64_t m_stride;   // [r][max n][R]
+  double* Uscr;                        // [r][max n][R]
+  int maxit; double tol;
+};
+// ws sizes for a given problem (bytes); fills nb0/rows_per_block0 in *a.
+size_t dense_als_workspace(DenseAls* a);
+cudaError_t dense_als_bind_workspace(DenseAls* a, void* ws);
+cudaError_t launch_als_init(const DenseAls& a, uint64_t seed, uint32_t update_id,
+                            uint32_t rep0, bool init_factors, cudaStream_t st);
+cudaError_t launch_sumsq_dense(const float* Y, int64_t y_stride, int64_t rows, int64_t pitch,
+                               int64_t ncols, int r, double* out, cudaStream_t st);
+cudaError_t run_dense_als(const DenseAls& a, cudaStream_t st);
+// single-mode MTTKRP for the stateless API (r = 1): M (fp32 [n_mode][R])
+cudaError_t dense_mttkrp_single(const DenseAls& a, int mode, float* M, cudaStream_t st);
+
+// a5 / a6
+struct MatchArgs {
+  const float *A, *B, *C;            // model snapshot (fp32)
+  int R, r;
+  const int32_t* Is; const int32_t* Js; const int32_t* Ks;   // [r][nI] ...
+  int nI, nJ, nKs, nK;
+  int64_t ks_stride;                  // stride between reps' K_s lists (K' rows: nK)
+  const float* U[3]; int64_t u_stride[3];
+  const double* lamp;                 // [r][R]
+  double tau;
+  int* pi;           // [r][R]
+  double* scale;     // [r][3][R]
+  double* lam_hat;   // [r][R]
+  double* score_min; // [r]
+  int* accepted;     // [r]
+};
+cudaError_t launch_match(const MatchArgs& m, cudaStream_t st);
+
+struct MergeArgs {
+  const float *A, *B, *C, *lam;      // old model
+  float *An, *Bn, *Cn, *lamn;        // new model (pre-filled copy of the old one)
+  int64_t I, J, Ko, Kn; int R, r;
+  const int32_t* loc[3];             // [r][n_m] local index maps (-1 = not sampled)
+  int nKs;
+  const float* U[3]; int64_t u_stride[3];
+  const int* pi; const double* scale; const double* lam_hat; const int* accepted;
+  int policy;
+};
+cudaError_t launch_merge(const MergeArgs& m, cudaStream_t st);
+
+// a7: relative error of [[lam; A, B, C]] over a dense view (slices [0,K)); writes relerr.
+cudaError_t launch_fit_dense(const DenseView& X, const float* lam, const float* A,
+                             const float* B, const float* C, int R, double* ws /* >= 4 + nb */,
+                             double* relerr, cudaStream_t st);
+size_t fit_dense_ws_doubles(const DenseView& X);
+
+cudaError_t launch_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint64_t key,
+                          int64_t n, uint32_t* out, cudaStream_t st);
+cudaError_t launch_detlog(const double* u, int64_t n, double* out, cudaStream_t st);
+
+}  // namespace sbt

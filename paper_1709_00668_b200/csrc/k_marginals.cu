@@ -1,0 +1,335 @@
+// k_marginals.cu -- a1: fixed-point measure of importance (Eq. 1; R1, R7).
+//
+// q(x) = RNE(phi(x) * 2^S) as int64; x1[i] += q, x2[j] += q, x3[k] += q.  Integer sums are
+// exact, so the result does not depend on the launch configuration or atomic order.
+//
+// Dense layout: X(i,j,k) at base[(k*J + j)*pitch + i].  A "row" is (j,k): `pitch` floats.
+// Each thread owns a fixed set of column quads (float4) of every row it visits and keeps
+// their x1 partial sums in registers for the whole kernel; row totals (x2[j], x3[k]) are
+// reduced across the row's threads (warp shuffles, plus shared memory when a row spans
+// several warps).  Grid = a few blocks per SM, each streaming a contiguous row range, so
+// the pass is one coalesced sweep over HBM (4 B / entry algorithmic).
+#include "common.cuh"
+#include "internal.h"
+
+namespace sbt {
+
+template <int MOI>
+__device__ __forceinline__ long long quant(float x, float scf, double scd) {
+  if (MOI == 0) {
+    return __float2ll_rn(fabsf(x) * scf);      // exact product (power-of-two scale)
+  } else {
+    const double d = (double)x;
+    return __double2ll_rn(__dmul_rn(__dmul_rn(d, d), scd));   // d*d exact (48 bits)
+  }
+}
+
+template <int VEC> struct VecT;
+template <> struct VecT<4> { using T = float4; };
+template <> struct VecT<1> { using T = float; };
+
+template <int VEC>
+__device__ __forceinline__ typename VecT<VEC>::T ld_stream(const float* p);
+template <> __device__ __forceinline__ float4 ld_stream<4>(const float* p) {
+  return __ldcs(reinterpret_cast<const float4*>(p));
+}
+template <> __device__ __forceinline__ float ld_stream<1>(const float* p) { return __ldcs(p); }
+
+__device__ __forceinline__ float comp(const float4& v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ float comp(const float& v, int) { return v; }
+
+constexpr int kMargThreads = 256;
+constexpr int kMargWarps = kMargThreads / 32;
+constexpr int kX3Slots = 64;
+
+// wpr = warps per row (1, 2, 4, 8); G = 8 / wpr rows in flight per block step.
+template <int MOI, int VEC, int V, int UR>
+__global__ void __launch_bounds__(kMargThreads) marg_dense_kernel(
+    const float* __restrict__ X, int64_t pitch, int I, int J, int64_t row0, int64_t nrows,
+    int wpr, int64_t rows_per_block, float scf, double scd, unsigned long long* __restrict__ x1,
+    unsigned long long* __restrict__ x2, unsigned long long* __restrict__ x3) {
+  __shared__ long long red[2][kMargWarps][UR];
+  __shared__ unsigned long long x3s[kX3Slots];
+  extern __shared__ unsigned long long x1s[];   // [I] when G > 1
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = kMargWarps / wpr;
+  const int g = warp / wpr, wr = warp - g * wpr;
+  const int t = wr * 32 + lane;
+  const int TPR = wpr * 32;
+  const int Q = (int)(pitch / VEC);
+  const int64_t rb = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t re = min(rb + rows_per_block, nrows);
+  if (rb >= re) return;
+  const int64_t kfirst = (row0 + rb) / J;
+  const bool x3_local = ((row0 + re - 1) / J - kfirst) < kX3Slots;
+  for (int s = threadIdx.x; s < kX3Slots; s += blockDim.x) x3s[s] = 0;
+  if (G > 1)
+    for (int s = threadIdx.x; s < I; s += blockDim.x) x1s[s] = 0;
+  __syncthreads();
+
+  long long acc[V][VEC];
+#pragma unroll
+  for (int c = 0; c < V; ++c)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[c][e] = 0;
+
+  int buf = 0;
+  for (int64_t r0 = rb; r0 < re; r0 += (int64_t)G * UR) {
+    typename VecT<VEC>::T v[UR][V];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      const int64_t row = r0 + (int64_t)u * G + g;
+#pragma unroll
+      for (int c = 0; c < V; ++c) {
+        const int qd = t + c * TPR;
+        if (row < re && qd < Q) {
+          v[u][c] = ld_stream<VEC>(X + (row0 + row) * pitch + (int64_t)qd * VEC);
+        } else {
+          if constexpr (VEC == 4) v[u][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          else v[u][c] = 0.f;
+        }
+      }
+    }
+    long long rs[UR];
+#pragma unroll
+    for (int u = 0; u < UR; ++u) {
+      rs[u] = 0;
+#pragma unroll
+      for (int c = 0; c < V; ++c)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const long long q = quant<MOI>(comp(v[u][c], e), scf, scd);
+          acc[c][e] += q;
+          rs[u] += q;
+        }
+      rs[u] = warp_sum_ll(rs[u]);
+    }
+    if (wpr == 1) {
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          const int64_t row = r0 + (int64_t)u * G + g;
+          if (row < re && rs[u] != 0) {
+            const int64_t gr = row0 + row;
+            const int64_t k = gr / J, j = gr - k * J;
+            atomicAdd(&x2[j], (unsigned long long)rs[u]);
+            if (x3_local) atomicAdd(&x3s[k - kfirst], (unsigned long long)rs[u]);
+            else atomicAdd(&x3[k], (unsigned long long)rs[u]);
+          }
+        }
+      }
+    } else {
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < UR; ++u) red[buf][warp][u] = rs[u];
+      }
+      __syncthreads();
+      if (wr == 0 && lane < UR) {
+        const int64_t row = r0 + (int64_t)lane * G + g;
+        if (row < re) {
+          long long s = 0;
+          for (int w = 0; w < wpr; ++w) s += red[buf][g * wpr + w][lane];
+          if (s != 0) {
+            const int64_t gr = row0 + row;
+            const int64_t k = gr / J, j = gr - k * J;
+            atomicAdd(&x2[j], (unsigned long long)s);
+            if (x3_local) atomicAdd(&x3s[k - kfirst], (unsigned long long)s);
+            else atomicAdd(&x3[k], (unsigned long long)s);
+          }
+        }
+      }
+      buf ^= 1;
+    }
+  }
+  // x1: combine the G row groups in shared memory, then one global atomic per column.
+#pragma unroll
+  for (int c = 0; c < V; ++c)
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const int col = (t + c * TPR) * VEC + e;
+      if (col < I && acc[c][e] != 0) {
+        if (G > 1) atomicAdd(&x1s[col], (unsigned long long)acc[c][e]);
+        else atomicAdd(&x1[col], (unsigned long long)acc[c][e]);
+      }
+    }
+  __syncthreads();
+  if (G > 1)
+    for (int s = threadIdx.x; s < I; s += blockDim.x)
+      if (x1s[s]) atomicAdd(&x1[s], x1s[s]);
+  if (x3_local)
+    for (int s = threadIdx.x; s < kX3Slots; s += blockDim.x)
+      if (x3s[s]) atomicAdd(&x3[kfirst + s], x3s[s]);
+}
+
+static inline float pow2f(int S) { return ldexpf(1.0f, S); }  // exact for S in [-126, 127]
+
+template <int MOI, int VEC, int V>
+static cudaError_t marg_launch(const DenseView& X, int64_t row0, int64_t nrows, int wpr,
+                               float scf, double scd, unsigned long long* x1,
+                               unsigned long long* x2, unsigned long long* x3, cudaStream_t st) {
+  constexpr int UR = 2;
+  const int G = kMargWarps / wpr;
+  const int64_t step = (int64_t)G * UR;
+  int64_t nblocks = (int64_t)kNumSMs * 6;
+  int64_t rpb = ceil_div(ceil_div(nrows, nblocks), step) * step;
+  if (rpb < step) rpb = step;
+  nblocks = ceil_div(nrows, rpb);
+  const size_t smem = G > 1 ? sizeof(unsigned long long) * (size_t)X.I : 0;
+  marg_dense_kernel<MOI, VEC, V, UR><<<(unsigned)nblocks, kMargThreads, smem, st>>>(
+      X.base, X.pitch, (int)X.I, (int)X.J, row0, nrows, wpr, rpb, scf, scd, x1, x2, x3);
+  return cudaGetLastError();
+}
+
+template <int MOI, int VEC>
+static cudaError_t marg_dispatch_v(const DenseView& X, int64_t row0, int64_t nrows, float scf,
+                                   double scd, unsigned long long* x1, unsigned long long* x2,
+                                   unsigned long long* x3, cudaStream_t st) {
+  const int64_t Q = X.pitch / VEC;
+  // smallest warps-per-row such that V = ceil(Q / (32*wpr)) <= 4
+  int wpr = 1;
+  while (wpr < 8 && ceil_div(Q, 32 * wpr) > 4) wpr *= 2;
+  const int64_t V = ceil_div(Q, 32 * wpr);
+  if (V > 4) return cudaErrorInvalidValue;   // rows longer than 4096 (VEC=4) unsupported
+  switch (V) {
+    case 1: return marg_launch<MOI, VEC, 1>(X, row0, nrows, wpr, scf, scd, x1, x2, x3, st);
+    case 2: return marg_launch<MOI, VEC, 2>(X, row0, nrows, wpr, scf, scd, x1, x2, x3, st);
+    case 3: return marg_launch<MOI, VEC, 3>(X, row0, nrows, wpr, scf, scd, x1, x2, x3, st);
+    default: return marg_launch<MOI, VEC, 4>(X, row0, nrows, wpr, scf, scd, x1, x2, x3, st);
+  }
+}
+
+cudaError_t launch_marginals_dense(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
+                                   int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st) {
+  if (nk <= 0 || X.I <= 0 || X.J <= 0) return cudaSuccess;
+  const int64_t row0 = k0 * X.J, nrows = nk * X.J;
+  const float scf = pow2f(S < -126 ? -126 : (S > 127 ? 127 : S));
+  const double scd = ldexp(1.0, S);
+  auto* u1 = reinterpret_cast<unsigned long long*>(x1);
+  auto* u2 = reinterpret_cast<unsigned long long*>(x2);
+  auto* u3 = reinterpret_cast<unsigned long long*>(x3);
+  const bool vec4 = (X.pitch % 4 == 0) && ((uintptr_t)X.base % 16 == 0);
+  if (moi == 0) {
+    return vec4 ? marg_dispatch_v<0, 4>(X, row0, nrows, scf, scd, u1, u2, u3, st)
+                : marg_dispatch_v<0, 1>(X, row0, nrows, scf, scd, u1, u2, u3, st);
+  }
+  return vec4 ? marg_dispatch_v<1, 4>(X, row0, nrows, scf, scd, u1, u2, u3, st)
+              : marg_dispatch_v<1, 1>(X, row0, nrows, scf, scd, u1, u2, u3, st);
+}
+
+// ---------------------------------------------------------------------------------------
+// COO marginals: one thread per stored entry.  Entries are sorted by (k, j, i), so x3 is
+// aggregated over runs of equal k inside a warp before its atomic.
+// ---------------------------------------------------------------------------------------
+template <int MOI>
+__global__ void marg_coo_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                const int32_t* __restrict__ kk, const float* __restrict__ vv,
+                                int64_t nnz, float scf, double scd, unsigned long long* x1,
+                                unsigned long long* x2, unsigned long long* x3) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < nnz;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = base + threadIdx.x;
+    long long q = 0;
+    int k = -1;
+    if (n < nnz) {
+      q = quant<MOI>(vv[n], scf, scd);
+      if (q) {
+        atomicAdd(&x1[ii[n]], (unsigned long long)q);
+        atomicAdd(&x2[jj[n]], (unsigned long long)q);
+      }
+      k = kk[n];
+    }
+    // segmented reduction of q over equal k within the warp
+    const unsigned same = __match_any_sync(0xffffffffu, k);
+    const int leader = __ffs(same) - 1;
+    long long s = 0;
+    for (unsigned m = same; m; m &= m - 1) {
+      const int src = __ffs(m) - 1;
+      s += __shfl_sync(same, q, src);
+    }
+    if (lane == leader && k >= 0 && s) atomicAdd(&x3[k], (unsigned long long)s);
+  }
+}
+
+cudaError_t launch_marginals_coo(const int32_t* i, const int32_t* j, const int32_t* k,
+                                 const float* v, int64_t nnz, int moi, int S, int64_t* x1,
+                                 int64_t* x2, int64_t* x3, cudaStream_t st) {
+  if (nnz <= 0) return cudaSuccess;
+  const float scf = pow2f(S < -126 ? -126 : (S > 127 ? 127 : S));
+  const double scd = ldexp(1.0, S);
+  const int threads = 256;
+  int64_t blocks = ceil_div(nnz, threads);
+  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+  auto* u1 = reinterpret_cast<unsigned long long*>(x1);
+  auto* u2 = reinterpret_cast<unsigned long long*>(x2);
+  auto* u3 = reinterpret_cast<unsigned long long*>(x3);
+  if (moi == 0)
+    marg_coo_kernel<0><<<(unsigned)blocks, threads, 0, st>>>(i, j, k, v, nnz, scf, scd, u1, u2, u3);
+  else
+    marg_coo_kernel<1><<<(unsigned)blocks, threads, 0, st>>>(i, j, k, v, nnz, scf, scd, u1, u2, u3);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// max phi (fixed-point range, R7)
+// ---------------------------------------------------------------------------------------
+template <int MOI>
+__device__ __forceinline__ double phi_d(float x) {
+  const double d = (double)x;
+  return MOI == 0 ? fabs(d) : d * d;
+}
+
+template <int MOI>
+__global__ void max_phi_dense_kernel(const float* __restrict__ X, int64_t pitch, int64_t I,
+                                     int64_t row0, int64_t nrows, unsigned long long* out) {
+  double m = 0.0;
+  const int64_t total = nrows * I;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / I, col = e - row * I;
+    m = fmax(m, phi_d<MOI>(X[(row0 + row) * pitch + col]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+template <int MOI>
+__global__ void max_phi_vals_kernel(const float* __restrict__ v, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, phi_d<MOI>(v[e]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0)
+    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+cudaError_t launch_max_phi_dense(const DenseView& X, int64_t k0, int64_t nk, int moi,
+                                 unsigned long long* out, cudaStream_t st) {
+  const int64_t nrows = nk * X.J;
+  if (nrows <= 0) return cudaSuccess;
+  int64_t blocks = ceil_div(nrows * X.I, 256);
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  if (moi == 0)
+    max_phi_dense_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(X.base, X.pitch, X.I, k0 * X.J, nrows, out);
+  else
+    max_phi_dense_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(X.base, X.pitch, X.I, k0 * X.J, nrows, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_phi_vals(const float* v, int64_t n, int moi, unsigned long long* out,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = ceil_div(n, 256);
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  if (moi == 0) max_phi_vals_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(v, n, out);
+  else max_phi_vals_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(v, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace sbt

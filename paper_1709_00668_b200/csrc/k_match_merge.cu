@@ -1,0 +1,244 @@
+// k_match_merge.cu -- a5: anchor congruence and optimal matching (Lemma 1;
+// R13-R16, R26) and a6: merge (R17-R20).
+#include "common.cuh"
+#include "internal.h"
+
+namespace sbt {
+
+constexpr int kMatchThreads = 256;
+
+// Hungarian method (potentials; O(R^3)) maximising sum_f S[f][pi f]; single thread.
+__device__ void hungarian_max(const double* S, int R, int* pi) {
+  double u[kMaxR + 1], v[kMaxR + 1], minv[kMaxR + 1];
+  int p[kMaxR + 1], way[kMaxR + 1];
+  bool used[kMaxR + 1];
+  for (int j = 0; j <= R; ++j) { u[j] = 0; v[j] = 0; p[j] = 0; way[j] = 0; }
+  for (int i = 1; i <= R; ++i) {
+    p[0] = i;
+    int j0 = 0;
+    for (int j = 0; j <= R; ++j) { minv[j] = 1e300; used[j] = false; }
+    do {
+      used[j0] = true;
+      const int i0 = p[j0];
+      double delta = 1e300;
+      int j1 = 0;
+      for (int j = 1; j <= R; ++j) {
+        if (!used[j]) {
+          const double cur = -S[(i0 - 1) * R + (j - 1)] - u[i0] - v[j];
+          if (cur < minv[j]) { minv[j] = cur; way[j] = j0; }
+          if (minv[j] < delta) { delta = minv[j]; j1 = j; }
+        }
+      }
+      for (int j = 0; j <= R; ++j) {
+        if (used[j]) { u[p[j]] += delta; v[j] -= delta; }
+        else minv[j] -= delta;
+      }
+      j0 = j1;
+    } while (p[j0] != 0);
+    do {
+      const int j1 = way[j0];
+      p[j0] = p[j1];
+      j0 = j1;
+    } while (j0);
+  }
+  for (int j = 1; j <= R; ++j) pi[p[j] - 1] = j - 1;
+}
+
+__device__ __forceinline__ void unrank_perm(long long k, int R, int* perm) {
+  int avail[8];
+  long long fact[9];
+  fact[0] = 1;
+  for (int i = 1; i <= R; ++i) fact[i] = fact[i - 1] * i;
+  for (int i = 0; i < R; ++i) avail[i] = i;
+  int na = R;
+  for (int i = 0; i < R; ++i) {
+    const long long f = fact[R - 1 - i];
+    const int d = (int)(k / f);
+    k -= d * f;
+    perm[i] = avail[d];
+    for (int t = d; t < na - 1; ++t) avail[t] = avail[t + 1];
+    --na;
+  }
+}
+
+__global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m) {
+  const int rep = blockIdx.x;
+  const int R = m.R;
+  __shared__ double Phi[3][kMaxR * kMaxR];
+  __shared__ double al[3][kMaxR], an[3][kMaxR];
+  __shared__ double S[kMaxR * kMaxR];
+  __shared__ double bval[kMatchThreads];
+  __shared__ long long bidx[kMatchThreads];
+  __shared__ int pi_s[kMaxR];
+  extern __shared__ unsigned char anchor[];
+  for (int mode = 0; mode < 3; ++mode) {
+    const float* F = mode == 0 ? m.A : mode == 1 ? m.B : m.C;
+    const int32_t* idx = mode == 0 ? m.Is + (int64_t)rep * m.nI
+                       : mode == 1 ? m.Js + (int64_t)rep * m.nJ : m.Ks + (int64_t)rep * m.ks_stride;
+    const int n = mode == 0 ? m.nI : mode == 1 ? m.nJ : m.nKs;
+    const float* U = m.U[mode] + rep * m.u_stride[mode];
+    for (int p = threadIdx.x; p < n; p += blockDim.x) {
+      const float* o = F + (int64_t)idx[p] * R;
+      bool nz = false;
+      for (int f = 0; f < R; ++f) nz |= (o[f] != 0.0f);
+      anchor[p] = nz ? 1 : 0;
+    }
+    __syncthreads();
+    const int npair = R * R + 2 * R;
+    for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
+      double s = 0.0;
+      if (pr < R * R) {
+        const int f = pr / R, g = pr - f * R;
+        for (int p = 0; p < n; ++p)
+          if (anchor[p]) s += (double)F[(int64_t)idx[p] * R + f] * (double)U[(int64_t)p * R + g];
+        Phi[mode][pr] = s;
+      } else if (pr < R * R + R) {
+        const int f = pr - R * R;
+        for (int p = 0; p < n; ++p)
+          if (anchor[p]) { const double o = F[(int64_t)idx[p] * R + f]; s += o * o; }
+        al[mode][f] = sqrt(s);
+      } else {
+        const int g = pr - R * R - R;
+        for (int p = 0; p < n; ++p)
+          if (anchor[p]) { const double c = U[(int64_t)p * R + g]; s += c * c; }
+        an[mode][g] = sqrt(s);
+      }
+    }
+    __syncthreads();
+  }
+  for (int pr = threadIdx.x; pr < R * R; pr += blockDim.x) {
+    const int f = pr / R, g = pr - f * R;
+    double t = 0.0;
+    for (int mode = 0; mode < 3; ++mode) {
+      const double d = al[mode][f] * an[mode][g];
+      const double ph = d > 0.0 ? Phi[mode][pr] / d : 0.0;
+      Phi[mode][pr] = ph;
+      t += fabs(ph);
+    }
+    S[pr] = t / 3.0;
+  }
+  __syncthreads();
+  if (R <= 8) {
+    // exhaustive search in lexicographic order; first maximum wins (R15)
+    long long nperm = 1;
+    for (int i = 2; i <= R; ++i) nperm *= i;
+    double best = -1e300;
+    long long bk = 0x7fffffffffffffffll;
+    int perm[8];
+    for (long long k = threadIdx.x; k < nperm; k += blockDim.x) {
+      unrank_perm(k, R, perm);
+      double v = 0.0;
+      for (int f = 0; f < R; ++f) v += S[f * R + perm[f]];
+      if (v > best) { best = v; bk = k; }
+    }
+    bval[threadIdx.x] = best;
+    bidx[threadIdx.x] = bk;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = bval[0];
+      long long k = bidx[0];
+      for (int t = 1; t < (int)blockDim.x; ++t)
+        if (bval[t] > b || (bval[t] == b && bidx[t] < k)) { b = bval[t]; k = bidx[t]; }
+      unrank_perm(k, R, perm);
+      for (int f = 0; f < R; ++f) pi_s[f] = perm[f];
+    }
+  } else {
+    if (threadIdx.x == 0) hungarian_max(S, R, pi_s);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double smin = 1e300;
+    bool nan = false;
+    for (int f = 0; f < R; ++f) {
+      const int g = pi_s[f];
+      m.pi[rep * R + f] = g;
+      double lh = m.lamp[rep * R + g];
+      bool ok_all = true;
+      for (int mode = 0; mode < 3; ++mode) {
+        const double sig = Phi[mode][f * R + g] < 0.0 ? -1.0 : 1.0;
+        const double a0 = al[mode][f], a1 = an[mode][g];
+        const bool ok = a0 > 0.0 && a1 > 0.0;
+        m.scale[((int64_t)rep * 3 + mode) * R + f] = ok ? sig * a0 / a1 : 0.0;
+        if (ok) lh = lh * sig * a1 / a0; else ok_all = false;
+      }
+      m.lam_hat[rep * R + f] = ok_all ? lh : 0.0;
+      const double sc = S[f * R + g];
+      if (sc != sc) nan = true;
+      smin = fmin(smin, sc);
+    }
+    m.score_min[rep] = smin;
+    m.accepted[rep] = (!nan && smin >= m.tau) ? 1 : 0;
+  }
+}
+
+cudaError_t launch_match(const MatchArgs& m, cudaStream_t st) {
+  const int nmax = max(m.nI, max(m.nJ, m.nKs));
+  match_kernel<<<m.r, kMatchThreads, (size_t)nmax, st>>>(m);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// merge
+// ---------------------------------------------------------------------------------------
+__global__ void merge_rows_kernel(MergeArgs g, int mode) {
+  const int64_t n = mode == 0 ? g.I : mode == 1 ? g.J : g.Ko;
+  const int R = g.R;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * R) return;
+  const int64_t row = idx / R;
+  const int f = (int)(idx - row * R);
+  const float* Fo = mode == 0 ? g.A : mode == 1 ? g.B : g.C;
+  float* Fn = mode == 0 ? g.An : mode == 1 ? g.Bn : g.Cn;
+  const int32_t* loc = g.loc[mode];
+  double s = 0.0;
+  int cnt = 0;
+  for (int rep = 0; rep < g.r; ++rep) {
+    if (!g.accepted[rep]) continue;
+    const int l = loc[(int64_t)rep * n + row];
+    if (l < 0) continue;
+    const float* U = g.U[mode] + rep * g.u_stride[mode];
+    s += g.scale[((int64_t)rep * 3 + mode) * R + f] * (double)U[(int64_t)l * R + g.pi[rep * R + f]];
+    ++cnt;
+  }
+  if (cnt) {
+    const float old = Fo[idx];
+    if (g.policy == 1 || old == 0.0f) Fn[idx] = (float)(s / cnt);
+  }
+}
+
+__global__ void merge_new_kernel(MergeArgs g) {
+  const int R = g.R;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int nacc = 0;
+  for (int rep = 0; rep < g.r; ++rep) nacc += g.accepted[rep] ? 1 : 0;
+  if (nacc == 0) return;
+  if (idx < g.Kn * R) {
+    const int64_t k = idx / R;
+    const int f = (int)(idx - k * R);
+    double s = 0.0;
+    for (int rep = 0; rep < g.r; ++rep) {
+      if (!g.accepted[rep]) continue;
+      const float* U = g.U[2] + rep * g.u_stride[2];
+      s += g.scale[((int64_t)rep * 3 + 2) * R + f] * (double)U[(g.nKs + k) * R + g.pi[rep * R + f]];
+    }
+    g.Cn[(g.Ko + k) * R + f] = (float)(s / nacc);
+  } else if (idx < g.Kn * R + R) {
+    const int f = (int)(idx - g.Kn * R);
+    double s = 0.0;
+    for (int rep = 0; rep < g.r; ++rep)
+      if (g.accepted[rep]) s += g.lam_hat[rep * R + f];
+    g.lamn[f] = (float)(((double)g.lam[f] + s / nacc) / 2.0);
+  }
+}
+
+cudaError_t launch_merge(const MergeArgs& g, cudaStream_t st) {
+  for (int mode = 0; mode < 3; ++mode) {
+    const int64_t n = mode == 0 ? g.I : mode == 1 ? g.J : g.Ko;
+    const int64_t tot = n * g.R;
+    if (tot > 0) merge_rows_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(g, mode);
+  }
+  merge_new_kernel<<<(unsigned)ceil_div(g.Kn * g.R + g.R, 256), 256, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
+}  // namespace sbt
