@@ -118,8 +118,12 @@ def ptr(x):
     if x is None:
         return None
     if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor passed to the C-ABI must be contiguous")
         return x.data_ptr()
     if isinstance(x, np.ndarray):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array passed to the C-ABI must be C-contiguous (row-major)")
         return x.ctypes.data
     if isinstance(x, int):
         return x
@@ -185,7 +189,13 @@ def sambaten_init(X0, R, s, r, seed, opts=None):
     return h
 
 
+def _c_in(x):
+    """Input-only host array: row-major copy if needed (factors are [rows][R] row-major)."""
+    return np.ascontiguousarray(x) if isinstance(x, np.ndarray) else x
+
+
 def sambaten_init_factors(X0, R, s, r, seed, A, B, Cm, lam, opts=None):
+    A, B, Cm, lam = _c_in(A), _c_in(B), _c_in(Cm), _c_in(lam)
     h = C.c_void_p()
     check(lib().sambaten_init_factors(C.byref(h), C.byref(X0), R, s, r, seed, ptr(A), ptr(B), ptr(Cm),
                                       ptr(lam), C.byref(opts) if opts else None))

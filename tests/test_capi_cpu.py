@@ -54,3 +54,12 @@ def test_no_gpu_means_loud_failure():
         assert e.name in ("E_CUDA",)
     else:
         raise AssertionError("init succeeded without a GPU")
+from paper_1709_00668_b200 import _lib as L
+def test_ptr_rejects_non_row_major():
+    import numpy as np
+    import pytest
+    from paper_1709_00668_b200 import _lib as L
+    a = np.asfortranarray(np.ones((5, 3), np.float32))
+    with pytest.raises(ValueError):
+        L.ptr(a)
+    assert L.ptr(np.ascontiguousarray(a)) is not None
