@@ -92,6 +92,8 @@ typedef struct {
   uint32_t reps_rejected_mask; /* bit rho set if repetition rho was rejected (R26; r <= 32)  */
   int scale_exp;               /* fixed-point exponent S of the marginals (R7)                */
   int kernel_launches;         /* CUDA kernels this update launched (all are this library's) */
+  uint32_t reps_pinv_mask;     /* bit rho set if repetition rho's ALS used the pseudo-inverse  */
+                               /* fallback (R12) at least once                                */
   double step_ms[8];           /* device time of steps a0..a7 (CUDA events)                   */
 } sambaten_info;
 

@@ -35,6 +35,8 @@ def _deps_mtime():
 def _compile(src):
     obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
     cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+    if os.environ.get("SBT_EXTRA_FLAGS"):
+        cmd += os.environ["SBT_EXTRA_FLAGS"].split()
     if os.environ.get("SBT_PTXAS_V"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -98,6 +100,9 @@ struct sambaten_s {
   // last sample sizes
   int64_t last_n[3] = {0, 0, 0};
   int64_t last_nKp = 0;
+  // cluster-ALS plans by summary shape (host-side planning kept out of the timed path)
+  struct PlanEntry { int nI, nJ, nK, R, r; bool ok; ClusterPlan pl; };
+  std::vector<PlanEntry> plans;
 
   float* A(int b) const { return model[b].as<float>(); }
   float* B(int b) const { return A(b) + I * R; }
@@ -106,6 +111,24 @@ struct sambaten_s {
   size_t model_floats() const { return (size_t)(I + J + Kcap + 1) * R; }
   DenseView view() const { return DenseView{X.as<float>(), I, J, K, pitch}; }
 };
+
+static bool cluster_plan(sambaten_s* h, const DenseAls& a, ClusterPlan* pl) {
+  if (a.r < 2 || getenv("SAMBATEN_NO_CLUSTER_ALS")) return false;
+  for (auto& e : h->plans)
+    if (e.nI == a.nI && e.nJ == a.nJ && e.nK == a.nK && e.R == a.R && e.r == a.r) {
+      *pl = e.pl;
+      return e.ok;
+    }
+  sambaten_s::PlanEntry e{a.nI, a.nJ, a.nK, a.R, a.r, false, ClusterPlan{}};
+  e.ok = plan_als_cluster(a, &e.pl);
+  if (getenv("SAMBATEN_DEBUG"))
+    fprintf(stderr, "[sambaten] cluster ALS plan nI=%d nJ=%d nK=%d R=%d r=%d -> ok=%d CS=%d smem=%zu act=%d RB=%d stage_fl=%d\n",
+            a.nI, a.nJ, a.nK, a.R, a.r, (int)e.ok, e.pl.CS, e.pl.smem, e.pl.act, e.pl.RB,
+            e.pl.stage_fl);
+  h->plans.push_back(e);
+  *pl = e.pl;
+  return e.ok;
+}
 
 extern "C" {
 
@@ -365,27 +388,50 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   CK(launch_sample(h->segs.as<SampleSeg>(), 3 * r, h->seed, uid, st));
   CK(cudaEventRecord(h->ev[3], st));
   // ---- a3: gather the r summaries ------------------------------------------------------
-  const int64_t y_stride = nKp * nJ * nI;
-  CK(h->summ.ensure(sizeof(float) * r * y_stride));
-  float* Y = h->summ.as<float>();
-  CK(launch_gather_dense(V, Is, Js, Kp, (int)nI, (int)nJ, (int)nKp, r, nI, nJ, nKp, Y, y_stride, st));
-  CK(cudaEventRecord(h->ev[4], st));
-  // ---- a4: batched CP-ALS ---------------------------------------------------------------
+  int64_t y_stride = (nKp * nJ * nI + 3) & ~int64_t(3);
   const size_t u0 = align256(sizeof(float) * r * nI * R), u1 = align256(sizeof(float) * r * nJ * R);
   const size_t u2 = align256(sizeof(float) * r * nKp * R);
   CK(h->fac.ensure(u0 + u1 + u2));
   DenseAls a{};
-  a.Y = Y; a.y_stride = y_stride; a.pitch = nI;
+  a.y_stride = y_stride; a.pitch = nI;
   a.nI = (int)nI; a.nJ = (int)nJ; a.nK = (int)nKp; a.R = R; a.r = r;
   a.U[0] = h->fac.as<float>();
   a.U[1] = reinterpret_cast<float*>(h->fac.as<char>() + u0);
   a.U[2] = reinterpret_cast<float*>(h->fac.as<char>() + u0 + u1);
   a.u_stride[0] = nI * R; a.u_stride[1] = nJ * R; a.u_stride[2] = nKp * R;
   a.maxit = h->opts.als_max_iters; a.tol = h->opts.als_tol;
-  CK(h->als.ensure(dense_als_workspace(&a)));
+  a.Yt = reinterpret_cast<const float*>(1);   // planning only needs "transpose available"
+  ClusterPlan cpl;
+  const bool use_cluster = cluster_plan(h, a, &cpl);
+  const int pI = use_cluster ? cluster_pitch((int)nI) : (int)nI;
+  const int pJ = use_cluster ? cluster_pitch((int)nJ) : (int)nJ;
+  if (use_cluster) y_stride = (nKp * std::max<int64_t>(nJ * pI, nI * pJ) + 3) & ~int64_t(3);
+  a.y_stride = y_stride;
+  a.pitch = pI;
+  CK(h->summ.ensure(sizeof(float) * r * y_stride * (use_cluster ? 2 : 1)));
+  float* Y = h->summ.as<float>();
+  float* Yt = use_cluster ? Y + r * y_stride : nullptr;
+  a.Y = Y;
+  a.Yt = Yt;
+  CK(launch_gather_dense(V, Is, Js, Kp, (int)nI, (int)nJ, (int)nKp, r, nI, nJ, nKp, Y, y_stride, st,
+                         Yt, pI, pJ));
+  CK(cudaEventRecord(h->ev[4], st));
+  // ---- a4: batched CP-ALS ---------------------------------------------------------------
+  const size_t ws_als = align256(dense_als_workspace(&a));
+  const size_t ws_d = use_cluster ? als_cluster_dscratch_bytes(a, cpl) : 0;
+  CK(h->als.ensure(ws_als + ws_d));
   CK(dense_als_bind_workspace(&a, h->als.p));
-  CK(launch_als_init(a, h->seed, uid, 0, true, st));
-  CK(run_dense_als(a, st));
+  int als_launches;
+  if (use_cluster) {
+    CK(launch_als_init_factors(a, h->seed, uid, 0, st));
+    CK(run_als_cluster(a, cpl, reinterpret_cast<float*>(h->als.as<char>() + ws_als), st));
+    if (getenv("SAMBATEN_DEBUG")) als_phase_dump();
+    als_launches = 2;
+  } else {
+    CK(launch_als_init(a, h->seed, uid, 0, true, st));
+    CK(run_dense_als(a, st));
+    als_launches = 4 + 7 * a.maxit;
+  }
   CK(cudaEventRecord(h->ev[5], st));
   // ---- a5: match against the batch-start model (R13-R16, R26) ---------------------------
   const int b = h->cur, nb = 1 - h->cur;
@@ -464,9 +510,12 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     info->k_total = h->K;
     info->reps_rejected_mask = rejected;
     info->scale_exp = h->S;
+    uint32_t pm = 0;
+    for (int rho = 0; rho < r; ++rho) if (hs->flags[rho] & 1) pm |= 1u << rho;
+    info->reps_pinv_mask = pm;
     // max_phi, marginals, sample, gather, als_init + gram + 2 sumsq, 7 per ALS iteration
     // (all iterations are launched; converged reps exit at once), match, 3 + 1 merge, 2 fit
-    info->kernel_launches = 1 + 1 + 1 + 1 + 4 + 7 * a.maxit + 1 + 4 + (h->opts.full_fit ? 2 : 0);
+    info->kernel_launches = 1 + 1 + 1 + 1 + als_launches + 1 + 4 + (h->opts.full_fit ? 2 : 0);
     for (int e = 0; e < 8; ++e) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);

@@ -55,14 +55,18 @@ cudaError_t launch_sample(const SampleSeg* segs_dev, int nseg, uint64_t seed, ui
 
 // a3 dense: Y[rep][u][q][p] = X(Is[rep][p], Js[rep][q], Kp[rep][u]) ; Y pitch = nI.
 // ysq_part (optional) [rep][gridDim.x] gets per-block sums of squares (fp64).
+// Y rows have pitch pI (>= nI); Yt (optional, may be null) is the per-slice transpose
+// Yt[rep][u][p][q] with row pitch pJ (>= nJ) and the same y_stride.
 cudaError_t launch_gather_dense(const DenseView& X, const int32_t* Is, const int32_t* Js,
                                 const int32_t* Kp, int nI, int nJ, int nK, int r,
                                 int64_t idx_stride_I, int64_t idx_stride_J, int64_t idx_stride_K,
-                                float* Y, int64_t y_stride, cudaStream_t st);
+                                float* Y, int64_t y_stride, cudaStream_t st, float* Yt = nullptr,
+                                int pI = 0, int pJ = 0);
 
 // ---- dense batched CP-ALS -------------------------------------------------------------
 struct DenseAls {
   const float* Y;  int64_t y_stride;   // [r][nK][nJ][pitch]
+  const float* Yt;                     // optional per-slice transpose [r][nK][nI][nJ] (cluster path)
   int64_t pitch;
   int nI, nJ, nK, R, r;
   float* U[3]; int64_t u_stride[3];    // [r][n_m][R]
@@ -85,6 +89,17 @@ size_t dense_als_workspace(DenseAls* a);
 cudaError_t dense_als_bind_workspace(DenseAls* a, void* ws);
 cudaError_t launch_als_init(const DenseAls& a, uint64_t seed, uint32_t update_id,
                             uint32_t rep0, bool init_factors, cudaStream_t st);
+// factor init only (Philox U(0,1) -> fp32, R10) and per-rep state reset
+cudaError_t launch_als_init_factors(const DenseAls& a, uint64_t seed, uint32_t update_id,
+                                    uint32_t rep0, cudaStream_t st);
+// cluster-per-repetition ALS (k_als_cluster.cu): all iterations in one launch
+struct ClusterPlan { int CS = 0; size_t smem = 0; int act = 0; int RB = 0; int stage_fl = 0; };
+// row pitch (floats) of the summary layouts Y[u][q][p] / Yt[u][p][q] the cluster path reads
+int cluster_pitch(int n);
+bool plan_als_cluster(const DenseAls& a, ClusterPlan* pl);
+size_t als_cluster_dscratch_bytes(const DenseAls& a, const ClusterPlan& pl);
+void als_phase_dump();   // SBT_ALS_PHASES builds only (debug)
+cudaError_t run_als_cluster(const DenseAls& a, const ClusterPlan& pl, float* Dglob, cudaStream_t st);
 cudaError_t launch_sumsq_dense(const float* Y, int64_t y_stride, int64_t rows, int64_t pitch,
                                int64_t ncols, int r, double* out, cudaStream_t st);
 cudaError_t run_dense_als(const DenseAls& a, cudaStream_t st);

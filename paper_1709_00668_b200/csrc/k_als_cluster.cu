@@ -1,0 +1,831 @@
+// k_als_cluster.cu -- a4: batched CP-ALS, one thread-block CLUSTER per repetition
+// (Alg. 1 l.5 P:213; readings R10-R12).
+//
+// The r summaries are independent ALS problems ("does not require any
+// synchronization").  Each one is owned by a cluster of CS CTAs (CS <= 16) that runs ALL
+// iterations in one launch; the CTAs exchange partial results through distributed shared
+// memory (DSMEM) and cluster barriers instead of kernel boundaries.
+//
+// Layouts (written by the gather, k_gather.cu):  Y[u][q][p] (p fastest) and its per-slice
+// transpose Yt[u][p][q] (q fastest).  CTA c owns the K' slices u in [u0, u1).  Both
+// streaming passes are column-parallel (consecutive threads read consecutive floats of a
+// row; no cross-thread reduction inside a row):
+//   mode 0 (pass A over Y):   T_u(p,f) = sum_q Y(u,q,p) U1(q,f);  P(p,f) = sum_u U2(u,f) T_u(p,f)
+//   mode 1 (pass B over Yt):  D(u,q,f) = sum_p Yt(u,p,q) U0(p,f);  P(q,f) = sum_u U2(u,f) D(u,q,f)
+//   mode 2 (no pass):         M2(u,f) = sum_q D(u,q,f) U1(q,f)   (local to the owner of u)
+// (U0 is fixed between modes 1 and 2, so D serves both: 2 passes per iteration, not 3.)
+// Mode 0/1 step: barrier; CTA c sums the CS partials of its chunk of rows (fixed rank
+// order), solves U = M V^-1 (V = Hadamard of the other two Grams, inverted by warp 0 while
+// the pass runs; pseudo-inverse fallback R12) and the chunk's partial Gram; barrier; every
+// CTA sums the Grams -> lambda (column norms), normalised Gram, and pulls all normalised
+// rows into its fp32 copy of U.  Mode 2: solve of the own rows, partial Gram and the fit
+// inner product; one barrier.  Every CTA then computes the same fit -> uniform stop test.
+// Precision: fp32 products; per-thread fp32 runs of one slice (<= nI or nJ terms), scaled by
+// U2 into per-thread fp32 sums over the CTA's <= ceil(K'/CS) slices; fp64 across threads and
+// CTAs (fixed order, deterministic); Grams, solves, norms and the fit in fp64.
+#include <cooperative_groups.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "als_small.cuh"
+#include "common.cuh"
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace sbt {
+
+constexpr int kCT = 512;          // threads per CTA
+constexpr int kCW = kCT / 32;     // warps per CTA
+
+
+constexpr int kTS = 2;            // TMA stages per team
+
+struct ClLayout {
+  size_t G, Gp, Gs, Vi, W1, lam, sc, bars, P, Xun, Xun2, Msh, U0s, U1s, U2s, Wt, stage, total;
+  int chunk0, chunk1, ownK, stage_fl, T, NT;
+};
+
+__host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
+__host__ __device__ inline int imax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+__host__ __device__ inline int pitch4(int n) { return (n + 3) & ~3; }
+
+// Teams: warp-aligned groups of T threads, one thread per column pair of the wider layout;
+// NT = teams per CTA (<= 15: one named barrier each).
+__host__ __device__ inline void cl_teams(int nI, int nJ, int* T, int* NT) {
+  const int pairs = pitch4(nI > nJ ? nI : nJ) / 2;
+  *T = 32 * ((pairs + 31) / 32);
+  int nt = kCT / *T;
+  *NT = nt > 15 ? 15 : nt;
+}
+
+// Shared-memory layout; identical on host (sizing) and device.
+__host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, int CS, int stage_fl) {
+  ClLayout L{};
+  L.chunk0 = (nI + CS - 1) / CS;
+  L.chunk1 = (nJ + CS - 1) / CS;
+  L.ownK = (nK + CS - 1) / CS;
+  cl_teams(nI, nJ, &L.T, &L.NT);
+  const int mrows = imax3(L.chunk0, L.chunk1, L.ownK);
+  size_t o = 0;
+  auto take = [&](size_t b) { size_t r = o; o += al16(b); return r; };
+  const size_t RR = (size_t)RB * RB;
+  L.G = take(sizeof(double) * 3 * RR);
+  L.Gp = take(sizeof(double) * 3 * RR);
+  L.Gs = take(sizeof(double) * RR);
+  L.Vi = take(sizeof(double) * RR);
+  L.W1 = take(sizeof(double) * 2 * RR);       // W1 | W2 (Gauss-Jordan / pinv scratch)
+  L.lam = take(sizeof(double) * RB);
+  L.sc = take(sizeof(double) * 64);
+  L.bars = take(sizeof(unsigned long long) * kTS * 16);
+  L.P = take(sizeof(double) * (size_t)(nI > nJ ? nI : nJ) * RB);
+  L.Xun = take(sizeof(double) * (size_t)mrows * RB);
+  L.Xun2 = take(sizeof(double) * (size_t)L.ownK * RB);
+  L.Msh = take(sizeof(double) * (size_t)mrows * RB);
+  L.U0s = take(sizeof(float) * (size_t)nI * RB);
+  L.U1s = take(sizeof(float) * (size_t)nJ * RB);
+  L.U2s = take(sizeof(float) * (size_t)L.ownK * RB);
+  L.Wt = take(sizeof(float) * (size_t)L.NT * nJ * RB);   // per-team Khatri-Rao rows (pass A)
+  // per-team TMA rings (kTS stages of whole rows, at least one row of the wider layout); the
+  // rings double as the end-of-pass reduction buffer (2 * RB * kCT floats)
+  const int rowmax = pitch4(nI > nJ ? nI : nJ);
+  L.stage_fl = stage_fl > rowmax ? stage_fl : rowmax;
+  const size_t ring = sizeof(float) * (size_t)L.NT * kTS * L.stage_fl;
+  const size_t red = sizeof(float) * (size_t)2 * RB * kCT;
+  L.stage = take(ring > red ? ring : red);
+  L.total = o;
+  return L;
+}
+
+// ---- mbarrier / TMA bulk-copy helpers (cp.async.bulk, sm_90+) ----------------------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int RB>
+__device__ __forceinline__ void ld_row(const float* p, float (&w)[RB]) {
+#pragma unroll
+  for (int f4 = 0; f4 < RB / 4; ++f4) {
+    const float4 v = reinterpret_cast<const float4*>(p)[f4];
+    w[4 * f4 + 0] = v.x; w[4 * f4 + 1] = v.y; w[4 * f4 + 2] = v.z; w[4 * f4 + 3] = v.w;
+  }
+}
+
+// Sum over the cluster's CTAs (fixed rank order) of element idx of an exported smem array;
+// the CS remote loads are issued before the ordered additions.
+__device__ __noinline__ double cluster_sum(double* local, int idx, int CS) {
+  cg::cluster_group cl = cg::this_cluster();
+  double v[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) v[c] = c < CS ? cl.map_shared_rank(local, c)[idx] : 0.0;
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 16; ++c)
+    if (c < CS) s += v[c];
+  return s;
+}
+
+// Inverse of the SPD R x R matrix V (R-stride) by Gauss-Jordan without pivoting in one warp
+// (every pivot of an SPD matrix is positive; a non-positive pivot means "not positive
+// definite" -> pseudo-inverse fallback, R12).  Ag: R x 2R scratch, fc: R doubles.
+__device__ __noinline__ bool warp_spd_inverse(const double* V, double* Vi, double* Ag, double* fc,
+                                              int R) {
+  const int lane = threadIdx.x & 31;
+  const int W = 2 * R;
+  for (int e = lane; e < R * W; e += 32) {
+    const int i = e / W, c = e - i * W;
+    Ag[e] = c < R ? V[i * R + c] : (c - R == i ? 1.0 : 0.0);
+  }
+  __syncwarp();
+  bool ok = true;
+  for (int j = 0; j < R; ++j) {
+    const double piv = Ag[j * W + j];
+    if (!(piv > 0.0)) { ok = false; break; }
+    for (int i = lane; i < R; i += 32) fc[i] = Ag[i * W + j];
+    __syncwarp();
+    const double rp = 1.0 / piv;
+    for (int c = lane; c < W; c += 32) Ag[j * W + c] *= rp;
+    __syncwarp();
+    for (int e = lane; e < R * W; e += 32) {
+      const int i = e / W, c = e - i * W;
+      if (i != j) Ag[e] -= fc[i] * Ag[j * W + c];
+    }
+    __syncwarp();
+  }
+  if (ok)
+    for (int e = lane; e < R * R; e += 32) {
+      const int i = e / R, c = e - i * R;
+      Vi[e] = Ag[i * W + R + c];
+    }
+  __syncwarp();
+  return ok;
+}
+
+// Register Gauss-Jordan for R <= RB <= 16: lane c < 2R holds column c of [V | I] in
+// registers; step j broadcasts the pivot and the R entries of column j by shuffles.
+template <int RB>
+__device__ __forceinline__ bool warp_spd_inverse_reg(const double* V, double* Vi, int R) {
+  const int lane = threadIdx.x & 31;
+  double col[RB];
+#pragma unroll
+  for (int i = 0; i < RB; ++i) {
+    double v = 0.0;
+    if (i < R) v = lane < R ? V[i * R + lane] : (lane - R == i ? 1.0 : 0.0);
+    col[i] = v;
+  }
+  bool ok = true;
+#pragma unroll
+  for (int j = 0; j < RB; ++j) {
+    if (j < R) {
+      const double piv = __shfl_sync(0xffffffffu, col[j], j);
+      ok = ok && (piv > 0.0);
+      double fcol[RB];
+#pragma unroll
+      for (int i = 0; i < RB; ++i) fcol[i] = __shfl_sync(0xffffffffu, col[i], j);
+      col[j] = col[j] / piv;
+#pragma unroll
+      for (int i = 0; i < RB; ++i)
+        if (i < R && i != j) col[i] = fma(-fcol[i], col[j], col[i]);
+    }
+  }
+  if (ok && lane >= R && lane < 2 * R)
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+      if (i < R) Vi[i * R + (lane - R)] = col[i];
+  __syncwarp();
+  return ok;
+}
+
+// Warp 0: Vi = (G_o1 * G_o2)^-1 for mode m (Hadamard of the other two normalised Grams).
+template <int RB>
+__device__ __noinline__ void warp_normal_inverse(const double* G, int m, int R, double* Vm,
+                                                 double* Vi, double* W1, double* fc, int* flags) {
+  const int lane = threadIdx.x & 31;
+  const int o1 = m == 0 ? 1 : 0, o2 = m == 2 ? 1 : 2;
+  for (int idx = lane; idx < R * R; idx += 32) Vm[idx] = G[o1 * RB * RB + idx] * G[o2 * RB * RB + idx];
+  __syncwarp();
+  bool ok;
+  if constexpr (RB <= 16) ok = warp_spd_inverse_reg<RB>(Vm, Vi, R);
+  else ok = warp_spd_inverse(Vm, Vi, W1, fc, R);
+  if (!ok && lane == 0) {
+    pinv_R(Vm, Vi, R, W1, W1 + RB * RB);
+    *flags |= 1;
+  }
+  __syncwarp();
+}
+
+#ifdef SBT_ALS_PHASES
+__device__ unsigned long long g_als_phase[32];
+#define PH(k)                                                                            \
+  do {                                                                                   \
+    if (tid == 0 && rep == 0 && rank == 0) {                                             \
+      const long long t_ = clock64();                                                    \
+      atomicAdd(&g_als_phase[k], (unsigned long long)(t_ - ph_t));                       \
+      ph_t = t_;                                                                         \
+    }                                                                                    \
+  } while (0)
+#else
+#define PH(k) do { } while (0)
+#endif
+
+__device__ __forceinline__ void team_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// One streaming pass over the CTA's own slices of a layout Src[u][row][col] (row pitch
+// `pitch` floats, multiple of 4, zero padded; slices contiguous).  Team t (T threads, one
+// per column pair) owns the slices t, t+NT, ... and streams them through its own kTS-deep
+// TMA ring (its thread 0 issues cp.async.bulk copies of whole-row stages; the team syncs
+// on a named barrier), so every thread sees whole columns and no reduction inside a slice
+// is needed:
+//   Pass A (!PASSB): acc(c,f) += Src(u,q,col_c) W_u(q,f), W_u(q,f) = U1(q,f) U2(u,f) (the
+//     Khatri-Rao rows, built per slice in the team's smem); fp32 per slice, tot += acc.
+//   Pass B (PASSB):  acc(c,f) += Src(u,p,col_c) U0(p,f) = D(u,col_c,f), stored (fp32,
+//     global); tot(c,f) += U2(u,f) D(u,col_c,f).
+// At the end P(col,f) = sum over the teams (fixed order, fp64) of tot.  tseq: stages this
+// team has consumed so far (same value in every thread of the team).
+template <int RB, bool PASSB>
+__device__ __noinline__ void team_pass(const float* __restrict__ region, int nu, int nrow, int ncol,
+                                       int pitch, const float* Uw, const float* U2s, float* Wt,
+                                       float* rings, int stage_fl, unsigned long long* bars,
+                                       int T, int NT, unsigned tseq, float* Dg, double* P) {
+  const int tid = threadIdx.x;
+  const int team = tid / T, lt = tid - team * T;
+  const bool in_team = team < NT;
+  const bool valid = in_team && 2 * lt < pitch;
+  const int trmax = stage_fl / pitch > 0 ? stage_fl / pitch : 1;
+  const int nch = (nrow + trmax - 1) / trmax;
+  const int tr = (nrow + nch - 1) / nch;
+  const int nsl = in_team && team < nu ? (nu - team + NT - 1) / NT : 0;   // slices of this team
+  const int total = nsl * nch;
+  float* ring = rings + (size_t)(in_team ? team : 0) * kTS * stage_fl;
+  unsigned long long* tb = bars + (in_team ? team : 0) * kTS;
+  float* W = Wt + (size_t)(in_team ? team : 0) * nrow * RB;
+  const int bar_id = 1 + team;
+  auto issue = [&](int s) {
+    const int ul = team + (s / nch) * NT, k = s % nch;
+    const int r0 = k * tr, nr = min(tr, nrow - r0);
+    const unsigned buf = (tseq + s) % kTS;
+    const unsigned bytes = (unsigned)(nr * pitch * sizeof(float));
+    mbar_expect_tx(&tb[buf], bytes);
+    bulk_g2s(ring + buf * stage_fl, region + ((int64_t)ul * nrow + r0) * pitch, bytes, &tb[buf]);
+  };
+  if (lt == 0 && total > 0) {
+    fence_proxy_async();
+    for (int s = 0; s < total && s < kTS; ++s) issue(s);
+  }
+  auto build_w = [&](int ul) {   // W_u = U1 * U2(u)   (pass A)
+    for (int e = lt; e < nrow * RB; e += T) W[e] = Uw[e] * U2s[ul * RB + (e % RB)];
+  };
+  if (!PASSB && total > 0) {
+    build_w(team);
+    team_bar(bar_id, T);
+  }
+  float acc[2][RB], tot[2][RB];
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int f = 0; f < RB; ++f) { acc[c][f] = 0.f; tot[c][f] = 0.f; }
+  const float* Wr = PASSB ? Uw : W;
+  for (int s = 0; s < total; ++s) {
+    const int ul = team + (s / nch) * NT, k = s % nch;
+    const int r0 = k * tr, nr = min(tr, nrow - r0);
+    const unsigned buf = (tseq + s) % kTS;
+    mbar_wait(&tb[buf], ((tseq + s) / kTS) & 1u);
+    if (valid) {
+      const float* st = ring + buf * stage_fl + 2 * lt;
+      const float* wr = Wr + r0 * RB;
+#pragma unroll 4
+      for (int row = 0; row < nr; ++row) {
+        const float2 y = *reinterpret_cast<const float2*>(st + row * pitch);
+        float w[RB];
+        ld_row<RB>(wr + row * RB, w);
+#pragma unroll
+        for (int f = 0; f < RB; ++f) {
+          acc[0][f] = fmaf(y.x, w[f], acc[0][f]);
+          acc[1][f] = fmaf(y.y, w[f], acc[1][f]);
+        }
+      }
+    }
+    const bool slice_end = k == nch - 1;
+    if (slice_end && valid) {
+      if (!PASSB) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int f = 0; f < RB; ++f) { tot[c][f] += acc[c][f]; acc[c][f] = 0.f; }
+      } else {
+        float u2[RB];
+        ld_row<RB>(U2s + ul * RB, u2);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int col = 2 * lt + c;
+          if (col < ncol) {
+            float* d = Dg + ((int64_t)ul * ncol + col) * RB;
+#pragma unroll
+            for (int f4 = 0; f4 < RB / 4; ++f4)
+              reinterpret_cast<float4*>(d)[f4] = make_float4(acc[c][4 * f4], acc[c][4 * f4 + 1],
+                                                             acc[c][4 * f4 + 2], acc[c][4 * f4 + 3]);
+          }
+#pragma unroll
+          for (int f = 0; f < RB; ++f) { tot[c][f] = fmaf(u2[f], acc[c][f], tot[c][f]); acc[c][f] = 0.f; }
+        }
+      }
+    }
+    team_bar(bar_id, T);   // stage (and, at a slice end, W) consumed by the whole team
+    if (!PASSB && slice_end && s + 1 < total) {
+      build_w(ul + NT);
+      team_bar(bar_id, T);
+    }
+    if (lt == 0 && s + kTS < total) {
+      fence_proxy_async();
+      issue(s + kTS);
+    }
+  }
+  __syncthreads();   // every team done: rings free (no copy in flight) -> reduction buffer
+  float* red = rings;
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int f = 0; f < RB; ++f) red[(c * RB + f) * kCT + tid] = tot[c][f];
+  __syncthreads();
+  for (int e = tid; e < ncol * RB; e += kCT) {
+    const int col = e / RB, f = e - col * RB;
+    const float* rr = red + ((col & 1) * RB + f) * kCT + (col >> 1);
+    double v[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = t < NT ? (double)rr[t * T] : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      if (t < NT) sum += v[t];
+    P[e] = sum;
+  }
+}
+
+// stages a team consumes in one pass (the same formula as in team_pass)
+__device__ __forceinline__ int team_stages(int team, int nu, int NT, int nrow, int pitch, int stage_fl) {
+  const int trmax = stage_fl / pitch > 0 ? stage_fl / pitch : 1;
+  const int nch = (nrow + trmax - 1) / trmax;
+  const int nsl = team < nu ? (nu - team + NT - 1) / NT : 0;
+  return nsl * nch;
+}
+
+template <int RB>
+__global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS, float* Dglob,
+                                                             int stage_fl) {
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int rep = blockIdx.x / CS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int R = a.R, nI = a.nI, nJ = a.nJ, nK = a.nK;
+  const ClLayout Ly = cl_layout(nI, nJ, nK, RB, CS, stage_fl);
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* G = reinterpret_cast<double*>(smem + Ly.G);        // [3][RB*RB] normalised Grams (R-stride)
+  double* Gp = reinterpret_cast<double*>(smem + Ly.Gp);      // [3][RB*RB] partial Grams (exported)
+  double* Gs = reinterpret_cast<double*>(smem + Ly.Gs);
+  double* Vi = reinterpret_cast<double*>(smem + Ly.Vi);
+  double* W1 = reinterpret_cast<double*>(smem + Ly.W1);
+  double* lam = reinterpret_cast<double*>(smem + Ly.lam);
+  double* sc = reinterpret_cast<double*>(smem + Ly.sc);      // [0] ysq, [1] inner (exported)
+  double* P = reinterpret_cast<double*>(smem + Ly.P);        // partial MTTKRP (exported)
+  double* Xun = reinterpret_cast<double*>(smem + Ly.Xun);    // solved chunk rows (exported)
+  double* Xun2 = reinterpret_cast<double*>(smem + Ly.Xun2);  // solved mode-2 rows (local)
+  double* Msh = reinterpret_cast<double*>(smem + Ly.Msh);
+  float* U0s = reinterpret_cast<float*>(smem + Ly.U0s);
+  float* U1s = reinterpret_cast<float*>(smem + Ly.U1s);
+  float* U2s = reinterpret_cast<float*>(smem + Ly.U2s);
+  float* ring = reinterpret_cast<float*>(smem + Ly.stage);
+  float* Wt = reinterpret_cast<float*>(smem + Ly.Wt);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + Ly.bars);
+  __shared__ double s_fc[kMaxR];
+  __shared__ double s_red[32];
+  __shared__ int s_flags, s_stop;
+  __shared__ double s_fit;
+#ifdef SBT_ALS_PHASES
+  long long ph_t = clock64();
+#endif
+
+  const float* Y = a.Y + (int64_t)rep * a.y_stride;
+  const float* Yt = a.Yt + (int64_t)rep * a.y_stride;
+  const int u0 = min(nK, rank * Ly.ownK), u1 = min(nK, u0 + Ly.ownK);
+  const int nu = u1 - u0;
+  const int pI = pitch4(nI), pJ = pitch4(nJ);
+  // own regions of the two layouts (16 B aligned: pitches and y_stride are multiples of 4)
+  const float* regA = Y + (int64_t)u0 * nJ * pI;
+  const float* regB = Yt + (int64_t)u0 * nI * pJ;
+  float* D = Dglob + ((int64_t)rep * nK + u0) * nJ * RB;   // D of the own slices (L2-resident)
+  const int myteam = tid / Ly.T;
+  unsigned tseq = 0;                                       // TMA stages this team consumed
+  float* gU0 = a.U[0] + rep * a.u_stride[0];
+  float* gU1 = a.U[1] + rep * a.u_stride[1];
+  float* gU2 = a.U[2] + rep * a.u_stride[2];
+  const int RR = R * R;
+
+  // ---- initial factors (zero-padded to RB columns), Grams, ||Y||^2 -------------------------
+  for (int e = tid; e < nI * RB; e += kCT) {
+    const int p = e / RB, f = e - p * RB;
+    U0s[e] = f < R ? gU0[(int64_t)p * R + f] : 0.f;
+  }
+  for (int e = tid; e < nJ * RB; e += kCT) {
+    const int q = e / RB, f = e - q * RB;
+    U1s[e] = f < R ? gU1[(int64_t)q * R + f] : 0.f;
+  }
+  for (int e = tid; e < nu * RB; e += kCT) {
+    const int ul = e / RB, f = e - ul * RB;
+    U2s[e] = f < R ? gU2[(int64_t)(u0 + ul) * R + f] : 0.f;
+  }
+  if (tid == 0) {
+    s_flags = 0; s_stop = 0;
+    for (int b = 0; b < kTS * 16; ++b) mbar_init(&bars[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int pr = tid; pr < 3 * RR; pr += kCT) {
+    const int m = pr / RR, fg = pr - m * RR, f = fg / R, g = fg - f * R;
+    double s = 0.0;
+    if (m == 0) for (int p = 0; p < nI; ++p) s += (double)U0s[p * RB + f] * (double)U0s[p * RB + g];
+    if (m == 1) for (int q = 0; q < nJ; ++q) s += (double)U1s[q * RB + f] * (double)U1s[q * RB + g];
+    if (m == 2) for (int u = 0; u < nK; ++u) s += (double)gU2[(int64_t)u * R + f] * (double)gU2[(int64_t)u * R + g];
+    G[m * RB * RB + fg] = s;
+  }
+  {
+    double s = 0.0;
+    const int tot = nu * nJ * nI;
+    for (int e = tid; e < tot; e += kCT) {
+      const int row = e / nI, p = e - row * nI;
+      const double v = regA[(int64_t)row * pI + p];
+      s += v * v;
+    }
+    s = block_sum_d(s, s_red);
+    if (tid == 0) sc[0] = s;
+  }
+  cluster.sync();
+  const double ysq = cluster_sum(sc, 0, CS);
+  PH(0);
+
+  double fit = 0.0, fit_prev = 0.0;
+  int it = 0;
+#pragma unroll 1
+  for (;;) {
+    // ================================ mode 0 and mode 1 ================================
+#pragma unroll 1
+    for (int m = 0; m < 2; ++m) {
+      const int n = m == 0 ? nI : nJ;
+      const int ch = m == 0 ? Ly.chunk0 : Ly.chunk1;
+      // warp 0: Vi = (G_o1 * G_o2)^-1 while the other warps stream
+      if (warp == 0) warp_normal_inverse<RB>(G, m, R, Gs, Vi, W1, s_fc, &s_flags);
+      if (m == 0) {
+        team_pass<RB, false>(regA, nu, nJ, nI, pI, U1s, U2s, Wt, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
+                             tseq, D, P);
+        if (myteam < Ly.NT) tseq += team_stages(myteam, nu, Ly.NT, nJ, pI, Ly.stage_fl);
+        __syncthreads();   // the rings (reduction buffer) are re-armed by the next pass
+        PH(1);
+      } else {
+        team_pass<RB, true>(regB, nu, nI, nJ, pJ, U0s, U2s, Wt, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
+                            tseq, D, P);
+        if (myteam < Ly.NT) tseq += team_stages(myteam, nu, Ly.NT, nI, pJ, Ly.stage_fl);
+        __syncthreads();
+        // D rows written by other threads (global) are read in mode 2
+        PH(6);
+      }
+      cluster.sync();   // S1: partials of every CTA complete
+      PH(m == 0 ? 2 : 8);
+      // ---- rows [c0, c1) of this mode: sum the CS partials, solve, partial Gram ----
+      const int c0 = min(n, rank * ch), c1 = min(n, c0 + ch);
+      const int nr = c1 - c0;
+#pragma unroll 1
+      for (int e = tid; e < nr * R; e += kCT) {
+        const int pl = e / R, f = e - pl * R;
+        Msh[pl * RB + f] = cluster_sum(P, (c0 + pl) * RB + f, CS);
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int e = tid; e < nr * R; e += kCT) {
+        const int pl = e / R, f = e - pl * R;
+        double s = 0.0;
+        for (int g = 0; g < R; ++g) s += Msh[pl * RB + g] * Vi[g * R + f];
+        Xun[pl * RB + f] = s;
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int pr = tid; pr < RR; pr += kCT) {
+        const int f = pr / R, g = pr - f * R;
+        double s = 0.0;
+        for (int pl = 0; pl < nr; ++pl) s += Xun[pl * RB + f] * Xun[pl * RB + g];
+        Gp[m * RB * RB + pr] = s;
+      }
+      PH(m == 0 ? 3 : 9);
+      cluster.sync();   // S2: solved rows and partial Grams of every CTA complete
+      PH(m == 0 ? 4 : 10);
+#pragma unroll 1
+      for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = cluster_sum(Gp, m * RB * RB + pr, CS);
+      __syncthreads();
+      if (tid < R) lam[tid] = sqrt(Gs[tid * R + tid]);
+      __syncthreads();
+#pragma unroll 1
+      for (int pr = tid; pr < RR; pr += kCT) {
+        const int f = pr / R, g = pr - f * R;
+        const double lf = lam[f] > 0.0 ? lam[f] : 1.0, lg = lam[g] > 0.0 ? lam[g] : 1.0;
+        G[m * RB * RB + pr] = Gs[pr] / (lf * lg);
+      }
+      float* Us = m == 0 ? U0s : U1s;
+#pragma unroll 1
+      for (int e = tid; e < n * R; e += kCT) {
+        const int p = e / R, f = e - p * R;
+        const int c = p / ch;
+        const double x = cluster.map_shared_rank(Xun, c)[(p - c * ch) * RB + f];
+        const double l = lam[f];
+        Us[p * RB + f] = __double2float_rn(l > 0.0 ? x / l : x);
+      }
+      __syncthreads();
+      PH(m == 0 ? 5 : 11);
+    }
+    // ==================================== mode 2 ====================================
+    if (warp == 0) warp_normal_inverse<RB>(G, 2, R, Gs, Vi, W1, s_fc, &s_flags);
+    // M2(u,f) = sum_q D(u,q,f) U1(q,f) for the own slices: warp per (u, f-group of 4)
+    {
+      const int nfg = RB / 4;
+#pragma unroll 1
+      for (int wi = warp; wi < nu * nfg; wi += kCW) {
+        const int ul = wi / nfg, f4 = wi - ul * nfg;
+        const float* d = D + (int64_t)ul * nJ * RB + 4 * f4;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int q = lane; q < nJ; q += 32) {
+          const float4 dv = *reinterpret_cast<const float4*>(d + (int64_t)q * RB);
+          const float4 uv = *reinterpret_cast<const float4*>(U1s + q * RB + 4 * f4);
+          s0 += (double)dv.x * (double)uv.x; s1 += (double)dv.y * (double)uv.y;
+          s2 += (double)dv.z * (double)uv.z; s3 += (double)dv.w * (double)uv.w;
+        }
+        s0 = warp_sum_d(s0); s1 = warp_sum_d(s1); s2 = warp_sum_d(s2); s3 = warp_sum_d(s3);
+        if (lane == 0) {
+          double* mr = Msh + ul * RB + 4 * f4;
+          mr[0] = s0; mr[1] = s1; mr[2] = s2; mr[3] = s3;
+        }
+      }
+    }
+    __syncthreads();
+    PH(12);
+#pragma unroll 1
+    for (int e = tid; e < nu * R; e += kCT) {
+      const int ul = e / R, f = e - ul * R;
+      double s = 0.0;
+      for (int g = 0; g < R; ++g) s += Msh[ul * RB + g] * Vi[g * R + f];
+      Xun2[ul * RB + f] = s;
+    }
+    __syncthreads();
+    {
+      double inner = 0.0;
+      for (int e = tid; e < nu * R; e += kCT) {
+        const int ul = e / R, f = e - ul * R;
+        inner += Xun2[ul * RB + f] * Msh[ul * RB + f];
+      }
+      inner = block_sum_d(inner, s_red);
+      if (tid == 0) sc[1] = inner;
+    }
+#pragma unroll 1
+    for (int pr = tid; pr < RR; pr += kCT) {
+      const int f = pr / R, g = pr - f * R;
+      double s = 0.0;
+      for (int ul = 0; ul < nu; ++ul) s += Xun2[ul * RB + f] * Xun2[ul * RB + g];
+      Gp[2 * RB * RB + pr] = s;
+    }
+    PH(13);
+    cluster.sync();   // S3
+    PH(14);
+#pragma unroll 1
+    for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = cluster_sum(Gp, 2 * RB * RB + pr, CS);
+    __syncthreads();
+    if (tid < R) lam[tid] = sqrt(Gs[tid * R + tid]);
+    __syncthreads();
+#pragma unroll 1
+    for (int pr = tid; pr < RR; pr += kCT) {
+      const int f = pr / R, g = pr - f * R;
+      const double lf = lam[f] > 0.0 ? lam[f] : 1.0, lg = lam[g] > 0.0 ? lam[g] : 1.0;
+      G[2 * RB * RB + pr] = Gs[pr] / (lf * lg);
+    }
+#pragma unroll 1
+    for (int e = tid; e < nu * R; e += kCT) {
+      const int ul = e / R, f = e - ul * R;
+      const double l = lam[f];
+      const double x = Xun2[ul * RB + f];
+      U2s[ul * RB + f] = __double2float_rn(l > 0.0 ? x / l : x);
+    }
+    __syncthreads();
+    // fit (warp 0; every CTA computes the same value -> uniform control flow)
+    if (warp == 0) {
+      double mn = 0.0;
+      for (int pr = lane; pr < RR; pr += 32) {
+        const int f = pr / R, g = pr - f * R;
+        mn += lam[f] * lam[g] * G[pr] * G[RB * RB + pr] * G[2 * RB * RB + pr];
+      }
+      mn = warp_sum_d(mn);
+      const double inner = lane == 0 ? cluster_sum(sc, 1, CS) : 0.0;
+      if (lane == 0) {
+        const double res = fmax(0.0, ysq - 2.0 * inner + mn);
+        const double f = ysq > 0.0 ? 1.0 - sqrt(res) / sqrt(ysq) : 0.0;
+        s_fit = f;
+        const int itn = it + 1;
+        int stop = itn >= a.maxit;
+        if (itn >= 2 && fabs(f - fit) < a.tol) stop = 1;
+        if (!isfinite(f)) { stop = 1; s_flags |= 2; }
+        s_stop = stop;
+      }
+    }
+    __syncthreads();
+    fit_prev = fit;
+    fit = s_fit;
+    ++it;
+    PH(15);
+    if (s_stop) break;
+  }
+  // ---- write back: U0 / U1 chunks, own U2 rows, lambda, fit, iterations -------------------
+  {
+    const int c0 = min(nI, rank * Ly.chunk0), c1 = min(nI, c0 + Ly.chunk0);
+    for (int e = tid; e < (c1 - c0) * R; e += kCT) {
+      const int pl = e / R, f = e - pl * R;
+      gU0[(int64_t)(c0 + pl) * R + f] = U0s[(c0 + pl) * RB + f];
+    }
+    const int d0 = min(nJ, rank * Ly.chunk1), d1 = min(nJ, d0 + Ly.chunk1);
+    for (int e = tid; e < (d1 - d0) * R; e += kCT) {
+      const int ql = e / R, f = e - ql * R;
+      gU1[(int64_t)(d0 + ql) * R + f] = U1s[(d0 + ql) * RB + f];
+    }
+    for (int e = tid; e < nu * R; e += kCT) {
+      const int ul = e / R, f = e - ul * R;
+      gU2[(int64_t)(u0 + ul) * R + f] = U2s[ul * RB + f];
+    }
+  }
+  if (rank == 0) {
+    if (tid < R) a.lam[rep * R + tid] = lam[tid];
+    for (int pr = tid; pr < 3 * RR; pr += kCT) {
+      const int m = pr / RR, fg = pr - m * RR;
+      a.G[(int64_t)rep * 3 * RR + pr] = G[m * RB * RB + fg];
+    }
+    if (tid == 0) {
+      a.fit[rep] = fit; a.fit_prev[rep] = fit_prev; a.iters[rep] = it; a.flags[rep] = s_flags;
+      a.ysq[rep] = ysq; a.done[rep] = 1;
+    }
+  }
+  cluster.sync();   // keep every CTA's shared memory alive until all remote reads are done
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------
+constexpr size_t kSmemCap = 227 * 1024 - 1024;   // minus the kernel's static smem
+
+static int rb_of(int R) { return R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32; }
+
+template <int RB>
+static cudaError_t cluster_setup(int CS, size_t smem) {
+  auto k = als_cluster_kernel<RB>;
+  (void)smem;   // always allow the cap: plans of several shapes share the kernel
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
+  if (e != cudaSuccess) return e;
+  if (CS > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return e;
+}
+
+static void fill_cfg(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* attr, int CS, int nclusters,
+                     size_t smem, cudaStream_t st) {
+  *cfg = cudaLaunchConfig_t{};
+  cfg->gridDim = dim3((unsigned)(CS * nclusters), 1, 1);
+  cfg->blockDim = dim3(kCT, 1, 1);
+  cfg->dynamicSmemBytes = smem;
+  cfg->stream = st;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg->attrs = attr;
+  cfg->numAttrs = 1;
+}
+
+
+template <int RB>
+static bool plan_rb(const DenseAls& a, ClusterPlan* pl) {
+  if (a.nI > 2 * kCT || a.nJ > 2 * kCT) return false;
+  // the stage size: what is left of the smem budget, split over kNS stages, capped at one
+  // slice of the larger layout and at 48 KB
+  double best = 1e300;
+  bool found = false;
+  for (int CS = 16; CS >= 1; --CS) {
+    if (CS > a.nK) continue;
+    const ClLayout L0 = cl_layout(a.nI, a.nJ, a.nK, RB, CS, 4);
+    const size_t fixed = L0.stage;   // the rings are the last region of the layout
+    if (fixed + sizeof(float) * 2 * RB * kCT > kSmemCap) continue;
+    const int slice_fl = pitch4(a.nI > a.nJ ? a.nI : a.nJ) * (a.nI > a.nJ ? a.nJ : a.nI);
+    int sfl = (int)((kSmemCap - fixed) / (sizeof(float) * kTS * L0.NT)) & ~3;
+    if (sfl > ((slice_fl + 3) & ~3)) sfl = (slice_fl + 3) & ~3;
+    if (sfl > 12288) sfl = 12288;
+    ClLayout L = cl_layout(a.nI, a.nJ, a.nK, RB, CS, sfl);
+    if (L.total > kSmemCap) continue;
+    if (cluster_setup<RB>(CS, L.total) != cudaSuccess) { cudaGetLastError(); continue; }
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute attr[1];
+    fill_cfg(&cfg, attr, CS, 1, L.total, nullptr);
+    int act = 0;
+    if (cudaOccupancyMaxActiveClusters(&act, als_cluster_kernel<RB>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      act = 0;
+    }
+    if (act < 1) continue;
+    // time ~ waves * slices per team
+    const double waves = (double)((a.r + act - 1) / act);
+    const int nu = (a.nK + CS - 1) / CS;
+    // ties: fewer waves, then the smaller cluster (cheaper DSMEM reductions)
+    const double t = waves * (double)((nu + L.NT - 1) / L.NT) + 1e-3 * waves + 1e-5 * CS;
+    if (t < best) {
+      best = t;
+      found = true;
+      pl->CS = CS;
+      pl->smem = L.total;
+      pl->act = act;
+      pl->RB = RB;
+      pl->stage_fl = L.stage_fl;
+    }
+  }
+  return found;
+}
+
+bool plan_als_cluster(const DenseAls& a, ClusterPlan* pl) {
+  if (a.r < 1 || a.nI < 1 || a.nJ < 1 || a.nK < 1 || !a.Yt) return false;
+  switch (rb_of(a.R)) {
+    case 4: return plan_rb<4>(a, pl);
+    case 8: return plan_rb<8>(a, pl);
+    case 12: return plan_rb<12>(a, pl);
+    case 16: return plan_rb<16>(a, pl);
+    case 24: return plan_rb<24>(a, pl);
+    default: return plan_rb<32>(a, pl);
+  }
+}
+
+size_t als_cluster_dscratch_bytes(const DenseAls& a, const ClusterPlan& pl) {
+  return sizeof(float) * (size_t)a.r * ((size_t)a.nK + pl.CS) * a.nJ * pl.RB;
+}
+
+int cluster_pitch(int n) { return pitch4(n); }
+
+#ifdef SBT_ALS_PHASES
+void als_phase_dump() {
+  unsigned long long h[32];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, g_als_phase, sizeof(h));
+  fprintf(stderr, "[sambaten] als phases (cycles, rank 0 of rep 0):");
+  for (int k = 0; k < 16; ++k) fprintf(stderr, " %d:%llu", k, h[k]);
+  fprintf(stderr, "\n");
+  memset(h, 0, sizeof(h));
+  cudaMemcpyToSymbol(g_als_phase, h, sizeof(h));
+}
+#else
+void als_phase_dump() {}
+#endif
+
+template <int RB>
+static cudaError_t cluster_launch(const DenseAls& a, const ClusterPlan& pl, float* Dglob,
+                                  cudaStream_t st) {
+  cudaLaunchConfig_t cfg;
+  cudaLaunchAttribute attr[1];
+  fill_cfg(&cfg, attr, pl.CS, a.r, pl.smem, st);
+  return cudaLaunchKernelEx(&cfg, als_cluster_kernel<RB>, a, pl.CS, Dglob, pl.stage_fl);
+}
+
+cudaError_t run_als_cluster(const DenseAls& a, const ClusterPlan& pl, float* Dglob, cudaStream_t st) {
+  switch (pl.RB) {
+    case 4: return cluster_launch<4>(a, pl, Dglob, st);
+    case 8: return cluster_launch<8>(a, pl, Dglob, st);
+    case 12: return cluster_launch<12>(a, pl, Dglob, st);
+    case 16: return cluster_launch<16>(a, pl, Dglob, st);
+    case 24: return cluster_launch<24>(a, pl, Dglob, st);
+    default: return cluster_launch<32>(a, pl, Dglob, st);
+  }
+}
+
+}  // namespace sbt

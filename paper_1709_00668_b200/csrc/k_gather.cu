@@ -1,10 +1,11 @@
 // k_gather.cu -- a3 (dense): the summaries X_s = X(I_s, J_s, K_s U new).
 //
-// Y[rep][u][q][p] = X(Is[p], Js[q], Kp[u]).  One warp per output row (rep, u, q): the lanes
-// walk the sorted I_s list (held in shared memory for the block's repetition) and load
-// X at those columns of source row (Kp[u], Js[q]).  Sorted indices make neighbouring lanes
-// share 32 B sectors; output rows are written contiguously.  Pure data movement: the
-// summary is a bit-exact copy.
+// Y[rep][u][q][p] = X(Is[p], Js[q], Kp[u]) and, for the cluster ALS, its per-slice transpose
+// Yt[rep][u][p][q].  Block = (32-row q tile, slice u, rep); for each 32-column p tile the
+// 8 warps gather 4 source rows each (lanes walk the sorted I_s list held in shared memory,
+// so neighbouring lanes share 32 B sectors of the source row), write the Y rows coalesced
+// and stage the 32 x 32 block in shared memory (padded, conflict-free) for the coalesced Yt
+// rows.  Pure data movement: both layouts are bit-exact copies.
 #include "common.cuh"
 #include "internal.h"
 
@@ -15,43 +16,61 @@ constexpr int kGatherThreads = 256;
 __global__ void __launch_bounds__(kGatherThreads) gather_dense_kernel(
     const float* __restrict__ X, int64_t J, int64_t pitch, const int32_t* __restrict__ Is,
     const int32_t* __restrict__ Js, const int32_t* __restrict__ Kp, int nI, int nJ, int nK,
-    int64_t sI, int64_t sJ, int64_t sK, float* __restrict__ Y, int64_t y_stride,
-    int rows_per_block) {
+    int64_t sI, int64_t sJ, int64_t sK, float* __restrict__ Y, float* __restrict__ Yt,
+    int64_t y_stride, int pI, int pJ) {
   extern __shared__ int32_t is_sh[];
-  const int rep = blockIdx.y;
+  __shared__ float tile[32][33];
+  const int qt = blockIdx.x, u = blockIdx.y, rep = blockIdx.z;
   const int32_t* is = Is + rep * sI;
   for (int p = threadIdx.x; p < nI; p += blockDim.x) is_sh[p] = is[p];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nrows = (int64_t)nK * nJ;
-  const int64_t rb = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t re = min(rb + rows_per_block, nrows);
-  float* Yr = Y + rep * y_stride;
+  const int q0 = qt * 32;
+  const int nq = min(32, nJ - q0);
   const int32_t* js = Js + rep * sJ;
-  const int32_t* kp = Kp + rep * sK;
-  for (int64_t row = rb + warp; row < re; row += kGatherThreads / 32) {
-    const int u = (int)(row / nJ), q = (int)(row - (int64_t)u * nJ);
-    const float* src = X + ((int64_t)kp[u] * J + js[q]) * pitch;
-    float* dst = Yr + row * nI;
-    for (int p = lane; p < nI; p += 32) dst[p] = __ldg(src + is_sh[p]);
+  const int64_t ku = Kp[rep * sK + u];
+  float* Ys = Y + rep * y_stride + (int64_t)u * nJ * pI;
+  float* Yts = Yt ? Yt + rep * y_stride + (int64_t)u * nI * pJ : nullptr;
+  const float* srow[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int ql = warp * 4 + k;
+    srow[k] = ql < nq ? X + (ku * J + js[q0 + ql]) * pitch : nullptr;
+  }
+  for (int p0 = 0; p0 < pI; p0 += 32) {
+    const int p = p0 + lane;
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = (srow[k] && p < nI) ? __ldg(srow[k] + is_sh[p]) : 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int ql = warp * 4 + k;
+      if (srow[k] && p < pI) Ys[(int64_t)(q0 + ql) * pI + p] = v[k];   // zero pad p >= nI
+      tile[ql][lane] = v[k];
+    }
+    if (Yts) {
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int pl = warp * 4 + k;   // p offset within the tile
+        if (p0 + pl < nI && q0 + lane < pJ)
+          Yts[(int64_t)(p0 + pl) * pJ + q0 + lane] = lane < nq ? tile[lane][pl] : 0.f;
+      }
+      __syncthreads();
+    }
   }
 }
 
 cudaError_t launch_gather_dense(const DenseView& X, const int32_t* Is, const int32_t* Js,
                                 const int32_t* Kp, int nI, int nJ, int nK, int r,
                                 int64_t sI, int64_t sJ, int64_t sK, float* Y, int64_t y_stride,
-                                cudaStream_t st) {
-  const int64_t nrows = (int64_t)nK * nJ;
-  if (nrows <= 0 || nI <= 0 || r <= 0) return cudaSuccess;
-  // ~4 waves of 256-thread blocks over the chip, at least 8 rows (one per warp) per block
-  int64_t want = (int64_t)kNumSMs * 8 / r;
-  if (want < 1) want = 1;
-  int64_t rpb = ceil_div(nrows, want);
-  if (rpb < 8) rpb = 8;
-  const int64_t nb = ceil_div(nrows, rpb);
-  dim3 grid((unsigned)nb, (unsigned)r);
+                                cudaStream_t st, float* Yt, int pI, int pJ) {
+  if (nK <= 0 || nJ <= 0 || nI <= 0 || r <= 0) return cudaSuccess;
+  if (pI < nI) pI = nI;
+  if (pJ < nJ) pJ = nJ;
+  dim3 grid((unsigned)ceil_div(pJ, 32), (unsigned)nK, (unsigned)r);
   gather_dense_kernel<<<grid, kGatherThreads, sizeof(int32_t) * nI, st>>>(
-      X.base, X.J, X.pitch, Is, Js, Kp, nI, nJ, nK, sI, sJ, sK, Y, y_stride, (int)rpb);
+      X.base, X.J, X.pitch, Is, Js, Kp, nI, nJ, nK, sI, sJ, sK, Y, Yt, y_stride, pI, pJ);
   return cudaGetLastError();
 }
 
