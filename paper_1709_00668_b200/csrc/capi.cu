@@ -38,6 +38,22 @@ using namespace sbt;
     }                                                                         \
   } while (0)
 
+// a1 / a7 dispatch: the TMA-ring streaming kernels when the view allows them (pitch % 4 == 0,
+// 16 B aligned; R <= 16 for the fit), else the tiled kernels.
+static cudaError_t marginals_any(const DenseView& V, int64_t k0, int64_t nk, int moi, int S,
+                                 int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st) {
+  if (stream_supported(V)) return launch_marginals_stream(V, k0, nk, moi, S, x1, x2, x3, st);
+  return launch_marginals_dense(V, k0, nk, moi, S, x1, x2, x3, st);
+}
+static size_t fit_ws_doubles_any(const DenseView& V) {
+  return std::max(fit_dense_ws_doubles(V), fit_stream_ws_doubles(V));
+}
+static cudaError_t fit_any(const DenseView& V, const float* lam, const float* A, const float* B,
+                           const float* C, int R, double* ws, double* relerr, cudaStream_t st) {
+  if (stream_supported(V) && R <= 16) return launch_fit_stream(V, lam, A, B, C, R, ws, relerr, st);
+  return launch_fit_dense(V, lam, A, B, C, R, ws, relerr, st);
+}
+
 static int ceil_log2_d(double v) {
   int e;
   const double m = frexp(v, &e);
@@ -93,7 +109,7 @@ struct sambaten_s {
   int64_t K_ck = -1;
   uint32_t uid_ck = 0;
   // workspaces
-  DevBuf marg, samp, summ, fac, als, match, misc, segs;
+  DevBuf marg, samp, summ, fac, als, match, misc, segs, fitws;
   SampleSeg* segs_host = nullptr;   // pinned
   HostStatus* hs = nullptr;         // pinned
   cudaEvent_t ev[9] = {};
@@ -242,7 +258,7 @@ extern "C" void sambaten_destroy(sambaten_t h) {
   h->X.release();
   h->model[0].release(); h->model[1].release(); h->ck.release();
   h->marg.release(); h->samp.release(); h->summ.release(); h->fac.release();
-  h->als.release(); h->match.release(); h->misc.release(); h->segs.release();
+  h->als.release(); h->match.release(); h->misc.release(); h->segs.release(); h->fitws.release();
   if (h->segs_host) cudaFreeHost(h->segs_host);
   if (h->hs) cudaFreeHost(h->hs);
   for (int e = 0; e < 9; ++e)
@@ -351,7 +367,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   int64_t* x2 = x1 + h->I;
   int64_t* x3 = x2 + h->J;
   CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
-  CK(launch_marginals_dense(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, st));
+  CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, st));
   CK(cudaEventRecord(h->ev[2], st));
   // ---- a2: sampling (R4-R6); K_s from the old slices only, then K' = K_s ++ new ----------
   const size_t is_b = align256(sizeof(int32_t) * r * nI), js_b = align256(sizeof(int32_t) * r * nJ);
@@ -467,13 +483,10 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   CK(cudaEventRecord(h->ev[7], st));
   // ---- a7: full fit of the new model (optional) ------------------------------------------
   if (h->opts.full_fit) {
-    DevBuf& fw = h->misc;
-    const size_t need = 128 + sizeof(double) * fit_dense_ws_doubles(V);
-    CK(fw.ensure(std::max<size_t>(4096, need)));
-    d_maxphi = fw.as<unsigned long long>();
-    d_relerr = reinterpret_cast<double*>(fw.as<char>() + 64);
-    CK(launch_fit_dense(V, h->lam(nb), h->A(nb), h->B(nb), h->C(nb), R,
-                        reinterpret_cast<double*>(fw.as<char>() + 128), d_relerr, st));
+    // separate workspace: reallocating misc here would lose the max-phi word written in a0
+    const size_t need = sizeof(double) * fit_ws_doubles_any(V);
+    CK(h->fitws.ensure(need));
+    CK(fit_any(V, h->lam(nb), h->A(nb), h->B(nb), h->C(nb), R, h->fitws.as<double>(), d_relerr, st));
   }
   CK(cudaEventRecord(h->ev[8], st));
   // ---- status readback and commit ------------------------------------------------------
@@ -515,7 +528,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     info->reps_pinv_mask = pm;
     // max_phi, marginals, sample, gather, als_init + gram + 2 sumsq, 7 per ALS iteration
     // (all iterations are launched; converged reps exit at once), match, 3 + 1 merge, 2 fit
-    info->kernel_launches = 1 + 1 + 1 + 1 + als_launches + 1 + 4 + (h->opts.full_fit ? 2 : 0);
+    info->kernel_launches = 1 + 1 + 1 + 1 + als_launches + 1 + 4 + (h->opts.full_fit ? 3 : 0);
     for (int e = 0; e < 8; ++e) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);
@@ -565,9 +578,9 @@ extern "C" sambaten_status sambaten_relative_error(sambaten_t h, double* relerr)
   if (!h || !relerr) FAIL(SAMBATEN_E_INVALID, "relative_error: NULL argument");
   DenseView V = h->view();
   DevBuf ws;
-  CK(ws.ensure(sizeof(double) * (fit_dense_ws_doubles(V) + 8)));
+  CK(ws.ensure(sizeof(double) * (fit_ws_doubles_any(V) + 8)));
   double* d = ws.as<double>();
-  CK(launch_fit_dense(V, h->lam(h->cur), h->A(h->cur), h->B(h->cur), h->C(h->cur), h->R, d + 8, d, h->st));
+  CK(fit_any(V, h->lam(h->cur), h->A(h->cur), h->B(h->cur), h->C(h->cur), h->R, d + 8, d, h->st));
   CK(cudaMemcpyAsync(relerr, d, 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   ws.release();
@@ -614,7 +627,7 @@ extern "C" sambaten_status sambaten_marginals(const sambaten_tensor* X, int moi,
   CK(cudaMemsetAsync(x3, 0, sizeof(int64_t) * X->dims[2], st));
   if (X->fmt == SAMBATEN_DENSE) {
     if (X->dims[0] > 4096) FAIL(SAMBATEN_E_INVALID, "marginals: dense I > 4096 not supported");
-    CK(launch_marginals_dense(user_view(X), 0, X->dims[2], moi, scale_exp, x1, x2, x3, st));
+    CK(marginals_any(user_view(X), 0, X->dims[2], moi, scale_exp, x1, x2, x3, st));
   } else {
     CK(launch_marginals_coo(X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, moi, scale_exp, x1,
                             x2, x3, st));
@@ -724,8 +737,8 @@ extern "C" sambaten_status sambaten_fit(const sambaten_tensor* X, const float* l
   cudaStream_t st = stream_of(stream);
   const DenseView V = user_view(X);
   void* ws = nullptr;
-  CK(cudaMallocAsync(&ws, sizeof(double) * fit_dense_ws_doubles(V), st));
-  CK(launch_fit_dense(V, lambda, A, B, C, R, static_cast<double*>(ws), relerr, st));
+  CK(cudaMallocAsync(&ws, sizeof(double) * fit_ws_doubles_any(V), st));
+  CK(fit_any(V, lambda, A, B, C, R, static_cast<double*>(ws), relerr, st));
   CK(cudaFreeAsync(ws, st));
   return SAMBATEN_OK;
 }

@@ -142,6 +142,14 @@ cudaError_t launch_fit_dense(const DenseView& X, const float* lam, const float* 
                              double* relerr, cudaStream_t st);
 size_t fit_dense_ws_doubles(const DenseView& X);
 
+// k_stream.cu: TMA-ring streaming passes over the dense store (pitch % 4 == 0, 16 B aligned)
+bool stream_supported(const DenseView& X);
+cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
+                                    int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st);
+size_t fit_stream_ws_doubles(const DenseView& X);
+cudaError_t launch_fit_stream(const DenseView& X, const float* lam, const float* A, const float* B,
+                              const float* C, int R, double* ws, double* relerr, cudaStream_t st);
+
 cudaError_t launch_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint64_t key,
                           int64_t n, uint32_t* out, cudaStream_t st);
 cudaError_t launch_detlog(const double* u, int64_t n, double* out, cudaStream_t st);

@@ -25,6 +25,7 @@
 // CTAs (fixed order, deterministic); Grams, solves, norms and the fit in fp64.
 #include <cooperative_groups.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "als_small.cuh"
@@ -39,10 +40,10 @@ constexpr int kCT = 512;          // threads per CTA
 constexpr int kCW = kCT / 32;     // warps per CTA
 
 
-constexpr int kTS = 2;            // TMA stages per team
+constexpr int kTS = 3;            // TMA stages per team
 
 struct ClLayout {
-  size_t G, Gp, Gs, Vi, W1, lam, sc, bars, P, Xun, Xun2, Msh, U0s, U1s, U2s, Wt, stage, total;
+  size_t G, Gp, Gs, Vi, W1, lam, sc, bars, P, Xun, Xun2, Msh, U0s, U1s, U2s, stage, total;
   int chunk0, chunk1, ownK, stage_fl, T, NT;
 };
 
@@ -50,22 +51,26 @@ __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15
 __host__ __device__ inline int imax3(int a, int b, int c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
 __host__ __device__ inline int pitch4(int n) { return (n + 3) & ~3; }
 
-// Teams: warp-aligned groups of T threads, one thread per column pair of the wider layout;
-// NT = teams per CTA (<= 15: one named barrier each).
+// Teams: warp-aligned groups of T threads, one thread per column quad (4 floats) of the wider
+// layout; NT = teams per CTA (<= 15: one named barrier each).
 __host__ __device__ inline void cl_teams(int nI, int nJ, int* T, int* NT) {
-  const int pairs = pitch4(nI > nJ ? nI : nJ) / 2;
-  *T = 32 * ((pairs + 31) / 32);
+  const int quads = pitch4(nI > nJ ? nI : nJ) / 4;
+  *T = 32 * ((quads + 31) / 32);
   int nt = kCT / *T;
   *NT = nt > 15 ? 15 : nt;
 }
 
 // Shared-memory layout; identical on host (sizing) and device.
-__host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, int CS, int stage_fl) {
+// nt_cap: at most this many teams (no more than a CTA has slices).
+__host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, int CS, int stage_fl,
+                                              int nt_cap = 16) {
   ClLayout L{};
   L.chunk0 = (nI + CS - 1) / CS;
   L.chunk1 = (nJ + CS - 1) / CS;
   L.ownK = (nK + CS - 1) / CS;
   cl_teams(nI, nJ, &L.T, &L.NT);
+  if (L.NT > nt_cap) L.NT = nt_cap;
+  if (L.NT > L.ownK) L.NT = L.ownK > 0 ? L.ownK : 1;
   const int mrows = imax3(L.chunk0, L.chunk1, L.ownK);
   size_t o = 0;
   auto take = [&](size_t b) { size_t r = o; o += al16(b); return r; };
@@ -85,13 +90,12 @@ __host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, in
   L.U0s = take(sizeof(float) * (size_t)nI * RB);
   L.U1s = take(sizeof(float) * (size_t)nJ * RB);
   L.U2s = take(sizeof(float) * (size_t)L.ownK * RB);
-  L.Wt = take(sizeof(float) * (size_t)L.NT * nJ * RB);   // per-team Khatri-Rao rows (pass A)
   // per-team TMA rings (kTS stages of whole rows, at least one row of the wider layout); the
-  // rings double as the end-of-pass reduction buffer (2 * RB * kCT floats)
+  // rings double as the end-of-pass reduction buffer (4 * RB * kCT floats)
   const int rowmax = pitch4(nI > nJ ? nI : nJ);
   L.stage_fl = stage_fl > rowmax ? stage_fl : rowmax;
   const size_t ring = sizeof(float) * (size_t)L.NT * kTS * L.stage_fl;
-  const size_t red = sizeof(float) * (size_t)2 * RB * kCT;
+  const size_t red = sizeof(float) * (size_t)4 * RB * kCT;
   L.stage = take(ring > red ? ring : red);
   L.total = o;
   return L;
@@ -259,25 +263,24 @@ __device__ __forceinline__ void team_bar(int id, int nthreads) {
 
 // One streaming pass over the CTA's own slices of a layout Src[u][row][col] (row pitch
 // `pitch` floats, multiple of 4, zero padded; slices contiguous).  Team t (T threads, one
-// per column pair) owns the slices t, t+NT, ... and streams them through its own kTS-deep
+// per column quad) owns the slices t, t+NT, ... and streams them through its own kTS-deep
 // TMA ring (its thread 0 issues cp.async.bulk copies of whole-row stages; the team syncs
 // on a named barrier), so every thread sees whole columns and no reduction inside a slice
 // is needed:
-//   Pass A (!PASSB): acc(c,f) += Src(u,q,col_c) W_u(q,f), W_u(q,f) = U1(q,f) U2(u,f) (the
-//     Khatri-Rao rows, built per slice in the team's smem); fp32 per slice, tot += acc.
-//   Pass B (PASSB):  acc(c,f) += Src(u,p,col_c) U0(p,f) = D(u,col_c,f), stored (fp32,
-//     global); tot(c,f) += U2(u,f) D(u,col_c,f).
-// At the end P(col,f) = sum over the teams (fixed order, fp64) of tot.  tseq: stages this
-// team has consumed so far (same value in every thread of the team).
+//   Pass A (!PASSB): acc(c,f) += Src(u,q,col_c) U1(q,f) U2(u,f)   (Khatri-Rao row formed on
+//     the fly), accumulated over the team's slices; P(col,f) = sum over teams (fp64).
+//   Pass B (PASSB):  acc(c,f) = sum_p Src(u,p,col_c) U0(p,f) = D(u,col_c,f), stored (fp32,
+//     global) at each slice end; P is formed afterwards from D (see mode 1).
+// tseq: stages this team has consumed so far (same value in every thread of the team).
 template <int RB, bool PASSB>
-__device__ __noinline__ void team_pass(const float* __restrict__ region, int nu, int nrow, int ncol,
-                                       int pitch, const float* Uw, const float* U2s, float* Wt,
-                                       float* rings, int stage_fl, unsigned long long* bars,
-                                       int T, int NT, unsigned tseq, float* Dg, double* P) {
+__device__ __forceinline__ void team_pass(const float* __restrict__ region, int nu, int nrow, int ncol,
+                                       int pitch, const float* Uw, const float* U2s, float* rings,
+                                       int stage_fl, unsigned long long* bars, int T, int NT,
+                                       unsigned tseq, float* Dg, double* P) {
   const int tid = threadIdx.x;
   const int team = tid / T, lt = tid - team * T;
   const bool in_team = team < NT;
-  const bool valid = in_team && 2 * lt < pitch;
+  const bool valid = in_team && 4 * lt < pitch;
   const int trmax = stage_fl / pitch > 0 ? stage_fl / pitch : 1;
   const int nch = (nrow + trmax - 1) / trmax;
   const int tr = (nrow + nch - 1) / nch;
@@ -285,7 +288,6 @@ __device__ __noinline__ void team_pass(const float* __restrict__ region, int nu,
   const int total = nsl * nch;
   float* ring = rings + (size_t)(in_team ? team : 0) * kTS * stage_fl;
   unsigned long long* tb = bars + (in_team ? team : 0) * kTS;
-  float* W = Wt + (size_t)(in_team ? team : 0) * nrow * RB;
   const int bar_id = 1 + team;
   auto issue = [&](int s) {
     const int ul = team + (s / nch) * NT, k = s % nch;
@@ -299,92 +301,80 @@ __device__ __noinline__ void team_pass(const float* __restrict__ region, int nu,
     fence_proxy_async();
     for (int s = 0; s < total && s < kTS; ++s) issue(s);
   }
-  auto build_w = [&](int ul) {   // W_u = U1 * U2(u)   (pass A)
-    for (int e = lt; e < nrow * RB; e += T) W[e] = Uw[e] * U2s[ul * RB + (e % RB)];
-  };
-  if (!PASSB && total > 0) {
-    build_w(team);
-    team_bar(bar_id, T);
-  }
-  float acc[2][RB], tot[2][RB];
+  float acc[4][RB];
 #pragma unroll
-  for (int c = 0; c < 2; ++c)
+  for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int f = 0; f < RB; ++f) { acc[c][f] = 0.f; tot[c][f] = 0.f; }
-  const float* Wr = PASSB ? Uw : W;
+    for (int f = 0; f < RB; ++f) acc[c][f] = 0.f;
+  float u2[RB];
   for (int s = 0; s < total; ++s) {
     const int ul = team + (s / nch) * NT, k = s % nch;
     const int r0 = k * tr, nr = min(tr, nrow - r0);
     const unsigned buf = (tseq + s) % kTS;
+    if (!PASSB && k == 0) ld_row<RB>(U2s + ul * RB, u2);
     mbar_wait(&tb[buf], ((tseq + s) / kTS) & 1u);
     if (valid) {
-      const float* st = ring + buf * stage_fl + 2 * lt;
-      const float* wr = Wr + r0 * RB;
-#pragma unroll 4
+      const float* st = ring + buf * stage_fl + 4 * lt;
+      const float* wr = Uw + r0 * RB;
+#pragma unroll 2
       for (int row = 0; row < nr; ++row) {
-        const float2 y = *reinterpret_cast<const float2*>(st + row * pitch);
+        const float4 y = *reinterpret_cast<const float4*>(st + row * pitch);
         float w[RB];
         ld_row<RB>(wr + row * RB, w);
+        if (!PASSB) {
+#pragma unroll
+          for (int f = 0; f < RB; ++f) w[f] *= u2[f];
+        }
 #pragma unroll
         for (int f = 0; f < RB; ++f) {
           acc[0][f] = fmaf(y.x, w[f], acc[0][f]);
           acc[1][f] = fmaf(y.y, w[f], acc[1][f]);
+          acc[2][f] = fmaf(y.z, w[f], acc[2][f]);
+          acc[3][f] = fmaf(y.w, w[f], acc[3][f]);
         }
       }
     }
-    const bool slice_end = k == nch - 1;
-    if (slice_end && valid) {
-      if (!PASSB) {
+    if (PASSB && k == nch - 1 && valid) {   // D(u, col, :) complete
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+      for (int c = 0; c < 4; ++c) {
+        const int col = 4 * lt + c;
+        if (col < ncol) {
+          float* d = Dg + ((int64_t)ul * ncol + col) * RB;
 #pragma unroll
-          for (int f = 0; f < RB; ++f) { tot[c][f] += acc[c][f]; acc[c][f] = 0.f; }
-      } else {
-        float u2[RB];
-        ld_row<RB>(U2s + ul * RB, u2);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int col = 2 * lt + c;
-          if (col < ncol) {
-            float* d = Dg + ((int64_t)ul * ncol + col) * RB;
-#pragma unroll
-            for (int f4 = 0; f4 < RB / 4; ++f4)
-              reinterpret_cast<float4*>(d)[f4] = make_float4(acc[c][4 * f4], acc[c][4 * f4 + 1],
-                                                             acc[c][4 * f4 + 2], acc[c][4 * f4 + 3]);
-          }
-#pragma unroll
-          for (int f = 0; f < RB; ++f) { tot[c][f] = fmaf(u2[f], acc[c][f], tot[c][f]); acc[c][f] = 0.f; }
+          for (int f4 = 0; f4 < RB / 4; ++f4)
+            reinterpret_cast<float4*>(d)[f4] = make_float4(acc[c][4 * f4], acc[c][4 * f4 + 1],
+                                                           acc[c][4 * f4 + 2], acc[c][4 * f4 + 3]);
         }
+#pragma unroll
+        for (int f = 0; f < RB; ++f) acc[c][f] = 0.f;
       }
     }
-    team_bar(bar_id, T);   // stage (and, at a slice end, W) consumed by the whole team
-    if (!PASSB && slice_end && s + 1 < total) {
-      build_w(ul + NT);
-      team_bar(bar_id, T);
-    }
+    team_bar(bar_id, T);   // stage consumed by the whole team
     if (lt == 0 && s + kTS < total) {
       fence_proxy_async();
       issue(s + kTS);
     }
   }
-  __syncthreads();   // every team done: rings free (no copy in flight) -> reduction buffer
-  float* red = rings;
+  if (!PASSB) {
+    __syncthreads();   // every team done: rings free (no copy in flight) -> reduction buffer
+    float* red = rings;
 #pragma unroll
-  for (int c = 0; c < 2; ++c)
+    for (int c = 0; c < 4; ++c)
 #pragma unroll
-    for (int f = 0; f < RB; ++f) red[(c * RB + f) * kCT + tid] = tot[c][f];
-  __syncthreads();
-  for (int e = tid; e < ncol * RB; e += kCT) {
-    const int col = e / RB, f = e - col * RB;
-    const float* rr = red + ((col & 1) * RB + f) * kCT + (col >> 1);
-    double v[16];
+      for (int f = 0; f < RB; ++f) red[(c * RB + f) * kCT + tid] = acc[c][f];
+    __syncthreads();
+    for (int e = tid; e < ncol * RB; e += kCT) {
+      const int col = e / RB, f = e - col * RB;
+      const float* rr = red + ((col & 3) * RB + f) * kCT + (col >> 2);
+      double v[16];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) v[t] = t < NT ? (double)rr[t * T] : 0.0;
-    double sum = 0.0;
+      for (int t = 0; t < 16; ++t) v[t] = t < NT ? (double)rr[t * T] : 0.0;
+      double sum = 0.0;
 #pragma unroll
-    for (int t = 0; t < 16; ++t)
-      if (t < NT) sum += v[t];
-    P[e] = sum;
+      for (int t = 0; t < 16; ++t)
+        if (t < NT) sum += v[t];
+      P[e] = sum;
+    }
   }
 }
 
@@ -421,7 +411,6 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
   float* U1s = reinterpret_cast<float*>(smem + Ly.U1s);
   float* U2s = reinterpret_cast<float*>(smem + Ly.U2s);
   float* ring = reinterpret_cast<float*>(smem + Ly.stage);
-  float* Wt = reinterpret_cast<float*>(smem + Ly.Wt);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + Ly.bars);
   __shared__ double s_fc[kMaxR];
   __shared__ double s_red[32];
@@ -500,19 +489,26 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       const int n = m == 0 ? nI : nJ;
       const int ch = m == 0 ? Ly.chunk0 : Ly.chunk1;
       // warp 0: Vi = (G_o1 * G_o2)^-1 while the other warps stream
-      if (warp == 0) warp_normal_inverse<RB>(G, m, R, Gs, Vi, W1, s_fc, &s_flags);
+      if (warp == kCW - 1) warp_normal_inverse<RB>(G, m, R, Gs, Vi, W1, s_fc, &s_flags);
       if (m == 0) {
-        team_pass<RB, false>(regA, nu, nJ, nI, pI, U1s, U2s, Wt, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
+        team_pass<RB, false>(regA, nu, nJ, nI, pI, U1s, U2s, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
                              tseq, D, P);
         if (myteam < Ly.NT) tseq += team_stages(myteam, nu, Ly.NT, nJ, pI, Ly.stage_fl);
         __syncthreads();   // the rings (reduction buffer) are re-armed by the next pass
         PH(1);
       } else {
-        team_pass<RB, true>(regB, nu, nI, nJ, pJ, U0s, U2s, Wt, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
+        team_pass<RB, true>(regB, nu, nI, nJ, pJ, U0s, U2s, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
                             tseq, D, P);
         if (myteam < Ly.NT) tseq += team_stages(myteam, nu, Ly.NT, nI, pJ, Ly.stage_fl);
-        __syncthreads();
-        // D rows written by other threads (global) are read in mode 2
+        __syncthreads();   // D of the own slices complete (global, visible to the CTA)
+        // P(q,f) = sum_{own u} U2(u,f) D(u,q,f)   (fixed order, fp64)
+        for (int e = tid; e < nJ * RB; e += kCT) {
+          const int f = e % RB;
+          double s = 0.0;
+          for (int ul = 0; ul < nu; ++ul)
+            s += (double)U2s[ul * RB + f] * (double)D[(int64_t)ul * nJ * RB + e];
+          P[e] = s;
+        }
         PH(6);
       }
       cluster.sync();   // S1: partials of every CTA complete
@@ -568,7 +564,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       PH(m == 0 ? 5 : 11);
     }
     // ==================================== mode 2 ====================================
-    if (warp == 0) warp_normal_inverse<RB>(G, 2, R, Gs, Vi, W1, s_fc, &s_flags);
+    if (warp == kCW - 1) warp_normal_inverse<RB>(G, 2, R, Gs, Vi, W1, s_fc, &s_flags);
     // M2(u,f) = sum_q D(u,q,f) U1(q,f) for the own slices: warp per (u, f-group of 4)
     {
       const int nfg = RB / 4;
@@ -760,8 +756,16 @@ static bool plan_rb(const DenseAls& a, ClusterPlan* pl) {
     // time ~ waves * slices per team
     const double waves = (double)((a.r + act - 1) / act);
     const int nu = (a.nK + CS - 1) / CS;
-    // ties: fewer waves, then the smaller cluster (cheaper DSMEM reductions)
-    const double t = waves * (double)((nu + L.NT - 1) / L.NT) + 1e-3 * waves + 1e-5 * CS;
+    // model: a team (warp group) streams whole slices; ~8 busy warps saturate an SM's issue
+    // slots, so a CTA's pass time ~ nu / min(busy teams * warps per team, 8) * warps per
+    // team.  Ties: fewer waves, then the smaller cluster (cheaper DSMEM reductions).
+    const int wpt = L.T / 32;
+    const int busy = nu < L.NT ? nu : L.NT;
+    const double rate = (double)(busy * wpt < 8 ? busy * wpt : 8) / wpt;   // slices in parallel
+    const double t = waves * (double)nu / rate + 1e-3 * waves + 1e-5 * CS;
+    if (getenv("SAMBATEN_DEBUG"))
+      fprintf(stderr, "[sambaten]   plan candidate CS=%d act=%d nu=%d NT=%d T=%d smem=%zu t=%.3f\n",
+              CS, act, nu, L.NT, L.T, L.total, t);
     if (t < best) {
       best = t;
       found = true;
