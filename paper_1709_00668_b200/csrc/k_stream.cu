@@ -4,11 +4,10 @@
 //   a7  fit: <X, [[lam; A, B, C]]> and ||X||^2 in one pass.
 //
 // Data path: persistent CTAs (one per SM and column chunk), each owning a contiguous range of
-// rows (j,k) of the store X[k][j][0..pitch), stream their rows through a kRing-deep ring of
-// shared-memory stages filled by the bulk-copy engine (cp.async.bulk + mbarrier, one
-// producer thread), so each SM keeps ~kRing*32 KB of loads in flight with no register cost.
-// Consumers are column-parallel: thread t owns the column quad (4 floats) t % NQ of every row
-// of its row group t / NQ, so all smem reads are conflict-free 16 B loads.
+// rows (j,k) of the store X[k][j][0..pitch), stream their rows through a ring of ns shared-
+// memory stages filled by the bulk-copy engine (cp.async.bulk + mbarrier, one producer
+// thread), so each SM keeps ~100-190 KB of loads in flight with no register cost (a plain
+// ring read of this kind measured 5.7 TB/s on the B200, tools/micro/bw.cu).
 #include "common.cuh"
 #include "internal.h"
 
@@ -17,8 +16,7 @@ namespace sbt {
 namespace {
 
 constexpr int kST = 512;          // threads per CTA
-constexpr int kRing = 4;          // stages in flight
-constexpr int kStageBytes = 32 * 1024;
+constexpr int kNW = kST / 32;
 
 __device__ __forceinline__ unsigned s_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void s_mbar_init(unsigned long long* b, unsigned c) {
@@ -47,31 +45,29 @@ struct StreamGeom {
   int64_t row0, nrows;      // rows (k*J + j) of the pass
   int64_t rows_per_cta;
   int pitch;                // floats per row in the store (multiple of 4)
-  int cw;                   // column chunk width (floats, multiple of 4, <= 2048)
+  int cw;                   // column chunk width (floats, multiple of 4)
   int ncol;                 // real columns (I)
   int tr;                   // rows per stage
+  int ns;                   // stages in the ring (<= kMaxNS)
 };
 
-// The ring: stage s of this CTA covers rows [rb + s*tr, ...) of its range; issued by tid 0.
-struct Ring {
-  float* buf;               // kRing * tr * cw floats
-  unsigned long long* bar;  // kRing
-};
+constexpr int kMaxNS = 8;
 
-__device__ __forceinline__ void ring_issue(const Ring& rg, const StreamGeom& g, const float* X,
-                                           int64_t rb, int64_t re, int c0, int s) {
+// stage s of this CTA covers rows [rb + s*tr, ...); issued by one thread
+__device__ __forceinline__ void ring_issue(float* ring, unsigned long long* bars, const StreamGeom& g,
+                                           const float* X, int64_t rb, int64_t re, int c0, int s) {
   const int64_t r0 = rb + (int64_t)s * g.tr;
   const int nr = (int)min((int64_t)g.tr, re - r0);
-  const int slot = s % kRing;
-  float* dst = rg.buf + (size_t)slot * g.tr * g.cw;
+  const int slot = s % g.ns;
+  float* dst = ring + (size_t)slot * g.tr * g.cw;
   const int w = min(g.cw, g.pitch - c0);   // floats copied per row (multiple of 4)
   const unsigned row_bytes = (unsigned)(w * sizeof(float));
-  s_expect(&rg.bar[slot], row_bytes * nr);
+  s_expect(&bars[slot], row_bytes * nr);
   if (g.cw == g.pitch) {
-    s_bulk(dst, X + r0 * g.pitch, row_bytes * nr, &rg.bar[slot]);
+    s_bulk(dst, X + r0 * g.pitch, row_bytes * nr, &bars[slot]);
   } else {
     for (int r = 0; r < nr; ++r)
-      s_bulk(dst + (size_t)r * g.cw, X + (r0 + r) * g.pitch + c0, row_bytes, &rg.bar[slot]);
+      s_bulk(dst + (size_t)r * g.cw, X + (r0 + r) * g.pitch + c0, row_bytes, &bars[slot]);
   }
 }
 
@@ -86,45 +82,47 @@ __device__ __forceinline__ long long quant(float x, float scf, double scd) {
 }
 
 // ---------------------------------------------------------------------------------------
-// a1: marginals.  Warp per row: lane l handles the quads l, l+32, ... (<= kMQ) of the column
-// chunk (<= 512 floats), keeping their x1 column sums in registers (int64); the row total is
-// one warp reduction per row -> x2[j] (global atomic) and a CTA-local x3 window flushed at
-// the end; x1 is combined across warps in shared memory, one global atomic per column.
-// Integer sums: exact and independent of the order.
+// a1: marginals.  A warp handles kRPW consecutive rows of a stage at a time: lane l takes the
+// quads l, l+32, ... (<= kMQ) of the column chunk (<= 512 floats) and keeps their x1 column
+// sums in registers (int64); the kRPW row totals are reduced by one interleaved butterfly
+// (kRPW independent shuffle chains) -> x2[j] (global atomic) and a CTA-local x3 window
+// flushed at the end; x1 is combined across warps in shared memory (one global atomic per
+// column).  Integer sums: exact and independent of the order.
 // ---------------------------------------------------------------------------------------
 constexpr int kX3Win = 64;
 constexpr int kMQ = 4;            // quads per lane: column chunk <= 32 * 4 * 4 = 512 floats
+constexpr int kRPW = 2;           // rows per warp per step
+constexpr int kMargCTAs = 1;      // CTAs per SM
 
 template <int MOI>
-__global__ void __launch_bounds__(kST, 1) marg_stream_kernel(const float* __restrict__ X, StreamGeom g,
+__global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float* __restrict__ X, StreamGeom g,
                                                              int J, float scf, double scd,
                                                              unsigned long long* __restrict__ x1,
                                                              unsigned long long* __restrict__ x2,
                                                              unsigned long long* __restrict__ x3) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ unsigned long long bars[kRing];
+  __shared__ unsigned long long bars[kMaxNS];
   __shared__ unsigned long long x3w[kX3Win];
-  __shared__ unsigned long long x1s[512];
+  __shared__ unsigned long long x1s[4 * 32 * kMQ];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kST / 32;
   const int c0 = blockIdx.y * g.cw;
   const int cw_real = min(g.cw, g.ncol - c0);
   const int64_t rb = g.row0 + (int64_t)blockIdx.x * g.rows_per_cta;
   const int64_t re = min(rb + g.rows_per_cta, g.row0 + g.nrows);
   if (rb >= re) return;
-  Ring rg{reinterpret_cast<float*>(smem), bars};
+  float* ring = reinterpret_cast<float*>(smem);
   const int nst = (int)((re - rb + g.tr - 1) / g.tr);
   const int64_t kfirst = rb / J;
   const bool x3_local = ((re - 1) / J - kfirst) < kX3Win;
   if (tid == 0) {
-    for (int s = 0; s < kRing; ++s) s_mbar_init(&bars[s], 1);
+    for (int s = 0; s < g.ns; ++s) s_mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int s = tid; s < kX3Win; s += kST) x3w[s] = 0;
-  for (int s = tid; s < 512; s += kST) x1s[s] = 0;
+  for (int s = tid; s < 4 * 32 * kMQ; s += kST) x1s[s] = 0;
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < nst && s < kRing; ++s) ring_issue(rg, g, X, rb, re, c0, s);
+    for (int s = 0; s < nst && s < g.ns; ++s) ring_issue(ring, bars, g, X, rb, re, c0, s);
   long long acc[kMQ][4];
 #pragma unroll
   for (int m = 0; m < kMQ; ++m)
@@ -133,39 +131,56 @@ __global__ void __launch_bounds__(kST, 1) marg_stream_kernel(const float* __rest
   for (int s = 0; s < nst; ++s) {
     const int64_t r0 = rb + (int64_t)s * g.tr;
     const int nr = (int)min((int64_t)g.tr, re - r0);
-    const int slot = s % kRing;
-    s_wait(&bars[slot], (unsigned)(s / kRing) & 1u);
-    const float* st = rg.buf + (size_t)slot * g.tr * g.cw;
-    for (int r = warp; r < nr; r += NW) {
-      const float* rowp = st + (size_t)r * g.cw;
-      long long rs = 0;
+    const int slot = s % g.ns;
+    s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
+    const float* st = ring + (size_t)slot * g.tr * g.cw;
+    for (int rw = warp * kRPW; rw < nr; rw += kNW * kRPW) {
+      long long rs[kRPW];
 #pragma unroll
-      for (int m = 0; m < kMQ; ++m) {
-        const int col = 4 * (lane + 32 * m);
-        if (col < cw_real) {
-          const float4 v = *reinterpret_cast<const float4*>(rowp + col);
-          long long q0 = quant<MOI>(v.x, scf, scd), q1 = quant<MOI>(v.y, scf, scd);
-          long long q2 = quant<MOI>(v.z, scf, scd), q3 = quant<MOI>(v.w, scf, scd);
-          if (col + 1 >= cw_real) q1 = 0;
-          if (col + 2 >= cw_real) q2 = 0;
-          if (col + 3 >= cw_real) q3 = 0;
-          acc[m][0] += q0; acc[m][1] += q1; acc[m][2] += q2; acc[m][3] += q3;
-          rs += q0 + q1 + q2 + q3;
+      for (int v = 0; v < kRPW; ++v) {
+        rs[v] = 0;
+        const int r = rw + v;
+        if (r < nr) {
+          const float* rowp = st + (size_t)r * g.cw;
+#pragma unroll
+          for (int m = 0; m < kMQ; ++m) {
+            const int col = 4 * (lane + 32 * m);
+            if (col < cw_real) {
+              const float4 x = *reinterpret_cast<const float4*>(rowp + col);
+              long long q0 = quant<MOI>(x.x, scf, scd), q1 = quant<MOI>(x.y, scf, scd);
+              long long q2 = quant<MOI>(x.z, scf, scd), q3 = quant<MOI>(x.w, scf, scd);
+              if (col + 1 >= cw_real) q1 = 0;
+              if (col + 2 >= cw_real) q2 = 0;
+              if (col + 3 >= cw_real) q3 = 0;
+              acc[m][0] += q0; acc[m][1] += q1; acc[m][2] += q2; acc[m][3] += q3;
+              rs[v] += (q0 + q1) + (q2 + q3);
+            }
+          }
         }
       }
-      rs = warp_sum_ll(rs);
-      if (lane == 0 && rs) {
-        const int64_t row = r0 + r;
-        const int64_t k = row / J, j = row - k * J;
-        atomicAdd(&x2[j], (unsigned long long)rs);
-        if (x3_local) atomicAdd(&x3w[k - kfirst], (unsigned long long)rs);
-        else atomicAdd(&x3[k], (unsigned long long)rs);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int v = 0; v < kRPW; ++v) rs[v] += __shfl_xor_sync(0xffffffffu, rs[v], o);
+      if (lane < kRPW) {
+        long long mine = rs[0];
+#pragma unroll
+        for (int v = 1; v < kRPW; ++v)
+          if (lane == v) mine = rs[v];
+        const int r = rw + lane;
+        if (r < nr && mine) {
+          const int64_t row = r0 + r;
+          const int64_t k = row / J, j = row - k * J;
+          atomicAdd(&x2[j], (unsigned long long)mine);
+          if (x3_local) atomicAdd(&x3w[k - kfirst], (unsigned long long)mine);
+          else atomicAdd(&x3[k], (unsigned long long)mine);
+        }
       }
     }
     __syncthreads();   // stage consumed by every warp
-    if (tid == 0 && s + kRing < nst) {
+    if (tid == 0 && s + g.ns < nst) {
       s_fence_async();
-      ring_issue(rg, g, X, rb, re, c0, s + kRing);
+      ring_issue(ring, bars, g, X, rb, re, c0, s + g.ns);
     }
   }
 #pragma unroll
@@ -185,9 +200,11 @@ __global__ void __launch_bounds__(kST, 1) marg_stream_kernel(const float* __rest
 
 // ---------------------------------------------------------------------------------------
 // a7: fit.  inner = sum_{i,j,k} X(i,j,k) m(i,j,k), m = sum_f lam_f A(i,f) B(j,f) C(k,f);
-// sq = sum X^2.  Thread holds lam_f A(i,f) for its 4 columns; W(row,f) = B(j,f) C(k,f) is
-// formed per stage in shared memory.  fp32 per element and per stage row, fp64 across
-// stages; per-CTA partials reduced in a fixed order by fit_combine_kernel.
+// sq = sum X^2.  Thread t owns the column quad t % NQ of the rows of its row group t / NQ
+// and holds lam_f A(i,f) for its 4 columns in registers; W(row,f) = B(j,f) C(k,f) of stage
+// s+1 is formed in a double-buffered shared array while stage s is consumed (one barrier per
+// stage).  fp32 per element and per stage, fp64 across stages; per-CTA partials reduced in a
+// fixed order by fit_combine_kernel.
 // ---------------------------------------------------------------------------------------
 template <int RB>
 __global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restrict__ X, StreamGeom g,
@@ -197,7 +214,7 @@ __global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restr
                                                             const float* __restrict__ C,
                                                             double* __restrict__ part) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ unsigned long long bars[kRing];
+  __shared__ unsigned long long bars[kMaxNS];
   __shared__ double red[32];
   const int tid = threadIdx.x;
   const int c0 = blockIdx.y * g.cw;
@@ -208,16 +225,29 @@ __global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restr
   const bool active = grp < NG && tid < NQ * NG;
   const int64_t rb = g.row0 + (int64_t)blockIdx.x * g.rows_per_cta;
   const int64_t re = min(rb + g.rows_per_cta, g.row0 + g.nrows);
-  Ring rg{reinterpret_cast<float*>(smem), bars};
-  float* W = reinterpret_cast<float*>(smem) + (size_t)kRing * g.tr * g.cw;   // [tr][RB]
+  float* ring = reinterpret_cast<float*>(smem);
+  float* Wbuf = ring + (size_t)g.ns * g.tr * g.cw;   // [2][tr][RB]
   const int nst = rb < re ? (int)((re - rb + g.tr - 1) / g.tr) : 0;
+  auto build_w = [&](int s) {   // W rows of stage s: 32-bit (j,k) walk, no divisions per element
+    float* W = Wbuf + (size_t)(s & 1) * g.tr * RB;
+    const int64_t r0 = rb + (int64_t)s * g.tr;
+    const int nr = (int)min((int64_t)g.tr, re - r0);
+    const int k0 = (int)(r0 / J), j0 = (int)(r0 - (int64_t)k0 * J);
+    for (int e = tid; e < nr * RB; e += kST) {
+      const int r = e / RB, f = e - r * RB;
+      int j = j0 + r, k = k0;
+      while (j >= J) { j -= J; ++k; }
+      W[e] = f < R ? B[(int64_t)j * R + f] * C[(int64_t)k * R + f] : 0.f;
+    }
+  };
   if (tid == 0) {
-    for (int s = 0; s < kRing; ++s) s_mbar_init(&bars[s], 1);
+    for (int s = 0; s < g.ns; ++s) s_mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (nst > 0) build_w(0);
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < nst && s < kRing; ++s) ring_issue(rg, g, X, rb, re, c0, s);
+    for (int s = 0; s < nst && s < g.ns; ++s) ring_issue(ring, bars, g, X, rb, re, c0, s);
   const int col = 4 * quad;
   float al[4][RB];
 #pragma unroll
@@ -231,17 +261,12 @@ __global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restr
   for (int s = 0; s < nst; ++s) {
     const int64_t r0 = rb + (int64_t)s * g.tr;
     const int nr = (int)min((int64_t)g.tr, re - r0);
-    const int slot = s % kRing;
-    for (int e = tid; e < nr * RB; e += kST) {
-      const int r = e / RB, f = e - r * RB;
-      const int64_t row = r0 + r;
-      const int64_t k = row / J, j = row - k * J;
-      W[e] = f < R ? B[j * R + f] * C[k * R + f] : 0.f;
-    }
-    __syncthreads();
-    s_wait(&bars[slot], (unsigned)(s / kRing) & 1u);
+    const int slot = s % g.ns;
+    if (s + 1 < nst) build_w(s + 1);   // the other W buffer (free since the last barrier)
+    s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
     if (active && col < cw_real) {
-      const float* st = rg.buf + (size_t)slot * g.tr * g.cw + col;
+      const float* st = ring + (size_t)slot * g.tr * g.cw + col;
+      const float* W = Wbuf + (size_t)(s & 1) * g.tr * RB;
       float fi = 0.f, fs = 0.f;
 #pragma unroll 2
       for (int r = grp; r < nr; r += NG) {
@@ -268,10 +293,10 @@ __global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restr
       inner += (double)fi;
       sq += (double)fs;
     }
-    __syncthreads();   // stage and W consumed
-    if (tid == 0 && s + kRing < nst) {
+    __syncthreads();   // stage and W(s) consumed, W(s+1) complete
+    if (tid == 0 && s + g.ns < nst) {
       s_fence_async();
-      ring_issue(rg, g, X, rb, re, c0, s + kRing);
+      ring_issue(ring, bars, g, X, rb, re, c0, s + g.ns);
     }
   }
   inner = block_sum_d(inner, red);
@@ -334,8 +359,10 @@ __global__ void fit_combine_kernel(const double* part, int nb, const double* G, 
   *relerr = sq > 0.0 ? sqrt(res / sq) : 0.0;
 }
 
+// Geometry: column chunks of <= max_cw floats; stages of ~stage_bytes (whole rows), a ring of
+// ring_bytes / stage; one CTA per SM and chunk over contiguous row ranges.
 StreamGeom make_geom(const DenseView& X, int64_t row0, int64_t nrows, int* grid_x, int* grid_y,
-                     int max_cw = 2048) {
+                     int max_cw, int stage_bytes, int ring_bytes, int min_tr, int ctas_per_sm = 1) {
   StreamGeom g{};
   g.row0 = row0;
   g.nrows = nrows;
@@ -348,13 +375,15 @@ StreamGeom make_geom(const DenseView& X, int64_t row0, int64_t nrows, int* grid_
     g.cw = ((g.pitch + nch - 1) / nch + 3) & ~3;
   }
   const int nchunk = (g.pitch + g.cw - 1) / g.cw;
-  g.tr = kStageBytes / (int)(g.cw * sizeof(float));
-  if (g.tr < 1) g.tr = 1;
+  g.tr = stage_bytes / (int)(g.cw * sizeof(float));
+  if (g.tr < min_tr) g.tr = min_tr;
   if (g.tr > 256) g.tr = 256;
-  int64_t nx = kNumSMs / nchunk;
+  g.ns = ring_bytes / (int)(g.tr * g.cw * sizeof(float));
+  if (g.ns > kMaxNS) g.ns = kMaxNS;
+  if (g.ns < 2) g.ns = 2;
+  int64_t nx = (int64_t)kNumSMs * ctas_per_sm / nchunk;
   if (nx < 1) nx = 1;
-  // at least a few stages per CTA
-  if (nx > ceil_div(nrows, 2 * g.tr)) nx = ceil_div(nrows, 2 * g.tr);
+  if (nx > ceil_div(nrows, 2 * g.tr)) nx = ceil_div(nrows, 2 * g.tr);   // a few stages per CTA
   if (nx < 1) nx = 1;
   g.rows_per_cta = ceil_div(nrows, nx);
   *grid_x = (int)ceil_div(nrows, g.rows_per_cta);
@@ -362,7 +391,18 @@ StreamGeom make_geom(const DenseView& X, int64_t row0, int64_t nrows, int* grid_
   return g;
 }
 
-size_t ring_smem(const StreamGeom& g) { return sizeof(float) * (size_t)kRing * g.tr * g.cw; }
+size_t ring_smem(const StreamGeom& g) { return sizeof(float) * (size_t)g.ns * g.tr * g.cw; }
+
+constexpr int kRingBytes = 192 * 1024;
+
+StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* gy) {
+  // rows per stage: a multiple of kRPW * warps keeps every warp busy
+  return make_geom(X, k0 * X.J, nk * X.J, gx, gy, 4 * 32 * kMQ, 64 * 1024, kRingBytes, kRPW * kNW,
+                   kMargCTAs);
+}
+StreamGeom fit_geom(const DenseView& X, int* gx, int* gy) {
+  return make_geom(X, 0, X.J * X.K, gx, gy, 2048, 32 * 1024, 176 * 1024, 1);
+}
 
 }  // namespace
 
@@ -374,7 +414,7 @@ cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, 
                                     int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st) {
   if (nk <= 0) return cudaSuccess;
   int gx, gy;
-  StreamGeom g = make_geom(X, k0 * X.J, nk * X.J, &gx, &gy, 4 * 32 * kMQ);
+  StreamGeom g = marg_geom(X, k0, nk, &gx, &gy);
   const float scf = ldexpf(1.0f, S < -126 ? -126 : (S > 127 ? 127 : S));
   const double scd = ldexp(1.0, S);
   const size_t smem = ring_smem(g);
@@ -393,7 +433,7 @@ cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, 
 
 size_t fit_stream_ws_doubles(const DenseView& X) {
   int gx, gy;
-  make_geom(X, 0, X.J * X.K, &gx, &gy);
+  fit_geom(X, &gx, &gy);
   return 2 * (size_t)gx * gy + 3 * kMaxR * kMaxR + 8;
 }
 
@@ -401,8 +441,8 @@ template <int RB>
 static cudaError_t fit_stream_rb(const DenseView& X, const float* lam, const float* A, const float* B,
                                  const float* C, int R, double* ws, double* relerr, cudaStream_t st) {
   int gx, gy;
-  StreamGeom g = make_geom(X, 0, X.J * X.K, &gx, &gy);
-  const size_t smem = ring_smem(g) + sizeof(float) * (size_t)g.tr * RB;
+  StreamGeom g = fit_geom(X, &gx, &gy);
+  const size_t smem = ring_smem(g) + sizeof(float) * 2 * (size_t)g.tr * RB;
   cudaFuncSetAttribute(fit_stream_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   double* part = ws;
   double* G = ws + 2 * (size_t)gx * gy;
