@@ -78,6 +78,7 @@ typedef struct {
   double accept_tau;      /* rep acceptance threshold on min_f S(f, pi f) (R26); default 0.9 */
   int full_fit;           /* 1: sambaten_update also computes the full relative error (a7)   */
   int64_t capacity;       /* dense: total K slices to preallocate; COO: total nnz; 0 = 2x X0 */
+  int64_t capacity_k;     /* COO: mode-3 rows of C to preallocate; 0 = 2 K0 + 1024          */
   int init_max_iters;     /* sambaten_init: ALS iterations on X0 (default 1000)       */
   double init_tol;        /* sambaten_init: tolerance (default 1e-6)                         */
   void* stream;           /* cudaStream_t for all work of this handle; NULL = default       */

@@ -34,7 +34,8 @@ class Tensor(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("als_max_iters", C.c_int), ("als_tol", C.c_double), ("moi", C.c_int),
                 ("s_mode", C.c_int * 3), ("merge_policy", C.c_int), ("accept_tau", C.c_double),
-                ("full_fit", C.c_int), ("capacity", C.c_int64), ("init_max_iters", C.c_int),
+                ("full_fit", C.c_int), ("capacity", C.c_int64), ("capacity_k", C.c_int64),
+                ("init_max_iters", C.c_int),
                 ("init_tol", C.c_double), ("stream", C.c_void_p)]
 
 

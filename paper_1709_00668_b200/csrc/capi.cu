@@ -85,6 +85,7 @@ struct DevBuf {
 
 struct HostStatus {        // pinned; filled by one D2H copy at the end of an update
   unsigned long long maxphi_bits;
+  unsigned vflags;
   int accepted[kMaxReps];
   int iters[kMaxReps];
   int flags[kMaxReps];
@@ -110,6 +111,14 @@ struct sambaten_s {
   uint32_t uid_ck = 0;
   // workspaces
   DevBuf marg, samp, summ, fac, als, match, misc, segs, fitws;
+  // COO store (fmt == SAMBATEN_COO): i | j | k (int32) and v (fp32), capacity nnz_cap
+  int64_t nnz = 0, nnz_cap = 0, nnz_ck = 0;
+  DevBuf coo_ws;            // gather / sort / ALS workspace of the COO path
+  int32_t* ci() const { return X.as<int32_t>(); }
+  int32_t* cj() const { return ci() + nnz_cap; }
+  int32_t* ck_() const { return cj() + nnz_cap; }
+  float* cv() const { return reinterpret_cast<float*>(ck_() + nnz_cap); }
+  CooView coo_view(int64_t n) const { return CooView{ci(), cj(), ck_(), cv(), n, I, J, K}; }
   SampleSeg* segs_host = nullptr;   // pinned
   HostStatus* hs = nullptr;         // pinned
   cudaEvent_t ev[9] = {};
@@ -198,7 +207,9 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
   if (!out) FAIL(SAMBATEN_E_INVALID, "init: NULL handle pointer");
   *out = nullptr;
   if (sambaten_status st = check_dense(X0, "init")) return st;
-  if (X0->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "init: COO store not available in this build");
+  if (X0->fmt == SAMBATEN_COO && X0->nnz > 0 && (!X0->idx[0] || !X0->idx[1] || !X0->idx[2] || !X0->vals))
+    FAIL(SAMBATEN_E_INVALID, "init: NULL COO array");
+  if (X0->fmt == SAMBATEN_COO && X0->nnz < 1) FAIL(SAMBATEN_E_DEGENERATE, "init: empty COO tensor");
   if (R < 1 || R > kMaxR) FAIL(SAMBATEN_E_INVALID, "init: R must be in [1, 32]");
   if (r < 1 || r > kMaxReps) FAIL(SAMBATEN_E_INVALID, "init: r must be in [1, 32]");
   if (s < 1) FAIL(SAMBATEN_E_INVALID, "init: s must be >= 1");
@@ -216,8 +227,16 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
   h->I = X0->dims[0]; h->J = X0->dims[1]; h->K = X0->dims[2];
   h->R = R; h->r = r; h->seed = seed; h->update_id = 0;
   for (int m = 0; m < 3; ++m) h->s[m] = h->opts.s_mode[m] > 0 ? h->opts.s_mode[m] : s;
-  h->Kcap = h->opts.capacity > 0 ? h->opts.capacity : 2 * h->K;
-  if (h->Kcap < h->K) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity < K0"); }
+  if (h->fmt == SAMBATEN_DENSE) {
+    h->Kcap = h->opts.capacity > 0 ? h->opts.capacity : 2 * h->K;
+    if (h->Kcap < h->K) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity < K0"); }
+  } else {
+    h->nnz = X0->nnz;
+    h->nnz_cap = h->opts.capacity > 0 ? h->opts.capacity : 2 * X0->nnz;
+    if (h->nnz_cap < h->nnz) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity < nnz0"); }
+    h->Kcap = h->opts.capacity_k > 0 ? h->opts.capacity_k : 2 * h->K + 1024;
+    if (h->Kcap < h->K) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity_k < K0"); }
+  }
   h->st = stream_of(h->opts.stream);
   h->pitch = (h->I + 3) & ~int64_t(3);
   *out = h;
@@ -225,11 +244,20 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
 }
 
 static sambaten_status alloc_store_and_model(sambaten_s* h, const sambaten_tensor* X0) {
-  const size_t store = (size_t)h->Kcap * h->J * h->pitch * sizeof(float);
-  CK(h->X.ensure(store));
-  CK(cudaMemsetAsync(h->X.p, 0, store, h->st));
-  CK(cudaMemcpy2DAsync(h->X.p, h->pitch * sizeof(float), X0->vals, h->I * sizeof(float),
-                       h->I * sizeof(float), h->J * h->K, cudaMemcpyDefault, h->st));
+  if (h->fmt == SAMBATEN_DENSE) {
+    const size_t store = (size_t)h->Kcap * h->J * h->pitch * sizeof(float);
+    CK(h->X.ensure(store));
+    CK(cudaMemsetAsync(h->X.p, 0, store, h->st));
+    CK(cudaMemcpy2DAsync(h->X.p, h->pitch * sizeof(float), X0->vals, h->I * sizeof(float),
+                         h->I * sizeof(float), h->J * h->K, cudaMemcpyDefault, h->st));
+  } else {
+    CK(h->X.ensure((size_t)h->nnz_cap * (3 * sizeof(int32_t) + sizeof(float))));
+    const size_t n = (size_t)h->nnz;
+    CK(cudaMemcpyAsync(h->ci(), X0->idx[0], n * sizeof(int32_t), cudaMemcpyDefault, h->st));
+    CK(cudaMemcpyAsync(h->cj(), X0->idx[1], n * sizeof(int32_t), cudaMemcpyDefault, h->st));
+    CK(cudaMemcpyAsync(h->ck_(), X0->idx[2], n * sizeof(int32_t), cudaMemcpyDefault, h->st));
+    CK(cudaMemcpyAsync(h->cv(), X0->vals, n * sizeof(float), cudaMemcpyDefault, h->st));
+  }
   for (int b = 0; b < 2; ++b) {
     CK(h->model[b].ensure(h->model_floats() * sizeof(float)));
     CK(cudaMemsetAsync(h->model[b].p, 0, h->model_floats() * sizeof(float), h->st));
@@ -239,15 +267,27 @@ static sambaten_status alloc_store_and_model(sambaten_s* h, const sambaten_tenso
   for (int e = 0; e < 9; ++e) CK(cudaEventCreate(&h->ev[e]));
   // fixed-point scale from X0 (R7)
   CK(h->misc.ensure(4096));
-  CK(cudaMemsetAsync(h->misc.p, 0, 8, h->st));
-  CK(launch_max_phi_dense(h->view(), 0, h->K, h->opts.moi, h->misc.as<unsigned long long>(), h->st));
+  CK(cudaMemsetAsync(h->misc.p, 0, 16, h->st));
+  if (h->fmt == SAMBATEN_DENSE) {
+    CK(launch_max_phi_dense(h->view(), 0, h->K, h->opts.moi, h->misc.as<unsigned long long>(), h->st));
+  } else {
+    CK(launch_coo_max_phi(h->cv(), h->nnz, h->opts.moi, h->misc.as<unsigned long long>(), h->st));
+    // the initial tensor must be canonical (R28)
+    CK(launch_coo_validate(h->ci(), h->cj(), h->ck_(), h->cv(), h->nnz, h->I, h->J, h->K,
+                           reinterpret_cast<unsigned*>(h->misc.as<char>() + 8), h->st));
+  }
   unsigned long long bits = 0;
+  unsigned vflags = 0;
+  CK(cudaMemcpyAsync(&vflags, h->misc.as<char>() + 8, 4, cudaMemcpyDeviceToHost, h->st));
   CK(cudaMemcpyAsync(&bits, h->misc.p, 8, cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   double maxphi;
   memcpy(&maxphi, &bits, 8);
+  if (vflags & 1u) FAIL(SAMBATEN_E_INDEX_RANGE, "init: COO index out of range (S:77)");
+  if (vflags & 6u) FAIL(SAMBATEN_E_INVALID, "init: COO tensor not canonical (sorted by (k,j,i), unique, nonzero; R28)");
   if (!(maxphi > 0.0)) FAIL(SAMBATEN_E_DEGENERATE, "init: all-zero initial tensor");
-  h->S = sambaten_fixed_point_scale(h->I * h->J * h->Kcap, maxphi);
+  const int64_t cap_entries = h->fmt == SAMBATEN_DENSE ? h->I * h->J * h->Kcap : h->nnz_cap;
+  h->S = sambaten_fixed_point_scale(cap_entries, maxphi);
   h->maxphi_log2 = ceil_log2_d(maxphi);
   return SAMBATEN_OK;
 }
@@ -259,6 +299,7 @@ extern "C" void sambaten_destroy(sambaten_t h) {
   h->model[0].release(); h->model[1].release(); h->ck.release();
   h->marg.release(); h->samp.release(); h->summ.release(); h->fac.release();
   h->als.release(); h->match.release(); h->misc.release(); h->segs.release(); h->fitws.release();
+  h->coo_ws.release();
   if (h->segs_host) cudaFreeHost(h->segs_host);
   if (h->hs) cudaFreeHost(h->hs);
   for (int e = 0; e < 9; ++e)
@@ -270,11 +311,17 @@ __global__ static void lam_to_f32_kernel(const double* l, int R, float* out) {
   if (threadIdx.x < R) out[threadIdx.x] = (float)l[threadIdx.x];
 }
 
+static sambaten_status init_als_coo(sambaten_s* h);
+
 extern "C" sambaten_status sambaten_init(sambaten_t* out, const sambaten_tensor* X0, int R, int s,
                                          int r, uint64_t seed, const sambaten_opts* opts) {
   if (sambaten_status e = create_common(out, X0, R, s, r, seed, opts)) return e;
   sambaten_s* h = *out;
   if (sambaten_status e = alloc_store_and_model(h, X0)) { sambaten_destroy(h); *out = nullptr; return e; }
+  if (h->fmt == SAMBATEN_COO) {
+    if (sambaten_status e = init_als_coo(h)) { sambaten_destroy(h); *out = nullptr; return e; }
+    return SAMBATEN_OK;
+  }
   // full CP-ALS on X0, r = 1, Philox init with update_id 0 (R10)
   DenseAls a{};
   a.Y = h->X.as<float>(); a.y_stride = 0; a.pitch = h->pitch;
@@ -329,6 +376,427 @@ static inline int64_t sample_n(int64_t n, int s) { return std::min<int64_t>(n, (
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+// ---------------------------------------------------------------------------------------
+// update steps shared by the dense and COO paths
+// ---------------------------------------------------------------------------------------
+// a2: sampling (R4-R6); K_s from the old slices only, then K' = K_s ++ new.  Outputs point
+// into h->samp: Is [r][nI], Js [r][nJ], Kp [r][nKp], loc maps [r][I], [r][J], [r][Ko].
+static cudaError_t run_sampling(sambaten_s* h, const int64_t* x1, const int64_t* x2, const int64_t* x3,
+                                int64_t Ko, int64_t Kn, int64_t nI, int64_t nJ, int64_t nKs,
+                                int64_t nKp, uint32_t uid, int32_t** Is_, int32_t** Js_, int32_t** Kp_,
+                                int32_t** locI_, int32_t** locJ_, int32_t** locK_) {
+  const int r = h->r;
+  const size_t is_b = align256(sizeof(int32_t) * r * nI), js_b = align256(sizeof(int32_t) * r * nJ);
+  const size_t kp_b = align256(sizeof(int32_t) * r * nKp);
+  const size_t li_b = align256(sizeof(int32_t) * r * h->I), lj_b = align256(sizeof(int32_t) * r * h->J);
+  const size_t lk_b = align256(sizeof(int32_t) * r * std::max<int64_t>(Ko, 1));
+  const size_t key_b = align256(sizeof(uint64_t) * 3 * r * std::max(h->I, std::max(h->J, Ko)));
+  cudaError_t e = h->samp.ensure(is_b + js_b + kp_b + li_b + lj_b + lk_b + key_b);
+  if (e != cudaSuccess) return e;
+  char* sp = h->samp.as<char>();
+  int32_t* Is = (int32_t*)sp; sp += is_b;
+  int32_t* Js = (int32_t*)sp; sp += js_b;
+  int32_t* Kp = (int32_t*)sp; sp += kp_b;
+  int32_t* locI = (int32_t*)sp; sp += li_b;
+  int32_t* locJ = (int32_t*)sp; sp += lj_b;
+  int32_t* locK = (int32_t*)sp; sp += lk_b;
+  uint64_t* keys = (uint64_t*)sp;
+  const int64_t kstride = std::max(h->I, std::max(h->J, Ko));
+  for (int rho = 0; rho < r; ++rho) {
+    for (int m = 0; m < 3; ++m) {
+      SampleSeg& g = h->segs_host[rho * 3 + m];
+      g.rep = rho; g.mode = m;
+      g.keys = keys + (int64_t)(rho * 3 + m) * kstride;
+      g.kp_tail = nullptr; g.tail0 = 0; g.ntail = 0;
+      if (m == 0) { g.w = x1; g.n = h->I; g.ns = nI; g.out = Is + rho * nI; g.loc = locI + rho * h->I; }
+      if (m == 1) { g.w = x2; g.n = h->J; g.ns = nJ; g.out = Js + rho * nJ; g.loc = locJ + rho * h->J; }
+      if (m == 2) {
+        g.w = x3; g.n = Ko; g.ns = nKs; g.out = Kp + rho * nKp; g.loc = locK + rho * Ko;
+        g.kp_tail = Kp + rho * nKp + nKs; g.tail0 = Ko; g.ntail = Kn;
+      }
+    }
+  }
+  e = h->segs.ensure(sizeof(SampleSeg) * 3 * kMaxReps);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(h->segs.p, h->segs_host, sizeof(SampleSeg) * 3 * r, cudaMemcpyHostToDevice, h->st);
+  if (e != cudaSuccess) return e;
+  e = launch_sample(h->segs.as<SampleSeg>(), 3 * r, h->seed, uid, h->st);
+  *Is_ = Is; *Js_ = Js; *Kp_ = Kp; *locI_ = locI; *locJ_ = locJ; *locK_ = locK;
+  return e;
+}
+
+// a5 (match against the batch-start model, R13-R16, R26) and a6 (merge into the shadow model,
+// P:216-227).  Records ev[6] between the two.
+static cudaError_t run_match_merge(sambaten_s* h, const DenseAls& a, const int32_t* Is, const int32_t* Js,
+                                   const int32_t* Kp, const int32_t* locI, const int32_t* locJ,
+                                   const int32_t* locK, int64_t Ko, int64_t Kn, int64_t nI, int64_t nJ,
+                                   int64_t nKs, int64_t nKp, int** accepted) {
+  const int R = h->R, r = h->r;
+  cudaStream_t st = h->st;
+  const int b = h->cur, nb = 1 - h->cur;
+  cudaError_t e = h->match.ensure(align256(sizeof(int) * r * R) + align256(sizeof(double) * r * 3 * R) +
+                                  align256(sizeof(double) * r * R) + align256(sizeof(double) * r) +
+                                  align256(sizeof(int) * r));
+  if (e != cudaSuccess) return e;
+  char* mp = h->match.as<char>();
+  MatchArgs ma{};
+  ma.A = h->A(b); ma.B = h->B(b); ma.C = h->C(b); ma.R = R; ma.r = r;
+  ma.Is = Is; ma.Js = Js; ma.Ks = Kp;
+  ma.nI = (int)nI; ma.nJ = (int)nJ; ma.nKs = (int)nKs; ma.nK = (int)nKp; ma.ks_stride = nKp;
+  for (int m = 0; m < 3; ++m) { ma.U[m] = a.U[m]; ma.u_stride[m] = a.u_stride[m]; }
+  ma.lamp = a.lam; ma.tau = h->opts.accept_tau;
+  ma.pi = (int*)mp; mp += align256(sizeof(int) * r * R);
+  ma.scale = (double*)mp; mp += align256(sizeof(double) * r * 3 * R);
+  ma.lam_hat = (double*)mp; mp += align256(sizeof(double) * r * R);
+  ma.score_min = (double*)mp; mp += align256(sizeof(double) * r);
+  ma.accepted = (int*)mp;
+  e = launch_match(ma, st);
+  if (e != cudaSuccess) return e;
+  e = cudaEventRecord(h->ev[6], st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpyAsync(h->model[nb].p, h->model[b].p, h->model_floats() * sizeof(float),
+                      cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  MergeArgs g{};
+  g.A = h->A(b); g.B = h->B(b); g.C = h->C(b); g.lam = h->lam(b);
+  g.An = h->A(nb); g.Bn = h->B(nb); g.Cn = h->C(nb); g.lamn = h->lam(nb);
+  g.I = h->I; g.J = h->J; g.Ko = Ko; g.Kn = Kn; g.R = R; g.r = r;
+  g.loc[0] = locI; g.loc[1] = locJ; g.loc[2] = locK; g.nKs = (int)nKs;
+  for (int m = 0; m < 3; ++m) { g.U[m] = a.U[m]; g.u_stride[m] = a.u_stride[m]; }
+  g.pi = ma.pi; g.scale = ma.scale; g.lam_hat = ma.lam_hat; g.accepted = ma.accepted;
+  g.policy = h->opts.merge_policy;
+  *accepted = ma.accepted;
+  return launch_merge(g, st);
+}
+
+// Status readback, validation outcome, commit (strong guarantee: nothing above is visible
+// before this point), info and copy-out.
+static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int* accepted,
+                                     const unsigned long long* d_maxphi, const unsigned* d_vflags,
+                                     const double* d_relerr, int64_t Ko, int64_t Kn, int64_t nI,
+                                     int64_t nJ, int64_t nKs, int64_t nKp, int b, int nb, int launches,
+                                     int64_t batch_nnz, float* Aout, float* Bout, float* Cout,
+                                     float* lamout, sambaten_info* info) {
+  const int R = h->R, r = h->r;
+  cudaStream_t st = h->st;
+  (void)b;
+  HostStatus* hs = h->hs;
+  unsigned vflags = 0;
+  CK(cudaMemcpyAsync(&hs->maxphi_bits, d_maxphi, 8, cudaMemcpyDeviceToHost, st));
+  if (d_vflags) CK(cudaMemcpyAsync(&hs->vflags, d_vflags, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs->accepted, accepted, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs->iters, a.iters, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs->flags, a.flags, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hs->fit, a.fit, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
+  if (h->opts.full_fit) CK(cudaMemcpyAsync(&hs->relerr, d_relerr, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (d_vflags) vflags = hs->vflags;
+  if (vflags & 1u) FAIL(SAMBATEN_E_INDEX_RANGE, "update: COO index out of range (S:77)");
+  if (vflags & 6u) FAIL(SAMBATEN_E_INVALID, "update: COO batch not canonical (sorted by (k,j,i), unique, nonzero; R28)");
+  double maxphi;
+  memcpy(&maxphi, &hs->maxphi_bits, 8);
+  if (maxphi > ldexp(1.0, h->maxphi_log2 + 8))
+    FAIL(SAMBATEN_E_FIXEDPOINT_RANGE, "update: batch value outside the fixed-point range (R7)");
+  uint32_t rejected = 0, pm = 0;
+  int nacc = 0, itmax = 0;
+  double fsum = 0.0;
+  for (int rho = 0; rho < r; ++rho) {
+    if (hs->accepted[rho]) ++nacc; else rejected |= 1u << rho;
+    if (hs->flags[rho] & 1) pm |= 1u << rho;
+    itmax = std::max(itmax, hs->iters[rho]);
+    fsum += hs->fit[rho];
+  }
+  if (nacc == 0) FAIL(SAMBATEN_E_BATCH_REJECTED, "update: every repetition was rejected (R26)");
+  // commit
+  h->cur = nb;
+  h->K = Ko + Kn;
+  if (h->fmt == SAMBATEN_COO) h->nnz += batch_nnz;
+  h->update_id += 1;
+  h->last_n[0] = nI; h->last_n[1] = nJ; h->last_n[2] = nKs; h->last_nKp = nKp;
+  if (info) {
+    info->fit_summary = fsum / r;
+    info->fit_full = h->opts.full_fit ? 1.0 - hs->relerr : -1.0;
+    info->als_iters_max = itmax;
+    info->k_total = h->K;
+    info->reps_rejected_mask = rejected;
+    info->scale_exp = h->S;
+    info->reps_pinv_mask = pm;
+    info->kernel_launches = launches;
+    for (int e = 0; e < 8; ++e) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);
+      info->step_ms[e] = ms;
+    }
+  }
+  if (Aout) CK(cudaMemcpyAsync(Aout, h->A(nb), sizeof(float) * h->I * R, cudaMemcpyDefault, st));
+  if (Bout) CK(cudaMemcpyAsync(Bout, h->B(nb), sizeof(float) * h->J * R, cudaMemcpyDefault, st));
+  if (Cout) CK(cudaMemcpyAsync(Cout, h->C(nb), sizeof(float) * h->K * R, cudaMemcpyDefault, st));
+  if (lamout) CK(cudaMemcpyAsync(lamout, h->lam(nb), sizeof(float) * R, cudaMemcpyDefault, st));
+  if (Aout || Bout || Cout || lamout) CK(cudaStreamSynchronize(st));
+  return SAMBATEN_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// COO: batched CP-ALS on r concatenated COO summaries (entries [off[rho], off[rho+1]) of rep
+// rho, canonical (u, q, p)).  Mode-0/1 row structure by stable radix sort, mode 2 by the
+// natural order; per iteration and mode: MTTKRP (warp per row) -> R x R solve / normalise /
+// Gram / fit (k_als.cu solve kernel).  Returns the ALS state in `d`.
+// ---------------------------------------------------------------------------------------
+struct Bump {
+  char* base = nullptr;
+  size_t off = 0;
+  template <class T> T* take(size_t n) {
+    T* p = reinterpret_cast<T*>(base ? base + off : nullptr);
+    off += (sizeof(T) * n + 255) & ~(size_t)255;
+    return p;
+  }
+};
+
+static int bits_for(int64_t n) { int b = 1; while (((int64_t)1 << b) < n) ++b; return b; }
+
+static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int32_t* p, const int32_t* q,
+                               const int32_t* u, const float* v, const int64_t* d_off, int64_t ntot,
+                               int nI, int nJ, int nK, int r, float* U0, float* U1, float* U2,
+                               uint64_t seed, uint32_t uid, int maxit, double tol, bool init_factors,
+                               DenseAls* d, int* launches) {
+  const int64_t maxn = std::max<int64_t>(nI, std::max<int64_t>(nJ, nK));
+  const int kb0 = bits_for(nI), kb1 = bits_for(nJ), kb2 = bits_for(nK);
+  const int64_t n = std::max<int64_t>(ntot, 1);
+  const int64_t pmax = (int64_t)r * maxn + 1;
+  const size_t sws_n = std::max(scan_ws_elems(radix_ws_elems(n)), scan_ws_elems(pmax));
+  auto layout = [&](Bump& b, bool assign) {
+    uint32_t* keys = b.take<uint32_t>(n);
+    int32_t* perm0 = b.take<int32_t>(n);
+    int32_t* perm1 = b.take<int32_t>(n);
+    uint32_t* wk = b.take<uint32_t>(n);
+    int32_t* wv = b.take<int32_t>(n);
+    int64_t* hist = b.take<int64_t>(radix_ws_elems(n));
+    int64_t* offs = b.take<int64_t>(radix_ws_elems(n));
+    int64_t* sws = b.take<int64_t>(sws_n);
+    int64_t* cnt = b.take<int64_t>(pmax);
+    int64_t* ptr0 = b.take<int64_t>((int64_t)r * nI + 1);
+    int64_t* ptr1 = b.take<int64_t>((int64_t)r * nJ + 1);
+    int64_t* ptr2 = b.take<int64_t>((int64_t)r * nK + 1);
+    double* G = b.take<double>((size_t)r * 3 * R * R);
+    double* lam = b.take<double>((size_t)r * R);
+    double* ysq = b.take<double>((size_t)r * 257);
+    double* fit = b.take<double>(r);
+    double* fitp = b.take<double>(r);
+    int* iters = b.take<int>(r);
+    int* done = b.take<int>(r);
+    int* flags = b.take<int>(r);
+    double* M0 = b.take<double>((size_t)r * nI * R);
+    double* Mb = b.take<double>((size_t)r * maxn * R);
+    double* Us = b.take<double>((size_t)r * maxn * R);
+    if (!assign) return;
+    *d = DenseAls{};
+    d->nI = nI; d->nJ = nJ; d->nK = nK; d->R = R; d->r = r;
+    d->U[0] = U0; d->U[1] = U1; d->U[2] = U2;
+    d->u_stride[0] = (int64_t)nI * R; d->u_stride[1] = (int64_t)nJ * R; d->u_stride[2] = (int64_t)nK * R;
+    d->G = G; d->lam = lam; d->ysq = ysq; d->fit = fit; d->fit_prev = fitp; d->iters = iters;
+    d->done = done; d->flags = flags; d->part0 = M0; d->nb0 = 1; d->rows_per_block0 = 0;
+    d->M = Mb; d->m_stride = maxn * R; d->Uscr = Us; d->maxit = maxit; d->tol = tol;
+    // sort / row pointers
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = coo_sort_by_index(p, d_off, r, kb0, ntot, keys, perm0, wk, wv, hist, offs, sws, st);
+    if (e == cudaSuccess) e = coo_row_pointers(keys, ntot, kb0, r, nI, cnt, ptr0, sws, st);
+    if (e == cudaSuccess) e = coo_sort_by_index(q, d_off, r, kb1, ntot, keys, perm1, wk, wv, hist, offs, sws, st);
+    if (e == cudaSuccess) e = coo_row_pointers(keys, ntot, kb1, r, nJ, cnt, ptr1, sws, st);
+    if (e == cudaSuccess) e = coo_make_keys(u, d_off, r, kb2, ntot, keys, st);
+    if (e == cudaSuccess) e = coo_row_pointers(keys, ntot, kb2, r, nK, cnt, ptr2, sws, st);
+    CooAls a{};
+    a.nI = nI; a.nJ = nJ; a.nK = nK; a.R = R; a.r = r;
+    a.RB = R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
+    a.p = p; a.q = q; a.u = u; a.v = v;
+    a.perm[0] = perm0; a.perm[1] = perm1; a.perm[2] = nullptr;
+    a.ptr[0] = ptr0; a.ptr[1] = ptr1; a.ptr[2] = ptr2;
+    for (int m = 0; m < 3; ++m) { a.U[m] = d->U[m]; a.u_stride[m] = d->u_stride[m]; }
+    a.M[0] = M0; a.m_stride[0] = (int64_t)nI * R;
+    a.M[1] = a.M[2] = Mb; a.m_stride[1] = a.m_stride[2] = maxn * R;
+    a.done = done;
+    if (e == cudaSuccess && init_factors) e = launch_als_init_factors(*d, seed, uid, 0, st);
+    if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(done, 0, sizeof(int) * r, st);
+    if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(iters, 0, sizeof(int) * r, st);
+    if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(flags, 0, sizeof(int) * r, st);
+    if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(fit, 0, sizeof(double) * r, st);
+    if (e == cudaSuccess) e = launch_als_gram(*d, st);
+    if (e == cudaSuccess) e = launch_coo_sumsq(v, d_off, r, ysq, st);
+    for (int it = 0; it < maxit && e == cudaSuccess; ++it)
+      for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
+        e = launch_coo_mttkrp(a, m, st);
+        if (e == cudaSuccess) e = launch_als_solve(*d, m, st);
+      }
+    *launches = 2 * 3 + 9 + 3 + 3 + 3 + 6 * maxit;
+    if (e != cudaSuccess) {
+      set_error(std::string("COO ALS: ") + cudaGetErrorString(e));
+      d->nI = -1;
+    }
+  };
+  Bump sz;
+  layout(sz, false);
+  CK(wsbuf.ensure(sz.off));
+  Bump b{wsbuf.as<char>(), 0};
+  layout(b, true);
+  if (d->nI < 0) return SAMBATEN_E_CUDA;
+  return SAMBATEN_OK;
+}
+
+__global__ static void two_offsets_kernel(int64_t* off, int64_t n) {
+  if (threadIdx.x == 0) { off[0] = 0; off[1] = n; }
+}
+
+// Full CP-ALS of the initial COO tensor: the store itself is the single "summary"
+// (identity maps p = i, q = j, u = k), Philox init with update_id 0 (R10).
+static sambaten_status init_als_coo(sambaten_s* h) {
+  DevBuf offb;
+  CK(offb.ensure(2 * sizeof(int64_t)));
+  two_offsets_kernel<<<1, 32, 0, h->st>>>(offb.as<int64_t>(), h->nnz);
+  DenseAls d{};
+  int nl = 0;
+  if (sambaten_status e = coo_als(h->coo_ws, h->st, h->R, h->ci(), h->cj(), h->ck_(), h->cv(),
+                                  offb.as<int64_t>(), h->nnz, (int)h->I, (int)h->J, (int)h->K, 1,
+                                  h->A(h->cur), h->B(h->cur), h->C(h->cur), h->seed, 0,
+                                  h->opts.init_max_iters, h->opts.init_tol, true, &d, &nl))
+    return e;
+  lam_to_f32_kernel<<<1, 32, 0, h->st>>>(d.lam, h->R, h->lam(h->cur));
+  CK(cudaStreamSynchronize(h->st));
+  return SAMBATEN_OK;
+}
+
+__global__ static void rep_offsets_kernel(const int64_t* scan, int64_t nb, int r, int64_t* off) {
+  const int t = threadIdx.x;
+  if (t <= r) off[t] = scan[(int64_t)t * nb];
+}
+
+// The COO update (Alg. 1 with the sparse store): see the dense update for the step structure.
+static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, float* Aout,
+                                  float* Bout, float* Cout, float* lamout, sambaten_info* info) {
+  const int64_t Kn = batch->dims[2];
+  const int64_t bn = batch->nnz;
+  if (bn < 0) FAIL(SAMBATEN_E_INVALID, "update: negative nnz");
+  if (bn > 0 && (!batch->idx[0] || !batch->idx[1] || !batch->idx[2] || !batch->vals))
+    FAIL(SAMBATEN_E_INVALID, "update: NULL COO array");
+  const int64_t Ko = h->K;
+  if (Ko + Kn > h->Kcap) FAIL(SAMBATEN_E_OOM, "update: mode-3 capacity exceeded (opts.capacity_k)");
+  if (h->nnz + bn > h->nnz_cap) FAIL(SAMBATEN_E_OOM, "update: nnz capacity exceeded (opts.capacity)");
+  cudaStream_t st = h->st;
+  const int R = h->R, r = h->r;
+  const uint32_t uid = h->update_id + 1;
+  const int64_t nI = sample_n(h->I, h->s[0]), nJ = sample_n(h->J, h->s[1]);
+  const int64_t nKs = sample_n(Ko, h->s[2]), nKp = nKs + Kn;
+  const int64_t ntot = h->nnz + bn;
+  int launches = 0;
+
+  CK(cudaEventRecord(h->ev[0], st));
+  // ---- a0: validate + append the batch (not visible until commit), max phi ---------------
+  CK(h->misc.ensure(4096));
+  unsigned long long* d_maxphi = h->misc.as<unsigned long long>();
+  unsigned* d_vflags = reinterpret_cast<unsigned*>(h->misc.as<char>() + 8);
+  double* d_relerr = reinterpret_cast<double*>(h->misc.as<char>() + 64);
+  CK(cudaMemsetAsync(h->misc.p, 0, 16, st));
+  // copy (host or device arrays) into the store capacity, validate there, then shift k
+  int32_t* ti = h->ci() + h->nnz;
+  int32_t* tj = h->cj() + h->nnz;
+  int32_t* tk = h->ck_() + h->nnz;
+  float* tv = h->cv() + h->nnz;
+  if (bn > 0) {
+    CK(cudaMemcpyAsync(ti, batch->idx[0], sizeof(int32_t) * bn, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(tj, batch->idx[1], sizeof(int32_t) * bn, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(tk, batch->idx[2], sizeof(int32_t) * bn, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(tv, batch->vals, sizeof(float) * bn, cudaMemcpyDefault, st));
+  }
+  CK(launch_coo_validate(ti, tj, tk, tv, bn, h->I, h->J, Kn, d_vflags, st));
+  CK(launch_coo_append(ti, tj, tk, tv, bn, (int32_t)Ko, ti, tj, tk, tv, st));
+  CK(launch_coo_max_phi(h->cv() + h->nnz, bn, h->opts.moi, d_maxphi, st));
+  launches += 3;
+  CK(cudaEventRecord(h->ev[1], st));
+  // ---- a1: marginals over X_old U X_new (R2, R3) ----------------------------------------
+  const size_t marg_bytes = sizeof(int64_t) * (h->I + h->J + h->Kcap);
+  CK(h->marg.ensure(marg_bytes));
+  int64_t* x1 = h->marg.as<int64_t>();
+  int64_t* x2 = x1 + h->I;
+  int64_t* x3 = x2 + h->J;
+  CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
+  CK(launch_marginals_coo(h->ci(), h->cj(), h->ck_(), h->cv(), ntot, h->opts.moi, h->S, x1, x2, x3, st));
+  launches += 1;
+  CK(cudaEventRecord(h->ev[2], st));
+  // ---- a2: sampling ---------------------------------------------------------------------
+  int32_t *Is, *Js, *Kp, *locI, *locJ, *locK;
+  CK(run_sampling(h, x1, x2, x3, Ko, Kn, nI, nJ, nKs, nKp, uid, &Is, &Js, &Kp, &locI, &locJ, &locK));
+  launches += 1;
+  CK(cudaEventRecord(h->ev[3], st));
+  // ---- a3: gather (membership bitmaps, count, scan, write) ------------------------------
+  const int64_t nbk = coo_gather_blocks(ntot);
+  Bump gsz;
+  auto glayout = [&](Bump& b) {
+    b.take<uint32_t>(h->I); b.take<uint32_t>(h->J); b.take<uint32_t>(Ko + Kn);
+    b.take<int64_t>((int64_t)r * nbk + 1); b.take<int64_t>((int64_t)r * nbk + 1);
+    b.take<int64_t>(scan_ws_elems((int64_t)r * nbk + 1)); b.take<int64_t>(r + 1);
+  };
+  glayout(gsz);
+  CK(h->summ.ensure(gsz.off));
+  Bump gb{h->summ.as<char>(), 0};
+  uint32_t* mI = gb.take<uint32_t>(h->I);
+  uint32_t* mJ = gb.take<uint32_t>(h->J);
+  uint32_t* mK = gb.take<uint32_t>(Ko + Kn);
+  int64_t* counts = gb.take<int64_t>((int64_t)r * nbk + 1);
+  int64_t* goffs = gb.take<int64_t>((int64_t)r * nbk + 1);
+  int64_t* gsws = gb.take<int64_t>(scan_ws_elems((int64_t)r * nbk + 1));
+  int64_t* d_off = gb.take<int64_t>(r + 1);
+  CK(launch_build_mask(locI, h->I, r, mI, h->I, st));
+  CK(launch_build_mask(locJ, h->J, r, mJ, h->J, st));
+  CK(launch_build_mask(locK, Ko, r, mK, Ko + Kn, st));
+  CK(cudaMemsetAsync(counts + (int64_t)r * nbk, 0, sizeof(int64_t), st));
+  const CooView Xall = h->coo_view(ntot);
+  CK(launch_coo_gather_count(Xall, mI, mJ, mK, r, counts, st));
+  CK(exclusive_scan_i64(counts, (int64_t)r * nbk + 1, goffs, gsws, st));
+  rep_offsets_kernel<<<1, 64, 0, st>>>(goffs, nbk, r, d_off);
+  CK(cudaGetLastError());
+  int64_t h_off[kMaxReps + 1];
+  CK(cudaMemcpyAsync(h_off, d_off, sizeof(int64_t) * (r + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));   // summary sizes decide the allocation below
+  const int64_t nsum = h_off[r];
+  const size_t sbytes = align256(sizeof(int32_t) * std::max<int64_t>(nsum, 1));
+  CK(h->fac.ensure(4 * sbytes + align256(sizeof(float) * r * (nI + nJ + nKp) * R)));
+  int32_t* sp = h->fac.as<int32_t>();
+  int32_t* sq = reinterpret_cast<int32_t*>(h->fac.as<char>() + sbytes);
+  int32_t* su = reinterpret_cast<int32_t*>(h->fac.as<char>() + 2 * sbytes);
+  float* sv = reinterpret_cast<float*>(h->fac.as<char>() + 3 * sbytes);
+  float* U0 = reinterpret_cast<float*>(h->fac.as<char>() + 4 * sbytes);
+  float* U1 = U0 + (size_t)r * nI * R;
+  float* U2 = U1 + (size_t)r * nJ * R;
+  CK(launch_coo_gather_write(Xall, mI, mJ, mK, locI, locJ, locK, Ko, (int)nKs, r, goffs, sp, sq, su, sv, st));
+  launches += 3 + 1 + 3 + 1 + 1;
+  CK(cudaEventRecord(h->ev[4], st));
+  // ---- a4: batched CP-ALS on the COO summaries ----------------------------------------------
+  DenseAls a{};
+  int als_launches = 0;
+  if (sambaten_status e = coo_als(h->coo_ws, st, R, sp, sq, su, sv, d_off, nsum, (int)nI, (int)nJ,
+                                  (int)nKp, r, U0, U1, U2, h->seed, uid, h->opts.als_max_iters,
+                                  h->opts.als_tol, true, &a, &als_launches))
+    return e;
+  launches += als_launches;
+  CK(cudaEventRecord(h->ev[5], st));
+  // ---- a5 / a6: match and merge (format independent) -----------------------------------------
+  const int b = h->cur, nbuf = 1 - h->cur;
+  int* accepted = nullptr;
+  CK(run_match_merge(h, a, Is, Js, Kp, locI, locJ, locK, Ko, Kn, nI, nJ, nKs, nKp, &accepted));
+  launches += 1 + 4;
+  CK(cudaEventRecord(h->ev[7], st));
+  // ---- a7: full fit of the new model (optional) ----------------------------------------------
+  if (h->opts.full_fit) {
+    CK(h->fitws.ensure(sizeof(double) * coo_fit_ws_doubles()));
+    CooView Xn = Xall;
+    Xn.K = Ko + Kn;
+    CK(launch_coo_fit(Xn, h->lam(nbuf), h->A(nbuf), h->B(nbuf), h->C(nbuf), R, h->fitws.as<double>(),
+                      d_relerr, st));
+    launches += 3;
+  }
+  CK(cudaEventRecord(h->ev[8], st));
+  return finish_update(h, a, accepted, d_maxphi, d_vflags, d_relerr, Ko, Kn, nI, nJ, nKs, nKp, b, nbuf,
+                       launches, bn, Aout, Bout, Cout, lamout, info);
+}
+
 extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* batch, float* Aout,
                                            float* Bout, float* Cout, float* lamout,
                                            sambaten_info* info) {
@@ -339,6 +807,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     FAIL(SAMBATEN_E_SHAPE, "update: batch I x J differs from the state's (S:68)");
   const int64_t Kn = batch->dims[2];
   if (Kn < 1) FAIL(SAMBATEN_E_EMPTY_BATCH, "update: empty batch (S:275)");
+  if (h->fmt == SAMBATEN_COO) return update_coo(h, batch, Aout, Bout, Cout, lamout, info);
   const int64_t Ko = h->K;
   if (Ko + Kn > h->Kcap) FAIL(SAMBATEN_E_OOM, "update: capacity exceeded (opts.capacity)");
   cudaStream_t st = h->st;
@@ -369,39 +838,9 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
   CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, st));
   CK(cudaEventRecord(h->ev[2], st));
-  // ---- a2: sampling (R4-R6); K_s from the old slices only, then K' = K_s ++ new ----------
-  const size_t is_b = align256(sizeof(int32_t) * r * nI), js_b = align256(sizeof(int32_t) * r * nJ);
-  const size_t kp_b = align256(sizeof(int32_t) * r * nKp);
-  const size_t li_b = align256(sizeof(int32_t) * r * h->I), lj_b = align256(sizeof(int32_t) * r * h->J);
-  const size_t lk_b = align256(sizeof(int32_t) * r * Ko);
-  const size_t key_b = align256(sizeof(uint64_t) * 3 * r * std::max(h->I, std::max(h->J, Ko)));
-  CK(h->samp.ensure(is_b + js_b + kp_b + li_b + lj_b + lk_b + key_b));
-  char* sp = h->samp.as<char>();
-  int32_t* Is = (int32_t*)sp; sp += is_b;
-  int32_t* Js = (int32_t*)sp; sp += js_b;
-  int32_t* Kp = (int32_t*)sp; sp += kp_b;
-  int32_t* locI = (int32_t*)sp; sp += li_b;
-  int32_t* locJ = (int32_t*)sp; sp += lj_b;
-  int32_t* locK = (int32_t*)sp; sp += lk_b;
-  uint64_t* keys = (uint64_t*)sp;
-  const int64_t kstride = std::max(h->I, std::max(h->J, Ko));
-  for (int rho = 0; rho < r; ++rho) {
-    for (int m = 0; m < 3; ++m) {
-      SampleSeg& g = h->segs_host[rho * 3 + m];
-      g.rep = rho; g.mode = m;
-      g.keys = keys + (int64_t)(rho * 3 + m) * kstride;
-      g.kp_tail = nullptr; g.tail0 = 0; g.ntail = 0;
-      if (m == 0) { g.w = x1; g.n = h->I; g.ns = nI; g.out = Is + rho * nI; g.loc = locI + rho * h->I; }
-      if (m == 1) { g.w = x2; g.n = h->J; g.ns = nJ; g.out = Js + rho * nJ; g.loc = locJ + rho * h->J; }
-      if (m == 2) {
-        g.w = x3; g.n = Ko; g.ns = nKs; g.out = Kp + rho * nKp; g.loc = locK + rho * Ko;
-        g.kp_tail = Kp + rho * nKp + nKs; g.tail0 = Ko; g.ntail = Kn;
-      }
-    }
-  }
-  CK(h->segs.ensure(sizeof(SampleSeg) * 3 * kMaxReps));
-  CK(cudaMemcpyAsync(h->segs.p, h->segs_host, sizeof(SampleSeg) * 3 * r, cudaMemcpyHostToDevice, st));
-  CK(launch_sample(h->segs.as<SampleSeg>(), 3 * r, h->seed, uid, st));
+  // ---- a2: sampling ---------------------------------------------------------------------
+  int32_t *Is, *Js, *Kp, *locI, *locJ, *locK;
+  CK(run_sampling(h, x1, x2, x3, Ko, Kn, nI, nJ, nKs, nKp, uid, &Is, &Js, &Kp, &locI, &locJ, &locK));
   CK(cudaEventRecord(h->ev[3], st));
   // ---- a3: gather the r summaries ------------------------------------------------------
   int64_t y_stride = (nKp * nJ * nI + 3) & ~int64_t(3);
@@ -449,37 +888,10 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     als_launches = 4 + 7 * a.maxit;
   }
   CK(cudaEventRecord(h->ev[5], st));
-  // ---- a5: match against the batch-start model (R13-R16, R26) ---------------------------
+  // ---- a5 / a6: match and merge -----------------------------------------------------------
   const int b = h->cur, nb = 1 - h->cur;
-  CK(h->match.ensure(align256(sizeof(int) * r * R) + align256(sizeof(double) * r * 3 * R) +
-                     align256(sizeof(double) * r * R) + align256(sizeof(double) * r) +
-                     align256(sizeof(int) * r)));
-  char* mp = h->match.as<char>();
-  MatchArgs ma{};
-  ma.A = h->A(b); ma.B = h->B(b); ma.C = h->C(b); ma.R = R; ma.r = r;
-  ma.Is = Is; ma.Js = Js; ma.Ks = Kp;
-  ma.nI = (int)nI; ma.nJ = (int)nJ; ma.nKs = (int)nKs; ma.nK = (int)nKp; ma.ks_stride = nKp;
-  for (int m = 0; m < 3; ++m) { ma.U[m] = a.U[m]; ma.u_stride[m] = a.u_stride[m]; }
-  ma.lamp = a.lam; ma.tau = h->opts.accept_tau;
-  ma.pi = (int*)mp; mp += align256(sizeof(int) * r * R);
-  ma.scale = (double*)mp; mp += align256(sizeof(double) * r * 3 * R);
-  ma.lam_hat = (double*)mp; mp += align256(sizeof(double) * r * R);
-  ma.score_min = (double*)mp; mp += align256(sizeof(double) * r);
-  ma.accepted = (int*)mp;
-  CK(launch_match(ma, st));
-  CK(cudaEventRecord(h->ev[6], st));
-  // ---- a6: merge into the shadow model --------------------------------------
-  CK(cudaMemcpyAsync(h->model[nb].p, h->model[b].p, h->model_floats() * sizeof(float),
-                     cudaMemcpyDeviceToDevice, st));
-  MergeArgs g{};
-  g.A = h->A(b); g.B = h->B(b); g.C = h->C(b); g.lam = h->lam(b);
-  g.An = h->A(nb); g.Bn = h->B(nb); g.Cn = h->C(nb); g.lamn = h->lam(nb);
-  g.I = h->I; g.J = h->J; g.Ko = Ko; g.Kn = Kn; g.R = R; g.r = r;
-  g.loc[0] = locI; g.loc[1] = locJ; g.loc[2] = locK; g.nKs = (int)nKs;
-  for (int m = 0; m < 3; ++m) { g.U[m] = a.U[m]; g.u_stride[m] = a.u_stride[m]; }
-  g.pi = ma.pi; g.scale = ma.scale; g.lam_hat = ma.lam_hat; g.accepted = ma.accepted;
-  g.policy = h->opts.merge_policy;
-  CK(launch_merge(g, st));
+  int* accepted = nullptr;
+  CK(run_match_merge(h, a, Is, Js, Kp, locI, locJ, locK, Ko, Kn, nI, nJ, nKs, nKp, &accepted));
   CK(cudaEventRecord(h->ev[7], st));
   // ---- a7: full fit of the new model (optional) ------------------------------------------
   if (h->opts.full_fit) {
@@ -489,58 +901,10 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     CK(fit_any(V, h->lam(nb), h->A(nb), h->B(nb), h->C(nb), R, h->fitws.as<double>(), d_relerr, st));
   }
   CK(cudaEventRecord(h->ev[8], st));
-  // ---- status readback and commit ------------------------------------------------------
-  HostStatus* hs = h->hs;
-  CK(cudaMemcpyAsync(&hs->maxphi_bits, d_maxphi, 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hs->accepted, ma.accepted, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hs->iters, a.iters, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hs->flags, a.flags, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(hs->fit, a.fit, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
-  if (h->opts.full_fit) CK(cudaMemcpyAsync(&hs->relerr, d_relerr, 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  double maxphi;
-  memcpy(&maxphi, &hs->maxphi_bits, 8);
-  if (maxphi > ldexp(1.0, h->maxphi_log2 + 8))
-    FAIL(SAMBATEN_E_FIXEDPOINT_RANGE, "update: batch value outside the fixed-point range (R7)");
-  uint32_t rejected = 0;
-  int nacc = 0, itmax = 0;
-  double fsum = 0.0;
-  for (int rho = 0; rho < r; ++rho) {
-    if (hs->accepted[rho]) ++nacc; else rejected |= 1u << rho;
-    itmax = std::max(itmax, hs->iters[rho]);
-    fsum += hs->fit[rho];
-  }
-  if (nacc == 0) FAIL(SAMBATEN_E_BATCH_REJECTED, "update: every repetition was rejected (R26)");
-  // commit
-  h->cur = nb;
-  h->K = Ko + Kn;
-  h->update_id = uid;
-  h->last_n[0] = nI; h->last_n[1] = nJ; h->last_n[2] = nKs; h->last_nKp = nKp;
-  if (info) {
-    info->fit_summary = fsum / r;
-    info->fit_full = h->opts.full_fit ? 1.0 - hs->relerr : -1.0;
-    info->als_iters_max = itmax;
-    info->k_total = h->K;
-    info->reps_rejected_mask = rejected;
-    info->scale_exp = h->S;
-    uint32_t pm = 0;
-    for (int rho = 0; rho < r; ++rho) if (hs->flags[rho] & 1) pm |= 1u << rho;
-    info->reps_pinv_mask = pm;
-    // max_phi, marginals, sample, gather, als_init + gram + 2 sumsq, 7 per ALS iteration
-    // (all iterations are launched; converged reps exit at once), match, 3 + 1 merge, 2 fit
-    info->kernel_launches = 1 + 1 + 1 + 1 + als_launches + 1 + 4 + (h->opts.full_fit ? 3 : 0);
-    for (int e = 0; e < 8; ++e) {
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);
-      info->step_ms[e] = ms;
-    }
-  }
-  if (Aout) CK(cudaMemcpyAsync(Aout, h->A(nb), sizeof(float) * h->I * R, cudaMemcpyDefault, st));
-  if (Bout) CK(cudaMemcpyAsync(Bout, h->B(nb), sizeof(float) * h->J * R, cudaMemcpyDefault, st));
-  if (Cout) CK(cudaMemcpyAsync(Cout, h->C(nb), sizeof(float) * h->K * R, cudaMemcpyDefault, st));
-  if (lamout) CK(cudaMemcpyAsync(lamout, h->lam(nb), sizeof(float) * R, cudaMemcpyDefault, st));
-  if (Aout || Bout || Cout || lamout) CK(cudaStreamSynchronize(st));
-  return SAMBATEN_OK;
+  // copy-in, max_phi, marginals, sample, gather, ALS, match, 3 + 1 merge, 3 fit
+  const int launches = 1 + 1 + 1 + 1 + als_launches + 1 + 4 + (h->opts.full_fit ? 3 : 0);
+  return finish_update(h, a, accepted, d_maxphi, nullptr, d_relerr, Ko, Kn, nI, nJ, nKs, nKp, b, nb,
+                       launches, 0, Aout, Bout, Cout, lamout, info);
 }
 
 extern "C" sambaten_status sambaten_get_factors(sambaten_t h, const float** A, const float** B,
@@ -576,6 +940,16 @@ extern "C" sambaten_status sambaten_last_samples(sambaten_t h, int32_t* Is, int3
 
 extern "C" sambaten_status sambaten_relative_error(sambaten_t h, double* relerr) {
   if (!h || !relerr) FAIL(SAMBATEN_E_INVALID, "relative_error: NULL argument");
+  if (h->fmt == SAMBATEN_COO) {
+    DevBuf ws;
+    CK(ws.ensure(sizeof(double) * (coo_fit_ws_doubles() + 8)));
+    double* d = ws.as<double>();
+    CK(launch_coo_fit(h->coo_view(h->nnz), h->lam(h->cur), h->A(h->cur), h->B(h->cur), h->C(h->cur),
+                      h->R, d + 8, d, h->st));
+    CK(cudaMemcpyAsync(relerr, d, 8, cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    return SAMBATEN_OK;
+  }
   DenseView V = h->view();
   DevBuf ws;
   CK(ws.ensure(sizeof(double) * (fit_ws_doubles_any(V) + 8)));
@@ -594,6 +968,7 @@ extern "C" sambaten_status sambaten_checkpoint(sambaten_t h) {
                      cudaMemcpyDeviceToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
   h->K_ck = h->K;
+  h->nnz_ck = h->nnz;
   h->uid_ck = h->update_id;
   return SAMBATEN_OK;
 }
@@ -605,6 +980,7 @@ extern "C" sambaten_status sambaten_restore(sambaten_t h) {
                      cudaMemcpyDeviceToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
   h->K = h->K_ck;
+  h->nnz = h->nnz_ck;
   h->update_id = h->uid_ck;
   return SAMBATEN_OK;
 }

@@ -142,6 +142,61 @@ cudaError_t launch_fit_dense(const DenseView& X, const float* lam, const float* 
                              double* relerr, cudaStream_t st);
 size_t fit_dense_ws_doubles(const DenseView& X);
 
+// ---- COO (k_coo.cu) -----------------------------------------------------------------
+struct CooView {                       // canonical COO tensor, device arrays
+  const int32_t *i, *j, *k;
+  const float* v;
+  int64_t nnz, I, J, K;
+};
+struct CooAls {                        // the r COO summaries (concatenated) + ALS buffers
+  int nI, nJ, nK, R, RB, r;
+  const int32_t *p, *q, *u;            // local coordinates, canonical (u, q, p) per rep
+  const float* v;
+  const int32_t* perm[3];              // entry order sorted by mode index (perm[2] = null)
+  const int64_t* ptr[3];               // row pointers: rep rho, row x -> ptr[m][rho*rows + x]
+  float* U[3]; int64_t u_stride[3];
+  double* M[3]; int64_t m_stride[3];
+  const int* done;
+};
+cudaError_t launch_coo_validate(const int32_t* i, const int32_t* j, const int32_t* k, const float* v,
+                                int64_t n, int64_t I, int64_t J, int64_t K, unsigned* flags,
+                                cudaStream_t st);
+cudaError_t launch_coo_append(const int32_t* bi, const int32_t* bj, const int32_t* bk, const float* bv,
+                              int64_t n, int32_t k_shift, int32_t* si, int32_t* sj, int32_t* sk,
+                              float* sv, cudaStream_t st);
+cudaError_t launch_build_mask(const int32_t* loc, int64_t n, int r, uint32_t* mask, int64_t total,
+                              cudaStream_t st);
+int64_t coo_gather_blocks(int64_t nnz);
+cudaError_t launch_coo_gather_count(const CooView& X, const uint32_t* mI, const uint32_t* mJ,
+                                    const uint32_t* mK, int r, int64_t* counts, cudaStream_t st);
+cudaError_t launch_coo_gather_write(const CooView& X, const uint32_t* mI, const uint32_t* mJ,
+                                    const uint32_t* mK, const int32_t* locI, const int32_t* locJ,
+                                    const int32_t* locK, int64_t Ko, int nKs, int r,
+                                    const int64_t* offsets, int32_t* op, int32_t* oq, int32_t* ou,
+                                    float* ov, cudaStream_t st);
+size_t scan_ws_elems(int64_t n);
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* ws, cudaStream_t st);
+size_t radix_ws_elems(int64_t n);
+cudaError_t coo_sort_by_index(const int32_t* idx, const int64_t* off, int r, int kb, int64_t n,
+                              uint32_t* keys, int32_t* perm, uint32_t* ws_keys, int32_t* ws_vals,
+                              int64_t* hist, int64_t* offs, int64_t* sws, cudaStream_t st);
+cudaError_t coo_make_keys(const int32_t* idx, const int64_t* off, int r, int kb, int64_t n,
+                          uint32_t* keys, cudaStream_t st);
+cudaError_t coo_row_pointers(const uint32_t* sorted_keys, int64_t n, int kb, int r, int64_t rows,
+                             int64_t* cnt, int64_t* ptr, int64_t* sws, cudaStream_t st);
+cudaError_t launch_coo_mttkrp(const CooAls& a, int mode, cudaStream_t st);
+cudaError_t launch_coo_sumsq(const float* v, const int64_t* off, int r, double* ysq, cudaStream_t st);
+size_t coo_fit_ws_doubles();
+cudaError_t launch_coo_fit(const CooView& X, const float* lam, const float* A, const float* B,
+                           const float* C, int R, double* ws, double* relerr, cudaStream_t st);
+cudaError_t launch_coo_max_phi(const float* v, int64_t n, int moi, unsigned long long* out, cudaStream_t st);
+// ALS pieces shared with the COO path (k_als.cu)
+cudaError_t launch_als_solve(const DenseAls& a, int mode, cudaStream_t st);
+cudaError_t launch_als_gram(const DenseAls& a, cudaStream_t st);
+// Grams of three factors, fp64 [3][R][R] (k_stream.cu)
+cudaError_t launch_gram3(const float* A, const float* B, const float* C, int64_t I, int64_t J,
+                         int64_t K, int R, double* G, cudaStream_t st);
+
 // k_stream.cu: TMA-ring streaming passes over the dense store (pitch % 4 == 0, 16 B aligned)
 bool stream_supported(const DenseView& X);
 cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,

@@ -498,6 +498,22 @@ cudaError_t launch_als_init_factors(const DenseAls& a, uint64_t seed, uint32_t u
   return cudaGetLastError();
 }
 
+cudaError_t launch_als_gram(const DenseAls& a, cudaStream_t st) {
+  gram_kernel<<<dim3(3, a.r), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_als_solve(const DenseAls& a, int mode, cudaStream_t st) {
+  if (a.R <= 4) solve_kernel<4><<<a.r, kAlsThreads, 0, st>>>(a, mode);
+  else if (a.R <= 8) solve_kernel<8><<<a.r, kAlsThreads, 0, st>>>(a, mode);
+  else if (a.R <= 10) solve_kernel<10><<<a.r, kAlsThreads, 0, st>>>(a, mode);
+  else if (a.R <= 12) solve_kernel<12><<<a.r, kAlsThreads, 0, st>>>(a, mode);
+  else if (a.R <= 16) solve_kernel<16><<<a.r, kAlsThreads, 0, st>>>(a, mode);
+  else if (a.R <= 24) solve_kernel<24><<<a.r, kAlsThreads, 0, st>>>(a, mode);
+  else solve_kernel<32><<<a.r, kAlsThreads, 0, st>>>(a, mode);
+  return cudaGetLastError();
+}
+
 template <int RB>
 static void als_iteration(const DenseAls& a, cudaStream_t st) {
   int cw, nz, RP;

@@ -1,0 +1,621 @@
+// k_coo.cu -- the sparse (COO) variant of the hot path.
+//
+//   a0  validation of a canonical batch (sorted by (k,j,i), unique, nonzero, in range; R28)
+//       and append into the store's capacity with k shifted by K_old;
+//   a3  summaries X(I_s, J_s, K') of all r repetitions in one pass over the nnz:
+//       per-mode membership bitmaps (bit rho = sampled in repetition rho) -> per-entry rep
+//       mask -> order-preserving two-pass compaction (ballot ranks), relabelled to local
+//       coordinates (p, q, u).  The input order (k,j,i) maps to (u,q,p) monotonically, so every
+//       summary comes out canonical without a sort;
+//   a4  per-mode row structure for the ALS: a stable LSD radix sort (8-bit digits, warp
+//       match_any ranks -> deterministic) of each summary by its mode-0 / mode-1 index, row
+//       pointers by histogram + scan; MTTKRP with one warp per output row, lanes over the
+//       row's entries and a fixed butterfly -> deterministic, no float atomics;
+//   a7  fit of the model over the whole COO store.
+// All integer work (counts, ranks, offsets) is exact; the gathered values are bit copies.
+#include "common.cuh"
+#include "internal.h"
+
+namespace sbt {
+
+namespace {
+
+constexpr int kCT = 256;
+
+// ---------------------------------------------------------------------------------------
+// a0: validation and append
+// ---------------------------------------------------------------------------------------
+__global__ void coo_validate_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                    const int32_t* __restrict__ kk, const float* __restrict__ vv,
+                                    int64_t n, int64_t I, int64_t J, int64_t K, unsigned* flags) {
+  unsigned f = 0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t i = ii[e], j = jj[e], k = kk[e];
+    if (i < 0 || i >= I || j < 0 || j >= J || k < 0 || k >= K) f |= 1u;   // index range
+    const float v = vv[e];
+    if (v == 0.0f || !(fabsf(v) <= 3.4e38f)) f |= 2u;                     // zero / non-finite
+    if (e + 1 < n) {
+      const int32_t i2 = ii[e + 1], j2 = jj[e + 1], k2 = kk[e + 1];
+      const bool less = k < k2 || (k == k2 && (j < j2 || (j == j2 && i < i2)));
+      if (!less) f |= 4u;                                                 // order / duplicate
+    }
+  }
+  if (f) atomicOr(flags, f);
+}
+
+// (may run in place: bi == si etc.)
+__global__ void coo_append_kernel(const int32_t* bi, const int32_t* bj, const int32_t* bk,
+                                  const float* bv, int64_t n, int32_t k_shift, int32_t* si,
+                                  int32_t* sj, int32_t* sk, float* sv) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    si[e] = bi[e];
+    sj[e] = bj[e];
+    sk[e] = bk[e] + k_shift;
+    sv[e] = bv[e];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// exclusive scan of int64 (small arrays: up to a few million) -- 3 kernels
+// ---------------------------------------------------------------------------------------
+constexpr int kScanTile = 2048;
+
+__global__ void scan_tile_kernel(const int64_t* __restrict__ in, int64_t n, int64_t* __restrict__ out,
+                                 int64_t* __restrict__ tile_sums) {
+  __shared__ int64_t sh[kCT];
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  constexpr int PER = kScanTile / kCT;
+  int64_t v[PER];
+  int64_t s = 0;
+#pragma unroll
+  for (int t = 0; t < PER; ++t) {
+    const int64_t e = base + threadIdx.x * PER + t;
+    v[t] = e < n ? in[e] : 0;
+    s += v[t];
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 1; o < kCT; o <<= 1) {   // Hillis-Steele inclusive scan of the thread sums
+    const int64_t x = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += x;
+    __syncthreads();
+  }
+  int64_t run = threadIdx.x > 0 ? sh[threadIdx.x - 1] : 0;
+#pragma unroll
+  for (int t = 0; t < PER; ++t) {
+    const int64_t e = base + threadIdx.x * PER + t;
+    if (e < n) out[e] = run;
+    run += v[t];
+  }
+  if (threadIdx.x == kCT - 1) tile_sums[blockIdx.x] = sh[kCT - 1];
+}
+
+__global__ void scan_sums_kernel(int64_t* sums, int64_t n) {   // single block, sequential chunks
+  __shared__ int64_t sh[kCT];
+  int64_t carry = 0;
+  for (int64_t b = 0; b < n; b += kCT) {
+    const int64_t e = b + threadIdx.x;
+    const int64_t v = e < n ? sums[e] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < kCT; o <<= 1) {
+      const int64_t x = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += x;
+      __syncthreads();
+    }
+    if (e < n) sums[e] = carry + sh[threadIdx.x] - v;   // exclusive
+    carry += sh[kCT - 1];
+    __syncthreads();
+  }
+}
+
+__global__ void scan_add_kernel(int64_t* out, int64_t n, const int64_t* tile_offsets) {
+  const int64_t e = (int64_t)blockIdx.x * kScanTile + threadIdx.x;
+  const int64_t off = tile_offsets[blockIdx.x];
+  for (int t = 0; t < kScanTile / kCT; ++t) {
+    const int64_t x = e + (int64_t)t * kCT;
+    if (x < n && x < ((int64_t)blockIdx.x + 1) * kScanTile) out[x] += off;
+  }
+}
+
+}  // namespace
+
+size_t scan_ws_elems(int64_t n) { return (size_t)ceil_div(n > 0 ? n : 1, kScanTile) + 1; }
+
+// out[e] = sum_{e' < e} in[e'] (in and out may not alias); ws: scan_ws_elems(n) int64
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* ws, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t tiles = ceil_div(n, kScanTile);
+  scan_tile_kernel<<<(unsigned)tiles, kCT, 0, st>>>(in, n, out, ws);
+  scan_sums_kernel<<<1, kCT, 0, st>>>(ws, tiles);
+  scan_add_kernel<<<(unsigned)tiles, kCT, 0, st>>>(out, n, ws);
+  return cudaGetLastError();
+}
+
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// a3: gather.  Membership bitmaps from the sampling's local-index maps, then the two passes.
+// ---------------------------------------------------------------------------------------
+__global__ void build_mask_kernel(const int32_t* __restrict__ loc, int64_t n, int r,
+                                  uint32_t* __restrict__ mask, int64_t n_all_after, int64_t total) {
+  // mask[x] = OR_rho (loc[rho][x] >= 0) << rho for x < n; entries n <= x < total (the new
+  // slices of mode 3) belong to every repetition
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t m = 0;
+    if (x < n) {
+      for (int rho = 0; rho < r; ++rho) m |= (loc[(int64_t)rho * n + x] >= 0 ? 1u : 0u) << rho;
+    } else {
+      m = r == 32 ? 0xffffffffu : ((1u << r) - 1u);
+    }
+    mask[x] = m;
+  }
+  (void)n_all_after;
+}
+
+constexpr int kGTile = kCT * 8;   // entries per gather block
+
+// pass 1: counts[rho][block] of entries with bit rho set
+__global__ void coo_gather_count_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                        const int32_t* __restrict__ kk, int64_t n,
+                                        const uint32_t* __restrict__ mI, const uint32_t* __restrict__ mJ,
+                                        const uint32_t* __restrict__ mK, int r, int64_t nblocks,
+                                        int64_t* __restrict__ counts) {
+  __shared__ int cnt[32];
+  if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kGTile;
+  int local[32];
+  for (int rho = 0; rho < r; ++rho) local[rho] = 0;
+  for (int t = 0; t < kGTile / kCT; ++t) {
+    const int64_t e = base + (int64_t)t * kCT + threadIdx.x;
+    const uint32_t m = e < n ? (mI[ii[e]] & mJ[jj[e]] & mK[kk[e]]) : 0u;
+    const int lane = threadIdx.x & 31;
+    for (int rho = 0; rho < r; ++rho) {
+      const unsigned b = __ballot_sync(0xffffffffu, (m >> rho) & 1u);
+      if (lane == 0) local[rho] += __popc(b);
+    }
+  }
+  if ((threadIdx.x & 31) == 0)
+    for (int rho = 0; rho < r; ++rho)
+      if (local[rho]) atomicAdd(&cnt[rho], local[rho]);
+  __syncthreads();
+  if (threadIdx.x < r) counts[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+}
+
+// pass 2: write the entries of every repetition in input order at offsets[rho][block]
+__global__ void coo_gather_write_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                        const int32_t* __restrict__ kk, const float* __restrict__ vv,
+                                        int64_t n, const uint32_t* __restrict__ mI,
+                                        const uint32_t* __restrict__ mJ, const uint32_t* __restrict__ mK,
+                                        const int32_t* __restrict__ locI, const int32_t* __restrict__ locJ,
+                                        const int32_t* __restrict__ locK, int64_t nIall, int64_t nJall,
+                                        int64_t Ko, int nKs, int r, int64_t nblocks,
+                                        const int64_t* __restrict__ offsets, int32_t* __restrict__ op,
+                                        int32_t* __restrict__ oq, int32_t* __restrict__ ou,
+                                        float* __restrict__ ov) {
+  __shared__ int wcnt[kCT / 32][32];
+  __shared__ int64_t woff[kCT / 32][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kCT / 32;
+  constexpr int PER = kGTile / kCT;
+  // each warp owns a contiguous sub-tile of kGTile / NW entries, processed in rounds of 32
+  const int64_t base = (int64_t)blockIdx.x * kGTile + (int64_t)warp * (kGTile / NW);
+  int c[32];
+  for (int rho = 0; rho < r; ++rho) c[rho] = 0;
+  for (int t = 0; t < PER; ++t) {
+    const int64_t e = base + (int64_t)t * 32 + lane;
+    const uint32_t m = e < n ? (mI[ii[e]] & mJ[jj[e]] & mK[kk[e]]) : 0u;
+    for (int rho = 0; rho < r; ++rho) c[rho] += __popc(__ballot_sync(0xffffffffu, (m >> rho) & 1u));
+  }
+  if (lane == 0)
+    for (int rho = 0; rho < r; ++rho) wcnt[warp][rho] = c[rho];
+  __syncthreads();
+  if (threadIdx.x < r) {   // warp offsets within the block, in warp order
+    int64_t run = offsets[(int64_t)threadIdx.x * nblocks + blockIdx.x];
+    for (int w = 0; w < NW; ++w) { woff[w][threadIdx.x] = run; run += wcnt[w][threadIdx.x]; }
+  }
+  __syncthreads();
+  int64_t pos[32];
+  for (int rho = 0; rho < r; ++rho) pos[rho] = woff[warp][rho];
+  const unsigned lt = (1u << lane) - 1u;
+  for (int t = 0; t < PER; ++t) {
+    const int64_t e = base + (int64_t)t * 32 + lane;
+    uint32_t m = 0;
+    int32_t i = 0, j = 0, k = 0;
+    float v = 0.f;
+    if (e < n) {
+      i = ii[e]; j = jj[e]; k = kk[e];
+      m = mI[i] & mJ[j] & mK[k];
+      if (m) v = vv[e];
+    }
+    for (int rho = 0; rho < r; ++rho) {
+      const bool in = (m >> rho) & 1u;
+      const unsigned b = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const int64_t d = pos[rho] + __popc(b & lt);
+        op[d] = locI[(int64_t)rho * nIall + i];
+        oq[d] = locJ[(int64_t)rho * nJall + j];
+        ou[d] = k < Ko ? locK[(int64_t)rho * Ko + k] : nKs + (k - (int32_t)Ko);
+        ov[d] = v;
+      }
+      pos[rho] += __popc(b);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// stable LSD radix sort of (key, val) pairs, 8-bit digits (used per summary by mode index)
+// ---------------------------------------------------------------------------------------
+constexpr int kRTile = 4096;          // elements per block
+constexpr int kRW = kCT / 32;         // warps per block
+constexpr int kRSub = kRTile / kRW;   // contiguous elements per warp
+
+__global__ void radix_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                                  int64_t nblocks, int64_t* __restrict__ hist /* [256][nblocks] */) {
+  __shared__ int h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRTile;
+  for (int t = threadIdx.x; t < kRTile; t += kCT) {
+    const int64_t e = base + t;
+    if (e < n) atomicAdd(&h[(keys[e] >> shift) & 255u], 1);
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void radix_scatter_kernel(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
+                                     int64_t n, int shift, int64_t nblocks,
+                                     const int64_t* __restrict__ offs /* [256][nblocks] excl */,
+                                     uint32_t* __restrict__ kout, int32_t* __restrict__ vout) {
+  __shared__ int cnt[kRW][256];
+  __shared__ int64_t woff[kRW][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = threadIdx.x; d < kRW * 256; d += kCT) cnt[d / 256][d % 256] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kRTile + (int64_t)warp * kRSub;
+  const unsigned lt = (1u << lane) - 1u;
+  // per-warp digit counts
+  for (int t = 0; t < kRSub; t += 32) {
+    const int64_t e = base + t + lane;
+    const bool ok = e < n;
+    const unsigned d = ok ? (kin[e] >> shift) & 255u : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (ok && (peers & lt) == 0) cnt[warp][d] += __popc(peers);   // the lowest lane of each group
+    __syncwarp();
+  }
+  __syncthreads();
+  {   // warp offsets per digit: global block offset + earlier warps
+    const int d = threadIdx.x;   // kCT == 256 digits
+    int64_t run = offs[(int64_t)d * nblocks + blockIdx.x];
+    for (int w = 0; w < kRW; ++w) { woff[w][d] = run; run += cnt[w][d]; }
+  }
+  __syncthreads();
+  for (int t = 0; t < kRSub; t += 32) {
+    const int64_t e = base + t + lane;
+    const bool ok = e < n;
+    const uint32_t key = ok ? kin[e] : 0u;
+    const unsigned d = ok ? (key >> shift) & 255u : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    int64_t dst = 0;
+    if (ok) dst = woff[warp][d] + __popc(peers & lt);
+    __syncwarp();
+    if (ok && (peers & lt) == 0) woff[warp][d] += __popc(peers);
+    __syncwarp();
+    if (ok) {
+      kout[dst] = key;
+      vout[dst] = vin[e];
+    }
+  }
+}
+
+__global__ void iota_kernel(int32_t* v, int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    v[e] = (int32_t)e;
+}
+
+// composite key rep << kb | idx for the entries of every repetition (offsets off[0..r])
+__global__ void make_keys_kernel(const int32_t* __restrict__ idx, const int64_t* __restrict__ off, int r,
+                                 int kb, int64_t n, uint32_t* __restrict__ keys) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int rho = 0;
+    while (rho + 1 < r && off[rho + 1] <= e) ++rho;
+    keys[e] = ((uint32_t)rho << kb) | (uint32_t)idx[e];
+  }
+}
+
+// ptr[rho][x] = first position (in the sorted order) of the entries of rep rho with index x;
+// from the sorted composite keys: counts then scan.
+__global__ void key_count_kernel(const uint32_t* __restrict__ keys, int64_t n, int kb, int64_t rows,
+                                 int64_t* __restrict__ cnt /* [r*rows] */) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t k = keys[e];
+    const int64_t rho = k >> kb, x = k & ((1u << kb) - 1u);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[rho * rows + x]), 1ull);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// a4: MTTKRP over a COO summary, one warp per (rep, output row):
+//   M(row, f) = sum_{e in row} v_e U_a(a_e, f) U_b(b_e, f)
+// Lane l takes entries l, l+32, ... of the row (fp32 products, fp64 per-lane sums), then a
+// fixed butterfly -> deterministic.
+// ---------------------------------------------------------------------------------------
+template <int RB>
+__global__ void coo_mttkrp_kernel(CooAls a, int mode) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
+  const int64_t tot = (int64_t)a.r * rows;
+  if (gw >= tot) return;
+  const int rep = (int)(gw / rows);
+  const int row = (int)(gw - (int64_t)rep * rows);
+  if (a.done[rep]) return;
+  const int64_t* ptr = a.ptr[mode] + (int64_t)rep * rows;
+  const int64_t b = ptr[row], e = ptr[row + 1];
+  const int32_t* perm = a.perm[mode];   // null for mode 2 (natural order)
+  const int R = a.R;
+  const int oa = mode == 0 ? 1 : 0, ob = mode == 2 ? 1 : 2;
+  const int32_t* ia = oa == 0 ? a.p : a.q;
+  const int32_t* ib = ob == 1 ? a.q : a.u;
+  const float* Ua = a.U[oa] + rep * a.u_stride[oa];
+  const float* Ub = a.U[ob] + rep * a.u_stride[ob];
+  double acc[RB];
+#pragma unroll
+  for (int f = 0; f < RB; ++f) acc[f] = 0.0;
+  for (int64_t t = b + lane; t < e; t += 32) {
+    const int64_t x = perm ? perm[t] : t;
+    const float v = a.v[x];
+    const float* ra = Ua + (int64_t)ia[x] * R;
+    const float* rb = Ub + (int64_t)ib[x] * R;
+#pragma unroll
+    for (int f = 0; f < RB; ++f)
+      if (f < R) acc[f] += (double)(v * ra[f] * rb[f]);
+  }
+#pragma unroll
+  for (int f = 0; f < RB; ++f) {
+    double s = acc[f];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    acc[f] = s;
+  }
+  if (lane == 0) {
+    double* M = a.M[mode] + (int64_t)rep * a.m_stride[mode] + (int64_t)row * R;
+#pragma unroll
+    for (int f = 0; f < RB; ++f)
+      if (f < R) M[f] = acc[f];
+  }
+}
+
+__global__ void coo_sumsq_kernel(const float* __restrict__ v, const int64_t* __restrict__ off, int r,
+                                 double* __restrict__ ysq) {
+  __shared__ double red[32];
+  const int rep = blockIdx.x;
+  double s = 0.0;
+  for (int64_t e = off[rep] + threadIdx.x; e < off[rep + 1]; e += blockDim.x) {
+    const double x = v[e];
+    s += x * x;
+  }
+  s = block_sum_d(s, red);
+  if (threadIdx.x == 0) ysq[rep] = s;
+  (void)r;
+}
+
+// ---------------------------------------------------------------------------------------
+// a7: fit over the COO store: inner = sum_e v_e sum_f lam_f A(i_e,f) B(j_e,f) C(k_e,f), sq
+// ---------------------------------------------------------------------------------------
+template <int RB>
+__global__ void coo_fit_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                               const int32_t* __restrict__ kk, const float* __restrict__ vv, int64_t n,
+                               const float* __restrict__ lam, const float* __restrict__ A,
+                               const float* __restrict__ B, const float* __restrict__ C, int R,
+                               double* __restrict__ part) {
+  __shared__ double red[32];
+  __shared__ float ls[RB];
+  if (threadIdx.x < RB) ls[threadIdx.x] = threadIdx.x < R ? lam[threadIdx.x] : 0.f;
+  __syncthreads();
+  double inner = 0.0, sq = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float v = vv[e];
+    const float* a = A + (int64_t)ii[e] * R;
+    const float* b = B + (int64_t)jj[e] * R;
+    const float* c = C + (int64_t)kk[e] * R;
+    float m = 0.f;
+#pragma unroll
+    for (int f = 0; f < RB; ++f)
+      if (f < R) m = fmaf(ls[f] * a[f], b[f] * c[f], m);
+    inner += (double)v * (double)m;
+    sq += (double)v * (double)v;
+  }
+  inner = block_sum_d(inner, red);
+  sq = block_sum_d(sq, red);
+  if (threadIdx.x == 0) { part[2 * blockIdx.x] = inner; part[2 * blockIdx.x + 1] = sq; }
+}
+
+__global__ void coo_fit_combine_kernel(const double* part, int nb, const double* G, const float* lam,
+                                       int R, double* relerr) {
+  if (threadIdx.x != 0) return;
+  double inner = 0.0, sq = 0.0, mn = 0.0;
+  for (int b = 0; b < nb; ++b) { inner += part[2 * b]; sq += part[2 * b + 1]; }
+  for (int f = 0; f < R; ++f)
+    for (int g = 0; g < R; ++g)
+      mn += (double)lam[f] * (double)lam[g] * G[f * R + g] * G[R * R + f * R + g] * G[2 * R * R + f * R + g];
+  const double res = fmax(0.0, sq - 2.0 * inner + mn);
+  *relerr = sq > 0.0 ? sqrt(res / sq) : 0.0;
+}
+
+inline unsigned grid_for(int64_t n, int per_block = kCT, int cap = kNumSMs * 8) {
+  int64_t g = ceil_div(n > 0 ? n : 1, per_block);
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------
+cudaError_t launch_coo_validate(const int32_t* i, const int32_t* j, const int32_t* k, const float* v,
+                                int64_t n, int64_t I, int64_t J, int64_t K, unsigned* flags,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  coo_validate_kernel<<<grid_for(n), kCT, 0, st>>>(i, j, k, v, n, I, J, K, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coo_append(const int32_t* bi, const int32_t* bj, const int32_t* bk, const float* bv,
+                              int64_t n, int32_t k_shift, int32_t* si, int32_t* sj, int32_t* sk,
+                              float* sv, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  coo_append_kernel<<<grid_for(n), kCT, 0, st>>>(bi, bj, bk, bv, n, k_shift, si, sj, sk, sv);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_mask(const int32_t* loc, int64_t n, int r, uint32_t* mask, int64_t total,
+                              cudaStream_t st) {
+  if (total <= 0) return cudaSuccess;
+  build_mask_kernel<<<grid_for(total), kCT, 0, st>>>(loc, n, r, mask, 0, total);
+  return cudaGetLastError();
+}
+
+int64_t coo_gather_blocks(int64_t nnz) { return ceil_div(nnz > 0 ? nnz : 1, kGTile); }
+
+cudaError_t launch_coo_gather_count(const CooView& X, const uint32_t* mI, const uint32_t* mJ,
+                                    const uint32_t* mK, int r, int64_t* counts, cudaStream_t st) {
+  const int64_t nb = coo_gather_blocks(X.nnz);
+  coo_gather_count_kernel<<<(unsigned)nb, kCT, 0, st>>>(X.i, X.j, X.k, X.nnz, mI, mJ, mK, r, nb, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coo_gather_write(const CooView& X, const uint32_t* mI, const uint32_t* mJ,
+                                    const uint32_t* mK, const int32_t* locI, const int32_t* locJ,
+                                    const int32_t* locK, int64_t Ko, int nKs, int r,
+                                    const int64_t* offsets, int32_t* op, int32_t* oq, int32_t* ou,
+                                    float* ov, cudaStream_t st) {
+  const int64_t nb = coo_gather_blocks(X.nnz);
+  coo_gather_write_kernel<<<(unsigned)nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, mI, mJ, mK, locI,
+                                                        locJ, locK, X.I, X.J, Ko, nKs, r, nb, offsets,
+                                                        op, oq, ou, ov);
+  return cudaGetLastError();
+}
+
+size_t radix_ws_elems(int64_t n) { return 256 * (size_t)ceil_div(n > 0 ? n : 1, kRTile); }
+
+// Sort the composite keys (rep << kb | idx[e]) stably; perm receives the entry order, keys the
+// sorted keys.  ws_keys/ws_vals: n elements each; hist/offs: radix_ws_elems(n) int64 each,
+// sws: scan workspace.
+cudaError_t coo_sort_by_index(const int32_t* idx, const int64_t* off, int r, int kb, int64_t n,
+                              uint32_t* keys, int32_t* perm, uint32_t* ws_keys, int32_t* ws_vals,
+                              int64_t* hist, int64_t* offs, int64_t* sws, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  make_keys_kernel<<<grid_for(n), kCT, 0, st>>>(idx, off, r, kb, n, keys);
+  iota_kernel<<<grid_for(n), kCT, 0, st>>>(perm, n);
+  const int bits = kb + 6;   // rep <= 32 needs 6 bits
+  const int64_t nb = ceil_div(n, kRTile);
+  uint32_t* ka = keys; int32_t* va = perm;
+  uint32_t* kb_ = ws_keys; int32_t* vb = ws_vals;
+  int passes = 0;
+  for (int shift = 0; shift < bits; shift += 8, ++passes) {
+    radix_hist_kernel<<<(unsigned)nb, kCT, 0, st>>>(ka, n, shift, nb, hist);
+    cudaError_t e = exclusive_scan_i64(hist, 256 * nb, offs, sws, st);
+    if (e != cudaSuccess) return e;
+    radix_scatter_kernel<<<(unsigned)nb, kCT, 0, st>>>(ka, va, n, shift, nb, offs, kb_, vb);
+    uint32_t* tk = ka; ka = kb_; kb_ = tk;
+    int32_t* tv = va; va = vb; vb = tv;
+  }
+  if (passes & 1) {   // result is in the workspace: copy back
+    cudaMemcpyAsync(keys, ka, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(perm, va, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t coo_make_keys(const int32_t* idx, const int64_t* off, int r, int kb, int64_t n,
+                          uint32_t* keys, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  make_keys_kernel<<<grid_for(n), kCT, 0, st>>>(idx, off, r, kb, n, keys);
+  return cudaGetLastError();
+}
+
+// Row pointers from the composite keys (sorted by (rep, index)): ptr = exclusive scan of the
+// per-(rep, index) counts, r*rows + 1 entries; rep rho's row x spans [ptr[rho*rows + x],
+// ptr[rho*rows + x + 1]).  cnt: r*rows + 1 int64 scratch.
+cudaError_t coo_row_pointers(const uint32_t* sorted_keys, int64_t n, int kb, int r, int64_t rows,
+                             int64_t* cnt, int64_t* ptr, int64_t* sws, cudaStream_t st) {
+  const int64_t m = (int64_t)r * rows + 1;
+  cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(int64_t) * m, st);
+  if (e != cudaSuccess) return e;
+  if (n > 0) key_count_kernel<<<grid_for(n), kCT, 0, st>>>(sorted_keys, n, kb, rows, cnt);
+  return exclusive_scan_i64(cnt, m, ptr, sws, st);
+}
+
+__global__ void coo_max_phi_kernel(const float* __restrict__ v, int64_t n, int moi,
+                                   unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)v[e];
+    m = fmax(m, moi == 0 ? fabs(d) : d * d);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+cudaError_t launch_coo_max_phi(const float* v, int64_t n, int moi, unsigned long long* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  coo_max_phi_kernel<<<grid_for(n), kCT, 0, st>>>(v, n, moi, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coo_mttkrp(const CooAls& a, int mode, cudaStream_t st) {
+  const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
+  const int64_t warps = (int64_t)a.r * rows;
+  const unsigned grid = (unsigned)ceil_div(warps * 32, kCT);
+  switch (a.RB) {
+    case 4: coo_mttkrp_kernel<4><<<grid, kCT, 0, st>>>(a, mode); break;
+    case 8: coo_mttkrp_kernel<8><<<grid, kCT, 0, st>>>(a, mode); break;
+    case 12: coo_mttkrp_kernel<12><<<grid, kCT, 0, st>>>(a, mode); break;
+    case 16: coo_mttkrp_kernel<16><<<grid, kCT, 0, st>>>(a, mode); break;
+    case 24: coo_mttkrp_kernel<24><<<grid, kCT, 0, st>>>(a, mode); break;
+    default: coo_mttkrp_kernel<32><<<grid, kCT, 0, st>>>(a, mode); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coo_sumsq(const float* v, const int64_t* off, int r, double* ysq, cudaStream_t st) {
+  coo_sumsq_kernel<<<r, kCT, 0, st>>>(v, off, r, ysq);
+  return cudaGetLastError();
+}
+
+size_t coo_fit_ws_doubles() { return 2 * (size_t)kNumSMs * 4 + 3 * kMaxR * kMaxR + 8; }
+
+cudaError_t launch_coo_fit(const CooView& X, const float* lam, const float* A, const float* B,
+                           const float* C, int R, double* ws, double* relerr, cudaStream_t st) {
+  const int nb = kNumSMs * 4;
+  double* G = ws + 2 * nb;
+  switch (R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32) {
+    case 4: coo_fit_kernel<4><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
+    case 8: coo_fit_kernel<8><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
+    case 12: coo_fit_kernel<12><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
+    case 16: coo_fit_kernel<16><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
+    case 24: coo_fit_kernel<24><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
+    default: coo_fit_kernel<32><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
+  }
+  cudaError_t e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, st);
+  if (e != cudaSuccess) return e;
+  coo_fit_combine_kernel<<<1, 32, 0, st>>>(ws, nb, G, lam, R, relerr);
+  return cudaGetLastError();
+}
+
+}  // namespace sbt

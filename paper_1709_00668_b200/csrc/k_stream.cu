@@ -406,6 +406,12 @@ StreamGeom fit_geom(const DenseView& X, int* gx, int* gy) {
 
 }  // namespace
 
+cudaError_t launch_gram3(const float* A, const float* B, const float* C, int64_t I, int64_t J,
+                         int64_t K, int R, double* G, cudaStream_t st) {
+  gram3_kernel<<<3, 512, 0, st>>>(A, B, C, I, J, K, R, G);
+  return cudaGetLastError();
+}
+
 bool stream_supported(const DenseView& X) {
   return X.pitch % 4 == 0 && ((uintptr_t)X.base & 15) == 0 && X.I >= 1 && X.I <= 8192 && X.J >= 1;
 }

@@ -1,0 +1,133 @@
+"""GPU parity of the sparse (COO) path against the oracle, through the C-ABI.
+
+Same bars as the dense path (BASELINE north_star): sampled indices bit-exact, FMS >= 0.99
+after alignment, |relative error difference| <= 1e-3; integer work (marginals) bit-exact."""
+import numpy as np
+import pytest
+
+from oracle import sambaten as O
+from synth import zipf_planted_coo, community_coo, split_coo
+from tests._helpers import dev, host, torch_cuda
+
+pytestmark = pytest.mark.gpu
+
+
+def L():
+    from paper_1709_00668_b200 import _lib
+    return _lib
+
+
+def _oc(X):
+    return O.Coo(X.i.astype(np.int64), X.j.astype(np.int64), X.k.astype(np.int64), X.v, X.dims)
+
+
+def _gc(X, on_device=True):
+    f = dev if on_device else np.ascontiguousarray
+    return L().coo(f(X.i.astype(np.int32)), f(X.j.astype(np.int32)), f(X.k.astype(np.int32)), f(X.v), X.dims)
+
+
+def _samples(h, r):
+    n = L().sambaten_last_samples(h)
+    Is = np.empty(r * n[0], np.int32); Js = np.empty(r * n[1], np.int32); Ks = np.empty(r * n[2], np.int32)
+    L().sambaten_last_samples(h, Is, Js, Ks)
+    return Is.reshape(r, -1), Js.reshape(r, -1), Ks.reshape(r, -1)
+
+
+def _run(X, truth, K0, batch, R, s, r, maxit, tol=0.0, seed=7, nb=None, tau=0.9):
+    X0, batches = split_coo(X, K0, batch)
+    if nb is not None:
+        batches = batches[:nb]
+    lam, A, B, C = truth
+    model = [np.ascontiguousarray(np.asarray(x, np.float32)) for x in (lam, A, B, C[:K0])]
+    cfg = O.Config(R=R, s=(s, s, s), r=r, seed=seed, maxit=maxit, tol=tol, tau=tau)
+    st = O.init_factors(_oc(X0), cfg, *model, X.nnz)
+    opts = L().default_opts(als_max_iters=maxit, als_tol=tol, accept_tau=tau, capacity=X.nnz,
+                            capacity_k=X.dims[2], full_fit=1)
+    h = L().sambaten_init_factors(_gc(X0), R, s, r, seed, model[1], model[2], model[3], model[0], opts)
+    out = []
+    try:
+        Kt = K0
+        for b in batches:
+            Kt += b.dims[2]
+            gA = np.empty((X.dims[0], R), np.float32); gB = np.empty((X.dims[1], R), np.float32)
+            gC = np.empty((Kt, R), np.float32); gl = np.empty(R, np.float32)
+            info = L().sambaten_update(h, _gc(b), gA, gB, gC, gl)
+            oinfo = O.update(st, _oc(b))
+            Is, Js, Ks = _samples(h, r)
+            for rho, rp in enumerate(oinfo["reps"]):
+                assert np.array_equal(Is[rho], rp["Is"]), rho
+                assert np.array_equal(Js[rho], rp["Js"]), rho
+                assert np.array_equal(Ks[rho], rp["Ks"]), rho
+            g64 = tuple(np.asarray(x, np.float64) for x in (gl, gA, gB, gC))
+            fms = O.fms(g64, (st.lam, st.A, st.B, st.C))
+            rel_o = O.relative_error(st.X, st.lam, st.A, st.B, st.C)
+            rel_g = O.relative_error(st.X, *g64)
+            gpu_rej = [i for i in range(r) if info.reps_rejected_mask >> i & 1]
+            out.append((fms, rel_g, rel_o, gpu_rej, oinfo["rejected"], info))
+            # continue both sides from the GPU model
+            st.lam, st.A, st.B, st.C = g64
+    finally:
+        L().sambaten_destroy(h)
+    return out
+
+
+def test_coo_update_parity_planted():
+    X, truth = zipf_planted_coo(400, 300, 60, 4, 30_000, alpha=1.2, seed=3)
+    res = _run(X, truth, 50, 5, R=4, s=2, r=4, maxit=30, nb=2)
+    for fms, rel_g, rel_o, gr, orr, info in res:
+        assert gr == orr
+        assert fms >= 0.99, fms
+        assert abs(rel_g - rel_o) <= 1e-3, (rel_g, rel_o)
+        assert abs((1 - info.fit_full) - rel_g) <= 1e-5
+
+
+def test_coo_update_parity_communities_ragged():
+    """C3-like community counts (Zipf 1.5), ragged sample sizes, paper-literal tau = 0."""
+    X = community_coo(1000, 90, 5, 40_000, alpha=1.5, seed=4)
+    rng = np.random.default_rng(0)
+    truth = (np.ones(5), rng.random((1000, 5)), rng.random((1000, 5)), rng.random((90, 5)))
+    res = _run(X, truth, 77, 13, R=5, s=3, r=3, maxit=10, nb=1, tau=0.0)
+    for fms, rel_g, rel_o, gr, orr, info in res:
+        assert gr == orr == []
+        assert fms >= 0.99, fms
+        assert abs(rel_g - rel_o) <= 1e-3, (rel_g, rel_o)
+
+
+def test_coo_errors_leave_state_unchanged():
+    X, truth = zipf_planted_coo(200, 100, 30, 3, 5_000, seed=5)
+    X0, batches = split_coo(X, 25, 5)
+    lam, A, B, C = (np.ascontiguousarray(np.asarray(x, np.float32)) for x in truth)
+    opts = L().default_opts(als_max_iters=5, capacity=X.nnz, capacity_k=30)
+    h = L().sambaten_init_factors(_gc(X0), 3, 2, 2, 0, A, B, C[:25].copy(), lam, opts)
+    try:
+        b = batches[0]
+        bad = type(b)(b.i[::-1].copy(), b.j[::-1].copy(), b.k[::-1].copy(), b.v[::-1].copy(), b.dims)
+        with pytest.raises(L().SambatenError) as e:
+            L().sambaten_update(h, _gc(bad))
+        assert e.value.name == "E_INVALID"
+        oob = type(b)(b.i.copy(), b.j.copy(), b.k.copy(), b.v.copy(), b.dims)
+        oob.k[-1] = 99
+        with pytest.raises(L().SambatenError) as e:
+            L().sambaten_update(h, _gc(oob))
+        assert e.value.name == "E_INDEX_RANGE"
+        assert L().sambaten_get_factors(h)["dims"][2] == 25
+        info = L().sambaten_update(h, _gc(b, on_device=False))   # host arrays work too
+        assert info.k_total == 30
+    finally:
+        L().sambaten_destroy(h)
+
+
+def test_coo_init_als_quality():
+    """sambaten_init on a COO tensor: full CP-ALS reaches the oracle's fit."""
+    X, truth = zipf_planted_coo(300, 200, 40, 3, 20_000, seed=6)
+    X0, _ = split_coo(X, 40, 10)
+    opts = L().default_opts(capacity=X.nnz, capacity_k=60, init_max_iters=100, init_tol=1e-9)
+    h = L().sambaten_init(_gc(X0), 3, 2, 2, 0, opts)
+    try:
+        rel = L().sambaten_relative_error(h)
+        cfg = O.Config(R=3, s=(2, 2, 2), r=2, seed=0)
+        st = O.init_als(_oc(X0), cfg, X.nnz, maxit=100, tol=1e-9)
+        rel_o = O.relative_error(st.X, st.lam, st.A, st.B, st.C)
+        assert abs(rel - rel_o) <= 1e-3, (rel, rel_o)
+    finally:
+        L().sambaten_destroy(h)
