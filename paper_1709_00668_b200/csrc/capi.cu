@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -1033,6 +1034,19 @@ extern "C" sambaten_status sambaten_sample(const int64_t* w, int64_t n, int64_t 
   return SAMBATEN_OK;
 }
 
+__global__ static void loc_from_list_kernel(const int32_t* list, int64_t n, int64_t nall, int32_t* loc,
+                                            unsigned* bad) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = list[t];
+    if (x < 0 || x >= nall) { atomicOr(bad, 1u); continue; }
+    loc[x] = (int32_t)t;
+  }
+}
+
+__global__ static void store_i64_kernel(const int64_t* src, int64_t* dst) {
+  if (threadIdx.x == 0) *dst = *src;
+}
+
 extern "C" sambaten_status sambaten_gather(const sambaten_tensor* X, const int32_t* Is, int64_t nI,
                                            const int32_t* Js, int64_t nJ, const int32_t* Ks,
                                            int64_t nK, float* out_dense, int32_t* oi, int32_t* oj,
@@ -1041,11 +1055,109 @@ extern "C" sambaten_status sambaten_gather(const sambaten_tensor* X, const int32
   if (sambaten_status e = check_dense(X, "gather")) return e;
   if (nI < 0 || nJ < 0 || nK < 0) FAIL(SAMBATEN_E_INVALID, "gather: negative size");
   cudaStream_t st = stream_of(stream);
-  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "gather: COO gather not available in this build");
-  if (!out_dense) FAIL(SAMBATEN_E_INVALID, "gather: NULL output");
-  CK(launch_gather_dense(user_view(X), Is, Js, Ks, (int)nI, (int)nJ, (int)nK, 1, nI, nJ, nK,
-                         out_dense, nK * nJ * nI, st));
-  (void)oi; (void)oj; (void)ok; (void)ov; (void)out_cap; (void)out_nnz;
+  if (X->fmt == SAMBATEN_DENSE) {
+    if (!out_dense) FAIL(SAMBATEN_E_INVALID, "gather: NULL output");
+    CK(launch_gather_dense(user_view(X), Is, Js, Ks, (int)nI, (int)nJ, (int)nK, 1, nI, nJ, nK,
+                           out_dense, nK * nJ * nI, st));
+    return SAMBATEN_OK;
+  }
+  // COO: membership bitmaps of the three index lists (r = 1), count, scan, write
+  if (!oi || !oj || !ok || !ov || !out_nnz) FAIL(SAMBATEN_E_INVALID, "gather: NULL COO output");
+  const int64_t I = X->dims[0], J = X->dims[1], K = X->dims[2], n = X->nnz;
+  const CooView V{X->idx[0], X->idx[1], X->idx[2], X->vals, n, I, J, K};
+  const int64_t nb = coo_gather_blocks(n);
+  DevBuf ws;
+  Bump sz;
+  auto lay = [&](Bump& b) {
+    int32_t* lI = b.take<int32_t>(I); int32_t* lJ = b.take<int32_t>(J); int32_t* lK = b.take<int32_t>(K);
+    uint32_t* mI = b.take<uint32_t>(I); uint32_t* mJ = b.take<uint32_t>(J); uint32_t* mK = b.take<uint32_t>(K);
+    int64_t* cnt = b.take<int64_t>(nb + 1); int64_t* off = b.take<int64_t>(nb + 1);
+    int64_t* sws = b.take<int64_t>(scan_ws_elems(nb + 1));
+    unsigned* bad = b.take<unsigned>(1);
+    return std::make_tuple(lI, lJ, lK, mI, mJ, mK, cnt, off, sws, bad);
+  };
+  lay(sz);
+  CK(ws.ensure(sz.off));
+  Bump b{ws.as<char>(), 0};
+  auto [lI, lJ, lK, mI, mJ, mK, cnt, off, sws, bad] = lay(b);
+  CK(cudaMemsetAsync(lI, 0xff, sizeof(int32_t) * I, st));
+  CK(cudaMemsetAsync(lJ, 0xff, sizeof(int32_t) * J, st));
+  CK(cudaMemsetAsync(lK, 0xff, sizeof(int32_t) * K, st));
+  CK(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
+  CK(cudaMemsetAsync(cnt + nb, 0, sizeof(int64_t), st));
+  if (nI) loc_from_list_kernel<<<64, 256, 0, st>>>(Is, nI, I, lI, bad);
+  if (nJ) loc_from_list_kernel<<<64, 256, 0, st>>>(Js, nJ, J, lJ, bad);
+  if (nK) loc_from_list_kernel<<<64, 256, 0, st>>>(Ks, nK, K, lK, bad);
+  CK(launch_build_mask(lI, I, 1, mI, I, st));
+  CK(launch_build_mask(lJ, J, 1, mJ, J, st));
+  CK(launch_build_mask(lK, K, 1, mK, K, st));
+  CK(launch_coo_gather_count(V, mI, mJ, mK, 1, cnt, st));
+  CK(exclusive_scan_i64(cnt, nb + 1, off, sws, st));
+  int64_t tot = 0;
+  unsigned hbad = 0;
+  CK(cudaMemcpyAsync(&tot, off + nb, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&hbad, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  store_i64_kernel<<<1, 32, 0, st>>>(off + nb, out_nnz);
+  if (hbad) FAIL(SAMBATEN_E_INDEX_RANGE, "gather: sampled index outside its mode");
+  if (tot > out_cap) {
+    CK(cudaStreamSynchronize(st));
+    FAIL(SAMBATEN_E_INVALID, "gather: out_cap smaller than the summary's nnz (*out_nnz has the size)");
+  }
+  CK(launch_coo_gather_write(V, mI, mJ, mK, lI, lJ, lK, K, (int)nK, 1, off, oi, oj, ok, ov, st));
+  CK(cudaStreamSynchronize(st));   // ws is released on return
+  return SAMBATEN_OK;
+}
+
+__global__ static void f64_to_f32_kernel(const double* in, int64_t n, float* out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = (float)in[t];
+}
+
+// MTTKRP of one COO tensor (r = 1): stable sort by the mode's index (modes 0, 1), row pointers,
+// warp-per-row sums; fp64 result rounded to fp32.
+static sambaten_status coo_mttkrp_single(const sambaten_tensor* X, const float* U0, const float* U1,
+                                         const float* U2, int R, int mode, float* M, cudaStream_t st) {
+  const int64_t I = X->dims[0], J = X->dims[1], K = X->dims[2], n = X->nnz;
+  const int64_t rows = mode == 0 ? I : mode == 1 ? J : K;
+  const int kb = bits_for(rows);
+  const int64_t nn = std::max<int64_t>(n, 1);
+  DevBuf ws;
+  Bump sz;
+  auto lay = [&](Bump& b) {
+    uint32_t* keys = b.take<uint32_t>(nn); int32_t* perm = b.take<int32_t>(nn);
+    uint32_t* wk = b.take<uint32_t>(nn); int32_t* wv = b.take<int32_t>(nn);
+    int64_t* hist = b.take<int64_t>(radix_ws_elems(nn)); int64_t* offs = b.take<int64_t>(radix_ws_elems(nn));
+    int64_t* sws = b.take<int64_t>(std::max(scan_ws_elems(radix_ws_elems(nn)), scan_ws_elems(rows + 1)));
+    int64_t* cnt = b.take<int64_t>(rows + 1); int64_t* ptr = b.take<int64_t>(rows + 1);
+    int64_t* off = b.take<int64_t>(2); double* Md = b.take<double>(rows * R); int* done = b.take<int>(1);
+    return std::make_tuple(keys, perm, wk, wv, hist, offs, sws, cnt, ptr, off, Md, done);
+  };
+  lay(sz);
+  CK(ws.ensure(sz.off));
+  Bump b{ws.as<char>(), 0};
+  auto [keys, perm, wk, wv, hist, offs, sws, cnt, ptr, off, Md, done] = lay(b);
+  two_offsets_kernel<<<1, 32, 0, st>>>(off, n);
+  CK(cudaMemsetAsync(done, 0, sizeof(int), st));
+  const int32_t* idx = X->idx[mode];
+  if (mode < 2) CK(coo_sort_by_index(idx, off, 1, kb, n, keys, perm, wk, wv, hist, offs, sws, st));
+  else CK(coo_make_keys(idx, off, 1, kb, n, keys, st));
+  CK(coo_row_pointers(keys, n, kb, 1, rows, cnt, ptr, sws, st));
+  CooAls a{};
+  a.nI = (int)I; a.nJ = (int)J; a.nK = (int)K; a.R = R; a.r = 1;
+  a.RB = R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
+  a.p = X->idx[0]; a.q = X->idx[1]; a.u = X->idx[2]; a.v = X->vals;
+  a.perm[0] = a.perm[1] = a.perm[2] = nullptr;
+  a.perm[mode] = mode < 2 ? perm : nullptr;
+  a.ptr[mode] = ptr;
+  a.U[0] = const_cast<float*>(U0); a.U[1] = const_cast<float*>(U1); a.U[2] = const_cast<float*>(U2);
+  a.u_stride[0] = a.u_stride[1] = a.u_stride[2] = 0;
+  a.M[mode] = Md; a.m_stride[mode] = rows * R;
+  a.done = done;
+  CK(launch_coo_mttkrp(a, mode, st));
+  f64_to_f32_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * R, 256), 4096), 256, 0, st>>>(Md, rows * R, M);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));   // ws is released on return
   return SAMBATEN_OK;
 }
 
@@ -1065,6 +1177,10 @@ extern "C" sambaten_status sambaten_mttkrp(const sambaten_tensor* X, const float
                                            const float* U2, int R, int mode, float* M, void* stream) {
   if (mode < 0 || mode > 2) FAIL(SAMBATEN_E_INVALID, "mttkrp: mode must be 0, 1 or 2");
   if (!M) FAIL(SAMBATEN_E_INVALID, "mttkrp: NULL output");
+  if (X && X->fmt == SAMBATEN_COO) {
+    if (R < 1 || R > kMaxR) FAIL(SAMBATEN_E_INVALID, "R must be in [1, 32]");
+    return coo_mttkrp_single(X, U0, U1, U2, R, mode, M, stream_of(stream));
+  }
   DenseAls a;
   if (sambaten_status e = single_als_setup(X, R, (float*)U0, (float*)U1, (float*)U2, &a)) return e;
   cudaStream_t st = stream_of(stream);
@@ -1089,6 +1205,23 @@ extern "C" sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, floa
                                            float* U2, double* lambda_out, int max_iters, double tol,
                                            double* fit_out, int32_t* iters_out, void* stream) {
   if (max_iters < 1) FAIL(SAMBATEN_E_INVALID, "cp_als: max_iters >= 1");
+  if (X && X->fmt == SAMBATEN_COO) {
+    if (R < 1 || R > kMaxR) FAIL(SAMBATEN_E_INVALID, "R must be in [1, 32]");
+    cudaStream_t st = stream_of(stream);
+    DevBuf ws, offb;
+    CK(offb.ensure(2 * sizeof(int64_t)));
+    two_offsets_kernel<<<1, 32, 0, st>>>(offb.as<int64_t>(), X->nnz);
+    DenseAls d{};
+    int nl = 0;
+    if (sambaten_status e = coo_als(ws, st, R, X->idx[0], X->idx[1], X->idx[2], X->vals, offb.as<int64_t>(),
+                                    X->nnz, (int)X->dims[0], (int)X->dims[1], (int)X->dims[2], 1, U0, U1,
+                                    U2, 0, 0, max_iters, tol, false, &d, &nl))
+      return e;
+    copy_als_out_kernel<<<1, 32, 0, st>>>(d.lam, d.fit, d.iters, R, lambda_out, fit_out, iters_out);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return SAMBATEN_OK;
+  }
   DenseAls a;
   if (sambaten_status e = single_als_setup(X, R, U0, U1, U2, &a)) return e;
   a.maxit = max_iters; a.tol = tol;
@@ -1108,9 +1241,16 @@ extern "C" sambaten_status sambaten_fit(const sambaten_tensor* X, const float* l
                                         const float* B, const float* C, int R, double* relerr,
                                         void* stream) {
   if (sambaten_status e = check_dense(X, "fit")) return e;
-  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "fit: COO fit not available in this build");
   if (R < 1 || R > kMaxR || !relerr) FAIL(SAMBATEN_E_INVALID, "fit: bad argument");
   cudaStream_t st = stream_of(stream);
+  if (X->fmt == SAMBATEN_COO) {
+    const CooView V{X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, X->dims[0], X->dims[1], X->dims[2]};
+    void* ws = nullptr;
+    CK(cudaMallocAsync(&ws, sizeof(double) * coo_fit_ws_doubles(), st));
+    CK(launch_coo_fit(V, lambda, A, B, C, R, static_cast<double*>(ws), relerr, st));
+    CK(cudaFreeAsync(ws, st));
+    return SAMBATEN_OK;
+  }
   const DenseView V = user_view(X);
   void* ws = nullptr;
   CK(cudaMallocAsync(&ws, sizeof(double) * fit_ws_doubles_any(V), st));

@@ -131,3 +131,72 @@ def test_coo_init_als_quality():
         assert abs(rel - rel_o) <= 1e-3, (rel, rel_o)
     finally:
         L().sambaten_destroy(h)
+
+
+# ------------------------------------------------------------------- stateless primitives
+def _rand_coo(dims, nnz, seed):
+    rng = np.random.default_rng(seed)
+    I, J, K = dims
+    lin = np.unique(rng.integers(0, I * J * K, nnz))
+    i = lin % I; j = (lin // I) % J; k = lin // (I * J)
+    v = rng.standard_normal(len(lin)).astype(np.float32)
+    return O.coo_canonical(i, j, k, v, dims)
+
+
+@pytest.mark.parametrize("dims,ns", [((50, 40, 30), (25, 13, 7)), ((300, 200, 64), (30, 200, 64)),
+                                     ((7, 5, 3), (7, 5, 3))])
+def test_gather_coo_bit_exact(dims, ns):
+    torch = torch_cuda()
+    X = _rand_coo(dims, 4000, 11)
+    rng = np.random.default_rng(3)
+    idx = [np.sort(rng.choice(d, n, replace=False)).astype(np.int32) for d, n in zip(dims, ns)]
+    cap = X.nnz
+    oi, oj, ok = (torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(3))
+    ov = torch.empty(cap, dtype=torch.float32, device="cuda")
+    onnz = torch.zeros(1, dtype=torch.int64, device="cuda")
+    L().sambaten_gather(_gc(X), dev(idx[0]), ns[0], dev(idx[1]), ns[1], dev(idx[2]), ns[2], oi=oi, oj=oj,
+                        ok=ok, ov=ov, cap=cap, out_nnz=onnz)
+    ref = O.gather_coo(X, idx[0], idx[1], idx[2])
+    n = int(host(onnz)[0])
+    assert n == ref.nnz
+    for g, r in zip((oi, oj, ok), (ref.i, ref.j, ref.k)):
+        assert np.array_equal(host(g)[:n], np.asarray(r, np.int32))
+    assert np.array_equal(host(ov)[:n].view(np.uint32), ref.v.astype(np.float32).view(np.uint32))
+
+
+@pytest.mark.parametrize("dims,nnz,R", [((60, 50, 40), 3000, 4), ((500, 400, 90), 40_000, 10),
+                                        ((9, 8, 7), 50, 1), ((200, 100, 64), 10_000, 15)])
+def test_mttkrp_coo(dims, nnz, R):
+    torch = torch_cuda()
+    X = _rand_coo(dims, nnz, R)
+    rng = np.random.default_rng(R + 1)
+    U = [rng.random((n, R)).astype(np.float32) for n in dims]
+    Ud = [dev(u) for u in U]
+    for mode in range(3):
+        M = torch.empty((dims[mode], R), dtype=torch.float32, device="cuda")
+        L().sambaten_mttkrp(_gc(X), Ud[0], Ud[1], Ud[2], R, mode, M)
+        ref = O.mttkrp(X, [u.astype(np.float64) for u in U], mode)
+        err = np.linalg.norm(host(M).astype(np.float64) - ref) / max(np.linalg.norm(ref), 1e-300)
+        assert err <= 1e-5, (mode, err)
+
+
+def test_fit_coo_and_cp_als_coo():
+    torch = torch_cuda()
+    X, truth = zipf_planted_coo(120, 100, 40, 3, 6000, seed=9)
+    Xo = _oc(X)
+    lam, A, B, C = (np.asarray(x, np.float32) for x in truth)
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    L().sambaten_fit(_gc(X), dev(lam), dev(A), dev(B), dev(C), 3, out)
+    ref = O.relative_error(Xo, *(x.astype(np.float64) for x in (lam, A, B, C)))
+    assert abs(float(host(out)[0]) - ref) <= 1e-6
+    U0 = O.als_init(X.dims, 3, 5, 1, 0)
+    Ud = [dev(u.astype(np.float32)) for u in U0]
+    lamd = torch.empty(3, dtype=torch.float64, device="cuda")
+    fit = torch.empty(1, dtype=torch.float64, device="cuda")
+    it = torch.empty(1, dtype=torch.int32, device="cuda")
+    L().sambaten_cp_als(_gc(X), 3, Ud[0], Ud[1], Ud[2], lamd, 40, 0.0, fit, it)
+    lo, Uo, fo, io, _ = O.cp_als(Xo, U0, 40, 0.0)
+    assert int(host(it)[0]) == io == 40
+    assert abs(float(host(fit)[0]) - fo) <= 1e-3
+    g = (host(lamd), *[host(u).astype(np.float64) for u in Ud])
+    assert O.fms(g, (lo, *Uo)) >= 0.99

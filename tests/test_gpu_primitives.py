@@ -167,10 +167,11 @@ def test_cp_als_tracks_oracle(shape, R, its):
 
 
 # ---------------------------------------------------------------------------------- fit
-def test_fit_dense():
+@pytest.mark.parametrize("K,J,I,R", [(40, 30, 50, 4), (40, 30, 64, 10), (6, 7, 3000, 3), (30, 20, 500, 16)])
+def test_fit_dense(K, J, I, R):
+    """Tiled (I % 4 != 0) and streamed (I % 4 == 0, column-chunked for I > 2048) fits."""
     torch = torch_cuda()
     rng = np.random.default_rng(4)
-    K, J, I, R = 40, 30, 50, 4
     F = [rng.random((n, R)).astype(np.float32) for n in (I, J, K)]
     lam = (rng.random(R) + 0.5).astype(np.float32)
     T = (np.einsum("f,if,jf,kf->kji", lam, *F) + 0.1 * rng.standard_normal((K, J, I))).astype(np.float32)
