@@ -3,21 +3,21 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
 
 A step is one whole update (a0..a7: ingest, marginals, sampling, gather, batched CP-ALS,
-matching, merge, full fit) of one batch of the BASELINE.json workload (default configs[1] =
-C2: 500^3 dense, R=10, K0=450, batches of 10 slices, s=5, r=8, 30 ALS iterations), with
-synthetic planted data.  The metric is BASELINE.json's: new tensor entries ingested per
+matching, merge, full fit) of one batch of a BASELINE.json workload with synthetic planted
+data.  Default: configs[1] = C2 (500^3 dense, R=10, K0=450, batches of 10 slices, s=5, r=8,
+30 ALS iterations).  --config C1/C3/C5 select the other single-GPU workloads (C3/C5: COO).
+The metric is BASELINE.json's: new tensor entries (dense) / nonzeros (COO) ingested per
 second per update.  Rank 0 prints one JSON line.
 
 Timing: W untimed warm-up steps, then K steps, each bracketed by a barrier and a device
 synchronisation and timed with CUDA events on the library's stream; L2 is flushed (a 512 MB
 write) before every step; the stream cycles through the config's batches, restoring the
 K0 checkpoint (untimed) after the last one.  Multi-GPU (torchrun): every rank runs its own
-replica of the update (weak scaling, no data-path collective yet) and the
+replica of the update (weak scaling, no data-path collective: DESIGN.md "Multi-GPU") and the
 time is the max over ranks.
 """
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -34,12 +34,13 @@ import numpy as np  # noqa: E402
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
-    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C2")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-full-fit", action="store_true", help="return the summary fit only (R21)")
     return p.parse_args()
 
 
@@ -52,7 +53,7 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled every 20 ms during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -66,10 +67,11 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.05)
         except OSError:
             self.proc = None
 
@@ -103,28 +105,59 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_workload(w):
-    from synth import planted_dense, split_dense
-    T, truth = planted_dense(w.I, w.J, w.K, w.R, noise=w.noise, seed=w.seed)
-    T0, batches = split_dense(T, w.K0, w.batch)
-    model = [np.asarray(x, np.float32) for x in (truth[0], truth[1], truth[2], truth[3][:w.K0])]
-    return T0, batches, model
+# ----------------------------------------------------------------------------- workloads
+class Work:
+    """Synthetic stand-in of a BASELINE config."""
+
+    def __init__(self, w):
+        self.w = w
+        self.coo = w.fmt == "coo"
+        if not self.coo:
+            from synth import planted_dense, split_dense
+            T, truth = planted_dense(w.I, w.J, w.K, w.R, noise=w.noise, seed=w.seed)
+            self.X0, self.batches = split_dense(T, w.K0, w.batch)
+            self.model = [np.asarray(x, np.float32) for x in (truth[0], truth[1], truth[2], truth[3][:w.K0])]
+            self.entries = [b.size for b in self.batches]
+            self.cap = w.I * w.J * w.K
+        else:
+            from synth import community_coo, zipf_planted_coo, split_coo
+            if w.name == "C3":
+                X = community_coo(w.I, w.K, w.R, w.nnz, alpha=w.alpha, seed=w.seed)
+                self.model = None           # no planted factors: sambaten_init (full ALS, untimed)
+            else:
+                X, truth = zipf_planted_coo(w.I, w.J, w.K, w.R, w.nnz, alpha=w.alpha, seed=w.seed)
+                self.model = [np.asarray(x, np.float32) for x in (truth[0], truth[1], truth[2], truth[3][:w.K0])]
+            self.X0, self.batches = split_coo(X, w.K0, w.batch)
+            self.entries = [b.nnz for b in self.batches]
+            self.cap = X.nnz
+        self.nb = len(self.batches)
+
+    def tensor(self, L, x, device, pin=False):
+        import torch
+        if not self.coo:
+            t = torch.from_numpy(np.ascontiguousarray(x))
+            return L.dense(t.cuda() if device else (t.pin_memory() if pin else t))
+        arrs = [torch.from_numpy(np.ascontiguousarray(a)) for a in (x.i, x.j, x.k, x.v)]
+        arrs = [a.cuda() if device else (a.pin_memory() if pin else a) for a in arrs]
+        return L.coo(*arrs, x.dims)
+
+    def bytes_in(self, i):
+        b = self.batches[i]
+        return int(b.size * 4) if not self.coo else int(b.nnz * 16)
+
+    def oracle_tensor(self, x):
+        from oracle import sambaten as O
+        if not self.coo:
+            return x
+        return O.Coo(x.i.astype(np.int64), x.j.astype(np.int64), x.k.astype(np.int64), x.v, x.dims)
 
 
-def cpu_baseline_run(w, T0, batches, model, max_batches=None):
-    """The oracle as it stands (oracle/), on this host's cores: the config's updates from the
-    K0 state (bounded sample: the first `max_batches` batches)."""
-    from oracle import sambaten as O
-    cfg = O.Config(R=w.R, s=(w.s,) * 3, r=w.r, seed=w.seed, maxit=w.maxit, tol=w.tol)
-    st = O.init_factors(T0, cfg, *model, w.I * w.J * w.K)
-    nb = len(batches) if max_batches is None else min(max_batches, len(batches))
-    t0 = time.perf_counter()
-    entries = 0
-    for b in batches[:nb]:
-        O.update(st, b)
-        entries += b.size
-    dt = time.perf_counter() - t0
-    return entries / dt, dt, nb
+def describe(w):
+    if w.fmt == "dense":
+        shape = f"dense {w.I}x{w.J}x{w.K}, K0={w.K0}, batch={w.batch} slices"
+    else:
+        shape = f"COO {w.I}x{w.J}x{w.K} ~{w.nnz} nnz (Zipf {w.alpha}), K0={w.K0}, batch={w.batch} slices"
+    return f"{w.name}: {shape}, R={w.R}, s={w.s}, r={w.r}, ALS {w.maxit} it tol {w.tol}"
 
 
 def threads_used():
@@ -136,6 +169,31 @@ def threads_used():
         return os.cpu_count()
 
 
+def oracle_state(work, model=None):
+    from oracle import sambaten as O
+    w = work.w
+    cfg = O.Config(R=w.R, s=(w.s,) * 3, r=w.r, seed=w.seed, maxit=w.maxit, tol=w.tol,
+                   tau=0.9 if not work.coo else 0.0)
+    m = model if model is not None else work.model
+    return O.init_factors(work.oracle_tensor(work.X0), cfg, *m, work.cap), O
+
+
+def cpu_baseline_run(work, model, budget_s=20.0):
+    """The oracle as it stands (oracle/), on this host's cores: consecutive updates of the
+    config's batches from the K0 state until ~budget_s seconds (bounded sample)."""
+    st, O = oracle_state(work, model)
+    t0 = time.perf_counter()
+    entries, nb = 0, 0
+    for i, b in enumerate(work.batches):
+        O.update(st, work.oracle_tensor(b))
+        entries += work.entries[i]
+        nb += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return entries / dt, dt, nb
+
+
 def main():
     args = parse()
     from synth import CONFIGS
@@ -143,36 +201,41 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    metric = "new tensor entries ingested/sec per update"
-    unit = "entries/s"
-    config = {"workload": f"{w.name}: dense {w.I}x{w.J}x{w.K}, K0={w.K0}, batch={w.batch} slices, "
-                          f"R={w.R}, s={w.s}, r={w.r}, ALS {w.maxit} it tol {w.tol}",
-              "l2": "flushed (512 MB write) before every step", "init": "planted truth factors"}
+    metric = "new tensor entries ingested/sec per update" if w.fmt == "dense" else \
+        "new tensor nonzeros ingested/sec per update"
+    unit = "entries/s" if w.fmt == "dense" else "nnz/s"
+    config = {"workload": describe(w), "l2": "flushed (512 MB write) before every step",
+              "init": "planted truth factors" if w.name != "C3" else "full CP-ALS of X0 (sambaten_init)",
+              "full_fit": not args.no_full_fit}
+    work = Work(w)
 
     if args.impl == "reference":
         if rank != 0:
             return
-        T0, batches, model = make_workload(w)
-        times = []
-        per = w.I * w.J * w.batch
-        for i in range(args.warmup + args.steps):
+        if work.model is None:
             from oracle import sambaten as O
-            cfg = O.Config(R=w.R, s=(w.s,) * 3, r=w.r, seed=w.seed, maxit=w.maxit, tol=w.tol)
-            st = O.init_factors(T0, cfg, *model, w.I * w.J * w.K)
+            cfg = O.Config(R=w.R, s=(w.s,) * 3, r=w.r, seed=w.seed)
+            st0 = O.init_als(work.oracle_tensor(work.X0), cfg, work.cap, maxit=50, tol=1e-6)
+            work.model = [np.asarray(x, np.float32) for x in (st0.lam, st0.A, st0.B, st0.C)]
+        times, ents = [], []
+        for i in range(args.warmup + args.steps):
+            st, O = oracle_state(work)
+            bi = i % work.nb
             t0 = time.perf_counter()
-            O.update(st, batches[0])
+            O.update(st, work.oracle_tensor(work.batches[bi]))
             dt = time.perf_counter() - t0
             if i >= args.warmup:
                 times.append(dt)
+                ents.append(work.entries[bi])
         tot = sum(times)
-        val = per * len(times) / tot
+        val = sum(ents) / tot
         cores = threads_used()
         line = {"impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / len(times),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic planted (numpy, seed 0)", "config": config,
+                "data": "synthetic (seeded numpy generators)", "config": config,
                 "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "oracle",
-                                 "sample": f"each step = one full oracle update of batch 0 from the K0 state"},
+                                 "sample": "each step = one full oracle update of one batch from the K0 state"},
                 "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -184,22 +247,39 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1709_00668_b200 import _lib as L
 
-    T0, batches, model = make_workload(w)
     stream = torch.cuda.Stream()
-    opts = L.default_opts(als_max_iters=w.maxit, als_tol=w.tol, capacity=w.K, full_fit=1,
-                          stream=stream.cuda_stream)
-    h = L.sambaten_init_factors(L.dense(torch.from_numpy(T0).cuda()), w.R, w.s, w.r, w.seed,
-                                model[1], model[2], model[3], model[0], opts)
+    # C3's community tensor has no planted model; with R = 15 and 30 summary iterations the
+    # acceptance test (R26, tau = 0.9) can reject every repetition, so the COO workloads run
+    # the paper-literal merge (tau = 0)
+    tau = 0.9 if not work.coo else 0.0
+    config["accept_tau"] = tau
+    opts = L.default_opts(als_max_iters=w.maxit, als_tol=w.tol, capacity=work.cap, full_fit=int(not args.no_full_fit),
+                          accept_tau=tau, stream=stream.cuda_stream)
+    if work.coo:
+        opts.capacity_k = w.K
+    else:
+        opts.capacity = w.K
+    X0 = work.tensor(L, work.X0, device=True)
+    if work.model is None:
+        opts.init_max_iters = 50
+        h = L.sambaten_init(X0, w.R, w.s, w.r, w.seed, opts)
+        m = [np.empty(w.R, np.float32), np.empty((w.I, w.R), np.float32), np.empty((w.J, w.R), np.float32),
+             np.empty((w.K0, w.R), np.float32)]
+        L.sambaten_copy_factors(h, m[1], m[2], m[3], m[0])
+        work.model = m                  # the oracle baseline starts from the same model
+    else:
+        h = L.sambaten_init_factors(X0, w.R, w.s, w.r, w.seed, work.model[1], work.model[2],
+                                    work.model[3], work.model[0], opts)
     L.sambaten_checkpoint(h)
-    dbatches = [torch.from_numpy(b).cuda() for b in batches]
-    hbatches = [torch.from_numpy(b).pin_memory() for b in batches]
+    dbatches = [work.tensor(L, b, device=True) for b in work.batches]
+    hbatches = [work.tensor(L, b, device=False, pin=True) for b in work.batches]
     out_A = torch.empty((w.I, w.R), dtype=torch.float32).pin_memory()
     out_B = torch.empty((w.J, w.R), dtype=torch.float32).pin_memory()
     out_C = torch.empty((w.K, w.R), dtype=torch.float32).pin_memory()
     out_l = torch.empty((w.R,), dtype=torch.float32).pin_memory()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    nb = len(batches)
+    nb = work.nb
     state = {"i": 0}
 
     def step(host=False):
@@ -214,52 +294,61 @@ def main():
         with torch.cuda.stream(stream):
             ev0.record(stream)
             if host:
-                info = L.sambaten_update(h, L.dense(hbatches[i % nb]), out_A, out_B, out_C, out_l)
+                info = L.sambaten_update(h, hbatches[i % nb], out_A, out_B, out_C, out_l)
             else:
-                info = L.sambaten_update(h, L.dense(dbatches[i % nb]))
+                info = L.sambaten_update(h, dbatches[i % nb])
             ev1.record(stream)
         torch.cuda.synchronize()
-        return ev0.elapsed_time(ev1), info
+        return ev0.elapsed_time(ev1), info, work.entries[i % nb], i % nb
 
     for _ in range(args.warmup):
         step()
     clk = ClockSampler(local)
     clk.start()
-    times, infos = [], []
+    times, infos, ents, kts = [], [], [], []
     for _ in range(args.steps):
-        ms, info = step()
+        ms, info, ne, bi = step()
         times.append(ms)
         infos.append(info.as_dict())
+        ents.append(ne)
     clocks = clk.stop()
-    e2e_times = []
+    e2e_times, e2e_ents, e2e_in = [], [], []
     if not args.no_e2e:
         state["i"] = 0
         L.sambaten_restore(h)
         for _ in range(args.warmup):
             step(host=True)
         for _ in range(args.steps):
-            ms, _ = step(host=True)
+            ms, _, ne, bi = step(host=True)
             e2e_times.append(ms)
+            e2e_ents.append(ne)
+            e2e_in.append(work.bytes_in(bi))
     tot = sum(times) / 1000.0
     e2e_tot = sum(e2e_times) / 1000.0 if e2e_times else None
     if world > 1:
         t = torch.tensor([tot, e2e_tot or 0.0], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot, e2e_tot = float(t[0]), (float(t[1]) if e2e_times else None)
-    per_step_entries = w.I * w.J * w.batch
-    value = world * per_step_entries * args.steps / tot
+    value = world * sum(ents) / tot
 
     peaks, peak_kind = measured_peaks()
     # dominant HBM-bound kernel of the step: the marginal pass a1 (one read of the whole tensor)
     a1_ms = statistics.mean(inf["step_ms"][1] for inf in infos)
     Kavg = statistics.mean(inf["k_total"] for inf in infos)
-    a1_bytes = 4.0 * w.I * w.J * Kavg + 8.0 * (w.I + w.J + Kavg)
+    if not work.coo:
+        a1_bytes = 4.0 * w.I * w.J * Kavg + 8.0 * (w.I + w.J + Kavg)
+        kname = "marg_stream_kernel (a1)"
+    else:
+        nnz_avg = work.X0.nnz + statistics.mean(
+            sum(work.entries[:(j % nb) + 1]) for j in range(args.warmup, args.warmup + args.steps))
+        a1_bytes = 16.0 * nnz_avg + 8.0 * (w.I + w.J + Kavg)
+        kname = "marg_coo_kernel (a1)"
     achieved = a1_bytes / (a1_ms / 1000.0) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(w.name, {}).get("marg_dense_kernel")
+            traffic = json.load(open(prof)).get(w.name, {}).get("a1")
         except Exception:
             traffic = None
     step_share = {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in infos) for k in range(8)}
@@ -267,9 +356,9 @@ def main():
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic planted rank-R + 1% Gaussian noise (numpy, seed 0)",
+        "data": "synthetic (seeded numpy generators; DESIGN.md 'Synthetic inputs')",
         "config": config,
-        "roofline": {"kernel": "marg_dense_kernel (a1)", "bound": "hbm", "achieved": achieved,
+        "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved,
                      "peak": peaks["hbm_gbs"], "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "bytes_per_launch": a1_bytes, "ms_per_launch": a1_ms},
@@ -277,17 +366,20 @@ def main():
         "gpu_launches": int(sum(inf["kernel_launches"] for inf in infos)),
         "clocks": clocks,
         "fit_full_last": infos[-1]["fit_full"],
+        "fit_summary_last": infos[-1]["fit_summary"],
         "reps_rejected_last": bin(infos[-1]["reps_rejected_mask"]).count("1"),
     }
     if e2e_tot:
-        hb = 4 * w.I * w.J * w.batch
+        hb = int(statistics.mean(e2e_in))
         db = 4 * (w.I + w.J + w.K + 1) * w.R
-        line["e2e"] = {"value": world * per_step_entries * args.steps / e2e_tot, "unit": unit,
+        line["e2e"] = {"value": world * sum(e2e_ents) / e2e_tot, "unit": unit,
                        "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, nbt = cpu_baseline_run(w, T0, batches, model)
-        line["cpu_baseline"] = {"value": v, "unit": unit, "cores": threads_used(), "kind": "oracle",
-                                "sample": f"{nbt} oracle updates (all batches of {w.name}) from the K0 state, {dt:.1f} s"}
+        model = work.model
+        if model is not None:
+            v, dt, nbt = cpu_baseline_run(work, model)
+            line["cpu_baseline"] = {"value": v, "unit": unit, "cores": threads_used(), "kind": "oracle",
+                                    "sample": f"{nbt} consecutive oracle updates of {w.name} from the K0 state, {dt:.1f} s"}
     L.sambaten_destroy(h)
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -136,6 +136,12 @@ SAMBATEN_API sambaten_status sambaten_get_factors(sambaten_t h, const float** A,
                                      const float** C, const float** lambda, int64_t dims[3],
                                      int* R);
 
+/* Copy the current model into caller buffers (host or device by pointer; any may be NULL):
+ * A [I][R], B [J][R], C [K][R] (K = current mode-3 extent), lambda [R], float32 row-major.
+ * Synchronises the handle's stream. */
+SAMBATEN_API sambaten_status sambaten_copy_factors(sambaten_t h, float* A, float* B, float* C,
+                                      float* lambda);
+
 /* Sample sets of the last update, copied to caller (host or device) buffers of
  * r * n_mode int32 each (rep-major): I_s, J_s, K_s (sorted, R9).  Any pointer may be NULL.
  * n_out[3] receives n_I, n_J, n_Ks. */

@@ -76,6 +76,7 @@ def lib():
         "sambaten_get_factors": (i32, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp),
                                        C.POINTER(i64), C.POINTER(ip)]),
         "sambaten_last_samples": (i32, [vp, vp, vp, vp, C.POINTER(i64)]),
+        "sambaten_copy_factors": (i32, [vp, vp, vp, vp, vp]),
         "sambaten_relative_error": (i32, [vp, C.POINTER(d)]),
         "sambaten_checkpoint": (i32, [vp]),
         "sambaten_restore": (i32, [vp]),
@@ -101,7 +102,7 @@ def lib():
 
 
 EXPORTED = ["sambaten_default_opts", "sambaten_init", "sambaten_init_factors", "sambaten_update",
-            "sambaten_get_factors", "sambaten_last_samples", "sambaten_relative_error",
+            "sambaten_get_factors", "sambaten_copy_factors", "sambaten_last_samples", "sambaten_relative_error",
             "sambaten_checkpoint", "sambaten_restore", "sambaten_destroy",
             "sambaten_fixed_point_scale", "sambaten_marginals", "sambaten_sample", "sambaten_gather",
             "sambaten_mttkrp", "sambaten_cp_als", "sambaten_fit", "sambaten_philox", "sambaten_detlog",
@@ -217,6 +218,10 @@ def sambaten_get_factors(h):
     R = C.c_int()
     check(lib().sambaten_get_factors(h, C.byref(a), C.byref(b), C.byref(c), C.byref(l), dims, C.byref(R)))
     return dict(A=a.value, B=b.value, C=c.value, lam=l.value, dims=tuple(dims), R=R.value)
+
+
+def sambaten_copy_factors(h, A=None, B=None, Cm=None, lam=None):
+    check(lib().sambaten_copy_factors(h, ptr(A), ptr(B), ptr(Cm), ptr(lam)))
 
 
 def sambaten_last_samples(h, Is=None, Js=None, Ks=None):

@@ -921,6 +921,18 @@ extern "C" sambaten_status sambaten_get_factors(sambaten_t h, const float** A, c
   return SAMBATEN_OK;
 }
 
+extern "C" sambaten_status sambaten_copy_factors(sambaten_t h, float* A, float* B, float* C,
+                                                 float* lambda) {
+  if (!h) FAIL(SAMBATEN_E_INVALID, "copy_factors: NULL handle");
+  const int b = h->cur, R = h->R;
+  if (A) CK(cudaMemcpyAsync(A, h->A(b), sizeof(float) * h->I * R, cudaMemcpyDefault, h->st));
+  if (B) CK(cudaMemcpyAsync(B, h->B(b), sizeof(float) * h->J * R, cudaMemcpyDefault, h->st));
+  if (C) CK(cudaMemcpyAsync(C, h->C(b), sizeof(float) * h->K * R, cudaMemcpyDefault, h->st));
+  if (lambda) CK(cudaMemcpyAsync(lambda, h->lam(b), sizeof(float) * R, cudaMemcpyDefault, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return SAMBATEN_OK;
+}
+
 extern "C" sambaten_status sambaten_last_samples(sambaten_t h, int32_t* Is, int32_t* Js,
                                                  int32_t* Ks, int64_t n_out[3]) {
   if (!h) FAIL(SAMBATEN_E_INVALID, "last_samples: NULL handle");
