@@ -435,15 +435,17 @@ static cudaError_t run_match_merge(sambaten_s* h, const DenseAls& a, const int32
   const int R = h->R, r = h->r;
   cudaStream_t st = h->st;
   const int b = h->cur, nb = 1 - h->cur;
-  cudaError_t e = h->match.ensure(align256(sizeof(int) * r * R) + align256(sizeof(double) * r * 3 * R) +
-                                  align256(sizeof(double) * r * R) + align256(sizeof(double) * r) +
-                                  align256(sizeof(int) * r));
-  if (e != cudaSuccess) return e;
-  char* mp = h->match.as<char>();
   MatchArgs ma{};
   ma.A = h->A(b); ma.B = h->B(b); ma.C = h->C(b); ma.R = R; ma.r = r;
   ma.Is = Is; ma.Js = Js; ma.Ks = Kp;
   ma.nI = (int)nI; ma.nJ = (int)nJ; ma.nKs = (int)nKs; ma.nK = (int)nKp; ma.ks_stride = nKp;
+  const size_t part_b = align256(sizeof(double) * match_part_doubles(ma));
+  cudaError_t e = h->match.ensure(align256(sizeof(int) * r * R) + align256(sizeof(double) * r * 3 * R) +
+                                  align256(sizeof(double) * r * R) + align256(sizeof(double) * r) +
+                                  align256(sizeof(int) * r) + part_b);
+  if (e != cudaSuccess) return e;
+  char* mp = h->match.as<char>();
+  ma.part = reinterpret_cast<double*>(mp + h->match.bytes - part_b);
   for (int m = 0; m < 3; ++m) { ma.U[m] = a.U[m]; ma.u_stride[m] = a.u_stride[m]; }
   ma.lamp = a.lam; ma.tau = h->opts.accept_tau;
   ma.pi = (int*)mp; mp += align256(sizeof(int) * r * R);
@@ -581,6 +583,7 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     double* G = b.take<double>((size_t)r * 3 * R * R);
     double* lam = b.take<double>((size_t)r * R);
     double* ysq = b.take<double>((size_t)r * 257);
+    double* gpart = b.take<double>(gram_part_doubles((int)maxn, R, r));
     double* fit = b.take<double>(r);
     double* fitp = b.take<double>(r);
     int* iters = b.take<int>(r);
@@ -589,7 +592,27 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     double* M0 = b.take<double>((size_t)r * nI * R);
     double* Mb = b.take<double>((size_t)r * maxn * R);
     double* Us = b.take<double>((size_t)r * maxn * R);
+    double* Vi = b.take<double>((size_t)r * R * R);
+    double* rpart = b.take<double>(als_rows_part_doubles((int)maxn, R, r));
+    int* stop = b.take<int>(r);
+    // per-mode MTTKRP plans: row pieces, sorted copies (modes 0, 1), piece partials
+    const int rows_m[3] = {nI, nJ, nK};
+    CooModePlan plan[3];
+    for (int m = 0; m < 3; ++m) {
+      const int64_t nrow = (int64_t)r * rows_m[m];
+      const size_t pe = coo_plan_elems(nrow, n);
+      plan[m].nrow = nrow; plan[m].n = ntot;
+      plan[m].pstart = b.take<int64_t>(nrow + 1);
+      plan[m].pb = b.take<int64_t>(pe);
+      plan[m].prow = b.take<int32_t>(pe);
+      plan[m].partial = b.take<double>(pe * R);
+      if (m < 2) {
+        plan[m].sa = b.take<int32_t>(n); plan[m].sb = b.take<int32_t>(n); plan[m].sv = b.take<float>(n);
+      }
+    }
     if (!assign) return;
+    plan[0].ptr = ptr0; plan[1].ptr = ptr1; plan[2].ptr = ptr2;
+    plan[2].sa = p; plan[2].sb = q; plan[2].sv = v;
     *d = DenseAls{};
     d->nI = nI; d->nJ = nJ; d->nK = nK; d->R = R; d->r = r;
     d->U[0] = U0; d->U[1] = U1; d->U[2] = U2;
@@ -605,12 +628,13 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     if (e == cudaSuccess) e = coo_row_pointers(keys, ntot, kb1, r, nJ, cnt, ptr1, sws, st);
     if (e == cudaSuccess) e = coo_make_keys(u, d_off, r, kb2, ntot, keys, st);
     if (e == cudaSuccess) e = coo_row_pointers(keys, ntot, kb2, r, nK, cnt, ptr2, sws, st);
+    if (e == cudaSuccess) e = coo_build_plan(plan[0], perm0, q, u, v, ntot, cnt, sws, st);
+    if (e == cudaSuccess) e = coo_build_plan(plan[1], perm1, p, u, v, ntot, cnt, sws, st);
+    if (e == cudaSuccess) e = coo_build_plan(plan[2], nullptr, p, q, v, ntot, cnt, sws, st);
     CooAls a{};
     a.nI = nI; a.nJ = nJ; a.nK = nK; a.R = R; a.r = r;
     a.RB = R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
-    a.p = p; a.q = q; a.u = u; a.v = v;
-    a.perm[0] = perm0; a.perm[1] = perm1; a.perm[2] = nullptr;
-    a.ptr[0] = ptr0; a.ptr[1] = ptr1; a.ptr[2] = ptr2;
+    for (int m = 0; m < 3; ++m) a.plan[m] = plan[m];
     for (int m = 0; m < 3; ++m) { a.U[m] = d->U[m]; a.u_stride[m] = d->u_stride[m]; }
     a.M[0] = M0; a.m_stride[0] = (int64_t)nI * R;
     a.M[1] = a.M[2] = Mb; a.m_stride[1] = a.m_stride[2] = maxn * R;
@@ -620,14 +644,33 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(iters, 0, sizeof(int) * r, st);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(flags, 0, sizeof(int) * r, st);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(fit, 0, sizeof(double) * r, st);
-    if (e == cudaSuccess) e = launch_als_gram(*d, st);
+    if (e == cudaSuccess) {
+      GramArgs ga{};
+      for (int m = 0; m < 3; ++m) { ga.U[m] = d->U[m]; ga.u_stride[m] = d->u_stride[m]; }
+      ga.n[0] = nI; ga.n[1] = nJ; ga.n[2] = nK; ga.R = R; ga.r = r;
+      ga.tmax = gram_tiles_for((int)maxn); ga.part = gpart; ga.G = G; ga.g_stride = 3 * R * R;
+      e = launch_gram_tiles(ga, st);
+    }
     if (e == cudaSuccess) e = launch_coo_sumsq(v, d_off, r, ysq, st);
-    for (int it = 0; it < maxit && e == cudaSuccess; ++it)
+    // row-parallel solve steps (k_als_rows.cu) for R <= 16, the one-block solve otherwise
+    RowsAls ra{};
+    ra.nI = nI; ra.nJ = nJ; ra.nK = nK; ra.R = R; ra.r = r; ra.maxit = maxit; ra.tol = tol;
+    for (int m = 0; m < 3; ++m) { ra.U[m] = d->U[m]; ra.u_stride[m] = d->u_stride[m]; }
+    ra.M[0] = M0; ra.m_stride[0] = (int64_t)nI * R;
+    ra.M[1] = ra.M[2] = Mb; ra.m_stride[1] = ra.m_stride[2] = maxn * R;
+    ra.X = Us; ra.x_stride = maxn * R; ra.Vi = Vi; ra.part = rpart; ra.G = G; ra.lam = lam;
+    ra.ysq = ysq; ra.fit = fit; ra.fit_prev = fitp; ra.iters = iters; ra.done = done;
+    ra.flags = flags; ra.stop = stop;
+    const bool rows = R <= 16;
+    if (e == cudaSuccess) e = cudaMemsetAsync(stop, 0, sizeof(int) * r, st);
+    for (int it = 0; it < maxit && e == cudaSuccess; ++it) {
+      if (rows && it > 0) e = launch_als_rows_commit(ra, st);
       for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
         e = launch_coo_mttkrp(a, m, st);
-        if (e == cudaSuccess) e = launch_als_solve(*d, m, st);
+        if (e == cudaSuccess) e = rows ? launch_als_rows_mode(ra, m, st) : launch_als_solve(*d, m, st);
       }
-    *launches = 2 * 3 + 9 + 3 + 3 + 3 + 6 * maxit;
+    }
+    *launches = 2 * 3 + 9 + 3 + 3 + 3 + (rows ? 16 : 6) * maxit;
     if (e != cudaSuccess) {
       set_error(std::string("COO ALS: ") + cudaGetErrorString(e));
       d->nI = -1;
@@ -786,7 +829,7 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
   CK(cudaEventRecord(h->ev[7], st));
   // ---- a7: full fit of the new model (optional) ----------------------------------------------
   if (h->opts.full_fit) {
-    CK(h->fitws.ensure(sizeof(double) * coo_fit_ws_doubles()));
+    CK(h->fitws.ensure(sizeof(double) * coo_fit_ws_doubles(h->I, h->J, h->Kcap)));
     CooView Xn = Xall;
     Xn.K = Ko + Kn;
     CK(launch_coo_fit(Xn, h->lam(nbuf), h->A(nbuf), h->B(nbuf), h->C(nbuf), R, h->fitws.as<double>(),
@@ -955,7 +998,7 @@ extern "C" sambaten_status sambaten_relative_error(sambaten_t h, double* relerr)
   if (!h || !relerr) FAIL(SAMBATEN_E_INVALID, "relative_error: NULL argument");
   if (h->fmt == SAMBATEN_COO) {
     DevBuf ws;
-    CK(ws.ensure(sizeof(double) * (coo_fit_ws_doubles() + 8)));
+    CK(ws.ensure(sizeof(double) * (coo_fit_ws_doubles(h->I, h->J, h->Kcap) + 8)));
     double* d = ws.as<double>();
     CK(launch_coo_fit(h->coo_view(h->nnz), h->lam(h->cur), h->A(h->cur), h->B(h->cur), h->C(h->cur),
                       h->R, d + 8, d, h->st));
@@ -1136,6 +1179,7 @@ static sambaten_status coo_mttkrp_single(const sambaten_tensor* X, const float* 
   const int64_t nn = std::max<int64_t>(n, 1);
   DevBuf ws;
   Bump sz;
+  const size_t pe = coo_plan_elems(rows, nn);
   auto lay = [&](Bump& b) {
     uint32_t* keys = b.take<uint32_t>(nn); int32_t* perm = b.take<int32_t>(nn);
     uint32_t* wk = b.take<uint32_t>(nn); int32_t* wv = b.take<int32_t>(nn);
@@ -1143,25 +1187,31 @@ static sambaten_status coo_mttkrp_single(const sambaten_tensor* X, const float* 
     int64_t* sws = b.take<int64_t>(std::max(scan_ws_elems(radix_ws_elems(nn)), scan_ws_elems(rows + 1)));
     int64_t* cnt = b.take<int64_t>(rows + 1); int64_t* ptr = b.take<int64_t>(rows + 1);
     int64_t* off = b.take<int64_t>(2); double* Md = b.take<double>(rows * R); int* done = b.take<int>(1);
-    return std::make_tuple(keys, perm, wk, wv, hist, offs, sws, cnt, ptr, off, Md, done);
+    CooModePlan pl{};
+    pl.nrow = rows; pl.n = n;
+    pl.pstart = b.take<int64_t>(rows + 1); pl.pb = b.take<int64_t>(pe); pl.prow = b.take<int32_t>(pe);
+    pl.partial = b.take<double>(pe * R);
+    pl.sa = b.take<int32_t>(nn); pl.sb = b.take<int32_t>(nn); pl.sv = b.take<float>(nn);
+    pl.ptr = ptr;
+    return std::make_tuple(keys, perm, wk, wv, hist, offs, sws, cnt, ptr, off, Md, done, pl);
   };
   lay(sz);
   CK(ws.ensure(sz.off));
   Bump b{ws.as<char>(), 0};
-  auto [keys, perm, wk, wv, hist, offs, sws, cnt, ptr, off, Md, done] = lay(b);
+  auto [keys, perm, wk, wv, hist, offs, sws, cnt, ptr, off, Md, done, pl] = lay(b);
   two_offsets_kernel<<<1, 32, 0, st>>>(off, n);
   CK(cudaMemsetAsync(done, 0, sizeof(int), st));
   const int32_t* idx = X->idx[mode];
   if (mode < 2) CK(coo_sort_by_index(idx, off, 1, kb, n, keys, perm, wk, wv, hist, offs, sws, st));
   else CK(coo_make_keys(idx, off, 1, kb, n, keys, st));
   CK(coo_row_pointers(keys, n, kb, 1, rows, cnt, ptr, sws, st));
+  const int oa = mode == 0 ? 1 : 0, ob = mode == 2 ? 1 : 2;
+  if (mode == 2) { pl.sa = X->idx[0]; pl.sb = X->idx[1]; pl.sv = X->vals; }
+  CK(coo_build_plan(pl, mode < 2 ? perm : nullptr, X->idx[oa], X->idx[ob], X->vals, n, cnt, sws, st));
   CooAls a{};
   a.nI = (int)I; a.nJ = (int)J; a.nK = (int)K; a.R = R; a.r = 1;
   a.RB = R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
-  a.p = X->idx[0]; a.q = X->idx[1]; a.u = X->idx[2]; a.v = X->vals;
-  a.perm[0] = a.perm[1] = a.perm[2] = nullptr;
-  a.perm[mode] = mode < 2 ? perm : nullptr;
-  a.ptr[mode] = ptr;
+  a.plan[mode] = pl;
   a.U[0] = const_cast<float*>(U0); a.U[1] = const_cast<float*>(U1); a.U[2] = const_cast<float*>(U2);
   a.u_stride[0] = a.u_stride[1] = a.u_stride[2] = 0;
   a.M[mode] = Md; a.m_stride[mode] = rows * R;
@@ -1258,7 +1308,7 @@ extern "C" sambaten_status sambaten_fit(const sambaten_tensor* X, const float* l
   if (X->fmt == SAMBATEN_COO) {
     const CooView V{X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, X->dims[0], X->dims[1], X->dims[2]};
     void* ws = nullptr;
-    CK(cudaMallocAsync(&ws, sizeof(double) * coo_fit_ws_doubles(), st));
+    CK(cudaMallocAsync(&ws, sizeof(double) * coo_fit_ws_doubles(V.I, V.J, V.K), st));
     CK(launch_coo_fit(V, lambda, A, B, C, R, static_cast<double*>(ws), relerr, st));
     CK(cudaFreeAsync(ws, st));
     return SAMBATEN_OK;

@@ -121,7 +121,10 @@ struct MatchArgs {
   double* lam_hat;   // [r][R]
   double* score_min; // [r]
   int* accepted;     // [r]
+  double* part;      // [r][3][match_chunks][R*R + 2R] partial anchor sums (workspace)
 };
+int match_chunks(const MatchArgs& m);
+size_t match_part_doubles(const MatchArgs& m);
 cudaError_t launch_match(const MatchArgs& m, cudaStream_t st);
 
 struct MergeArgs {
@@ -148,16 +151,26 @@ struct CooView {                       // canonical COO tensor, device arrays
   const float* v;
   int64_t nnz, I, J, K;
 };
+struct CooModePlan {                   // per-mode MTTKRP layout (k_coo.cu)
+  int64_t nrow, n;                     // r * rows, entries
+  const int64_t* ptr;                  // [nrow + 1] row pointers into the mode's order
+  int64_t* pstart;                     // [nrow + 1] first piece of each row (scan)
+  int64_t* pb;                         // [pieces] first entry of each piece
+  int32_t* prow;                       // [pieces] row (rep * rows + row) of each piece
+  const int32_t *sa, *sb;              // other two indices in the mode's order
+  const float* sv;                     // values in the mode's order
+  double* partial;                     // [pieces][R] partial sums of multi-piece rows
+};
 struct CooAls {                        // the r COO summaries (concatenated) + ALS buffers
   int nI, nJ, nK, R, RB, r;
-  const int32_t *p, *q, *u;            // local coordinates, canonical (u, q, p) per rep
-  const float* v;
-  const int32_t* perm[3];              // entry order sorted by mode index (perm[2] = null)
-  const int64_t* ptr[3];               // row pointers: rep rho, row x -> ptr[m][rho*rows + x]
+  CooModePlan plan[3];
   float* U[3]; int64_t u_stride[3];
   double* M[3]; int64_t m_stride[3];
   const int* done;
 };
+size_t coo_plan_elems(int64_t nrow, int64_t n);
+cudaError_t coo_build_plan(CooModePlan& pl, const int32_t* perm, const int32_t* ia, const int32_t* ib,
+                           const float* v, int64_t n, int64_t* cnt, int64_t* sws, cudaStream_t st);
 cudaError_t launch_coo_validate(const int32_t* i, const int32_t* j, const int32_t* k, const float* v,
                                 int64_t n, int64_t I, int64_t J, int64_t K, unsigned* flags,
                                 cudaStream_t st);
@@ -186,16 +199,43 @@ cudaError_t coo_row_pointers(const uint32_t* sorted_keys, int64_t n, int kb, int
                              int64_t* cnt, int64_t* ptr, int64_t* sws, cudaStream_t st);
 cudaError_t launch_coo_mttkrp(const CooAls& a, int mode, cudaStream_t st);
 cudaError_t launch_coo_sumsq(const float* v, const int64_t* off, int r, double* ysq, cudaStream_t st);
-size_t coo_fit_ws_doubles();
+size_t coo_fit_ws_doubles(int64_t I, int64_t J, int64_t K);
 cudaError_t launch_coo_fit(const CooView& X, const float* lam, const float* A, const float* B,
                            const float* C, int R, double* ws, double* relerr, cudaStream_t st);
 cudaError_t launch_coo_max_phi(const float* v, int64_t n, int moi, unsigned long long* out, cudaStream_t st);
+// row-parallel ALS solve steps (k_als_rows.cu), R <= 16
+struct RowsAls {
+  int nI, nJ, nK, R, r, maxit;
+  double tol;
+  float* U[3]; int64_t u_stride[3];
+  const double* M[3]; int64_t m_stride[3];
+  double* X; int64_t x_stride;         // [r][maxn][R] solved rows
+  double* Vi;                          // [r][R][R]
+  double* part;                        // [r][tiles][R*R + 1]
+  double* G;                           // [r][3][R][R]
+  double* lam;                         // [r][R]
+  double* ysq; double* fit; double* fit_prev;
+  int* iters; int* done; int* flags; int* stop;
+};
+cudaError_t launch_als_rows_mode(const RowsAls& a, int mode, cudaStream_t st);
+struct GramArgs {                      // G[rep][m] = U_m^T U_m for m < 3, rep < r (fp64)
+  const float* U[3]; int64_t u_stride[3]; int n[3];
+  int R, r, tmax;                      // tmax = gram_tiles_for(max n)
+  double* part;                        // gram_part_doubles(max n, R, r)
+  double* G; int64_t g_stride;         // per-rep stride of G (>= 3 R^2)
+};
+size_t gram_part_doubles(int maxn, int R, int r);
+int gram_tiles_for(int n);
+cudaError_t launch_gram_tiles(const GramArgs& g, cudaStream_t st);
+cudaError_t launch_als_rows_commit(const RowsAls& a, cudaStream_t st);
+size_t als_rows_part_doubles(int maxn, int R, int r);
 // ALS pieces shared with the COO path (k_als.cu)
 cudaError_t launch_als_solve(const DenseAls& a, int mode, cudaStream_t st);
 cudaError_t launch_als_gram(const DenseAls& a, cudaStream_t st);
-// Grams of three factors, fp64 [3][R][R] (k_stream.cu)
+// Grams of three factors, fp64 [3][R][R] (k_stream.cu), ws: gram3_ws_doubles
+size_t gram3_ws_doubles(int64_t I, int64_t J, int64_t K, int R);
 cudaError_t launch_gram3(const float* A, const float* B, const float* C, int64_t I, int64_t J,
-                         int64_t K, int R, double* G, cudaStream_t st);
+                         int64_t K, int R, double* G, double* ws, cudaStream_t st);
 
 // k_stream.cu: TMA-ring streaming passes over the dense store (pitch % 4 == 0, 16 B aligned)
 bool stream_supported(const DenseView& X);

@@ -345,69 +345,145 @@ __global__ void key_count_kernel(const uint32_t* __restrict__ keys, int64_t n, i
 }
 
 // ---------------------------------------------------------------------------------------
-// a4: MTTKRP over a COO summary, one warp per (rep, output row):
-//   M(row, f) = sum_{e in row} v_e U_a(a_e, f) U_b(b_e, f)
-// Lane l takes entries l, l+32, ... of the row (fp32 products, fp64 per-lane sums), then a
-// fixed butterfly -> deterministic.
+// a4: MTTKRP over the COO summaries:  M(row, f) = sum_{e in row} v_e U_a(a_e, f) U_b(b_e, f).
+// The entries of each mode are laid out contiguously by row (sorted copies of the other two
+// indices and the values), rows are cut into pieces of <= kPiece entries (Zipf-hot rows
+// spread over many warps), one warp per piece: lane l takes entries l, l+32, ... (fp32
+// products, fp64 per-lane sums) and a fixed butterfly; single-piece rows write M directly,
+// multi-piece rows write partials summed in piece order by a fix-up kernel -> deterministic,
+// no float atomics.
 // ---------------------------------------------------------------------------------------
-template <int RB>
-__global__ void coo_mttkrp_kernel(CooAls a, int mode) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
-  const int64_t tot = (int64_t)a.r * rows;
-  if (gw >= tot) return;
-  const int rep = (int)(gw / rows);
-  const int row = (int)(gw - (int64_t)rep * rows);
-  if (a.done[rep]) return;
-  const int64_t* ptr = a.ptr[mode] + (int64_t)rep * rows;
-  const int64_t b = ptr[row], e = ptr[row + 1];
-  const int32_t* perm = a.perm[mode];   // null for mode 2 (natural order)
-  const int R = a.R;
-  const int oa = mode == 0 ? 1 : 0, ob = mode == 2 ? 1 : 2;
-  const int32_t* ia = oa == 0 ? a.p : a.q;
-  const int32_t* ib = ob == 1 ? a.q : a.u;
-  const float* Ua = a.U[oa] + rep * a.u_stride[oa];
-  const float* Ub = a.U[ob] + rep * a.u_stride[ob];
-  double acc[RB];
-#pragma unroll
-  for (int f = 0; f < RB; ++f) acc[f] = 0.0;
-  for (int64_t t = b + lane; t < e; t += 32) {
-    const int64_t x = perm ? perm[t] : t;
-    const float v = a.v[x];
-    const float* ra = Ua + (int64_t)ia[x] * R;
-    const float* rb = Ub + (int64_t)ib[x] * R;
-#pragma unroll
-    for (int f = 0; f < RB; ++f)
-      if (f < R) acc[f] += (double)(v * ra[f] * rb[f]);
-  }
-#pragma unroll
-  for (int f = 0; f < RB; ++f) {
-    double s = acc[f];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    acc[f] = s;
-  }
-  if (lane == 0) {
-    double* M = a.M[mode] + (int64_t)rep * a.m_stride[mode] + (int64_t)row * R;
-#pragma unroll
-    for (int f = 0; f < RB; ++f)
-      if (f < R) M[f] = acc[f];
+constexpr int kPiece = 256;
+
+__global__ void piece_count_kernel(const int64_t* __restrict__ ptr, int64_t nrow, int64_t* __restrict__ cnt) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= nrow;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    if (x == nrow) { cnt[x] = 0; continue; }
+    const int64_t len = ptr[x + 1] - ptr[x];
+    cnt[x] = len <= kPiece ? 1 : (len + kPiece - 1) / kPiece;
   }
 }
 
+__global__ void piece_fill_kernel(const int64_t* __restrict__ ptr, const int64_t* __restrict__ pstart,
+                                  int64_t nrow, int64_t* __restrict__ pb, int32_t* __restrict__ prow) {
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < nrow;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = pstart[x], n = pstart[x + 1] - s;
+    for (int64_t k = 0; k < n; ++k) {
+      pb[s + k] = ptr[x] + k * kPiece;
+      prow[s + k] = (int32_t)x;
+    }
+  }
+}
+
+// sorted copies: sa[t] = ia[perm[t]], sb[t] = ib[perm[t]], sv[t] = v[perm[t]]
+__global__ void permute3_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ ia,
+                                const int32_t* __restrict__ ib, const float* __restrict__ v, int64_t n,
+                                int32_t* __restrict__ sa, int32_t* __restrict__ sb, float* __restrict__ sv) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = perm[t];
+    sa[t] = ia[x];
+    sb[t] = ib[x];
+    sv[t] = v[x];
+  }
+}
+
+// One warp per piece: lane l takes entries l, l+32, ... (fp32 products, fp64 per-lane sums),
+// then a fixed butterfly.  (A half-warp-per-entry variant with coalesced row gathers measured
+// slower on C3: fewer entries in flight per warp.)
+template <int RB>
+__global__ void coo_mttkrp_piece_kernel(CooAls a, int mode, int64_t npiece_max) {
+  const int lane = threadIdx.x & 31;
+  const CooModePlan& pl = a.plan[mode];
+  const int64_t P = pl.pstart[pl.nrow];
+  const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
+  const int R = a.R;
+  const int oa = mode == 0 ? 1 : 0, ob = mode == 2 ? 1 : 2;
+  for (int64_t piece = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; piece < P;
+       piece += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int x = pl.prow[piece];
+    const int rep = x / rows, row = x - rep * rows;
+    if (a.done[rep]) continue;
+    const int64_t b = pl.pb[piece];
+    const int64_t e = min(b + kPiece, pl.ptr[x + 1]);
+    const float* Ua = a.U[oa] + rep * a.u_stride[oa];
+    const float* Ub = a.U[ob] + rep * a.u_stride[ob];
+    double acc[RB];
+#pragma unroll
+    for (int f = 0; f < RB; ++f) acc[f] = 0.0;
+#pragma unroll 2
+    for (int64_t t = b + lane; t < e; t += 32) {
+      const float v = pl.sv[t];
+      const float* ra = Ua + (int64_t)pl.sa[t] * R;
+      const float* rb = Ub + (int64_t)pl.sb[t] * R;
+#pragma unroll
+      for (int f = 0; f < RB; ++f)
+        if (f < R) acc[f] += (double)(v * ra[f] * rb[f]);
+    }
+#pragma unroll
+    for (int f = 0; f < RB; ++f) {
+      double s = acc[f];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      acc[f] = s;
+    }
+    const bool single = pl.pstart[x + 1] - pl.pstart[x] == 1;
+    double* out = single ? a.M[mode] + (int64_t)rep * a.m_stride[mode] + (int64_t)row * R
+                         : pl.partial + piece * R;
+    if (lane < R) {
+      double v = 0.0;
+#pragma unroll
+      for (int f = 0; f < RB; ++f)
+        if (f == lane) v = acc[f];
+      out[lane] = v;
+    }
+  }
+  (void)npiece_max;
+}
+
+// rows with several pieces: sum the piece partials in order
+__global__ void coo_piece_fixup_kernel(CooAls a, int mode) {
+  const CooModePlan& pl = a.plan[mode];
+  const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
+  const int R = a.R;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < pl.nrow * R;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = t / R;
+    const int f = (int)(t - x * R);
+    const int64_t s = pl.pstart[x], n = pl.pstart[x + 1] - s;
+    if (n <= 1) continue;
+    const int rep = (int)(x / rows), row = (int)(x - (int64_t)rep * rows);
+    if (a.done[rep]) continue;
+    double sum = 0.0;
+    for (int64_t k = 0; k < n; ++k) sum += pl.partial[(s + k) * R + f];
+    a.M[mode][(int64_t)rep * a.m_stride[mode] + (int64_t)row * R + f] = sum;
+  }
+}
+
+// ||Y_rho||^2: block b of rep rho sums a fixed stride of its entries; partials combined in
+// block order (ysq holds r results followed by r * kSqBlocks partials).
+constexpr int kSqBlocks = 64;
 __global__ void coo_sumsq_kernel(const float* __restrict__ v, const int64_t* __restrict__ off, int r,
                                  double* __restrict__ ysq) {
   __shared__ double red[32];
-  const int rep = blockIdx.x;
+  const int b = blockIdx.x, rep = blockIdx.y;
   double s = 0.0;
-  for (int64_t e = off[rep] + threadIdx.x; e < off[rep + 1]; e += blockDim.x) {
+  for (int64_t e = off[rep] + (int64_t)b * blockDim.x + threadIdx.x; e < off[rep + 1];
+       e += (int64_t)kSqBlocks * blockDim.x) {
     const double x = v[e];
     s += x * x;
   }
   s = block_sum_d(s, red);
-  if (threadIdx.x == 0) ysq[rep] = s;
-  (void)r;
+  if (threadIdx.x == 0) ysq[r + rep * kSqBlocks + b] = s;
+}
+
+__global__ void coo_sumsq_combine_kernel(int r, double* ysq) {
+  const int rep = threadIdx.x;
+  if (rep >= r) return;
+  double s = 0.0;
+  for (int b = 0; b < kSqBlocks; ++b) s += ysq[r + rep * kSqBlocks + b];
+  ysq[rep] = s;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -578,27 +654,48 @@ cudaError_t launch_coo_max_phi(const float* v, int64_t n, int moi, unsigned long
   return cudaGetLastError();
 }
 
+size_t coo_plan_elems(int64_t nrow, int64_t n) { return (size_t)(nrow + n / kPiece + 2); }
+
+// Row pieces of one mode (from its row pointers) and, for the sorted modes, the permuted copies
+// of the other two indices and the values.  cnt: nrow+1 int64 scratch, sws: scan workspace.
+cudaError_t coo_build_plan(CooModePlan& pl, const int32_t* perm, const int32_t* ia, const int32_t* ib,
+                           const float* v, int64_t n, int64_t* cnt, int64_t* sws, cudaStream_t st) {
+  piece_count_kernel<<<grid_for(pl.nrow + 1), kCT, 0, st>>>(pl.ptr, pl.nrow, cnt);
+  cudaError_t e = exclusive_scan_i64(cnt, pl.nrow + 1, pl.pstart, sws, st);
+  if (e != cudaSuccess) return e;
+  piece_fill_kernel<<<grid_for(pl.nrow), kCT, 0, st>>>(pl.ptr, pl.pstart, pl.nrow, pl.pb, pl.prow);
+  if (perm && n > 0)
+    permute3_kernel<<<grid_for(n), kCT, 0, st>>>(perm, ia, ib, v, n, const_cast<int32_t*>(pl.sa),
+                                                const_cast<int32_t*>(pl.sb), const_cast<float*>(pl.sv));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_coo_mttkrp(const CooAls& a, int mode, cudaStream_t st) {
-  const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
-  const int64_t warps = (int64_t)a.r * rows;
-  const unsigned grid = (unsigned)ceil_div(warps * 32, kCT);
+  const CooModePlan& pl = a.plan[mode];
+  const int64_t pmax = (int64_t)coo_plan_elems(pl.nrow, pl.n);
+  int64_t blocks = ceil_div(pmax * 32, kCT);
+  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
   switch (a.RB) {
-    case 4: coo_mttkrp_kernel<4><<<grid, kCT, 0, st>>>(a, mode); break;
-    case 8: coo_mttkrp_kernel<8><<<grid, kCT, 0, st>>>(a, mode); break;
-    case 12: coo_mttkrp_kernel<12><<<grid, kCT, 0, st>>>(a, mode); break;
-    case 16: coo_mttkrp_kernel<16><<<grid, kCT, 0, st>>>(a, mode); break;
-    case 24: coo_mttkrp_kernel<24><<<grid, kCT, 0, st>>>(a, mode); break;
-    default: coo_mttkrp_kernel<32><<<grid, kCT, 0, st>>>(a, mode); break;
+    case 4: coo_mttkrp_piece_kernel<4><<<(unsigned)blocks, kCT, 0, st>>>(a, mode, pmax); break;
+    case 8: coo_mttkrp_piece_kernel<8><<<(unsigned)blocks, kCT, 0, st>>>(a, mode, pmax); break;
+    case 12: coo_mttkrp_piece_kernel<12><<<(unsigned)blocks, kCT, 0, st>>>(a, mode, pmax); break;
+    case 16: coo_mttkrp_piece_kernel<16><<<(unsigned)blocks, kCT, 0, st>>>(a, mode, pmax); break;
+    case 24: coo_mttkrp_piece_kernel<24><<<(unsigned)blocks, kCT, 0, st>>>(a, mode, pmax); break;
+    default: coo_mttkrp_piece_kernel<32><<<(unsigned)blocks, kCT, 0, st>>>(a, mode, pmax); break;
   }
+  coo_piece_fixup_kernel<<<grid_for(pl.nrow * a.R), kCT, 0, st>>>(a, mode);
   return cudaGetLastError();
 }
 
 cudaError_t launch_coo_sumsq(const float* v, const int64_t* off, int r, double* ysq, cudaStream_t st) {
-  coo_sumsq_kernel<<<r, kCT, 0, st>>>(v, off, r, ysq);
+  coo_sumsq_kernel<<<dim3(kSqBlocks, r), kCT, 0, st>>>(v, off, r, ysq);
+  coo_sumsq_combine_kernel<<<1, 32, 0, st>>>(r, ysq);
   return cudaGetLastError();
 }
 
-size_t coo_fit_ws_doubles() { return 2 * (size_t)kNumSMs * 4 + 3 * kMaxR * kMaxR + 8; }
+size_t coo_fit_ws_doubles(int64_t I, int64_t J, int64_t K) {
+  return 2 * (size_t)kNumSMs * 4 + 3 * kMaxR * kMaxR + 8 + gram3_ws_doubles(I, J, K, kMaxR);
+}
 
 cudaError_t launch_coo_fit(const CooView& X, const float* lam, const float* A, const float* B,
                            const float* C, int R, double* ws, double* relerr, cudaStream_t st) {
@@ -612,7 +709,7 @@ cudaError_t launch_coo_fit(const CooView& X, const float* lam, const float* A, c
     case 24: coo_fit_kernel<24><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
     default: coo_fit_kernel<32><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
   }
-  cudaError_t e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, st);
+  cudaError_t e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
   if (e != cudaSuccess) return e;
   coo_fit_combine_kernel<<<1, 32, 0, st>>>(ws, nb, G, lam, R, relerr);
   return cudaGetLastError();

@@ -61,7 +61,65 @@ __device__ __forceinline__ void unrank_perm(long long k, int R, int* perm) {
   }
 }
 
-__global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m) {
+// Partial anchor sums of one chunk of kMatchRows sampled rows of one mode and repetition:
+// part[rep][mode][chunk][0 .. R*R)      = sum_p old(p,f) cand(p,g)  (anchor rows only, R14)
+//                       [R*R .. R*R+R)   = sum_p old(p,f)^2
+//                       [R*R+R .. +2R)   = sum_p cand(p,g)^2
+// Rows are staged in shared memory; thread per entry sums the chunk's rows in order.
+constexpr int kMatchRows = 128;
+
+__global__ void __launch_bounds__(kMatchThreads) match_partial_kernel(MatchArgs m, int nchunk) {
+  const int chunk = blockIdx.x, mode = blockIdx.y, rep = blockIdx.z;
+  const int R = m.R;
+  __shared__ float sor[kMatchRows][kMaxR + 1];
+  __shared__ float scr[kMatchRows][kMaxR + 1];
+  __shared__ unsigned char anc[kMatchRows];
+  const float* F = mode == 0 ? m.A : mode == 1 ? m.B : m.C;
+  const int32_t* idx = mode == 0 ? m.Is + (int64_t)rep * m.nI
+                     : mode == 1 ? m.Js + (int64_t)rep * m.nJ : m.Ks + (int64_t)rep * m.ks_stride;
+  const int n = mode == 0 ? m.nI : mode == 1 ? m.nJ : m.nKs;
+  const float* U = m.U[mode] + rep * m.u_stride[mode];
+  const int p0 = chunk * kMatchRows;
+  const int nr = max(0, min(kMatchRows, n - p0));
+  for (int e = threadIdx.x; e < kMatchRows * R; e += blockDim.x) {
+    const int pl = e / R, f = e - pl * R;
+    float o = 0.f, c = 0.f;
+    if (pl < nr) {
+      o = F[(int64_t)idx[p0 + pl] * R + f];
+      c = U[(int64_t)(p0 + pl) * R + f];
+    }
+    sor[pl][f] = o;
+    scr[pl][f] = c;
+  }
+  __syncthreads();
+  for (int pl = threadIdx.x; pl < kMatchRows; pl += blockDim.x) {
+    bool nz = false;
+    for (int f = 0; f < R; ++f) nz |= (sor[pl][f] != 0.0f);
+    anc[pl] = (pl < nr && nz) ? 1 : 0;
+  }
+  __syncthreads();
+  const int npair = R * R + 2 * R;
+  double* out = m.part + (((int64_t)rep * 3 + mode) * nchunk + chunk) * npair;
+  for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
+    double s = 0.0;
+    if (pr < R * R) {
+      const int f = pr / R, g = pr - f * R;
+      for (int pl = 0; pl < nr; ++pl)
+        if (anc[pl]) s += (double)sor[pl][f] * (double)scr[pl][g];
+    } else if (pr < R * R + R) {
+      const int f = pr - R * R;
+      for (int pl = 0; pl < nr; ++pl)
+        if (anc[pl]) { const double o = sor[pl][f]; s += o * o; }
+    } else {
+      const int g = pr - R * R - R;
+      for (int pl = 0; pl < nr; ++pl)
+        if (anc[pl]) { const double c = scr[pl][g]; s += c * c; }
+    }
+    out[pr] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m, int nchunk) {
   const int rep = blockIdx.x;
   const int R = m.R;
   __shared__ double Phi[3][kMaxR * kMaxR];
@@ -70,42 +128,18 @@ __global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m) {
   __shared__ double bval[kMatchThreads];
   __shared__ long long bidx[kMatchThreads];
   __shared__ int pi_s[kMaxR];
-  extern __shared__ unsigned char anchor[];
+  const int npair = R * R + 2 * R;
   for (int mode = 0; mode < 3; ++mode) {
-    const float* F = mode == 0 ? m.A : mode == 1 ? m.B : m.C;
-    const int32_t* idx = mode == 0 ? m.Is + (int64_t)rep * m.nI
-                       : mode == 1 ? m.Js + (int64_t)rep * m.nJ : m.Ks + (int64_t)rep * m.ks_stride;
-    const int n = mode == 0 ? m.nI : mode == 1 ? m.nJ : m.nKs;
-    const float* U = m.U[mode] + rep * m.u_stride[mode];
-    for (int p = threadIdx.x; p < n; p += blockDim.x) {
-      const float* o = F + (int64_t)idx[p] * R;
-      bool nz = false;
-      for (int f = 0; f < R; ++f) nz |= (o[f] != 0.0f);
-      anchor[p] = nz ? 1 : 0;
-    }
-    __syncthreads();
-    const int npair = R * R + 2 * R;
+    const double* part = m.part + ((int64_t)rep * 3 + mode) * nchunk * npair;
     for (int pr = threadIdx.x; pr < npair; pr += blockDim.x) {
       double s = 0.0;
-      if (pr < R * R) {
-        const int f = pr / R, g = pr - f * R;
-        for (int p = 0; p < n; ++p)
-          if (anchor[p]) s += (double)F[(int64_t)idx[p] * R + f] * (double)U[(int64_t)p * R + g];
-        Phi[mode][pr] = s;
-      } else if (pr < R * R + R) {
-        const int f = pr - R * R;
-        for (int p = 0; p < n; ++p)
-          if (anchor[p]) { const double o = F[(int64_t)idx[p] * R + f]; s += o * o; }
-        al[mode][f] = sqrt(s);
-      } else {
-        const int g = pr - R * R - R;
-        for (int p = 0; p < n; ++p)
-          if (anchor[p]) { const double c = U[(int64_t)p * R + g]; s += c * c; }
-        an[mode][g] = sqrt(s);
-      }
+      for (int c = 0; c < nchunk; ++c) s += part[(int64_t)c * npair + pr];   // chunk order
+      if (pr < R * R) Phi[mode][pr] = s;
+      else if (pr < R * R + R) al[mode][pr - R * R] = sqrt(s);
+      else an[mode][pr - R * R - R] = sqrt(s);
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int pr = threadIdx.x; pr < R * R; pr += blockDim.x) {
     const int f = pr / R, g = pr - f * R;
     double t = 0.0;
@@ -171,9 +205,19 @@ __global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m) {
   }
 }
 
-cudaError_t launch_match(const MatchArgs& m, cudaStream_t st) {
+int match_chunks(const MatchArgs& m) {
   const int nmax = max(m.nI, max(m.nJ, m.nKs));
-  match_kernel<<<m.r, kMatchThreads, (size_t)nmax, st>>>(m);
+  return (nmax + kMatchRows - 1) / kMatchRows;
+}
+
+size_t match_part_doubles(const MatchArgs& m) {
+  return (size_t)m.r * 3 * match_chunks(m) * (m.R * m.R + 2 * m.R);
+}
+
+cudaError_t launch_match(const MatchArgs& m, cudaStream_t st) {
+  const int nchunk = match_chunks(m);
+  match_partial_kernel<<<dim3(nchunk, 3, m.r), kMatchThreads, 0, st>>>(m, nchunk);
+  match_kernel<<<m.r, kMatchThreads, 0, st>>>(m, nchunk);
   return cudaGetLastError();
 }
 

@@ -8,6 +8,8 @@
 // memory stages filled by the bulk-copy engine (cp.async.bulk + mbarrier, one producer
 // thread), so each SM keeps ~100-190 KB of loads in flight with no register cost (a plain
 // ring read of this kind measured 5.7 TB/s on the B200, tools/micro/bw.cu).
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -406,10 +408,20 @@ StreamGeom fit_geom(const DenseView& X, int* gx, int* gy) {
 
 }  // namespace
 
+size_t gram3_ws_doubles(int64_t I, int64_t J, int64_t K, int R) {
+  return gram_part_doubles((int)std::max(I, std::max(J, K)), R, 1);
+}
+
+// Grams of three factors (fp64 [3][R][R]) with tile partials in ws (gram3_ws_doubles).
 cudaError_t launch_gram3(const float* A, const float* B, const float* C, int64_t I, int64_t J,
-                         int64_t K, int R, double* G, cudaStream_t st) {
-  gram3_kernel<<<3, 512, 0, st>>>(A, B, C, I, J, K, R, G);
-  return cudaGetLastError();
+                         int64_t K, int R, double* G, double* ws, cudaStream_t st) {
+  GramArgs g{};
+  g.U[0] = A; g.U[1] = B; g.U[2] = C;
+  g.n[0] = (int)I; g.n[1] = (int)J; g.n[2] = (int)K;
+  g.R = R; g.r = 1;
+  g.tmax = gram_tiles_for((int)std::max(I, std::max(J, K)));
+  g.part = ws; g.G = G; g.g_stride = 3 * R * R;
+  return launch_gram_tiles(g, st);
 }
 
 bool stream_supported(const DenseView& X) {
@@ -440,7 +452,7 @@ cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, 
 size_t fit_stream_ws_doubles(const DenseView& X) {
   int gx, gy;
   fit_geom(X, &gx, &gy);
-  return 2 * (size_t)gx * gy + 3 * kMaxR * kMaxR + 8;
+  return 2 * (size_t)gx * gy + 3 * kMaxR * kMaxR + 8 + gram3_ws_doubles(X.I, X.J, X.K, kMaxR);
 }
 
 template <int RB>
@@ -453,7 +465,8 @@ static cudaError_t fit_stream_rb(const DenseView& X, const float* lam, const flo
   double* part = ws;
   double* G = ws + 2 * (size_t)gx * gy;
   fit_stream_kernel<RB><<<dim3(gx, gy), kST, smem, st>>>(X.base, g, (int)X.J, R, lam, A, B, C, part);
-  gram3_kernel<<<3, 512, 0, st>>>(A, B, C, X.I, X.J, X.K, R, G);
+  cudaError_t e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
+  if (e != cudaSuccess) return e;
   fit_combine_kernel<<<1, 32, 0, st>>>(part, gx * gy, G, lam, R, relerr);
   return cudaGetLastError();
 }

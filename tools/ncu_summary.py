@@ -19,8 +19,8 @@ def launches(path):
     for r in rows[hdr + 1:]:
         if len(r) <= mi:
             continue
-        name = r[ki].split("(")[0]
-        name = name.replace("void ", "").split("<")[0]
+        name = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("void ", "")
+        name = name.split("(")[0].split("<")[0]
         try:
             v = float(r[mi].replace(",", ""))
         except ValueError:
