@@ -161,6 +161,39 @@ SAMBATEN_API sambaten_status sambaten_restore(sambaten_t h);
 SAMBATEN_API void sambaten_destroy(sambaten_t h);
 
 /* ---------------------------------------------------------------------------------------
+ * Sharded update over G ranks (one process per GPU, NCCL, DESIGN.md
+ * "Multi-GPU").  Every rank holds the frontal slices it ingested (its slab of X0 and its
+ * share of every batch); marginals are combined by one int64 allreduce, repetition rho is
+ * decomposed on rank rho mod G from summary slices exchanged by one all-to-all-v, and the
+ * per-repetition results are allgathered before the (replicated) merge.  Dense stores only.
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int rank, world;              /* this process and the number of ranks                     */
+  unsigned char nccl_id[128];   /* from sambaten_dist_unique_id on one rank, broadcast by the */
+                                /* caller's own process-group plumbing                        */
+  int64_t k0;                   /* first global frontal slice of this rank's slab of X0       */
+  int64_t K0_global;            /* mode-3 extent of the whole initial tensor                   */
+} sambaten_dist;
+
+/* A fresh NCCL unique id (128 bytes) for sambaten_dist.nccl_id. */
+SAMBATEN_API sambaten_status sambaten_dist_unique_id(unsigned char id[128]);
+
+/* Collective: every rank passes its slab X0_local (dims[2] slices starting at global slice
+ * dist->k0; the slabs must tile [0, K0_global) exactly) and the same replicated model
+ * (C has K0_global rows).  r must be a multiple of world.  opts->capacity is the GLOBAL
+ * mode-3 capacity.  Errors as sambaten_init_factors, plus E_INVALID for a bad tiling. */
+SAMBATEN_API sambaten_status sambaten_init_factors_dist(sambaten_t* h, const sambaten_tensor* X0_local,
+                                           const sambaten_dist* dist, int R, int s, int r,
+                                           uint64_t seed, const float* A, const float* B,
+                                           const float* C, const float* lambda,
+                                           const sambaten_opts* opts);
+
+/* The slices [K_old + *k_begin, K_old + *k_begin + *k_count) of a batch of K_new slices that
+ * this rank passes to sambaten_update (contiguous, balanced; single-GPU handles: all). */
+SAMBATEN_API sambaten_status sambaten_batch_partition(sambaten_t h, int64_t K_new, int64_t* k_begin,
+                                         int64_t* k_count);
+
+/* ---------------------------------------------------------------------------------------
  * Stateless primitives (device pointers, enqueue on `stream`, no synchronisation).
  * ------------------------------------------------------------------------------------- */
 

@@ -39,6 +39,11 @@ class Opts(C.Structure):
                 ("init_tol", C.c_double), ("stream", C.c_void_p)]
 
 
+class Dist(C.Structure):
+    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_ubyte * 128),
+                ("k0", C.c_int64), ("K0_global", C.c_int64)]
+
+
 class Info(C.Structure):
     _fields_ = [("fit_summary", C.c_double), ("fit_full", C.c_double),
                 ("als_iters_max", C.c_int), ("k_total", C.c_int64),
@@ -90,6 +95,9 @@ def lib():
         "sambaten_fit": (i32, [T, vp, vp, vp, vp, ip, vp, vp]),
         "sambaten_philox": (i32, [u32, u32, u32, u32, u64, i64, vp, vp]),
         "sambaten_detlog": (i32, [vp, i64, vp, vp]),
+        "sambaten_dist_unique_id": (i32, [vp]),
+        "sambaten_init_factors_dist": (i32, [C.POINTER(vp), T, C.POINTER(Dist), ip, ip, ip, u64, vp, vp, vp, vp, O]),
+        "sambaten_batch_partition": (i32, [vp, i64, C.POINTER(i64), C.POINTER(i64)]),
         "sambaten_last_error": (C.c_char_p, []),
         "sambaten_version": (C.c_char_p, []),
     }
@@ -106,6 +114,7 @@ EXPORTED = ["sambaten_default_opts", "sambaten_init", "sambaten_init_factors", "
             "sambaten_checkpoint", "sambaten_restore", "sambaten_destroy",
             "sambaten_fixed_point_scale", "sambaten_marginals", "sambaten_sample", "sambaten_gather",
             "sambaten_mttkrp", "sambaten_cp_als", "sambaten_fit", "sambaten_philox", "sambaten_detlog",
+            "sambaten_dist_unique_id", "sambaten_init_factors_dist", "sambaten_batch_partition",
             "sambaten_last_error", "sambaten_version"]
 
 
@@ -204,6 +213,33 @@ def sambaten_init_factors(X0, R, s, r, seed, A, B, Cm, lam, opts=None):
     check(lib().sambaten_init_factors(C.byref(h), C.byref(X0), R, s, r, seed, ptr(A), ptr(B), ptr(Cm),
                                       ptr(lam), C.byref(opts) if opts else None))
     return h
+
+
+def sambaten_dist_unique_id():
+    buf = (C.c_ubyte * 128)()
+    check(lib().sambaten_dist_unique_id(buf))
+    return bytes(buf)
+
+
+def make_dist(rank, world, nccl_id, k0, K0_global):
+    d = Dist()
+    d.rank, d.world, d.k0, d.K0_global = rank, world, k0, K0_global
+    C.memmove(d.nccl_id, nccl_id, 128)
+    return d
+
+
+def sambaten_init_factors_dist(X0_local, dist, R, s, r, seed, A, B, Cm, lam, opts=None):
+    A, B, Cm, lam = _c_in(A), _c_in(B), _c_in(Cm), _c_in(lam)
+    h = C.c_void_p()
+    check(lib().sambaten_init_factors_dist(C.byref(h), C.byref(X0_local), C.byref(dist), R, s, r, seed, ptr(A),
+                                           ptr(B), ptr(Cm), ptr(lam), C.byref(opts) if opts else None))
+    return h
+
+
+def sambaten_batch_partition(h, K_new):
+    b, n = C.c_int64(), C.c_int64()
+    check(lib().sambaten_batch_partition(h, K_new, C.byref(b), C.byref(n)))
+    return b.value, n.value
 
 
 def sambaten_update(h, batch, A=None, B=None, Cm=None, lam=None):

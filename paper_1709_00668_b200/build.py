@@ -18,17 +18,20 @@ OUT_DIR = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libsambaten.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+NCCL_DIR = os.environ.get("SBT_NCCL_DIR", "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl")
+
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     "--expt-relaxed-constexpr", "-cudart", "static",
     "-I", os.path.join(ROOT, "include"),
+    "-I", os.path.join(NCCL_DIR, "include"),
 ]
 
 
 def _deps_mtime():
-    files = glob.glob(os.path.join(CSRC, "*")) + [os.path.join(ROOT, "include", "sambaten.h")]
+    files = glob.glob(os.path.join(CSRC, "*")) + [os.path.join(ROOT, "include", "sambaten.h")]  # incl. *.inc
     return max(os.path.getmtime(f) for f in files)
 
 
@@ -58,7 +61,9 @@ def build(force=False, verbose=False):
                 print(err)
     objs = [o for o, _ in results]
     tmp = LIB + ".tmp"
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", "-o", tmp, *objs,
+           "-L", os.path.join(NCCL_DIR, "lib"), "-l:libnccl.so.2",
+           "-Xlinker", "-rpath=" + os.path.join(NCCL_DIR, "lib")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -94,8 +94,11 @@ struct HostStatus {        // pinned; filled by one D2H copy at the end of an up
   double relerr;
 };
 
+struct DistState;   // capi_dist.inc
+
 struct sambaten_s {
   int fmt = SAMBATEN_DENSE;
+  DistState* dist = nullptr;   // set for handles of the sharded update (sambaten_init_factors_dist)
   int64_t I = 0, J = 0, K = 0, Kcap = 0, pitch = 0;
   int R = 0, r = 0, s[3] = {1, 1, 1};
   uint64_t seed = 0;
@@ -136,6 +139,7 @@ struct sambaten_s {
   float* lam(int b) const { return C(b) + Kcap * R; }
   size_t model_floats() const { return (size_t)(I + J + Kcap + 1) * R; }
   DenseView view() const { return DenseView{X.as<float>(), I, J, K, pitch}; }
+  DenseView view_local() const;   // the local slab of a sharded handle (capi_dist.inc)
 };
 
 static bool cluster_plan(sambaten_s* h, const DenseAls& a, ClusterPlan* pl) {
@@ -293,9 +297,13 @@ static sambaten_status alloc_store_and_model(sambaten_s* h, const sambaten_tenso
   return SAMBATEN_OK;
 }
 
+static void dist_destroy(DistState* d);
+
 extern "C" void sambaten_destroy(sambaten_t h) {
   if (!h) return;
   cudaStreamSynchronize(h->st);
+  dist_destroy(h->dist);
+  h->dist = nullptr;
   h->X.release();
   h->model[0].release(); h->model[1].release(); h->ck.release();
   h->marg.release(); h->samp.release(); h->summ.release(); h->fac.release();
@@ -841,6 +849,9 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
                        launches, bn, Aout, Bout, Cout, lamout, info);
 }
 
+static sambaten_status update_dense_dist(sambaten_t h, const sambaten_tensor* batch, float* Aout,
+                                         float* Bout, float* Cout, float* lamout, sambaten_info* info);
+
 extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* batch, float* Aout,
                                            float* Bout, float* Cout, float* lamout,
                                            sambaten_info* info) {
@@ -849,6 +860,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   if (batch->fmt != h->fmt) FAIL(SAMBATEN_E_INVALID, "update: batch format differs from the state's");
   if (batch->dims[0] != h->I || batch->dims[1] != h->J)
     FAIL(SAMBATEN_E_SHAPE, "update: batch I x J differs from the state's (S:68)");
+  if (h->dist) return update_dense_dist(h, batch, Aout, Bout, Cout, lamout, info);
   const int64_t Kn = batch->dims[2];
   if (Kn < 1) FAIL(SAMBATEN_E_EMPTY_BATCH, "update: empty batch (S:275)");
   if (h->fmt == SAMBATEN_COO) return update_coo(h, batch, Aout, Bout, Cout, lamout, info);
@@ -951,6 +963,12 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
                        launches, 0, Aout, Bout, Cout, lamout, info);
 }
 
+#include "capi_dist.inc"
+
+DenseView sambaten_s::view_local() const {
+  return DenseView{X.as<float>(), I, J, dist ? dist->K_local : K, pitch};
+}
+
 extern "C" sambaten_status sambaten_get_factors(sambaten_t h, const float** A, const float** B,
                                                 const float** C, const float** lambda,
                                                 int64_t dims[3], int* R) {
@@ -1025,6 +1043,7 @@ extern "C" sambaten_status sambaten_checkpoint(sambaten_t h) {
   CK(cudaStreamSynchronize(h->st));
   h->K_ck = h->K;
   h->nnz_ck = h->nnz;
+  if (h->dist) h->dist->K_local_ck = h->dist->K_local;
   h->uid_ck = h->update_id;
   return SAMBATEN_OK;
 }
@@ -1037,6 +1056,11 @@ extern "C" sambaten_status sambaten_restore(sambaten_t h) {
   CK(cudaStreamSynchronize(h->st));
   h->K = h->K_ck;
   h->nnz = h->nnz_ck;
+  if (h->dist) {
+    h->dist->K_local = h->dist->K_local_ck;
+    h->dist->kmap_h.resize(h->dist->K_local);
+    for (int64_t k = h->K; k < (int64_t)h->dist->owner.size(); ++k) { h->dist->owner[k] = -1; h->dist->kloc[k] = -1; }
+  }
   h->update_id = h->uid_ck;
   return SAMBATEN_OK;
 }

@@ -91,7 +91,7 @@ cudaError_t launch_als_init(const DenseAls& a, uint64_t seed, uint32_t update_id
                             uint32_t rep0, bool init_factors, cudaStream_t st);
 // factor init only (Philox U(0,1) -> fp32, R10) and per-rep state reset
 cudaError_t launch_als_init_factors(const DenseAls& a, uint64_t seed, uint32_t update_id,
-                                    uint32_t rep0, cudaStream_t st);
+                                    uint32_t rep0, cudaStream_t st, uint32_t rep_stride = 1);
 // cluster-per-repetition ALS (k_als_cluster.cu): all iterations in one launch
 struct ClusterPlan { int CS = 0; size_t smem = 0; int act = 0; int RB = 0; int stage_fl = 0; };
 // row pitch (floats) of the summary layouts Y[u][q][p] / Yt[u][p][q] the cluster path reads
@@ -113,6 +113,7 @@ struct MatchArgs {
   const int32_t* Is; const int32_t* Js; const int32_t* Ks;   // [r][nI] ...
   int nI, nJ, nKs, nK;
   int64_t ks_stride;                  // stride between reps' K_s lists (K' rows: nK)
+  int64_t is_stride, js_stride;       // strides between reps' I_s / J_s lists (0 = nI / nJ)
   const float* U[3]; int64_t u_stride[3];
   const double* lamp;                 // [r][R]
   double tau;
@@ -236,6 +237,25 @@ cudaError_t launch_als_gram(const DenseAls& a, cudaStream_t st);
 size_t gram3_ws_doubles(int64_t I, int64_t J, int64_t K, int R);
 cudaError_t launch_gram3(const float* A, const float* B, const float* C, int64_t I, int64_t J,
                          int64_t K, int R, double* G, double* ws, cudaStream_t st);
+
+// ---- distributed data movement (k_dist.cu) ----------------------------------------------
+struct SliceJob { int rep; int32_t k_local; float* dY; float* dYt; };
+struct CopyJob { const float* src; float* dY; float* dYt; };
+struct CopyBytes { const void* src; void* dst; int64_t bytes; };
+cudaError_t launch_multi_copy(const CopyBytes* jobs, int njobs, int64_t max_bytes, cudaStream_t st);
+cudaError_t launch_slice_gather(const DenseView& X, const SliceJob* jobs, int njobs, const int32_t* Is_all,
+                                const int32_t* Js_all, int nI, int nJ, int pI, int pJ, cudaStream_t st);
+cudaError_t launch_slice_copy(const CopyJob* jobs, int njobs, int64_t nY, int64_t nYt, cudaStream_t st);
+cudaError_t launch_x3_scatter(const int64_t* x3l, const int32_t* kmap, int64_t n, int64_t* x3g,
+                              cudaStream_t st);
+// fit partials of a slab: inner/sq summed into out2[0..1] (kmap: local slice -> global row of C)
+cudaError_t launch_fit_stream_partial(const DenseView& X, const float* lam, const float* A, const float* B,
+                                      const float* C, int R, const int32_t* kmap, double* ws,
+                                      double* out2, cudaStream_t st);
+// relerr from the (globally summed) inner/sq and the model's Grams
+cudaError_t launch_fit_finish(const double* in2, const float* lam, const float* A, const float* B,
+                              const float* C, int64_t I, int64_t J, int64_t K, int R, double* ws,
+                              double* relerr, cudaStream_t st);
 
 // k_stream.cu: TMA-ring streaming passes over the dense store (pitch % 4 == 0, 16 B aligned)
 bool stream_supported(const DenseView& X);

@@ -25,13 +25,14 @@ __host__ __device__ inline int rb4(int rb) { return (rb + 3) & ~3; }
 // init: Philox U(0,1) factors rounded to fp32 (R10) and per-rep state
 // ---------------------------------------------------------------------------------------
 __global__ void als_init_kernel(DenseAls a, uint64_t seed, uint32_t update_id, uint32_t rep0,
-                                int init_factors) {
+                                int init_factors, uint32_t rep_stride) {
   const int m = blockIdx.y, rep = blockIdx.z;
   const int n = m == 0 ? a.nI : m == 1 ? a.nJ : a.nK;
   const int64_t tot = (int64_t)n * a.R;
   if (init_factors) {
     float* U = a.U[m] + rep * a.u_stride[m];
-    const uint32_t w3 = ctr_word3(kDomainAlsInit, rep0 + rep, m);
+    // global repetition index (a rank owning reps rank, rank + G, ... passes rep_stride = G)
+    const uint32_t w3 = ctr_word3(kDomainAlsInit, rep0 + rep * rep_stride, m);
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot;
          e += (int64_t)gridDim.x * blockDim.x) {
       const U4 o = philox4x32_10(U4{(uint32_t)e, 0u, update_id, w3}, (uint32_t)seed, (uint32_t)(seed >> 32));
@@ -484,17 +485,17 @@ cudaError_t launch_als_init(const DenseAls& a, uint64_t seed, uint32_t update_id
   const int maxn = max(a.nI, max(a.nJ, a.nK));
   int bx = (int)ceil_div((int64_t)maxn * a.R, 256);
   if (bx > 64) bx = 64;
-  als_init_kernel<<<dim3(bx, 3, a.r), 256, 0, st>>>(a, seed, update_id, rep0, init_factors ? 1 : 0);
+  als_init_kernel<<<dim3(bx, 3, a.r), 256, 0, st>>>(a, seed, update_id, rep0, init_factors ? 1 : 0, 1u);
   gram_kernel<<<dim3(3, a.r), 256, 0, st>>>(a);
   return launch_sumsq_dense(a.Y, a.y_stride, (int64_t)a.nK * a.nJ, a.pitch, a.nI, a.r, a.ysq, st);
 }
 
 cudaError_t launch_als_init_factors(const DenseAls& a, uint64_t seed, uint32_t update_id,
-                                    uint32_t rep0, cudaStream_t st) {
+                                    uint32_t rep0, cudaStream_t st, uint32_t rep_stride) {
   const int maxn = max(a.nI, max(a.nJ, a.nK));
   int bx = (int)ceil_div((int64_t)maxn * a.R, 256);
   if (bx > 64) bx = 64;
-  als_init_kernel<<<dim3(bx, 3, a.r), 256, 0, st>>>(a, seed, update_id, rep0, 1);
+  als_init_kernel<<<dim3(bx, 3, a.r), 256, 0, st>>>(a, seed, update_id, rep0, 1, rep_stride);
   return cudaGetLastError();
 }
 

@@ -75,8 +75,9 @@ __global__ void __launch_bounds__(kMatchThreads) match_partial_kernel(MatchArgs 
   __shared__ float scr[kMatchRows][kMaxR + 1];
   __shared__ unsigned char anc[kMatchRows];
   const float* F = mode == 0 ? m.A : mode == 1 ? m.B : m.C;
-  const int32_t* idx = mode == 0 ? m.Is + (int64_t)rep * m.nI
-                     : mode == 1 ? m.Js + (int64_t)rep * m.nJ : m.Ks + (int64_t)rep * m.ks_stride;
+  const int64_t iss = m.is_stride ? m.is_stride : m.nI, jss = m.js_stride ? m.js_stride : m.nJ;
+  const int32_t* idx = mode == 0 ? m.Is + (int64_t)rep * iss
+                     : mode == 1 ? m.Js + (int64_t)rep * jss : m.Ks + (int64_t)rep * m.ks_stride;
   const int n = mode == 0 ? m.nI : mode == 1 ? m.nJ : m.nKs;
   const float* U = m.U[mode] + rep * m.u_stride[mode];
   const int p0 = chunk * kMatchRows;

@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restr
                                                             const float* __restrict__ A,
                                                             const float* __restrict__ B,
                                                             const float* __restrict__ C,
-                                                            double* __restrict__ part) {
+                                                            double* __restrict__ part,
+                                                            const int32_t* __restrict__ kmap) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned long long bars[kMaxNS];
   __shared__ double red[32];
@@ -239,7 +240,8 @@ __global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restr
       const int r = e / RB, f = e - r * RB;
       int j = j0 + r, k = k0;
       while (j >= J) { j -= J; ++k; }
-      W[e] = f < R ? B[(int64_t)j * R + f] * C[(int64_t)k * R + f] : 0.f;
+      const int64_t kg = kmap ? kmap[k] : k;
+      W[e] = f < R ? B[(int64_t)j * R + f] * C[kg * R + f] : 0.f;
     }
   };
   if (tid == 0) {
@@ -464,10 +466,66 @@ static cudaError_t fit_stream_rb(const DenseView& X, const float* lam, const flo
   cudaFuncSetAttribute(fit_stream_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   double* part = ws;
   double* G = ws + 2 * (size_t)gx * gy;
-  fit_stream_kernel<RB><<<dim3(gx, gy), kST, smem, st>>>(X.base, g, (int)X.J, R, lam, A, B, C, part);
+  fit_stream_kernel<RB><<<dim3(gx, gy), kST, smem, st>>>(X.base, g, (int)X.J, R, lam, A, B, C, part,
+                                                          nullptr);
   cudaError_t e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
   if (e != cudaSuccess) return e;
   fit_combine_kernel<<<1, 32, 0, st>>>(part, gx * gy, G, lam, R, relerr);
+  return cudaGetLastError();
+}
+
+__global__ void sum_pairs_kernel(const double* part, int nb, double* out2) {
+  if (threadIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (int i = 0; i < nb; ++i) { a += part[2 * i]; b += part[2 * i + 1]; }
+  out2[0] = a;
+  out2[1] = b;
+}
+
+__global__ void fit_finish_kernel(const double* in2, const double* G, const float* lam, int R,
+                                  double* relerr) {
+  if (threadIdx.x != 0) return;
+  double mn = 0.0;
+  for (int f = 0; f < R; ++f)
+    for (int g = 0; g < R; ++g)
+      mn += (double)lam[f] * (double)lam[g] * G[f * R + g] * G[R * R + f * R + g] * G[2 * R * R + f * R + g];
+  const double sq = in2[1];
+  const double res = fmax(0.0, sq - 2.0 * in2[0] + mn);
+  *relerr = sq > 0.0 ? sqrt(res / sq) : 0.0;
+}
+
+template <int RB>
+static cudaError_t fit_partial_rb(const DenseView& X, const float* lam, const float* A, const float* B,
+                                  const float* C, int R, const int32_t* kmap, double* ws, double* out2,
+                                  cudaStream_t st) {
+  int gx, gy;
+  StreamGeom g = fit_geom(X, &gx, &gy);
+  const size_t smem = ring_smem(g) + sizeof(float) * 2 * (size_t)g.tr * RB;
+  cudaFuncSetAttribute(fit_stream_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fit_stream_kernel<RB><<<dim3(gx, gy), kST, smem, st>>>(X.base, g, (int)X.J, R, lam, A, B, C, ws, kmap);
+  sum_pairs_kernel<<<1, 32, 0, st>>>(ws, gx * gy, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fit_stream_partial(const DenseView& X, const float* lam, const float* A, const float* B,
+                                      const float* C, int R, const int32_t* kmap, double* ws,
+                                      double* out2, cudaStream_t st) {
+  if (X.K <= 0) {   // nothing stored here
+    return cudaMemsetAsync(out2, 0, 2 * sizeof(double), st);
+  }
+  if (R <= 4) return fit_partial_rb<4>(X, lam, A, B, C, R, kmap, ws, out2, st);
+  if (R <= 8) return fit_partial_rb<8>(X, lam, A, B, C, R, kmap, ws, out2, st);
+  if (R <= 12) return fit_partial_rb<12>(X, lam, A, B, C, R, kmap, ws, out2, st);
+  if (R <= 16) return fit_partial_rb<16>(X, lam, A, B, C, R, kmap, ws, out2, st);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_fit_finish(const double* in2, const float* lam, const float* A, const float* B,
+                              const float* C, int64_t I, int64_t J, int64_t K, int R, double* ws,
+                              double* relerr, cudaStream_t st) {
+  cudaError_t e = launch_gram3(A, B, C, I, J, K, R, ws, ws + 3 * kMaxR * kMaxR, st);
+  if (e != cudaSuccess) return e;
+  fit_finish_kernel<<<1, 32, 0, st>>>(in2, ws, lam, R, relerr);
   return cudaGetLastError();
 }
 

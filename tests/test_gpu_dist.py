@@ -1,0 +1,57 @@
+"""The sharded update (sambaten_init_factors_dist, NCCL) on one GPU: a world-1 handle, with the
+exchange either short-circuited or forced through pack / ncclSend-to-self / ncclRecv /
+unpack (SAMBATEN_DIST_LOOPBACK), must produce the bit-identical model of the single-GPU
+handle on the same inputs (integer marginals, identical summaries, identical ALS)."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ROOT)
+from paper_1709_00668_b200 import _lib as L
+from synth import planted_dense, split_dense
+I, J, K, R, K0, bs = 64, 48, 40, 4, 30, 5
+T, truth = planted_dense(I, J, K, R, noise=0.01, seed=3)
+T0, batches = split_dense(T, K0, bs)
+model = [np.ascontiguousarray(np.asarray(x, np.float32)) for x in (truth[0], truth[1], truth[2], truth[3][:K0])]
+opts = L.default_opts(als_max_iters=15, als_tol=0.0, capacity=K, full_fit=1)
+dist = L.make_dist(0, 1, L.sambaten_dist_unique_id(), 0, K0)
+hd = L.sambaten_init_factors_dist(L.dense(torch.from_numpy(T0).cuda()), dist, R, 2, 4, 9,
+                                  model[1], model[2], model[3], model[0], opts)
+hs = L.sambaten_init_factors(L.dense(torch.from_numpy(T0).cuda()), R, 2, 4, 9,
+                             model[1], model[2], model[3], model[0], opts)
+Kt = K0
+for b in batches:
+    Kt += b.shape[0]
+    assert L.sambaten_batch_partition(hd, b.shape[0]) == (0, b.shape[0])
+    out = []
+    for h in (hd, hs):
+        A = np.empty((I, R), np.float32); B = np.empty((J, R), np.float32)
+        C = np.empty((Kt, R), np.float32); lam = np.empty(R, np.float32)
+        info = L.sambaten_update(h, L.dense(torch.from_numpy(b).cuda()), A, B, C, lam)
+        out.append((A, B, C, lam, info.fit_full, info.reps_rejected_mask))
+    for x, y in zip(out[0][:4], out[1][:4]):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    assert out[0][4] == out[1][4] and out[0][5] == out[1][5]
+L.sambaten_destroy(hd); L.sambaten_destroy(hs)
+print("DIST_OK")
+'''
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_world1_dist_handle_matches_single_gpu_bitwise(loopback):
+    env = dict(os.environ)
+    env.pop("SAMBATEN_DIST_LOOPBACK", None)
+    if loopback:
+        env["SAMBATEN_DIST_LOOPBACK"] = "1"
+    r = subprocess.run([sys.executable, "-c", "ROOT = %r\n" % ROOT + SCRIPT], env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert "DIST_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
