@@ -188,6 +188,16 @@ SAMBATEN_API sambaten_status sambaten_init_factors_dist(sambaten_t* h, const sam
                                            const float* C, const float* lambda,
                                            const sambaten_opts* opts);
 
+/* Host-only (no GPU): the summary-exchange plan of one rank.  Kp: the r K' lists (global
+ * slice indices, rep-major, nKp each); owner_old[k]: rank storing slice k < K_old; the new
+ * slices [K_old, K_old + K_new) are split by sambaten_batch_partition.  Repetition rho is
+ * owned by rank rho % world.  send_slices[g] / recv_slices[g] (world entries each): summary
+ * slices this rank sends to / receives from rank g (0 for g == rank).  Used by the sharded
+ * update; exposed for testing the plan across processes. */
+SAMBATEN_API sambaten_status sambaten_dist_plan(const int32_t* Kp, int r, int64_t nKp,
+                                   const int32_t* owner_old, int64_t K_old, int64_t K_new,
+                                   int world, int rank, int64_t* send_slices, int64_t* recv_slices);
+
 /* The slices [K_old + *k_begin, K_old + *k_begin + *k_count) of a batch of K_new slices that
  * this rank passes to sambaten_update (contiguous, balanced; single-GPU handles: all). */
 SAMBATEN_API sambaten_status sambaten_batch_partition(sambaten_t h, int64_t K_new, int64_t* k_begin,

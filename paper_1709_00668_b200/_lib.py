@@ -98,6 +98,7 @@ def lib():
         "sambaten_dist_unique_id": (i32, [vp]),
         "sambaten_init_factors_dist": (i32, [C.POINTER(vp), T, C.POINTER(Dist), ip, ip, ip, u64, vp, vp, vp, vp, O]),
         "sambaten_batch_partition": (i32, [vp, i64, C.POINTER(i64), C.POINTER(i64)]),
+        "sambaten_dist_plan": (i32, [vp, ip, i64, vp, i64, i64, ip, ip, vp, vp]),
         "sambaten_last_error": (C.c_char_p, []),
         "sambaten_version": (C.c_char_p, []),
     }
@@ -115,6 +116,7 @@ EXPORTED = ["sambaten_default_opts", "sambaten_init", "sambaten_init_factors", "
             "sambaten_fixed_point_scale", "sambaten_marginals", "sambaten_sample", "sambaten_gather",
             "sambaten_mttkrp", "sambaten_cp_als", "sambaten_fit", "sambaten_philox", "sambaten_detlog",
             "sambaten_dist_unique_id", "sambaten_init_factors_dist", "sambaten_batch_partition",
+            "sambaten_dist_plan",
             "sambaten_last_error", "sambaten_version"]
 
 
@@ -234,6 +236,17 @@ def sambaten_init_factors_dist(X0_local, dist, R, s, r, seed, A, B, Cm, lam, opt
     check(lib().sambaten_init_factors_dist(C.byref(h), C.byref(X0_local), C.byref(dist), R, s, r, seed, ptr(A),
                                            ptr(B), ptr(Cm), ptr(lam), C.byref(opts) if opts else None))
     return h
+
+
+def sambaten_dist_plan(Kp, owner_old, K_old, K_new, world, rank):
+    """Host-only exchange plan (no GPU): (send_slices[world], recv_slices[world])."""
+    Kp = np.ascontiguousarray(Kp, np.int32)
+    owner_old = np.ascontiguousarray(owner_old, np.int32)
+    send = np.zeros(world, np.int64)
+    recv = np.zeros(world, np.int64)
+    check(lib().sambaten_dist_plan(ptr(Kp), Kp.shape[0], Kp.shape[1], ptr(owner_old), K_old, K_new, world,
+                                   rank, ptr(send), ptr(recv)))
+    return send, recv
 
 
 def sambaten_batch_partition(h, K_new):

@@ -1,0 +1,179 @@
+"""Multi-process (gloo, CPU) tests of the sharded update's host logic and decomposition.
+
+1. The exchange plan (sambaten_dist_plan, host-only C-ABI call): what every rank plans to send
+   to every owner equals what that owner plans to receive, and every summary slice of every
+   repetition is delivered exactly once (world 2 and 3).
+2. The decomposition itself, run with the oracle's building blocks: slab-local fixed-point
+   marginals summed by an all-reduce equal the full-tensor marginals bit for bit; the
+   per-rank summary slices assembled on the repetition owners equal the full gather; owned
+   repetitions' ALS + all-gather + replicated merge equal the single-process oracle update.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import sambaten as O
+from synth import planted_dense, split_dense
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(world, fn, *args):
+    port = _free_port()
+    mp.spawn(_entry, args=(world, port, fn, args), nprocs=world, join=True)
+
+
+def _entry(rank, world, port, fn, args):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fn(rank, world, *args)
+    finally:
+        dist.destroy_process_group()
+
+
+def partition(Kn, world, rank):
+    base, rem = divmod(Kn, world)
+    return rank * base + min(rank, rem), base + (1 if rank < rem else 0)
+
+
+# --------------------------------------------------------------------------- 1. the plan
+def _plan_worker(rank, world, seed):
+    from paper_1709_00668_b200 import _lib as L
+    rng = np.random.default_rng(seed)
+    Ko, Kn, r, nKs = 53, 7, 6, 11
+    owner = rng.integers(0, world, Ko).astype(np.int32)       # arbitrary ownership of old slices
+    Kp = np.stack([np.concatenate([np.sort(rng.choice(Ko, nKs, replace=False)), np.arange(Ko, Ko + Kn)])
+                   for _ in range(r)]).astype(np.int32)
+    send, recv = L.sambaten_dist_plan(Kp, owner, Ko, Kn, world, rank)
+    mats = [None] * world
+    dist.all_gather_object(mats, (send.tolist(), recv.tolist()))
+    S = np.array([m[0] for m in mats])   # S[g][o]: g sends to o
+    Rv = np.array([m[1] for m in mats])  # Rv[o][g]: o receives from g
+    assert np.array_equal(S, Rv.T)
+    # every (rho, u) is delivered exactly once: local (own) + received = r_owned * nKp
+    def own_of(k):
+        if k < Ko:
+            return owner[k]
+        for g in range(world):
+            b, n = partition(Kn, world, g)
+            if b <= k - Ko < b + n:
+                return g
+    for o in range(world):
+        owned = [rho for rho in range(r) if rho % world == o]
+        local = sum(1 for rho in owned for k in Kp[rho] if own_of(k) == o)
+        assert local + Rv[o].sum() == len(owned) * Kp.shape[1]
+        assert Rv[o][o] == 0
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_exchange_plan_consistent_across_ranks(world):
+    _run(world, _plan_worker, 7)
+
+
+# ------------------------------------------------------------------ 2. the decomposition
+def _update_worker(rank, world, out_path):
+    I, J, K, R, K0, bs = 24, 20, 30, 3, 24, 6
+    T, truth = planted_dense(I, J, K, R, noise=0.01, seed=5)
+    T0, batches = split_dense(T, K0, bs)
+    model = [np.asarray(x, np.float32).astype(np.float64) for x in (truth[0], truth[1], truth[2], truth[3][:K0])]
+    r = 2 * world
+    cfg = O.Config(R=R, s=(2, 2, 2), r=r, seed=3, maxit=8, tol=0.0, tau=0.0)
+    # reference: single-process oracle update
+    ref = O.init_factors(T0, cfg, *(x.astype(np.float32) for x in model), T.size)
+    O.update(ref, batches[0])
+    # sharded: slabs of X0 (contiguous), the batch split by the partition rule
+    b0, n0 = partition(K0, world, rank)
+    Kn = batches[0].shape[0]
+    bb, bn = partition(Kn, world, rank)
+    slab = np.concatenate([T0[b0:b0 + n0], batches[0][bb:bb + bn]])          # local slices
+    kmap = np.concatenate([np.arange(b0, b0 + n0), K0 + np.arange(bb, bb + bn)])
+    st = O.init_factors(T0, cfg, *(x.astype(np.float32) for x in model), T.size)
+    S = st.S
+    # a1: local marginals -> all-reduce (int64)
+    x1, x2, x3l = O.marginals_dense(slab, S, cfg.moi)
+    x3 = np.zeros(K0 + Kn, np.int64)
+    x3[kmap] = x3l
+    buf = torch.from_numpy(np.concatenate([x1, x2, x3]).astype(np.int64))
+    dist.all_reduce(buf)
+    xs = buf.numpy()
+    g1, g2, g3 = O.marginals_dense(np.concatenate([T0, batches[0]]), S, cfg.moi)
+    assert np.array_equal(xs, np.concatenate([g1, g2, g3]))
+    x1, x2, x3 = xs[:I], xs[I:I + J], xs[I + J:]
+    uid = 1
+    owner_of = {int(k): g for g in range(world)
+                for k in np.concatenate([np.arange(*[partition(K0, world, g)[0], sum(partition(K0, world, g))]),
+                                         K0 + np.arange(partition(Kn, world, g)[0], sum(partition(Kn, world, g)))])}
+    local_of = {int(k): i for i, k in enumerate(kmap)}
+    owned = {}
+    parts = {}
+    for rho in range(r):
+        Is = O.sample_mode(x1, O.sample_size(I, 2), cfg.seed, uid, rho, 0)
+        Js = O.sample_mode(x2, O.sample_size(J, 2), cfg.seed, uid, rho, 1)
+        Ks = O.sample_mode(x3[:K0], O.sample_size(K0, 2), cfg.seed, uid, rho, 2)
+        Kp = O.k_prime(Ks, K0, Kn)
+        # a3: the slices of rep rho this rank stores
+        mine = {u: O.gather_dense(slab, Is, Js, np.array([local_of[int(k)]]))[:, :, 0]
+                for u, k in enumerate(Kp) if owner_of[int(k)] == rank}
+        parts[rho] = (Is, Js, Ks, Kp, mine)
+    # exchange (all-gather of the parts stands in for the all-to-all-v)
+    allparts = [None] * world
+    dist.all_gather_object(allparts, {rho: p[4] for rho, p in parts.items()})
+    recs = {}
+    for rho in range(r):
+        if rho % world != rank:
+            continue
+        Is, Js, Ks, Kp, _ = parts[rho]
+        Y = np.empty((len(Is), len(Js), len(Kp)), np.float32)
+        for g in range(world):
+            for u, sl in allparts[g][rho].items():
+                Y[:, :, u] = sl
+        assert np.array_equal(Y, O.gather_dense(np.concatenate([T0, batches[0]]), Is, Js, Kp))
+        U0 = O.als_init((len(Is), len(Js), len(Kp)), R, cfg.seed, uid, rho)
+        lam_p, Up, fit, its, _ = O.cp_als(Y, U0, cfg.maxit, cfg.tol)
+        rm = O.match_rep(st.A, st.B, st.C, Is, Js, Ks, lam_p, Up, cfg.tau)
+        recs[rho] = (Up, rm)
+    allrecs = [None] * world
+    dist.all_gather_object(allrecs, recs)
+    allr = {}
+    for d_ in allrecs:
+        allr.update(d_)
+    # a6: replicated merge in rep order (as O.update)
+    acc = [rho for rho in range(r) if allr[rho][1].accepted]
+    A, B, C = st.A.copy(), st.B.copy(), st.C.copy()
+    for m, (F, key) in enumerate(((A, 0), (B, 1), (C, 2))):
+        tot = np.zeros_like(F); cnt = np.zeros(F.shape[0])
+        for rho in acc:
+            rows = parts[rho][key]
+            Ut = O.rescaled(allr[rho][0], allr[rho][1], m)[:len(rows)]
+            tot[rows] += Ut
+            cnt[rows] += 1.0
+        hit = cnt > 0
+        mean = tot[hit] / cnt[hit][:, None]
+        F[hit] = np.where(F[hit] == 0.0, mean, F[hit])
+    C_new = sum(O.rescaled(allr[rho][0], allr[rho][1], 2)[len(parts[rho][2]):] for rho in acc) / len(acc)
+    lam = (st.lam + sum(allr[rho][1].lam_hat for rho in acc) / len(acc)) / 2.0
+    C = np.vstack([C, C_new])
+    for x, y in zip((lam, A, B, C), (ref.lam, ref.A, ref.B, ref.C)):
+        assert np.array_equal(x, y)
+    if rank == 0:
+        open(out_path, "w").write("ok")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_decomposition_equals_single_process_oracle(world, tmp_path):
+    out = tmp_path / "done"
+    _run(world, _update_worker, str(out))
+    assert out.read_text() == "ok"
