@@ -12,9 +12,12 @@ second per update.  Rank 0 prints one JSON line.
 Timing: W untimed warm-up steps, then K steps, each bracketed by a barrier and a device
 synchronisation and timed with CUDA events on the library's stream; L2 is flushed (a 512 MB
 write) before every step; the stream cycles through the config's batches, restoring the
-K0 checkpoint (untimed) after the last one.  Multi-GPU (torchrun): every rank runs its own
-replica of the update (weak scaling, no data-path collective: DESIGN.md "Multi-GPU") and the
-time is the max over ranks.
+K0 checkpoint (untimed) after the last one.  Multi-GPU (torchrun, dense configs): ONE update
+of the same workload sharded over the N ranks (sambaten_init_factors_dist: time-mode slabs,
+int64 allreduce of the marginals, all-to-all-v of summary slices, repetition rho on rank
+rho mod N, allgather before the replicated merge; DESIGN.md "Multi-GPU") -- strong scaling;
+the time is the max over ranks and `value` counts the batch's entries once.  COO configs at
+N>1 run independent replicas (weak scaling).
 """
 import argparse
 import json
@@ -41,6 +44,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-full-fit", action="store_true", help="return the summary fit only (R21)")
+    p.add_argument("--sharded", action="store_true",
+                   help="use the sharded (NCCL) handle even at N=1 (always used at N>1, dense configs)")
     return p.parse_args()
 
 
@@ -160,6 +165,12 @@ def describe(w):
     return f"{w.name}: {shape}, R={w.R}, s={w.s}, r={w.r}, ALS {w.maxit} it tol {w.tol}"
 
 
+def partition(n, world, rank):
+    """The library's balanced split (sambaten_batch_partition's rule) of n slices."""
+    base, rem = divmod(n, world)
+    return rank * base + min(rank, rem), base + (1 if rank < rem else 0)
+
+
 def threads_used():
     try:
         import threadpoolctl
@@ -247,6 +258,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1709_00668_b200 import _lib as L
 
+    sharded = (world > 1 or args.sharded) and not work.coo
     stream = torch.cuda.Stream()
     # C3's community tensor has no planted model; with R = 15 and 30 summary iterations the
     # acceptance test (R26, tau = 0.9) can reject every repetition, so the COO workloads run
@@ -259,8 +271,24 @@ def main():
         opts.capacity_k = w.K
     else:
         opts.capacity = w.K
-    X0 = work.tensor(L, work.X0, device=True)
-    if work.model is None:
+    local_batches = work.batches
+    if sharded:
+        nid = L.sambaten_dist_unique_id() if rank == 0 else None
+        if world > 1:
+            box = [nid]
+            dist.broadcast_object_list(box, src=0)
+            nid = box[0]
+        k0b, k0n = partition(w.K0, world, rank)
+        X0 = work.tensor(L, work.X0[k0b:k0b + k0n], device=True)
+        dd = L.make_dist(rank, world, nid, k0b, w.K0)
+        h = L.sambaten_init_factors_dist(X0, dd, w.R, w.s, w.r, w.seed, work.model[1], work.model[2],
+                                         work.model[3], work.model[0], opts)
+        parts = [L.sambaten_batch_partition(h, b.shape[0]) for b in work.batches]
+        local_batches = [b[pb:pb + pn] for b, (pb, pn) in zip(work.batches, parts)]
+        config["parallelism"] = f"sharded over {world} rank(s): time-mode slabs, rep rho on rank rho mod {world}"
+        config["slab"] = [k0b, k0n]
+    elif work.model is None:
+        X0 = work.tensor(L, work.X0, device=True)
         opts.init_max_iters = 50
         h = L.sambaten_init(X0, w.R, w.s, w.r, w.seed, opts)
         m = [np.empty(w.R, np.float32), np.empty((w.I, w.R), np.float32), np.empty((w.J, w.R), np.float32),
@@ -268,11 +296,14 @@ def main():
         L.sambaten_copy_factors(h, m[1], m[2], m[3], m[0])
         work.model = m                  # the oracle baseline starts from the same model
     else:
+        X0 = work.tensor(L, work.X0, device=True)
         h = L.sambaten_init_factors(X0, w.R, w.s, w.r, w.seed, work.model[1], work.model[2],
                                     work.model[3], work.model[0], opts)
+    if world > 1 and not sharded:
+        config["parallelism"] = f"{world} independent replicas"
     L.sambaten_checkpoint(h)
-    dbatches = [work.tensor(L, b, device=True) for b in work.batches]
-    hbatches = [work.tensor(L, b, device=False, pin=True) for b in work.batches]
+    dbatches = [work.tensor(L, b, device=True) for b in local_batches]
+    hbatches = [work.tensor(L, b, device=False, pin=True) for b in local_batches]
     out_A = torch.empty((w.I, w.R), dtype=torch.float32).pin_memory()
     out_B = torch.empty((w.J, w.R), dtype=torch.float32).pin_memory()
     out_C = torch.empty((w.K, w.R), dtype=torch.float32).pin_memory()
@@ -301,6 +332,16 @@ def main():
         torch.cuda.synchronize()
         return ev0.elapsed_time(ev1), info, work.entries[i % nb], i % nb
 
+    # priming (untimed, before the W warm-up steps): one pass over every batch through both
+    # entry points, so first-use costs (lazy kernel loading, per-shape ALS plans, workspace
+    # growth as K grows) are paid before timing; then back to the K0 checkpoint
+    for host in (False, True):
+        for i in range(nb):
+            with torch.cuda.stream(stream):
+                L.sambaten_update(h, hbatches[i] if host else dbatches[i],
+                                  *((out_A, out_B, out_C, out_l) if host else ()))
+        L.sambaten_restore(h)
+    torch.cuda.synchronize()
     for _ in range(args.warmup):
         step()
     clk = ClockSampler(local)
@@ -322,20 +363,26 @@ def main():
             ms, _, ne, bi = step(host=True)
             e2e_times.append(ms)
             e2e_ents.append(ne)
-            e2e_in.append(work.bytes_in(bi))
+            e2e_in.append(int(local_batches[bi].size * 4) if sharded else work.bytes_in(bi))
     tot = sum(times) / 1000.0
     e2e_tot = sum(e2e_times) / 1000.0 if e2e_times else None
     if world > 1:
         t = torch.tensor([tot, e2e_tot or 0.0], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot, e2e_tot = float(t[0]), (float(t[1]) if e2e_times else None)
-    value = world * sum(ents) / tot
+    reps = 1 if sharded else world      # replicas each ingest the whole batch
+    value = reps * sum(ents) / tot
 
     peaks, peak_kind = measured_peaks()
     # dominant HBM-bound kernel of the step: the marginal pass a1 (one read of the whole tensor)
     a1_ms = statistics.mean(inf["step_ms"][1] for inf in infos)
     Kavg = statistics.mean(inf["k_total"] for inf in infos)
-    if not work.coo:
+    if sharded:
+        # this rank's slab: its share of X0 plus its share of every batch ingested so far
+        kl = [k0n + sum(parts[j][1] for j in range((i % nb) + 1)) for i in range(args.warmup, args.warmup + args.steps)]
+        a1_bytes = 4.0 * w.I * w.J * statistics.mean(kl) + 8.0 * (w.I + w.J + Kavg)
+        kname = "marg_stream_kernel (a1, local slab)"
+    elif not work.coo:
         a1_bytes = 4.0 * w.I * w.J * Kavg + 8.0 * (w.I + w.J + Kavg)
         kname = "marg_stream_kernel (a1)"
     else:
@@ -354,8 +401,9 @@ def main():
     step_share = {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in infos) for k in range(8)}
     line = {
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "warmup": args.warmup, "ms_per_step": 1000.0 * tot / args.steps,
+        "ms_per_step_min_max": [min(times), max(times)], "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded numpy generators; DESIGN.md 'Synthetic inputs')",
         "config": config,
         "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved,
@@ -372,7 +420,7 @@ def main():
     if e2e_tot:
         hb = int(statistics.mean(e2e_in))
         db = 4 * (w.I + w.J + w.K + 1) * w.R
-        line["e2e"] = {"value": world * sum(e2e_ents) / e2e_tot, "unit": unit,
+        line["e2e"] = {"value": reps * sum(e2e_ents) / e2e_tot, "unit": unit,
                        "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         model = work.model

@@ -72,10 +72,19 @@ struct DevBuf {
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
-    cudaError_t e = cudaMalloc(&p, b);
-    if (e == cudaSuccess) bytes = b;
+    // growth by small steps (K grows with every batch) reallocates once per ~12%, not per call
+    size_t want = grown ? ((b + b / 8 + 255) & ~(size_t)255) : b;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess && want > b) {
+      cudaGetLastError();
+      want = b;
+      e = cudaMalloc(&p, want);
+    }
+    if (e == cudaSuccess) bytes = want;
+    grown = true;
     return e;
   }
+  bool grown = false;
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -152,9 +161,9 @@ static bool cluster_plan(sambaten_s* h, const DenseAls& a, ClusterPlan* pl) {
   sambaten_s::PlanEntry e{a.nI, a.nJ, a.nK, a.R, a.r, false, ClusterPlan{}};
   e.ok = plan_als_cluster(a, &e.pl);
   if (getenv("SAMBATEN_DEBUG"))
-    fprintf(stderr, "[sambaten] cluster ALS plan nI=%d nJ=%d nK=%d R=%d r=%d -> ok=%d CS=%d smem=%zu act=%d RB=%d stage_fl=%d\n",
+    fprintf(stderr, "[sambaten] cluster ALS plan nI=%d nJ=%d nK=%d R=%d r=%d -> ok=%d CS=%d smem=%zu act=%d RB=%d stage_fl=%d dsh=%d\n",
             a.nI, a.nJ, a.nK, a.R, a.r, (int)e.ok, e.pl.CS, e.pl.smem, e.pl.act, e.pl.RB,
-            e.pl.stage_fl);
+            e.pl.stage_fl, e.pl.dsh);
   h->plans.push_back(e);
   *pl = e.pl;
   return e.ok;

@@ -43,7 +43,7 @@ constexpr int kCW = kCT / 32;     // warps per CTA
 constexpr int kTS = 3;            // TMA stages per team
 
 struct ClLayout {
-  size_t G, Gp, Gs, Vi, W1, lam, sc, bars, P, Xun, Xun2, Msh, U0s, U1s, U2s, stage, total;
+  size_t G, Gp, Gs, Vi, W1, lam, sc, bars, P, Xun, Xun2, Msh, U0s, U1s, U2s, Dsh, stage, total;
   int chunk0, chunk1, ownK, stage_fl, T, NT;
 };
 
@@ -62,8 +62,9 @@ __host__ __device__ inline void cl_teams(int nI, int nJ, int* T, int* NT) {
 
 // Shared-memory layout; identical on host (sizing) and device.
 // nt_cap: at most this many teams (no more than a CTA has slices).
+// dsh: D of the own slices (ownK x nJ x RB fp32) in shared memory instead of global.
 __host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, int CS, int stage_fl,
-                                              int nt_cap = 16) {
+                                              int dsh, int nt_cap = 16) {
   ClLayout L{};
   L.chunk0 = (nI + CS - 1) / CS;
   L.chunk1 = (nJ + CS - 1) / CS;
@@ -90,6 +91,7 @@ __host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, in
   L.U0s = take(sizeof(float) * (size_t)nI * RB);
   L.U1s = take(sizeof(float) * (size_t)nJ * RB);
   L.U2s = take(sizeof(float) * (size_t)L.ownK * RB);
+  L.Dsh = take(dsh ? sizeof(float) * (size_t)L.ownK * nJ * RB : 0);
   // per-team TMA rings (kTS stages of whole rows, at least one row of the wider layout); the
   // rings double as the end-of-pass reduction buffer (4 * RB * kCT floats)
   const int rowmax = pitch4(nI > nJ ? nI : nJ);
@@ -278,6 +280,9 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
                                        int stage_fl, unsigned long long* bars, int T, int NT,
                                        unsigned tseq, float* Dg, double* P) {
   const int tid = threadIdx.x;
+#ifdef SBT_ALS_PHASES
+  const long long tp0 = clock64();
+#endif
   const int team = tid / T, lt = tid - team * T;
   const bool in_team = team < NT;
   const bool valid = in_team && 4 * lt < pitch;
@@ -312,7 +317,13 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
     const int r0 = k * tr, nr = min(tr, nrow - r0);
     const unsigned buf = (tseq + s) % kTS;
     if (!PASSB && k == 0) ld_row<RB>(U2s + ul * RB, u2);
+#ifdef SBT_ALS_PHASES
+    const long long tw0 = clock64();
+#endif
     mbar_wait(&tb[buf], ((tseq + s) / kTS) & 1u);
+#ifdef SBT_ALS_PHASES
+    if (tid == 0 && blockIdx.x == 0) atomicAdd(&g_als_phase[PASSB ? 17 : 16], (unsigned long long)(clock64() - tw0));
+#endif
     if (valid) {
       const float* st = ring + buf * stage_fl + 4 * lt;
       const float* wr = Uw + r0 * RB;
@@ -355,6 +366,9 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
       issue(s + kTS);
     }
   }
+#ifdef SBT_ALS_PHASES
+  if (tid == 0 && blockIdx.x == 0) atomicAdd(&g_als_phase[PASSB ? 19 : 18], (unsigned long long)(clock64() - tp0));
+#endif
   if (!PASSB) {
     __syncthreads();   // every team done: rings free (no copy in flight) -> reduction buffer
     float* red = rings;
@@ -388,13 +402,13 @@ __device__ __forceinline__ int team_stages(int team, int nu, int NT, int nrow, i
 
 template <int RB>
 __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS, float* Dglob,
-                                                             int stage_fl) {
+                                                             int stage_fl, int dsh) {
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int rep = blockIdx.x / CS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int R = a.R, nI = a.nI, nJ = a.nJ, nK = a.nK;
-  const ClLayout Ly = cl_layout(nI, nJ, nK, RB, CS, stage_fl);
+  const ClLayout Ly = cl_layout(nI, nJ, nK, RB, CS, stage_fl, dsh);
   extern __shared__ __align__(16) unsigned char smem[];
   double* G = reinterpret_cast<double*>(smem + Ly.G);        // [3][RB*RB] normalised Grams (R-stride)
   double* Gp = reinterpret_cast<double*>(smem + Ly.Gp);      // [3][RB*RB] partial Grams (exported)
@@ -428,7 +442,8 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
   // own regions of the two layouts (16 B aligned: pitches and y_stride are multiples of 4)
   const float* regA = Y + (int64_t)u0 * nJ * pI;
   const float* regB = Yt + (int64_t)u0 * nI * pJ;
-  float* D = Dglob + ((int64_t)rep * nK + u0) * nJ * RB;   // D of the own slices (L2-resident)
+  // D of the own slices: shared memory when it fits (plan), else global (L2-resident)
+  float* D = dsh ? reinterpret_cast<float*>(smem + Ly.Dsh) : Dglob + ((int64_t)rep * nK + u0) * nJ * RB;
   const int myteam = tid / Ly.T;
   unsigned tseq = 0;                                       // TMA stages this team consumed
   float* gU0 = a.U[0] + rep * a.u_stride[0];
@@ -734,15 +749,23 @@ static bool plan_rb(const DenseAls& a, ClusterPlan* pl) {
   bool found = false;
   for (int CS = 16; CS >= 1; --CS) {
     if (CS > a.nK) continue;
-    const ClLayout L0 = cl_layout(a.nI, a.nJ, a.nK, RB, CS, 4);
-    const size_t fixed = L0.stage;   // the rings are the last region of the layout
-    if (fixed + sizeof(float) * 2 * RB * kCT > kSmemCap) continue;
-    const int slice_fl = pitch4(a.nI > a.nJ ? a.nI : a.nJ) * (a.nI > a.nJ ? a.nJ : a.nI);
-    int sfl = (int)((kSmemCap - fixed) / (sizeof(float) * kTS * L0.NT)) & ~3;
-    if (sfl > ((slice_fl + 3) & ~3)) sfl = (slice_fl + 3) & ~3;
-    if (sfl > 12288) sfl = 12288;
-    ClLayout L = cl_layout(a.nI, a.nJ, a.nK, RB, CS, sfl);
-    if (L.total > kSmemCap) continue;
+    // D in shared memory when the rings keep stages of >= 4 rows of the wider layout
+    const int rowmax = pitch4(a.nI > a.nJ ? a.nI : a.nJ);
+    const int slice_fl = rowmax * (a.nI > a.nJ ? a.nJ : a.nI);
+    ClLayout L{};
+    int dsh = -1;
+    for (int d = getenv("SAMBATEN_ALS_GLOBAL_D") ? 0 : 1; d >= 0 && dsh < 0; --d) {
+      const ClLayout L0 = cl_layout(a.nI, a.nJ, a.nK, RB, CS, 4, d);
+      const size_t fixed = L0.stage;   // the rings are the last region of the layout
+      if (fixed + sizeof(float) * 4 * RB * kCT > kSmemCap) continue;
+      int sfl = (int)((kSmemCap - fixed) / (sizeof(float) * kTS * L0.NT)) & ~3;
+      if (sfl > ((slice_fl + 3) & ~3)) sfl = (slice_fl + 3) & ~3;
+      if (sfl > 12288) sfl = 12288;
+      if (d == 1 && sfl < 4 * rowmax) continue;
+      L = cl_layout(a.nI, a.nJ, a.nK, RB, CS, sfl, d);
+      if (L.total <= kSmemCap) dsh = d;
+    }
+    if (dsh < 0) continue;
     if (cluster_setup<RB>(CS, L.total) != cudaSuccess) { cudaGetLastError(); continue; }
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute attr[1];
@@ -764,8 +787,8 @@ static bool plan_rb(const DenseAls& a, ClusterPlan* pl) {
     const double rate = (double)(busy * wpt < 8 ? busy * wpt : 8) / wpt;   // slices in parallel
     const double t = waves * (double)nu / rate + 1e-3 * waves + 1e-5 * CS;
     if (getenv("SAMBATEN_DEBUG"))
-      fprintf(stderr, "[sambaten]   plan candidate CS=%d act=%d nu=%d NT=%d T=%d smem=%zu t=%.3f\n",
-              CS, act, nu, L.NT, L.T, L.total, t);
+      fprintf(stderr, "[sambaten]   plan candidate CS=%d act=%d nu=%d NT=%d T=%d smem=%zu dsh=%d sfl=%d t=%.3f\n",
+              CS, act, nu, L.NT, L.T, L.total, dsh, L.stage_fl, t);
     if (t < best) {
       best = t;
       found = true;
@@ -774,6 +797,7 @@ static bool plan_rb(const DenseAls& a, ClusterPlan* pl) {
       pl->act = act;
       pl->RB = RB;
       pl->stage_fl = L.stage_fl;
+      pl->dsh = dsh;
     }
   }
   return found;
@@ -792,7 +816,7 @@ bool plan_als_cluster(const DenseAls& a, ClusterPlan* pl) {
 }
 
 size_t als_cluster_dscratch_bytes(const DenseAls& a, const ClusterPlan& pl) {
-  return sizeof(float) * (size_t)a.r * ((size_t)a.nK + pl.CS) * a.nJ * pl.RB;
+  return pl.dsh ? 16 : sizeof(float) * (size_t)a.r * ((size_t)a.nK + pl.CS) * a.nJ * pl.RB;
 }
 
 int cluster_pitch(int n) { return pitch4(n); }
@@ -803,7 +827,7 @@ void als_phase_dump() {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(h, g_als_phase, sizeof(h));
   fprintf(stderr, "[sambaten] als phases (cycles, rank 0 of rep 0):");
-  for (int k = 0; k < 16; ++k) fprintf(stderr, " %d:%llu", k, h[k]);
+  for (int k = 0; k < 20; ++k) fprintf(stderr, " %d:%llu", k, h[k]);
   fprintf(stderr, "\n");
   memset(h, 0, sizeof(h));
   cudaMemcpyToSymbol(g_als_phase, h, sizeof(h));
@@ -818,7 +842,7 @@ static cudaError_t cluster_launch(const DenseAls& a, const ClusterPlan& pl, floa
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[1];
   fill_cfg(&cfg, attr, pl.CS, a.r, pl.smem, st);
-  return cudaLaunchKernelEx(&cfg, als_cluster_kernel<RB>, a, pl.CS, Dglob, pl.stage_fl);
+  return cudaLaunchKernelEx(&cfg, als_cluster_kernel<RB>, a, pl.CS, Dglob, pl.stage_fl, pl.dsh);
 }
 
 cudaError_t run_als_cluster(const DenseAls& a, const ClusterPlan& pl, float* Dglob, cudaStream_t st) {
