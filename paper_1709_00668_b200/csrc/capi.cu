@@ -51,7 +51,7 @@ static size_t fit_ws_doubles_any(const DenseView& V) {
 }
 static cudaError_t fit_any(const DenseView& V, const float* lam, const float* A, const float* B,
                            const float* C, int R, double* ws, double* relerr, cudaStream_t st) {
-  if (stream_supported(V) && R <= 16) return launch_fit_stream(V, lam, A, B, C, R, ws, relerr, st);
+  if (fit_stream_supported(V, R)) return launch_fit_stream(V, lam, A, B, C, R, ws, relerr, st);
   return launch_fit_dense(V, lam, A, B, C, R, ws, relerr, st);
 }
 
@@ -93,6 +93,12 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
 struct HostStatus {        // pinned; filled by one D2H copy at the end of an update
   unsigned long long maxphi_bits;
   unsigned vflags;
@@ -109,6 +115,7 @@ struct sambaten_s {
   int fmt = SAMBATEN_DENSE;
   DistState* dist = nullptr;   // set for handles of the sharded update (sambaten_init_factors_dist)
   int64_t I = 0, J = 0, K = 0, Kcap = 0, pitch = 0;
+  bool X_borrowed = false;   // opts.borrow_store: X is the caller's buffer
   int R = 0, r = 0, s[3] = {1, 1, 1};
   uint64_t seed = 0;
   uint32_t update_id = 0;
@@ -260,10 +267,24 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
 static sambaten_status alloc_store_and_model(sambaten_s* h, const sambaten_tensor* X0) {
   if (h->fmt == SAMBATEN_DENSE) {
     const size_t store = (size_t)h->Kcap * h->J * h->pitch * sizeof(float);
-    CK(h->X.ensure(store));
-    CK(cudaMemsetAsync(h->X.p, 0, store, h->st));
-    CK(cudaMemcpy2DAsync(h->X.p, h->pitch * sizeof(float), X0->vals, h->I * sizeof(float),
-                         h->I * sizeof(float), h->J * h->K, cudaMemcpyDefault, h->st));
+    if (h->opts.borrow_store) {
+      // the caller's device buffer becomes the store (X0 in place, room for Kcap slices)
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, X0->vals) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        FAIL(SAMBATEN_E_INVALID, "init: borrow_store needs X0 in device memory");
+      }
+      if (h->pitch != h->I) FAIL(SAMBATEN_E_INVALID, "init: borrow_store needs I % 4 == 0");
+      if (h->opts.capacity <= 0) FAIL(SAMBATEN_E_INVALID, "init: borrow_store needs opts.capacity (slices in the buffer)");
+      h->X.p = const_cast<float*>(X0->vals);
+      h->X.bytes = store;
+      h->X_borrowed = true;
+    } else {
+      CK(h->X.ensure(store));
+      CK(cudaMemsetAsync(h->X.p, 0, store, h->st));
+      CK(cudaMemcpy2DAsync(h->X.p, h->pitch * sizeof(float), X0->vals, h->I * sizeof(float),
+                           h->I * sizeof(float), h->J * h->K, cudaMemcpyDefault, h->st));
+    }
   } else {
     CK(h->X.ensure((size_t)h->nnz_cap * (3 * sizeof(int32_t) + sizeof(float))));
     const size_t n = (size_t)h->nnz;
@@ -313,6 +334,7 @@ extern "C" void sambaten_destroy(sambaten_t h) {
   cudaStreamSynchronize(h->st);
   dist_destroy(h->dist);
   h->dist = nullptr;
+  if (h->X_borrowed) h->X.p = nullptr;   // the caller's buffer: not ours to free
   h->X.release();
   h->model[0].release(); h->model[1].release(); h->ck.release();
   h->marg.release(); h->samp.release(); h->summ.release(); h->fac.release();
@@ -884,15 +906,22 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   CK(cudaEventRecord(h->ev[0], st));
   // ---- a0: ingest into the preallocated capacity (not visible until commit) --------------
   float* dst = h->X.as<float>() + Ko * h->J * h->pitch;
-  CK(cudaMemcpy2DAsync(dst, h->pitch * sizeof(float), batch->vals, h->I * sizeof(float),
-                       h->I * sizeof(float), h->J * Kn, cudaMemcpyDefault, st));
   CK(h->misc.ensure(4096));
   unsigned long long* d_maxphi = h->misc.as<unsigned long long>();
   double* d_relerr = reinterpret_cast<double*>(h->misc.as<char>() + 64);
   CK(cudaMemsetAsync(d_maxphi, 0, 8, st));
   DenseView V = h->view();
   V.K = Ko + Kn;
-  CK(launch_max_phi_dense(V, Ko, Kn, h->opts.moi, d_maxphi, st));
+  const int64_t nb_fl = h->I * h->J * Kn;
+  if (h->pitch == h->I && nb_fl % 4 == 0 && is_device_ptr(batch->vals) &&
+      (((uintptr_t)batch->vals | (uintptr_t)dst) & 15) == 0) {
+    // device batch, contiguous store: one pass copies and tracks max |x|
+    CK(launch_ingest_dense(batch->vals, dst, nb_fl, h->opts.moi, d_maxphi, st));
+  } else {
+    CK(cudaMemcpy2DAsync(dst, h->pitch * sizeof(float), batch->vals, h->I * sizeof(float),
+                         h->I * sizeof(float), h->J * Kn, cudaMemcpyDefault, st));
+    CK(launch_max_phi_dense(V, Ko, Kn, h->opts.moi, d_maxphi, st));
+  }
   CK(cudaEventRecord(h->ev[1], st));
   // ---- a1: marginals over X_old U X_new (R2, R3) ----------------------------------------
   const size_t marg_bytes = sizeof(int64_t) * (h->I + h->J + h->Kcap);

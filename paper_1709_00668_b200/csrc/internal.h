@@ -33,6 +33,9 @@ cudaError_t launch_marginals_coo(const int32_t* i, const int32_t* j, const int32
                                  int64_t* x2, int64_t* x3, cudaStream_t st);
 // max phi over a dense view (slices [k0,k0+nk)) or COO values; result as double bits in
 // *out (callers zero it; phi >= 0 so the bit pattern is monotone).
+// a0 fused copy + max |x| of a contiguous device batch (n floats, n % 4 == 0, 16 B aligned)
+cudaError_t launch_ingest_dense(const float* src, float* dst, int64_t n, int moi, unsigned long long* out,
+                                cudaStream_t st);
 cudaError_t launch_max_phi_dense(const DenseView& X, int64_t k0, int64_t nk, int moi,
                                  unsigned long long* out, cudaStream_t st);
 cudaError_t launch_max_phi_vals(const float* v, int64_t n, int moi, unsigned long long* out,
@@ -259,6 +262,7 @@ cudaError_t launch_fit_finish(const double* in2, const float* lam, const float* 
 
 // k_stream.cu: TMA-ring streaming passes over the dense store (pitch % 4 == 0, 16 B aligned)
 bool stream_supported(const DenseView& X);
+bool fit_stream_supported(const DenseView& X, int R);
 cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
                                     int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st);
 size_t fit_stream_ws_doubles(const DenseView& X);

@@ -281,20 +281,53 @@ __device__ __forceinline__ double phi_d(float x) {
   return MOI == 0 ? fabs(d) : d * d;
 }
 
+// max phi(x) = phi(max |x|) (phi monotone in |x|): the scan keeps max |x| in fp32 (exact) and
+// converts once.  Rows (pitch-strided) are walked by a warp each, float4 when aligned.
+template <int MOI>
+__device__ __forceinline__ void flush_max(float mx, unsigned long long* out) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const double m = phi_d<MOI>(mx);
+  if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
 template <int MOI>
 __global__ void max_phi_dense_kernel(const float* __restrict__ X, int64_t pitch, int64_t I,
                                      int64_t row0, int64_t nrows, unsigned long long* out) {
-  double m = 0.0;
-  const int64_t total = nrows * I;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / I, col = e - row * I;
-    m = fmax(m, phi_d<MOI>(X[(row0 + row) * pitch + col]));
+  float mx = 0.f;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec = (pitch % 4) == 0 && (((uintptr_t)X) & 15) == 0;
+  for (int64_t row = wid; row < nrows; row += nw) {
+    const float* p = X + (row0 + row) * pitch;
+    if (vec) {
+      const int64_t n4 = I / 4;
+      for (int64_t c = lane; c < n4; c += 32) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(p) + c);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+      for (int64_t c = 4 * n4 + lane; c < I; c += 32) mx = fmaxf(mx, fabsf(p[c]));
+    } else {
+      for (int64_t c = lane; c < I; c += 32) mx = fmaxf(mx, fabsf(p[c]));
+    }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0 && m > 0.0)
-    atomicMax(out, (unsigned long long)__double_as_longlong(m));
+  flush_max<MOI>(mx, out);
+}
+
+// a0 fused: copy a contiguous device batch into the store (contiguous: pitch == I) and
+// track max |x| in the same pass (16 B vectors; n4 = floats / 4).
+template <int MOI>
+__global__ void ingest_dense_kernel(const float4* __restrict__ src, float4* __restrict__ dst, int64_t n4,
+                                    unsigned long long* out) {
+  float mx = 0.f;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldcs(src + e);
+    __stcg(dst + e, v);
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  flush_max<MOI>(mx, out);
 }
 
 template <int MOI>
@@ -309,11 +342,24 @@ __global__ void max_phi_vals_kernel(const float* __restrict__ v, int64_t n, unsi
     atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+cudaError_t launch_ingest_dense(const float* src, float* dst, int64_t n, int moi, unsigned long long* out,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = ceil_div(n / 4, 256);
+  if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
+  if (blocks < 1) blocks = 1;
+  auto* s4 = reinterpret_cast<const float4*>(src);
+  auto* d4 = reinterpret_cast<float4*>(dst);
+  if (moi == 0) ingest_dense_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(s4, d4, n / 4, out);
+  else ingest_dense_kernel<1><<<(unsigned)blocks, 256, 0, st>>>(s4, d4, n / 4, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_max_phi_dense(const DenseView& X, int64_t k0, int64_t nk, int moi,
                                  unsigned long long* out, cudaStream_t st) {
   const int64_t nrows = nk * X.J;
   if (nrows <= 0) return cudaSuccess;
-  int64_t blocks = ceil_div(nrows * X.I, 256);
+  int64_t blocks = ceil_div(nrows, 8);   // a warp per row, 8 warps per block
   if (blocks > kNumSMs * 8) blocks = kNumSMs * 8;
   if (moi == 0)
     max_phi_dense_kernel<0><<<(unsigned)blocks, 256, 0, st>>>(X.base, X.pitch, X.I, k0 * X.J, nrows, out);

@@ -51,26 +51,23 @@ struct StreamGeom {
   int ncol;                 // real columns (I)
   int tr;                   // rows per stage
   int ns;                   // stages in the ring (<= kMaxNS)
+  int nch = 1, wpc = 1;     // marginals: column chunks per row and warps per chunk in a CTA
+  int qpt = 1, tpg = 1, ng = 1;   // fit: quads per thread, threads per row group, row groups
+  bool bres = false;              // fit: B resident in shared memory (J x kMaxR floats)
 };
 
 constexpr int kMaxNS = 8;
+constexpr int kWPT = 2;           // fit: W elements per thread per stage
 
-// stage s of this CTA covers rows [rb + s*tr, ...); issued by one thread
-__device__ __forceinline__ void ring_issue(float* ring, unsigned long long* bars, const StreamGeom& g,
-                                           const float* X, int64_t rb, int64_t re, int c0, int s) {
+// marginal stages: whole rows, one bulk copy (rows are contiguous in the store)
+__device__ __forceinline__ void marg_issue(float* ring, unsigned long long* bars, const StreamGeom& g,
+                                           const float* X, int64_t rb, int64_t re, int s) {
   const int64_t r0 = rb + (int64_t)s * g.tr;
   const int nr = (int)min((int64_t)g.tr, re - r0);
   const int slot = s % g.ns;
-  float* dst = ring + (size_t)slot * g.tr * g.cw;
-  const int w = min(g.cw, g.pitch - c0);   // floats copied per row (multiple of 4)
-  const unsigned row_bytes = (unsigned)(w * sizeof(float));
-  s_expect(&bars[slot], row_bytes * nr);
-  if (g.cw == g.pitch) {
-    s_bulk(dst, X + r0 * g.pitch, row_bytes * nr, &bars[slot]);
-  } else {
-    for (int r = 0; r < nr; ++r)
-      s_bulk(dst + (size_t)r * g.cw, X + (r0 + r) * g.pitch + c0, row_bytes, &bars[slot]);
-  }
+  const unsigned bytes = (unsigned)((size_t)nr * g.pitch * sizeof(float));
+  s_expect(&bars[slot], bytes);
+  s_bulk(ring + (size_t)slot * g.tr * g.pitch, X + r0 * g.pitch, bytes, &bars[slot]);
 }
 
 template <int MOI>
@@ -91,7 +88,6 @@ __device__ __forceinline__ long long quant(float x, float scf, double scd) {
 // flushed at the end; x1 is combined across warps in shared memory (one global atomic per
 // column).  Integer sums: exact and independent of the order.
 // ---------------------------------------------------------------------------------------
-constexpr int kX3Win = 64;
 constexpr int kMQ = 4;            // quads per lane: column chunk <= 32 * 4 * 4 = 512 floats
 constexpr int kRPW = 2;           // rows per warp per step
 constexpr int kMargCTAs = 1;      // CTAs per SM
@@ -104,46 +100,46 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
                                                              unsigned long long* __restrict__ x3) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned long long bars[kMaxNS];
-  __shared__ unsigned long long x3w[kX3Win];
-  __shared__ unsigned long long x1s[4 * 32 * kMQ];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c0 = blockIdx.y * g.cw;
+  const int nwarps = blockDim.x >> 5;
+  // stages hold whole rows; warp w works on column chunk w % nch of the rows w / nch,
+  // w / nch + wpc, ... (kRPW at a time)
+  const int chunk = warp % g.nch, wslot = warp / g.nch;
+  const int c0 = chunk * g.cw;
   const int cw_real = min(g.cw, g.ncol - c0);
   const int64_t rb = g.row0 + (int64_t)blockIdx.x * g.rows_per_cta;
   const int64_t re = min(rb + g.rows_per_cta, g.row0 + g.nrows);
   if (rb >= re) return;
   float* ring = reinterpret_cast<float*>(smem);
   const int nst = (int)((re - rb + g.tr - 1) / g.tr);
-  const int64_t kfirst = rb / J;
-  const bool x3_local = ((re - 1) / J - kfirst) < kX3Win;
   if (tid == 0) {
     for (int s = 0; s < g.ns; ++s) s_mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int s = tid; s < kX3Win; s += kST) x3w[s] = 0;
-  for (int s = tid; s < 4 * 32 * kMQ; s += kST) x1s[s] = 0;
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < nst && s < g.ns; ++s) ring_issue(ring, bars, g, X, rb, re, c0, s);
+    for (int s = 0; s < nst && s < g.ns; ++s) marg_issue(ring, bars, g, X, rb, re, s);
   long long acc[kMQ][4];
 #pragma unroll
   for (int m = 0; m < kMQ; ++m)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[m][e] = 0;
+  long long x3run = 0;   // lane 0: running sum of slice x3k
+  int64_t x3k = -1;
   for (int s = 0; s < nst; ++s) {
     const int64_t r0 = rb + (int64_t)s * g.tr;
     const int nr = (int)min((int64_t)g.tr, re - r0);
     const int slot = s % g.ns;
     s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
-    const float* st = ring + (size_t)slot * g.tr * g.cw;
-    for (int rw = warp * kRPW; rw < nr; rw += kNW * kRPW) {
+    const float* st = ring + (size_t)slot * g.tr * g.pitch + c0;
+    for (int rw = wslot * kRPW; rw < nr; rw += g.wpc * kRPW) {
       long long rs[kRPW];
 #pragma unroll
       for (int v = 0; v < kRPW; ++v) {
         rs[v] = 0;
         const int r = rw + v;
         if (r < nr) {
-          const float* rowp = st + (size_t)r * g.cw;
+          const float* rowp = st + (size_t)r * g.pitch;
 #pragma unroll
           for (int m = 0; m < kMQ; ++m) {
             const int col = 4 * (lane + 32 * m);
@@ -164,6 +160,9 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
       for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
         for (int v = 0; v < kRPW; ++v) rs[v] += __shfl_xor_sync(0xffffffffu, rs[v], o);
+      // every lane holds the kRPW row totals: lane v adds row v to x2; lane 0 folds them into
+      // the warp's running x3 sum of slice x3k (flushed when the slice changes: one global
+      // reduction per slice and warp instead of a contended shared 64-bit atomic per row)
       if (lane < kRPW) {
         long long mine = rs[0];
 #pragma unroll
@@ -174,30 +173,49 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
           const int64_t row = r0 + r;
           const int64_t k = row / J, j = row - k * J;
           atomicAdd(&x2[j], (unsigned long long)mine);
-          if (x3_local) atomicAdd(&x3w[k - kfirst], (unsigned long long)mine);
-          else atomicAdd(&x3[k], (unsigned long long)mine);
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int v = 0; v < kRPW; ++v) {
+          const int r = rw + v;
+          if (r < nr) {
+            const int64_t k = (r0 + r) / J;
+            if (k != x3k) {
+              if (x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
+              x3k = k;
+              x3run = 0;
+            }
+            x3run += rs[v];
+          }
         }
       }
     }
     __syncthreads();   // stage consumed by every warp
     if (tid == 0 && s + g.ns < nst) {
       s_fence_async();
-      ring_issue(ring, bars, g, X, rb, re, c0, s + g.ns);
+      marg_issue(ring, bars, g, X, rb, re, s + g.ns);
     }
   }
+  if (lane == 0 && x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
+  // x1: the warps' column sums through the (now idle) ring, summed per column in warp order
+  __syncthreads();
+  long long* xw = reinterpret_cast<long long*>(smem);   // [kNW][cw]
 #pragma unroll
   for (int m = 0; m < kMQ; ++m)
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int col = 4 * (lane + 32 * m) + e;
-      if (col < cw_real && acc[m][e]) atomicAdd(&x1s[col], (unsigned long long)acc[m][e]);
+      if (col < cw_real && warp < g.nch * g.wpc) xw[(size_t)warp * g.cw + col] = acc[m][e];
     }
   __syncthreads();
-  for (int c = tid; c < cw_real; c += kST)
-    if (x1s[c]) atomicAdd(&x1[c0 + c], x1s[c]);
-  if (x3_local)
-    for (int s = tid; s < kX3Win; s += kST)
-      if (x3w[s]) atomicAdd(&x3[kfirst + s], x3w[s]);
+  for (int c = tid; c < g.ncol; c += blockDim.x) {
+    const int ch = c / g.cw, cc = c - ch * g.cw;
+    long long t = 0;
+    for (int w = ch; w < g.nch * g.wpc; w += g.nch) t += xw[(size_t)w * g.cw + cc];
+    if (t) atomicAdd(&x1[c], (unsigned long long)t);
+  }
+  (void)nwarps;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -208,8 +226,16 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
 // stage).  fp32 per element and per stage, fp64 across stages; per-CTA partials reduced in a
 // fixed order by fit_combine_kernel.
 // ---------------------------------------------------------------------------------------
-template <int RB>
-__global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restrict__ X, StreamGeom g,
+// a7 fit: inner = <X, [[lam; A, B, C]]> and ||X||^2 in one pass over whole-row stages.  A
+// thread owns QPT column quads and folds C(k, :) into its registers, alc(i, f) = lam_f A(i,f)
+// C(k,f) (reloaded when the slice k changes), so row (j, k) needs only B(j, :):
+// m(i) = sum_f alc(i,f) B(j,f), inner += X(i,j,k) m(i).  BRES: B (J x RB, zero padded) resident
+// in shared memory; else the B rows of stage s+1 are loaded into registers while stage s is
+// consumed and stored to a double buffer after it.  fp32 per element and stage, fp64 across.
+constexpr int kFitT2 = 384;       // fit: threads per CTA at 2 quads per thread (<= 168 registers)
+
+template <int RB, int QPT, bool BRES>
+__global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) fit_stream_kernel(const float* __restrict__ X, StreamGeom g,
                                                             int J, int R, const float* __restrict__ lam,
                                                             const float* __restrict__ A,
                                                             const float* __restrict__ B,
@@ -219,135 +245,154 @@ __global__ void __launch_bounds__(kST, 1) fit_stream_kernel(const float* __restr
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned long long bars[kMaxNS];
   __shared__ double red[32];
-  const int tid = threadIdx.x;
-  const int c0 = blockIdx.y * g.cw;
-  const int cw_real = min(g.cw, g.ncol - c0);
-  const int NQ = g.cw / 4;
-  const int NG = kST / NQ > 0 ? kST / NQ : 1;
-  const int quad = tid % NQ, grp = tid / NQ;
-  const bool active = grp < NG && tid < NQ * NG;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int nq = g.pitch / 4;
+  const int tq = tid % g.tpg, grp = tid / g.tpg;
+  const bool active = grp < g.ng;
   const int64_t rb = g.row0 + (int64_t)blockIdx.x * g.rows_per_cta;
   const int64_t re = min(rb + g.rows_per_cta, g.row0 + g.nrows);
   float* ring = reinterpret_cast<float*>(smem);
-  float* Wbuf = ring + (size_t)g.ns * g.tr * g.cw;   // [2][tr][RB]
+  float* Wbuf = ring + (size_t)g.ns * g.tr * g.pitch;   // BRES: Bs [J][RB]; else W [2][tr][RB]
   const int nst = rb < re ? (int)((re - rb + g.tr - 1) / g.tr) : 0;
-  auto build_w = [&](int s) {   // W rows of stage s: 32-bit (j,k) walk, no divisions per element
-    float* W = Wbuf + (size_t)(s & 1) * g.tr * RB;
-    const int64_t r0 = rb + (int64_t)s * g.tr;
+  float wb[kWPT];
+  // B rows of the stage starting at row r0 = (j0 of some slice): row r has j = (j0 + r) mod J
+  auto load_w = [&](int64_t r0, int j0) {
     const int nr = (int)min((int64_t)g.tr, re - r0);
-    const int k0 = (int)(r0 / J), j0 = (int)(r0 - (int64_t)k0 * J);
-    for (int e = tid; e < nr * RB; e += kST) {
-      const int r = e / RB, f = e - r * RB;
-      int j = j0 + r, k = k0;
-      while (j >= J) { j -= J; ++k; }
-      const int64_t kg = kmap ? kmap[k] : k;
-      W[e] = f < R ? B[(int64_t)j * R + f] * C[kg * R + f] : 0.f;
+#pragma unroll
+    for (int t = 0; t < kWPT; ++t) {
+      const int e = tid + t * nthr;
+      wb[t] = 0.f;
+      if (e < nr * RB) {
+        const int r = e / RB, f = e - r * RB;
+        int j = j0 + r;
+        if (j >= J) j -= (j / J) * J;
+        if (f < R) wb[t] = __ldg(B + (int64_t)j * R + f);
+      }
+    }
+  };
+  auto store_w = [&](int s) {
+    float* W = Wbuf + (size_t)(s & 1) * g.tr * RB;
+#pragma unroll
+    for (int t = 0; t < kWPT; ++t) {
+      const int e = tid + t * nthr;
+      if (e < g.tr * RB) W[e] = wb[t];
     }
   };
   if (tid == 0) {
     for (int s = 0; s < g.ns; ++s) s_mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (nst > 0) build_w(0);
+  // stage cursor: slice ks and row js of the first row of the current stage (no divisions
+  // in the loop), ring slot and its phase
+  int64_t ks = rb / J;
+  int js = (int)(rb - ks * J);
+  if constexpr (BRES) {
+    for (int e = tid; e < J * RB; e += nthr) {
+      const int j = e / RB, f = e - j * RB;
+      Wbuf[e] = f < R ? B[(int64_t)j * R + f] : 0.f;
+    }
+  } else {
+    if (nst > 0) { load_w(rb, js); store_w(0); }
+  }
   __syncthreads();
   if (tid == 0)
-    for (int s = 0; s < nst && s < g.ns; ++s) ring_issue(ring, bars, g, X, rb, re, c0, s);
-  const int col = 4 * quad;
-  float al[4][RB];
+    for (int s = 0; s < nst && s < g.ns; ++s) marg_issue(ring, bars, g, X, rb, re, s);
+  // lam_f A(i,f) [* C(k,f) when BRES] of the thread's QPT column quads (tq + u * tpg)
+  float al[QPT][4][RB];
+  int64_t kc = -1;
+  auto load_al = [&](int64_t k) {
+    const int64_t kg = kmap ? kmap[k] : k;
 #pragma unroll
-  for (int e = 0; e < 4; ++e)
+    for (int u = 0; u < QPT; ++u)
 #pragma unroll
-    for (int f = 0; f < RB; ++f) {
-      const int i = c0 + col + e;
-      al[e][f] = (active && col + e < cw_real && f < R) ? lam[f] * A[(int64_t)i * R + f] : 0.f;
-    }
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int f = 0; f < RB; ++f) {
+          const int i = 4 * (tq + u * g.tpg) + e;
+          float v = 0.f;
+          if (active && i < g.ncol && f < R) {
+            v = lam[f] * A[(int64_t)i * R + f] * C[kg * R + f];
+          }
+          al[u][e][f] = v;
+        }
+  };
   double inner = 0.0, sq = 0.0;
   for (int s = 0; s < nst; ++s) {
+    const int slot = s % g.ns;
     const int64_t r0 = rb + (int64_t)s * g.tr;
     const int nr = (int)min((int64_t)g.tr, re - r0);
-    const int slot = s % g.ns;
-    if (s + 1 < nst) build_w(s + 1);   // the other W buffer (free since the last barrier)
-    s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
-    if (active && col < cw_real) {
-      const float* st = ring + (size_t)slot * g.tr * g.cw + col;
-      const float* W = Wbuf + (size_t)(s & 1) * g.tr * RB;
+    int jn = js + g.tr;   // the next stage's first row
+    int64_t kn = ks;
+    if (jn >= J) { kn += jn / J; jn -= (jn / J) * J; }
+    if (!BRES && s + 1 < nst) load_w(r0 + g.tr, jn);   // loads in flight while stage s is consumed
+    s_wait(&bars[s % g.ns], (unsigned)(s / g.ns) & 1u);
+    if (active) {
+      const float* st = ring + (size_t)slot * g.tr * g.pitch;
+      const float* W = Wbuf + (BRES ? 0 : (size_t)(s & 1) * g.tr * RB);
       float fi = 0.f, fs = 0.f;
-#pragma unroll 2
-      for (int r = grp; r < nr; r += NG) {
-        const float4 v = *reinterpret_cast<const float4*>(st + (size_t)r * g.cw);
-        const float* w = W + r * RB;
-        float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+      auto rows = [&](int ra, int rb2, int jbase) {   // rows [ra, rb2) of the stage, row r has j = jbase + r - ra
+#pragma unroll 1
+        for (int r = ra + ((grp - ra) % g.ng + g.ng) % g.ng; r < rb2; r += g.ng) {
+          const float* wr = BRES ? W + (size_t)(jbase + r - ra) * RB : W + r * RB;
+          float w[RB];
 #pragma unroll
-        for (int f4 = 0; f4 < RB / 4; ++f4) {
-          const float4 wv = *reinterpret_cast<const float4*>(w + 4 * f4);
-          const float ww[4] = {wv.x, wv.y, wv.z, wv.w};
+          for (int f4 = 0; f4 < RB / 4; ++f4) {
+            const float4 wv = *reinterpret_cast<const float4*>(wr + 4 * f4);
+            w[4 * f4] = wv.x; w[4 * f4 + 1] = wv.y; w[4 * f4 + 2] = wv.z; w[4 * f4 + 3] = wv.w;
+          }
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int f = 4 * f4 + t;
-            m0 = fmaf(al[0][f], ww[t], m0);
-            m1 = fmaf(al[1][f], ww[t], m1);
-            m2 = fmaf(al[2][f], ww[t], m2);
-            m3 = fmaf(al[3][f], ww[t], m3);
+          for (int u = 0; u < QPT; ++u) {
+            const int q = tq + u * g.tpg;
+            if (q < nq) {
+              const float4 v = *reinterpret_cast<const float4*>(st + (size_t)r * g.pitch + 4 * q);
+              float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+#pragma unroll
+              for (int f = 0; f < RB; ++f) {
+                m0 = fmaf(al[u][0][f], w[f], m0);
+                m1 = fmaf(al[u][1][f], w[f], m1);
+                m2 = fmaf(al[u][2][f], w[f], m2);
+                m3 = fmaf(al[u][3][f], w[f], m3);
+              }
+              fi = fmaf(v.x, m0, fmaf(v.y, m1, fmaf(v.z, m2, fmaf(v.w, m3, fi))));
+              // padding columns are zero in the store (and carry al == 0)
+              fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
+            }
           }
         }
-        fi = fmaf(v.x, m0, fmaf(v.y, m1, fmaf(v.z, m2, fmaf(v.w, m3, fi))));
-        // padding columns are zero in the store (and carry al == 0)
-        fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
+      };
+      // segments of the stage with one slice k each; C(k, :) folded into al at a change
+      int64_t k = r0 / J;
+      int j = (int)(r0 - k * J);
+      for (int ra = 0; ra < nr;) {
+        const int seg = min(nr - ra, J - j);
+        if (k != kc) {
+          inner += (double)fi;
+          fi = 0.f;
+          load_al(k);
+          kc = k;
+        }
+        rows(ra, ra + seg, j);
+        ra += seg;
+        j = 0;
+        ++k;
       }
       inner += (double)fi;
       sq += (double)fs;
     }
-    __syncthreads();   // stage and W(s) consumed, W(s+1) complete
+    if (!BRES && s + 1 < nst) store_w(s + 1);   // the other W buffer (free since the last barrier)
+    __syncthreads();   // stage (and W(s)) consumed
     if (tid == 0 && s + g.ns < nst) {
       s_fence_async();
-      ring_issue(ring, bars, g, X, rb, re, c0, s + g.ns);
+      marg_issue(ring, bars, g, X, rb, re, s + g.ns);
     }
+    ks = kn;
+    js = jn;
   }
   inner = block_sum_d(inner, red);
   sq = block_sum_d(sq, red);
   if (tid == 0) {
-    const int64_t b = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-    part[2 * b] = inner;
-    part[2 * b + 1] = sq;
-  }
-}
-
-// Grams of the three factors (fp64, fixed order): block m stages rows of factor m in shared
-// memory; thread (pair, segment) accumulates, segments summed in order.
-__global__ void gram3_kernel(const float* A, const float* B, const float* C, int64_t I, int64_t J,
-                             int64_t K, int R, double* G /* [3][R][R] */) {
-  __shared__ float rows[1024 * 8];
-  __shared__ double segsum[512];
-  const int m = blockIdx.x;
-  const float* U = m == 0 ? A : m == 1 ? B : C;
-  const int64_t n = m == 0 ? I : m == 1 ? J : K;
-  const int npair = R * (R + 1) / 2;
-  const int nseg = blockDim.x / npair > 0 ? blockDim.x / npair : 1;
-  const int pair = threadIdx.x % npair, seg = threadIdx.x / npair;
-  int f = 0, gg = pair;
-  while (gg >= R - f) { gg -= R - f; ++f; }
-  gg += f;
-  const int64_t chunk_rows = (int64_t)(sizeof(rows) / sizeof(float)) / R;
-  double acc = 0.0;
-  for (int64_t c0 = 0; c0 < n; c0 += chunk_rows) {
-    const int64_t nr = min(chunk_rows, n - c0);
-    __syncthreads();
-    for (int64_t e = threadIdx.x; e < nr * R; e += blockDim.x) rows[e] = U[c0 * R + e];
-    __syncthreads();
-    if (seg < nseg && threadIdx.x < nseg * npair) {
-      const int64_t per = (nr + nseg - 1) / nseg;
-      const int64_t a = seg * per, b = min(nr, a + per);
-      for (int64_t r = a; r < b; ++r) acc += (double)rows[r * R + f] * (double)rows[r * R + gg];
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < nseg * npair) segsum[threadIdx.x] = acc;
-  __syncthreads();
-  if (threadIdx.x < npair) {
-    double s = 0.0;
-    for (int k = 0; k < nseg; ++k) s += segsum[k * npair + threadIdx.x];
-    G[(int64_t)m * R * R + f * R + gg] = s;
-    G[(int64_t)m * R * R + gg * R + f] = s;
+    part[2 * blockIdx.x] = inner;
+    part[2 * blockIdx.x + 1] = sq;
   }
 }
 
@@ -363,49 +408,78 @@ __global__ void fit_combine_kernel(const double* part, int nb, const double* G, 
   *relerr = sq > 0.0 ? sqrt(res / sq) : 0.0;
 }
 
-// Geometry: column chunks of <= max_cw floats; stages of ~stage_bytes (whole rows), a ring of
-// ring_bytes / stage; one CTA per SM and chunk over contiguous row ranges.
-StreamGeom make_geom(const DenseView& X, int64_t row0, int64_t nrows, int* grid_x, int* grid_y,
-                     int max_cw, int stage_bytes, int ring_bytes, int min_tr, int ctas_per_sm = 1) {
-  StreamGeom g{};
-  g.row0 = row0;
-  g.nrows = nrows;
-  g.pitch = (int)X.pitch;
-  g.ncol = (int)X.I;
-  if (g.pitch <= max_cw) {
-    g.cw = g.pitch;
-  } else {   // equal chunks, multiples of 4 floats
-    const int nch = (g.pitch + max_cw - 1) / max_cw;
-    g.cw = ((g.pitch + nch - 1) / nch + 3) & ~3;
-  }
-  const int nchunk = (g.pitch + g.cw - 1) / g.cw;
-  g.tr = stage_bytes / (int)(g.cw * sizeof(float));
-  if (g.tr < min_tr) g.tr = min_tr;
-  if (g.tr > 256) g.tr = 256;
-  g.ns = ring_bytes / (int)(g.tr * g.cw * sizeof(float));
-  if (g.ns > kMaxNS) g.ns = kMaxNS;
-  if (g.ns < 2) g.ns = 2;
-  int64_t nx = (int64_t)kNumSMs * ctas_per_sm / nchunk;
-  if (nx < 1) nx = 1;
-  if (nx > ceil_div(nrows, 2 * g.tr)) nx = ceil_div(nrows, 2 * g.tr);   // a few stages per CTA
-  if (nx < 1) nx = 1;
-  g.rows_per_cta = ceil_div(nrows, nx);
-  *grid_x = (int)ceil_div(nrows, g.rows_per_cta);
-  *grid_y = nchunk;
-  return g;
-}
-
-size_t ring_smem(const StreamGeom& g) { return sizeof(float) * (size_t)g.ns * g.tr * g.cw; }
-
 constexpr int kRingBytes = 192 * 1024;
 
-StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* gy) {
-  // rows per stage: a multiple of kRPW * warps keeps every warp busy
-  return make_geom(X, k0 * X.J, nk * X.J, gx, gy, 4 * 32 * kMQ, 64 * 1024, kRingBytes, kRPW * kNW,
-                   kMargCTAs);
+// Marginal pass: stages of whole rows (one bulk copy each, contiguous in the store); a row is
+// split into nch chunks of <= 512 floats, each worked by wpc warps (nch * wpc <= 16); rows per
+// stage a multiple of kRPW * wpc, stages of ~48-64 KB in a 192 KB ring.
+StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* gy, int* threads) {
+  StreamGeom g{};
+  g.row0 = k0 * X.J;
+  g.nrows = nk * X.J;
+  g.pitch = (int)X.pitch;
+  g.ncol = (int)X.I;
+  const int maxcw = 4 * 32 * kMQ;
+  g.nch = (g.pitch + maxcw - 1) / maxcw;
+  g.cw = ((g.pitch + g.nch - 1) / g.nch + 3) & ~3;
+  g.wpc = kNW / g.nch;
+  if (g.wpc < 1) g.wpc = 1;
+  const int unit = kRPW * g.wpc;
+  const int row_b = g.pitch * (int)sizeof(float);
+  int m = (64 * 1024) / (unit * row_b);
+  if (m < 1) m = 1;
+  g.tr = unit * m;
+  g.ns = kRingBytes / (g.tr * row_b);
+  if (g.ns > kMaxNS) g.ns = kMaxNS;
+  if (g.ns < 2) { g.ns = 2; }
+  int64_t nx = (int64_t)kNumSMs * kMargCTAs;
+  if (nx > ceil_div(g.nrows, 2 * g.tr)) nx = ceil_div(g.nrows, 2 * g.tr);
+  if (nx < 1) nx = 1;
+  g.rows_per_cta = ceil_div(g.nrows, nx);
+  *gx = (int)ceil_div(g.nrows, g.rows_per_cta);
+  *gy = 1;
+  *threads = 32 * g.nch * g.wpc;
+  return g;
 }
-StreamGeom fit_geom(const DenseView& X, int* gx, int* gy) {
-  return make_geom(X, 0, X.J * X.K, gx, gy, 2048, 32 * 1024, 176 * 1024, 1);
+// Fit pass: stages of whole rows (one bulk copy); thread (group grp, lane tq) owns the column
+// quads tq + u * tpg (u < qpt) and the rows grp, grp + ng, ... of each stage; stages of ~32 KB.
+StreamGeom fit_geom(const DenseView& X, int RB, int* gx, int* gy, int* threads) {
+  StreamGeom g{};
+  g.row0 = 0;
+  g.nrows = X.J * X.K;
+  g.pitch = (int)X.pitch;
+  g.ncol = (int)X.I;
+  const int nq = g.pitch / 4;
+  g.qpt = nq <= kST ? 1 : 2;   // 2: nq <= 2 * kFitT2 (fit_stream_supported)
+  g.tpg = (nq + g.qpt - 1) / g.qpt;
+  const int tmax = g.qpt == 1 ? kST : kFitT2;
+  g.ng = tmax / g.tpg > 0 ? tmax / g.tpg : 1;
+  int nthr = ((g.ng * g.tpg + 31) / 32) * 32;
+  if (nthr > tmax) nthr = tmax;
+  const int row_b = g.pitch * (int)sizeof(float);
+  const size_t bres_b = sizeof(float) * (size_t)X.J * RB;
+  g.bres = bres_b <= 48 * 1024;
+  g.tr = (48 * 1024) / row_b;
+  if (g.tr < 1) g.tr = 1;
+  if (!g.bres && g.tr * RB > kWPT * nthr) g.tr = kWPT * nthr / RB;   // the B prefetch registers
+  if (g.tr > 256) g.tr = 256;
+  const size_t extra = g.bres ? bres_b : sizeof(float) * 2 * (size_t)g.tr * RB;
+  const int ring_b = (int)(208 * 1024 - extra);
+  g.cw = g.pitch;
+  g.ns = ring_b / (g.tr * row_b);
+  if (g.ns > kMaxNS) g.ns = kMaxNS;
+  if (g.ns < 2) {   // very long rows: two stages of fewer rows
+    g.ns = 2;
+    g.tr = std::max(1, ring_b / (2 * row_b));
+  }
+  int64_t nx = kNumSMs;
+  if (nx > ceil_div(g.nrows, 2 * g.tr)) nx = ceil_div(g.nrows, 2 * g.tr);
+  if (nx < 1) nx = 1;
+  g.rows_per_cta = ceil_div(g.nrows, nx);
+  *gx = (int)ceil_div(g.nrows, g.rows_per_cta);
+  *gy = 1;
+  *threads = nthr;
+  return g;
 }
 
 }  // namespace
@@ -426,6 +500,13 @@ cudaError_t launch_gram3(const float* A, const float* B, const float* C, int64_t
   return launch_gram_tiles(g, st);
 }
 
+// the fit pass additionally needs its quads in registers: <= 2 per thread, and R <= 12 at 2
+bool fit_stream_supported(const DenseView& X, int R) {
+  if (!stream_supported(X) || R > 16) return false;
+  const int nq = (int)(X.pitch / 4);
+  return nq <= kST || (nq <= 2 * kFitT2 && R <= 12);
+}
+
 bool stream_supported(const DenseView& X) {
   return X.pitch % 4 == 0 && ((uintptr_t)X.base & 15) == 0 && X.I >= 1 && X.I <= 8192 && X.J >= 1;
 }
@@ -433,44 +514,69 @@ bool stream_supported(const DenseView& X) {
 cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
                                     int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st) {
   if (nk <= 0) return cudaSuccess;
-  int gx, gy;
-  StreamGeom g = marg_geom(X, k0, nk, &gx, &gy);
+  int gx, gy, nthr;
+  StreamGeom g = marg_geom(X, k0, nk, &gx, &gy, &nthr);
   const float scf = ldexpf(1.0f, S < -126 ? -126 : (S > 127 ? 127 : S));
   const double scd = ldexp(1.0, S);
-  const size_t smem = ring_smem(g);
+  const size_t smem = sizeof(float) * (size_t)g.ns * g.tr * g.pitch;
   auto* u1 = reinterpret_cast<unsigned long long*>(x1);
   auto* u2 = reinterpret_cast<unsigned long long*>(x2);
   auto* u3 = reinterpret_cast<unsigned long long*>(x3);
   if (moi == 0) {
     cudaFuncSetAttribute(marg_stream_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    marg_stream_kernel<0><<<dim3(gx, gy), kST, smem, st>>>(X.base, g, (int)X.J, scf, scd, u1, u2, u3);
+    marg_stream_kernel<0><<<dim3(gx, gy), nthr, smem, st>>>(X.base, g, (int)X.J, scf, scd, u1, u2, u3);
   } else {
     cudaFuncSetAttribute(marg_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    marg_stream_kernel<1><<<dim3(gx, gy), kST, smem, st>>>(X.base, g, (int)X.J, scf, scd, u1, u2, u3);
+    marg_stream_kernel<1><<<dim3(gx, gy), nthr, smem, st>>>(X.base, g, (int)X.J, scf, scd, u1, u2, u3);
   }
   return cudaGetLastError();
 }
 
-size_t fit_stream_ws_doubles(const DenseView& X) {
-  int gx, gy;
-  fit_geom(X, &gx, &gy);
-  return 2 * (size_t)gx * gy + 3 * kMaxR * kMaxR + 8 + gram3_ws_doubles(X.I, X.J, X.K, kMaxR);
+size_t fit_stream_ws_doubles(const DenseView& X) {   // <= kNumSMs CTA partials
+  return 2 * (size_t)kNumSMs + 3 * kMaxR * kMaxR + 8 + gram3_ws_doubles(X.I, X.J, X.K, kMaxR);
+}
+
+template <int RB, int QPT, bool BRES>
+static cudaError_t fit_go(const DenseView& X, const StreamGeom& g, int gx, int nt, size_t smem, int R,
+                          const float* lam, const float* A, const float* B, const float* C, double* part,
+                          const int32_t* kmap, cudaStream_t st) {
+  cudaFuncSetAttribute(fit_stream_kernel<RB, QPT, BRES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fit_stream_kernel<RB, QPT, BRES><<<gx, nt, smem, st>>>(X.base, g, (int)X.J, R, lam, A, B, C, part, kmap);
+  return cudaGetLastError();
+}
+
+// one fit pass (per-CTA partials in part[2 * gx]); QPT from the geometry
+template <int RB>
+static cudaError_t fit_pass(const DenseView& X, const float* lam, const float* A, const float* B, const float* C,
+                            int R, const int32_t* kmap, double* part, int* nparts, cudaStream_t st) {
+  int gx, gy, nt;
+  StreamGeom g = fit_geom(X, RB, &gx, &gy, &nt);
+  const size_t extra = g.bres ? (size_t)X.J * RB : 2 * (size_t)g.tr * RB;
+  const size_t smem = sizeof(float) * ((size_t)g.ns * g.tr * g.pitch + extra);
+  *nparts = gx;
+  if (g.qpt == 1) {
+    if (g.bres) return fit_go<RB, 1, true>(X, g, gx, nt, smem, R, lam, A, B, C, part, kmap, st);
+    return fit_go<RB, 1, false>(X, g, gx, nt, smem, R, lam, A, B, C, part, kmap, st);
+  }
+  if constexpr (RB <= 12) {
+    if (g.bres) return fit_go<RB, 2, true>(X, g, gx, nt, smem, R, lam, A, B, C, part, kmap, st);
+    return fit_go<RB, 2, false>(X, g, gx, nt, smem, R, lam, A, B, C, part, kmap, st);
+  } else {
+    return cudaErrorInvalidValue;   // excluded by fit_stream_supported
+  }
 }
 
 template <int RB>
 static cudaError_t fit_stream_rb(const DenseView& X, const float* lam, const float* A, const float* B,
                                  const float* C, int R, double* ws, double* relerr, cudaStream_t st) {
-  int gx, gy;
-  StreamGeom g = fit_geom(X, &gx, &gy);
-  const size_t smem = ring_smem(g) + sizeof(float) * 2 * (size_t)g.tr * RB;
-  cudaFuncSetAttribute(fit_stream_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   double* part = ws;
-  double* G = ws + 2 * (size_t)gx * gy;
-  fit_stream_kernel<RB><<<dim3(gx, gy), kST, smem, st>>>(X.base, g, (int)X.J, R, lam, A, B, C, part,
-                                                          nullptr);
-  cudaError_t e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
+  int nparts = 0;
+  cudaError_t e = fit_pass<RB>(X, lam, A, B, C, R, nullptr, part, &nparts, st);
   if (e != cudaSuccess) return e;
-  fit_combine_kernel<<<1, 32, 0, st>>>(part, gx * gy, G, lam, R, relerr);
+  double* G = ws + 2 * (size_t)kNumSMs;
+  e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
+  if (e != cudaSuccess) return e;
+  fit_combine_kernel<<<1, 32, 0, st>>>(part, nparts, G, lam, R, relerr);
   return cudaGetLastError();
 }
 
@@ -498,12 +604,10 @@ template <int RB>
 static cudaError_t fit_partial_rb(const DenseView& X, const float* lam, const float* A, const float* B,
                                   const float* C, int R, const int32_t* kmap, double* ws, double* out2,
                                   cudaStream_t st) {
-  int gx, gy;
-  StreamGeom g = fit_geom(X, &gx, &gy);
-  const size_t smem = ring_smem(g) + sizeof(float) * 2 * (size_t)g.tr * RB;
-  cudaFuncSetAttribute(fit_stream_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fit_stream_kernel<RB><<<dim3(gx, gy), kST, smem, st>>>(X.base, g, (int)X.J, R, lam, A, B, C, ws, kmap);
-  sum_pairs_kernel<<<1, 32, 0, st>>>(ws, gx * gy, out2);
+  int nparts = 0;
+  cudaError_t e = fit_pass<RB>(X, lam, A, B, C, R, kmap, ws, &nparts, st);
+  if (e != cudaSuccess) return e;
+  sum_pairs_kernel<<<1, 32, 0, st>>>(ws, nparts, out2);
   return cudaGetLastError();
 }
 

@@ -177,3 +177,59 @@ def split_coo(X, K0, batch):
         out.append(take(k, min(k + batch, K)))
         k += batch
     return init, out
+
+
+# ---------------------------------------------------------------------------------------
+# Counter-based dense generator (the large dense configs, C4): the same recipe as
+# dense_from_factors, with the noise drawn from Philox4x32-10 (counter domain GEN = 3) by
+# Box-Muller so that any slab can be produced independently -- on the device by
+# synth/csrc/gen.cu (synth_dense_slab), here by the numpy twin below (small slabs; tests).
+# ---------------------------------------------------------------------------------------
+_M0, _M1, _W0, _W1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57), 0x9E3779B9, 0xBB67AE85
+_MASK = np.uint64(0xFFFFFFFF)
+
+
+def _philox_np(seed, c0, c1, c2, c3):
+    """Philox4x32-10 on uint32 counter arrays (numpy uint64 carriers)."""
+    k0, k1 = seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF
+    x0, x1, x2, x3 = (np.asarray(c, np.uint64) & _MASK for c in (c0, c1, c2, c3))
+    for _ in range(10):
+        p0 = _M0 * x0
+        p1 = _M1 * x2
+        n0 = (p1 >> np.uint64(32)) ^ x1 ^ np.uint64(k0)
+        n2 = (p0 >> np.uint64(32)) ^ x3 ^ np.uint64(k1)
+        x0, x1, x2, x3 = n0 & _MASK, p1 & _MASK, n2 & _MASK, p0 & _MASK
+        k0 = (k0 + _W0) & 0xFFFFFFFF
+        k1 = (k1 + _W1) & 0xFFFFFFFF
+    return x0, x1, x2, x3
+
+
+def _unit(a, b):
+    m52 = (a << np.uint64(20)) | (b >> np.uint64(12))
+    return (2.0 * m52.astype(np.float64) + 1.0) * 2.0 ** -53
+
+
+def planted_sigma(A, B, C, noise):
+    """sigma = noise * ||[[A, B, C]]||_F / sqrt(N) (closed-form norm from the Grams)."""
+    G = (A.T @ A) * (B.T @ B) * (C.T @ C)
+    return noise * float(np.sqrt(G.sum())) / np.sqrt(float(A.shape[0]) * B.shape[0] * C.shape[0])
+
+
+def dense_philox_slab(A, B, C, sigma, seed, k0, nk):
+    """numpy twin of synth_dense_slab: float32 [nk][J][I] of slices [k0, k0 + nk)."""
+    I, J, R = A.shape[0], B.shape[0], A.shape[1]
+    e0, e1 = k0 * I * J, (k0 + nk) * I * J
+    e = np.arange(e0, e1, dtype=np.int64)
+    k, rem = np.divmod(e, I * J)
+    j, i = np.divmod(rem, I)
+    s = np.zeros(e.shape[0])
+    for f in range(R):
+        s = s + (A[i, f] * B[j, f]) * C[k, f]
+    if sigma != 0.0:
+        p = (e >> 1).astype(np.uint64)
+        x0, x1, x2, x3 = _philox_np(seed, p & _MASK, p >> np.uint64(32), 0, 3 << 24)
+        u1, u2 = _unit(x0, x1), _unit(x2, x3)
+        r = np.sqrt(-2.0 * np.log(u1))
+        z = np.where((e & 1) == 0, r * np.cos(2.0 * np.pi * u2), r * np.sin(2.0 * np.pi * u2))
+        s = s + sigma * z
+    return s.astype(np.float32).reshape(nk, J, I)
