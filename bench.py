@@ -202,6 +202,72 @@ def describe(w):
     return f"{w.name}: {shape}, R={w.R}, s={w.s}, r={w.r}, ALS {w.maxit} it tol {w.tol}"
 
 
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FP32 lanes x FMA x max clock
+L2_RESIDENT_BYTES = 100e6                           # summaries below this stay in the 126 MB L2
+
+
+def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
+    """Per-step roofline of the dominant kernel of each streaming / ALS step, from the steps'
+    CUDA-event times (info.step_ms, on the library's stream) and the algorithmic work of
+    DESIGN.md "Kernels": a1 4 B per stored entry (+ 8 B per marginal), a3 8 B per summary entry
+    (read + write), a4 per ALS iteration 2 passes x 4 B (HBM) or 2R flops (fp32 FMA) per summary
+    entry, a7 4 B per stored entry."""
+    def ms(k):
+        return statistics.mean(inf["step_ms"][k] for inf in infos)
+    traffic = {}
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(w.name, {})
+        except Exception:
+            traffic = {}
+    hbm = peaks["hbm_gbs"]
+    out = {}
+
+    def hbm_line(name, step, byts):
+        t = ms(step)
+        ach = byts / (t / 1e3) / 1e9
+        return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": ach / hbm, "traffic": traffic.get(f"a{step}"),
+                "bytes_per_launch": byts, "ms_per_launch": t}
+    Ks = [inf["k_total"] for inf in infos]
+    if work.coo:
+        nnz_avg = work.X0.nnz + statistics.mean(
+            sum(work.entries[:(j % work.nb) + 1]) for j in range(args.warmup, args.warmup + args.steps))
+        out["a1"] = hbm_line("marg_coo_kernel", 1, 16.0 * nnz_avg + 8.0 * (w.I + w.J + statistics.mean(Ks)))
+        out["a4"] = {"kernel": "COO ALS (sort, piece MTTKRP, row solves)", "bound": "latency",
+                     "ms_per_launch": ms(4), "frac": None,
+                     "note": "gather-latency bound sparse MTTKRP on L2-resident summaries; not modelled"}
+        return out
+    Kloc = k_local if k_local is not None else Ks
+    IJ = w.I * w.J
+    out["a1"] = hbm_line("marg_stream_kernel", 1,
+                         statistics.mean(4.0 * IJ * kl for kl in Kloc) + 8.0 * (w.I + w.J + statistics.mean(Ks)))
+    out["a7"] = hbm_line("fit_stream_kernel", 7, statistics.mean(4.0 * IJ * kl for kl in Kloc))
+    nI, nJ = -(-w.I // w.s), -(-w.J // w.s)
+    Y = []
+    for inf, kt in zip(infos, Ks):
+        Kn = w.batch if kt - w.K0 >= w.batch else kt - w.K0
+        Ko = kt - Kn
+        Y.append(nI * nJ * (-(-Ko // w.s) + Kn))
+    Ymean = statistics.mean(Y)
+    rl = w.r / G
+    out["a3"] = hbm_line("gather_dense_kernel", 3, 8.0 * rl * Ymean)
+    it = statistics.mean(inf["als_iters_sum"] for inf in infos) / G
+    t4 = ms(4)
+    if rl * Ymean * 8.0 <= L2_RESIDENT_BYTES:     # Y and its transpose stay in L2: fp32 FMA bound
+        fl = it * 2 * Ymean * 2 * w.R
+        ach = fl / (t4 / 1e3) / 1e12
+        out["a4"] = {"kernel": "als_cluster_kernel", "bound": "alu", "achieved": ach,
+                     "peak": FP32_PEAK_TFLOPS, "peak_kind": "derived (148 SMs x 128 FP32 lanes x 2 x 1.965 GHz)",
+                     "unit": "TFLOP/s", "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic.get("a4"),
+                     "flops_per_launch": fl, "ms_per_launch": t4,
+                     "note": "summaries L2-resident (SURVEY 8(d)): HBM fraction not meaningful"}
+    else:
+        out["a4"] = hbm_line("als_cluster_kernel", 4, it * 2 * Ymean * 4.0)
+    return out
+
+
 def partition(n, world, rank):
     """The library's balanced split (sambaten_batch_partition's rule) of n slices."""
     base, rem = divmod(n, world)
@@ -434,30 +500,11 @@ def main():
     value = reps * sum(ents) / tot
 
     peaks, peak_kind = measured_peaks()
-    # dominant HBM-bound kernel of the step: the marginal pass a1 (one read of the whole tensor)
-    a1_ms = statistics.mean(inf["step_ms"][1] for inf in infos)
-    Kavg = statistics.mean(inf["k_total"] for inf in infos)
-    if sharded:
-        # this rank's slab: its share of X0 plus its share of every batch ingested so far
-        kl = [k0n + sum(parts[j][1] for j in range((i % nb) + 1)) for i in range(args.warmup, args.warmup + args.steps)]
-        a1_bytes = 4.0 * w.I * w.J * statistics.mean(kl) + 8.0 * (w.I + w.J + Kavg)
-        kname = "marg_stream_kernel (a1, local slab)"
-    elif not work.coo:
-        a1_bytes = 4.0 * w.I * w.J * Kavg + 8.0 * (w.I + w.J + Kavg)
-        kname = "marg_stream_kernel (a1)"
-    else:
-        nnz_avg = work.X0.nnz + statistics.mean(
-            sum(work.entries[:(j % nb) + 1]) for j in range(args.warmup, args.warmup + args.steps))
-        a1_bytes = 16.0 * nnz_avg + 8.0 * (w.I + w.J + Kavg)
-        kname = "marg_coo_kernel (a1)"
-    achieved = a1_bytes / (a1_ms / 1000.0) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get(w.name, {}).get("a1")
-        except Exception:
-            traffic = None
+    kern = kernel_rooflines(w, work, infos, peaks, peak_kind, world if sharded else 1,
+                            ([k0n + sum(parts[j][1] for j in range((i % nb) + 1))
+                              for i in range(args.warmup, args.warmup + args.steps)] if sharded else None),
+                            args)
+    dominant = max(kern, key=lambda k: kern[k]["ms_per_launch"] if kern[k].get("frac") is not None else -1)
     step_share = {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in infos) for k in range(8)}
     line = {
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
@@ -466,10 +513,8 @@ def main():
         "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded numpy generators; DESIGN.md 'Synthetic inputs')",
         "config": config,
-        "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved,
-                     "peak": peaks["hbm_gbs"], "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                     "bytes_per_launch": a1_bytes, "ms_per_launch": a1_ms},
+        "roofline": dict(kern[dominant], step=dominant),
+        "kernels": kern,
         "step_ms": step_share,
         "gpu_launches": int(sum(inf["kernel_launches"] for inf in infos)),
         "clocks": clocks,

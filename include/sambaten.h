@@ -100,6 +100,7 @@ typedef struct {
   uint32_t reps_pinv_mask;     /* bit rho set if repetition rho's ALS used the pseudo-inverse  */
                                /* fallback (R12) at least once                                */
   double step_ms[8];           /* device time of steps a0..a7 (CUDA events)                   */
+  int als_iters_sum;           /* ALS iterations summed over the repetitions (work accounting) */
 } sambaten_info;
 
 /* Fill *opts with the defaults listed above. */

@@ -49,14 +49,14 @@ class Info(C.Structure):
                 ("als_iters_max", C.c_int), ("k_total", C.c_int64),
                 ("reps_rejected_mask", C.c_uint32), ("scale_exp", C.c_int),
                 ("kernel_launches", C.c_int), ("reps_pinv_mask", C.c_uint32),
-                ("step_ms", C.c_double * 8)]
+                ("step_ms", C.c_double * 8), ("als_iters_sum", C.c_int)]
 
     def as_dict(self):
         return dict(fit_summary=self.fit_summary, fit_full=self.fit_full,
                     als_iters_max=self.als_iters_max, k_total=self.k_total,
                     reps_rejected_mask=self.reps_rejected_mask, scale_exp=self.scale_exp,
                     kernel_launches=self.kernel_launches, reps_pinv_mask=self.reps_pinv_mask,
-                    step_ms=list(self.step_ms))
+                    step_ms=list(self.step_ms), als_iters_sum=self.als_iters_sum)
 
 
 _lib = None

@@ -540,12 +540,13 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
   if (maxphi > ldexp(1.0, h->maxphi_log2 + 8))
     FAIL(SAMBATEN_E_FIXEDPOINT_RANGE, "update: batch value outside the fixed-point range (R7)");
   uint32_t rejected = 0, pm = 0;
-  int nacc = 0, itmax = 0;
+  int nacc = 0, itmax = 0, itsum = 0;
   double fsum = 0.0;
   for (int rho = 0; rho < r; ++rho) {
     if (hs->accepted[rho]) ++nacc; else rejected |= 1u << rho;
     if (hs->flags[rho] & 1) pm |= 1u << rho;
     itmax = std::max(itmax, hs->iters[rho]);
+    itsum += hs->iters[rho];
     fsum += hs->fit[rho];
   }
   if (nacc == 0) FAIL(SAMBATEN_E_BATCH_REJECTED, "update: every repetition was rejected (R26)");
@@ -559,6 +560,7 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
     info->fit_summary = fsum / r;
     info->fit_full = h->opts.full_fit ? 1.0 - hs->relerr : -1.0;
     info->als_iters_max = itmax;
+    info->als_iters_sum = itsum;
     info->k_total = h->K;
     info->reps_rejected_mask = rejected;
     info->scale_exp = h->S;
