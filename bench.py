@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--config", default="C2")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-variant", action="store_true", help="skip the incremental-marginals variant run")
     p.add_argument("--no-full-fit", action="store_true", help="return the summary fit only (R21)")
     p.add_argument("--sharded", action="store_true",
                    help="use the sharded (NCCL) handle even at N=1 (always used at N>1, dense configs)")
@@ -268,6 +269,33 @@ def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
     return out
 
 
+def init_single(L, work, w, opts, config):
+    """A single-GPU handle for the workload (untimed): planted factors, full CP-ALS of X0 (C3),
+    or the device-generated store held in place (C4)."""
+    import torch
+    if work.model is None:
+        X0 = work.tensor(L, work.X0, device=True)
+        opts.init_max_iters = 50
+        h = L.sambaten_init(X0, w.R, w.s, w.r, w.seed, opts)
+        m = [np.empty(w.R, np.float32), np.empty((w.I, w.R), np.float32), np.empty((w.J, w.R), np.float32),
+             np.empty((w.K0, w.R), np.float32)]
+        L.sambaten_copy_factors(h, m[1], m[2], m[3], m[0])
+        work.model = m                  # the oracle baseline (and a re-init) start from the same model
+        return h
+    if getattr(work, "device_gen", False):
+        # the whole-tensor store is one device buffer holding X0 in place (no second copy)
+        if getattr(work, "store", None) is None:
+            work.store = torch.empty((w.K, w.J, w.I), dtype=torch.float32, device="cuda")
+            work.gen(work.store[:w.K0], 0, w.K0)
+        opts.borrow_store = 1
+        config["store"] = "caller buffer (opts.borrow_store), X0 generated in place on the device"
+        return L.sambaten_init_factors(L.dense(work.store[:w.K0]), w.R, w.s, w.r, w.seed, work.model[1],
+                                       work.model[2], work.model[3], work.model[0], opts)
+    X0 = work.tensor(L, work.X0, device=True)
+    return L.sambaten_init_factors(X0, w.R, w.s, w.r, w.seed, work.model[1], work.model[2],
+                                   work.model[3], work.model[0], opts)
+
+
 def partition(n, world, rank):
     """The library's balanced split (sambaten_batch_partition's rule) of n slices."""
     base, rem = divmod(n, world)
@@ -404,26 +432,8 @@ def main():
         local_batches = [b[pb:pb + pn] for b, (pb, pn) in zip(work.batches, parts)]
         config["parallelism"] = f"sharded over {world} rank(s): time-mode slabs, rep rho on rank rho mod {world}"
         config["slab"] = [k0b, k0n]
-    elif work.model is None:
-        X0 = work.tensor(L, work.X0, device=True)
-        opts.init_max_iters = 50
-        h = L.sambaten_init(X0, w.R, w.s, w.r, w.seed, opts)
-        m = [np.empty(w.R, np.float32), np.empty((w.I, w.R), np.float32), np.empty((w.J, w.R), np.float32),
-             np.empty((w.K0, w.R), np.float32)]
-        L.sambaten_copy_factors(h, m[1], m[2], m[3], m[0])
-        work.model = m                  # the oracle baseline starts from the same model
-    elif device_gen:
-        # the whole-tensor store is one device buffer holding X0 in place (no second copy)
-        store = torch.empty((w.K, w.J, w.I), dtype=torch.float32, device="cuda")
-        work.gen(store[:w.K0], 0, w.K0)
-        opts.borrow_store = 1
-        h = L.sambaten_init_factors(L.dense(store[:w.K0]), w.R, w.s, w.r, w.seed, work.model[1],
-                                    work.model[2], work.model[3], work.model[0], opts)
-        config["store"] = "caller buffer (opts.borrow_store), X0 generated in place on the device"
     else:
-        X0 = work.tensor(L, work.X0, device=True)
-        h = L.sambaten_init_factors(X0, w.R, w.s, w.r, w.seed, work.model[1], work.model[2],
-                                    work.model[3], work.model[0], opts)
+        h = init_single(L, work, w, opts, config)
     if world > 1 and not sharded:
         config["parallelism"] = f"{world} independent replicas"
     L.sambaten_checkpoint(h)
@@ -533,6 +543,31 @@ def main():
             v, dt, nbt = cpu_baseline_run(work, model)
             line["cpu_baseline"] = {"value": v, "unit": unit, "cores": threads_used(), "kind": "oracle",
                                     "sample": f"{nbt} consecutive oracle updates of {w.name} from the K0 state, {dt:.1f} s"}
+    if world == 1 and not sharded and not args.no_variant:
+        # the same workload with incremental marginals (bit-identical a1):
+        # a fresh handle, primed, W warm-up and K timed steps exactly as above
+        L.sambaten_destroy(h)
+        opts.incremental_marginals = 1
+        h = init_single(L, work, w, opts, config)
+        L.sambaten_checkpoint(h)
+        for i in range(nb):
+            with torch.cuda.stream(stream):
+                L.sambaten_update(h, dbatches[i])
+        L.sambaten_restore(h)
+        state["i"] = 0
+        for _ in range(args.warmup):
+            step()
+        vt, vi, ve = [], [], []
+        for _ in range(args.steps):
+            ms, info, ne, bi = step()
+            vt.append(ms)
+            vi.append(info.as_dict())
+            ve.append(ne)
+        line["variants"] = {"incremental_marginals": {
+            "value": sum(ve) / (sum(vt) / 1000.0), "unit": unit, "ms_per_step": statistics.mean(vt),
+            "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in vi) for k in range(8)},
+            "note": "opts.incremental_marginals=1: a1 adds the batch's contribution to the committed "
+                    "int64 marginals (bit-identical to the full pass; tests/test_gpu_incremental.py)"}}
     L.sambaten_destroy(h)
     if rank == 0:
         print(json.dumps(line), flush=True)

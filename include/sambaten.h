@@ -86,6 +86,10 @@ typedef struct {
                           /* room for `capacity` slices (I % 4 == 0); the handle uses it as   */
                           /* its tensor store in place (no copy of X0).  The caller keeps it  */
                           /* alive and unmodified until sambaten_destroy.  Default 0 (copy).  */
+  int incremental_marginals; /* 1: a1 adds the batch's contribution to the marginals kept from */
+                          /* the previous update instead of re-reading the whole tensor --    */
+                          /* bit-identical (integer sums); the first     */
+                          /* update after init / restore makes the full pass.  Default 0.     */
 } sambaten_opts;
 
 typedef struct {

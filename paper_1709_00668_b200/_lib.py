@@ -36,7 +36,8 @@ class Opts(C.Structure):
                 ("s_mode", C.c_int * 3), ("merge_policy", C.c_int), ("accept_tau", C.c_double),
                 ("full_fit", C.c_int), ("capacity", C.c_int64), ("capacity_k", C.c_int64),
                 ("init_max_iters", C.c_int),
-                ("init_tol", C.c_double), ("stream", C.c_void_p), ("borrow_store", C.c_int)]
+                ("init_tol", C.c_double), ("stream", C.c_void_p), ("borrow_store", C.c_int),
+                ("incremental_marginals", C.c_int)]
 
 
 class Dist(C.Structure):

@@ -116,6 +116,8 @@ struct sambaten_s {
   DistState* dist = nullptr;   // set for handles of the sharded update (sambaten_init_factors_dist)
   int64_t I = 0, J = 0, K = 0, Kcap = 0, pitch = 0;
   bool X_borrowed = false;   // opts.borrow_store: X is the caller's buffer
+  DevBuf xm, xm_ck;          // committed marginals of the current tensor (incremental a1)
+  bool xm_valid = false, xm_ck_valid = false;
   int R = 0, r = 0, s[3] = {1, 1, 1};
   uint64_t seed = 0;
   uint32_t update_id = 0;
@@ -337,7 +339,7 @@ extern "C" void sambaten_destroy(sambaten_t h) {
   if (h->X_borrowed) h->X.p = nullptr;   // the caller's buffer: not ours to free
   h->X.release();
   h->model[0].release(); h->model[1].release(); h->ck.release();
-  h->marg.release(); h->samp.release(); h->summ.release(); h->fac.release();
+  h->marg.release(); h->xm.release(); h->xm_ck.release(); h->samp.release(); h->summ.release(); h->fac.release();
   h->als.release(); h->match.release(); h->misc.release(); h->segs.release(); h->fitws.release();
   h->coo_ws.release();
   if (h->segs_host) cudaFreeHost(h->segs_host);
@@ -551,6 +553,10 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
   }
   if (nacc == 0) FAIL(SAMBATEN_E_BATCH_REJECTED, "update: every repetition was rejected (R26)");
   // commit
+  if (h->opts.incremental_marginals) {   // this update's marginals are the new committed ones
+    std::swap(h->marg, h->xm);
+    h->xm_valid = true;
+  }
   h->cur = nb;
   h->K = Ko + Kn;
   if (h->fmt == SAMBATEN_COO) h->nnz += batch_nnz;
@@ -801,8 +807,15 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
   int64_t* x1 = h->marg.as<int64_t>();
   int64_t* x2 = x1 + h->I;
   int64_t* x3 = x2 + h->J;
-  CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
-  CK(launch_marginals_coo(h->ci(), h->cj(), h->ck_(), h->cv(), ntot, h->opts.moi, h->S, x1, x2, x3, st));
+  if (h->opts.incremental_marginals && h->xm_valid) {
+    CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(x3 + Ko, 0, sizeof(int64_t) * (h->Kcap - Ko), st));
+    CK(launch_marginals_coo(h->ci() + h->nnz, h->cj() + h->nnz, h->ck_() + h->nnz, h->cv() + h->nnz,
+                            ntot - h->nnz, h->opts.moi, h->S, x1, x2, x3, st));
+  } else {
+    CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
+    CK(launch_marginals_coo(h->ci(), h->cj(), h->ck_(), h->cv(), ntot, h->opts.moi, h->S, x1, x2, x3, st));
+  }
   launches += 1;
   CK(cudaEventRecord(h->ev[2], st));
   // ---- a2: sampling ---------------------------------------------------------------------
@@ -931,8 +944,16 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   int64_t* x1 = h->marg.as<int64_t>();
   int64_t* x2 = x1 + h->I;
   int64_t* x3 = x2 + h->J;
-  CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
-  CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, st));
+  if (h->opts.incremental_marginals && h->xm_valid) {
+    // committed marginals of X_old plus the batch's contribution (integer sums: bit-identical
+    // to the full pass)
+    CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(x3 + Ko, 0, sizeof(int64_t) * (h->Kcap - Ko), st));
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, st));
+  } else {
+    CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
+    CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, st));
+  }
   CK(cudaEventRecord(h->ev[2], st));
   // ---- a2: sampling ---------------------------------------------------------------------
   int32_t *Is, *Js, *Kp, *locI, *locJ, *locK;
@@ -1075,14 +1096,41 @@ extern "C" sambaten_status sambaten_relative_error(sambaten_t h, double* relerr)
   return SAMBATEN_OK;
 }
 
+// Committed marginals of the current tensor for the incremental a1 (one full pass; single-GPU
+// handles -- a sharded handle computes them in its first update).
+static cudaError_t compute_committed_marginals(sambaten_s* h) {
+  if (h->dist || h->xm_valid || !h->opts.incremental_marginals) return cudaSuccess;
+  const size_t xb = sizeof(int64_t) * (h->I + h->J + h->Kcap);
+  cudaError_t e = h->xm.ensure(xb);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->xm.p, 0, xb, h->st);
+  int64_t* x1 = h->xm.as<int64_t>();
+  if (e == cudaSuccess) {
+    if (h->fmt == SAMBATEN_DENSE)
+      e = marginals_any(h->view(), 0, h->K, h->opts.moi, h->S, x1, x1 + h->I, x1 + h->I + h->J, h->st);
+    else
+      e = launch_marginals_coo(h->ci(), h->cj(), h->ck_(), h->cv(), h->nnz, h->opts.moi, h->S, x1, x1 + h->I,
+                               x1 + h->I + h->J, h->st);
+  }
+  if (e == cudaSuccess) h->xm_valid = true;
+  return e;
+}
+
 extern "C" sambaten_status sambaten_checkpoint(sambaten_t h) {
   if (!h) FAIL(SAMBATEN_E_INVALID, "checkpoint: NULL handle");
+  CK(compute_committed_marginals(h));
   CK(h->ck.ensure(h->model_floats() * sizeof(float)));
   CK(cudaMemcpyAsync(h->ck.p, h->model[h->cur].p, h->model_floats() * sizeof(float),
                      cudaMemcpyDeviceToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
   h->K_ck = h->K;
   h->nnz_ck = h->nnz;
+  h->xm_ck_valid = h->xm_valid;
+  if (h->xm_valid) {
+    const size_t xb = sizeof(int64_t) * (h->I + h->J + h->K);
+    CK(h->xm_ck.ensure(xb));
+    CK(cudaMemcpyAsync(h->xm_ck.p, h->xm.p, xb, cudaMemcpyDeviceToDevice, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  }
   if (h->dist) h->dist->K_local_ck = h->dist->K_local;
   h->uid_ck = h->update_id;
   return SAMBATEN_OK;
@@ -1096,6 +1144,12 @@ extern "C" sambaten_status sambaten_restore(sambaten_t h) {
   CK(cudaStreamSynchronize(h->st));
   h->K = h->K_ck;
   h->nnz = h->nnz_ck;
+  h->xm_valid = h->xm_ck_valid;
+  if (h->xm_valid) {
+    CK(cudaMemcpyAsync(h->xm.p, h->xm_ck.p, sizeof(int64_t) * (h->I + h->J + h->K), cudaMemcpyDeviceToDevice,
+                       h->st));
+    CK(cudaStreamSynchronize(h->st));
+  }
   if (h->dist) {
     h->dist->K_local = h->dist->K_local_ck;
     h->dist->kmap_h.resize(h->dist->K_local);

@@ -249,6 +249,7 @@ cudaError_t launch_multi_copy(const CopyBytes* jobs, int njobs, int64_t max_byte
 cudaError_t launch_slice_gather(const DenseView& X, const SliceJob* jobs, int njobs, const int32_t* Is_all,
                                 const int32_t* Js_all, int nI, int nJ, int pI, int pJ, cudaStream_t st);
 cudaError_t launch_slice_copy(const CopyJob* jobs, int njobs, int64_t nY, int64_t nYt, cudaStream_t st);
+cudaError_t launch_add_i64(int64_t* dst, const int64_t* src, int64_t n, cudaStream_t st);
 cudaError_t launch_x3_scatter(const int64_t* x3l, const int32_t* kmap, int64_t n, int64_t* x3g,
                               cudaStream_t st);
 // fit partials of a slab: inner/sq summed into out2[0..1] (kmap: local slice -> global row of C)

@@ -45,6 +45,7 @@ constexpr int kTS = 3;            // TMA stages per team
 struct ClLayout {
   size_t G, Gp, Gs, Vi, W1, lam, sc, bars, P, Xun, Xun2, Msh, U0s, U1s, U2s, Dsh, stage, total;
   int chunk0, chunk1, ownK, stage_fl, T, NT;
+  int NTA, sfla;       // pass A: teams (all warps but the inverse warp), floats per ring stage
 };
 
 __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
@@ -100,6 +101,15 @@ __host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, in
   const size_t red = sizeof(float) * (size_t)4 * RB * kCT;
   L.stage = take(ring > red ? ring : red);
   L.total = o;
+  // pass A: every team of the CTA (all warps but the inverse warp) streams a row range through
+  // its own ring of kTS stages carved from the same region (>= one row per stage)
+  const size_t region = ring > red ? ring : red;
+  L.NTA = (kCW - 1) / (L.T / 32);
+  if (L.NTA < 1) L.NTA = 1;
+  if (L.NTA > 15) L.NTA = 15;
+  L.sfla = (int)(region / (sizeof(float) * kTS * L.NTA)) & ~3;
+  if (L.sfla > 12288) L.sfla = 12288;
+  if (L.sfla < pitch4(nI)) L.sfla = 0;   // too little room: pass A keeps the slice teams
   return L;
 }
 
@@ -133,12 +143,32 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// rows of RB floats (RB even): 16 B vectors when RB % 4 == 0, else 8 B
 template <int RB>
 __device__ __forceinline__ void ld_row(const float* p, float (&w)[RB]) {
+  if constexpr (RB % 4 == 0) {
 #pragma unroll
-  for (int f4 = 0; f4 < RB / 4; ++f4) {
-    const float4 v = reinterpret_cast<const float4*>(p)[f4];
-    w[4 * f4 + 0] = v.x; w[4 * f4 + 1] = v.y; w[4 * f4 + 2] = v.z; w[4 * f4 + 3] = v.w;
+    for (int f4 = 0; f4 < RB / 4; ++f4) {
+      const float4 v = reinterpret_cast<const float4*>(p)[f4];
+      w[4 * f4 + 0] = v.x; w[4 * f4 + 1] = v.y; w[4 * f4 + 2] = v.z; w[4 * f4 + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int f2 = 0; f2 < RB / 2; ++f2) {
+      const float2 v = reinterpret_cast<const float2*>(p)[f2];
+      w[2 * f2 + 0] = v.x; w[2 * f2 + 1] = v.y;
+    }
+  }
+}
+template <int RB>
+__device__ __forceinline__ void st_row(float* p, const float (&w)[RB]) {
+  if constexpr (RB % 4 == 0) {
+#pragma unroll
+    for (int f4 = 0; f4 < RB / 4; ++f4)
+      reinterpret_cast<float4*>(p)[f4] = make_float4(w[4 * f4], w[4 * f4 + 1], w[4 * f4 + 2], w[4 * f4 + 3]);
+  } else {
+#pragma unroll
+    for (int f2 = 0; f2 < RB / 2; ++f2) reinterpret_cast<float2*>(p)[f2] = make_float2(w[2 * f2], w[2 * f2 + 1]);
   }
 }
 
@@ -350,11 +380,7 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
       for (int c = 0; c < 4; ++c) {
         const int col = 4 * lt + c;
         if (col < ncol) {
-          float* d = Dg + ((int64_t)ul * ncol + col) * RB;
-#pragma unroll
-          for (int f4 = 0; f4 < RB / 4; ++f4)
-            reinterpret_cast<float4*>(d)[f4] = make_float4(acc[c][4 * f4], acc[c][4 * f4 + 1],
-                                                           acc[c][4 * f4 + 2], acc[c][4 * f4 + 3]);
+          st_row<RB>(Dg + ((int64_t)ul * ncol + col) * RB, acc[c]);
         }
 #pragma unroll
         for (int f = 0; f < RB; ++f) acc[c][f] = 0.f;
@@ -390,6 +416,115 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
       P[e] = sum;
     }
   }
+}
+
+// Pass A with the CTA's row space split into NTA contiguous ranges, one per team (all warps
+// but the inverse warp), each streamed through the team's own TMA ring: row g = (u, q) of the
+// CTA's own slices (contiguous in Y).  acc(c,f) += Y(u,q,col_c) U1(q,f) U2(u,f);
+// P = sum over teams (fp64, fixed order).  Ranges may cross slice boundaries.
+__device__ __forceinline__ void pass_a_range(int team, int NTA, int total, int* g0, int* g1) {
+  const int L = (total + NTA - 1) / NTA;
+  *g0 = min(total, team * L);
+  *g1 = min(total, *g0 + L);
+}
+
+template <int RB>
+__device__ __forceinline__ void team_pass_a(const float* __restrict__ region, int nu, int nrow, int ncol,
+                                            int pitch, const float* Uw, const float* U2s, float* rings,
+                                            int sfl, unsigned long long* bars, int T, int NTA, unsigned tseq,
+                                            double* P) {
+  const int tid = threadIdx.x;
+  const int team = tid / T, lt = tid - team * T;
+  const bool in_team = team < NTA;
+  const bool valid = in_team && 4 * lt < pitch;
+  const int trmax = sfl / pitch > 0 ? sfl / pitch : 1;
+  int g0 = 0, g1 = 0;
+  if (in_team) pass_a_range(team, NTA, nu * nrow, &g0, &g1);
+  const int total = (g1 - g0 + trmax - 1) / trmax;
+  float* ring = rings + (size_t)(in_team ? team : 0) * kTS * sfl;
+  unsigned long long* tb = bars + (in_team ? team : 0) * kTS;
+  auto issue = [&](int s) {
+    const int r0 = g0 + s * trmax, nr = min(trmax, g1 - r0);
+    const unsigned buf = (tseq + s) % kTS;
+    const unsigned bytes = (unsigned)(nr * pitch * sizeof(float));
+    mbar_expect_tx(&tb[buf], bytes);
+    bulk_g2s(ring + buf * sfl, region + (int64_t)r0 * pitch, bytes, &tb[buf]);
+  };
+  if (lt == 0 && total > 0) {
+    fence_proxy_async();
+    for (int s = 0; s < total && s < kTS; ++s) issue(s);
+  }
+  float acc[4][RB];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int f = 0; f < RB; ++f) acc[c][f] = 0.f;
+  float u2[RB];
+  int ul = g0 / nrow, q = g0 - ul * nrow;
+  if (in_team && g0 < g1) ld_row<RB>(U2s + ul * RB, u2);
+  for (int s = 0; s < total; ++s) {
+    const int r0 = g0 + s * trmax, nr = min(trmax, g1 - r0);
+    const unsigned buf = (tseq + s) % kTS;
+    mbar_wait(&tb[buf], ((tseq + s) / kTS) & 1u);
+    if (valid) {
+      const float* st = ring + buf * sfl + 4 * lt;
+#pragma unroll 2
+      for (int row = 0; row < nr; ++row) {
+        const float4 y = *reinterpret_cast<const float4*>(st + row * pitch);
+        float w[RB];
+        ld_row<RB>(Uw + q * RB, w);
+#pragma unroll
+        for (int f = 0; f < RB; ++f) w[f] *= u2[f];
+#pragma unroll
+        for (int f = 0; f < RB; ++f) {
+          acc[0][f] = fmaf(y.x, w[f], acc[0][f]);
+          acc[1][f] = fmaf(y.y, w[f], acc[1][f]);
+          acc[2][f] = fmaf(y.z, w[f], acc[2][f]);
+          acc[3][f] = fmaf(y.w, w[f], acc[3][f]);
+        }
+        if (++q == nrow) {   // next slice: its U2 row
+          q = 0;
+          ++ul;
+          if (r0 + row + 1 < g1) ld_row<RB>(U2s + ul * RB, u2);
+        }
+      }
+    } else if (in_team) {
+      // lanes without a column still track the slice cursor (uniform control flow)
+      q += nr;
+      while (q >= nrow) { q -= nrow; ++ul; }
+    }
+    team_bar(1 + team, T);   // stage consumed by the whole team
+    if (lt == 0 && s + kTS < total) {
+      fence_proxy_async();
+      issue(s + kTS);
+    }
+  }
+  __syncthreads();   // every team done: rings free (no copy in flight) -> reduction buffer
+  float* red = rings;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int f = 0; f < RB; ++f) red[(c * RB + f) * kCT + tid] = acc[c][f];
+  __syncthreads();
+  for (int e = tid; e < ncol * RB; e += kCT) {
+    const int col = e / RB, f = e - col * RB;
+    const float* rr = red + ((col & 3) * RB + f) * kCT + (col >> 2);
+    double v[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = t < NTA ? (double)rr[t * T] : 0.0;
+    double sum = 0.0;
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      if (t < NTA) sum += v[t];
+    P[e] = sum;
+  }
+}
+
+__device__ __forceinline__ int team_stages_a(int team, int NTA, int total, int pitch, int sfl) {
+  const int trmax = sfl / pitch > 0 ? sfl / pitch : 1;
+  int g0, g1;
+  pass_a_range(team, NTA, total, &g0, &g1);
+  return (g1 - g0 + trmax - 1) / trmax;
 }
 
 // stages a team consumes in one pass (the same formula as in team_pass)
@@ -506,9 +641,14 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       // warp 0: Vi = (G_o1 * G_o2)^-1 while the other warps stream
       if (warp == kCW - 1) warp_normal_inverse<RB>(G, m, R, Gs, Vi, W1, s_fc, &s_flags);
       if (m == 0) {
-        team_pass<RB, false>(regA, nu, nJ, nI, pI, U1s, U2s, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
-                             tseq, D, P);
-        if (myteam < Ly.NT) tseq += team_stages(myteam, nu, Ly.NT, nJ, pI, Ly.stage_fl);
+        if (Ly.sfla > 0) {
+          team_pass_a<RB>(regA, nu, nJ, nI, pI, U1s, U2s, ring, Ly.sfla, bars, Ly.T, Ly.NTA, tseq, P);
+          if (myteam < Ly.NTA) tseq += team_stages_a(myteam, Ly.NTA, nu * nJ, pI, Ly.sfla);
+        } else {
+          team_pass<RB, false>(regA, nu, nJ, nI, pI, U1s, U2s, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
+                               tseq, D, P);
+          if (myteam < Ly.NT) tseq += team_stages(myteam, nu, Ly.NT, nJ, pI, Ly.stage_fl);
+        }
         __syncthreads();   // the rings (reduction buffer) are re-armed by the next pass
         PH(1);
       } else {
@@ -580,24 +720,34 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
     }
     // ==================================== mode 2 ====================================
     if (warp == kCW - 1) warp_normal_inverse<RB>(G, 2, R, Gs, Vi, W1, s_fc, &s_flags);
-    // M2(u,f) = sum_q D(u,q,f) U1(q,f) for the own slices: warp per (u, f-group of 4)
+    // M2(u,f) = sum_q D(u,q,f) U1(q,f) for the own slices: warp per (u, f-group), on the
+    // warps other than the one inverting V2 (the two overlap)
     {
-      const int nfg = RB / 4;
+      constexpr int VW = RB % 4 == 0 ? 4 : 2;   // f-group width (vector loads)
+      const int nfg = RB / VW;
 #pragma unroll 1
-      for (int wi = warp; wi < nu * nfg; wi += kCW) {
-        const int ul = wi / nfg, f4 = wi - ul * nfg;
-        const float* d = D + (int64_t)ul * nJ * RB + 4 * f4;
+      for (int wi = warp; warp < kCW - 1 && wi < nu * nfg; wi += kCW - 1) {   // warp kCW-1: the inverse
+        const int ul = wi / nfg, fg = wi - ul * nfg;
+        const float* d = D + (int64_t)ul * nJ * RB + VW * fg;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         for (int q = lane; q < nJ; q += 32) {
-          const float4 dv = *reinterpret_cast<const float4*>(d + (int64_t)q * RB);
-          const float4 uv = *reinterpret_cast<const float4*>(U1s + q * RB + 4 * f4);
-          s0 += (double)dv.x * (double)uv.x; s1 += (double)dv.y * (double)uv.y;
-          s2 += (double)dv.z * (double)uv.z; s3 += (double)dv.w * (double)uv.w;
+          if constexpr (VW == 4) {
+            const float4 dv = *reinterpret_cast<const float4*>(d + (int64_t)q * RB);
+            const float4 uv = *reinterpret_cast<const float4*>(U1s + q * RB + 4 * fg);
+            s0 += (double)dv.x * (double)uv.x; s1 += (double)dv.y * (double)uv.y;
+            s2 += (double)dv.z * (double)uv.z; s3 += (double)dv.w * (double)uv.w;
+          } else {
+            const float2 dv = *reinterpret_cast<const float2*>(d + (int64_t)q * RB);
+            const float2 uv = *reinterpret_cast<const float2*>(U1s + q * RB + 2 * fg);
+            s0 += (double)dv.x * (double)uv.x; s1 += (double)dv.y * (double)uv.y;
+          }
         }
-        s0 = warp_sum_d(s0); s1 = warp_sum_d(s1); s2 = warp_sum_d(s2); s3 = warp_sum_d(s3);
+        s0 = warp_sum_d(s0); s1 = warp_sum_d(s1);
+        if (VW == 4) { s2 = warp_sum_d(s2); s3 = warp_sum_d(s3); }
         if (lane == 0) {
-          double* mr = Msh + ul * RB + 4 * f4;
-          mr[0] = s0; mr[1] = s1; mr[2] = s2; mr[3] = s3;
+          double* mr = Msh + ul * RB + VW * fg;
+          mr[0] = s0; mr[1] = s1;
+          if (VW == 4) { mr[2] = s2; mr[3] = s3; }
         }
       }
     }
@@ -712,7 +862,9 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
 // ---------------------------------------------------------------------------------------
 constexpr size_t kSmemCap = 227 * 1024 - 1024;   // minus the kernel's static smem
 
-static int rb_of(int R) { return R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32; }
+static int rb_of(int R) {
+  return R <= 4 ? 4 : R <= 8 ? 8 : R <= 10 ? 10 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
+}
 
 template <int RB>
 static cudaError_t cluster_setup(int CS, size_t smem) {
@@ -808,6 +960,7 @@ bool plan_als_cluster(const DenseAls& a, ClusterPlan* pl) {
   switch (rb_of(a.R)) {
     case 4: return plan_rb<4>(a, pl);
     case 8: return plan_rb<8>(a, pl);
+    case 10: return plan_rb<10>(a, pl);
     case 12: return plan_rb<12>(a, pl);
     case 16: return plan_rb<16>(a, pl);
     case 24: return plan_rb<24>(a, pl);
@@ -849,6 +1002,7 @@ cudaError_t run_als_cluster(const DenseAls& a, const ClusterPlan& pl, float* Dgl
   switch (pl.RB) {
     case 4: return cluster_launch<4>(a, pl, Dglob, st);
     case 8: return cluster_launch<8>(a, pl, Dglob, st);
+    case 10: return cluster_launch<10>(a, pl, Dglob, st);
     case 12: return cluster_launch<12>(a, pl, Dglob, st);
     case 16: return cluster_launch<16>(a, pl, Dglob, st);
     case 24: return cluster_launch<24>(a, pl, Dglob, st);

@@ -91,7 +91,19 @@ __global__ void x3_scatter_kernel(const int64_t* __restrict__ x3l, const int32_t
     x3g[kmap[l]] = x3l[l];
 }
 
+__global__ void add_i64_kernel(int64_t* __restrict__ dst, const int64_t* __restrict__ src, int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] += src[e];
+}
+
 }  // namespace
+
+cudaError_t launch_add_i64(int64_t* dst, const int64_t* src, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t b = ceil_div(n, kDT);
+  add_i64_kernel<<<(unsigned)(b < 1024 ? b : 1024), kDT, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_slice_gather(const DenseView& X, const SliceJob* jobs, int njobs, const int32_t* Is_all,
                                 const int32_t* Js_all, int nI, int nJ, int pI, int pJ, cudaStream_t st) {

@@ -12,4 +12,6 @@ for f in ("gpurun_out/t_bench_c2.log", "gpurun_out/t_bench_c4.log"):
             d = json.loads(ln)
             print(f, round(d["ms_per_step"], 3), "value %.3g" % d["value"], "e2e %.3g" % d.get("e2e", {}).get("value", 0),
                   "frac %.3f" % d["roofline"]["frac"], {k: round(v, 3) for k, v in d["step_ms"].items()})
+            v = d.get("variants", {}).get("incremental_marginals")
+            if v: print("   incremental:", round(v["ms_per_step"], 3), "value %.3g" % v["value"], {k: round(x, 3) for k, x in v["step_ms"].items()})
 PY
