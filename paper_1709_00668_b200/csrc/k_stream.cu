@@ -335,10 +335,18 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) fit_stream_kernel(
         for (int r = ra + ((grp - ra) % g.ng + g.ng) % g.ng; r < rb2; r += g.ng) {
           const float* wr = BRES ? W + (size_t)(jbase + r - ra) * RB : W + r * RB;
           float w[RB];
+          if constexpr (RB % 4 == 0) {
 #pragma unroll
-          for (int f4 = 0; f4 < RB / 4; ++f4) {
-            const float4 wv = *reinterpret_cast<const float4*>(wr + 4 * f4);
-            w[4 * f4] = wv.x; w[4 * f4 + 1] = wv.y; w[4 * f4 + 2] = wv.z; w[4 * f4 + 3] = wv.w;
+            for (int f4 = 0; f4 < RB / 4; ++f4) {
+              const float4 wv = *reinterpret_cast<const float4*>(wr + 4 * f4);
+              w[4 * f4] = wv.x; w[4 * f4 + 1] = wv.y; w[4 * f4 + 2] = wv.z; w[4 * f4 + 3] = wv.w;
+            }
+          } else {
+#pragma unroll
+            for (int f2 = 0; f2 < RB / 2; ++f2) {
+              const float2 wv = *reinterpret_cast<const float2*>(wr + 2 * f2);
+              w[2 * f2] = wv.x; w[2 * f2 + 1] = wv.y;
+            }
           }
 #pragma unroll
           for (int u = 0; u < QPT; ++u) {
@@ -619,6 +627,7 @@ cudaError_t launch_fit_stream_partial(const DenseView& X, const float* lam, cons
   }
   if (R <= 4) return fit_partial_rb<4>(X, lam, A, B, C, R, kmap, ws, out2, st);
   if (R <= 8) return fit_partial_rb<8>(X, lam, A, B, C, R, kmap, ws, out2, st);
+  if (R <= 10) return fit_partial_rb<10>(X, lam, A, B, C, R, kmap, ws, out2, st);
   if (R <= 12) return fit_partial_rb<12>(X, lam, A, B, C, R, kmap, ws, out2, st);
   if (R <= 16) return fit_partial_rb<16>(X, lam, A, B, C, R, kmap, ws, out2, st);
   return cudaErrorInvalidValue;
@@ -637,6 +646,7 @@ cudaError_t launch_fit_stream(const DenseView& X, const float* lam, const float*
                               const float* C, int R, double* ws, double* relerr, cudaStream_t st) {
   if (R <= 4) return fit_stream_rb<4>(X, lam, A, B, C, R, ws, relerr, st);
   if (R <= 8) return fit_stream_rb<8>(X, lam, A, B, C, R, ws, relerr, st);
+  if (R <= 10) return fit_stream_rb<10>(X, lam, A, B, C, R, ws, relerr, st);
   if (R <= 12) return fit_stream_rb<12>(X, lam, A, B, C, R, ws, relerr, st);
   if (R <= 16) return fit_stream_rb<16>(X, lam, A, B, C, R, ws, relerr, st);
   return cudaErrorInvalidValue;   // callers use the tiled kernel for R > 16
