@@ -243,7 +243,7 @@ __device__ __forceinline__ bool warp_spd_inverse_reg(const double* V, double* Vi
       double fcol[RB];
 #pragma unroll
       for (int i = 0; i < RB; ++i) fcol[i] = __shfl_sync(0xffffffffu, col[i], j);
-      col[j] = col[j] / piv;
+      col[j] = col[j] * __drcp_rn(piv);   // correctly rounded reciprocal: ~4x shorter chain than a division
 #pragma unroll
       for (int i = 0; i < RB; ++i)
         if (i < R && i != j) col[i] = fma(-fcol[i], col[j], col[i]);
@@ -562,6 +562,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
   float* ring = reinterpret_cast<float*>(smem + Ly.stage);
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + Ly.bars);
   __shared__ double s_fc[kMaxR];
+  __shared__ double s_linv[kMaxR];   // 1 / lambda_f (1 for a zero column)
   __shared__ double s_red[32];
   __shared__ int s_flags, s_stop;
   __shared__ double s_fit;
@@ -698,13 +699,15 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
 #pragma unroll 1
       for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = cluster_sum(Gp, m * RB * RB + pr, CS);
       __syncthreads();
-      if (tid < R) lam[tid] = sqrt(Gs[tid * R + tid]);
+      if (tid < R) {
+        lam[tid] = sqrt(Gs[tid * R + tid]);
+        s_linv[tid] = lam[tid] > 0.0 ? __drcp_rn(lam[tid]) : 1.0;
+      }
       __syncthreads();
 #pragma unroll 1
       for (int pr = tid; pr < RR; pr += kCT) {
         const int f = pr / R, g = pr - f * R;
-        const double lf = lam[f] > 0.0 ? lam[f] : 1.0, lg = lam[g] > 0.0 ? lam[g] : 1.0;
-        G[m * RB * RB + pr] = Gs[pr] / (lf * lg);
+        G[m * RB * RB + pr] = Gs[pr] * (s_linv[f] * s_linv[g]);
       }
       float* Us = m == 0 ? U0s : U1s;
 #pragma unroll 1
@@ -712,45 +715,50 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         const int p = e / R, f = e - p * R;
         const int c = p / ch;
         const double x = cluster.map_shared_rank(Xun, c)[(p - c * ch) * RB + f];
-        const double l = lam[f];
-        Us[p * RB + f] = __double2float_rn(l > 0.0 ? x / l : x);
+        Us[p * RB + f] = __double2float_rn(x * s_linv[f]);
       }
       __syncthreads();
       PH(m == 0 ? 5 : 11);
     }
     // ==================================== mode 2 ====================================
+#ifdef SBT_ALS_PHASES
+    const long long tinv0 = clock64();
+#endif
     if (warp == kCW - 1) warp_normal_inverse<RB>(G, 2, R, Gs, Vi, W1, s_fc, &s_flags);
-    // M2(u,f) = sum_q D(u,q,f) U1(q,f) for the own slices: warp per (u, f-group), on the
-    // warps other than the one inverting V2 (the two overlap)
-    {
-      constexpr int VW = RB % 4 == 0 ? 4 : 2;   // f-group width (vector loads)
-      const int nfg = RB / VW;
+#ifdef SBT_ALS_PHASES
+    if (warp == kCW - 1 && lane == 0 && rep == 0 && rank == 0) atomicAdd(&g_als_phase[20], (unsigned long long)(clock64() - tinv0));
+    if (tid == 0 && rep == 0 && rank == 0) atomicAdd(&g_als_phase[22], 1ull);
+#endif
+    // M2(u,f) = sum_q D(u,q,f) U1(q,f) for the own slices: a warp per slice (the warps other
+    // than the one inverting V2, which overlaps): lane partials over q = lane + 32 t in fp32
+    // (<= nJ / 32 terms), then one fp64 butterfly per f
 #pragma unroll 1
-      for (int wi = warp; warp < kCW - 1 && wi < nu * nfg; wi += kCW - 1) {   // warp kCW-1: the inverse
-        const int ul = wi / nfg, fg = wi - ul * nfg;
-        const float* d = D + (int64_t)ul * nJ * RB + VW * fg;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        for (int q = lane; q < nJ; q += 32) {
-          if constexpr (VW == 4) {
-            const float4 dv = *reinterpret_cast<const float4*>(d + (int64_t)q * RB);
-            const float4 uv = *reinterpret_cast<const float4*>(U1s + q * RB + 4 * fg);
-            s0 += (double)dv.x * (double)uv.x; s1 += (double)dv.y * (double)uv.y;
-            s2 += (double)dv.z * (double)uv.z; s3 += (double)dv.w * (double)uv.w;
-          } else {
-            const float2 dv = *reinterpret_cast<const float2*>(d + (int64_t)q * RB);
-            const float2 uv = *reinterpret_cast<const float2*>(U1s + q * RB + 2 * fg);
-            s0 += (double)dv.x * (double)uv.x; s1 += (double)dv.y * (double)uv.y;
-          }
-        }
-        s0 = warp_sum_d(s0); s1 = warp_sum_d(s1);
-        if (VW == 4) { s2 = warp_sum_d(s2); s3 = warp_sum_d(s3); }
-        if (lane == 0) {
-          double* mr = Msh + ul * RB + VW * fg;
-          mr[0] = s0; mr[1] = s1;
-          if (VW == 4) { mr[2] = s2; mr[3] = s3; }
-        }
+    for (int ul = warp; warp < kCW - 1 && ul < nu; ul += kCW - 1) {
+      const float* d = D + (int64_t)ul * nJ * RB;
+      float pa[RB];
+#pragma unroll
+      for (int f = 0; f < RB; ++f) pa[f] = 0.f;
+      for (int q = lane; q < nJ; q += 32) {
+        float dv[RB], uv[RB];
+        ld_row<RB>(d + (int64_t)q * RB, dv);
+        ld_row<RB>(U1s + q * RB, uv);
+#pragma unroll
+        for (int f = 0; f < RB; ++f) pa[f] = fmaf(dv[f], uv[f], pa[f]);
       }
+      double sv[RB];
+#pragma unroll
+      for (int f = 0; f < RB; ++f) sv[f] = (double)pa[f];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int f = 0; f < RB; ++f) sv[f] += __shfl_xor_sync(0xffffffffu, sv[f], o);
+      if (lane == 0)
+#pragma unroll
+        for (int f = 0; f < RB; ++f) Msh[ul * RB + f] = sv[f];
     }
+#ifdef SBT_ALS_PHASES
+    if (tid == 0 && rep == 0 && rank == 0) atomicAdd(&g_als_phase[21], (unsigned long long)(clock64() - tinv0));
+#endif
     __syncthreads();
     PH(12);
 #pragma unroll 1
@@ -783,20 +791,20 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
 #pragma unroll 1
     for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = cluster_sum(Gp, 2 * RB * RB + pr, CS);
     __syncthreads();
-    if (tid < R) lam[tid] = sqrt(Gs[tid * R + tid]);
+    if (tid < R) {
+      lam[tid] = sqrt(Gs[tid * R + tid]);
+      s_linv[tid] = lam[tid] > 0.0 ? __drcp_rn(lam[tid]) : 1.0;
+    }
     __syncthreads();
 #pragma unroll 1
     for (int pr = tid; pr < RR; pr += kCT) {
       const int f = pr / R, g = pr - f * R;
-      const double lf = lam[f] > 0.0 ? lam[f] : 1.0, lg = lam[g] > 0.0 ? lam[g] : 1.0;
-      G[2 * RB * RB + pr] = Gs[pr] / (lf * lg);
+      G[2 * RB * RB + pr] = Gs[pr] * (s_linv[f] * s_linv[g]);
     }
 #pragma unroll 1
     for (int e = tid; e < nu * R; e += kCT) {
       const int ul = e / R, f = e - ul * R;
-      const double l = lam[f];
-      const double x = Xun2[ul * RB + f];
-      U2s[ul * RB + f] = __double2float_rn(l > 0.0 ? x / l : x);
+      U2s[ul * RB + f] = __double2float_rn(Xun2[ul * RB + f] * s_linv[f]);
     }
     __syncthreads();
     // fit (warp 0; every CTA computes the same value -> uniform control flow)
@@ -980,7 +988,7 @@ void als_phase_dump() {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(h, g_als_phase, sizeof(h));
   fprintf(stderr, "[sambaten] als phases (cycles, rank 0 of rep 0):");
-  for (int k = 0; k < 20; ++k) fprintf(stderr, " %d:%llu", k, h[k]);
+  for (int k = 0; k < 23; ++k) fprintf(stderr, " %d:%llu", k, h[k]);
   fprintf(stderr, "\n");
   memset(h, 0, sizeof(h));
   cudaMemcpyToSymbol(g_als_phase, h, sizeof(h));
