@@ -12,12 +12,12 @@ second per update.  Rank 0 prints one JSON line.
 Timing: W untimed warm-up steps, then K steps, each bracketed by a barrier and a device
 synchronisation and timed with CUDA events on the library's stream; L2 is flushed (a 512 MB
 write) before every step; the stream cycles through the config's batches, restoring the
-K0 checkpoint (untimed) after the last one.  Multi-GPU (torchrun, dense configs): ONE update
-of the same workload sharded over the N ranks (sambaten_init_factors_dist: time-mode slabs,
+K0 checkpoint (untimed) after the last one.  Multi-GPU (torchrun): ONE update of the same
+workload sharded over the N ranks (sambaten_init_factors_dist: time-mode slabs,
 int64 allreduce of the marginals, all-to-all-v of summary slices, repetition rho on rank
 rho mod N, allgather before the replicated merge; DESIGN.md "Multi-GPU") -- strong scaling;
-the time is the max over ranks and `value` counts the batch's entries once.  COO configs at
-N>1 run independent replicas (weak scaling).
+the time is the max over ranks and `value` counts the batch's entries once (dense and COO
+stores alike).
 """
 import argparse
 import json
@@ -296,6 +296,15 @@ def init_single(L, work, w, opts, config):
                                    work.model[3], work.model[0], opts)
 
 
+def slab_of(x, k0, n, coo):
+    """Slices [k0, k0 + n) of a dense (K, J, I) array or of a canonical COO (k re-based to 0)."""
+    if not coo:
+        return x[k0:k0 + n]
+    from synth import CooArrays
+    a, b = np.searchsorted(x.k, [k0, k0 + n])
+    return CooArrays(x.i[a:b], x.j[a:b], (x.k[a:b] - k0).astype(np.int32), x.v[a:b], (x.dims[0], x.dims[1], n))
+
+
 def partition(n, world, rank):
     """The library's balanced split (sambaten_batch_partition's rule) of n slices."""
     base, rem = divmod(n, world)
@@ -396,7 +405,7 @@ def main():
     if device_gen:
         work = DeviceWork(w, world, rank)
 
-    sharded = (world > 1 or args.sharded) and not work.coo
+    sharded = world > 1 or args.sharded
     stream = torch.cuda.Stream()
     # C3's community tensor has no planted model; with R = 15 and 30 summary iterations the
     # acceptance test (R26, tau = 0.9) can reject every repetition, so the COO workloads run
@@ -418,18 +427,21 @@ def main():
             box = [nid]
             dist.broadcast_object_list(box, src=0)
             nid = box[0]
+        if work.model is None:
+            # C3: the initial model = full CP-ALS of X0, computed identically on every rank
+            L.sambaten_destroy(init_single(L, work, w, opts, config))
         k0b, k0n = partition(w.K0, world, rank)
         if device_gen:
             x0buf = torch.empty((k0n, w.J, w.I), dtype=torch.float32, device="cuda")
             work.gen(x0buf, k0b, k0n)
             X0 = L.dense(x0buf)
         else:
-            X0 = work.tensor(L, work.X0[k0b:k0b + k0n], device=True)
+            X0 = work.tensor(L, slab_of(work.X0, k0b, k0n, work.coo), device=True)
         dd = L.make_dist(rank, world, nid, k0b, w.K0)
         h = L.sambaten_init_factors_dist(X0, dd, w.R, w.s, w.r, w.seed, work.model[1], work.model[2],
                                          work.model[3], work.model[0], opts)
-        parts = [L.sambaten_batch_partition(h, b.shape[0]) for b in work.batches]
-        local_batches = [b[pb:pb + pn] for b, (pb, pn) in zip(work.batches, parts)]
+        parts = [L.sambaten_batch_partition(h, b.dims[2] if work.coo else b.shape[0]) for b in work.batches]
+        local_batches = [slab_of(b, pb, pn, work.coo) for b, (pb, pn) in zip(work.batches, parts)]
         config["parallelism"] = f"sharded over {world} rank(s): time-mode slabs, rep rho on rank rho mod {world}"
         config["slab"] = [k0b, k0n]
     else:
@@ -499,7 +511,7 @@ def main():
             e2e_times.append(ms)
             e2e_ents.append(ne)
             lb = local_batches[bi]
-            e2e_in.append(int(lb.nbytes) if sharded else work.bytes_in(bi))
+            e2e_in.append((int(lb.nnz) * 16 if work.coo else int(lb.nbytes)) if sharded else work.bytes_in(bi))
     tot = sum(times) / 1000.0
     e2e_tot = sum(e2e_times) / 1000.0 if e2e_times else None
     if world > 1:

@@ -608,7 +608,7 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
                                const int32_t* u, const float* v, const int64_t* d_off, int64_t ntot,
                                int nI, int nJ, int nK, int r, float* U0, float* U1, float* U2,
                                uint64_t seed, uint32_t uid, int maxit, double tol, bool init_factors,
-                               DenseAls* d, int* launches) {
+                               DenseAls* d, int* launches, uint32_t rep0 = 0, uint32_t rep_stride = 1) {
   const int64_t maxn = std::max<int64_t>(nI, std::max<int64_t>(nJ, nK));
   const int kb0 = bits_for(nI), kb1 = bits_for(nJ), kb2 = bits_for(nK);
   const int64_t n = std::max<int64_t>(ntot, 1);
@@ -686,7 +686,7 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     a.M[0] = M0; a.m_stride[0] = (int64_t)nI * R;
     a.M[1] = a.M[2] = Mb; a.m_stride[1] = a.m_stride[2] = maxn * R;
     a.done = done;
-    if (e == cudaSuccess && init_factors) e = launch_als_init_factors(*d, seed, uid, 0, st);
+    if (e == cudaSuccess && init_factors) e = launch_als_init_factors(*d, seed, uid, rep0, st, rep_stride);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(done, 0, sizeof(int) * r, st);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(iters, 0, sizeof(int) * r, st);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(flags, 0, sizeof(int) * r, st);
@@ -895,6 +895,8 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
                        launches, bn, Aout, Bout, Cout, lamout, info);
 }
 
+static sambaten_status update_coo_dist(sambaten_t h, const sambaten_tensor* batch, float* Aout, float* Bout,
+                                       float* Cout, float* lamout, sambaten_info* info);
 static sambaten_status update_dense_dist(sambaten_t h, const sambaten_tensor* batch, float* Aout,
                                          float* Bout, float* Cout, float* lamout, sambaten_info* info);
 
@@ -906,7 +908,9 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   if (batch->fmt != h->fmt) FAIL(SAMBATEN_E_INVALID, "update: batch format differs from the state's");
   if (batch->dims[0] != h->I || batch->dims[1] != h->J)
     FAIL(SAMBATEN_E_SHAPE, "update: batch I x J differs from the state's (S:68)");
-  if (h->dist) return update_dense_dist(h, batch, Aout, Bout, Cout, lamout, info);
+  if (h->dist)
+    return h->fmt == SAMBATEN_COO ? update_coo_dist(h, batch, Aout, Bout, Cout, lamout, info)
+                                  : update_dense_dist(h, batch, Aout, Bout, Cout, lamout, info);
   const int64_t Kn = batch->dims[2];
   if (Kn < 1) FAIL(SAMBATEN_E_EMPTY_BATCH, "update: empty batch (S:275)");
   if (h->fmt == SAMBATEN_COO) return update_coo(h, batch, Aout, Bout, Cout, lamout, info);

@@ -194,6 +194,9 @@ cudaError_t launch_coo_gather_write(const CooView& X, const uint32_t* mI, const 
 size_t scan_ws_elems(int64_t n);
 cudaError_t exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* ws, cudaStream_t st);
 size_t radix_ws_elems(int64_t n);
+cudaError_t launch_coo_permute4(const int32_t* perm, const int32_t* a, const int32_t* b, const int32_t* c,
+                                const float* v, int64_t n, int32_t* oa, int32_t* ob, int32_t* oc, float* ov,
+                                cudaStream_t st);
 cudaError_t coo_sort_by_index(const int32_t* idx, const int64_t* off, int r, int kb, int64_t n,
                               uint32_t* keys, int32_t* perm, uint32_t* ws_keys, int32_t* ws_vals,
                               int64_t* hist, int64_t* offs, int64_t* sws, cudaStream_t st);
@@ -204,6 +207,9 @@ cudaError_t coo_row_pointers(const uint32_t* sorted_keys, int64_t n, int kb, int
 cudaError_t launch_coo_mttkrp(const CooAls& a, int mode, cudaStream_t st);
 cudaError_t launch_coo_sumsq(const float* v, const int64_t* off, int r, double* ysq, cudaStream_t st);
 size_t coo_fit_ws_doubles(int64_t I, int64_t J, int64_t K);
+cudaError_t launch_coo_fit_partial(const CooView& X, const float* lam, const float* A, const float* B,
+                                   const float* C, int R, const int32_t* kmap, double* ws, double* out2,
+                                   cudaStream_t st);
 cudaError_t launch_coo_fit(const CooView& X, const float* lam, const float* A, const float* B,
                            const float* C, int R, double* ws, double* relerr, cudaStream_t st);
 cudaError_t launch_coo_max_phi(const float* v, int64_t n, int moi, unsigned long long* out, cudaStream_t st);
@@ -250,6 +256,8 @@ cudaError_t launch_slice_gather(const DenseView& X, const SliceJob* jobs, int nj
                                 const int32_t* Js_all, int nI, int nJ, int pI, int pJ, cudaStream_t st);
 cudaError_t launch_slice_copy(const CopyJob* jobs, int njobs, int64_t nY, int64_t nYt, cudaStream_t st);
 cudaError_t launch_add_i64(int64_t* dst, const int64_t* src, int64_t n, cudaStream_t st);
+cudaError_t launch_local_kmaps(const int32_t* kmap, int64_t Kl, const uint32_t* mK, const int32_t* locK, int64_t Ko,
+                               int nKs, int r, uint32_t* mKl, int32_t* locKl, cudaStream_t st);
 cudaError_t launch_x3_scatter(const int64_t* x3l, const int32_t* kmap, int64_t n, int64_t* x3g,
                               cudaStream_t st);
 // fit partials of a slab: inner/sq summed into out2[0..1] (kmap: local slice -> global row of C)

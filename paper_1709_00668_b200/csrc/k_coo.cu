@@ -389,6 +389,20 @@ __global__ void permute3_kernel(const int32_t* __restrict__ perm, const int32_t*
   }
 }
 
+__global__ void permute4_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ ia,
+                                const int32_t* __restrict__ ib, const int32_t* __restrict__ ic,
+                                const float* __restrict__ v, int64_t n, int32_t* __restrict__ sa,
+                                int32_t* __restrict__ sb, int32_t* __restrict__ sc, float* __restrict__ sv) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = perm[t];
+    sa[t] = ia[x];
+    sb[t] = ib[x];
+    sc[t] = ic[x];
+    sv[t] = v[x];
+  }
+}
+
 // One warp per piece: lane l takes entries l, l+32, ... (fp32 products, fp64 per-lane sums),
 // then a fixed butterfly.  (A half-warp-per-entry variant with coalesced row gathers measured
 // slower on C3: fewer entries in flight per warp.)
@@ -494,7 +508,7 @@ __global__ void coo_fit_kernel(const int32_t* __restrict__ ii, const int32_t* __
                                const int32_t* __restrict__ kk, const float* __restrict__ vv, int64_t n,
                                const float* __restrict__ lam, const float* __restrict__ A,
                                const float* __restrict__ B, const float* __restrict__ C, int R,
-                               double* __restrict__ part) {
+                               double* __restrict__ part, const int32_t* __restrict__ kmap) {
   __shared__ double red[32];
   __shared__ float ls[RB];
   if (threadIdx.x < RB) ls[threadIdx.x] = threadIdx.x < R ? lam[threadIdx.x] : 0.f;
@@ -505,7 +519,7 @@ __global__ void coo_fit_kernel(const int32_t* __restrict__ ii, const int32_t* __
     const float v = vv[e];
     const float* a = A + (int64_t)ii[e] * R;
     const float* b = B + (int64_t)jj[e] * R;
-    const float* c = C + (int64_t)kk[e] * R;
+    const float* c = C + (int64_t)(kmap ? kmap[kk[e]] : kk[e]) * R;   // kmap: local -> global slice
     float m = 0.f;
 #pragma unroll
     for (int f = 0; f < RB; ++f)
@@ -590,6 +604,14 @@ size_t radix_ws_elems(int64_t n) { return 256 * (size_t)ceil_div(n > 0 ? n : 1, 
 // Sort the composite keys (rep << kb | idx[e]) stably; perm receives the entry order, keys the
 // sorted keys.  ws_keys/ws_vals: n elements each; hist/offs: radix_ws_elems(n) int64 each,
 // sws: scan workspace.
+cudaError_t launch_coo_permute4(const int32_t* perm, const int32_t* a, const int32_t* b, const int32_t* c,
+                                const float* v, int64_t n, int32_t* oa, int32_t* ob, int32_t* oc, float* ov,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  permute4_kernel<<<grid_for(n), kCT, 0, st>>>(perm, a, b, c, v, n, oa, ob, oc, ov);
+  return cudaGetLastError();
+}
+
 cudaError_t coo_sort_by_index(const int32_t* idx, const int64_t* off, int r, int kb, int64_t n,
                               uint32_t* keys, int32_t* perm, uint32_t* ws_keys, int32_t* ws_vals,
                               int64_t* hist, int64_t* offs, int64_t* sws, cudaStream_t st) {
@@ -697,19 +719,46 @@ size_t coo_fit_ws_doubles(int64_t I, int64_t J, int64_t K) {
   return 2 * (size_t)kNumSMs * 4 + 3 * kMaxR * kMaxR + 8 + gram3_ws_doubles(I, J, K, kMaxR);
 }
 
+static cudaError_t coo_fit_parts(const CooView& X, const float* lam, const float* A, const float* B,
+                                 const float* C, int R, const int32_t* kmap, double* ws, int nb, cudaStream_t st) {
+  switch (R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32) {
+    case 4: coo_fit_kernel<4><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws, kmap); break;
+    case 8: coo_fit_kernel<8><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws, kmap); break;
+    case 12: coo_fit_kernel<12><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws, kmap); break;
+    case 16: coo_fit_kernel<16><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws, kmap); break;
+    case 24: coo_fit_kernel<24><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws, kmap); break;
+    default: coo_fit_kernel<32><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws, kmap); break;
+  }
+  return cudaGetLastError();
+}
+
+__global__ void coo_sum_parts_kernel(const double* part, int nb, double* out2) {
+  if (threadIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (int i = 0; i < nb; ++i) { a += part[2 * i]; b += part[2 * i + 1]; }
+  out2[0] = a;
+  out2[1] = b;
+}
+
+// sharded fit: this rank's (<X, M>, ||X||^2) over its local store (k local, kmap to global C rows)
+cudaError_t launch_coo_fit_partial(const CooView& X, const float* lam, const float* A, const float* B,
+                                   const float* C, int R, const int32_t* kmap, double* ws, double* out2,
+                                   cudaStream_t st) {
+  const int nb = kNumSMs * 4;
+  if (X.nnz <= 0) return cudaMemsetAsync(out2, 0, 2 * sizeof(double), st);
+  cudaError_t e = coo_fit_parts(X, lam, A, B, C, R, kmap, ws, nb, st);
+  if (e != cudaSuccess) return e;
+  coo_sum_parts_kernel<<<1, 32, 0, st>>>(ws, nb, out2);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_coo_fit(const CooView& X, const float* lam, const float* A, const float* B,
                            const float* C, int R, double* ws, double* relerr, cudaStream_t st) {
   const int nb = kNumSMs * 4;
   double* G = ws + 2 * nb;
-  switch (R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32) {
-    case 4: coo_fit_kernel<4><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
-    case 8: coo_fit_kernel<8><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
-    case 12: coo_fit_kernel<12><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
-    case 16: coo_fit_kernel<16><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
-    case 24: coo_fit_kernel<24><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
-    default: coo_fit_kernel<32><<<nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, lam, A, B, C, R, ws); break;
-  }
-  cudaError_t e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
+  cudaError_t e = coo_fit_parts(X, lam, A, B, C, R, nullptr, ws, nb, st);
+  if (e != cudaSuccess) return e;
+  e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
   if (e != cudaSuccess) return e;
   coo_fit_combine_kernel<<<1, 32, 0, st>>>(ws, nb, G, lam, R, relerr);
   return cudaGetLastError();

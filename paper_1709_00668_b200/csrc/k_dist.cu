@@ -96,7 +96,29 @@ __global__ void add_i64_kernel(int64_t* __restrict__ dst, const int64_t* __restr
     dst[e] += src[e];
 }
 
+// COO sharded gather: per-rep membership / local-index maps over this rank's LOCAL slices.
+// kg = kmap[kl]; mKl[kl] = mK[kg] (bit rho: slice sampled in rep rho, new slices every rep);
+// locKl[rho][kl] = u of slice kg in rep rho's K' (locK for old slices, nKs + kg - Ko for new).
+__global__ void local_kmaps_kernel(const int32_t* __restrict__ kmap, int64_t Kl, const uint32_t* __restrict__ mK,
+                                   const int32_t* __restrict__ locK, int64_t Ko, int nKs, int r,
+                                   uint32_t* __restrict__ mKl, int32_t* __restrict__ locKl) {
+  for (int64_t kl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; kl < Kl; kl += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t kg = kmap[kl];
+    mKl[kl] = mK[kg];
+    for (int rho = 0; rho < r; ++rho)
+      locKl[(int64_t)rho * Kl + kl] = kg < Ko ? locK[(int64_t)rho * Ko + kg] : (int32_t)(nKs + (kg - Ko));
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_local_kmaps(const int32_t* kmap, int64_t Kl, const uint32_t* mK, const int32_t* locK, int64_t Ko,
+                               int nKs, int r, uint32_t* mKl, int32_t* locKl, cudaStream_t st) {
+  if (Kl <= 0) return cudaSuccess;
+  const int64_t b = ceil_div(Kl, kDT);
+  local_kmaps_kernel<<<(unsigned)(b < 1024 ? b : 1024), kDT, 0, st>>>(kmap, Kl, mK, locK, Ko, nKs, r, mKl, locKl);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_add_i64(int64_t* dst, const int64_t* src, int64_t n, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;

@@ -177,3 +177,60 @@ def test_sharded_decomposition_equals_single_process_oracle(world, tmp_path):
     out = tmp_path / "done"
     _run(world, _update_worker, str(out))
     assert out.read_text() == "ok"
+
+
+# ------------------------------------------------------------- 3. the sharded COO summaries
+def _coo_worker(rank, world, out_path):
+    """COO store sharded by slice ownership (X0 slabs, then every batch split by the partition
+    rule, so after the first update a rank's old slices interleave with the others'): local
+    marginals + all-reduce equal the global ones; each rank's local gather of a summary
+    (canonical within its slices), concatenated on the owner in rank order and stably sorted by
+    u, equals the gather over the whole tensor -- the owner assembly of the sharded COO update."""
+    from synth import zipf_planted_coo, split_coo
+    I, J, K, R, K0, bs = 300, 240, 60, 3, 40, 5
+    Xa, truth = zipf_planted_coo(I, J, K, R, 30000, alpha=1.2, seed=3)
+    X = O.Coo(Xa.i.astype(np.int64), Xa.j.astype(np.int64), Xa.k.astype(np.int64), Xa.v, Xa.dims)
+    owner = np.empty(K, np.int64)
+    b0, n0 = partition(K0, world, rank)
+    for g in range(world):
+        gb, gn = partition(K0, world, g)
+        owner[gb:gb + gn] = g
+    for k0 in range(K0, K, bs):
+        kn = min(bs, K - k0)
+        for g in range(world):
+            gb, gn = partition(kn, world, g)
+            owner[k0 + gb:k0 + gb + gn] = g
+    S = O.fixed_point_scale(X.nnz, float(np.abs(X.v).max()))
+    for Ko in (K0, K0 + bs, K0 + 2 * bs):      # three consecutive updates
+        Kt = Ko + bs
+        sel = X.k < Kt
+        full = O.Coo(X.i[sel], X.j[sel], X.k[sel], X.v[sel], (I, J, Kt))
+        mine = sel & (owner[X.k] == rank)
+        loc = O.Coo(X.i[mine], X.j[mine], X.k[mine], X.v[mine], (I, J, Kt))
+        x = np.concatenate(O.marginals_coo(loc, S, O.MOI_ABS)).astype(np.int64)
+        t = torch.from_numpy(x.copy())
+        dist.all_reduce(t)
+        g1, g2, g3 = O.marginals_coo(full, S, O.MOI_ABS)
+        assert np.array_equal(t.numpy(), np.concatenate([g1, g2, g3]))
+        for rho in range(2 * world):
+            Is = O.sample_mode(g1, O.sample_size(I, 2), 5, 1, rho, 0)
+            Js = O.sample_mode(g2, O.sample_size(J, 2), 5, 1, rho, 1)
+            Ks = O.sample_mode(g3[:Ko], O.sample_size(Ko, 2), 5, 1, rho, 2)
+            Kp = O.k_prime(Ks, Ko, bs)
+            part = O.gather_coo(loc, Is, Js, Kp)
+            parts = [None] * world
+            dist.all_gather_object(parts, (part.i, part.j, part.k, part.v))
+            cat = [np.concatenate([p[a] for p in parts]) for a in range(4)]
+            order = np.argsort(cat[2], kind="stable")   # stable sort by u
+            ref = O.gather_coo(full, Is, Js, Kp)
+            for got, want in zip((c[order] for c in cat), (ref.i, ref.j, ref.k, ref.v)):
+                assert np.array_equal(got, want)
+    if rank == 0:
+        open(out_path, "w").write("ok")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_coo_summaries_equal_full_gather(world, tmp_path):
+    out = tmp_path / "done"
+    _run(world, _coo_worker, str(out))
+    assert out.read_text() == "ok"

@@ -55,3 +55,54 @@ def test_world1_dist_handle_matches_single_gpu_bitwise(loopback):
     r = subprocess.run([sys.executable, "-c", "ROOT = %r\n" % ROOT + SCRIPT], env=env, capture_output=True,
                        text=True, timeout=600)
     assert "DIST_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+SCRIPT_COO = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, ROOT)
+from paper_1709_00668_b200 import _lib as L
+from synth import zipf_planted_coo, split_coo
+I, J, K, R, K0, bs = 400, 300, 60, 4, 40, 5
+X, truth = zipf_planted_coo(I, J, K, R, 40000, alpha=1.2, seed=6)
+X0, batches = split_coo(X, K0, bs)
+model = [np.ascontiguousarray(np.asarray(x, np.float32)) for x in (truth[0], truth[1], truth[2], truth[3][:K0])]
+def coo(x):
+    return L.coo(*[torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (x.i, x.j, x.k, x.v)], x.dims)
+opts = L.default_opts(als_max_iters=8, als_tol=0.0, capacity=X.nnz, full_fit=1, accept_tau=0.0,
+                      incremental_marginals=INC)
+opts.capacity_k = K
+dist = L.make_dist(0, 1, L.sambaten_dist_unique_id(), 0, K0)
+hd = L.sambaten_init_factors_dist(coo(X0), dist, R, 2, 4, 9, model[1], model[2], model[3], model[0], opts)
+hs = L.sambaten_init_factors(coo(X0), R, 2, 4, 9, model[1], model[2], model[3], model[0], opts)
+for h in (hd, hs):
+    L.sambaten_checkpoint(h)
+for rnd in range(2):
+    Kt = K0
+    for b in batches:
+        Kt += b.dims[2]
+        assert L.sambaten_batch_partition(hd, b.dims[2]) == (0, b.dims[2])
+        out = []
+        for h in (hd, hs):
+            A = np.empty((I, R), np.float32); B = np.empty((J, R), np.float32)
+            C = np.empty((Kt, R), np.float32); lam = np.empty(R, np.float32)
+            info = L.sambaten_update(h, coo(b), A, B, C, lam)
+            out.append((A, B, C, lam, info.fit_full, info.reps_rejected_mask))
+        for x, y in zip(out[0][:4], out[1][:4]):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+        assert out[0][4] == out[1][4] and out[0][5] == out[1][5]
+    for h in (hd, hs):
+        L.sambaten_restore(h)
+L.sambaten_destroy(hd); L.sambaten_destroy(hs)
+print("DIST_COO_OK")
+"""
+
+
+@pytest.mark.parametrize("loopback,inc", [(False, 0), (True, 0), (True, 1)])
+def test_world1_coo_dist_handle_matches_single_gpu_bitwise(loopback, inc):
+    env = dict(os.environ)
+    env.pop("SAMBATEN_DIST_LOOPBACK", None)
+    if loopback:
+        env["SAMBATEN_DIST_LOOPBACK"] = "1"
+    code = "ROOT = %r\nINC = %d\n" % (ROOT, inc) + SCRIPT_COO
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert "DIST_COO_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
