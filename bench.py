@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-variant", action="store_true", help="skip the incremental-marginals variant run")
+    p.add_argument("--no-getrank", action="store_true", help="skip the GetRank timing (SURVEY 8(f) NEXT #2)")
     p.add_argument("--no-full-fit", action="store_true", help="return the summary fit only (R21)")
     p.add_argument("--sharded", action="store_true",
                    help="use the sharded (NCCL) handle even at N=1 (always used at N>1, dense configs)")
@@ -303,6 +304,29 @@ def slab_of(x, k0, n, coo):
     from synth import CooArrays
     a, b = np.searchsorted(x.k, [k0, k0 + n])
     return CooArrays(x.i[a:b], x.j[a:b], (x.k[a:b] - k0).astype(np.int32), x.v[a:b], (x.dims[0], x.dims[1], n))
+
+
+def getrank_timing(L, w, stream):
+    """GetRank (Alg. 2) on one summary-sized planted tensor of the config
+    (n_I x n_J x n_K' of the first batch, rank R, 1 % noise): candidate ranks 1..R+2, one trial,
+    the config's ALS iterations; device time with CUDA events on the library's stream."""
+    import torch
+    from synth import planted_dense
+    nI, nJ = -(-w.I // w.s), -(-w.J // w.s)
+    nK = -(-w.K0 // w.s) + w.batch
+    T, _ = planted_dense(nI, nJ, nK, w.R, noise=0.01, seed=w.seed + 17)
+    X = L.dense(torch.from_numpy(T).cuda())
+    Rmax = w.R + 2
+    L.sambaten_getrank(X, Rmax, 1, w.seed, w.maxit, 0.0, 90.0, stream.cuda_stream)   # warm-up
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    rn, cc = L.sambaten_getrank(X, Rmax, 1, w.seed, w.maxit, 0.0, 90.0, stream.cuda_stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return {"ms": e0.elapsed_time(e1), "R_new": rn, "R_planted": w.R, "candidate_ranks": Rmax, "trials": 1,
+            "shape": [nI, nJ, nK], "als_iters": w.maxit,
+            "best_cc": [round(float(x), 3) for x in cc.max(axis=1)]}
 
 
 def partition(n, world, rank):
@@ -581,6 +605,8 @@ def main():
             "note": "opts.incremental_marginals=1: a1 adds the batch's contribution to the committed "
                     "int64 marginals (bit-identical to the full pass; tests/test_gpu_incremental.py)"}}
     L.sambaten_destroy(h)
+    if rank == 0 and not work.coo and not args.no_getrank:
+        line["getrank"] = getrank_timing(L, w, stream)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

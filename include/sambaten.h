@@ -262,6 +262,24 @@ SAMBATEN_API sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, fl
                                 float* U2, double* lambda_out, int max_iters, double tol,
                                 double* fit_out, int32_t* iters_out, void* stream);
 
+/* ---- GetRank quality control (Alg. 2) ------------------------
+ * Core consistency (CorConDia, P:266 [bro2003new]; reading R29) of the rank-F model
+ * [[lambda; A, B, C]] of the DENSE tensor X: with lambda absorbed into A, the least-squares core
+ * G = X x1 pinv(A) x2 pinv(B) x3 pinv(C) and cc = 100 (1 - sum (G - T)^2 / F), T the
+ * superdiagonal unit core.  A, B, C: device float32 [dims][F] row-major; lambda: device
+ * float64[F]; cc: host or device float64[1].  fp64 throughout; E_INVALID on bad arguments. */
+SAMBATEN_API sambaten_status sambaten_corcondia(const sambaten_tensor* X, int F, const float* A, const float* B,
+                                   const float* C, const double* lambda, double* cc, void* stream);
+
+/* Alg. 2 on the dense (summary) tensor X: for every candidate rank F = 1..R_max and trial
+ * j < trials, CP-ALS (max_iters, tol as sambaten_cp_als) from the Philox initialisation with
+ * update_id = 0x47520000 + F and repetition j (R30), rated by CorConDia; R_new = the largest F
+ * whose best trial reaches `threshold` (R31; 90 is customary), else 1.  cc: host float64
+ * [R_max][trials] (may be NULL); the call synchronises the stream. */
+SAMBATEN_API sambaten_status sambaten_getrank(const sambaten_tensor* X, int R_max, int trials, uint64_t seed,
+                                 int max_iters, double tol, double threshold, int* R_new, double* cc,
+                                 void* stream);
+
 /* Relative error ||X - [[lambda; A, B, C]]||_F / ||X||_F of a dense or COO
  * tensor X against a model (device float32); relerr: device float64[1]. */
 SAMBATEN_API sambaten_status sambaten_fit(const sambaten_tensor* X, const float* lambda, const float* A,

@@ -100,6 +100,8 @@ def lib():
         "sambaten_init_factors_dist": (i32, [C.POINTER(vp), T, C.POINTER(Dist), ip, ip, ip, u64, vp, vp, vp, vp, O]),
         "sambaten_batch_partition": (i32, [vp, i64, C.POINTER(i64), C.POINTER(i64)]),
         "sambaten_dist_plan": (i32, [vp, ip, i64, vp, i64, i64, ip, ip, vp, vp]),
+        "sambaten_corcondia": (i32, [T, ip, vp, vp, vp, vp, vp, vp]),
+        "sambaten_getrank": (i32, [T, ip, ip, u64, ip, d, d, C.POINTER(ip), vp, vp]),
         "sambaten_last_error": (C.c_char_p, []),
         "sambaten_version": (C.c_char_p, []),
     }
@@ -117,7 +119,7 @@ EXPORTED = ["sambaten_default_opts", "sambaten_init", "sambaten_init_factors", "
             "sambaten_fixed_point_scale", "sambaten_marginals", "sambaten_sample", "sambaten_gather",
             "sambaten_mttkrp", "sambaten_cp_als", "sambaten_fit", "sambaten_philox", "sambaten_detlog",
             "sambaten_dist_unique_id", "sambaten_init_factors_dist", "sambaten_batch_partition",
-            "sambaten_dist_plan",
+            "sambaten_dist_plan", "sambaten_corcondia", "sambaten_getrank",
             "sambaten_last_error", "sambaten_version"]
 
 
@@ -327,6 +329,22 @@ def sambaten_cp_als(X, R, U0, U1, U2, lam_out, max_iters, tol, fit_out, iters_ou
 
 def sambaten_fit(X, lam, A, B, Cm, R, relerr, stream=None):
     check(lib().sambaten_fit(C.byref(X), ptr(lam), ptr(A), ptr(B), ptr(Cm), R, ptr(relerr), stream))
+
+
+def sambaten_corcondia(X, F, A, B, Cm, lam, stream=None):
+    """CorConDia (R29) of [[lam; A, B, C]] (device fp32 factors, device fp64 lam) of dense X."""
+    out = np.zeros(1, np.float64)
+    check(lib().sambaten_corcondia(C.byref(X), F, ptr(A), ptr(B), ptr(Cm), ptr(lam), ptr(out), stream))
+    return float(out[0])
+
+
+def sambaten_getrank(X, R_max, trials, seed, max_iters, tol, threshold=90.0, stream=None):
+    """GetRank (Alg. 2, R29-R31) of dense X: (R_new, cc[R_max][trials])."""
+    cc = np.zeros((R_max, trials), np.float64)
+    rn = C.c_int(0)
+    check(lib().sambaten_getrank(C.byref(X), R_max, trials, seed, max_iters, tol, threshold, C.byref(rn),
+                                 ptr(cc), stream))
+    return rn.value, cc
 
 
 def sambaten_philox(c0, c1, c2, c3, key, n, out, stream=None):

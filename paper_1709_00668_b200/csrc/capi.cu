@@ -1421,6 +1421,77 @@ extern "C" sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, floa
   return SAMBATEN_OK;
 }
 
+extern "C" sambaten_status sambaten_corcondia(const sambaten_tensor* X, int F, const float* A, const float* B,
+                                              const float* C, const double* lambda, double* cc, void* stream) {
+  if (sambaten_status e = check_dense(X, "corcondia")) return e;
+  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "corcondia: dense tensors only");
+  if (F < 1 || F > kMaxR || !A || !B || !C || !lambda || !cc) FAIL(SAMBATEN_E_INVALID, "corcondia: bad argument");
+  cudaStream_t st = stream_of(stream);
+  const int I = (int)X->dims[0], J = (int)X->dims[1], K = (int)X->dims[2];
+  void* ws = nullptr;
+  CK(cudaMallocAsync(&ws, sizeof(double) * (corcondia_ws_doubles(I, J, K, F, 1) + 1), st));
+  double* out = static_cast<double*>(ws) + corcondia_ws_doubles(I, J, K, F, 1);
+  const float* U[3] = {A, B, C};
+  const int64_t us[3] = {0, 0, 0};
+  CK(launch_corcondia(X->vals, X->dims[0], I, J, K, F, 1, U, us, lambda, static_cast<double*>(ws), out, st));
+  CK(cudaMemcpyAsync(cc, out, sizeof(double), cudaMemcpyDefault, st));
+  CK(cudaFreeAsync(ws, st));
+  CK(cudaStreamSynchronize(st));
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_getrank(const sambaten_tensor* X, int R_max, int trials, uint64_t seed,
+                                            int max_iters, double tol, double threshold, int* R_new, double* cc,
+                                            void* stream) {
+  if (sambaten_status e = check_dense(X, "getrank")) return e;
+  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "getrank: dense tensors only");
+  if (R_max < 1 || R_max > kMaxR || trials < 1 || trials > kMaxReps || max_iters < 1 || !R_new)
+    FAIL(SAMBATEN_E_INVALID, "getrank: bad argument");
+  cudaStream_t st = stream_of(stream);
+  const int I = (int)X->dims[0], J = (int)X->dims[1], K = (int)X->dims[2];
+  constexpr uint32_t kGetRankId = 0x47520000u;   // R30
+  // one workspace for the largest candidate rank, reused by every rank
+  DenseAls a{};
+  a.Y = X->vals; a.y_stride = 0; a.pitch = X->dims[0];   // the same tensor for every trial
+  a.nI = I; a.nJ = J; a.nK = K; a.R = R_max; a.r = trials;
+  const size_t ub = align256(sizeof(float) * (size_t)trials * (I + J + K) * R_max);
+  const size_t als_b = align256(dense_als_workspace(&a));
+  const size_t cc_b = align256(sizeof(double) * (corcondia_ws_doubles(I, J, K, R_max, trials) + (size_t)R_max * trials));
+  void* ws = nullptr;
+  CK(cudaMallocAsync(&ws, ub + als_b + cc_b, st));
+  char* base = static_cast<char*>(ws);
+  double* ccws = reinterpret_cast<double*>(base + ub + als_b);
+  double* ccd = ccws + corcondia_ws_doubles(I, J, K, R_max, trials);
+  for (int F = 1; F <= R_max; ++F) {
+    a.R = F;
+    a.U[0] = reinterpret_cast<float*>(base);
+    a.U[1] = a.U[0] + (size_t)trials * I * F;
+    a.U[2] = a.U[1] + (size_t)trials * J * F;
+    a.u_stride[0] = (int64_t)I * F; a.u_stride[1] = (int64_t)J * F; a.u_stride[2] = (int64_t)K * F;
+    a.maxit = max_iters; a.tol = tol;
+    dense_als_workspace(&a);
+    CK(dense_als_bind_workspace(&a, base + ub));
+    CK(launch_als_init(a, seed, kGetRankId + (uint32_t)F, 0, true, st));
+    CK(run_dense_als(a, st));
+    const float* U[3] = {a.U[0], a.U[1], a.U[2]};
+    CK(launch_corcondia(X->vals, X->dims[0], I, J, K, F, trials, U, a.u_stride, a.lam, ccws,
+                        ccd + (size_t)(F - 1) * trials, st));
+  }
+  std::vector<double> h((size_t)R_max * trials);
+  CK(cudaMemcpyAsync(h.data(), ccd, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(ws, st));
+  CK(cudaStreamSynchronize(st));
+  int best = 1;
+  for (int F = 1; F <= R_max; ++F) {
+    double m = -1e300;
+    for (int j = 0; j < trials; ++j) m = std::max(m, h[(size_t)(F - 1) * trials + j]);
+    if (m >= threshold) best = F;
+  }
+  *R_new = best;
+  if (cc) memcpy(cc, h.data(), sizeof(double) * h.size());
+  return SAMBATEN_OK;
+}
+
 extern "C" sambaten_status sambaten_fit(const sambaten_tensor* X, const float* lambda, const float* A,
                                         const float* B, const float* C, int R, double* relerr,
                                         void* stream) {

@@ -109,6 +109,12 @@ cudaError_t run_dense_als(const DenseAls& a, cudaStream_t st);
 // single-mode MTTKRP for the stateless API (r = 1): M (fp32 [n_mode][R])
 cudaError_t dense_mttkrp_single(const DenseAls& a, int mode, float* M, cudaStream_t st);
 
+// GetRank (k_getrank.cu): CorConDia of nm models of one dense tensor (fp64)
+size_t corcondia_ws_doubles(int I, int J, int K, int F, int nm);
+cudaError_t launch_corcondia(const float* X, int64_t pitch, int I, int J, int K, int F, int nm,
+                             const float* const U[3], const int64_t u_stride[3], const double* lam, double* ws,
+                             double* cc, cudaStream_t st);
+
 // a5 / a6
 struct MatchArgs {
   const float *A, *B, *C;            // model snapshot (fp32)

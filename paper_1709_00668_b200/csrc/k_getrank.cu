@@ -1,0 +1,164 @@
+// k_getrank.cu -- GetRank quality control (Alg. 2): the
+// core consistency diagnostic CorConDia ([bro2003new]) of batched CP models of one dense
+// summary (readings R29-R31).  Everything in fp64 (a quality rating, not a hot loop):
+//   corcondia_pinv_kernel  block per (model, mode): Gram of the loading matrix (lambda absorbed
+//                          into mode 0), its inverse (Gauss-Jordan; pseudo-inverse if singular)
+//                          and P_m = Gram^-1 U_m^T (F x n_m) -- pinv for full column rank (R29)
+//   corcondia_t1_kernel    T1(f, j, k) = sum_i P_0(f, i) X(i, j, k)
+//   corcondia_t2_kernel    T2(f, g, k) = sum_j P_1(g, j) T1(f, j, k)
+//   corcondia_core_kernel  G(f, g, h) = sum_k P_2(h, k) T2(f, g, k); cc = 100 (1 - sum (G - T)^2 / F)
+#include "als_small.cuh"
+#include "common.cuh"
+#include "internal.h"
+
+namespace sbt {
+
+namespace {
+
+constexpr int kGT = 256;
+
+struct CcArgs {
+  const float* X;  int64_t pitch;      // dense [K][J][pitch]
+  int I, J, K, F, nm;                  // nm models
+  const float* U[3]; int64_t u_stride[3];   // [nm][n][F] fp32 loadings
+  const double* lam;                   // [nm][F]
+  double* P;                           // [nm][3][F][nmax]
+  double* T1;                          // [nm][F][J][K]
+  double* T2;                          // [nm][F][F][K]
+  double* W;                           // [nm][3][4][F][F] scratch (Gram, inverse, pinv scratch)
+  double* cc;                          // [nm]
+  int nmax;
+};
+
+__global__ void corcondia_pinv_kernel(CcArgs a) {
+  const int mdl = blockIdx.x / 3, m = blockIdx.x % 3;
+  const int F = a.F, n = m == 0 ? a.I : m == 1 ? a.J : a.K;
+  const float* U = a.U[m] + (int64_t)mdl * a.u_stride[m];
+  const double* lam = a.lam + (int64_t)mdl * F;
+  double* Gm = a.W + ((int64_t)mdl * 3 + m) * 4 * F * F;
+  double* Gi = Gm + F * F;
+  double* S1 = Gi + F * F;
+  double* S2 = S1 + F * F;
+  auto u = [&](int p, int f) { return (double)U[(int64_t)p * F + f] * (m == 0 ? lam[f] : 1.0); };
+  for (int e = threadIdx.x; e < F * F; e += blockDim.x) {
+    const int f = e / F, g = e - f * F;
+    double s = 0.0;
+    for (int p = 0; p < n; ++p) s += u(p, f) * u(p, g);
+    Gm[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // Gauss-Jordan with partial pivoting on [Gm | I]; singular -> pseudo-inverse (pinv_R)
+    bool ok = true;
+    for (int e = 0; e < F * F; ++e) { S1[e] = Gm[e]; Gi[e] = (e / F == e % F) ? 1.0 : 0.0; }
+    double scale = 0.0;
+    for (int f = 0; f < F; ++f) scale = fmax(scale, fabs(Gm[f * F + f]));
+    for (int c = 0; c < F && ok; ++c) {
+      int piv = c;
+      for (int rr = c + 1; rr < F; ++rr)
+        if (fabs(S1[rr * F + c]) > fabs(S1[piv * F + c])) piv = rr;
+      if (!(fabs(S1[piv * F + c]) > 1e-13 * scale)) { ok = false; break; }
+      if (piv != c)
+        for (int k = 0; k < F; ++k) {
+          double t = S1[c * F + k]; S1[c * F + k] = S1[piv * F + k]; S1[piv * F + k] = t;
+          t = Gi[c * F + k]; Gi[c * F + k] = Gi[piv * F + k]; Gi[piv * F + k] = t;
+        }
+      const double inv = 1.0 / S1[c * F + c];
+      for (int k = 0; k < F; ++k) { S1[c * F + k] *= inv; Gi[c * F + k] *= inv; }
+      for (int rr = 0; rr < F; ++rr)
+        if (rr != c) {
+          const double fct = S1[rr * F + c];
+          if (fct != 0.0)
+            for (int k = 0; k < F; ++k) { S1[rr * F + k] -= fct * S1[c * F + k]; Gi[rr * F + k] -= fct * Gi[c * F + k]; }
+        }
+    }
+    if (!ok) pinv_R(Gm, Gi, F, S1, S2);
+  }
+  __syncthreads();
+  double* P = a.P + ((int64_t)mdl * 3 + m) * F * a.nmax;
+  for (int e = threadIdx.x; e < F * n; e += blockDim.x) {
+    const int f = e / n, p = e - f * n;
+    double s = 0.0;
+    for (int g = 0; g < F; ++g) s += Gi[f * F + g] * u(p, g);
+    P[(int64_t)f * a.nmax + p] = s;
+  }
+}
+
+__global__ void corcondia_t1_kernel(CcArgs a) {
+  const int64_t tot = (int64_t)a.nm * a.F * a.J * a.K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int f = (int)(e % a.F);
+    int64_t r = e / a.F;
+    const int j = (int)(r % a.J); r /= a.J;
+    const int k = (int)(r % a.K);
+    const int mdl = (int)(r / a.K);
+    const double* P0 = a.P + ((int64_t)mdl * 3 + 0) * a.F * a.nmax + (int64_t)f * a.nmax;
+    const float* x = a.X + ((int64_t)k * a.J + j) * a.pitch;
+    double s = 0.0;
+    for (int i = 0; i < a.I; ++i) s += P0[i] * (double)x[i];
+    a.T1[(((int64_t)mdl * a.F + f) * a.J + j) * a.K + k] = s;
+  }
+}
+
+__global__ void corcondia_t2_kernel(CcArgs a) {
+  const int64_t tot = (int64_t)a.nm * a.F * a.F * a.K;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e % a.K);
+    int64_t r = e / a.K;
+    const int g = (int)(r % a.F); r /= a.F;
+    const int f = (int)(r % a.F);
+    const int mdl = (int)(r / a.F);
+    const double* P1 = a.P + ((int64_t)mdl * 3 + 1) * a.F * a.nmax + (int64_t)g * a.nmax;
+    const double* t1 = a.T1 + ((int64_t)mdl * a.F + f) * a.J * a.K + k;
+    double s = 0.0;
+    for (int j = 0; j < a.J; ++j) s += P1[j] * t1[(int64_t)j * a.K];
+    a.T2[(((int64_t)mdl * a.F + f) * a.F + g) * a.K + k] = s;
+  }
+}
+
+__global__ void corcondia_core_kernel(CcArgs a) {
+  __shared__ double red[32];
+  const int mdl = blockIdx.x, F = a.F;
+  const double* P2 = a.P + ((int64_t)mdl * 3 + 2) * F * a.nmax;
+  double dev = 0.0;
+  for (int e = threadIdx.x; e < F * F * F; e += blockDim.x) {
+    const int h = e % F, g = (e / F) % F, f = e / (F * F);
+    const double* t2 = a.T2 + (((int64_t)mdl * F + f) * F + g) * a.K;
+    double s = 0.0;
+    for (int k = 0; k < a.K; ++k) s += P2[(int64_t)h * a.nmax + k] * t2[k];
+    const double d = s - ((f == g && g == h) ? 1.0 : 0.0);
+    dev += d * d;
+  }
+  dev = block_sum_d(dev, red);
+  if (threadIdx.x == 0) a.cc[mdl] = 100.0 * (1.0 - dev / F);
+}
+
+}  // namespace
+
+size_t corcondia_ws_doubles(int I, int J, int K, int F, int nm) {
+  const int nmax = max(I, max(J, K));
+  return (size_t)nm * (3 * (size_t)F * nmax + (size_t)F * J * K + (size_t)F * F * K + 12 * (size_t)F * F + 1);
+}
+
+cudaError_t launch_corcondia(const float* X, int64_t pitch, int I, int J, int K, int F, int nm,
+                             const float* const U[3], const int64_t u_stride[3], const double* lam, double* ws,
+                             double* cc, cudaStream_t st) {
+  CcArgs a{};
+  a.X = X; a.pitch = pitch; a.I = I; a.J = J; a.K = K; a.F = F; a.nm = nm;
+  for (int m = 0; m < 3; ++m) { a.U[m] = U[m]; a.u_stride[m] = u_stride[m]; }
+  a.lam = lam;
+  a.nmax = max(I, max(J, K));
+  a.P = ws;
+  a.T1 = a.P + (size_t)nm * 3 * F * a.nmax;
+  a.T2 = a.T1 + (size_t)nm * F * J * K;
+  a.W = a.T2 + (size_t)nm * F * F * K;
+  a.cc = cc;
+  corcondia_pinv_kernel<<<nm * 3, kGT, 0, st>>>(a);
+  const auto blocks = [](int64_t n) { return (unsigned)(ceil_div(n, kGT) < kNumSMs * 8 ? ceil_div(n, kGT) : kNumSMs * 8); };
+  corcondia_t1_kernel<<<blocks((int64_t)nm * F * J * K), kGT, 0, st>>>(a);
+  corcondia_t2_kernel<<<blocks((int64_t)nm * F * F * K), kGT, 0, st>>>(a);
+  corcondia_core_kernel<<<nm, kGT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sbt
