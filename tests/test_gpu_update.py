@@ -187,3 +187,31 @@ def test_init_als_on_gpu_matches_oracle_quality():
         assert abs(rel - rel_o) <= 1e-3, (rel, rel_o)
     finally:
         L().sambaten_destroy(h)
+
+
+@pytest.mark.parametrize("s_mode,policy,moi", [((2, 3, 4), 0, 0), ((3, 2, 2), 1, 0), ((2, 2, 3), 0, 1)])
+def test_variant_flags_parity(s_mode, policy, moi):
+    """SURVEY 8(f) NEXT #4 flags against the oracle: per-mode sampling factors, the
+    overwrite merge policy (R17) and the squared measure of importance (Eq. 1, R1)."""
+    I, J, K, R, K0, batch = 60, 52, 40, 4, 30, 5
+    T, truth = planted_dense(I, J, K, R, noise=0.01, seed=6)
+    T0, batches = split_dense(T, K0, batch)
+    model = [np.asarray(x, np.float32) for x in (truth[0], truth[1], truth[2], truth[3][:K0])]
+    cfg = O.Config(R=R, s=s_mode, r=4, seed=13, maxit=20, tol=0.0, tau=0.9, merge_policy=policy, moi=moi)
+    st = O.init_factors(T0, cfg, *model, I * J * K)
+    lam, A, B, C = model
+    opts = L().default_opts(als_max_iters=20, als_tol=0.0, accept_tau=0.9, capacity=K, full_fit=1,
+                            merge_policy=policy, moi=moi, s_mode=s_mode)
+    h = L().sambaten_init_factors(L().dense(dev(T0)), R, 2, 4, 13, A, B, C, lam, opts)
+    try:
+        Kt = K0
+        for b in batches[:2]:
+            Kt += b.shape[0]
+            gm, info, oinfo = _update_both(h, st, b, Kt)
+            fms, rel_g, rel_o, gpu_rej = _check(h, st, gm, info, oinfo)
+            assert gpu_rej == oinfo["rejected"]
+            assert fms >= 0.99, fms
+            assert abs(rel_g - rel_o) <= 1e-3, (rel_g, rel_o)
+            st.lam, st.A, st.B, st.C = (np.asarray(x, np.float64) for x in gm)
+    finally:
+        L().sambaten_destroy(h)
