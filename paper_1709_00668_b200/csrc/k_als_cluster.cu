@@ -259,7 +259,7 @@ __device__ __forceinline__ bool warp_spd_inverse_reg(const double* V, double* Vi
 
 // Warp 0: Vi = (G_o1 * G_o2)^-1 for mode m (Hadamard of the other two normalised Grams).
 template <int RB>
-__device__ __noinline__ void warp_normal_inverse(const double* G, int m, int R, double* Vm,
+__device__ __forceinline__ void warp_normal_inverse(const double* G, int m, int R, double* Vm,
                                                  double* Vi, double* W1, double* fc, int* flags) {
   const int lane = threadIdx.x & 31;
   const int o1 = m == 0 ? 1 : 0, o2 = m == 2 ? 1 : 2;
