@@ -116,6 +116,8 @@ struct sambaten_s {
   DistState* dist = nullptr;   // set for handles of the sharded update (sambaten_init_factors_dist)
   int64_t I = 0, J = 0, K = 0, Kcap = 0, pitch = 0;
   bool X_borrowed = false;   // opts.borrow_store: X is the caller's buffer
+  cudaStream_t st2 = nullptr;     // side stream: host batch copy overlapped with a1 (old slices)
+  cudaEvent_t ev_side[2] = {nullptr, nullptr};
   DevBuf xm, xm_ck;          // committed marginals of the current tensor (incremental a1)
   bool xm_valid = false, xm_ck_valid = false;
   int R = 0, r = 0, s[3] = {1, 1, 1};
@@ -336,6 +338,12 @@ extern "C" void sambaten_destroy(sambaten_t h) {
   cudaStreamSynchronize(h->st);
   dist_destroy(h->dist);
   h->dist = nullptr;
+  if (h->st2) {
+    cudaStreamSynchronize(h->st2);
+    cudaStreamDestroy(h->st2);
+    cudaEventDestroy(h->ev_side[0]);
+    cudaEventDestroy(h->ev_side[1]);
+  }
   if (h->X_borrowed) h->X.p = nullptr;   // the caller's buffer: not ours to free
   h->X.release();
   h->model[0].release(); h->model[1].release(); h->ck.release();
@@ -932,8 +940,33 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   DenseView V = h->view();
   V.K = Ko + Kn;
   const int64_t nb_fl = h->I * h->J * Kn;
-  if (h->pitch == h->I && nb_fl % 4 == 0 && is_device_ptr(batch->vals) &&
-      (((uintptr_t)batch->vals | (uintptr_t)dst) & 15) == 0) {
+  const size_t marg_bytes = sizeof(int64_t) * (h->I + h->J + h->Kcap);
+  CK(h->marg.ensure(marg_bytes));
+  int64_t* x1 = h->marg.as<int64_t>();
+  int64_t* x2 = x1 + h->I;
+  int64_t* x3 = x2 + h->J;
+  const bool inc = h->opts.incremental_marginals && h->xm_valid;
+  const bool dev_batch = is_device_ptr(batch->vals);
+  // A host batch crosses PCIe on a side stream while a1 reads the old slices (they do not
+  // depend on it); the batch's own marginals follow once it has landed.
+  const bool overlap = !dev_batch && !inc && Ko > 0;
+  if (overlap) {
+    if (!h->st2) {
+      CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h->ev_side[0], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_side[1], cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(h->ev_side[0], st));
+    CK(cudaStreamWaitEvent(h->st2, h->ev_side[0], 0));
+    CK(cudaMemcpy2DAsync(dst, h->pitch * sizeof(float), batch->vals, h->I * sizeof(float),
+                         h->I * sizeof(float), h->J * Kn, cudaMemcpyDefault, h->st2));
+    CK(cudaEventRecord(h->ev_side[1], h->st2));
+    CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
+    CK(marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, st));   // a1, old slices
+    CK(cudaStreamWaitEvent(st, h->ev_side[1], 0));
+    CK(launch_max_phi_dense(V, Ko, Kn, h->opts.moi, d_maxphi, st));
+  } else if (h->pitch == h->I && nb_fl % 4 == 0 && dev_batch &&
+             (((uintptr_t)batch->vals | (uintptr_t)dst) & 15) == 0) {
     // device batch, contiguous store: one pass copies and tracks max |x|
     CK(launch_ingest_dense(batch->vals, dst, nb_fl, h->opts.moi, d_maxphi, st));
   } else {
@@ -943,12 +976,9 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   }
   CK(cudaEventRecord(h->ev[1], st));
   // ---- a1: marginals over X_old U X_new (R2, R3) ----------------------------------------
-  const size_t marg_bytes = sizeof(int64_t) * (h->I + h->J + h->Kcap);
-  CK(h->marg.ensure(marg_bytes));
-  int64_t* x1 = h->marg.as<int64_t>();
-  int64_t* x2 = x1 + h->I;
-  int64_t* x3 = x2 + h->J;
-  if (h->opts.incremental_marginals && h->xm_valid) {
+  if (overlap) {
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, st));   // the batch's slices
+  } else if (inc) {
     // committed marginals of X_old plus the batch's contribution (integer sums: bit-identical
     // to the full pass)
     CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, st));
