@@ -650,6 +650,9 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     double* Vi = b.take<double>((size_t)r * R * R);
     double* rpart = b.take<double>(als_rows_part_doubles((int)maxn, R, r));
     int* stop = b.take<int>(r);
+    const int RBp = R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
+    const bool padded = R <= 16;   // the row-parallel solve keeps the padded copies in sync
+    float* Upad = padded ? b.take<float>((size_t)r * ((int64_t)nI + nJ + nK) * RBp) : nullptr;
     // per-mode MTTKRP plans: row pieces, sorted copies (modes 0, 1), piece partials
     const int rows_m[3] = {nI, nJ, nK};
     CooModePlan plan[3];
@@ -694,6 +697,14 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     a.M[0] = M0; a.m_stride[0] = (int64_t)nI * R;
     a.M[1] = a.M[2] = Mb; a.m_stride[1] = a.m_stride[2] = maxn * R;
     a.done = done;
+    float* Up3[3] = {nullptr, nullptr, nullptr};
+    if (padded) {
+      Up3[0] = Upad;
+      Up3[1] = Up3[0] + (size_t)r * nI * RBp;
+      Up3[2] = Up3[1] + (size_t)r * nJ * RBp;
+    }
+    const int64_t ups[3] = {(int64_t)nI * RBp, (int64_t)nJ * RBp, (int64_t)nK * RBp};
+    for (int m = 0; m < 3; ++m) { a.Up[m] = Up3[m]; a.up_stride[m] = ups[m]; }
     if (e == cudaSuccess && init_factors) e = launch_als_init_factors(*d, seed, uid, rep0, st, rep_stride);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(done, 0, sizeof(int) * r, st);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(iters, 0, sizeof(int) * r, st);
@@ -716,6 +727,9 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     ra.X = Us; ra.x_stride = maxn * R; ra.Vi = Vi; ra.part = rpart; ra.G = G; ra.lam = lam;
     ra.ysq = ysq; ra.fit = fit; ra.fit_prev = fitp; ra.iters = iters; ra.done = done;
     ra.flags = flags; ra.stop = stop;
+    for (int m = 0; m < 3; ++m) { ra.Up[m] = Up3[m]; ra.up_stride[m] = ups[m]; }
+    ra.RBp = RBp;
+    if (e == cudaSuccess) e = launch_pad_factors(ra, st);
     const bool rows = R <= 16;
     if (e == cudaSuccess) e = cudaMemsetAsync(stop, 0, sizeof(int) * r, st);
     for (int it = 0; it < maxit && e == cudaSuccess; ++it) {

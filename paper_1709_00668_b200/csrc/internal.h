@@ -175,6 +175,7 @@ struct CooAls {                        // the r COO summaries (concatenated) + A
   int nI, nJ, nK, R, RB, r;
   CooModePlan plan[3];
   float* U[3]; int64_t u_stride[3];
+  const float* Up[3]; int64_t up_stride[3];   // optional copies of U with rows padded to RB floats
   double* M[3]; int64_t m_stride[3];
   const int* done;
 };
@@ -224,6 +225,7 @@ struct RowsAls {
   int nI, nJ, nK, R, r, maxit;
   double tol;
   float* U[3]; int64_t u_stride[3];
+  float* Up[3]; int64_t up_stride[3]; int RBp;   // optional padded copies (16 B rows), kept in sync
   const double* M[3]; int64_t m_stride[3];
   double* X; int64_t x_stride;         // [r][maxn][R] solved rows
   double* Vi;                          // [r][R][R]
@@ -234,6 +236,8 @@ struct RowsAls {
   int* iters; int* done; int* flags; int* stop;
 };
 cudaError_t launch_als_rows_mode(const RowsAls& a, int mode, cudaStream_t st);
+// Up[m] = U[m] with rows padded to RBp floats (zeros), every mode and repetition
+cudaError_t launch_pad_factors(const RowsAls& a, cudaStream_t st);
 struct GramArgs {                      // G[rep][m] = U_m^T U_m for m < 3, rep < r (fp64)
   const float* U[3]; int64_t u_stride[3]; int n[3];
   int R, r, tmax;                      // tmax = gram_tiles_for(max n)

@@ -223,10 +223,27 @@ __global__ void als_scale_kernel(RowsAls a, int mode) {
   const double* X = a.X + (int64_t)rep * a.x_stride;
   float* U = a.U[mode] + rep * a.u_stride[mode];
   const int64_t b = (int64_t)tile * kRT * R, e = min((int64_t)(tile + 1) * kRT, (int64_t)n) * R;
+  float* Up = a.Up[mode] ? a.Up[mode] + rep * a.up_stride[mode] : nullptr;
   for (int64_t t = b + threadIdx.x; t < e; t += blockDim.x) {
-    const int f = (int)(t % R);
+    const int64_t row = t / R;
+    const int f = (int)(t - row * R);
     const double l = lam[f];
-    U[t] = __double2float_rn(l > 0.0 ? X[t] / l : X[t]);
+    const float u = __double2float_rn(l > 0.0 ? X[t] / l : X[t]);
+    U[t] = u;
+    if (Up) Up[row * a.RBp + f] = u;
+  }
+}
+
+__global__ void pad_factors_kernel(RowsAls a) {
+  const int m = blockIdx.y, rep = blockIdx.z;
+  const int n = m == 0 ? a.nI : m == 1 ? a.nJ : a.nK;
+  const float* U = a.U[m] + rep * a.u_stride[m];
+  float* Up = a.Up[m] + rep * a.up_stride[m];
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (int64_t)n * a.RBp;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / a.RBp;
+    const int f = (int)(t - row * a.RBp);
+    Up[t] = f < a.R ? U[row * a.R + f] : 0.f;
   }
 }
 
@@ -295,6 +312,12 @@ int gram_tiles_for(int n) { return (n + kRT - 1) / kRT; }
 
 cudaError_t launch_als_rows_commit(const RowsAls& a, cudaStream_t st) {
   als_commit_stop_kernel<<<1, 32, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_factors(const RowsAls& a, cudaStream_t st) {
+  if (!a.Up[0]) return cudaSuccess;
+  pad_factors_kernel<<<dim3(64, 3, a.r), kRT, 0, st>>>(a);
   return cudaGetLastError();
 }
 

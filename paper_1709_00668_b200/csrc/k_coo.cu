@@ -421,19 +421,45 @@ __global__ void coo_mttkrp_piece_kernel(CooAls a, int mode, int64_t npiece_max) 
     if (a.done[rep]) continue;
     const int64_t b = pl.pb[piece];
     const int64_t e = min(b + kPiece, pl.ptr[x + 1]);
-    const float* Ua = a.U[oa] + rep * a.u_stride[oa];
-    const float* Ub = a.U[ob] + rep * a.u_stride[ob];
     double acc[RB];
+    if (a.Up[oa]) {
+      // padded factor rows (16 B aligned): vector gathers; fp32 lane runs of <= kPiece / 32
+      // products, fp64 across lanes
+      const float4* Ua = reinterpret_cast<const float4*>(a.Up[oa] + rep * a.up_stride[oa]);
+      const float4* Ub = reinterpret_cast<const float4*>(a.Up[ob] + rep * a.up_stride[ob]);
+      float ac[RB];
 #pragma unroll
-    for (int f = 0; f < RB; ++f) acc[f] = 0.0;
+      for (int f = 0; f < RB; ++f) ac[f] = 0.f;
 #pragma unroll 2
-    for (int64_t t = b + lane; t < e; t += 32) {
-      const float v = pl.sv[t];
-      const float* ra = Ua + (int64_t)pl.sa[t] * R;
-      const float* rb = Ub + (int64_t)pl.sb[t] * R;
+      for (int64_t t = b + lane; t < e; t += 32) {
+        const float v = pl.sv[t];
+        const float4* ra = Ua + (int64_t)pl.sa[t] * (RB / 4);
+        const float4* rb = Ub + (int64_t)pl.sb[t] * (RB / 4);
 #pragma unroll
-      for (int f = 0; f < RB; ++f)
-        if (f < R) acc[f] += (double)(v * ra[f] * rb[f]);
+        for (int f4 = 0; f4 < RB / 4; ++f4) {
+          const float4 x = __ldg(ra + f4), y = __ldg(rb + f4);
+          ac[4 * f4 + 0] = fmaf(v * x.x, y.x, ac[4 * f4 + 0]);
+          ac[4 * f4 + 1] = fmaf(v * x.y, y.y, ac[4 * f4 + 1]);
+          ac[4 * f4 + 2] = fmaf(v * x.z, y.z, ac[4 * f4 + 2]);
+          ac[4 * f4 + 3] = fmaf(v * x.w, y.w, ac[4 * f4 + 3]);
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < RB; ++f) acc[f] = (double)ac[f];
+    } else {
+      const float* Ua = a.U[oa] + rep * a.u_stride[oa];
+      const float* Ub = a.U[ob] + rep * a.u_stride[ob];
+#pragma unroll
+      for (int f = 0; f < RB; ++f) acc[f] = 0.0;
+#pragma unroll 2
+      for (int64_t t = b + lane; t < e; t += 32) {
+        const float v = pl.sv[t];
+        const float* ra = Ua + (int64_t)pl.sa[t] * R;
+        const float* rb = Ub + (int64_t)pl.sb[t] * R;
+#pragma unroll
+        for (int f = 0; f < RB; ++f)
+          if (f < R) acc[f] += (double)(v * ra[f] * rb[f]);
+      }
     }
 #pragma unroll
     for (int f = 0; f < RB; ++f) {
