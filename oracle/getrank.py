@@ -13,8 +13,9 @@ R29  CorConDia of a rank-F model [[lambda; A, B, C]] of X: with lambda absorbed 
      G = X x1 pinv(A') x2 pinv(B) x3 pinv(C) (F x F x F); with T the superdiagonal unit core,
      cc = 100 (1 - sum (G - T)^2 / F).  cc = 100 for an exact, consistent model.
 R30  The CP runs: cp_als (this oracle's Alg. 1 step) from the Philox initialisation als_init with
-     update_id = GETRANK_ID + i (candidate rank) and rep = j (trial), so the runs are
-     reproducible and independent of launch geometry.
+     update_id = GETRANK_ID + i (candidate rank) and rep = rep_base + j (trial j; inside an
+     update rep_base = rho * trials for repetition rho), so the runs are reproducible and
+     independent of launch geometry.
 R31  "sort p and get top 1 index" taken literally always returns rank 1: a converged
      rank-1 model has cc = 100 (its core is the 1 x 1 x 1 scalar 1).  Reading: R_new = the
      largest candidate rank whose best trial reaches the threshold (default 90, the customary
@@ -48,13 +49,13 @@ def corcondia(Y, lam, A, B, C):
     return 100.0 * (1.0 - float(np.sum((G - superdiagonal(F)) ** 2)) / F)
 
 
-def getrank(Y, Rmax, trials, seed, maxit, tol, threshold=90.0):
+def getrank(Y, Rmax, trials, seed, maxit, tol, threshold=90.0, rep_base=0):
     """Alg. 2 (R30, R31): returns (R_new, cc[Rmax][trials])."""
     Y = np.asarray(Y, np.float64)
     cc = np.zeros((Rmax, trials))
     for F in range(1, Rmax + 1):
         for j in range(trials):
-            U0 = als_init(Y.shape, F, seed, GETRANK_ID + F, j)
+            U0 = als_init(Y.shape, F, seed, GETRANK_ID + F, rep_base + j)
             lam, U, _, _, _ = cp_als(Y, U0, maxit, tol)
             cc[F - 1, j] = corcondia(Y, lam, *U)
     best = cc.max(axis=1)

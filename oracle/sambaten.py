@@ -335,6 +335,7 @@ class RepMatch:
     score: np.ndarray        # S[f, pi f]
     accepted: bool
     congruence: list         # Phi_A, Phi_B, Phi_C
+    valid: np.ndarray = None # old component f has a (non-padded) candidate (GetRank, R33)
 
 
 def _anchor_congruence(old_rows, cand_rows):
@@ -348,14 +349,19 @@ def _anchor_congruence(old_rows, cand_rows):
     return Phi, alpha, a
 
 
-def match_rep(A, B, C, Is, Js, Ks, lam_p, Up, tau):
+def match_rep(A, B, C, Is, Js, Ks, lam_p, Up, tau, rnew=None):
     """Match candidate [lam'; A', B', C'] (rows at I_s, J_s, K' = K_s ++ new) to the old model.
 
     Anchors (reading R14): sampled rows whose old factor row is not all zero; for C only the
     first |K_s| rows of C' (old slices).  S = (|Phi_A| + |Phi_B| + |Phi_C|)/3 (reading R15),
     pi = argmax sum S, sigma = sign Phi(f, pi f) (0 -> +1), rescale to the old frame by the
     anchor norms and lambda_hat_f = lam'_{pi f} sigma_A sigma_B sigma_C abc/(alpha beta gamma)
-    (reading R16).  Accepted iff min_f S(f, pi f) >= tau (reading R26)."""
+    (reading R16).  Accepted iff min_f S(f, pi f) >= tau (reading R26).
+
+    rnew < R (GetRank, reading R33): the candidate has R_new real columns followed by zero
+    padding; zero columns have congruence 0, so the assignment matches the R_new real columns to
+    their best old components and only those (valid f: pi f < R_new) count for the
+    acceptance test and the merge."""
     nKs = len(Ks)
     olds = [A[np.asarray(Is)], B[np.asarray(Js)], C[np.asarray(Ks)]]
     cands = [Up[0], Up[1], Up[2][:nKs]]
@@ -376,7 +382,8 @@ def match_rep(A, B, C, Is, Js, Ks, lam_p, Up, tau):
         scale.append(np.where(ok, sig * al / np.where(ok, a, 1.0), 0.0))
         lam_hat = np.where(ok, lam_hat * sig * a / np.where(ok, al, 1.0), 0.0)
     score = S[np.arange(R), pi]
-    return RepMatch(pi, scale, lam_hat, score, bool(score.min() >= tau), Phis)
+    valid = pi < (R if rnew is None else rnew)
+    return RepMatch(pi, scale, lam_hat, score, bool(score[valid].min() >= tau), Phis, valid)
 
 
 def rescaled(Up, rm, m):
@@ -398,6 +405,9 @@ class Config:
     moi: int = MOI_ABS
     tau: float = 0.9         # reading R26 (0 = paper-literal)
     merge_policy: int = 0    # 0 = zero entries only, 1 = overwrite sampled rows
+    getrank: bool = False    # GetRank before each summary decomposition (Alg. 2; R29-R33)
+    getrank_trials: int = 1
+    getrank_threshold: float = 90.0
 
 
 @dataclass
@@ -488,41 +498,53 @@ def update(st, batch, keep_reps=False):
         Kp = k_prime(Ks, K_o, K_n)
         # a3: gather the summary
         Y = gather_dense(X, Is, Js, Kp) if dense else gather_coo(X, Is, Js, Kp)
-        # a4: CP-ALS at the universal rank R
-        U0 = als_init((len(Is), len(Js), len(Kp)), cfg.R, cfg.seed, uid, rho)
+        # a4: CP-ALS at the universal rank R, or at the rank GetRank estimates for the
+        # summary (Alg. 2; dense summaries, readings R29-R33)
+        R_use = cfg.R
+        if cfg.getrank:
+            from .getrank import getrank
+            R_use, _ = getrank(Y, cfg.R, cfg.getrank_trials, cfg.seed, cfg.maxit, cfg.tol,
+                               cfg.getrank_threshold, rep_base=rho * cfg.getrank_trials)
+        U0 = als_init((len(Is), len(Js), len(Kp)), R_use, cfg.seed, uid, rho)
         lam_p, Up, fit, its, _ = cp_als(Y, U0, cfg.maxit, cfg.tol)
+        if R_use < cfg.R:   # zero columns up to R (reading R33)
+            pad = cfg.R - R_use
+            lam_p = np.concatenate([lam_p, np.zeros(pad)])
+            Up = [np.hstack([u, np.zeros((u.shape[0], pad))]) for u in Up]
         # a5: match against the batch-start snapshot
-        rm = match_rep(st.A, st.B, st.C, Is, Js, Ks, lam_p, Up, cfg.tau)
+        rm = match_rep(st.A, st.B, st.C, Is, Js, Ks, lam_p, Up, cfg.tau, rnew=R_use)
         reps.append(dict(Is=Is, Js=Js, Ks=Ks, Kp=Kp, Y=Y if keep_reps else None, lam_p=lam_p,
-                         Up=Up, fit=fit, iters=its, match=rm))
+                         Up=Up, fit=fit, iters=its, match=rm, rank=R_use))
     acc = [rp for rp in reps if rp["match"].accepted]
     if not acc:
         raise BatchRejected("every repetition failed the acceptance test")
-    # a6: merge (readings R17-R20)
+    # a6: merge (readings R17-R20), element by element over the accepted reps that
+    # carry component f (all of them unless GetRank reduced a rep's rank, reading R33)
     A, B, C = st.A.copy(), st.B.copy(), st.C.copy()
     for m, (F, key) in enumerate(((A, "Is"), (B, "Js"), (C, "Ks"))):
-        tot = np.zeros_like(F); cnt = np.zeros(F.shape[0])
+        tot = np.zeros_like(F); cnt = np.zeros_like(F)
         for rp in acc:
             rows = rp[key]
+            v = rp["match"].valid.astype(np.float64)
             Ut = rescaled(rp["Up"], rp["match"], m)[: len(rows)]
-            tot[rows] += Ut
-            cnt[rows] += 1.0
+            tot[rows] += Ut * v[None, :]
+            cnt[rows] += v[None, :]
         hit = cnt > 0
-        mean = tot[hit] / cnt[hit][:, None]
-        old = F[hit]
+        mean = np.where(hit, tot / np.where(hit, cnt, 1.0), 0.0)
         if cfg.merge_policy == 0:
-            F[hit] = np.where(old == 0.0, mean, old)
+            F[:] = np.where(hit & (F == 0.0), mean, F)
         else:
-            F[hit] = mean
+            F[:] = np.where(hit, mean, F)
     C_new = np.zeros((K_n, cfg.R))
-    for rp in acc:
-        C_new += rescaled(rp["Up"], rp["match"], 2)[len(rp["Ks"]):]
-    C_new /= len(acc)
+    nval = np.zeros(cfg.R)
     lam_hat = np.zeros(cfg.R)
     for rp in acc:
-        lam_hat += rp["match"].lam_hat
-    lam_hat /= len(acc)
-    lam = (st.lam + lam_hat) / 2.0
+        v = rp["match"].valid.astype(np.float64)
+        C_new += rescaled(rp["Up"], rp["match"], 2)[len(rp["Ks"]):] * v[None, :]
+        lam_hat += rp["match"].lam_hat * v
+        nval += v
+    C_new = np.where(nval > 0, C_new / np.where(nval > 0, nval, 1.0), 0.0)
+    lam = np.where(nval > 0, (st.lam + lam_hat / np.where(nval > 0, nval, 1.0)) / 2.0, st.lam)
     # commit
     st.X, st.A, st.B, st.C, st.lam = X, A, B, np.vstack([C, C_new]), lam
     st.update_id = uid

@@ -73,3 +73,51 @@ def test_getrank_recovers_planted_rank(F, seed):
     R_new, cc = GR.getrank(Y, 4, 2, 7, 300, 1e-12)
     assert R_new == F, cc
     assert cc[F - 1].max() > 99.0
+
+
+def _stream(F_true, R, seed, I=40, J=36, K=30, K0=24, noise=0.0):
+    """Planted tensor of rank F_true; the model carries R >= F_true components (the extra ones
+    with all-zero time factors, i.e. absent from the data)."""
+    rng = np.random.default_rng(seed)
+    A, B, C = rng.random((I, R)), rng.random((J, R)), rng.random((K, R))
+    C[:, F_true:] = 0.0
+    X = np.einsum("if,jf,kf->ijk", A, B, C)
+    T = np.ascontiguousarray(np.transpose(X, (2, 1, 0))).astype(np.float32)
+    return T[:K0], T[K0:], (np.ones(R), A, B, C[:K0])
+
+
+def test_update_with_getrank_equals_plain_update_when_full_rank():
+    """GetRank finds the universal rank -> the update is the plain Alg. 1 update, bit for bit."""
+    T0, batch, model = _stream(3, 3, 0)
+    outs = []
+    for gr in (False, True):
+        cfg = O.Config(R=3, s=(2, 2, 2), r=3, seed=4, maxit=300, tol=1e-12, tau=0.0, getrank=gr)
+        st = O.init_factors(T0, cfg, *model, T0.size * 2)
+        last = O.update(st, batch)
+        if gr:
+            assert all(rp["rank"] == 3 for rp in last["reps"])
+        outs.append((st.lam.copy(), st.A.copy(), st.B.copy(), st.C.copy()))
+    for x, y in zip(*outs):
+        assert np.array_equal(x, y)
+
+
+def test_update_with_getrank_matches_only_the_present_components():
+    """Rank-deficient update: the data has 2 of the model's 3 components; GetRank picks 2,
+    only 2 candidate columns are matched, the third component keeps its lambda and gets zero
+    time rows for the new slices."""
+    T0, batch, model = _stream(2, 3, 1)
+    cfg = O.Config(R=3, s=(2, 2, 2), r=3, seed=6, maxit=400, tol=1e-12, tau=0.0, getrank=True)
+    st = O.init_factors(T0, cfg, *model, T0.size * 2)
+    lam0 = st.lam.copy()
+    last = O.update(st, batch)
+    assert all(rp["rank"] == 2 for rp in last["reps"])
+    for rp in last["reps"]:
+        assert rp["match"].valid.sum() == 2 and not rp["match"].valid[2]
+    assert st.lam[2] == lam0[2]
+    Kn = batch.shape[0]
+    assert np.all(st.C[-Kn:, 2] == 0.0)
+    # the present components are recovered in the old frame (noiseless, model = truth with
+    # lambda = 1): the new time rows equal the planted ones
+    rng = np.random.default_rng(1)
+    _, _, Ct = rng.random((40, 3)), rng.random((36, 3)), rng.random((30, 3))
+    assert np.allclose(st.C[-Kn:, :2], Ct[-Kn:, :2], rtol=1e-3, atol=1e-6)
