@@ -90,6 +90,13 @@ typedef struct {
                           /* the previous update instead of re-reading the whole tensor --    */
                           /* bit-identical (integer sums); the first     */
                           /* update after init / restore makes the full pass.  Default 0.     */
+  int getrank;            /* 1: before each summary decomposition run GetRank (Alg. 2,        */
+                          /* P:279-294) on the summary and decompose at the rank it returns;  */
+                          /* only those components are matched and merged (P:264-266,        */
+                          /* readings R29-R33).  Dense single-GPU handles only (else          */
+                          /* SAMBATEN_E_INVALID at init).  Default 0.                         */
+  int getrank_trials;     /* CP runs per candidate rank (Alg. 2 `it`); default 1              */
+  double getrank_threshold; /* CorConDia cut-off of R31; default 90                           */
 } sambaten_opts;
 
 typedef struct {
@@ -105,6 +112,8 @@ typedef struct {
                                /* fallback (R12) at least once                                */
   double step_ms[8];           /* device time of steps a0..a7 (CUDA events)                   */
   int als_iters_sum;           /* ALS iterations summed over the repetitions (work accounting) */
+  int rep_rank[32];            /* rank each repetition decomposed its summary at (R unless    */
+                               /* opts.getrank reduced it, R33); entries >= r are 0           */
 } sambaten_info;
 
 /* Fill *opts with the defaults listed above. */

@@ -37,7 +37,8 @@ class Opts(C.Structure):
                 ("full_fit", C.c_int), ("capacity", C.c_int64), ("capacity_k", C.c_int64),
                 ("init_max_iters", C.c_int),
                 ("init_tol", C.c_double), ("stream", C.c_void_p), ("borrow_store", C.c_int),
-                ("incremental_marginals", C.c_int)]
+                ("incremental_marginals", C.c_int), ("getrank", C.c_int),
+                ("getrank_trials", C.c_int), ("getrank_threshold", C.c_double)]
 
 
 class Dist(C.Structure):
@@ -50,14 +51,16 @@ class Info(C.Structure):
                 ("als_iters_max", C.c_int), ("k_total", C.c_int64),
                 ("reps_rejected_mask", C.c_uint32), ("scale_exp", C.c_int),
                 ("kernel_launches", C.c_int), ("reps_pinv_mask", C.c_uint32),
-                ("step_ms", C.c_double * 8), ("als_iters_sum", C.c_int)]
+                ("step_ms", C.c_double * 8), ("als_iters_sum", C.c_int),
+                ("rep_rank", C.c_int * 32)]
 
     def as_dict(self):
         return dict(fit_summary=self.fit_summary, fit_full=self.fit_full,
                     als_iters_max=self.als_iters_max, k_total=self.k_total,
                     reps_rejected_mask=self.reps_rejected_mask, scale_exp=self.scale_exp,
                     kernel_launches=self.kernel_launches, reps_pinv_mask=self.reps_pinv_mask,
-                    step_ms=list(self.step_ms), als_iters_sum=self.als_iters_sum)
+                    step_ms=list(self.step_ms), als_iters_sum=self.als_iters_sum,
+                    rep_rank=list(self.rep_rank))
 
 
 _lib = None

@@ -138,6 +138,8 @@ struct sambaten_s {
   // COO store (fmt == SAMBATEN_COO): i | j | k (int32) and v (fp32), capacity nnz_cap
   int64_t nnz = 0, nnz_cap = 0, nnz_ck = 0;
   DevBuf coo_ws;            // gather / sort / ALS workspace of the COO path
+  DevBuf grws, grk;         // GetRank in the update (R33): trial workspace, per-rep ranks [r]
+  int rep_rank[kMaxReps] = {};   // rank each rep of the last update decomposed at
   int32_t* ci() const { return X.as<int32_t>(); }
   int32_t* cj() const { return ci() + nnz_cap; }
   int32_t* ck_() const { return cj() + nnz_cap; }
@@ -195,6 +197,9 @@ void sambaten_default_opts(sambaten_opts* o) {
   o->init_max_iters = 1000;
   o->init_tol = 1e-6;
   o->stream = nullptr;
+  o->getrank = 0;
+  o->getrank_trials = 1;
+  o->getrank_threshold = 90.0;
 }
 
 const char* sambaten_last_error(void) { return sbt::g_err.c_str(); }
@@ -261,6 +266,12 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
     if (h->nnz_cap < h->nnz) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity < nnz0"); }
     h->Kcap = h->opts.capacity_k > 0 ? h->opts.capacity_k : 2 * h->K + 1024;
     if (h->Kcap < h->K) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity_k < K0"); }
+  }
+  if (h->opts.getrank) {
+    if (h->fmt != SAMBATEN_DENSE) { delete h; FAIL(SAMBATEN_E_INVALID, "init: getrank needs a dense tensor (R33)"); }
+    if (h->opts.getrank_trials < 1 || h->opts.getrank_trials > kMaxReps) {
+      delete h; FAIL(SAMBATEN_E_INVALID, "init: getrank_trials must be in [1, 32]");
+    }
   }
   h->st = stream_of(h->opts.stream);
   h->pitch = (h->I + 3) & ~int64_t(3);
@@ -349,7 +360,7 @@ extern "C" void sambaten_destroy(sambaten_t h) {
   h->model[0].release(); h->model[1].release(); h->ck.release();
   h->marg.release(); h->xm.release(); h->xm_ck.release(); h->samp.release(); h->summ.release(); h->fac.release();
   h->als.release(); h->match.release(); h->misc.release(); h->segs.release(); h->fitws.release();
-  h->coo_ws.release();
+  h->coo_ws.release(); h->grws.release(); h->grk.release();
   if (h->segs_host) cudaFreeHost(h->segs_host);
   if (h->hs) cudaFreeHost(h->hs);
   for (int e = 0; e < 9; ++e)
@@ -477,10 +488,108 @@ static cudaError_t run_sampling(sambaten_s* h, const int64_t* x1, const int64_t*
 
 // a5 (match against the batch-start model, R13-R16, R26) and a6 (merge into the shadow model,
 // P:216-227).  Records ev[6] between the two.
+// GetRank (Alg. 2; readings R29-R31) on nsum dense summaries Y + s * y_stride
+// ([K][J][pitch] each): for every candidate rank F = 1..R_max, `trials` CP-ALS runs (Philox
+// update_id 0x47520000 + F, rep = s * trials + j, R30) rated by CorConDia; R_new[s] = the largest
+// F whose best trial reaches `threshold` (R31), else 1.  cc (host, optional) gets [s][F-1][j].
+// Synchronises st: the rank fixes the launch shapes of what follows.
+static cudaError_t getrank_batch(const float* Y, int64_t y_stride, int64_t pitch, int I, int J, int K,
+                                 int nsum, int R_max, int trials, uint64_t seed, int max_iters, double tol,
+                                 double threshold, DevBuf& ws, cudaStream_t st, int* R_new, double* cc,
+                                 int* launches) {
+  constexpr uint32_t kGetRankId = 0x47520000u;   // R30
+  // trials == 1: the nsum summaries are one batch of models (rep = s); else one batch of
+  // `trials` models per summary (rep = s * trials + j)
+  const bool by_summary = trials == 1;
+  const int groups = by_summary ? 1 : nsum, nm = by_summary ? nsum : trials;
+  DenseAls a{};
+  a.y_stride = by_summary ? y_stride : 0; a.pitch = pitch;
+  a.nI = I; a.nJ = J; a.nK = K; a.R = R_max; a.r = nm;
+  a.maxit = max_iters; a.tol = tol;
+  const size_t ub = align256(sizeof(float) * (size_t)nm * (I + J + K) * R_max);
+  const size_t als_b = align256(dense_als_workspace(&a));
+  const size_t ccn = corcondia_ws_doubles(I, J, K, R_max, nm);
+  const size_t cc_b = align256(sizeof(double) * (ccn + (size_t)groups * R_max * nm));
+  cudaError_t e = ws.ensure(ub + als_b + cc_b);
+  if (e != cudaSuccess) return e;
+  char* base = ws.as<char>();
+  double* ccws = reinterpret_cast<double*>(base + ub + als_b);
+  double* ccd = ccws + ccn;   // [group][F-1][nm]
+  int nl = 0;
+  for (int g = 0; g < groups; ++g) {
+    a.Y = Y + (by_summary ? 0 : g * y_stride);
+    for (int F = 1; F <= R_max; ++F) {
+      a.R = F;
+      a.U[0] = reinterpret_cast<float*>(base);
+      a.U[1] = a.U[0] + (size_t)nm * I * F;
+      a.U[2] = a.U[1] + (size_t)nm * J * F;
+      a.u_stride[0] = (int64_t)I * F; a.u_stride[1] = (int64_t)J * F; a.u_stride[2] = (int64_t)K * F;
+      dense_als_workspace(&a);
+      if ((e = dense_als_bind_workspace(&a, base + ub)) != cudaSuccess) return e;
+      if ((e = launch_als_init(a, seed, kGetRankId + (uint32_t)F, (uint32_t)(g * trials), true, st)) != cudaSuccess)
+        return e;
+      if ((e = run_dense_als(a, st)) != cudaSuccess) return e;
+      const float* U[3] = {a.U[0], a.U[1], a.U[2]};
+      e = launch_corcondia(a.Y, a.y_stride, pitch, I, J, K, F, nm, U, a.u_stride, a.lam, ccws,
+                           ccd + ((size_t)g * R_max + F - 1) * nm, st);
+      if (e != cudaSuccess) return e;
+      nl += 4 + 7 * max_iters + 4;
+    }
+  }
+  std::vector<double> hc((size_t)groups * R_max * nm);
+  if ((e = cudaMemcpyAsync(hc.data(), ccd, sizeof(double) * hc.size(), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return e;
+  if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+  for (int s = 0; s < nsum; ++s) {
+    int best = 1;
+    for (int F = 1; F <= R_max; ++F) {
+      double m = -1e300;
+      for (int j = 0; j < trials; ++j) {
+        const double v = by_summary ? hc[(size_t)(F - 1) * nm + s] : hc[((size_t)s * R_max + F - 1) * nm + j];
+        if (cc) cc[((size_t)s * R_max + F - 1) * trials + j] = v;
+        m = std::max(m, v);
+      }
+      if (m >= threshold) best = F;
+    }
+    R_new[s] = best;
+  }
+  if (launches) *launches += nl;
+  return cudaSuccess;
+}
+
+// a4 with GetRank's ranks (R33): every repetition decomposes its summary at its own rank
+// R_new[rho] (Philox rep rho, as the plain path) and is padded with zero columns into the
+// R-column candidate buffers of `a` (whose workspace is bound).
+static cudaError_t rank_als(sambaten_s* h, const DenseAls& a, const int* R_new, uint32_t uid,
+                            cudaStream_t st, int* launches) {
+  DenseAls b{};
+  b.y_stride = 0; b.pitch = a.pitch; b.nI = a.nI; b.nJ = a.nJ; b.nK = a.nK; b.r = 1;
+  b.maxit = a.maxit; b.tol = a.tol;
+  b.R = a.R;
+  const size_t ub = align256(sizeof(float) * (size_t)(a.nI + a.nJ + a.nK) * a.R);
+  cudaError_t e = h->grws.ensure(ub + align256(dense_als_workspace(&b)));
+  if (e != cudaSuccess) return e;
+  for (int rho = 0; rho < a.r; ++rho) {
+    b.Y = a.Y + rho * a.y_stride;
+    b.R = R_new[rho];
+    b.U[0] = h->grws.as<float>();
+    b.U[1] = b.U[0] + (size_t)a.nI * b.R;
+    b.U[2] = b.U[1] + (size_t)a.nJ * b.R;
+    b.u_stride[0] = (int64_t)a.nI * b.R; b.u_stride[1] = (int64_t)a.nJ * b.R; b.u_stride[2] = (int64_t)a.nK * b.R;
+    dense_als_workspace(&b);
+    if ((e = dense_als_bind_workspace(&b, h->grws.as<char>() + ub)) != cudaSuccess) return e;
+    if ((e = launch_als_init(b, h->seed, uid, (uint32_t)rho, true, st)) != cudaSuccess) return e;
+    if ((e = run_dense_als(b, st)) != cudaSuccess) return e;
+    if ((e = launch_rank_pad(b, a, rho, st)) != cudaSuccess) return e;
+    *launches += 4 + 7 * a.maxit + 1;
+  }
+  return cudaSuccess;
+}
+
 static cudaError_t run_match_merge(sambaten_s* h, const DenseAls& a, const int32_t* Is, const int32_t* Js,
                                    const int32_t* Kp, const int32_t* locI, const int32_t* locJ,
                                    const int32_t* locK, int64_t Ko, int64_t Kn, int64_t nI, int64_t nJ,
-                                   int64_t nKs, int64_t nKp, int** accepted) {
+                                   int64_t nKs, int64_t nKp, int** accepted, const int* rnew = nullptr) {
   const int R = h->R, r = h->r;
   cudaStream_t st = h->st;
   const int b = h->cur, nb = 1 - h->cur;
@@ -502,6 +611,7 @@ static cudaError_t run_match_merge(sambaten_s* h, const DenseAls& a, const int32
   ma.lam_hat = (double*)mp; mp += align256(sizeof(double) * r * R);
   ma.score_min = (double*)mp; mp += align256(sizeof(double) * r);
   ma.accepted = (int*)mp;
+  ma.rnew = rnew;
   e = launch_match(ma, st);
   if (e != cudaSuccess) return e;
   e = cudaEventRecord(h->ev[6], st);
@@ -516,6 +626,7 @@ static cudaError_t run_match_merge(sambaten_s* h, const DenseAls& a, const int32
   g.loc[0] = locI; g.loc[1] = locJ; g.loc[2] = locK; g.nKs = (int)nKs;
   for (int m = 0; m < 3; ++m) { g.U[m] = a.U[m]; g.u_stride[m] = a.u_stride[m]; }
   g.pi = ma.pi; g.scale = ma.scale; g.lam_hat = ma.lam_hat; g.accepted = ma.accepted;
+  g.rnew = rnew;
   g.policy = h->opts.merge_policy;
   *accepted = ma.accepted;
   return launch_merge(g, st);
@@ -580,6 +691,7 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
     info->scale_exp = h->S;
     info->reps_pinv_mask = pm;
     info->kernel_launches = launches;
+    for (int rho = 0; rho < 32; ++rho) info->rep_rank[rho] = rho < r ? (h->opts.getrank ? h->rep_rank[rho] : R) : 0;
     for (int e = 0; e < 8; ++e) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);
@@ -1041,22 +1153,39 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   const size_t ws_d = use_cluster ? als_cluster_dscratch_bytes(a, cpl) : 0;
   CK(h->als.ensure(ws_als + ws_d));
   CK(dense_als_bind_workspace(&a, h->als.p));
-  int als_launches;
-  if (use_cluster) {
+  int als_launches = 0;
+  // GetRank on every summary (Alg. 2; R33): a rep whose summary shows fewer than R
+  // consistent components is decomposed at that rank and matches / merges only those
+  const int* d_rnew = nullptr;
+  if (h->opts.getrank) {
+    CK(getrank_batch(Y, y_stride, pI, (int)nI, (int)nJ, (int)nKp, r, R, h->opts.getrank_trials, h->seed,
+                     h->opts.als_max_iters, h->opts.als_tol, h->opts.getrank_threshold, h->grws, st,
+                     h->rep_rank, nullptr, &als_launches));
+    bool deficient = false;
+    for (int rho = 0; rho < r; ++rho) deficient |= h->rep_rank[rho] < R;
+    if (deficient) {
+      CK(h->grk.ensure(sizeof(int) * r));
+      CK(cudaMemcpyAsync(h->grk.p, h->rep_rank, sizeof(int) * r, cudaMemcpyHostToDevice, st));
+      d_rnew = h->grk.as<int>();
+    }
+  }
+  if (d_rnew) {
+    CK(rank_als(h, a, h->rep_rank, uid, st, &als_launches));
+  } else if (use_cluster) {
     CK(launch_als_init_factors(a, h->seed, uid, 0, st));
     CK(run_als_cluster(a, cpl, reinterpret_cast<float*>(h->als.as<char>() + ws_als), st));
     if (getenv("SAMBATEN_DEBUG")) als_phase_dump();
-    als_launches = 2;
+    als_launches += 2;
   } else {
     CK(launch_als_init(a, h->seed, uid, 0, true, st));
     CK(run_dense_als(a, st));
-    als_launches = 4 + 7 * a.maxit;
+    als_launches += 4 + 7 * a.maxit;
   }
   CK(cudaEventRecord(h->ev[5], st));
   // ---- a5 / a6: match and merge -----------------------------------------------------------
   const int b = h->cur, nb = 1 - h->cur;
   int* accepted = nullptr;
-  CK(run_match_merge(h, a, Is, Js, Kp, locI, locJ, locK, Ko, Kn, nI, nJ, nKs, nKp, &accepted));
+  CK(run_match_merge(h, a, Is, Js, Kp, locI, locJ, locK, Ko, Kn, nI, nJ, nKs, nKp, &accepted, d_rnew));
   CK(cudaEventRecord(h->ev[7], st));
   // ---- a7: full fit of the new model (optional) ------------------------------------------
   if (h->opts.full_fit) {
@@ -1477,7 +1606,7 @@ extern "C" sambaten_status sambaten_corcondia(const sambaten_tensor* X, int F, c
   double* out = static_cast<double*>(ws) + corcondia_ws_doubles(I, J, K, F, 1);
   const float* U[3] = {A, B, C};
   const int64_t us[3] = {0, 0, 0};
-  CK(launch_corcondia(X->vals, X->dims[0], I, J, K, F, 1, U, us, lambda, static_cast<double*>(ws), out, st));
+  CK(launch_corcondia(X->vals, 0, X->dims[0], I, J, K, F, 1, U, us, lambda, static_cast<double*>(ws), out, st));
   CK(cudaMemcpyAsync(cc, out, sizeof(double), cudaMemcpyDefault, st));
   CK(cudaFreeAsync(ws, st));
   CK(cudaStreamSynchronize(st));
@@ -1491,48 +1620,12 @@ extern "C" sambaten_status sambaten_getrank(const sambaten_tensor* X, int R_max,
   if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "getrank: dense tensors only");
   if (R_max < 1 || R_max > kMaxR || trials < 1 || trials > kMaxReps || max_iters < 1 || !R_new)
     FAIL(SAMBATEN_E_INVALID, "getrank: bad argument");
-  cudaStream_t st = stream_of(stream);
-  const int I = (int)X->dims[0], J = (int)X->dims[1], K = (int)X->dims[2];
-  constexpr uint32_t kGetRankId = 0x47520000u;   // R30
-  // one workspace for the largest candidate rank, reused by every rank
-  DenseAls a{};
-  a.Y = X->vals; a.y_stride = 0; a.pitch = X->dims[0];   // the same tensor for every trial
-  a.nI = I; a.nJ = J; a.nK = K; a.R = R_max; a.r = trials;
-  const size_t ub = align256(sizeof(float) * (size_t)trials * (I + J + K) * R_max);
-  const size_t als_b = align256(dense_als_workspace(&a));
-  const size_t cc_b = align256(sizeof(double) * (corcondia_ws_doubles(I, J, K, R_max, trials) + (size_t)R_max * trials));
-  void* ws = nullptr;
-  CK(cudaMallocAsync(&ws, ub + als_b + cc_b, st));
-  char* base = static_cast<char*>(ws);
-  double* ccws = reinterpret_cast<double*>(base + ub + als_b);
-  double* ccd = ccws + corcondia_ws_doubles(I, J, K, R_max, trials);
-  for (int F = 1; F <= R_max; ++F) {
-    a.R = F;
-    a.U[0] = reinterpret_cast<float*>(base);
-    a.U[1] = a.U[0] + (size_t)trials * I * F;
-    a.U[2] = a.U[1] + (size_t)trials * J * F;
-    a.u_stride[0] = (int64_t)I * F; a.u_stride[1] = (int64_t)J * F; a.u_stride[2] = (int64_t)K * F;
-    a.maxit = max_iters; a.tol = tol;
-    dense_als_workspace(&a);
-    CK(dense_als_bind_workspace(&a, base + ub));
-    CK(launch_als_init(a, seed, kGetRankId + (uint32_t)F, 0, true, st));
-    CK(run_dense_als(a, st));
-    const float* U[3] = {a.U[0], a.U[1], a.U[2]};
-    CK(launch_corcondia(X->vals, X->dims[0], I, J, K, F, trials, U, a.u_stride, a.lam, ccws,
-                        ccd + (size_t)(F - 1) * trials, st));
-  }
-  std::vector<double> h((size_t)R_max * trials);
-  CK(cudaMemcpyAsync(h.data(), ccd, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st));
-  CK(cudaFreeAsync(ws, st));
-  CK(cudaStreamSynchronize(st));
-  int best = 1;
-  for (int F = 1; F <= R_max; ++F) {
-    double m = -1e300;
-    for (int j = 0; j < trials; ++j) m = std::max(m, h[(size_t)(F - 1) * trials + j]);
-    if (m >= threshold) best = F;
-  }
-  *R_new = best;
-  if (cc) memcpy(cc, h.data(), sizeof(double) * h.size());
+  DevBuf ws;
+  const cudaError_t e = getrank_batch(X->vals, 0, X->dims[0], (int)X->dims[0], (int)X->dims[1], (int)X->dims[2],
+                                      1, R_max, trials, seed, max_iters, tol, threshold, ws, stream_of(stream),
+                                      R_new, cc, nullptr);
+  ws.release();
+  CK(e);
   return SAMBATEN_OK;
 }
 

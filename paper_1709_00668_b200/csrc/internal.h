@@ -109,11 +109,15 @@ cudaError_t run_dense_als(const DenseAls& a, cudaStream_t st);
 // single-mode MTTKRP for the stateless API (r = 1): M (fp32 [n_mode][R])
 cudaError_t dense_mttkrp_single(const DenseAls& a, int mode, float* M, cudaStream_t st);
 
-// GetRank (k_getrank.cu): CorConDia of nm models of one dense tensor (fp64)
+// GetRank (k_getrank.cu): CorConDia of nm models of dense tensors X + model * x_stride (fp64)
 size_t corcondia_ws_doubles(int I, int J, int K, int F, int nm);
-cudaError_t launch_corcondia(const float* X, int64_t pitch, int I, int J, int K, int F, int nm,
-                             const float* const U[3], const int64_t u_stride[3], const double* lam, double* ws,
-                             double* cc, cudaStream_t st);
+cudaError_t launch_corcondia(const float* X, int64_t x_stride, int64_t pitch, int I, int J, int K, int F,
+                             int nm, const float* const U[3], const int64_t u_stride[3], const double* lam,
+                             double* ws, double* cc, cudaStream_t st);
+// GetRank inside the update (R33): copy the r = 1 rank-src.R decomposition `src` into
+// repetition rho of the rank-dst.R candidate buffers of `dst` (columns >= src.R and their
+// lambda zero; fit / iters / flags copied)
+cudaError_t launch_rank_pad(const DenseAls& src, const DenseAls& dst, int rho, cudaStream_t st);
 
 // a5 / a6
 struct MatchArgs {
@@ -131,6 +135,8 @@ struct MatchArgs {
   double* lam_hat;   // [r][R]
   double* score_min; // [r]
   int* accepted;     // [r]
+  const int* rnew;   // [r] or null: rank of rep's candidate (GetRank, R33); only old components
+                     // matched to a real column (pi f < rnew) count for acceptance and merge
   double* part;      // [r][3][match_chunks][R*R + 2R] partial anchor sums (workspace)
 };
 int match_chunks(const MatchArgs& m);
@@ -145,6 +151,7 @@ struct MergeArgs {
   int nKs;
   const float* U[3]; int64_t u_stride[3];
   const int* pi; const double* scale; const double* lam_hat; const int* accepted;
+  const int* rnew;                   // [r] or null (see MatchArgs::rnew)
   int policy;
 };
 cudaError_t launch_merge(const MergeArgs& m, cudaStream_t st);

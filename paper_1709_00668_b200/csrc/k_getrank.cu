@@ -18,7 +18,7 @@ namespace {
 constexpr int kGT = 256;
 
 struct CcArgs {
-  const float* X;  int64_t pitch;      // dense [K][J][pitch]
+  const float* X;  int64_t x_stride, pitch;   // dense [nm][K][J][pitch] (x_stride 0: one tensor)
   int I, J, K, F, nm;                  // nm models
   const float* U[3]; int64_t u_stride[3];   // [nm][n][F] fp32 loadings
   const double* lam;                   // [nm][F]
@@ -93,7 +93,7 @@ __global__ void corcondia_t1_kernel(CcArgs a) {
     const int k = (int)(r % a.K);
     const int mdl = (int)(r / a.K);
     const double* P0 = a.P + ((int64_t)mdl * 3 + 0) * a.F * a.nmax + (int64_t)f * a.nmax;
-    const float* x = a.X + ((int64_t)k * a.J + j) * a.pitch;
+    const float* x = a.X + mdl * a.x_stride + ((int64_t)k * a.J + j) * a.pitch;
     double s = 0.0;
     for (int i = 0; i < a.I; ++i) s += P0[i] * (double)x[i];
     a.T1[(((int64_t)mdl * a.F + f) * a.J + j) * a.K + k] = s;
@@ -140,11 +140,11 @@ size_t corcondia_ws_doubles(int I, int J, int K, int F, int nm) {
   return (size_t)nm * (3 * (size_t)F * nmax + (size_t)F * J * K + (size_t)F * F * K + 12 * (size_t)F * F + 1);
 }
 
-cudaError_t launch_corcondia(const float* X, int64_t pitch, int I, int J, int K, int F, int nm,
-                             const float* const U[3], const int64_t u_stride[3], const double* lam, double* ws,
-                             double* cc, cudaStream_t st) {
+cudaError_t launch_corcondia(const float* X, int64_t x_stride, int64_t pitch, int I, int J, int K, int F,
+                             int nm, const float* const U[3], const int64_t u_stride[3], const double* lam,
+                             double* ws, double* cc, cudaStream_t st) {
   CcArgs a{};
-  a.X = X; a.pitch = pitch; a.I = I; a.J = J; a.K = K; a.F = F; a.nm = nm;
+  a.X = X; a.x_stride = x_stride; a.pitch = pitch; a.I = I; a.J = J; a.K = K; a.F = F; a.nm = nm;
   for (int m = 0; m < 3; ++m) { a.U[m] = U[m]; a.u_stride[m] = u_stride[m]; }
   a.lam = lam;
   a.nmax = max(I, max(J, K));
@@ -158,6 +158,50 @@ cudaError_t launch_corcondia(const float* X, int64_t pitch, int I, int J, int K,
   corcondia_t1_kernel<<<blocks((int64_t)nm * F * J * K), kGT, 0, st>>>(a);
   corcondia_t2_kernel<<<blocks((int64_t)nm * F * F * K), kGT, 0, st>>>(a);
   corcondia_core_kernel<<<nm, kGT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ---- GetRank inside the update (R33) -----------------------------------------------------
+namespace {
+struct PadArgs {
+  const float* Us[3]; const double* lams; const double* fits; const int* iters_s; const int* flags_s;
+  float* Ud[3]; double* lamd; double* fitd; int* itersd; int* flagsd;
+  int64_t n[3]; int Rs, Rd;
+};
+
+__global__ void rank_pad_kernel(PadArgs p) {
+  const int64_t n0 = p.n[0] * p.Rd, n1 = n0 + p.n[1] * p.Rd, n2 = n1 + p.n[2] * p.Rd;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= n2 + p.Rd; e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < n2) {
+      const int m = e < n0 ? 0 : e < n1 ? 1 : 2;
+      const int64_t o = e - (m == 0 ? 0 : m == 1 ? n0 : n1);
+      const int64_t row = o / p.Rd;
+      const int f = (int)(o - row * p.Rd);
+      p.Ud[m][o] = f < p.Rs ? p.Us[m][row * p.Rs + f] : 0.0f;
+    } else if (e < n2 + p.Rd) {
+      const int f = (int)(e - n2);
+      p.lamd[f] = f < p.Rs ? p.lams[f] : 0.0;
+    } else {
+      p.fitd[0] = p.fits[0]; p.itersd[0] = p.iters_s[0]; p.flagsd[0] = p.flags_s[0];
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_rank_pad(const DenseAls& src, const DenseAls& dst, int rho, cudaStream_t st) {
+  PadArgs p{};
+  for (int m = 0; m < 3; ++m) {
+    p.Us[m] = src.U[m];
+    p.Ud[m] = dst.U[m] + rho * dst.u_stride[m];
+  }
+  p.n[0] = dst.nI; p.n[1] = dst.nJ; p.n[2] = dst.nK;
+  p.Rs = src.R; p.Rd = dst.R;
+  p.lams = src.lam; p.fits = src.fit; p.iters_s = src.iters; p.flags_s = src.flags;
+  p.lamd = dst.lam + (int64_t)rho * dst.R; p.fitd = dst.fit + rho; p.itersd = dst.iters + rho;
+  p.flagsd = dst.flags + rho;
+  const int64_t tot = (p.n[0] + p.n[1] + p.n[2]) * p.Rd + p.Rd + 1;
+  const int64_t nb = ceil_div(tot, kGT);
+  rank_pad_kernel<<<(unsigned)(nb < kNumSMs * 4 ? nb : kNumSMs * 4), kGT, 0, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m, int n
         if (ok) lh = lh * sig * a1 / a0; else ok_all = false;
       }
       m.lam_hat[rep * R + f] = ok_all ? lh : 0.0;
+      if (m.rnew && g >= m.rnew[rep]) continue;   // matched to a zero padding column (R33)
       const double sc = S[f * R + g];
       if (sc != sc) nan = true;
       smin = fmin(smin, sc);
@@ -239,6 +240,7 @@ __global__ void merge_rows_kernel(MergeArgs g, int mode) {
   int cnt = 0;
   for (int rep = 0; rep < g.r; ++rep) {
     if (!g.accepted[rep]) continue;
+    if (g.rnew && g.pi[rep * R + f] >= g.rnew[rep]) continue;   // no candidate column (R33)
     const int l = loc[(int64_t)rep * n + row];
     if (l < 0) continue;
     const float* U = g.U[mode] + rep * g.u_stride[mode];
@@ -252,27 +254,31 @@ __global__ void merge_rows_kernel(MergeArgs g, int mode) {
 }
 
 __global__ void merge_new_kernel(MergeArgs g) {
+  // per component f: mean over the accepted reps that carry it (all accepted reps unless
+  // GetRank reduced a rep's rank, R33); no such rep -> C_new(:, f) = 0, lambda_f unchanged
   const int R = g.R;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int f = idx < g.Kn * R ? (int)(idx % R) : (int)(idx - g.Kn * R);
+  if (idx >= g.Kn * R + R) return;
+  auto carries = [&](int rep) {
+    return g.accepted[rep] && !(g.rnew && g.pi[rep * R + f] >= g.rnew[rep]);
+  };
   int nacc = 0;
-  for (int rep = 0; rep < g.r; ++rep) nacc += g.accepted[rep] ? 1 : 0;
-  if (nacc == 0) return;
+  for (int rep = 0; rep < g.r; ++rep) nacc += carries(rep) ? 1 : 0;
   if (idx < g.Kn * R) {
     const int64_t k = idx / R;
-    const int f = (int)(idx - k * R);
     double s = 0.0;
     for (int rep = 0; rep < g.r; ++rep) {
-      if (!g.accepted[rep]) continue;
+      if (!carries(rep)) continue;
       const float* U = g.U[2] + rep * g.u_stride[2];
       s += g.scale[((int64_t)rep * 3 + 2) * R + f] * (double)U[(g.nKs + k) * R + g.pi[rep * R + f]];
     }
-    g.Cn[(g.Ko + k) * R + f] = (float)(s / nacc);
-  } else if (idx < g.Kn * R + R) {
-    const int f = (int)(idx - g.Kn * R);
+    g.Cn[(g.Ko + k) * R + f] = nacc ? (float)(s / nacc) : 0.0f;
+  } else {
     double s = 0.0;
     for (int rep = 0; rep < g.r; ++rep)
-      if (g.accepted[rep]) s += g.lam_hat[rep * R + f];
-    g.lamn[f] = (float)(((double)g.lam[f] + s / nacc) / 2.0);
+      if (carries(rep)) s += g.lam_hat[rep * R + f];
+    g.lamn[f] = nacc ? (float)(((double)g.lam[f] + s / nacc) / 2.0) : g.lam[f];
   }
 }
 

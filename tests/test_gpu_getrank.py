@@ -68,3 +68,67 @@ def test_getrank_on_a_noisy_planted_summary():
     rn_o, cc_o = GR.getrank(Y, 7, 1, 3, 100, 0.0)
     rn_g, cc_g = L().sambaten_getrank(_dense(Y), 7, 1, 3, 100, 0.0)
     assert rn_g == rn_o == F, (cc_g.ravel(), cc_o.ravel())
+
+
+# ---- GetRank inside the update (opts.getrank, reading R33) --------------------------------
+def _stream(F_true, R, seed, I=40, J=36, K=30, K0=24):
+    """The oracle pin's stream (tests/test_oracle_getrank.py): planted rank F_true, the model
+    carries R >= F_true components (the extra ones with all-zero time factors)."""
+    rng = np.random.default_rng(seed)
+    A, B, C = rng.random((I, R)), rng.random((J, R)), rng.random((K, R))
+    C[:, F_true:] = 0.0
+    X = np.einsum("if,jf,kf->ijk", A, B, C)
+    T = np.ascontiguousarray(np.transpose(X, (2, 1, 0))).astype(np.float32)
+    model = [np.ascontiguousarray(x, dtype=np.float32) for x in (np.ones(R), A, B, C[:K0])]
+    return T[:K0], T[K0:], model
+
+
+def _run_gpu(T0, batch, model, R, seed, maxit, tol, getrank):
+    lam, A, B, C = model
+    opts = L().default_opts(als_max_iters=maxit, als_tol=tol, accept_tau=0.0, capacity=T0.shape[0] + batch.shape[0],
+                            full_fit=1, getrank=getrank)
+    h = L().sambaten_init_factors(_dense_kji(T0), R, 2, 3, seed, A, B, C, lam, opts)
+    try:
+        K = T0.shape[0] + batch.shape[0]
+        I, J = T0.shape[2], T0.shape[1]
+        out = [np.empty(R, np.float32), np.empty((I, R), np.float32), np.empty((J, R), np.float32),
+               np.empty((K, R), np.float32)]
+        info = L().sambaten_update(h, _dense_kji(batch), out[1], out[2], out[3], out[0])
+    finally:
+        L().sambaten_destroy(h)
+    return out, info
+
+
+def _dense_kji(T):
+    import torch
+    return L().dense(torch.from_numpy(np.ascontiguousarray(T)).cuda())
+
+
+def test_update_getrank_full_rank_is_the_plain_update():
+    """GetRank finds the universal rank on every summary -> bit-identical to the plain update."""
+    T0, batch, model = _stream(3, 3, 0)
+    plain, _ = _run_gpu(T0, batch, model, 3, 4, 300, 1e-12, 0)
+    gr, info = _run_gpu(T0, batch, model, 3, 4, 300, 1e-12, 1)
+    assert list(info.rep_rank[:3]) == [3, 3, 3]
+    for x, y in zip(plain, gr):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
+def test_update_getrank_rank_deficient_matches_oracle():
+    """Rank-deficient batch: per-rep ranks equal the oracle's; the third component keeps
+    its lambda bit for bit and gets exact-zero new time rows; the merged model agrees with the
+    oracle's (fp32 vs fp64 converged rank-2 ALS: 1e-3 relative)."""
+    from oracle import sambaten as O
+    T0, batch, model = _stream(2, 3, 1)
+    cfg = O.Config(R=3, s=(2, 2, 2), r=3, seed=6, maxit=400, tol=1e-12, tau=0.0, getrank=True)
+    st = O.init_factors(T0, cfg, *[np.asarray(x, np.float64) for x in model], T0.size * 2)
+    last = O.update(st, batch)
+    got, info = _run_gpu(T0, batch, model, 3, 6, 400, 1e-12, 1)
+    assert list(info.rep_rank[:3]) == [rp["rank"] for rp in last["reps"]] == [2, 2, 2]
+    assert info.reps_rejected_mask == 0
+    lam, A, B, C = got
+    assert lam[2] == model[0][2]
+    Kn = batch.shape[0]
+    assert np.all(C[-Kn:, 2] == 0.0)
+    for g, o in zip((lam, A, B, C), (st.lam, st.A, st.B, st.C)):
+        assert np.allclose(g, o, rtol=1e-3, atol=1e-5), np.abs(g - o).max()
