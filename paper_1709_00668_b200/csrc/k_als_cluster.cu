@@ -46,6 +46,8 @@ struct ClLayout {
   size_t G, Gp, Gs, Vi, W1, lam, sc, bars, P, Xun, Xun2, Msh, U0s, U1s, U2s, Dsh, stage, total;
   int chunk0, chunk1, ownK, stage_fl, T, NT;
   int NTA, sfla;       // pass A: teams (all warps but the inverse warp), floats per ring stage
+  int wideA, RPT, trA; // wide pass A: one team of all warps but the inverse warp, RPT rows per
+                       // step (thread = (row offset, column quad)), trA rows per ring stage
 };
 
 __host__ __device__ inline size_t al16(size_t b) { return (b + 15) & ~(size_t)15; }
@@ -110,6 +112,18 @@ __host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, in
   L.sfla = (int)(region / (sizeof(float) * kTS * L.NTA)) & ~3;
   if (L.sfla > 12288) L.sfla = 12288;
   if (L.sfla < pitch4(nI)) L.sfla = 0;   // too little room: pass A keeps the slice teams
+  // wide pass A: kTS stages of trA rows (a multiple of RPT when room allows) plus two W
+  // buffers of trA rows (W(u,q,:) = U1(q,:) * U2(u,:), row stride wstride(RB))
+  {
+    const int pA = pitch4(nI), qa = pA / 4;
+    L.RPT = (kCT - 32) / qa;
+    const size_t regf = region / sizeof(float);
+    int tr = (int)(regf / ((size_t)kTS * pA + 2 * (size_t)((RB + 3) & ~3)));
+    if (tr * pA > 12288) tr = 12288 / pA;
+    if (tr >= L.RPT && L.RPT > 0) tr -= tr % L.RPT;
+    L.trA = tr;
+    L.wideA = L.RPT >= 1 && tr >= 1;
+  }
   return L;
 }
 
@@ -520,6 +534,130 @@ __device__ __forceinline__ void team_pass_a(const float* __restrict__ region, in
   }
 }
 
+// Wide pass A: all warps but the inverse warp form ONE team over the CTA's row space
+// (rows g = (u, q) of the own slices, contiguous in Y), streamed through one ring of kTS
+// stages of trA rows.  Thread (sr, qd) handles column quad qd of rows sr, sr + RPT, ... of a
+// stage, so RPT * quads of the 480 lanes carry columns (>= 94 % for nI >= 100, vs 78 % for a
+// warp per row at nI = 100).  W(g, :) = U1(q, :) * U2(u, :) is formed once per row (one thread
+// per row, a stage ahead, into the W buffer the previous stage no longer reads) instead of by
+// every thread: the inner step is one float4 of Y, the W row and 4 * RB FMAs.
+// acc(c, f) += Y(u, q, col_c) W(g, f); P = sum over the RPT row offsets (fp64, fixed order).
+__device__ __forceinline__ int wstride(int RB) { return (RB + 3) & ~3; }
+
+template <int RB>
+__device__ __forceinline__ void ld_wrow(const float* p, float (&w)[RB]) {
+#pragma unroll
+  for (int f4 = 0; f4 < RB / 4; ++f4) {
+    const float4 v = reinterpret_cast<const float4*>(p)[f4];
+    w[4 * f4 + 0] = v.x; w[4 * f4 + 1] = v.y; w[4 * f4 + 2] = v.z; w[4 * f4 + 3] = v.w;
+  }
+  if constexpr (RB % 4 == 2) {
+    const float2 v = reinterpret_cast<const float2*>(p)[RB / 2 - 1];
+    w[RB - 2] = v.x; w[RB - 1] = v.y;
+  }
+}
+
+template <int RB>
+__device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, int nu, int nrow, int pitch,
+                                            const float* U1s, const float* U2s, float* rings, int tr,
+                                            int RPT, unsigned long long* bars, unsigned seq, double* P,
+                                            int ncol) {
+  constexpr int TA = kCT - 32;
+  constexpr int WS = (RB + 3) & ~3;
+  const int tid = threadIdx.x;
+  const bool in_team = tid < TA;
+  const int quads = pitch / 4;
+  const int sr = tid / quads, qd = tid - sr * quads;
+  const bool valid = in_team && sr < RPT;
+  const int rows = nu * nrow;
+  const int nst = (rows + tr - 1) / tr;
+  float* W = rings + (size_t)kTS * tr * pitch;
+  const float invn = 1.0f / (float)nrow;
+  auto issue = [&](int s) {
+    const int r0 = s * tr, nr = min(tr, rows - r0);
+    const unsigned buf = (seq + s) % kTS;
+    const unsigned bytes = (unsigned)(nr * pitch * sizeof(float));
+    mbar_expect_tx(&bars[buf], bytes);
+    bulk_g2s(rings + (size_t)buf * tr * pitch, region + (int64_t)r0 * pitch, bytes, &bars[buf]);
+  };
+  auto make_w = [&](int s) {   // one thread per row of stage s
+    const int r0 = s * tr, nr = min(tr, rows - r0);
+    float* w = W + (size_t)(s & 1) * tr * WS;
+    for (int row = tid; row < nr; row += TA) {
+      const int g = r0 + row;
+      int ul = __float2int_rz((float)g * invn);
+      if (ul * nrow > g) --ul;
+      else if ((ul + 1) * nrow <= g) ++ul;
+      const int q = g - ul * nrow;
+      float a[RB], b[RB];
+      ld_row<RB>(U1s + q * RB, a);
+      ld_row<RB>(U2s + ul * RB, b);
+#pragma unroll
+      for (int f = 0; f < RB; ++f) a[f] *= b[f];
+      float* wr = w + row * WS;
+#pragma unroll
+      for (int f4 = 0; f4 < RB / 4; ++f4)
+        reinterpret_cast<float4*>(wr)[f4] = make_float4(a[4 * f4], a[4 * f4 + 1], a[4 * f4 + 2], a[4 * f4 + 3]);
+      if constexpr (RB % 4 == 2) reinterpret_cast<float2*>(wr)[RB / 2 - 1] = make_float2(a[RB - 2], a[RB - 1]);
+    }
+  };
+  float acc[4][RB];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int f = 0; f < RB; ++f) acc[c][f] = 0.f;
+  if (in_team) {
+    if (tid == 0 && nst > 0) {
+      fence_proxy_async();
+      for (int s = 0; s < nst && s < kTS; ++s) issue(s);
+    }
+    if (nst > 0) make_w(0);
+    team_bar(1, TA);   // W of stage 0
+    for (int s = 0; s < nst; ++s) {
+      const int nr = min(tr, rows - s * tr);
+      const unsigned buf = (seq + s) % kTS;
+      if (s + 1 < nst) make_w(s + 1);   // its W buffer was last read in stage s - 1
+      mbar_wait(&bars[buf], ((seq + s) / kTS) & 1u);
+      if (valid) {
+        const float* st = rings + (size_t)buf * tr * pitch + 4 * qd;
+        const float* w = W + (size_t)(s & 1) * tr * WS;
+#pragma unroll 2
+        for (int row = sr; row < nr; row += RPT) {
+          const float4 y = *reinterpret_cast<const float4*>(st + row * pitch);
+          float wv[RB];
+          ld_wrow<RB>(w + row * WS, wv);
+#pragma unroll
+          for (int f = 0; f < RB; ++f) {
+            acc[0][f] = fmaf(y.x, wv[f], acc[0][f]);
+            acc[1][f] = fmaf(y.y, wv[f], acc[1][f]);
+            acc[2][f] = fmaf(y.z, wv[f], acc[2][f]);
+            acc[3][f] = fmaf(y.w, wv[f], acc[3][f]);
+          }
+        }
+      }
+      team_bar(1, TA);   // stage s consumed, W of stage s + 1 complete
+      if (tid == 0 && s + kTS < nst) {
+        fence_proxy_async();
+        issue(s + kTS);
+      }
+    }
+  }
+  __syncthreads();   // no copy in flight: the ring region becomes the reduction buffer
+  float* red = rings;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int f = 0; f < RB; ++f) red[(c * RB + f) * kCT + tid] = acc[c][f];
+  __syncthreads();
+  for (int e = tid; e < ncol * RB; e += kCT) {
+    const int col = e / RB, f = e - col * RB;
+    const float* rr = red + ((col & 3) * RB + f) * kCT + (col >> 2);
+    double sum = 0.0;
+    for (int t = 0; t < RPT; ++t) sum += (double)rr[t * quads];
+    P[e] = sum;
+  }
+}
+
 __device__ __forceinline__ int team_stages_a(int team, int NTA, int total, int pitch, int sfl) {
   const int trmax = sfl / pitch > 0 ? sfl / pitch : 1;
   int g0, g1;
@@ -537,7 +675,9 @@ __device__ __forceinline__ int team_stages(int team, int nu, int NT, int nrow, i
 
 template <int RB>
 __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS, float* Dglob,
-                                                             int stage_fl, int dsh) {
+                                                             int stage_fl, int dshw) {
+  // dshw: bit 0 = D in shared memory (plan), bit 1 = narrow pass A (SAMBATEN_ALS_NARROW_A)
+  const int dsh = dshw & 1;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int rep = blockIdx.x / CS;
@@ -582,6 +722,8 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
   float* D = dsh ? reinterpret_cast<float*>(smem + Ly.Dsh) : Dglob + ((int64_t)rep * nK + u0) * nJ * RB;
   const int myteam = tid / Ly.T;
   unsigned tseq = 0;                                       // TMA stages this team consumed
+  unsigned seqA = 0;                                       // stages of the wide pass A (barrier set 15)
+  const bool wideA = Ly.wideA && !(dshw & 2);
   float* gU0 = a.U[0] + rep * a.u_stride[0];
   float* gU1 = a.U[1] + rep * a.u_stride[1];
   float* gU2 = a.U[2] + rep * a.u_stride[2];
@@ -642,7 +784,10 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       // warp 0: Vi = (G_o1 * G_o2)^-1 while the other warps stream
       if (warp == kCW - 1) warp_normal_inverse<RB>(G, m, R, Gs, Vi, W1, s_fc, &s_flags);
       if (m == 0) {
-        if (Ly.sfla > 0) {
+        if (wideA) {
+          wide_pass_a<RB>(regA, nu, nJ, pI, U1s, U2s, ring, Ly.trA, Ly.RPT, bars + 15 * kTS, seqA, P, nI);
+          seqA += (unsigned)((nu * nJ + Ly.trA - 1) / Ly.trA);
+        } else if (Ly.sfla > 0) {
           team_pass_a<RB>(regA, nu, nJ, nI, pI, U1s, U2s, ring, Ly.sfla, bars, Ly.T, Ly.NTA, tseq, P);
           if (myteam < Ly.NTA) tseq += team_stages_a(myteam, Ly.NTA, nu * nJ, pI, Ly.sfla);
         } else {
@@ -678,12 +823,17 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         Msh[pl * RB + f] = cluster_sum(P, (c0 + pl) * RB + f, CS);
       }
       __syncthreads();
+      float* Us = m == 0 ? U0s : U1s;
 #pragma unroll 1
       for (int e = tid; e < nr * R; e += kCT) {
         const int pl = e / R, f = e - pl * R;
         double s = 0.0;
         for (int g = 0; g < R; ++g) s += Msh[pl * RB + g] * Vi[g * R + f];
         Xun[pl * RB + f] = s;
+        // push the solved row (unnormalised, fp32) into every CTA's copy of U_m: no CTA reads
+        // U_m between S1 and S2 (pass A reads U1/U2, pass B U0/U2), and S2 publishes the stores
+        const float xf = __double2float_rn(s);
+        for (int c = 0; c < CS; ++c) cluster.map_shared_rank(Us, c)[(c0 + pl) * RB + f] = xf;
       }
       __syncthreads();
 #pragma unroll 1
@@ -709,31 +859,48 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         const int f = pr / R, g = pr - f * R;
         G[m * RB * RB + pr] = Gs[pr] * (s_linv[f] * s_linv[g]);
       }
-      float* Us = m == 0 ? U0s : U1s;
+      if (m == 1) __syncthreads();   // G_1 complete: warp 15 inverts V_2 = G_0 * G_1 below
+      if (m == 0) {
 #pragma unroll 1
-      for (int e = tid; e < n * R; e += kCT) {
-        const int p = e / R, f = e - p * R;
-        const int c = p / ch;
-        const double x = cluster.map_shared_rank(Xun, c)[(p - c * ch) * RB + f];
-        Us[p * RB + f] = __double2float_rn(x * s_linv[f]);
+        for (int e = tid; e < n * R; e += kCT) {
+          const int p = e / R, f = e - p * R;
+          Us[p * RB + f] = __double2float_rn((double)Us[p * RB + f] * s_linv[f]);
+        }
+      } else if (warp < kCW - 1) {
+        // the 12 warps off the inverting warp's scheduler (warp % 4 != 3) normalise U_1: the
+        // inverse is a latency chain and gets its sub-partition's issue slots to itself
+        if ((warp & 3) != 3) {
+          const int wt = warp - (warp >> 2);   // 0..11
+#pragma unroll 1
+          for (int e = wt * 32 + lane; e < n * R; e += 12 * 32) {
+            const int p = e / R, f = e - p * R;
+            Us[p * RB + f] = __double2float_rn((double)Us[p * RB + f] * s_linv[f]);
+          }
+        }
+      } else {
+        // V_2 = (G_0 * G_1)^-1 overlaps the normalisation of U_1 and the M2 loop below
+#ifdef SBT_ALS_PHASES
+        const long long tinv0 = clock64();
+#endif
+        warp_normal_inverse<RB>(G, 2, R, Gs, Vi, W1, s_fc, &s_flags);
+#ifdef SBT_ALS_PHASES
+        if (lane == 0 && rep == 0 && rank == 0) atomicAdd(&g_als_phase[20], (unsigned long long)(clock64() - tinv0));
+#endif
       }
-      __syncthreads();
+      if (m == 0) __syncthreads();
+      else if (warp < kCW - 1) team_bar(1, kCT - 32);   // U_1 normalised (the inverting warp runs on)
       PH(m == 0 ? 5 : 11);
     }
     // ==================================== mode 2 ====================================
 #ifdef SBT_ALS_PHASES
     const long long tinv0 = clock64();
-#endif
-    if (warp == kCW - 1) warp_normal_inverse<RB>(G, 2, R, Gs, Vi, W1, s_fc, &s_flags);
-#ifdef SBT_ALS_PHASES
-    if (warp == kCW - 1 && lane == 0 && rep == 0 && rank == 0) atomicAdd(&g_als_phase[20], (unsigned long long)(clock64() - tinv0));
     if (tid == 0 && rep == 0 && rank == 0) atomicAdd(&g_als_phase[22], 1ull);
 #endif
-    // M2(u,f) = sum_q D(u,q,f) U1(q,f) for the own slices: a warp per slice (the warps other
-    // than the one inverting V2, which overlaps): lane partials over q = lane + 32 t in fp32
-    // (<= nJ / 32 terms), then one fp64 butterfly per f
+    // M2(u,f) = sum_q D(u,q,f) U1(q,f) for the own slices: a warp per slice (the 12 warps
+    // off the scheduler of warp 15, which is still inverting V2): lane partials over
+    // q = lane + 32 t in fp32 (<= nJ / 32 terms), then one fp64 butterfly per f
 #pragma unroll 1
-    for (int ul = warp; warp < kCW - 1 && ul < nu; ul += kCW - 1) {
+    for (int ul = warp - (warp >> 2); (warp & 3) != 3 && ul < nu; ul += 12) {   // the 12 warps off the inverse's scheduler
       const float* d = D + (int64_t)ul * nJ * RB;
       float pa[RB];
 #pragma unroll
@@ -796,23 +963,25 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       s_linv[tid] = lam[tid] > 0.0 ? __drcp_rn(lam[tid]) : 1.0;
     }
     __syncthreads();
+    if (warp < kCW - 1) {
 #pragma unroll 1
-    for (int pr = tid; pr < RR; pr += kCT) {
-      const int f = pr / R, g = pr - f * R;
-      G[2 * RB * RB + pr] = Gs[pr] * (s_linv[f] * s_linv[g]);
-    }
+      for (int pr = tid; pr < RR; pr += kCT - 32) {
+        const int f = pr / R, g = pr - f * R;
+        G[2 * RB * RB + pr] = Gs[pr] * (s_linv[f] * s_linv[g]);
+      }
 #pragma unroll 1
-    for (int e = tid; e < nu * R; e += kCT) {
-      const int ul = e / R, f = e - ul * R;
-      U2s[ul * RB + f] = __double2float_rn(Xun2[ul * RB + f] * s_linv[f]);
-    }
-    __syncthreads();
-    // fit (warp 0; every CTA computes the same value -> uniform control flow)
-    if (warp == 0) {
+      for (int e = tid; e < nu * R; e += kCT - 32) {
+        const int ul = e / R, f = e - ul * R;
+        U2s[ul * RB + f] = __double2float_rn(Xun2[ul * RB + f] * s_linv[f]);
+      }
+    } else {
+      // fit (the last warp, overlapping the two loops above; every CTA computes the same
+      // value -> uniform control flow).  G_2 formed here as the loop above forms it.
       double mn = 0.0;
       for (int pr = lane; pr < RR; pr += 32) {
         const int f = pr / R, g = pr - f * R;
-        mn += lam[f] * lam[g] * G[pr] * G[RB * RB + pr] * G[2 * RB * RB + pr];
+        const double g2 = Gs[pr] * (s_linv[f] * s_linv[g]);
+        mn += lam[f] * lam[g] * G[pr] * G[RB * RB + pr] * g2;
       }
       mn = warp_sum_d(mn);
       const double inner = lane == 0 ? cluster_sum(sc, 1, CS) : 0.0;
@@ -1003,7 +1172,8 @@ static cudaError_t cluster_launch(const DenseAls& a, const ClusterPlan& pl, floa
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[1];
   fill_cfg(&cfg, attr, pl.CS, a.r, pl.smem, st);
-  return cudaLaunchKernelEx(&cfg, als_cluster_kernel<RB>, a, pl.CS, Dglob, pl.stage_fl, pl.dsh);
+  return cudaLaunchKernelEx(&cfg, als_cluster_kernel<RB>, a, pl.CS, Dglob, pl.stage_fl,
+                            pl.dsh | (getenv("SAMBATEN_ALS_NARROW_A") ? 2 : 0));
 }
 
 cudaError_t run_als_cluster(const DenseAls& a, const ClusterPlan& pl, float* Dglob, cudaStream_t st) {
