@@ -417,9 +417,13 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
 #pragma unroll
       for (int f = 0; f < RB; ++f) red[(c * RB + f) * kCT + tid] = acc[c][f];
     __syncthreads();
-    for (int e = tid; e < ncol * RB; e += kCT) {
-      const int col = e / RB, f = e - col * RB;
-      const float* rr = red + ((col & 3) * RB + f) * kCT + (col >> 2);
+    // (c, f) outer, column quad inner: a warp reads consecutive words (conflict-free)
+    const int nq = (ncol + 3) >> 2;
+    for (int e = tid; e < 4 * RB * nq; e += kCT) {
+      const int cf = e / nq, qd = e - cf * nq;
+      const int col = 4 * qd + cf / RB, f = cf % RB;
+      if (col >= ncol) continue;
+      const float* rr = red + cf * kCT + qd;
       double v[16];
 #pragma unroll
       for (int t = 0; t < 16; ++t) v[t] = t < NT ? (double)rr[t * T] : 0.0;
@@ -427,7 +431,7 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
 #pragma unroll
       for (int t = 0; t < 16; ++t)
         if (t < NT) sum += v[t];
-      P[e] = sum;
+      P[col * RB + f] = sum;
     }
   }
 }
@@ -520,9 +524,13 @@ __device__ __forceinline__ void team_pass_a(const float* __restrict__ region, in
 #pragma unroll
     for (int f = 0; f < RB; ++f) red[(c * RB + f) * kCT + tid] = acc[c][f];
   __syncthreads();
-  for (int e = tid; e < ncol * RB; e += kCT) {
-    const int col = e / RB, f = e - col * RB;
-    const float* rr = red + ((col & 3) * RB + f) * kCT + (col >> 2);
+  // (c, f) outer, column quad inner: a warp reads consecutive words (conflict-free)
+  const int nq = (ncol + 3) >> 2;
+  for (int e = tid; e < 4 * RB * nq; e += kCT) {
+    const int cf = e / nq, qd = e - cf * nq;
+    const int col = 4 * qd + cf / RB, f = cf % RB;
+    if (col >= ncol) continue;
+    const float* rr = red + cf * kCT + qd;
     double v[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t) v[t] = t < NTA ? (double)rr[t * T] : 0.0;
@@ -530,7 +538,7 @@ __device__ __forceinline__ void team_pass_a(const float* __restrict__ region, in
 #pragma unroll
     for (int t = 0; t < 16; ++t)
       if (t < NTA) sum += v[t];
-    P[e] = sum;
+    P[col * RB + f] = sum;
   }
 }
 
@@ -611,13 +619,23 @@ __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, in
       fence_proxy_async();
       for (int s = 0; s < nst && s < kTS; ++s) issue(s);
     }
+#ifdef SBT_ALS_PHASES
+    const long long tp0 = clock64();
+    long long tw = 0, tb = 0;
+#endif
     if (nst > 0) make_w(0);
     team_bar(1, TA);   // W of stage 0
     for (int s = 0; s < nst; ++s) {
       const int nr = min(tr, rows - s * tr);
       const unsigned buf = (seq + s) % kTS;
       if (s + 1 < nst) make_w(s + 1);   // its W buffer was last read in stage s - 1
+#ifdef SBT_ALS_PHASES
+      const long long tw0 = clock64();
+#endif
       mbar_wait(&bars[buf], ((seq + s) / kTS) & 1u);
+#ifdef SBT_ALS_PHASES
+      tw += clock64() - tw0;
+#endif
       if (valid) {
         const float* st = rings + (size_t)buf * tr * pitch + 4 * qd;
         const float* w = W + (size_t)(s & 1) * tr * WS;
@@ -635,12 +653,25 @@ __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, in
           }
         }
       }
+#ifdef SBT_ALS_PHASES
+      const long long tb0 = clock64();
+#endif
       team_bar(1, TA);   // stage s consumed, W of stage s + 1 complete
+#ifdef SBT_ALS_PHASES
+      tb += clock64() - tb0;
+#endif
       if (tid == 0 && s + kTS < nst) {
         fence_proxy_async();
         issue(s + kTS);
       }
     }
+#ifdef SBT_ALS_PHASES
+    if ((tid == 0 || tid == 448) && blockIdx.x == 0) {
+      atomicAdd(&g_als_phase[tid == 0 ? 16 : 23], (unsigned long long)tw);
+      atomicAdd(&g_als_phase[tid == 0 ? 18 : 24], (unsigned long long)(clock64() - tp0));
+      atomicAdd(&g_als_phase[tid == 0 ? 25 : 26], (unsigned long long)tb);
+    }
+#endif
   }
   __syncthreads();   // no copy in flight: the ring region becomes the reduction buffer
   float* red = rings;
@@ -649,12 +680,16 @@ __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, in
 #pragma unroll
     for (int f = 0; f < RB; ++f) red[(c * RB + f) * kCT + tid] = acc[c][f];
   __syncthreads();
-  for (int e = tid; e < ncol * RB; e += kCT) {
-    const int col = e / RB, f = e - col * RB;
-    const float* rr = red + ((col & 3) * RB + f) * kCT + (col >> 2);
+  // (c, f) outer, column quad inner: a warp reads consecutive words (conflict-free)
+  const int nq = (ncol + 3) >> 2;
+  for (int e = tid; e < 4 * RB * nq; e += kCT) {
+    const int cf = e / nq, qd = e - cf * nq;
+    const int col = 4 * qd + cf / RB, f = cf % RB;
+    if (col >= ncol) continue;
+    const float* rr = red + cf * kCT + qd;
     double sum = 0.0;
     for (int t = 0; t < RPT; ++t) sum += (double)rr[t * quads];
-    P[e] = sum;
+    P[col * RB + f] = sum;
   }
 }
 
@@ -782,7 +817,14 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       const int n = m == 0 ? nI : nJ;
       const int ch = m == 0 ? Ly.chunk0 : Ly.chunk1;
       // warp 0: Vi = (G_o1 * G_o2)^-1 while the other warps stream
+#ifdef SBT_ALS_PHASES
+      const long long ti0 = clock64();
+#endif
       if (warp == kCW - 1) warp_normal_inverse<RB>(G, m, R, Gs, Vi, W1, s_fc, &s_flags);
+#ifdef SBT_ALS_PHASES
+      if (warp == kCW - 1 && lane == 0 && rep == 0 && rank == 0)
+        atomicAdd(&g_als_phase[27 + m], (unsigned long long)(clock64() - ti0));
+#endif
       if (m == 0) {
         if (wideA) {
           wide_pass_a<RB>(regA, nu, nJ, pI, U1s, U2s, ring, Ly.trA, Ly.RPT, bars + 15 * kTS, seqA, P, nI);
@@ -1157,7 +1199,7 @@ void als_phase_dump() {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(h, g_als_phase, sizeof(h));
   fprintf(stderr, "[sambaten] als phases (cycles, rank 0 of rep 0):");
-  for (int k = 0; k < 23; ++k) fprintf(stderr, " %d:%llu", k, h[k]);
+  for (int k = 0; k < 32; ++k) fprintf(stderr, " %d:%llu", k, h[k]);
   fprintf(stderr, "\n");
   memset(h, 0, sizeof(h));
   cudaMemcpyToSymbol(g_als_phase, h, sizeof(h));

@@ -11,7 +11,8 @@ w = CONFIGS[cfg]
 T, truth = planted_dense(w.I, w.J, w.K, w.R, noise=w.noise, seed=w.seed)
 T0, batches = split_dense(T, w.K0, w.batch)
 model = [np.ascontiguousarray(np.asarray(x, np.float32)) for x in (truth[0], truth[1], truth[2], truth[3][:w.K0])]
-opts = L.default_opts(als_max_iters=w.maxit, als_tol=w.tol, capacity=w.K, full_fit=1)
+tol = float(os.environ.get("PROBE_TOL", w.tol))   # PROBE_TOL=0: fixed iteration count
+opts = L.default_opts(als_max_iters=w.maxit, als_tol=tol, capacity=w.K, full_fit=1, accept_tau=0.0 if os.environ.get("PROBE_TOL") else w.tau if hasattr(w, "tau") else 0.9)
 h = L.sambaten_init_factors(L.dense(torch.from_numpy(T0).cuda()), w.R, w.s, w.r, w.seed,
                             model[1], model[2], model[3], model[0], opts)
 L.sambaten_checkpoint(h)
