@@ -91,8 +91,8 @@ __host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, in
   L.Xun = take(sizeof(double) * (size_t)mrows * RB);
   L.Xun2 = take(sizeof(double) * (size_t)L.ownK * RB);
   L.Msh = take(sizeof(double) * (size_t)mrows * RB);
-  L.U0s = take(sizeof(float) * (size_t)nI * RB);
-  L.U1s = take(sizeof(float) * (size_t)nJ * RB);
+  L.U0s = take(sizeof(float) * (size_t)nI * ((RB + 3) & ~3));
+  L.U1s = take(sizeof(float) * (size_t)nJ * ((RB + 3) & ~3));
   L.U2s = take(sizeof(float) * (size_t)L.ownK * RB);
   L.Dsh = take(dsh ? sizeof(float) * (size_t)L.ownK * nJ * RB : 0);
   // per-team TMA rings (kTS stages of whole rows, at least one row of the wider layout); the
@@ -174,6 +174,23 @@ __device__ __forceinline__ void ld_row(const float* p, float (&w)[RB]) {
     }
   }
 }
+// Row stride (floats) of the CTA's U0 / U1 copies and of the wide pass's W rows: RB rounded
+// up to a float4 multiple, so a row is whole float4 loads (+ one float2 when RB % 4 == 2).
+__host__ __device__ __forceinline__ int wstride(int RB) { return (RB + 3) & ~3; }
+
+template <int RB>
+__device__ __forceinline__ void ld_wrow(const float* p, float (&w)[RB]) {
+#pragma unroll
+  for (int f4 = 0; f4 < RB / 4; ++f4) {
+    const float4 v = reinterpret_cast<const float4*>(p)[f4];
+    w[4 * f4 + 0] = v.x; w[4 * f4 + 1] = v.y; w[4 * f4 + 2] = v.z; w[4 * f4 + 3] = v.w;
+  }
+  if constexpr (RB % 4 == 2) {
+    const float2 v = reinterpret_cast<const float2*>(p)[RB / 2 - 1];
+    w[RB - 2] = v.x; w[RB - 1] = v.y;
+  }
+}
+
 template <int RB>
 __device__ __forceinline__ void st_row(float* p, const float (&w)[RB]) {
   if constexpr (RB % 4 == 0) {
@@ -370,12 +387,12 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
 #endif
     if (valid) {
       const float* st = ring + buf * stage_fl + 4 * lt;
-      const float* wr = Uw + r0 * RB;
+      const float* wr = Uw + r0 * ((RB + 3) & ~3);
 #pragma unroll 2
       for (int row = 0; row < nr; ++row) {
         const float4 y = *reinterpret_cast<const float4*>(st + row * pitch);
         float w[RB];
-        ld_row<RB>(wr + row * RB, w);
+        ld_wrow<RB>(wr + row * ((RB + 3) & ~3), w);
         if (!PASSB) {
 #pragma unroll
           for (int f = 0; f < RB; ++f) w[f] *= u2[f];
@@ -490,7 +507,7 @@ __device__ __forceinline__ void team_pass_a(const float* __restrict__ region, in
       for (int row = 0; row < nr; ++row) {
         const float4 y = *reinterpret_cast<const float4*>(st + row * pitch);
         float w[RB];
-        ld_row<RB>(Uw + q * RB, w);
+        ld_wrow<RB>(Uw + q * ((RB + 3) & ~3), w);
 #pragma unroll
         for (int f = 0; f < RB; ++f) w[f] *= u2[f];
 #pragma unroll
@@ -550,21 +567,6 @@ __device__ __forceinline__ void team_pass_a(const float* __restrict__ region, in
 // per row, a stage ahead, into the W buffer the previous stage no longer reads) instead of by
 // every thread: the inner step is one float4 of Y, the W row and 4 * RB FMAs.
 // acc(c, f) += Y(u, q, col_c) W(g, f); P = sum over the RPT row offsets (fp64, fixed order).
-__device__ __forceinline__ int wstride(int RB) { return (RB + 3) & ~3; }
-
-template <int RB>
-__device__ __forceinline__ void ld_wrow(const float* p, float (&w)[RB]) {
-#pragma unroll
-  for (int f4 = 0; f4 < RB / 4; ++f4) {
-    const float4 v = reinterpret_cast<const float4*>(p)[f4];
-    w[4 * f4 + 0] = v.x; w[4 * f4 + 1] = v.y; w[4 * f4 + 2] = v.z; w[4 * f4 + 3] = v.w;
-  }
-  if constexpr (RB % 4 == 2) {
-    const float2 v = reinterpret_cast<const float2*>(p)[RB / 2 - 1];
-    w[RB - 2] = v.x; w[RB - 1] = v.y;
-  }
-}
-
 template <int RB>
 __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, int nu, int nrow, int pitch,
                                             const float* U1s, const float* U2s, float* rings, int tr,
@@ -598,7 +600,7 @@ __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, in
       else if ((ul + 1) * nrow <= g) ++ul;
       const int q = g - ul * nrow;
       float a[RB], b[RB];
-      ld_row<RB>(U1s + q * RB, a);
+      ld_wrow<RB>(U1s + q * WS, a);
       ld_row<RB>(U2s + ul * RB, b);
 #pragma unroll
       for (int f = 0; f < RB; ++f) a[f] *= b[f];
@@ -763,14 +765,15 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
   float* gU1 = a.U[1] + rep * a.u_stride[1];
   float* gU2 = a.U[2] + rep * a.u_stride[2];
   const int RR = R * R;
+  constexpr int US = (RB + 3) & ~3;   // row stride of U0s / U1s
 
   // ---- initial factors (zero-padded to RB columns), Grams, ||Y||^2 -------------------------
-  for (int e = tid; e < nI * RB; e += kCT) {
-    const int p = e / RB, f = e - p * RB;
+  for (int e = tid; e < nI * US; e += kCT) {
+    const int p = e / US, f = e - p * US;
     U0s[e] = f < R ? gU0[(int64_t)p * R + f] : 0.f;
   }
-  for (int e = tid; e < nJ * RB; e += kCT) {
-    const int q = e / RB, f = e - q * RB;
+  for (int e = tid; e < nJ * US; e += kCT) {
+    const int q = e / US, f = e - q * US;
     U1s[e] = f < R ? gU1[(int64_t)q * R + f] : 0.f;
   }
   for (int e = tid; e < nu * RB; e += kCT) {
@@ -787,8 +790,8 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
   for (int pr = tid; pr < 3 * RR; pr += kCT) {
     const int m = pr / RR, fg = pr - m * RR, f = fg / R, g = fg - f * R;
     double s = 0.0;
-    if (m == 0) for (int p = 0; p < nI; ++p) s += (double)U0s[p * RB + f] * (double)U0s[p * RB + g];
-    if (m == 1) for (int q = 0; q < nJ; ++q) s += (double)U1s[q * RB + f] * (double)U1s[q * RB + g];
+    if (m == 0) for (int p = 0; p < nI; ++p) s += (double)U0s[p * US + f] * (double)U0s[p * US + g];
+    if (m == 1) for (int q = 0; q < nJ; ++q) s += (double)U1s[q * US + f] * (double)U1s[q * US + g];
     if (m == 2) for (int u = 0; u < nK; ++u) s += (double)gU2[(int64_t)u * R + f] * (double)gU2[(int64_t)u * R + g];
     G[m * RB * RB + fg] = s;
   }
@@ -844,13 +847,13 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
                             tseq, D, P);
         if (myteam < Ly.NT) tseq += team_stages(myteam, nu, Ly.NT, nI, pJ, Ly.stage_fl);
         __syncthreads();   // D of the own slices complete (global, visible to the CTA)
-        // P(q,f) = sum_{own u} U2(u,f) D(u,q,f)   (fixed order, fp64)
+        // P(q,f) = sum_{own u} U2(u,f) D(u,q,f)   (fixed order; an fp32 run of <= ceil(K'/CS)
+        // terms, like the passes' per-thread runs, widened once)
         for (int e = tid; e < nJ * RB; e += kCT) {
           const int f = e % RB;
-          double s = 0.0;
-          for (int ul = 0; ul < nu; ++ul)
-            s += (double)U2s[ul * RB + f] * (double)D[(int64_t)ul * nJ * RB + e];
-          P[e] = s;
+          float s = 0.f;
+          for (int ul = 0; ul < nu; ++ul) s = fmaf(U2s[ul * RB + f], D[(int64_t)ul * nJ * RB + e], s);
+          P[e] = (double)s;
         }
         PH(6);
       }
@@ -875,7 +878,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         // push the solved row (unnormalised, fp32) into every CTA's copy of U_m: no CTA reads
         // U_m between S1 and S2 (pass A reads U1/U2, pass B U0/U2), and S2 publishes the stores
         const float xf = __double2float_rn(s);
-        for (int c = 0; c < CS; ++c) cluster.map_shared_rank(Us, c)[(c0 + pl) * RB + f] = xf;
+        for (int c = 0; c < CS; ++c) cluster.map_shared_rank(Us, c)[(c0 + pl) * US + f] = xf;
       }
       __syncthreads();
 #pragma unroll 1
@@ -906,7 +909,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
 #pragma unroll 1
         for (int e = tid; e < n * R; e += kCT) {
           const int p = e / R, f = e - p * R;
-          Us[p * RB + f] = __double2float_rn((double)Us[p * RB + f] * s_linv[f]);
+          Us[p * US + f] = __double2float_rn((double)Us[p * US + f] * s_linv[f]);
         }
       } else if (warp < kCW - 1) {
         // the 12 warps off the inverting warp's scheduler (warp % 4 != 3) normalise U_1: the
@@ -916,7 +919,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
 #pragma unroll 1
           for (int e = wt * 32 + lane; e < n * R; e += 12 * 32) {
             const int p = e / R, f = e - p * R;
-            Us[p * RB + f] = __double2float_rn((double)Us[p * RB + f] * s_linv[f]);
+            Us[p * US + f] = __double2float_rn((double)Us[p * US + f] * s_linv[f]);
           }
         }
       } else {
@@ -950,7 +953,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       for (int q = lane; q < nJ; q += 32) {
         float dv[RB], uv[RB];
         ld_row<RB>(d + (int64_t)q * RB, dv);
-        ld_row<RB>(U1s + q * RB, uv);
+        ld_wrow<RB>(U1s + q * US, uv);
 #pragma unroll
         for (int f = 0; f < RB; ++f) pa[f] = fmaf(dv[f], uv[f], pa[f]);
       }
@@ -1050,12 +1053,12 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
     const int c0 = min(nI, rank * Ly.chunk0), c1 = min(nI, c0 + Ly.chunk0);
     for (int e = tid; e < (c1 - c0) * R; e += kCT) {
       const int pl = e / R, f = e - pl * R;
-      gU0[(int64_t)(c0 + pl) * R + f] = U0s[(c0 + pl) * RB + f];
+      gU0[(int64_t)(c0 + pl) * R + f] = U0s[(c0 + pl) * US + f];
     }
     const int d0 = min(nJ, rank * Ly.chunk1), d1 = min(nJ, d0 + Ly.chunk1);
     for (int e = tid; e < (d1 - d0) * R; e += kCT) {
       const int ql = e / R, f = e - ql * R;
-      gU1[(int64_t)(d0 + ql) * R + f] = U1s[(d0 + ql) * RB + f];
+      gU1[(int64_t)(d0 + ql) * R + f] = U1s[(d0 + ql) * US + f];
     }
     for (int e = tid; e < nu * R; e += kCT) {
       const int ul = e / R, f = e - ul * R;
