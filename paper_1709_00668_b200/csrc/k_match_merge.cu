@@ -44,6 +44,68 @@ __device__ void hungarian_max(const double* S, int R, int* pi) {
   for (int j = 1; j <= R; ++j) pi[p[j] - 1] = j - 1;
 }
 
+// The same Hungarian method with the column loops spread over the lanes of one warp
+// (lane j - 1 owns column j): the arithmetic per element and the choice of j1 (first column
+// of minimal minv, strict <) are those of hungarian_max, so pi is identical.  Shared state
+// sh: u, v, minv [kMaxR + 1] doubles; p, way [kMaxR + 1] ints.
+__device__ void hungarian_max_warp(const double* S, int R, int* pi, double* u, double* v, int* p,
+                                   int* way) {
+  const int lane = threadIdx.x & 31;
+  const int j = lane + 1;                   // this lane's column (valid if j <= R)
+  const bool col = j <= R;
+  if (lane <= R) { u[lane] = 0.0; v[lane] = 0.0; p[lane] = 0; way[lane] = 0; }
+  __syncwarp();
+  for (int i = 1; i <= R; ++i) {
+    if (lane == 0) p[0] = i;
+    int j0 = 0;
+    double minv = 1e300;
+    bool used = false;      // lane's column used; column 0 is tracked by used0
+    bool used0 = false;
+    __syncwarp();
+    do {
+      if (j0 == 0) used0 = true;
+      else if (j == j0) used = true;
+      const int i0 = p[j0];
+      const double ui0 = u[i0];
+      // candidate of this lane
+      double cand = 1e300;
+      int cj = 0x7fffffff;
+      if (col && !used) {
+        const double cur = -S[(i0 - 1) * R + (j - 1)] - ui0 - v[j];
+        if (cur < minv) { minv = cur; way[j] = j0; }
+        cand = minv; cj = j;
+      }
+      // delta = min over unused columns, first column on ties
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double oc = __shfl_xor_sync(0xffffffffu, cand, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, cj, o);
+        if (oc < cand || (oc == cand && oj < cj)) { cand = oc; cj = oj; }
+      }
+      const double delta = cand;
+      const int j1 = cj == 0x7fffffff ? 0 : cj;
+      __syncwarp();   // every lane has read u[i0], v[j] before the updates
+      if (col) {
+        if (used) { u[p[j]] += delta; v[j] -= delta; }
+        else minv -= delta;
+      }
+      if (lane == 0 && used0) { u[p[0]] += delta; v[0] -= delta; }
+      __syncwarp();
+      j0 = j1;
+    } while (p[j0] != 0);
+    if (lane == 0) {
+      do {
+        const int j1 = way[j0];
+        p[j0] = p[j1];
+        j0 = j1;
+      } while (j0);
+    }
+    __syncwarp();
+  }
+  if (col) pi[p[j] - 1] = j - 1;
+  __syncwarp();
+}
+
 __device__ __forceinline__ void unrank_perm(long long k, int R, int* perm) {
   int avail[8];
   long long fact[9];
@@ -129,6 +191,8 @@ __global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m, int n
   __shared__ double bval[kMatchThreads];
   __shared__ long long bidx[kMatchThreads];
   __shared__ int pi_s[kMaxR];
+  __shared__ double hu[kMaxR + 1], hv[kMaxR + 1];
+  __shared__ int hp[kMaxR + 1], hway[kMaxR + 1];
   const int npair = R * R + 2 * R;
   for (int mode = 0; mode < 3; ++mode) {
     const double* part = m.part + ((int64_t)rep * 3 + mode) * nchunk * npair;
@@ -178,7 +242,7 @@ __global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m, int n
       for (int f = 0; f < R; ++f) pi_s[f] = perm[f];
     }
   } else {
-    if (threadIdx.x == 0) hungarian_max(S, R, pi_s);
+    if (threadIdx.x < 32) hungarian_max_warp(S, R, pi_s, hu, hv, hp, hway);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
