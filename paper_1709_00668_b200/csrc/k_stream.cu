@@ -227,11 +227,13 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
 // fixed order by fit_combine_kernel.
 // ---------------------------------------------------------------------------------------
 // a7 fit: inner = <X, [[lam; A, B, C]]> and ||X||^2 in one pass over whole-row stages.  A
-// thread owns QPT column quads and folds C(k, :) into its registers, alc(i, f) = lam_f A(i,f)
-// C(k,f) (reloaded when the slice k changes), so row (j, k) needs only B(j, :):
-// m(i) = sum_f alc(i,f) B(j,f), inner += X(i,j,k) m(i).  BRES: B (J x RB, zero padded) resident
-// in shared memory; else the B rows of stage s+1 are loaded into registers while stage s is
-// consumed and stored to a double buffer after it.  fp32 per element and stage, fp64 across.
+// thread owns QPT column quads; row (j, k) needs only B(j, :).  QPT = 1: the thread
+// accumulates acc(i, f) += X(i,j,k) B(j,f) over its rows of a slice (independent FMA chains)
+// and the slice's lam_f A(i,f) C(k,f) multiplies acc at a fold (slice change, or a stage end
+// after >= kFoldRows = 128 rows).  QPT = 2: alc(i,f) = lam_f A(i,f) C(k,f) in registers,
+// m(i) = sum_f alc(i,f) B(j,f), inner += X(i,j,k) m(i) (measured faster at 2 quads).  BRES: B (J x RB, zero padded) resident in
+// shared memory; else the B rows of stage s+1 are loaded into registers while stage s is
+// consumed and stored to a double buffer after it.  fp32 runs, fp64 across folds / stages.
 constexpr int kFitT2 = 384;       // fit: threads per CTA at 2 quads per thread (<= 168 registers)
 
 template <int RB, int QPT, bool BRES>
@@ -297,6 +299,119 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) fit_stream_kernel(
   __syncthreads();
   if (tid == 0)
     for (int s = 0; s < nst && s < g.ns; ++s) marg_issue(ring, bars, g, X, rb, re, s);
+  double inner = 0.0, sq = 0.0;
+  if constexpr (QPT == 1) {
+  // acc(i, f) = sum over the thread's rows (j, k) of one slice k of X(i, j, k) B(j, f) for its
+  // QPT column quads: a mode-1 MTTKRP row kept in registers (independent FMA chains); folded
+  // into inner += sum_{i,f} lam_f A(i,f) C(k,f) acc(i,f) when the slice changes or at the end
+  // of a stage after >= kFoldRows rows (fp32 runs of < kFoldRows + a stage's rows, fp64 across
+  // folds).
+  constexpr int kFoldRows = 128;
+  float acc[QPT][4][RB];
+#pragma unroll
+  for (int u = 0; u < QPT; ++u)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int f = 0; f < RB; ++f) acc[u][e][f] = 0.f;
+  int64_t kc = -1;
+  int run = 0;
+  auto fold = [&](int64_t k) {
+    const int64_t kg = kmap ? kmap[k] : k;
+    float lc[RB];
+#pragma unroll
+    for (int f = 0; f < RB; ++f) lc[f] = f < R ? lam[f] * C[kg * R + f] : 0.f;
+    float t = 0.f;
+#pragma unroll
+    for (int u = 0; u < QPT; ++u)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 4 * (tq + u * g.tpg) + e;
+#pragma unroll
+        for (int f = 0; f < RB; ++f) {
+          if (i < g.ncol && f < R) t = fmaf(A[(int64_t)i * R + f] * lc[f], acc[u][e][f], t);
+          acc[u][e][f] = 0.f;
+        }
+      }
+    inner += (double)t;
+    run = 0;
+  };
+  for (int s = 0; s < nst; ++s) {
+    const int slot = s % g.ns;
+    const int64_t r0 = rb + (int64_t)s * g.tr;
+    const int nr = (int)min((int64_t)g.tr, re - r0);
+    int jn = js + g.tr;   // the next stage's first row
+    int64_t kn = ks;
+    if (jn >= J) { kn += jn / J; jn -= (jn / J) * J; }
+    if (!BRES && s + 1 < nst) load_w(r0 + g.tr, jn);   // loads in flight while stage s is consumed
+    s_wait(&bars[s % g.ns], (unsigned)(s / g.ns) & 1u);
+    if (active) {
+      const float* st = ring + (size_t)slot * g.tr * g.pitch;
+      const float* W = Wbuf + (BRES ? 0 : (size_t)(s & 1) * g.tr * RB);
+      float fs = 0.f;
+      // segments of the stage with one slice k each
+      int64_t k = r0 / J;
+      int j = (int)(r0 - k * J);
+      for (int ra = 0; ra < nr;) {
+        const int seg = min(nr - ra, J - j);
+        if (k != kc) {
+          if (kc >= 0) fold(kc);
+          kc = k;
+        }
+#pragma unroll 1
+        for (int r = ra + ((grp - ra) % g.ng + g.ng) % g.ng; r < ra + seg; r += g.ng) {
+          const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
+          float w[RB];
+          if constexpr (RB % 4 == 0) {
+#pragma unroll
+            for (int f4 = 0; f4 < RB / 4; ++f4) {
+              const float4 wv = *reinterpret_cast<const float4*>(wr + 4 * f4);
+              w[4 * f4] = wv.x; w[4 * f4 + 1] = wv.y; w[4 * f4 + 2] = wv.z; w[4 * f4 + 3] = wv.w;
+            }
+          } else {
+#pragma unroll
+            for (int f2 = 0; f2 < RB / 2; ++f2) {
+              const float2 wv = *reinterpret_cast<const float2*>(wr + 2 * f2);
+              w[2 * f2] = wv.x; w[2 * f2 + 1] = wv.y;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < QPT; ++u) {
+            const int q = tq + u * g.tpg;
+            if (q < nq) {
+              const float4 v = *reinterpret_cast<const float4*>(st + (size_t)r * g.pitch + 4 * q);
+#pragma unroll
+              for (int f = 0; f < RB; ++f) {
+                acc[u][0][f] = fmaf(v.x, w[f], acc[u][0][f]);
+                acc[u][1][f] = fmaf(v.y, w[f], acc[u][1][f]);
+                acc[u][2][f] = fmaf(v.z, w[f], acc[u][2][f]);
+                acc[u][3][f] = fmaf(v.w, w[f], acc[u][3][f]);
+              }
+              // padding columns are zero in the store
+              fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
+            }
+          }
+          ++run;
+        }
+        ra += seg;
+        j = 0;
+        ++k;
+      }
+      if (run >= kFoldRows) fold(kc);   // at stage ends only: the row loop stays branch-free
+      sq += (double)fs;
+    }
+    if (!BRES && s + 1 < nst) store_w(s + 1);   // the other W buffer (free since the last barrier)
+    __syncthreads();   // stage (and W(s)) consumed
+    if (tid == 0 && s + g.ns < nst) {
+      s_fence_async();
+      marg_issue(ring, bars, g, X, rb, re, s + g.ns);
+    }
+    ks = kn;
+    js = jn;
+  }
+  if (active && kc >= 0) fold(kc);
+  } else {
+  // QPT = 2 (rows of > 2048 floats): the earlier form measures faster there (C4: 30 vs 33 ms)
   // lam_f A(i,f) [* C(k,f) when BRES] of the thread's QPT column quads (tq + u * tpg)
   float al[QPT][4][RB];
   int64_t kc = -1;
@@ -316,7 +431,6 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) fit_stream_kernel(
           al[u][e][f] = v;
         }
   };
-  double inner = 0.0, sq = 0.0;
   for (int s = 0; s < nst; ++s) {
     const int slot = s % g.ns;
     const int64_t r0 = rb + (int64_t)s * g.tr;
@@ -395,6 +509,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) fit_stream_kernel(
     }
     ks = kn;
     js = jn;
+  }
   }
   inner = block_sum_d(inner, red);
   sq = block_sum_d(sq, red);
