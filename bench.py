@@ -604,6 +604,33 @@ def main():
             "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in vi) for k in range(8)},
             "note": "opts.incremental_marginals=1: a1 adds the batch's contribution to the committed "
                     "int64 marginals (bit-identical to the full pass; tests/test_gpu_incremental.py)"}}
+        if not work.coo and not device_gen:
+            # GetRank before every summary decomposition (opts.getrank, reading R33): Alg. 2 over
+            # candidate ranks 1..R on all r summaries, then ALS at the chosen ranks
+            L.sambaten_destroy(h)
+            opts.incremental_marginals = 0
+            opts.getrank = 1
+            h = init_single(L, work, w, opts, config)
+            L.sambaten_checkpoint(h)
+            for i in range(nb):
+                with torch.cuda.stream(stream):
+                    L.sambaten_update(h, dbatches[i])
+            L.sambaten_restore(h)
+            state["i"] = 0
+            for _ in range(args.warmup):
+                step()
+            gt, gi, ge = [], [], []
+            for _ in range(min(args.steps, 5)):
+                ms, info, ne, bi = step()
+                gt.append(ms)
+                gi.append(info.as_dict())
+                ge.append(ne)
+            line["variants"]["getrank_in_update"] = {
+                "value": sum(ge) / (sum(gt) / 1000.0), "unit": unit, "ms_per_step": statistics.mean(gt),
+                "steps": len(gt), "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in gi) for k in range(8)},
+                "rep_rank_last": gi[-1]["rep_rank"][:w.r],
+                "note": "opts.getrank=1 (P:266, Alg. 2; R33): a4 includes GetRank over ranks 1..R on every summary"}
+            opts.getrank = 0
     L.sambaten_destroy(h)
     if rank == 0 and not work.coo and not args.no_getrank:
         line["getrank"] = getrank_timing(L, w, stream)

@@ -132,6 +132,17 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
     const int slot = s % g.ns;
     s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
     const float* st = ring + (size_t)slot * g.tr * g.pitch + c0;
+    // (slice, row) of the stage's first row: one division per stage; rows within the stage
+    // step from it (a 32-bit division only where a stage wraps past a slice end)
+    const int64_t sk0 = r0 / J;
+    const int sj0 = (int)(r0 - sk0 * J);
+    auto slice_of = [&](int r, int* jo) -> int64_t {
+      int jj = sj0 + r;
+      int64_t kk = sk0;
+      if (jj >= J) { const int q = jj / J; kk += q; jj -= q * J; }
+      *jo = jj;
+      return kk;
+    };
     for (int rw = wslot * kRPW; rw < nr; rw += g.wpc * kRPW) {
       long long rs[kRPW];
 #pragma unroll
@@ -170,8 +181,8 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
           if (lane == v) mine = rs[v];
         const int r = rw + lane;
         if (r < nr && mine) {
-          const int64_t row = r0 + r;
-          const int64_t k = row / J, j = row - k * J;
+          int j;
+          slice_of(r, &j);
           atomicAdd(&x2[j], (unsigned long long)mine);
         }
       }
@@ -180,7 +191,8 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
         for (int v = 0; v < kRPW; ++v) {
           const int r = rw + v;
           if (r < nr) {
-            const int64_t k = (r0 + r) / J;
+            int jdummy;
+            const int64_t k = slice_of(r, &jdummy);
             if (k != x3k) {
               if (x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
               x3k = k;
@@ -350,8 +362,8 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) fit_stream_kernel(
       const float* W = Wbuf + (BRES ? 0 : (size_t)(s & 1) * g.tr * RB);
       float fs = 0.f;
       // segments of the stage with one slice k each
-      int64_t k = r0 / J;
-      int j = (int)(r0 - k * J);
+      int64_t k = ks;   // the stage cursor: (slice, row) of row r0
+      int j = js;
       for (int ra = 0; ra < nr;) {
         const int seg = min(nr - ra, J - j);
         if (k != kc) {
@@ -483,8 +495,8 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) fit_stream_kernel(
         }
       };
       // segments of the stage with one slice k each; C(k, :) folded into al at a change
-      int64_t k = r0 / J;
-      int j = (int)(r0 - k * J);
+      int64_t k = ks;   // the stage cursor: (slice, row) of row r0
+      int j = js;
       for (int ra = 0; ra < nr;) {
         const int seg = min(nr - ra, J - j);
         if (k != kc) {
@@ -519,14 +531,24 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) fit_stream_kernel(
   }
 }
 
-__global__ void fit_combine_kernel(const double* part, int nb, const double* G, const float* lam,
-                                   int R, double* relerr) {
+// The block stages the partials and Grams in shared memory with coalesced loads; thread 0 then
+// sums them in the fixed sequential order (no global-load latency chain).
+constexpr int kCombT = 256;
+__global__ void __launch_bounds__(kCombT) fit_combine_kernel(const double* part, int nb, const double* G,
+                                                            const float* lam, int R, double* relerr) {
+  __shared__ double sp[2 * kNumSMs];
+  __shared__ double sg[3 * kMaxR * kMaxR];
+  __shared__ double sl[kMaxR];
+  for (int e = threadIdx.x; e < 2 * nb; e += blockDim.x) sp[e] = part[e];
+  for (int e = threadIdx.x; e < 3 * R * R; e += blockDim.x) sg[e] = G[e];
+  for (int e = threadIdx.x; e < R; e += blockDim.x) sl[e] = (double)lam[e];
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double inner = 0.0, sq = 0.0, mn = 0.0;
-  for (int b = 0; b < nb; ++b) { inner += part[2 * b]; sq += part[2 * b + 1]; }
+  for (int b = 0; b < nb; ++b) { inner += sp[2 * b]; sq += sp[2 * b + 1]; }
   for (int f = 0; f < R; ++f)
     for (int g = 0; g < R; ++g)
-      mn += (double)lam[f] * (double)lam[g] * G[f * R + g] * G[R * R + f * R + g] * G[2 * R * R + f * R + g];
+      mn += sl[f] * sl[g] * sg[f * R + g] * sg[R * R + f * R + g] * sg[2 * R * R + f * R + g];
   const double res = fmax(0.0, sq - 2.0 * inner + mn);
   *relerr = sq > 0.0 ? sqrt(res / sq) : 0.0;
 }
@@ -699,7 +721,7 @@ static cudaError_t fit_stream_rb(const DenseView& X, const float* lam, const flo
   double* G = ws + 2 * (size_t)kNumSMs;
   e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
   if (e != cudaSuccess) return e;
-  fit_combine_kernel<<<1, 32, 0, st>>>(part, nparts, G, lam, R, relerr);
+  fit_combine_kernel<<<1, kCombT, 0, st>>>(part, nparts, G, lam, R, relerr);
   return cudaGetLastError();
 }
 
