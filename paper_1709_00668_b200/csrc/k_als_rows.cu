@@ -190,10 +190,13 @@ __global__ void als_reduce_kernel(RowsAls a, int mode) {
     G[pr] = Gx[pr] / (lf * lg);
   }
   __syncthreads();
+  __shared__ double G0[3 * kMaxR * kMaxR];   // the three Grams, staged for thread 0's sum
+  if (mode == 2)
+    for (int e = threadIdx.x; e < 3 * npair; e += blockDim.x) G0[e] = a.G[(int64_t)rep * 3 * npair + e];
+  __syncthreads();
   if (mode == 2 && threadIdx.x == 0) {
     // fit = 1 - sqrt(||Y||^2 - 2 <Y, M> + ||M||^2) / ||Y||  with <Y, M> = sum x M2 (lambda
     // cancels) and ||M||^2 = lam^T (G0 * G1 * G2) lam
-    const double* G0 = a.G + (int64_t)rep * 3 * R * R;
     double mn = 0.0;
     for (int f = 0; f < R; ++f)
       for (int g = 0; g < R; ++g)
@@ -222,15 +225,16 @@ __global__ void als_scale_kernel(RowsAls a, int mode) {
   const double* lam = a.lam + rep * R;
   const double* X = a.X + (int64_t)rep * a.x_stride;
   float* U = a.U[mode] + rep * a.u_stride[mode];
-  const int64_t b = (int64_t)tile * kRT * R, e = min((int64_t)(tile + 1) * kRT, (int64_t)n) * R;
+  const int row0 = tile * kRT;
+  const int nel = (min(row0 + kRT, n) - row0) * R;   // the tile's elements (32-bit index math)
   float* Up = a.Up[mode] ? a.Up[mode] + rep * a.up_stride[mode] : nullptr;
-  for (int64_t t = b + threadIdx.x; t < e; t += blockDim.x) {
-    const int64_t row = t / R;
-    const int f = (int)(t - row * R);
+  for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+    const int rl = e / R, f = e - rl * R;
+    const int64_t t = (int64_t)row0 * R + e;
     const double l = lam[f];
     const float u = __double2float_rn(l > 0.0 ? X[t] / l : X[t]);
     U[t] = u;
-    if (Up) Up[row * a.RBp + f] = u;
+    if (Up) Up[(int64_t)(row0 + rl) * a.RBp + f] = u;
   }
 }
 
