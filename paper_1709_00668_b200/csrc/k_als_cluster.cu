@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
   __shared__ double s_linv[kMaxR];   // 1 / lambda_f (1 for a zero column)
   __shared__ double s_red[32];
   __shared__ int s_flags, s_stop;
-  __shared__ double s_fit;
+  __shared__ double s_fit, s_inner;
 #ifdef SBT_ALS_PHASES
   long long ph_t = clock64();
 #endif
@@ -1002,6 +1002,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
     PH(14);
 #pragma unroll 1
     for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = cluster_sum(Gp, 2 * RB * RB + pr, CS);
+    if (tid == kCT - 1) s_inner = cluster_sum(sc, 1, CS);   // the fit's <Y, M>, fetched alongside
     __syncthreads();
     if (tid < R) {
       lam[tid] = sqrt(Gs[tid * R + tid]);
@@ -1029,7 +1030,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         mn += lam[f] * lam[g] * G[pr] * G[RB * RB + pr] * g2;
       }
       mn = warp_sum_d(mn);
-      const double inner = lane == 0 ? cluster_sum(sc, 1, CS) : 0.0;
+      const double inner = s_inner;
       if (lane == 0) {
         const double res = fmax(0.0, ysq - 2.0 * inner + mn);
         const double f = ysq > 0.0 ? 1.0 - sqrt(res) / sqrt(ysq) : 0.0;
