@@ -530,8 +530,10 @@ def main():
         L.sambaten_restore(h)
         for _ in range(args.warmup):
             step(host=True)
+        e2e_infos = []
         for _ in range(args.steps):
-            ms, _, ne, bi = step(host=True)
+            ms, einfo, ne, bi = step(host=True)
+            e2e_infos.append(einfo.as_dict())
             e2e_times.append(ms)
             e2e_ents.append(ne)
             lb = local_batches[bi]
@@ -572,7 +574,10 @@ def main():
         hb = int(statistics.mean(e2e_in))
         db = 4 * (w.I + w.J + w.K + 1) * w.R
         line["e2e"] = {"value": reps * sum(e2e_ents) / e2e_tot, "unit": unit,
-                       "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db}
+                       "h2d_bytes_per_step": hb, "d2h_bytes_per_step": db,
+                       "ms_per_step": 1000.0 * e2e_tot / len(e2e_times),
+                       "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in e2e_infos)
+                                   for k in range(8)}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not device_gen:
         model = work.model
         if model is not None:

@@ -279,6 +279,15 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
   return SAMBATEN_OK;
 }
 
+// Rows of `width` bytes between pitched buffers: one linear copy when both sides are
+// contiguous (a 2D copy of many short rows runs far below the link rate from host memory),
+// else a 2D copy.
+static cudaError_t copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                             size_t rows, cudaStream_t st) {
+  if (dpitch == width && spitch == width) return cudaMemcpyAsync(dst, src, width * rows, cudaMemcpyDefault, st);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDefault, st);
+}
+
 static sambaten_status alloc_store_and_model(sambaten_s* h, const sambaten_tensor* X0) {
   if (h->fmt == SAMBATEN_DENSE) {
     const size_t store = (size_t)h->Kcap * h->J * h->pitch * sizeof(float);
@@ -297,8 +306,8 @@ static sambaten_status alloc_store_and_model(sambaten_s* h, const sambaten_tenso
     } else {
       CK(h->X.ensure(store));
       CK(cudaMemsetAsync(h->X.p, 0, store, h->st));
-      CK(cudaMemcpy2DAsync(h->X.p, h->pitch * sizeof(float), X0->vals, h->I * sizeof(float),
-                           h->I * sizeof(float), h->J * h->K, cudaMemcpyDefault, h->st));
+      CK(copy_rows(h->X.p, h->pitch * sizeof(float), X0->vals, h->I * sizeof(float),
+                        h->I * sizeof(float), h->J * h->K, h->st));
     }
   } else {
     CK(h->X.ensure((size_t)h->nnz_cap * (3 * sizeof(int32_t) + sizeof(float))));
@@ -1084,8 +1093,8 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     }
     CK(cudaEventRecord(h->ev_side[0], st));
     CK(cudaStreamWaitEvent(h->st2, h->ev_side[0], 0));
-    CK(cudaMemcpy2DAsync(dst, h->pitch * sizeof(float), batch->vals, h->I * sizeof(float),
-                         h->I * sizeof(float), h->J * Kn, cudaMemcpyDefault, h->st2));
+    CK(copy_rows(dst, h->pitch * sizeof(float), batch->vals, h->I * sizeof(float),
+                        h->I * sizeof(float), h->J * Kn, h->st2));
     CK(cudaEventRecord(h->ev_side[1], h->st2));
     CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
     CK(marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, st));   // a1, old slices
@@ -1096,8 +1105,8 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     // device batch, contiguous store: one pass copies and tracks max |x|
     CK(launch_ingest_dense(batch->vals, dst, nb_fl, h->opts.moi, d_maxphi, st));
   } else {
-    CK(cudaMemcpy2DAsync(dst, h->pitch * sizeof(float), batch->vals, h->I * sizeof(float),
-                         h->I * sizeof(float), h->J * Kn, cudaMemcpyDefault, st));
+    CK(copy_rows(dst, h->pitch * sizeof(float), batch->vals, h->I * sizeof(float),
+                        h->I * sizeof(float), h->J * Kn, st));
     CK(launch_max_phi_dense(V, Ko, Kn, h->opts.moi, d_maxphi, st));
   }
   CK(cudaEventRecord(h->ev[1], st));
