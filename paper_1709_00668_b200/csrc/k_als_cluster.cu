@@ -41,6 +41,7 @@ constexpr int kCW = kCT / 32;     // warps per CTA
 
 
 constexpr int kTS = 3;            // TMA stages per team
+constexpr int kTSA = 2;           // TMA stages of the wide pass A (larger stages, fewer team barriers)
 
 struct ClLayout {
   size_t G, Gp, Gs, Vi, W1, lam, sc, bars, P, Xun, Xun2, Msh, U0s, U1s, U2s, Dsh, stage, total;
@@ -112,14 +113,14 @@ __host__ __device__ inline ClLayout cl_layout(int nI, int nJ, int nK, int RB, in
   L.sfla = (int)(region / (sizeof(float) * kTS * L.NTA)) & ~3;
   if (L.sfla > 12288) L.sfla = 12288;
   if (L.sfla < pitch4(nI)) L.sfla = 0;   // too little room: pass A keeps the slice teams
-  // wide pass A: kTS stages of trA rows (a multiple of RPT when room allows) plus two W
+  // wide pass A: kTSA stages of trA rows (a multiple of RPT when room allows) plus two W
   // buffers of trA rows (W(u,q,:) = U1(q,:) * U2(u,:), row stride wstride(RB))
   {
     const int pA = pitch4(nI), qa = pA / 4;
     L.RPT = (kCT - 32) / qa;
     const size_t regf = region / sizeof(float);
-    int tr = (int)(regf / ((size_t)kTS * pA + 2 * (size_t)((RB + 3) & ~3)));
-    if (tr * pA > 12288) tr = 12288 / pA;
+    int tr = (int)(regf / ((size_t)kTSA * pA + 2 * (size_t)((RB + 3) & ~3)));
+    if ((size_t)tr * pA * sizeof(float) > (1u << 19)) tr = (int)((1u << 19) / (sizeof(float) * pA));   // mbarrier tx-count
     if (tr >= L.RPT && L.RPT > 0) tr -= tr % L.RPT;
     L.trA = tr;
     L.wideA = L.RPT >= 1 && tr >= 1;
@@ -581,11 +582,11 @@ __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, in
   const bool valid = in_team && sr < RPT;
   const int rows = nu * nrow;
   const int nst = (rows + tr - 1) / tr;
-  float* W = rings + (size_t)kTS * tr * pitch;
+  float* W = rings + (size_t)kTSA * tr * pitch;
   const float invn = 1.0f / (float)nrow;
   auto issue = [&](int s) {
     const int r0 = s * tr, nr = min(tr, rows - r0);
-    const unsigned buf = (seq + s) % kTS;
+    const unsigned buf = (seq + s) % kTSA;
     const unsigned bytes = (unsigned)(nr * pitch * sizeof(float));
     mbar_expect_tx(&bars[buf], bytes);
     bulk_g2s(rings + (size_t)buf * tr * pitch, region + (int64_t)r0 * pitch, bytes, &bars[buf]);
@@ -619,7 +620,7 @@ __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, in
   if (in_team) {
     if (tid == 0 && nst > 0) {
       fence_proxy_async();
-      for (int s = 0; s < nst && s < kTS; ++s) issue(s);
+      for (int s = 0; s < nst && s < kTSA; ++s) issue(s);
     }
 #ifdef SBT_ALS_PHASES
     const long long tp0 = clock64();
@@ -629,12 +630,12 @@ __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, in
     team_bar(1, TA);   // W of stage 0
     for (int s = 0; s < nst; ++s) {
       const int nr = min(tr, rows - s * tr);
-      const unsigned buf = (seq + s) % kTS;
+      const unsigned buf = (seq + s) % kTSA;
       if (s + 1 < nst) make_w(s + 1);   // its W buffer was last read in stage s - 1
 #ifdef SBT_ALS_PHASES
       const long long tw0 = clock64();
 #endif
-      mbar_wait(&bars[buf], ((seq + s) / kTS) & 1u);
+      mbar_wait(&bars[buf], ((seq + s) / kTSA) & 1u);
 #ifdef SBT_ALS_PHASES
       tw += clock64() - tw0;
 #endif
@@ -662,9 +663,9 @@ __device__ __forceinline__ void wide_pass_a(const float* __restrict__ region, in
 #ifdef SBT_ALS_PHASES
       tb += clock64() - tb0;
 #endif
-      if (tid == 0 && s + kTS < nst) {
+      if (tid == 0 && s + kTSA < nst) {
         fence_proxy_async();
-        issue(s + kTS);
+        issue(s + kTSA);
       }
     }
 #ifdef SBT_ALS_PHASES
