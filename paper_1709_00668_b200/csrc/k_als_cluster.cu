@@ -40,7 +40,7 @@ constexpr int kCT = 512;          // threads per CTA
 constexpr int kCW = kCT / 32;     // warps per CTA
 
 
-constexpr int kTS = 3;            // TMA stages per team
+constexpr int kTS = 2;            // TMA stages per team
 constexpr int kTSA = 2;           // TMA stages of the wide pass A (larger stages, fewer team barriers)
 
 struct ClLayout {
