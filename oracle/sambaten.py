@@ -386,6 +386,20 @@ def match_rep(A, B, C, Is, Js, Ks, lam_p, Up, tau, rnew=None):
     return RepMatch(pi, scale, lam_hat, score, bool(score[valid].min() >= tau), Phis, valid)
 
 
+def warm_init(U0, st, Is, Js, Ks):
+    """Warm start (reading R34): the summary ALS starts from the model's
+    rows instead of the random point -- U_0 = A(I_s, :), U_1 = B(J_s, :), the first |K_s| rows of
+    U_2 = C(K_s, :) diag(lambda) (product rounded to float32, as the model is held in float32);
+    the K_n new slices start at zero (the model has no rows for them; the first mode-0 and
+    mode-1 solves then see the old slices only, and the mode-2 solve fills them)."""
+    if st.cfg.getrank:
+        raise ValueError("warm_start and getrank are exclusive (R34)")
+    f32 = lambda x: np.asarray(x, np.float32).astype(np.float64)
+    U2 = np.zeros_like(U0[2])
+    U2[: len(Ks)] = (np.asarray(st.C, np.float32)[np.asarray(Ks)] * np.asarray(st.lam, np.float32)[None, :]).astype(np.float64)
+    return [f32(st.A[np.asarray(Is)]), f32(st.B[np.asarray(Js)]), U2]
+
+
 def rescaled(Up, rm, m):
     """Candidate factor of mode m in the old frame: U~(:, f) = scale_f * U'(:, pi f)."""
     return Up[m][:, rm.pi] * rm.scale[m][None, :]
@@ -408,6 +422,7 @@ class Config:
     getrank: bool = False    # GetRank before each summary decomposition (Alg. 2; R29-R33)
     getrank_trials: int = 1
     getrank_threshold: float = 90.0
+    warm_start: bool = False # summary ALS started from the model's rows
 
 
 @dataclass
@@ -506,6 +521,8 @@ def update(st, batch, keep_reps=False):
             R_use, _ = getrank(Y, cfg.R, cfg.getrank_trials, cfg.seed, cfg.maxit, cfg.tol,
                                cfg.getrank_threshold, rep_base=rho * cfg.getrank_trials)
         U0 = als_init((len(Is), len(Js), len(Kp)), R_use, cfg.seed, uid, rho)
+        if cfg.warm_start:
+            U0 = warm_init(U0, st, Is, Js, Ks)
         lam_p, Up, fit, its, _ = cp_als(Y, U0, cfg.maxit, cfg.tol)
         if R_use < cfg.R:   # zero columns up to R (reading R33)
             pad = cfg.R - R_use
