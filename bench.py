@@ -585,36 +585,14 @@ def main():
             line["cpu_baseline"] = {"value": v, "unit": unit, "cores": threads_used(), "kind": "oracle",
                                     "sample": f"{nbt} consecutive oracle updates of {w.name} from the K0 state, {dt:.1f} s"}
     if world == 1 and not sharded and not args.no_variant:
-        # the same workload with incremental marginals (bit-identical a1):
-        # a fresh handle, primed, W warm-up and K timed steps exactly as above
-        L.sambaten_destroy(h)
-        opts.incremental_marginals = 1
-        h = init_single(L, work, w, opts, config)
-        L.sambaten_checkpoint(h)
-        for i in range(nb):
-            with torch.cuda.stream(stream):
-                L.sambaten_update(h, dbatches[i])
-        L.sambaten_restore(h)
-        state["i"] = 0
-        for _ in range(args.warmup):
-            step()
-        vt, vi, ve = [], [], []
-        for _ in range(args.steps):
-            ms, info, ne, bi = step()
-            vt.append(ms)
-            vi.append(info.as_dict())
-            ve.append(ne)
-        line["variants"] = {"incremental_marginals": {
-            "value": sum(ve) / (sum(vt) / 1000.0), "unit": unit, "ms_per_step": statistics.mean(vt),
-            "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in vi) for k in range(8)},
-            "note": "opts.incremental_marginals=1: a1 adds the batch's contribution to the committed "
-                    "int64 marginals (bit-identical to the full pass; tests/test_gpu_incremental.py)"}}
-        if not work.coo and not device_gen:
-            # GetRank before every summary decomposition (opts.getrank, reading R33): Alg. 2 over
-            # candidate ranks 1..R on all r summaries, then ALS at the chosen ranks
+        # variants of the same workload: a fresh handle with one option changed,
+        # primed, W warm-up and K (GetRank: <= 5) timed steps exactly as above
+        def run_variant(nsteps, **changes):
+            nonlocal h
             L.sambaten_destroy(h)
-            opts.incremental_marginals = 0
-            opts.getrank = 1
+            saved = {k: getattr(opts, k) for k in changes}
+            for k, v in changes.items():
+                setattr(opts, k, v)
             h = init_single(L, work, w, opts, config)
             L.sambaten_checkpoint(h)
             for i in range(nb):
@@ -624,18 +602,31 @@ def main():
             state["i"] = 0
             for _ in range(args.warmup):
                 step()
-            gt, gi, ge = [], [], []
-            for _ in range(min(args.steps, 5)):
+            vt, vi, ve = [], [], []
+            for _ in range(nsteps):
                 ms, info, ne, bi = step()
-                gt.append(ms)
-                gi.append(info.as_dict())
-                ge.append(ne)
-            line["variants"]["getrank_in_update"] = {
-                "value": sum(ge) / (sum(gt) / 1000.0), "unit": unit, "ms_per_step": statistics.mean(gt),
-                "steps": len(gt), "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in gi) for k in range(8)},
-                "rep_rank_last": gi[-1]["rep_rank"][:w.r],
-                "note": "opts.getrank=1 (P:266, Alg. 2; R33): a4 includes GetRank over ranks 1..R on every summary"}
-            opts.getrank = 0
+                vt.append(ms)
+                vi.append(info.as_dict())
+                ve.append(ne)
+            for k, v in saved.items():
+                setattr(opts, k, v)
+            return {"value": sum(ve) / (sum(vt) / 1000.0), "unit": unit, "ms_per_step": statistics.mean(vt),
+                    "steps": len(vt),
+                    "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in vi) for k in range(8)},
+                    "als_iters_mean": statistics.mean(inf["als_iters_sum"] / w.r for inf in vi),
+                    "rep_rank_last": vi[-1]["rep_rank"][:w.r]}
+        line["variants"] = {"incremental_marginals": dict(
+            run_variant(args.steps, incremental_marginals=1),
+            note="opts.incremental_marginals=1: a1 adds the batch's contribution to the committed int64 "
+                 "marginals (bit-identical to the full pass; tests/test_gpu_incremental.py)")}
+        if not work.coo and not device_gen:
+            line["variants"]["warm_start"] = dict(
+                run_variant(args.steps, warm_start=1),
+                note="opts.warm_start=1 (SURVEY 8(f) NEXT #4, R34): summary ALS from the model's rows, "
+                     "the config's tolerance; tests/test_gpu_update.py::test_warm_start_*")
+            line["variants"]["getrank_in_update"] = dict(
+                run_variant(min(args.steps, 5), getrank=1),
+                note="opts.getrank=1 (P:266, Alg. 2; R33): a4 includes GetRank over ranks 1..R on every summary")
     L.sambaten_destroy(h)
     if rank == 0 and not work.coo and not args.no_getrank:
         line["getrank"] = getrank_timing(L, w, stream)

@@ -97,6 +97,10 @@ typedef struct {
                           /* SAMBATEN_E_INVALID at init).  Default 0.                         */
   int getrank_trials;     /* CP runs per candidate rank (Alg. 2 `it`); default 1              */
   double getrank_threshold; /* CorConDia cut-off of R31; default 90                           */
+  int warm_start;         /* 1: each summary ALS starts from the model's rows (A(I_s), B(J_s),  */
+                          /* C(K_s) diag(lambda), zero rows for the new slices   */
+                          /* NEXT #4, reading R34) instead of the Philox point.  Dense        */
+                          /* single-GPU handles, not with getrank (else SAMBATEN_E_INVALID).  */
 } sambaten_opts;
 
 typedef struct {

@@ -267,6 +267,10 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
     h->Kcap = h->opts.capacity_k > 0 ? h->opts.capacity_k : 2 * h->K + 1024;
     if (h->Kcap < h->K) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity_k < K0"); }
   }
+  if (h->opts.warm_start && (h->fmt != SAMBATEN_DENSE || h->opts.getrank)) {
+    delete h;
+    FAIL(SAMBATEN_E_INVALID, "init: warm_start needs a dense tensor and no getrank (R34)");
+  }
   if (h->opts.getrank) {
     if (h->fmt != SAMBATEN_DENSE) { delete h; FAIL(SAMBATEN_E_INVALID, "init: getrank needs a dense tensor (R33)"); }
     if (h->opts.getrank_trials < 1 || h->opts.getrank_trials > kMaxReps) {
@@ -1182,11 +1186,19 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     CK(rank_als(h, a, h->rep_rank, uid, st, &als_launches));
   } else if (use_cluster) {
     CK(launch_als_init_factors(a, h->seed, uid, 0, st));
+    if (h->opts.warm_start) {   // R34: the model's rows replace the Philox point
+      CK(launch_warm_init(a, h->A(h->cur), h->B(h->cur), h->C(h->cur), h->lam(h->cur), Is, Js, Kp, (int)nKs, st));
+      ++als_launches;
+    }
     CK(run_als_cluster(a, cpl, reinterpret_cast<float*>(h->als.as<char>() + ws_als), st));
     if (getenv("SAMBATEN_DEBUG")) als_phase_dump();
     als_launches += 2;
   } else {
     CK(launch_als_init(a, h->seed, uid, 0, true, st));
+    if (h->opts.warm_start) {
+      CK(launch_warm_init(a, h->A(h->cur), h->B(h->cur), h->C(h->cur), h->lam(h->cur), Is, Js, Kp, (int)nKs, st));
+      ++als_launches;
+    }
     CK(run_dense_als(a, st));
     als_launches += 4 + 7 * a.maxit;
   }

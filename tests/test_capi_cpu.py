@@ -29,6 +29,10 @@ def test_version_and_default_opts():
     o = _lib.default_opts()
     assert o.als_max_iters == 30 and o.accept_tau == 0.9 and o.init_max_iters == 1000
     assert o.moi == 0 and o.merge_policy == 0
+    # the fields appended last are filled by the C side: a ctypes layout that drifted from the
+    # header would read them at the wrong offsets
+    assert o.getrank == 0 and o.getrank_trials == 1 and o.getrank_threshold == 90.0
+    assert o.warm_start == 0 and o.incremental_marginals == 0 and o.borrow_store == 0
 
 
 def test_fixed_point_scale_matches_oracle():

@@ -215,3 +215,54 @@ def test_variant_flags_parity(s_mode, policy, moi):
             st.lam, st.A, st.B, st.C = (np.asarray(x, np.float64) for x in gm)
     finally:
         L().sambaten_destroy(h)
+
+
+@pytest.mark.parametrize("shape", [(60, 52, 40, 4, 30, 5, 4), (100, 100, 60, 10, 45, 5, 8)])
+def test_warm_start_parity(shape):
+    """Warm-started summary ALS (opts.warm_start, reading R34) against the
+    oracle with the same flag: the small shape runs the multi-kernel ALS, the C2-like one the
+    cluster kernel.  Same bars as the whole update."""
+    I, J, K, R, K0, batch, r = shape
+    T, truth = planted_dense(I, J, K, R, noise=0.01, seed=7)
+    T0, batches = split_dense(T, K0, batch)
+    model = [np.asarray(x, np.float32) for x in (truth[0], truth[1], truth[2], truth[3][:K0])]
+    cfg = O.Config(R=R, s=(2, 2, 2), r=r, seed=17, maxit=15, tol=0.0, tau=0.9, warm_start=True)
+    st = O.init_factors(T0, cfg, *model, I * J * K)
+    lam, A, B, C = model
+    opts = L().default_opts(als_max_iters=15, als_tol=0.0, accept_tau=0.9, capacity=K, full_fit=1, warm_start=1)
+    h = L().sambaten_init_factors(L().dense(dev(T0)), R, 2, r, 17, A, B, C, lam, opts)
+    try:
+        Kt = K0
+        for b in batches[:2]:
+            Kt += b.shape[0]
+            gm, info, oinfo = _update_both(h, st, b, Kt)
+            fms, rel_g, rel_o, gpu_rej = _check(h, st, gm, info, oinfo)
+            assert gpu_rej == oinfo["rejected"]
+            assert fms >= 0.99, fms
+            assert abs(rel_g - rel_o) <= 1e-3, (rel_g, rel_o)
+            assert abs(info.fit_summary - oinfo["fit_summary"]) <= 1e-4, (info.fit_summary, oinfo["fit_summary"])
+            st.lam, st.A, st.B, st.C = (np.asarray(x, np.float64) for x in gm)
+    finally:
+        L().sambaten_destroy(h)
+
+
+def test_warm_start_fixed_point():
+    """The oracle pin on the GPU (tests/test_oracle_warm.py): a noiseless model with zero new
+    slices is a fixed point of the warm-started sweep -> summary fits 1 to fp32 rounding after
+    one iteration; the invalid flag combinations are refused."""
+    rng = np.random.default_rng(2)
+    I, J, K0, Kn, R = 64, 48, 40, 4, 3
+    A, B, C = rng.random((I, R)), rng.random((J, R)), rng.random((K0, R))
+    lam = rng.random(R) + 0.5
+    A, B, C, lam = (np.asarray(x, np.float32) for x in (A, B, C, lam))
+    X0 = np.einsum("if,jf,kf,f->kji", *(x.astype(np.float64) for x in (A, B, C, lam))).astype(np.float32)
+    opts = L().default_opts(als_max_iters=1, als_tol=0.0, accept_tau=0.0, capacity=K0 + Kn, warm_start=1)
+    h = L().sambaten_init_factors(L().dense(dev(X0)), R, 2, 4, 3, A, B, C, lam, opts)
+    try:
+        info = L().sambaten_update(h, L().dense(dev(np.zeros((Kn, J, I), np.float32))))
+        assert info.fit_summary > 1.0 - 1e-5, info.fit_summary
+    finally:
+        L().sambaten_destroy(h)
+    with pytest.raises(L().SambatenError):
+        L().sambaten_init_factors(L().dense(dev(X0)), R, 2, 4, 3, A, B, C, lam,
+                                  L().default_opts(warm_start=1, getrank=1))
