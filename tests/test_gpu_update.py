@@ -260,7 +260,17 @@ def test_warm_start_fixed_point():
     h = L().sambaten_init_factors(L().dense(dev(X0)), R, 2, 4, 3, A, B, C, lam, opts)
     try:
         info = L().sambaten_update(h, L().dense(dev(np.zeros((Kn, J, I), np.float32))))
-        assert info.fit_summary > 1.0 - 1e-5, info.fit_summary
+        # the summary fit is formed as ||Y||^2 - 2 <Y, M> + ||M||^2 from fp32 MTTKRP runs: at a
+        # residual near 0 its square root exposes ~sqrt(1e-7) of rounding, hence 1e-3 (a cold
+        # start after one sweep is below 0.99 here)
+        assert info.fit_summary > 1.0 - 1e-3, info.fit_summary
+    finally:
+        L().sambaten_destroy(h)
+    opts.warm_start = 0
+    h = L().sambaten_init_factors(L().dense(dev(X0)), R, 2, 4, 3, A, B, C, lam, opts)
+    try:
+        info = L().sambaten_update(h, L().dense(dev(np.zeros((Kn, J, I), np.float32))))
+        assert info.fit_summary < 0.99, info.fit_summary
     finally:
         L().sambaten_destroy(h)
     with pytest.raises(L().SambatenError):
