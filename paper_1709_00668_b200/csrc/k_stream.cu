@@ -571,7 +571,7 @@ StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* g
   if (g.wpc < 1) g.wpc = 1;
   const int unit = kRPW * g.wpc;
   const int row_b = g.pitch * (int)sizeof(float);
-  int m = (64 * 1024) / (unit * row_b);
+  int m = (96 * 1024) / (unit * row_b);   // ~96 KB stages: two in the ring (fewer barriers)
   if (m < 1) m = 1;
   g.tr = unit * m;
   g.ns = kRingBytes / (g.tr * row_b);
@@ -604,7 +604,7 @@ StreamGeom fit_geom(const DenseView& X, int RB, int* gx, int* gy, int* threads) 
   const int row_b = g.pitch * (int)sizeof(float);
   const size_t bres_b = sizeof(float) * (size_t)X.J * RB;
   g.bres = bres_b <= 48 * 1024;
-  g.tr = (48 * 1024) / row_b;
+  g.tr = (96 * 1024) / row_b;   // ~96 KB stages: two in the ring (one barrier per stage)
   if (g.tr < 1) g.tr = 1;
   if (!g.bres && g.tr * RB > kWPT * nthr) g.tr = kWPT * nthr / RB;   // the B prefetch registers
   if (g.tr > 256) g.tr = 256;
