@@ -48,15 +48,32 @@ __global__ void __launch_bounds__(kSampleThreads) sample_kernel(const SampleSeg*
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      long long k = sh_k, cum = 0;
-      int d = 0;
-      for (; d < 256; ++d) {
-        if (cum + (long long)hist[d] >= k) break;
-        cum += hist[d];
+    if (threadIdx.x < 32) {
+      // the first digit d with (keys below d) + hist[d] >= k, as a warp: lane l holds digits
+      // 8l .. 8l+7; an inclusive scan of the lane sums finds the lane, the lane finds d
+      const int lane = threadIdx.x;
+      const long long k = sh_k;
+      long long loc[8], s = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { loc[t] = hist[lane * 8 + t]; s += loc[t]; }
+      long long incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
       }
-      sh_k = k - cum;
-      sh_prefix = prefix | ((unsigned long long)d << shift);
+      const unsigned ball = __ballot_sync(0xffffffffu, incl >= k);
+      if (ball && lane == __ffs(ball) - 1) {
+        long long cum = incl - s;
+        int d = lane * 8 + 7;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (cum + loc[t] >= k) { d = lane * 8 + t; break; }
+          cum += loc[t];
+        }
+        sh_k = k - cum;
+        sh_prefix = prefix | ((unsigned long long)d << shift);
+      }
     }
     mask |= 0xFFull << shift;
     __syncthreads();
