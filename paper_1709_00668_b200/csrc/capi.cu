@@ -1216,8 +1216,10 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     CK(fit_any(V, h->lam(nb), h->A(nb), h->B(nb), h->C(nb), R, h->fitws.as<double>(), d_relerr, st));
   }
   CK(cudaEventRecord(h->ev[8], st));
-  // copy-in, max_phi, marginals, sample, gather, ALS, match, 3 + 1 merge, 3 fit
-  const int launches = 1 + 1 + 1 + 1 + als_launches + 1 + 4 + (h->opts.full_fit ? 3 : 0);
+  // a0 ingest or max_phi (+ the old-slice marginal pass when a host batch overlaps its copy),
+  // a1 marginals, a2 sample, a3 gather, a4 ALS, a5 match partial + match, a6 merge, a7 fit +
+  // two Gram kernels + combine
+  const int launches = 1 + (overlap ? 1 : 0) + 1 + 1 + 1 + als_launches + 2 + 1 + (h->opts.full_fit ? 4 : 0);
   return finish_update(h, a, accepted, d_maxphi, nullptr, d_relerr, Ko, Kn, nI, nJ, nKs, nKp, b, nb,
                        launches, 0, Aout, Bout, Cout, lamout, info);
 }

@@ -245,24 +245,34 @@ __global__ void __launch_bounds__(kMatchThreads) match_kernel(MatchArgs m, int n
     if (threadIdx.x < 32) hungarian_max_warp(S, R, pi_s, hu, hv, hp, hway);
   }
   __syncthreads();
+  // one thread per old component f (the per-f arithmetic of the former sequential loop);
+  // the acceptance minimum and the NaN flag are order-free reductions
+  __shared__ double s_sc[kMaxR];
+  __shared__ int s_valid[kMaxR];
+  if (threadIdx.x < R) {
+    const int f = threadIdx.x;
+    const int g = pi_s[f];
+    m.pi[rep * R + f] = g;
+    double lh = m.lamp[rep * R + g];
+    bool ok_all = true;
+    for (int mode = 0; mode < 3; ++mode) {
+      const double sig = Phi[mode][f * R + g] < 0.0 ? -1.0 : 1.0;
+      const double a0 = al[mode][f], a1 = an[mode][g];
+      const bool ok = a0 > 0.0 && a1 > 0.0;
+      m.scale[((int64_t)rep * 3 + mode) * R + f] = ok ? sig * a0 / a1 : 0.0;
+      if (ok) lh = lh * sig * a1 / a0; else ok_all = false;
+    }
+    m.lam_hat[rep * R + f] = ok_all ? lh : 0.0;
+    s_sc[f] = S[f * R + g];
+    s_valid[f] = !(m.rnew && g >= m.rnew[rep]);   // not matched to a zero padding column (R33)
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     double smin = 1e300;
     bool nan = false;
     for (int f = 0; f < R; ++f) {
-      const int g = pi_s[f];
-      m.pi[rep * R + f] = g;
-      double lh = m.lamp[rep * R + g];
-      bool ok_all = true;
-      for (int mode = 0; mode < 3; ++mode) {
-        const double sig = Phi[mode][f * R + g] < 0.0 ? -1.0 : 1.0;
-        const double a0 = al[mode][f], a1 = an[mode][g];
-        const bool ok = a0 > 0.0 && a1 > 0.0;
-        m.scale[((int64_t)rep * 3 + mode) * R + f] = ok ? sig * a0 / a1 : 0.0;
-        if (ok) lh = lh * sig * a1 / a0; else ok_all = false;
-      }
-      m.lam_hat[rep * R + f] = ok_all ? lh : 0.0;
-      if (m.rnew && g >= m.rnew[rep]) continue;   // matched to a zero padding column (R33)
-      const double sc = S[f * R + g];
+      if (!s_valid[f]) continue;
+      const double sc = s_sc[f];
       if (sc != sc) nan = true;
       smin = fmin(smin, sc);
     }
@@ -290,10 +300,9 @@ cudaError_t launch_match(const MatchArgs& m, cudaStream_t st) {
 // ---------------------------------------------------------------------------------------
 // merge
 // ---------------------------------------------------------------------------------------
-__global__ void merge_rows_kernel(MergeArgs g, int mode) {
+__device__ __forceinline__ void merge_rows(const MergeArgs& g, int mode, int64_t idx) {
   const int64_t n = mode == 0 ? g.I : mode == 1 ? g.J : g.Ko;
   const int R = g.R;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * R) return;
   const int64_t row = idx / R;
   const int f = (int)(idx - row * R);
@@ -317,11 +326,10 @@ __global__ void merge_rows_kernel(MergeArgs g, int mode) {
   }
 }
 
-__global__ void merge_new_kernel(MergeArgs g) {
+__device__ __forceinline__ void merge_new(const MergeArgs& g, int64_t idx) {
   // per component f: mean over the accepted reps that carry it (all accepted reps unless
   // GetRank reduced a rep's rank, R33); no such rep -> C_new(:, f) = 0, lambda_f unchanged
   const int R = g.R;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int f = idx < g.Kn * R ? (int)(idx % R) : (int)(idx - g.Kn * R);
   if (idx >= g.Kn * R + R) return;
   auto carries = [&](int rep) {
@@ -346,13 +354,30 @@ __global__ void merge_new_kernel(MergeArgs g) {
   }
 }
 
+// one launch: blocks [0, b[0]) merge A's rows, [b[0], b[1]) B's, [b[1], b[2]) C's old rows,
+// [b[2], b[3]) the new rows of C and lambda
+struct MergeBlocks { unsigned b[4]; };
+__global__ void merge_kernel(MergeArgs g, MergeBlocks mb) {
+  const unsigned blk = blockIdx.x;
+  int part = 0;
+  while (part < 3 && blk >= mb.b[part]) ++part;
+  const unsigned b0 = part == 0 ? 0u : mb.b[part - 1];
+  const int64_t idx = (int64_t)(blk - b0) * blockDim.x + threadIdx.x;
+  if (part < 3) merge_rows(g, part, idx);
+  else merge_new(g, idx);
+}
+
 cudaError_t launch_merge(const MergeArgs& g, cudaStream_t st) {
+  MergeBlocks mb{};
+  unsigned acc = 0;
   for (int mode = 0; mode < 3; ++mode) {
     const int64_t n = mode == 0 ? g.I : mode == 1 ? g.J : g.Ko;
-    const int64_t tot = n * g.R;
-    if (tot > 0) merge_rows_kernel<<<(unsigned)ceil_div(tot, 256), 256, 0, st>>>(g, mode);
+    acc += (unsigned)ceil_div(n * g.R, 256);
+    mb.b[mode] = acc;
   }
-  merge_new_kernel<<<(unsigned)ceil_div(g.Kn * g.R + g.R, 256), 256, 0, st>>>(g);
+  acc += (unsigned)ceil_div(g.Kn * g.R + g.R, 256);
+  mb.b[3] = acc;
+  merge_kernel<<<acc, 256, 0, st>>>(g, mb);
   return cudaGetLastError();
 }
 
