@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(kGatherThreads) gather_dense_kernel(
     int64_t sI, int64_t sJ, int64_t sK, float* __restrict__ Y, float* __restrict__ Yt,
     int64_t y_stride, int pI, int pJ) {
   extern __shared__ int32_t is_sh[];
-  __shared__ float tile[32][33];
+  __shared__ float tile[2][32][33];
   const int qt = blockIdx.x, u = blockIdx.y, rep = blockIdx.z;
   const int32_t* is = Is + rep * sI;
   for (int p = threadIdx.x; p < nI; p += blockDim.x) is_sh[p] = is[p];
@@ -37,25 +37,36 @@ __global__ void __launch_bounds__(kGatherThreads) gather_dense_kernel(
     const int ql = warp * 4 + k;
     srow[k] = ql < nq ? X + (ku * J + js[q0 + ql]) * pitch : nullptr;
   }
-  for (int p0 = 0; p0 < pI; p0 += 32) {
-    const int p = p0 + lane;
-    float v[4];
+  // two 32-column tiles per step: 8 independent gathers in flight per thread, one barrier pair
+  for (int p0 = 0; p0 < pI; p0 += 64) {
+    float v[2][4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = (srow[k] && p < nI) ? __ldg(srow[k] + is_sh[p]) : 0.f;
+    for (int h = 0; h < 2; ++h) {
+      const int p = p0 + 32 * h + lane;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int ql = warp * 4 + k;
-      if (srow[k] && p < pI) Ys[(int64_t)(q0 + ql) * pI + p] = v[k];   // zero pad p >= nI
-      tile[ql][lane] = v[k];
+      for (int k = 0; k < 4; ++k) v[h][k] = (srow[k] && p < nI) ? __ldg(srow[k] + is_sh[p]) : 0.f;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int p = p0 + 32 * h + lane;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int ql = warp * 4 + k;
+        if (srow[k] && p < pI) Ys[(int64_t)(q0 + ql) * pI + p] = v[h][k];   // zero pad p >= nI
+        tile[h][ql][lane] = v[h][k];
+      }
     }
     if (Yts) {
       __syncthreads();
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int pl = warp * 4 + k;   // p offset within the tile
-        if (p0 + pl < nI && q0 + lane < pJ)
-          Yts[(int64_t)(p0 + pl) * pJ + q0 + lane] = lane < nq ? tile[lane][pl] : 0.f;
-      }
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int pl = warp * 4 + k;   // p offset within the tile
+          const int pp = p0 + 32 * h + pl;
+          if (pp < nI && q0 + lane < pJ)
+            Yts[(int64_t)pp * pJ + q0 + lane] = lane < nq ? tile[h][lane][pl] : 0.f;
+        }
       __syncthreads();
     }
   }
