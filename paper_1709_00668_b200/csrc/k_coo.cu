@@ -558,14 +558,24 @@ __global__ void coo_fit_kernel(const int32_t* __restrict__ ii, const int32_t* __
   if (threadIdx.x == 0) { part[2 * blockIdx.x] = inner; part[2 * blockIdx.x + 1] = sq; }
 }
 
-__global__ void coo_fit_combine_kernel(const double* part, int nb, const double* G, const float* lam,
-                                       int R, double* relerr) {
+// partials and Grams staged in shared memory by the block (coalesced), summed by thread 0 in
+// the fixed sequential order
+constexpr int kCooCombT = 256;
+__global__ void __launch_bounds__(kCooCombT) coo_fit_combine_kernel(const double* part, int nb, const double* G,
+                                                                   const float* lam, int R, double* relerr) {
+  __shared__ double sp[2 * kNumSMs * 4];
+  __shared__ double sg[3 * kMaxR * kMaxR];
+  __shared__ double sl[kMaxR];
+  for (int e = threadIdx.x; e < 2 * nb; e += blockDim.x) sp[e] = part[e];
+  for (int e = threadIdx.x; e < 3 * R * R; e += blockDim.x) sg[e] = G[e];
+  for (int e = threadIdx.x; e < R; e += blockDim.x) sl[e] = (double)lam[e];
+  __syncthreads();
   if (threadIdx.x != 0) return;
   double inner = 0.0, sq = 0.0, mn = 0.0;
-  for (int b = 0; b < nb; ++b) { inner += part[2 * b]; sq += part[2 * b + 1]; }
+  for (int b = 0; b < nb; ++b) { inner += sp[2 * b]; sq += sp[2 * b + 1]; }
   for (int f = 0; f < R; ++f)
     for (int g = 0; g < R; ++g)
-      mn += (double)lam[f] * (double)lam[g] * G[f * R + g] * G[R * R + f * R + g] * G[2 * R * R + f * R + g];
+      mn += sl[f] * sl[g] * sg[f * R + g] * sg[R * R + f * R + g] * sg[2 * R * R + f * R + g];
   const double res = fmax(0.0, sq - 2.0 * inner + mn);
   *relerr = sq > 0.0 ? sqrt(res / sq) : 0.0;
 }
@@ -786,7 +796,7 @@ cudaError_t launch_coo_fit(const CooView& X, const float* lam, const float* A, c
   if (e != cudaSuccess) return e;
   e = launch_gram3(A, B, C, X.I, X.J, X.K, R, G, G + 3 * kMaxR * kMaxR, st);
   if (e != cudaSuccess) return e;
-  coo_fit_combine_kernel<<<1, 32, 0, st>>>(ws, nb, G, lam, R, relerr);
+  coo_fit_combine_kernel<<<1, kCooCombT, 0, st>>>(ws, nb, G, lam, R, relerr);
   return cudaGetLastError();
 }
 
