@@ -187,7 +187,8 @@ SAMBATEN_API void sambaten_destroy(sambaten_t h);
  * "Multi-GPU").  Every rank holds the frontal slices it ingested (its slab of X0 and its
  * share of every batch); marginals are combined by one int64 allreduce, repetition rho is
  * decomposed on rank rho mod G from summary slices exchanged by one all-to-all-v, and the
- * per-repetition results are allgathered before the (replicated) merge.  Dense stores only.
+ * per-repetition results are allgathered before the (replicated) merge.  Dense and COO
+ * stores (the COO handle keeps the canonical entries of its slices; R32).
  * ------------------------------------------------------------------------------------- */
 typedef struct {
   int rank, world;              /* this process and the number of ranks                     */

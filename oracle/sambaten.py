@@ -250,16 +250,27 @@ def als_init(rows, R, seed, update_id, rep):
 
 def solve_normal(M, V):
     """U = M V^{-1} by Cholesky; if V is not positive definite, the pseudo-inverse from the
-    symmetric eigendecomposition with cutoff R*eps*lambda_max (reading R12)."""
+    symmetric eigendecomposition with cutoff R*eps*lambda_max (reading R12); exactly
+    zero rows / columns of V map to exactly zero rows / columns of V^+ (the exact pseudo-inverse
+    of a matrix with a decoupled zero block)."""
     try:
         L = np.linalg.cholesky(V)
         Z = np.linalg.solve(L, M.T)
         return np.linalg.solve(L.T, Z).T, False
     except np.linalg.LinAlgError:
-        w, Q = np.linalg.eigh(V)
-        cut = V.shape[0] * np.finfo(np.float64).eps * max(w.max(), 0.0)
-        winv = np.where(w > cut, 1.0 / np.where(w > cut, w, 1.0), 0.0)
-        return M @ (Q * winv) @ Q.T, True
+        # rows / columns of V that are exactly zero (a factor column that is exactly zero) are
+        # decoupled: V^+ is zero there and the eigendecomposition is taken of the rest, so the
+        # zero column stays exactly zero (no rounding-level mixing of eigenvectors into it)
+        R = V.shape[0]
+        live = np.flatnonzero(np.any(V != 0.0, axis=1))
+        P = np.zeros((R, R))
+        if live.size:
+            Vl = V[np.ix_(live, live)]
+            w, Q = np.linalg.eigh(Vl)
+            cut = R * np.finfo(np.float64).eps * max(w.max(), 0.0)
+            winv = np.where(w > cut, 1.0 / np.where(w > cut, w, 1.0), 0.0)
+            P[np.ix_(live, live)] = (Q * winv) @ Q.T
+        return M @ P, True
 
 
 def tensor_sqnorm(Y):
@@ -267,7 +278,7 @@ def tensor_sqnorm(Y):
     return float(np.sum(v * v))
 
 
-def cp_als(Y, U, maxit, tol):
+def cp_als(Y, U, maxit, tol, stats=None):
     """Alternating least squares for CP, starting from factors U (list of 3).
 
     Each iteration, for m = 0, 1, 2:  M = mttkrp(Y, U, m);  V = *_{n != m} U_n^T U_n;
@@ -275,7 +286,8 @@ def cp_als(Y, U, maxit, tol):
     fit = 1 - sqrt(max(0, ||Y||^2 - 2 sum_f lambda_f sum_k U_2(k,f) M_2(k,f)
                           + lambda^T (*_n U_n^T U_n) lambda)) / ||Y||.
     Stops when it >= 2 and |fit - fit_prev| < tol, or after maxit iterations (reading R11).
-    Returns (lambda, U, fit, iterations, fits)."""
+    Returns (lambda, U, fit, iterations, fits); ``stats["pinv"]`` (if a dict is passed) records
+    whether any solve fell back to the pseudo-inverse (reading R12)."""
     U = [np.array(u, np.float64) for u in U]
     R = U[0].shape[1]
     normY2 = tensor_sqnorm(Y)
@@ -291,7 +303,9 @@ def cp_als(Y, U, maxit, tol):
             for n in range(3):
                 if n != m:
                     V *= U[n].T @ U[n]
-            Um, _ = solve_normal(M, V)
+            Um, used_pinv = solve_normal(M, V)
+            if stats is not None and used_pinv:
+                stats["pinv"] = True
             lam = np.sqrt(np.sum(Um * Um, axis=0))
             Um = Um / np.where(lam > 0, lam, 1.0)
             U[m] = Um
@@ -523,7 +537,8 @@ def update(st, batch, keep_reps=False):
         U0 = als_init((len(Is), len(Js), len(Kp)), R_use, cfg.seed, uid, rho)
         if cfg.warm_start:
             U0 = warm_init(U0, st, Is, Js, Ks)
-        lam_p, Up, fit, its, _ = cp_als(Y, U0, cfg.maxit, cfg.tol)
+        als_stats = {"pinv": False}
+        lam_p, Up, fit, its, _ = cp_als(Y, U0, cfg.maxit, cfg.tol, als_stats)
         if R_use < cfg.R:   # zero columns up to R (reading R33)
             pad = cfg.R - R_use
             lam_p = np.concatenate([lam_p, np.zeros(pad)])
@@ -531,7 +546,7 @@ def update(st, batch, keep_reps=False):
         # a5: match against the batch-start snapshot
         rm = match_rep(st.A, st.B, st.C, Is, Js, Ks, lam_p, Up, cfg.tau, rnew=R_use)
         reps.append(dict(Is=Is, Js=Js, Ks=Ks, Kp=Kp, Y=Y if keep_reps else None, lam_p=lam_p,
-                         Up=Up, fit=fit, iters=its, match=rm, rank=R_use))
+                         Up=Up, fit=fit, iters=its, match=rm, rank=R_use, pinv=als_stats["pinv"]))
     acc = [rp for rp in reps if rp["match"].accepted]
     if not acc:
         raise BatchRejected("every repetition failed the acceptance test")

@@ -1194,10 +1194,16 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     if (getenv("SAMBATEN_DEBUG")) als_phase_dump();
     als_launches += 2;
   } else {
-    CK(launch_als_init(a, h->seed, uid, 0, true, st));
     if (h->opts.warm_start) {
+      // R34: the model's rows replace the Philox point BEFORE the Grams are formed (the first
+      // sweep's normal equations must see the warm factors)
+      CK(launch_als_init_factors(a, h->seed, uid, 0, st));
       CK(launch_warm_init(a, h->A(h->cur), h->B(h->cur), h->C(h->cur), h->lam(h->cur), Is, Js, Kp, (int)nKs, st));
+      CK(launch_als_gram(a, st));
+      CK(launch_sumsq_dense(a.Y, a.y_stride, (int64_t)a.nK * a.nJ, a.pitch, a.nI, a.r, a.ysq, st));
       ++als_launches;
+    } else {
+      CK(launch_als_init(a, h->seed, uid, 0, true, st));
     }
     CK(run_dense_als(a, st));
     als_launches += 4 + 7 * a.maxit;

@@ -53,7 +53,7 @@ __device__ void hungarian_max_warp(const double* S, int R, int* pi, double* u, d
   const int lane = threadIdx.x & 31;
   const int j = lane + 1;                   // this lane's column (valid if j <= R)
   const bool col = j <= R;
-  if (lane <= R) { u[lane] = 0.0; v[lane] = 0.0; p[lane] = 0; way[lane] = 0; }
+  for (int t = lane; t <= R; t += 32) { u[t] = 0.0; v[t] = 0.0; p[t] = 0; way[t] = 0; }   // R + 1 entries (33 at R = 32)
   __syncwarp();
   for (int i = 1; i <= R; ++i) {
     if (lane == 0) p[0] = i;

@@ -557,7 +557,7 @@ constexpr int kRingBytes = 192 * 1024;
 
 // Marginal pass: stages of whole rows (one bulk copy each, contiguous in the store); a row is
 // split into nch chunks of <= 512 floats, each worked by wpc warps (nch * wpc <= 16); rows per
-// stage a multiple of kRPW * wpc, stages of ~48-64 KB in a 192 KB ring.
+// stage a multiple of kRPW * wpc, two ~96 KB stages in a 192 KB ring.
 StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* gy, int* threads) {
   StreamGeom g{};
   g.row0 = k0 * X.J;

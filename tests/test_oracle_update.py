@@ -133,3 +133,137 @@ def test_coo_update_runs_and_matches_dense_of_same_tensor():
         assert np.array_equal(ra["Is"], rb["Is"]) and np.array_equal(ra["Kp"], rb["Kp"])
     assert np.allclose(sd.C, sc.C, rtol=1e-9, atol=1e-12)
     assert np.allclose(sd.lam, sc.lam, rtol=1e-9)
+
+
+def _noiseless_from_truth(seed, R=3, I=30, K0=24, Kn=6, r=4, s=2):
+    T, truth = planted_dense(I, I, K0 + Kn, R, noise=0.0, seed=seed)
+    T0, batches = split_dense(T, K0, Kn)
+    cfg = O.Config(R=R, s=(s, s, s), r=r, seed=seed, maxit=1000, tol=1e-13, tau=0.9)
+    st = _state_from_truth(T0, truth, cfg, T.size)
+    f32 = lambda x: np.asarray(x, np.float32).astype(np.float64)
+    return st, batches, (np.ones(R), f32(truth[1]), f32(truth[2]), f32(truth[3]))
+
+
+def test_zeroed_rows_restored_to_truth():
+    """P:216 / P:256 ("update only zero entries"), P:198 with reading R14 (rows not yet
+    computed are no anchors), R16 (old-frame rescale), R17 (mean over the reps that sampled
+    the row).  Noiseless planted tensor, model = truth with some rows of A and B zeroed, ALS
+    converged: every zeroed row that some accepted rep sampled comes back as the TRUE row (the
+    anchor norms exclude the zeroed rows; a sum instead of a mean, or zero rows kept as anchors,
+    scale it), every zeroed row no rep sampled stays exactly zero, every other cell is
+    bit-unchanged."""
+    st, batches, (lam_t, A_t, B_t, C_t) = _noiseless_from_truth(seed=11)
+    zA, zB = [1, 4, 7, 12, 20, 27], [0, 5, 9, 18, 29]
+    st.A[zA] = 0.0
+    st.B[zB] = 0.0
+    A0, B0 = st.A.copy(), st.B.copy()
+    info = O.update(st, batches[0])
+    assert info["rejected"] == []
+    hitA = set(np.concatenate([rp["Is"] for rp in info["reps"]]).tolist())
+    hitB = set(np.concatenate([rp["Js"] for rp in info["reps"]]).tolist())
+    restored = 0
+    for F, F0, T, zs, hit in ((st.A, A0, A_t, zA, hitA), (st.B, B0, B_t, zB, hitB)):
+        for i in zs:
+            if i in hit:
+                assert np.linalg.norm(F[i] - T[i]) <= 1e-6 * np.linalg.norm(T[i]), (i, F[i], T[i])
+                restored += 1
+            else:
+                assert np.all(F[i] == 0.0)
+        keep = np.ones(F.shape[0], bool); keep[zs] = False
+        assert np.array_equal(F[keep], F0[keep])
+    assert restored >= 6          # the pin exercises the fill on several rows of both modes
+
+
+def test_zeroed_row_sampled_by_one_rep_only():
+    """The fill value of a row hit by exactly one accepted rep is that rep's old-frame row
+    (R17: the mean over one rep), and a row hit by several reps is their mean: with a noisy
+    tensor the reps' rows differ, so the two cases separate a mean from a sum or a first-rep
+    pick.  Pinned by construction: the expected rows are re-derived here from the reps'
+    candidate factors by the old-frame rescale of Lemma 1's equality case (alpha/a over the
+    anchors) computed independently with numpy on the anchor rows."""
+    T, truth = planted_dense(30, 30, 30, 3, noise=0.01, seed=12)
+    T0, batches = split_dense(T, 24, 6)
+    cfg = O.Config(R=3, s=(3, 3, 3), r=3, seed=5, maxit=200, tol=1e-10, tau=0.0)
+    st = _state_from_truth(T0, truth, cfg, T.size)
+    zA = list(range(0, 30, 3))
+    st.A[zA] = 0.0
+    A0 = st.A.copy()
+    info = O.update(st, batches[0])
+    counts = {i: [k for k, rp in enumerate(info["reps"]) if i in set(rp["Is"].tolist())] for i in zA}
+    assert any(len(v) == 1 for v in counts.values()) and any(len(v) >= 2 for v in counts.values())
+    for i, reps in counts.items():
+        if not reps:
+            assert np.all(st.A[i] == 0.0)
+            continue
+        rows = []
+        for k in reps:
+            rp = info["reps"][k]
+            Is = rp["Is"]
+            anc = np.any(A0[Is] != 0.0, axis=1)
+            old, cand = A0[Is][anc], rp["Up"][0][anc]
+            pi = rp["match"].pi
+            row = np.empty(3)
+            for f in range(3):
+                g = pi[f]
+                dot = float(old[:, f] @ cand[:, g])
+                row[f] = np.sign(dot or 1.0) * np.linalg.norm(old[:, f]) / np.linalg.norm(cand[:, g]) \
+                    * rp["Up"][0][list(Is).index(i), g]
+            rows.append(row)
+        assert np.allclose(st.A[i], np.mean(rows, axis=0), rtol=1e-12, atol=1e-14)
+
+
+def test_lambda_average_of_old_and_new():
+    """P:227 "lambda = (lambda + new value)/2" with R19 (new value = mean of lambda_hat over the
+    accepted reps) and R16 (lambda_hat in the old frame).  Model = truth with lambda doubled on a
+    noiseless tensor: every converged rep recovers lambda_hat = 1 (the true scale relative to
+    the model's factor norms), so the update must give lambda = (2 + 1)/2 = 1.5 -- lambda <-
+    mean lambda_hat gives 1, leaving lambda unchanged gives 2."""
+    st, batches, _ = _noiseless_from_truth(seed=13)
+    st.lam = 2.0 * st.lam
+    info = O.update(st, batches[0])
+    assert info["rejected"] == []
+    for rp in info["reps"]:
+        assert np.allclose(rp["match"].lam_hat, 1.0, rtol=1e-5)
+    assert np.allclose(st.lam, 1.5, rtol=1e-5)
+
+
+def test_pinv_zero_column_equals_reduced_rank_als():
+    """R12 pseudo-inverse fallback: a start with factor column f of U_1 exactly zero makes every
+    normal matrix singular (zero row / column f), so every solve takes the pseudo-inverse
+    (cutoff R*eps*lambda_max).  Mathematically the pinv solve then equals the Cholesky solve of
+    the R-1 other columns and keeps column f at zero: cp_als with the zero column must equal
+    cp_als at rank R-1 from the same start without column f (a different code path: every
+    normal matrix there is positive definite)."""
+    T, truth = planted_dense(12, 11, 10, 3, noise=0.01, seed=14)
+    Y = O.view_ijk(T).astype(np.float64)
+    U0 = O.als_init(Y.shape, 3, 0, 1, 0)
+    U0[1][:, 1] = 0.0
+    st = {"pinv": False}
+    lam, U, fit, it, _ = O.cp_als(Y, U0, 40, 0.0, st)
+    assert st["pinv"]
+    red = [np.delete(u, 1, axis=1) for u in U0]
+    st2 = {"pinv": False}
+    lam2, U2, fit2, it2, _ = O.cp_als(Y, red, 40, 0.0, st2)
+    assert not st2["pinv"]
+    assert lam[1] == 0.0 and all(np.all(u[:, 1] == 0.0) for u in U)
+    assert np.allclose(np.delete(lam, 1), lam2, rtol=1e-8)
+    for u, u2 in zip(U, U2):
+        assert np.allclose(np.delete(u, 1, axis=1), u2, rtol=1e-7, atol=1e-10)
+    assert abs(fit - fit2) <= 1e-10
+
+
+def test_update_pinv_path_zero_model_column():
+    """A model component whose B column is all zero (a warm start from it, R34) drives every
+    summary ALS through the pseudo-inverse (R12); the paper-literal merge (tau = 0) then merges
+    a zero candidate column: lambda_hat_f = 0 (no anchor norm, R16) so lambda_f halves (P:227,
+    R19), and the new C rows of component f are zero."""
+    T, truth = planted_dense(24, 24, 24, 3, noise=0.01, seed=15)
+    T0, batches = split_dense(T, 18, 6)
+    cfg = O.Config(R=3, s=(2, 2, 2), r=3, seed=6, maxit=10, tol=0.0, tau=0.0, warm_start=True)
+    st = _state_from_truth(T0, truth, cfg, T.size)
+    st.B[:, 2] = 0.0
+    lam0 = st.lam.copy()
+    info = O.update(st, batches[0])
+    assert all(rp["pinv"] for rp in info["reps"])
+    assert st.lam[2] == lam0[2] / 2.0
+    assert np.all(st.C[18:, 2] == 0.0)
