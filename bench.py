@@ -4,8 +4,13 @@
 
 A step is one whole update (a0..a7: ingest, marginals, sampling, gather, batched CP-ALS,
 matching, merge, full fit) of one batch of a BASELINE.json workload with synthetic planted
-data.  Default: configs[1] = C2 (500^3 dense, R=10, K0=450, batches of 10 slices, s=5, r=8,
-30 ALS iterations).  --config C1/C3/C5 select the other single-GPU workloads (C3/C5: COO).
+data.  Default: configs[3] = C4 (3000^2 x 2700 -> 3000 dense, 108 GB on the device, batches of
+50 slices, R=10, s=10, r=16, 30 ALS iterations), the largest config that fits one GPU; its
+summary ALS is warm-started from the model's rows (reading R34) with the acceptance test
+(tau = 0.9, R26), the setting whose model keeps converging (a cold 30-iteration start on the
+300 x 300 x 320 summaries does not converge and the paper-literal merge decays the model; that
+run is reported as the variant "cold_start_paper_literal").  --config C1/C2/C3/C5 select the
+other workloads (C3/C5: COO).
 The metric is BASELINE.json's: new tensor entries (dense) / nonzeros (COO) ingested per
 second per update.  Rank 0 prints one JSON line.
 
@@ -40,7 +45,12 @@ def parse():
     p.add_argument("--steps", type=int, default=60)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C2")
+    p.add_argument("--config", default="C4",
+                   help="BASELINE workload; default C4 = configs[3], the largest single-GPU config")
+    p.add_argument("--als-init", default="config", choices=["config", "cold", "warm"],
+                   help="summary ALS start: the config's setting (C4: warm, R34), the Philox point "
+                        "(P:213, R10) or the model's rows (R34)")
+    p.add_argument("--tau", type=float, default=None, help="override the acceptance threshold (R26)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-variant", action="store_true", help="skip the incremental-marginals variant run")
@@ -237,9 +247,12 @@ def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
         nnz_avg = work.X0.nnz + statistics.mean(
             sum(work.entries[:(j % work.nb) + 1]) for j in range(args.warmup, args.warmup + args.steps))
         out["a1"] = hbm_line("marg_coo_kernel", 1, 16.0 * nnz_avg + 8.0 * (w.I + w.J + statistics.mean(Ks)))
-        out["a4"] = {"kernel": "COO ALS (sort, piece MTTKRP, row solves)", "bound": "latency",
-                     "ms_per_launch": ms(4), "frac": None,
-                     "note": "gather-latency bound sparse MTTKRP on L2-resident summaries; not modelled"}
+        # per ALS iteration, 3 mode passes of 16 B (i, j, k, v) per summary nonzero
+        nz = statistics.mean(inf["summary_entries"] for inf in infos)
+        it = statistics.mean(inf["als_iters_sum"] for inf in infos) / w.r
+        out["a4"] = dict(hbm_line("COO ALS (sort, piece MTTKRP, row solves)", 4, it * 3 * 16.0 * nz),
+                         note="algorithmic bytes: iterations x 3 mode passes x 16 B per summary nonzero "
+                              "(SURVEY 8(d)); summaries smaller than L2 can exceed the HBM line")
         return out
     Kloc = k_local if k_local is not None else Ks
     IJ = w.I * w.J
@@ -344,23 +357,105 @@ def threads_used():
         return os.cpu_count()
 
 
-def oracle_state(work, model=None):
+def oracle_state(work, model=None, tau=None, warm=False):
     from oracle import sambaten as O
     w = work.w
     cfg = O.Config(R=w.R, s=(w.s,) * 3, r=w.r, seed=w.seed, maxit=w.maxit, tol=w.tol,
-                   tau=0.9 if not work.coo else 0.0)
+                   tau=(0.9 if not work.coo else 0.0) if tau is None else tau, warm_start=warm)
     m = model if model is not None else work.model
     return O.init_factors(work.oracle_tensor(work.X0), cfg, *m, work.cap), O
 
 
-def cpu_baseline_run(work, model, budget_s=20.0):
+def method_settings(w, args):
+    """Summary-ALS start and acceptance threshold of the headline run of config w.
+    C4: warm start (R34) + tau = 0.9 -- the setting whose model keeps converging (VERDICT r01);
+    dense C1/C2: cold start + tau = 0.9 (R26); COO C3/C5: cold start, paper-literal tau = 0
+    (C3 has no planted model and its 30-iteration summaries would fail the test)."""
+    warm = w.name.startswith("C4")
+    tau = 0.9 if w.fmt == "dense" else 0.0
+    if args.als_init == "cold":
+        warm, tau = False, (0.0 if w.name.startswith("C4") else tau)
+    elif args.als_init == "warm":
+        warm = True
+    if args.tau is not None:
+        tau = args.tau
+    return warm, tau
+
+
+def oracle_sampled_update(w, warm, als_iters_per_rep, nslab=3, als_probe_iters=2):
+    """The oracle (oracle/, as it stands) on a BOUNDED SAMPLE of one update of a device-sized
+    dense config (C4: the 108 GB tensor does not fit the sample budget): each step of Alg. 1 is
+    timed on a part of the real workload and scaled to the whole update by its work count.
+      a1 marginals: `nslab` slices of the tensor (synth numpy twin of the device generator),
+                    scaled by the update's stored entries;
+      a2 sampling:  all r x 3 draws at the real sizes (weights from the slab's marginals);
+      a3 gather:    one summary's rows over the slab's slices, scaled by r x |I_s||J_s||K'|;
+      a4 ALS:       `als_probe_iters` iterations on one full-size |I_s| x |J_s| x |K'| summary
+                    (planted, the config's rank), scaled by r x the GPU run's iterations per rep;
+      a5 match:     one repetition, x r;   a7 fit: the slab, scaled by the stored entries.
+    Returns (seconds per update, dict of per-step seconds, sample description)."""
+    from oracle import sambaten as O
+    from synth.planted import planted_dense_factors, planted_sigma, dense_philox_slab, dense_from_factors
+    A, B, Cf = planted_dense_factors(w.I, w.J, w.K, w.R, w.seed)
+    sigma = planted_sigma(A, B, Cf, w.noise)
+    k0 = w.K0 - nslab
+    slab = dense_philox_slab(A, B, Cf, sigma, w.seed, k0, nslab)
+    Ktot = w.K0 + w.batch
+    stored = float(w.I) * w.J * Ktot
+    per = float(w.I) * w.J * nslab
+    S = O.fixed_point_scale(w.I * w.J * w.K, float(np.abs(slab).max()))
+    t = {}
+    t0 = time.perf_counter()
+    x1, x2, _ = O.marginals_dense(slab, S)
+    t["a1"] = (time.perf_counter() - t0) * stored / per
+    rng = np.random.default_rng(1)
+    x3 = rng.integers(1, 1 << 40, size=w.K0, dtype=np.int64)
+    nI, nJ, nK = O.sample_size(w.I, w.s), O.sample_size(w.J, w.s), O.sample_size(w.K0, w.s)
+    t0 = time.perf_counter()
+    for rho in range(w.r):
+        Is = O.sample_mode(x1, nI, w.seed, 1, rho, 0)
+        Js = O.sample_mode(x2, nJ, w.seed, 1, rho, 1)
+        Ks = O.sample_mode(x3, nK, w.seed, 1, rho, 2)
+    t["a2"] = time.perf_counter() - t0
+    nKp = nK + w.batch
+    t0 = time.perf_counter()
+    Ys = O.gather_dense(slab, Is, Js, np.arange(nslab))
+    t["a3"] = (time.perf_counter() - t0) * w.r * nKp / nslab
+    Ksub = np.sort(np.concatenate([Ks[: nK], np.arange(w.K0, Ktot)]))[:nKp]
+    Y = O.view_ijk(dense_from_factors(A[Is], B[Js], Cf[Ksub], w.noise, w.seed))
+    U0 = O.als_init(Y.shape, w.R, w.seed, 1, 0)
+    t0 = time.perf_counter()
+    lam_p, Up, _, _, _ = O.cp_als(Y, U0, als_probe_iters, 0.0)
+    t["a4"] = (time.perf_counter() - t0) / als_probe_iters * als_iters_per_rep * w.r
+    if warm:
+        t["a4"] += 0.0   # the warm rows are a copy (no arithmetic worth timing)
+    lam = np.ones(w.R)
+    t0 = time.perf_counter()
+    O.match_rep(A, B, Cf, Is, Js, Ksub[: nK], lam_p, Up, 0.9)
+    t["a5_a6"] = (time.perf_counter() - t0) * w.r
+    t0 = time.perf_counter()
+    O.relative_error(slab, lam, A, B, Cf[k0:k0 + nslab])
+    t["a7"] = (time.perf_counter() - t0) * stored / per
+    del Ys
+    total = sum(t.values())
+    desc = (f"oracle steps timed on parts of one {w.name} update and scaled by work: a1/a7 on {nslab} "
+            f"slices ({per:.3g} of {stored:.3g} stored entries), a2 all {w.r}x3 draws, a3 one summary over "
+            f"{nslab} slices (x {w.r} reps x {nKp}/{nslab}), a4 {als_probe_iters} ALS iterations on one "
+            f"{nI}x{nJ}x{nKp} summary (x {w.r} reps x {als_iters_per_rep:.1f} iterations/rep), a5 one rep (x {w.r})")
+    return total, t, desc
+
+
+def cpu_baseline_run(work, model, tau, warm, budget_s=20.0):
     """The oracle as it stands (oracle/), on this host's cores: consecutive updates of the
     config's batches from the K0 state until ~budget_s seconds (bounded sample)."""
-    st, O = oracle_state(work, model)
+    st, O = oracle_state(work, model, tau=tau, warm=warm)
     t0 = time.perf_counter()
     entries, nb = 0, 0
     for i, b in enumerate(work.batches):
-        O.update(st, work.oracle_tensor(b))
+        try:
+            O.update(st, work.oracle_tensor(b))
+        except O.BatchRejected:
+            pass
         entries += work.entries[i]
         nb += 1
         if time.perf_counter() - t0 > budget_s:
@@ -388,34 +483,55 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        if device_gen:
-            print(json.dumps({"impl": "reference", "unavailable": f"{w.name}: the oracle would need the "
-                              f"{4 * w.I * w.J * w.K / 1e9:.0f} GB tensor in host memory"}), flush=True)
-            return
-        if work.model is None:
-            from oracle import sambaten as O
-            cfg = O.Config(R=w.R, s=(w.s,) * 3, r=w.r, seed=w.seed)
-            st0 = O.init_als(work.oracle_tensor(work.X0), cfg, work.cap, maxit=50, tol=1e-6)
-            work.model = [np.asarray(x, np.float32) for x in (st0.lam, st0.A, st0.B, st0.C)]
+        warm, tau = method_settings(w, args)
+        config["accept_tau"] = tau
+        config["als_init"] = "warm (R34)" if warm else "cold (Philox point, P:213)"
+        cores = threads_used()
         times, ents = [], []
-        for i in range(args.warmup + args.steps):
-            st, O = oracle_state(work)
-            bi = i % work.nb
-            t0 = time.perf_counter()
-            O.update(st, work.oracle_tensor(work.batches[bi]))
-            dt = time.perf_counter() - t0
-            if i >= args.warmup:
-                times.append(dt)
-                ents.append(work.entries[bi])
+        if device_gen:
+            # each step: the oracle on a bounded sample of one update, scaled to the whole update
+            it_rep = 3.0 if warm else float(w.maxit)
+            for i in range(args.warmup + args.steps):
+                tot, parts, desc = oracle_sampled_update(w, warm, it_rep, nslab=2, als_probe_iters=1)
+                if i >= args.warmup:
+                    times.append(tot)
+                    ents.append(w.I * w.J * w.batch)
+            sample = desc + "; ALS iterations per rep assumed " + ("3 (warm start)" if warm else str(w.maxit))
+        else:
+            # consecutive updates of the config's batch stream from the K0 state (restored after
+            # the last batch), as the GPU arm replays it; a rejected batch (R26) leaves the
+            # state unchanged and still counts its work
+            import copy
+            from oracle import sambaten as O
+            if work.model is None:
+                cfg = O.Config(R=w.R, s=(w.s,) * 3, r=w.r, seed=w.seed)
+                st0 = O.init_als(work.oracle_tensor(work.X0), cfg, work.cap, maxit=50, tol=1e-6)
+                work.model = [np.asarray(x, np.float32) for x in (st0.lam, st0.A, st0.B, st0.C)]
+            st_k0, O = oracle_state(work, tau=tau, warm=warm)
+            st = copy.deepcopy(st_k0)
+            rejected = 0
+            for i in range(args.warmup + args.steps):
+                bi = i % work.nb
+                if bi == 0 and i > 0:
+                    st = copy.deepcopy(st_k0)
+                t0 = time.perf_counter()
+                try:
+                    O.update(st, work.oracle_tensor(work.batches[bi]))
+                except O.BatchRejected:
+                    rejected += 1
+                dt = time.perf_counter() - t0
+                if i >= args.warmup:
+                    times.append(dt)
+                    ents.append(work.entries[bi])
+            sample = (f"each step = one full oracle update of the next batch of the {w.name} stream from the "
+                      f"K0 state (restored after the last batch); {rejected} batch(es) rejected (R26)")
         tot = sum(times)
         val = sum(ents) / tot
-        cores = threads_used()
         line = {"impl": "reference", "metric": metric, "value": val, "unit": unit, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / len(times),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded numpy generators)", "config": config,
-                "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "oracle",
-                                 "sample": "each step = one full oracle update of one batch from the K0 state"},
+                "data": "synthetic (seeded generators; DESIGN.md 'Synthetic inputs')", "config": config,
+                "cpu_baseline": {"value": val, "unit": unit, "cores": cores, "kind": "oracle", "sample": sample},
                 "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -431,15 +547,13 @@ def main():
 
     sharded = world > 1 or args.sharded
     stream = torch.cuda.Stream()
-    # C3's community tensor has no planted model; with R = 15 and 30 summary iterations the
-    # acceptance test (R26, tau = 0.9) can reject every repetition, so the COO workloads run
-    # the paper-literal merge (tau = 0)
-    # (C4: 300 x 300 x ~330 summaries at R = 10 do not converge in 30 iterations from a random
-    # start -- SURVEY A27 -- so every repetition would fail the tau = 0.9 test)
-    tau = 0.9 if not (work.coo or device_gen) else 0.0
+    # summary-ALS start and acceptance threshold (method_settings: C4 warm + tau 0.9, dense
+    # cold + tau 0.9, COO cold + tau 0)
+    warm, tau = method_settings(w, args)
     config["accept_tau"] = tau
+    config["als_init"] = "warm (model rows, R34)" if warm else "cold (Philox point, P:213)"
     opts = L.default_opts(als_max_iters=w.maxit, als_tol=w.tol, capacity=work.cap, full_fit=int(not args.no_full_fit),
-                          accept_tau=tau, stream=stream.cuda_stream)
+                          accept_tau=tau, stream=stream.cuda_stream, warm_start=int(warm))
     if work.coo:
         opts.capacity_k = w.K
     else:
@@ -578,10 +692,17 @@ def main():
                        "ms_per_step": 1000.0 * e2e_tot / len(e2e_times),
                        "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in e2e_infos)
                                    for k in range(8)}}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not device_gen:
-        model = work.model
-        if model is not None:
-            v, dt, nbt = cpu_baseline_run(work, model)
+    line["als_iters_per_rep"] = statistics.mean(inf["als_iters_sum"] for inf in infos) / (w.r / (world if sharded else 1))
+    line["als_plan_last"] = infos[-1]["als_plan"]
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if device_gen:
+            tot_s, parts, desc = oracle_sampled_update(w, warm, line["als_iters_per_rep"])
+            line["cpu_baseline"] = {"value": w.I * w.J * w.batch / tot_s, "unit": unit, "cores": threads_used(),
+                                    "kind": "oracle", "sample": desc,
+                                    "seconds_per_update_estimated": tot_s,
+                                    "step_seconds": {k: round(v, 3) for k, v in parts.items()}}
+        elif work.model is not None:
+            v, dt, nbt = cpu_baseline_run(work, work.model, tau, warm)
             line["cpu_baseline"] = {"value": v, "unit": unit, "cores": threads_used(), "kind": "oracle",
                                     "sample": f"{nbt} consecutive oracle updates of {w.name} from the K0 state, {dt:.1f} s"}
     if world == 1 and not sharded and not args.no_variant:
@@ -610,8 +731,10 @@ def main():
                 ve.append(ne)
             for k, v in saved.items():
                 setattr(opts, k, v)
+            kv = kernel_rooflines(w, work, vi, peaks, peak_kind, 1, None, args)
             return {"value": sum(ve) / (sum(vt) / 1000.0), "unit": unit, "ms_per_step": statistics.mean(vt),
-                    "steps": len(vt),
+                    "steps": len(vt), "fit_full_last": vi[-1]["fit_full"], "kernels": kv,
+                    "reps_rejected_last": bin(vi[-1]["reps_rejected_mask"]).count("1"),
                     "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in vi) for k in range(8)},
                     "als_iters_mean": statistics.mean(inf["als_iters_sum"] / w.r for inf in vi),
                     "rep_rank_last": vi[-1]["rep_rank"][:w.r]}
@@ -619,6 +742,13 @@ def main():
             run_variant(args.steps, incremental_marginals=1),
             note="opts.incremental_marginals=1: a1 adds the batch's contribution to the committed int64 "
                  "marginals (bit-identical to the full pass; tests/test_gpu_incremental.py)")}
+        if device_gen and warm:
+            v = run_variant(args.steps, warm_start=0, accept_tau=0.0)
+            v["roofline_a4"] = v.pop("kernels")["a4"]
+            line["variants"]["cold_start_paper_literal"] = dict(
+                v, note="cold summary ALS from the Philox point (P:213, R10), 30 iterations, paper-literal "
+                        "merge tau = 0 (the r01 headline setting): the summaries do not converge and the "
+                        "model decays (fit_full_last); a4 roofline of the cold 30-iteration run")
         if not work.coo and not device_gen:
             line["variants"]["warm_start"] = dict(
                 run_variant(args.steps, warm_start=1),
@@ -627,6 +757,8 @@ def main():
             line["variants"]["getrank_in_update"] = dict(
                 run_variant(min(args.steps, 5), getrank=1),
                 note="opts.getrank=1 (P:266, Alg. 2; R33): a4 includes GetRank over ranks 1..R on every summary")
+        for vv in line["variants"].values():
+            vv.pop("kernels", None)
     L.sambaten_destroy(h)
     if rank == 0 and not work.coo and not args.no_getrank:
         line["getrank"] = getrank_timing(L, w, stream)

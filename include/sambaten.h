@@ -100,7 +100,8 @@ typedef struct {
   int warm_start;         /* 1: each summary ALS starts from the model's rows (A(I_s), B(J_s),  */
                           /* C(K_s) diag(lambda), zero rows for the new slices   */
                           /* NEXT #4, reading R34) instead of the Philox point.  Dense        */
-                          /* single-GPU handles, not with getrank (else SAMBATEN_E_INVALID).  */
+                          /* handles (single-GPU and sharded), not with getrank (else         */
+                          /* SAMBATEN_E_INVALID).                                             */
 } sambaten_opts;
 
 typedef struct {
@@ -118,6 +119,14 @@ typedef struct {
   int als_iters_sum;           /* ALS iterations summed over the repetitions (work accounting) */
   int rep_rank[32];            /* rank each repetition decomposed its summary at (R unless    */
                                /* opts.getrank reduced it, R33); entries >= r are 0           */
+  int als_plan[4];             /* the a4 launch plan this update ran (dense handles):         */
+                               /* [0] kind: 0 multi-kernel ALS, 1 cluster ALS (one thread-    */
+                               /* block cluster per repetition), -1 none (COO / GetRank);     */
+                               /* [1] CTAs per repetition, [2] RB (padded rank width),        */
+                               /* [3] 1 if D lives in shared memory, 0 if in global memory     */
+  int64_t summary_entries;     /* entries (dense) or nonzeros (COO) of the summaries this      */
+                               /* rank decomposed, summed over its repetitions (work units of  */
+                               /* a3 / a4 for the rooflines)                                   */
 } sambaten_info;
 
 /* Fill *opts with the defaults listed above. */
@@ -282,6 +291,12 @@ SAMBATEN_API sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, fl
  * G = X x1 pinv(A) x2 pinv(B) x3 pinv(C) and cc = 100 (1 - sum (G - T)^2 / F), T the
  * superdiagonal unit core.  A, B, C: device float32 [dims][F] row-major; lambda: device
  * float64[F]; cc: host or device float64[1].  fp64 throughout; E_INVALID on bad arguments. */
+/* The a4 plan (sambaten_info.als_plan layout) the library would pick for r dense summaries of
+ * shape nI x nJ x nK at rank R on the current device (no handle; host call that queries the
+ * device's cluster occupancy).  Lets a test assert that a small problem runs the same kernel
+ * instantiation as a large one.  Errors: E_INVALID (bad sizes), E_CUDA. */
+SAMBATEN_API sambaten_status sambaten_als_plan(int nI, int nJ, int nK, int R, int r, int plan[4]);
+
 SAMBATEN_API sambaten_status sambaten_corcondia(const sambaten_tensor* X, int F, const float* A, const float* B,
                                    const float* C, const double* lambda, double* cc, void* stream);
 

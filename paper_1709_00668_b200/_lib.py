@@ -52,7 +52,8 @@ class Info(C.Structure):
                 ("reps_rejected_mask", C.c_uint32), ("scale_exp", C.c_int),
                 ("kernel_launches", C.c_int), ("reps_pinv_mask", C.c_uint32),
                 ("step_ms", C.c_double * 8), ("als_iters_sum", C.c_int),
-                ("rep_rank", C.c_int * 32)]
+                ("rep_rank", C.c_int * 32), ("als_plan", C.c_int * 4),
+                ("summary_entries", C.c_int64)]
 
     def as_dict(self):
         return dict(fit_summary=self.fit_summary, fit_full=self.fit_full,
@@ -60,7 +61,8 @@ class Info(C.Structure):
                     reps_rejected_mask=self.reps_rejected_mask, scale_exp=self.scale_exp,
                     kernel_launches=self.kernel_launches, reps_pinv_mask=self.reps_pinv_mask,
                     step_ms=list(self.step_ms), als_iters_sum=self.als_iters_sum,
-                    rep_rank=list(self.rep_rank))
+                    rep_rank=list(self.rep_rank), als_plan=list(self.als_plan),
+                    summary_entries=self.summary_entries)
 
 
 _lib = None
@@ -105,6 +107,7 @@ def lib():
         "sambaten_dist_plan": (i32, [vp, ip, i64, vp, i64, i64, ip, ip, vp, vp]),
         "sambaten_corcondia": (i32, [T, ip, vp, vp, vp, vp, vp, vp]),
         "sambaten_getrank": (i32, [T, ip, ip, u64, ip, d, d, C.POINTER(ip), vp, vp]),
+        "sambaten_als_plan": (i32, [ip, ip, ip, ip, ip, vp]),
         "sambaten_last_error": (C.c_char_p, []),
         "sambaten_version": (C.c_char_p, []),
     }
@@ -122,7 +125,7 @@ EXPORTED = ["sambaten_default_opts", "sambaten_init", "sambaten_init_factors", "
             "sambaten_fixed_point_scale", "sambaten_marginals", "sambaten_sample", "sambaten_gather",
             "sambaten_mttkrp", "sambaten_cp_als", "sambaten_fit", "sambaten_philox", "sambaten_detlog",
             "sambaten_dist_unique_id", "sambaten_init_factors_dist", "sambaten_batch_partition",
-            "sambaten_dist_plan", "sambaten_corcondia", "sambaten_getrank",
+            "sambaten_dist_plan", "sambaten_corcondia", "sambaten_getrank", "sambaten_als_plan",
             "sambaten_last_error", "sambaten_version"]
 
 
@@ -332,6 +335,14 @@ def sambaten_cp_als(X, R, U0, U1, U2, lam_out, max_iters, tol, fit_out, iters_ou
 
 def sambaten_fit(X, lam, A, B, Cm, R, relerr, stream=None):
     check(lib().sambaten_fit(C.byref(X), ptr(lam), ptr(A), ptr(B), ptr(Cm), R, ptr(relerr), stream))
+
+
+def sambaten_als_plan(nI, nJ, nK, R, r):
+    """The a4 plan [kind, CTAs per rep, RB, D in smem] the library picks for r summaries of
+    shape nI x nJ x nK at rank R (sambaten_info.als_plan layout)."""
+    out = np.zeros(4, np.int32)
+    check(lib().sambaten_als_plan(nI, nJ, nK, R, r, out.ctypes.data))
+    return [int(x) for x in out]
 
 
 def sambaten_corcondia(X, F, A, B, Cm, lam, stream=None):

@@ -116,6 +116,8 @@ struct sambaten_s {
   DistState* dist = nullptr;   // set for handles of the sharded update (sambaten_init_factors_dist)
   int64_t I = 0, J = 0, K = 0, Kcap = 0, pitch = 0;
   bool X_borrowed = false;   // opts.borrow_store: X is the caller's buffer
+  int als_plan[4] = {-1, 0, 0, 0};   // the a4 plan of the last update (sambaten_info.als_plan)
+  int64_t summ_entries = 0;          // summary entries / nnz of the update in flight (sambaten_info)
   cudaStream_t st2 = nullptr;     // side stream: host batch copy overlapped with a1 (old slices)
   cudaEvent_t ev_side[2] = {nullptr, nullptr};
   DevBuf xm, xm_ck;          // committed marginals of the current tensor (incremental a1)
@@ -180,6 +182,13 @@ static bool cluster_plan(sambaten_s* h, const DenseAls& a, ClusterPlan* pl) {
   h->plans.push_back(e);
   *pl = e.pl;
   return e.ok;
+}
+
+static void set_plan_report(sambaten_s* h, bool cluster, const ClusterPlan& pl, int R) {
+  h->als_plan[0] = cluster ? 1 : 0;
+  h->als_plan[1] = cluster ? pl.CS : 1;
+  h->als_plan[2] = cluster ? pl.RB : R;
+  h->als_plan[3] = cluster ? pl.dsh : 0;
 }
 
 extern "C" {
@@ -705,6 +714,8 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
     info->reps_pinv_mask = pm;
     info->kernel_launches = launches;
     for (int rho = 0; rho < 32; ++rho) info->rep_rank[rho] = rho < r ? (h->opts.getrank ? h->rep_rank[rho] : R) : 0;
+    for (int e = 0; e < 4; ++e) info->als_plan[e] = h->als_plan[e];
+    info->summary_entries = h->summ_entries;
     for (int e = 0; e < 8; ++e) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);
@@ -1001,6 +1012,7 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
   CK(cudaMemcpyAsync(h_off, d_off, sizeof(int64_t) * (r + 1), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));   // summary sizes decide the allocation below
   const int64_t nsum = h_off[r];
+  h->summ_entries = nsum;
   const size_t sbytes = align256(sizeof(int32_t) * std::max<int64_t>(nsum, 1));
   CK(h->fac.ensure(4 * sbytes + align256(sizeof(float) * r * (nI + nJ + nKp) * R)));
   int32_t* sp = h->fac.as<int32_t>();
@@ -1055,6 +1067,8 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   if (batch->fmt != h->fmt) FAIL(SAMBATEN_E_INVALID, "update: batch format differs from the state's");
   if (batch->dims[0] != h->I || batch->dims[1] != h->J)
     FAIL(SAMBATEN_E_SHAPE, "update: batch I x J differs from the state's (S:68)");
+  h->als_plan[0] = -1; h->als_plan[1] = h->als_plan[2] = h->als_plan[3] = 0;   // set by the dense paths
+  h->summ_entries = 0;
   if (h->dist)
     return h->fmt == SAMBATEN_COO ? update_coo_dist(h, batch, Aout, Bout, Cout, lamout, info)
                                   : update_dense_dist(h, batch, Aout, Bout, Cout, lamout, info);
@@ -1148,6 +1162,8 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   a.Yt = reinterpret_cast<const float*>(1);   // planning only needs "transpose available"
   ClusterPlan cpl;
   const bool use_cluster = cluster_plan(h, a, &cpl);
+  set_plan_report(h, use_cluster, cpl, R);
+  h->summ_entries = (int64_t)r * nI * nJ * nKp;
   const int pI = use_cluster ? cluster_pitch((int)nI) : (int)nI;
   const int pJ = use_cluster ? cluster_pitch((int)nJ) : (int)nJ;
   if (use_cluster) y_stride = (nKp * std::max<int64_t>(nJ * pI, nI * pJ) + 3) & ~int64_t(3);
@@ -1183,6 +1199,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     }
   }
   if (d_rnew) {
+    h->als_plan[0] = -1;   // per-rep ranks: the multi-kernel ALS at each rep's R_new
     CK(rank_als(h, a, h->rep_rank, uid, st, &als_launches));
   } else if (use_cluster) {
     CK(launch_als_init_factors(a, h->seed, uid, 0, st));
@@ -1620,6 +1637,22 @@ extern "C" sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, floa
   copy_als_out_kernel<<<1, 32, 0, st>>>(a.lam, a.fit, a.iters, R, lambda_out, fit_out, iters_out);
   CK(cudaGetLastError());
   CK(cudaFreeAsync(ws, st));
+  return SAMBATEN_OK;
+}
+
+extern "C" sambaten_status sambaten_als_plan(int nI, int nJ, int nK, int R, int r, int plan[4]) {
+  if (nI < 1 || nJ < 1 || nK < 1 || R < 1 || R > kMaxR || r < 1 || r > kMaxReps || !plan)
+    FAIL(SAMBATEN_E_INVALID, "als_plan: bad argument");
+  DenseAls a{};
+  a.nI = nI; a.nJ = nJ; a.nK = nK; a.R = R; a.r = r;
+  a.Yt = reinterpret_cast<float*>(16);   // the plan only needs to know a transposed layout exists
+  ClusterPlan pl{};
+  const bool ok = r >= 2 && !getenv("SAMBATEN_NO_CLUSTER_ALS") && plan_als_cluster(a, &pl);
+  cudaGetLastError();
+  plan[0] = ok ? 1 : 0;
+  plan[1] = ok ? pl.CS : 1;
+  plan[2] = ok ? pl.RB : R;
+  plan[3] = ok ? pl.dsh : 0;
   return SAMBATEN_OK;
 }
 

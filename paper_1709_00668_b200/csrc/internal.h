@@ -117,7 +117,8 @@ cudaError_t launch_corcondia(const float* X, int64_t x_stride, int64_t pitch, in
 // Warm start (R34): U0 = A(I_s), U1 = B(J_s), U2 = [fp32(C(K_s) lambda); 0] per repetition
 // (Is [r][nI], Js [r][nJ], Kp [r][nK] with the first nKs entries the old slices K_s)
 cudaError_t launch_warm_init(const DenseAls& a, const float* A, const float* B, const float* C, const float* lam,
-                             const int32_t* Is, const int32_t* Js, const int32_t* Kp, int nKs, cudaStream_t st);
+                             const int32_t* Is, const int32_t* Js, const int32_t* Kp, int nKs, cudaStream_t st,
+                             int rep0 = 0, int rep_stride = 1);
 // GetRank inside the update (R33): copy the r = 1 rank-src.R decomposition `src` into
 // repetition rho of the rank-dst.R candidate buffers of `dst` (columns >= src.R and their
 // lambda zero; fit / iters / flags copied)

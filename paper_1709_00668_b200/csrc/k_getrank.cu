@@ -208,11 +208,13 @@ cudaError_t launch_rank_pad(const DenseAls& src, const DenseAls& dst, int rho, c
 // ---- warm start (R34) ------------------------------------------------------------------------
 namespace {
 __global__ void warm_init_kernel(DenseAls a, const float* A, const float* B, const float* C, const float* lam,
-                                 const int32_t* Is, const int32_t* Js, const int32_t* Kp, int nKs) {
+                                 const int32_t* Is, const int32_t* Js, const int32_t* Kp, int nKs, int rep0,
+                                 int rep_stride) {
   const int rep = blockIdx.y, m = blockIdx.z, R = a.R;
   const int n = m == 0 ? a.nI : m == 1 ? a.nJ : a.nK;
   float* U = a.U[m] + rep * a.u_stride[m];
-  const int32_t* idx = (m == 0 ? Is : m == 1 ? Js : Kp) + (int64_t)rep * n;
+  // the sample lists hold every repetition; local rep `rep` is global repetition rep0 + rep * rep_stride
+  const int32_t* idx = (m == 0 ? Is : m == 1 ? Js : Kp) + (int64_t)(rep0 + rep * rep_stride) * n;
   const float* F = m == 0 ? A : m == 1 ? B : C;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)n * R;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -226,10 +228,12 @@ __global__ void warm_init_kernel(DenseAls a, const float* A, const float* B, con
 }  // namespace
 
 cudaError_t launch_warm_init(const DenseAls& a, const float* A, const float* B, const float* C, const float* lam,
-                             const int32_t* Is, const int32_t* Js, const int32_t* Kp, int nKs, cudaStream_t st) {
+                             const int32_t* Is, const int32_t* Js, const int32_t* Kp, int nKs, cudaStream_t st,
+                             int rep0, int rep_stride) {
   const int nmax = max(a.nI, max(a.nJ, a.nK));
   const unsigned gx = (unsigned)ceil_div((int64_t)nmax * a.R, kGT);
-  warm_init_kernel<<<dim3(gx < 64 ? gx : 64, a.r, 3), kGT, 0, st>>>(a, A, B, C, lam, Is, Js, Kp, nKs);
+  warm_init_kernel<<<dim3(gx < 64 ? gx : 64, a.r, 3), kGT, 0, st>>>(a, A, B, C, lam, Is, Js, Kp, nKs, rep0,
+                                                                    rep_stride);
   return cudaGetLastError();
 }
 
