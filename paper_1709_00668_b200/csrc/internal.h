@@ -297,6 +297,14 @@ bool fit_stream_supported(const DenseView& X, int R);
 cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
                                     int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st);
 size_t fit_stream_ws_doubles(const DenseView& X);
+// a1 over slices [0, nk) fused with the fit partials of the model (lam; A, B, C) over the same
+// slices (SURVEY 8(f) NEXT #1 lag-1 fit): x1/x2/x3 accumulate (zero them first); out2 =
+// {<X, M>, ||X||^2} of those slices (finish with launch_fit_finish); kmap: local slice -> model
+// row (sharded stores) or NULL; ws: fit_stream_ws_doubles; needs fit_stream_supported(X, R)
+cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, const float* lam,
+                                   const float* A, const float* B, const float* C, int R, const int32_t* kmap,
+                                   int64_t* x1, int64_t* x2, int64_t* x3, double* ws, double* out2,
+                                   cudaStream_t st);
 cudaError_t launch_fit_stream(const DenseView& X, const float* lam, const float* A, const float* B,
                               const float* C, int R, double* ws, double* relerr, cudaStream_t st);
 

@@ -627,6 +627,355 @@ StreamGeom fit_geom(const DenseView& X, int RB, int* gx, int* gy, int* threads) 
   return g;
 }
 
+
+// ---------------------------------------------------------------------------------------
+// a1 + lag-1 a7 in ONE pass (second half; Alg. 1 l.2 and
+// P:409-413): while update t+1 streams the old slices [0, K_t) for its marginals, the same
+// bytes give <X_t, [[lam; A, B, C]]_t> and ||X_t||^2 of the model update t committed (its C
+// has exactly the rows of those slices).  Thread layout of the fit pass with the row groups
+// padded to whole warps (a warp never straddles two rows): thread (group grp, lane tq) owns
+// the column quads tq + u * tpg of rows grp, grp + ng, ...; per element: the fit's FMAs (as
+// fit_stream_kernel), fp32 sum of squares, and q(x) = RNE(phi(x) 2^S) added to the thread's
+// int64 column sums (x1) and to its row partial, reduced over the warp per row (butterfly)
+// -> one global atomic per row and warp (x2) and a per-warp running sum per slice (x3), as
+// marg_stream_kernel.  Integer marginals: bit-identical to the separate pass.
+// ---------------------------------------------------------------------------------------
+template <int MOI, int RB, int QPT, bool BRES>
+__global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_kernel(
+    const float* __restrict__ X, StreamGeom g, int J, int R, float scf, double scd,
+    const float* __restrict__ lam, const float* __restrict__ A, const float* __restrict__ B,
+    const float* __restrict__ C, double* __restrict__ part, unsigned long long* __restrict__ x1,
+    unsigned long long* __restrict__ x2, unsigned long long* __restrict__ x3, const int32_t* __restrict__ kmap) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned long long bars[kMaxNS];
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, nthr = blockDim.x;
+  const int nq = g.pitch / 4;
+  const int tq = tid % g.tpg, grp = tid / g.tpg;   // g.tpg: a multiple of 32
+  const bool active = grp < g.ng;
+  const int64_t rb = g.row0 + (int64_t)blockIdx.x * g.rows_per_cta;
+  const int64_t re = min(rb + g.rows_per_cta, g.row0 + g.nrows);
+  float* ring = reinterpret_cast<float*>(smem);
+  float* Wbuf = ring + (size_t)g.ns * g.tr * g.pitch;   // BRES: Bs [J][RB]; else W [2][tr][RB]
+  const int nst = rb < re ? (int)((re - rb + g.tr - 1) / g.tr) : 0;
+  float wb[kWPT];
+  auto load_w = [&](int64_t r0, int j0) {
+    const int nr = (int)min((int64_t)g.tr, re - r0);
+#pragma unroll
+    for (int t = 0; t < kWPT; ++t) {
+      const int e = tid + t * nthr;
+      wb[t] = 0.f;
+      if (e < nr * RB) {
+        const int r = e / RB, f = e - r * RB;
+        int j = j0 + r;
+        if (j >= J) j -= (j / J) * J;
+        if (f < R) wb[t] = __ldg(B + (int64_t)j * R + f);
+      }
+    }
+  };
+  auto store_w = [&](int s) {
+    float* W = Wbuf + (size_t)(s & 1) * g.tr * RB;
+#pragma unroll
+    for (int t = 0; t < kWPT; ++t) {
+      const int e = tid + t * nthr;
+      if (e < g.tr * RB) W[e] = wb[t];
+    }
+  };
+  if (tid == 0) {
+    for (int s = 0; s < g.ns; ++s) s_mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  int64_t ks = rb / J;
+  int js = (int)(rb - ks * J);
+  if constexpr (BRES) {
+    for (int e = tid; e < J * RB; e += nthr) {
+      const int j = e / RB, f = e - j * RB;
+      Wbuf[e] = f < R ? B[(int64_t)j * R + f] : 0.f;
+    }
+  } else {
+    if (nst > 0) { load_w(rb, js); store_w(0); }
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < nst && s < g.ns; ++s) marg_issue(ring, bars, g, X, rb, re, s);
+  double inner = 0.0, sq = 0.0;
+  long long xa[QPT][4];   // x1 column sums of the thread's quads
+#pragma unroll
+  for (int u = 0; u < QPT; ++u)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) xa[u][e] = 0;
+  long long x3run = 0;    // lane 0: the warp's running x3 sum of slice x3k
+  int64_t x3k = -1;
+  // the warp's row total: butterfly, then lane 0 adds it to x2[j] and to the running x3 sum
+  auto row_done = [&](long long rs, int j, int64_t k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+    if (lane == 0) {
+      if (rs) atomicAdd(&x2[j], (unsigned long long)rs);
+      if (k != x3k) {
+        if (x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
+        x3k = k;
+        x3run = 0;
+      }
+      x3run += rs;
+    }
+  };
+  auto quad_marg = [&](const float4& v, long long (&xq)[4]) -> long long {
+    const long long q0 = quant<MOI>(v.x, scf, scd), q1 = quant<MOI>(v.y, scf, scd);
+    const long long q2 = quant<MOI>(v.z, scf, scd), q3 = quant<MOI>(v.w, scf, scd);
+    xq[0] += q0; xq[1] += q1; xq[2] += q2; xq[3] += q3;
+    return (q0 + q1) + (q2 + q3);   // padding columns are zero in the store: q = 0
+  };
+  auto wrow = [&](const float* wr, float (&w)[RB]) {
+    if constexpr (RB % 4 == 0) {
+#pragma unroll
+      for (int f4 = 0; f4 < RB / 4; ++f4) {
+        const float4 wv = *reinterpret_cast<const float4*>(wr + 4 * f4);
+        w[4 * f4] = wv.x; w[4 * f4 + 1] = wv.y; w[4 * f4 + 2] = wv.z; w[4 * f4 + 3] = wv.w;
+      }
+    } else {
+#pragma unroll
+      for (int f2 = 0; f2 < RB / 2; ++f2) {
+        const float2 wv = *reinterpret_cast<const float2*>(wr + 2 * f2);
+        w[2 * f2] = wv.x; w[2 * f2 + 1] = wv.y;
+      }
+    }
+  };
+  if constexpr (QPT == 1) {
+    constexpr int kFoldRows = 128;
+    float acc[4][RB];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int f = 0; f < RB; ++f) acc[e][f] = 0.f;
+    int64_t kc = -1;
+    int run = 0;
+    auto fold = [&](int64_t k) {
+      const int64_t kg = kmap ? kmap[k] : k;   // sharded store: local slice -> model row
+      float lc[RB];
+#pragma unroll
+      for (int f = 0; f < RB; ++f) lc[f] = f < R ? lam[f] * C[kg * R + f] : 0.f;
+      float t = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 4 * tq + e;
+#pragma unroll
+        for (int f = 0; f < RB; ++f) {
+          if (i < g.ncol && f < R) t = fmaf(A[(int64_t)i * R + f] * lc[f], acc[e][f], t);
+          acc[e][f] = 0.f;
+        }
+      }
+      inner += (double)t;
+      run = 0;
+    };
+    const bool qok = tq < nq;
+    for (int s = 0; s < nst; ++s) {
+      const int slot = s % g.ns;
+      const int64_t r0 = rb + (int64_t)s * g.tr;
+      const int nr = (int)min((int64_t)g.tr, re - r0);
+      int jn = js + g.tr;
+      int64_t kn = ks;
+      if (jn >= J) { kn += jn / J; jn -= (jn / J) * J; }
+      if (!BRES && s + 1 < nst) load_w(r0 + g.tr, jn);
+      s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
+      if (active) {
+        const float* st = ring + (size_t)slot * g.tr * g.pitch;
+        const float* W = Wbuf + (BRES ? 0 : (size_t)(s & 1) * g.tr * RB);
+        float fs = 0.f;
+        int64_t k = ks;
+        int j = js;
+        for (int ra = 0; ra < nr;) {
+          const int seg = min(nr - ra, J - j);
+          if (k != kc) {
+            if (kc >= 0) fold(kc);
+            kc = k;
+          }
+#pragma unroll 1
+          for (int r = ra + ((grp - ra) % g.ng + g.ng) % g.ng; r < ra + seg; r += g.ng) {
+            const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
+            long long rs = 0;
+            if (qok) {
+              float w[RB];
+              wrow(wr, w);
+              const float4 v = *reinterpret_cast<const float4*>(st + (size_t)r * g.pitch + 4 * tq);
+#pragma unroll
+              for (int f = 0; f < RB; ++f) {
+                acc[0][f] = fmaf(v.x, w[f], acc[0][f]);
+                acc[1][f] = fmaf(v.y, w[f], acc[1][f]);
+                acc[2][f] = fmaf(v.z, w[f], acc[2][f]);
+                acc[3][f] = fmaf(v.w, w[f], acc[3][f]);
+              }
+              fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
+              rs = quad_marg(v, xa[0]);
+            }
+            row_done(rs, j + r - ra, k);
+            ++run;
+          }
+          ra += seg;
+          j = 0;
+          ++k;
+        }
+        if (run >= kFoldRows) fold(kc);
+        sq += (double)fs;
+      }
+      if (!BRES && s + 1 < nst) store_w(s + 1);
+      __syncthreads();
+      if (tid == 0 && s + g.ns < nst) {
+        s_fence_async();
+        marg_issue(ring, bars, g, X, rb, re, s + g.ns);
+      }
+      ks = kn;
+      js = jn;
+    }
+    if (active && kc >= 0) fold(kc);
+  } else {
+    float al[QPT][4][RB];
+    int64_t kc = -1;
+    auto load_al = [&](int64_t k) {
+      const int64_t kg = kmap ? kmap[k] : k;
+#pragma unroll
+      for (int u = 0; u < QPT; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int f = 0; f < RB; ++f) {
+            const int i = 4 * (tq + u * g.tpg) + e;
+            float v = 0.f;
+            if (active && i < g.ncol && f < R) v = lam[f] * A[(int64_t)i * R + f] * C[kg * R + f];
+            al[u][e][f] = v;
+          }
+    };
+    for (int s = 0; s < nst; ++s) {
+      const int slot = s % g.ns;
+      const int64_t r0 = rb + (int64_t)s * g.tr;
+      const int nr = (int)min((int64_t)g.tr, re - r0);
+      int jn = js + g.tr;
+      int64_t kn = ks;
+      if (jn >= J) { kn += jn / J; jn -= (jn / J) * J; }
+      if (!BRES && s + 1 < nst) load_w(r0 + g.tr, jn);
+      s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
+      if (active) {
+        const float* st = ring + (size_t)slot * g.tr * g.pitch;
+        const float* W = Wbuf + (BRES ? 0 : (size_t)(s & 1) * g.tr * RB);
+        float fi = 0.f, fs = 0.f;
+        int64_t k = ks;
+        int j = js;
+        for (int ra = 0; ra < nr;) {
+          const int seg = min(nr - ra, J - j);
+          if (k != kc) {
+            inner += (double)fi;
+            fi = 0.f;
+            load_al(k);
+            kc = k;
+          }
+#pragma unroll 1
+          for (int r = ra + ((grp - ra) % g.ng + g.ng) % g.ng; r < ra + seg; r += g.ng) {
+            const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
+            float w[RB];
+            wrow(wr, w);
+            long long rs = 0;
+#pragma unroll
+            for (int u = 0; u < QPT; ++u) {
+              const int q = tq + u * g.tpg;
+              if (q < nq) {
+                const float4 v = *reinterpret_cast<const float4*>(st + (size_t)r * g.pitch + 4 * q);
+                float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+#pragma unroll
+                for (int f = 0; f < RB; ++f) {
+                  m0 = fmaf(al[u][0][f], w[f], m0);
+                  m1 = fmaf(al[u][1][f], w[f], m1);
+                  m2 = fmaf(al[u][2][f], w[f], m2);
+                  m3 = fmaf(al[u][3][f], w[f], m3);
+                }
+                fi = fmaf(v.x, m0, fmaf(v.y, m1, fmaf(v.z, m2, fmaf(v.w, m3, fi))));
+                fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
+                rs += quad_marg(v, xa[u]);
+              }
+            }
+            row_done(rs, j + r - ra, k);
+          }
+          ra += seg;
+          j = 0;
+          ++k;
+        }
+        inner += (double)fi;
+        sq += (double)fs;
+      }
+      if (!BRES && s + 1 < nst) store_w(s + 1);
+      __syncthreads();
+      if (tid == 0 && s + g.ns < nst) {
+        s_fence_async();
+        marg_issue(ring, bars, g, X, rb, re, s + g.ns);
+      }
+      ks = kn;
+      js = jn;
+    }
+  }
+  if (lane == 0 && x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
+  inner = block_sum_d(inner, red);
+  sq = block_sum_d(sq, red);
+  if (tid == 0) {
+    part[2 * blockIdx.x] = inner;
+    part[2 * blockIdx.x + 1] = sq;
+  }
+  // x1: the groups' column sums through the (idle) ring, summed per column in group order
+  __syncthreads();
+  long long* xg = reinterpret_cast<long long*>(smem);   // [ng][pitch]
+  if (active)
+#pragma unroll
+    for (int u = 0; u < QPT; ++u)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = tq + u * g.tpg;
+        if (q < nq) xg[(size_t)grp * g.pitch + 4 * q + e] = xa[u][e];
+      }
+  __syncthreads();
+  for (int c = tid; c < g.ncol; c += nthr) {
+    long long t = 0;
+    for (int gi = 0; gi < g.ng; ++gi) t += xg[(size_t)gi * g.pitch + c];
+    if (t) atomicAdd(&x1[c], (unsigned long long)t);
+  }
+}
+
+// Fused pass geometry: the fit's, with the row groups padded to whole warps.
+StreamGeom margfit_geom(const DenseView& X, int64_t k0, int64_t nk, int RB, int* gx, int* threads) {
+  StreamGeom g{};
+  g.row0 = k0 * X.J;
+  g.nrows = nk * X.J;
+  g.pitch = (int)X.pitch;
+  g.ncol = (int)X.I;
+  const int nq = g.pitch / 4;
+  g.qpt = nq <= kST ? 1 : 2;
+  const int tpg = (nq + g.qpt - 1) / g.qpt;
+  g.tpg = (tpg + 31) & ~31;
+  const int tmax = g.qpt == 1 ? kST : kFitT2;
+  g.ng = tmax / g.tpg > 0 ? tmax / g.tpg : 1;
+  const int nthr = g.ng * g.tpg;
+  const int row_b = g.pitch * (int)sizeof(float);
+  const size_t bres_b = sizeof(float) * (size_t)X.J * RB;
+  g.bres = bres_b <= 48 * 1024;
+  g.tr = (96 * 1024) / row_b;
+  if (g.tr < 1) g.tr = 1;
+  if (!g.bres && g.tr * RB > kWPT * nthr) g.tr = kWPT * nthr / RB;
+  if (g.tr > 256) g.tr = 256;
+  const size_t extra = g.bres ? bres_b : sizeof(float) * 2 * (size_t)g.tr * RB;
+  const int ring_b = (int)(208 * 1024 - extra);
+  g.cw = g.pitch;
+  g.ns = ring_b / (g.tr * row_b);
+  if (g.ns > kMaxNS) g.ns = kMaxNS;
+  if (g.ns < 2) {
+    g.ns = 2;
+    g.tr = std::max(1, ring_b / (2 * row_b));
+  }
+  int64_t nx = kNumSMs;
+  if (nx > ceil_div(g.nrows, 2 * g.tr)) nx = ceil_div(g.nrows, 2 * g.tr);
+  if (nx < 1) nx = 1;
+  g.rows_per_cta = ceil_div(g.nrows, nx);
+  *gx = (int)ceil_div(g.nrows, g.rows_per_cta);
+  *threads = nthr;
+  return g;
+}
+
 }  // namespace
 
 size_t gram3_ws_doubles(int64_t I, int64_t J, int64_t K, int R) {
@@ -731,6 +1080,58 @@ __global__ void sum_pairs_kernel(const double* part, int nb, double* out2) {
   for (int i = 0; i < nb; ++i) { a += part[2 * i]; b += part[2 * i + 1]; }
   out2[0] = a;
   out2[1] = b;
+}
+
+// ---- a1 + lag-1 fit: one pass over slices [0, nk) ----------------------------------------------
+template <int RB, int MOI>
+static cudaError_t margfit_rb(const DenseView& X, int64_t nk, int S, const float* lam, const float* A,
+                              const float* B, const float* C, int R, const int32_t* kmap, int64_t* x1,
+                              int64_t* x2, int64_t* x3, double* ws, double* out2, cudaStream_t st) {
+  int gx, nt;
+  StreamGeom g = margfit_geom(X, 0, nk, RB, &gx, &nt);
+  const size_t extra = g.bres ? (size_t)X.J * RB : 2 * (size_t)g.tr * RB;
+  size_t smem = sizeof(float) * ((size_t)g.ns * g.tr * g.pitch + extra);
+  const size_t xg = sizeof(long long) * (size_t)g.ng * g.pitch;   // x1 combine reuses the region
+  if (smem < xg) smem = xg;
+  const float scf = ldexpf(1.0f, S < -126 ? -126 : (S > 127 ? 127 : S));
+  const double scd = ldexp(1.0, S);
+  auto* u1 = reinterpret_cast<unsigned long long*>(x1);
+  auto* u2 = reinterpret_cast<unsigned long long*>(x2);
+  auto* u3 = reinterpret_cast<unsigned long long*>(x3);
+  double* part = ws;
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<gx, nt, smem, st>>>(X.base, g, (int)X.J, R, scf, scd, lam, A, B, C, part, u1, u2, u3, kmap);
+  };
+  if (g.qpt == 1) {
+    if (g.bres) go(margfit_stream_kernel<MOI, RB, 1, true>);
+    else go(margfit_stream_kernel<MOI, RB, 1, false>);
+  } else {
+    if constexpr (RB <= 12) {
+      if (g.bres) go(margfit_stream_kernel<MOI, RB, 2, true>);
+      else go(margfit_stream_kernel<MOI, RB, 2, false>);
+    } else {
+      return cudaErrorInvalidValue;   // excluded by fit_stream_supported
+    }
+  }
+  sum_pairs_kernel<<<1, 32, 0, st>>>(part, gx, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, const float* lam,
+                                   const float* A, const float* B, const float* C, int R, const int32_t* kmap,
+                                   int64_t* x1, int64_t* x2, int64_t* x3, double* ws, double* out2,
+                                   cudaStream_t st) {
+  if (nk <= 0 || !fit_stream_supported(X, R)) return cudaErrorInvalidValue;
+#define SBT_MF(RBV)                                                                                       \
+  return moi == 0 ? margfit_rb<RBV, 0>(X, nk, S, lam, A, B, C, R, kmap, x1, x2, x3, ws, out2, st)         \
+                  : margfit_rb<RBV, 1>(X, nk, S, lam, A, B, C, R, kmap, x1, x2, x3, ws, out2, st)
+  if (R <= 4) { SBT_MF(4); }
+  if (R <= 8) { SBT_MF(8); }
+  if (R <= 10) { SBT_MF(10); }
+  if (R <= 12) { SBT_MF(12); }
+  SBT_MF(16);
+#undef SBT_MF
 }
 
 __global__ void fit_finish_kernel(const double* in2, const double* G, const float* lam, int R,
