@@ -56,6 +56,9 @@ def parse():
     p.add_argument("--no-variant", action="store_true", help="skip the incremental-marginals variant run")
     p.add_argument("--no-getrank", action="store_true", help="skip the GetRank timing (SURVEY 8(f) NEXT #2)")
     p.add_argument("--no-full-fit", action="store_true", help="return the summary fit only (R21)")
+    p.add_argument("--full-fit", type=int, default=2, choices=[1, 2],
+                   help="1: a7 pass after the merge; 2 (default): lag-1 fit inside the next update's a1 "
+                        "pass (SURVEY 8(f) NEXT #1; dense only, COO configs use 1)")
     p.add_argument("--sharded", action="store_true",
                    help="use the sharded (NCCL) handle even at N=1 (always used at N>1, dense configs)")
     return p.parse_args()
@@ -256,9 +259,12 @@ def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
         return out
     Kloc = k_local if k_local is not None else Ks
     IJ = w.I * w.J
-    out["a1"] = hbm_line("marg_stream_kernel", 1,
+    lag = all(inf.get("fit_full_prev", -1.0) != -1.0 for inf in infos)
+    out["a1"] = hbm_line("margfit_stream_kernel (a1 + lag-1 fit) + marg_stream_kernel (batch)" if lag
+                         else "marg_stream_kernel", 1,
                          statistics.mean(4.0 * IJ * kl for kl in Kloc) + 8.0 * (w.I + w.J + statistics.mean(Ks)))
-    out["a7"] = hbm_line("fit_stream_kernel", 7, statistics.mean(4.0 * IJ * kl for kl in Kloc))
+    if not lag:
+        out["a7"] = hbm_line("fit_stream_kernel", 7, statistics.mean(4.0 * IJ * kl for kl in Kloc))
     nI, nJ = -(-w.I // w.s), -(-w.J // w.s)
     Y = []
     for inf, kt in zip(infos, Ks):
@@ -552,7 +558,10 @@ def main():
     warm, tau = method_settings(w, args)
     config["accept_tau"] = tau
     config["als_init"] = "warm (model rows, R34)" if warm else "cold (Philox point, P:213)"
-    opts = L.default_opts(als_max_iters=w.maxit, als_tol=w.tol, capacity=work.cap, full_fit=int(not args.no_full_fit),
+    ff = 0 if args.no_full_fit else (args.full_fit if not work.coo else 1)
+    config["full_fit"] = {0: "none (summary fit only)", 1: "a7 pass after the merge",
+                          2: "lag-1: the previous model's fit inside this update's a1 pass (NEXT #1)"}[ff]
+    opts = L.default_opts(als_max_iters=w.maxit, als_tol=w.tol, capacity=work.cap, full_fit=ff,
                           accept_tau=tau, stream=stream.cuda_stream, warm_start=int(warm))
     if work.coo:
         opts.capacity_k = w.K
@@ -680,7 +689,8 @@ def main():
         "step_ms": step_share,
         "gpu_launches": int(sum(inf["kernel_launches"] for inf in infos)),
         "clocks": clocks,
-        "fit_full_last": infos[-1]["fit_full"],
+        "fit_full_last": infos[-1]["fit_full"] if infos[-1]["fit_full"] != -1.0 else infos[-1]["fit_full_prev"],
+        "fit_full_is_lag1": infos[-1]["fit_full"] == -1.0 and infos[-1]["fit_full_prev"] != -1.0,
         "fit_summary_last": infos[-1]["fit_summary"],
         "reps_rejected_last": bin(infos[-1]["reps_rejected_mask"]).count("1"),
     }
@@ -733,7 +743,8 @@ def main():
                 setattr(opts, k, v)
             kv = kernel_rooflines(w, work, vi, peaks, peak_kind, 1, None, args)
             return {"value": sum(ve) / (sum(vt) / 1000.0), "unit": unit, "ms_per_step": statistics.mean(vt),
-                    "steps": len(vt), "fit_full_last": vi[-1]["fit_full"], "kernels": kv,
+                    "steps": len(vt), "kernels": kv,
+                    "fit_full_last": vi[-1]["fit_full"] if vi[-1]["fit_full"] != -1.0 else vi[-1]["fit_full_prev"],
                     "reps_rejected_last": bin(vi[-1]["reps_rejected_mask"]).count("1"),
                     "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in vi) for k in range(8)},
                     "als_iters_mean": statistics.mean(inf["als_iters_sum"] / w.r for inf in vi),

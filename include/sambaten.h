@@ -76,7 +76,15 @@ typedef struct {
   int merge_policy;       /* 0 = update zero entries only (default); 1 = overwrite    */
                           /*     the sampled rows (R17)                              */
   double accept_tau;      /* rep acceptance threshold on min_f S(f, pi f) (R26); default 0.9 */
-  int full_fit;           /* 1: sambaten_update also computes the full relative error (a7)   */
+  int full_fit;           /* 1: sambaten_update also computes the full relative error of the   */
+                          /*    model it commits (a7: one extra pass over the tensor);          */
+                          /* 2: lag-1 fused fit: the relative error of the */
+                          /*    model the PREVIOUS update (or init) committed is computed inside  */
+                          /*    this update's marginal pass over the old slices, which reads the  */
+                          /*    same bytes (dense handles, full marginals, fit-stream shapes),    */
+                          /*    reported as info.fit_full_prev (info.fit_full = -1); where it     */
+                          /*    does not apply (incremental marginals, COO, unsupported shape)    */
+                          /*    it behaves as 1.  sambaten_relative_error gives the last model's. */
   int64_t capacity;       /* dense: total K slices to preallocate; COO: total nnz; 0 = 2x X0 */
   int64_t capacity_k;     /* COO: mode-3 rows of C to preallocate; 0 = 2 K0 + 1024          */
   int init_max_iters;     /* sambaten_init: ALS iterations on X0 (default 1000)       */
@@ -127,6 +135,9 @@ typedef struct {
   int64_t summary_entries;     /* entries (dense) or nonzeros (COO) of the summaries this      */
                                /* rank decomposed, summed over its repetitions (work units of  */
                                /* a3 / a4 for the rooflines)                                   */
+  double fit_full_prev;        /* full_fit = 2: 1 - ||X_prev - model_prev||/||X_prev|| of the    */
+                               /* model the previous update committed, over the tensor it was   */
+                               /* committed on (computed in this update's a1 pass); else -1     */
 } sambaten_info;
 
 /* Fill *opts with the defaults listed above. */

@@ -106,7 +106,7 @@ struct HostStatus {        // pinned; filled by one D2H copy at the end of an up
   int iters[kMaxReps];
   int flags[kMaxReps];
   double fit[kMaxReps];
-  double relerr;
+  double relerr, relerr_prev;
 };
 
 struct DistState;   // capi_dist.inc
@@ -118,6 +118,7 @@ struct sambaten_s {
   bool X_borrowed = false;   // opts.borrow_store: X is the caller's buffer
   int als_plan[4] = {-1, 0, 0, 0};   // the a4 plan of the last update (sambaten_info.als_plan)
   int64_t summ_entries = 0;          // summary entries / nnz of the update in flight (sambaten_info)
+  bool lag_now = false;              // this update computes the previous model's fit in a1 (full_fit = 2)
   cudaStream_t st2 = nullptr;     // side stream: host batch copy overlapped with a1 (old slices)
   cudaEvent_t ev_side[2] = {nullptr, nullptr};
   DevBuf xm, xm_ck;          // committed marginals of the current tensor (incremental a1)
@@ -183,6 +184,11 @@ static bool cluster_plan(sambaten_s* h, const DenseAls& a, ClusterPlan* pl) {
   *pl = e.pl;
   return e.ok;
 }
+
+// bound on the quantised values of the stored tensor: phi <= 2^(maxphi_log2 + 8) (R7: a batch
+// beyond it is rejected), so q = RNE(phi 2^S) <= 2^(maxphi_log2 + 8 + S) (x^2 measure: the
+// log of the squared bound)
+static int qbits(const sambaten_s* h) { return h->maxphi_log2 + 8 + h->S; }
 
 static void set_plan_report(sambaten_s* h, bool cluster, const ClusterPlan& pl, int R) {
   h->als_plan[0] = cluster ? 1 : 0;
@@ -673,7 +679,9 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
   CK(cudaMemcpyAsync(hs->iters, a.iters, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(hs->flags, a.flags, sizeof(int) * r, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(hs->fit, a.fit, sizeof(double) * r, cudaMemcpyDeviceToHost, st));
-  if (h->opts.full_fit) CK(cudaMemcpyAsync(&hs->relerr, d_relerr, 8, cudaMemcpyDeviceToHost, st));
+  const bool fit_now = h->opts.full_fit == 1 || (h->opts.full_fit == 2 && !h->lag_now);
+  if (fit_now) CK(cudaMemcpyAsync(&hs->relerr, d_relerr, 8, cudaMemcpyDeviceToHost, st));
+  if (h->lag_now) CK(cudaMemcpyAsync(&hs->relerr_prev, d_relerr + 4, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (d_vflags) vflags = hs->vflags;
   if (vflags & 1u) FAIL(SAMBATEN_E_INDEX_RANGE, "update: COO index out of range (S:77)");
@@ -705,7 +713,8 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
   h->last_n[0] = nI; h->last_n[1] = nJ; h->last_n[2] = nKs; h->last_nKp = nKp;
   if (info) {
     info->fit_summary = fsum / r;
-    info->fit_full = h->opts.full_fit ? 1.0 - hs->relerr : -1.0;
+    info->fit_full = fit_now ? 1.0 - hs->relerr : -1.0;
+    info->fit_full_prev = h->lag_now ? 1.0 - hs->relerr_prev : -1.0;
     info->als_iters_max = itmax;
     info->als_iters_sum = itsum;
     info->k_total = h->K;
@@ -1069,6 +1078,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     FAIL(SAMBATEN_E_SHAPE, "update: batch I x J differs from the state's (S:68)");
   h->als_plan[0] = -1; h->als_plan[1] = h->als_plan[2] = h->als_plan[3] = 0;   // set by the dense paths
   h->summ_entries = 0;
+  h->lag_now = false;
   if (h->dist)
     return h->fmt == SAMBATEN_COO ? update_coo_dist(h, batch, Aout, Bout, Cout, lamout, info)
                                   : update_dense_dist(h, batch, Aout, Bout, Cout, lamout, info);
@@ -1100,6 +1110,23 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   int64_t* x3 = x2 + h->J;
   const bool inc = h->opts.incremental_marginals && h->xm_valid;
   const bool dev_batch = is_device_ptr(batch->vals);
+  // full_fit = 2: the previous model's fit rides on the marginal pass over the old slices
+  DenseView Vold = V;
+  Vold.K = Ko;
+  const bool lag = h->opts.full_fit == 2 && !inc && Ko > 0 && fit_stream_supported(Vold, R);
+  h->lag_now = lag;
+  double* d_fit2 = reinterpret_cast<double*>(h->misc.as<char>() + 112);
+  double* d_relerr_prev = d_relerr + 4;
+  if (lag) CK(h->fitws.ensure(sizeof(double) * fit_ws_doubles_any(V)));
+  auto old_pass = [&]() -> cudaError_t {   // a1 over [0, Ko), with the lag-1 fit when asked
+    if (!lag) return marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, st);
+    cudaError_t e = launch_marg_fit_stream(Vold, Ko, h->opts.moi, h->S, qbits(h), h->lam(h->cur), h->A(h->cur),
+                                           h->B(h->cur), h->C(h->cur), R, nullptr, x1, x2, x3,
+                                           h->fitws.as<double>(), d_fit2, st);
+    if (e != cudaSuccess) return e;
+    return launch_fit_finish(d_fit2, h->lam(h->cur), h->A(h->cur), h->B(h->cur), h->C(h->cur), h->I, h->J, Ko,
+                             R, h->fitws.as<double>(), d_relerr_prev, st);
+  };
   // A host batch crosses PCIe on a side stream while a1 reads the old slices (they do not
   // depend on it); the batch's own marginals follow once it has landed.
   const bool overlap = !dev_batch && !inc && Ko > 0;
@@ -1115,7 +1142,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
                         h->I * sizeof(float), h->J * Kn, h->st2));
     CK(cudaEventRecord(h->ev_side[1], h->st2));
     CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
-    CK(marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, st));   // a1, old slices
+    CK(old_pass());   // a1, old slices (+ the previous model's fit)
     CK(cudaStreamWaitEvent(st, h->ev_side[1], 0));
     CK(launch_max_phi_dense(V, Ko, Kn, h->opts.moi, d_maxphi, st));
   } else if (h->pitch == h->I && nb_fl % 4 == 0 && dev_batch &&
@@ -1137,6 +1164,10 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, st));
     CK(cudaMemsetAsync(x3 + Ko, 0, sizeof(int64_t) * (h->Kcap - Ko), st));
     CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, st));
+  } else if (lag) {
+    CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
+    CK(old_pass());
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, st));   // the batch's slices
   } else {
     CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
     CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, st));
@@ -1231,8 +1262,9 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   int* accepted = nullptr;
   CK(run_match_merge(h, a, Is, Js, Kp, locI, locJ, locK, Ko, Kn, nI, nJ, nKs, nKp, &accepted, d_rnew));
   CK(cudaEventRecord(h->ev[7], st));
-  // ---- a7: full fit of the new model (optional) ------------------------------------------
-  if (h->opts.full_fit) {
+  // ---- a7: full fit of the new model (optional; with full_fit = 2 it rides on the next a1) --
+  const bool fit_now = h->opts.full_fit == 1 || (h->opts.full_fit == 2 && !lag);
+  if (fit_now) {
     // separate workspace: reallocating misc here would lose the max-phi word written in a0
     const size_t need = sizeof(double) * fit_ws_doubles_any(V);
     CK(h->fitws.ensure(need));
@@ -1240,9 +1272,10 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   }
   CK(cudaEventRecord(h->ev[8], st));
   // a0 ingest or max_phi (+ the old-slice marginal pass when a host batch overlaps its copy),
-  // a1 marginals, a2 sample, a3 gather, a4 ALS, a5 match partial + match, a6 merge, a7 fit +
-  // two Gram kernels + combine
-  const int launches = 1 + (overlap ? 1 : 0) + 1 + 1 + 1 + als_launches + 2 + 1 + (h->opts.full_fit ? 4 : 0);
+  // a1 marginals (lag: fused pass + pair sum + 2 Gram kernels + finish, then the batch's
+  // marginals), a2 sample, a3 gather, a4 ALS, a5 match partial + match, a6 merge, a7 fit + two
+  // Gram kernels + combine
+  const int launches = 1 + (overlap ? 1 : 0) + 1 + (lag ? 5 : 0) + 1 + 1 + als_launches + 2 + 1 + (fit_now ? 4 : 0);
   return finish_update(h, a, accepted, d_maxphi, nullptr, d_relerr, Ko, Kn, nI, nJ, nKs, nKp, b, nb,
                        launches, 0, Aout, Bout, Cout, lamout, info);
 }

@@ -301,7 +301,8 @@ size_t fit_stream_ws_doubles(const DenseView& X);
 // slices (SURVEY 8(f) NEXT #1 lag-1 fit): x1/x2/x3 accumulate (zero them first); out2 =
 // {<X, M>, ||X||^2} of those slices (finish with launch_fit_finish); kmap: local slice -> model
 // row (sharded stores) or NULL; ws: fit_stream_ws_doubles; needs fit_stream_supported(X, R)
-cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, const float* lam,
+// qb: every quantised value q = RNE(phi 2^S) of the pass is <= 2^qb (32-bit arithmetic when small)
+cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, int qb, const float* lam,
                                    const float* A, const float* B, const float* C, int R, const int32_t* kmap,
                                    int64_t* x1, int64_t* x2, int64_t* x3, double* ws, double* out2,
                                    cudaStream_t st);

@@ -9,6 +9,7 @@
 // thread), so each SM keeps ~100-190 KB of loads in flight with no register cost (a plain
 // ring read of this kind measured 5.7 TB/s on the B200, tools/micro/bw.cu).
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "internal.h"
@@ -640,12 +641,37 @@ StreamGeom fit_geom(const DenseView& X, int RB, int* gx, int* gy, int* threads) 
 // -> one global atomic per row and warp (x2) and a per-warp running sum per slice (x3), as
 // marg_stream_kernel.  Integer marginals: bit-identical to the separate pass.
 // ---------------------------------------------------------------------------------------
-template <int MOI, int RB, int QPT, bool BRES>
+// Exact warp sum of non-negative 64-bit values by 21-bit chunks through the warp-reduce unit
+// (REDUX: one instruction per chunk, no shuffle tree): each chunk's 32-lane sum is < 2^26.
+// NCH = 2 covers values < 2^42, NCH = 3 values < 2^63.
+template <int NCH>
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+  unsigned long long t = 0;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const unsigned part = (unsigned)(v >> (21 * c)) & 0x1FFFFFu;
+    t += (unsigned long long)__reduce_add_sync(0xffffffffu, part) << (21 * c);
+  }
+  return t;
+}
+
+template <int MOI>
+__device__ __forceinline__ unsigned quant32(float x, float scf, double scd) {
+  if (MOI == 0) return (unsigned)__float2uint_rn(fabsf(x) * scf);   // exact product; q < 2^31 (Q32 plan)
+  const double d = (double)x;
+  return (unsigned)__double2ull_rn(__dmul_rn(__dmul_rn(d, d), scd));
+}
+
+template <int MOI, int RB, int QPT, bool BRES, bool Q32>
 __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_kernel(
     const float* __restrict__ X, StreamGeom g, int J, int R, float scf, double scd,
     const float* __restrict__ lam, const float* __restrict__ A, const float* __restrict__ B,
     const float* __restrict__ C, double* __restrict__ part, unsigned long long* __restrict__ x1,
     unsigned long long* __restrict__ x2, unsigned long long* __restrict__ x3, const int32_t* __restrict__ kmap) {
+  // Q32 (plan-time guarantee: q <= 2^qb with qb small enough): 32-bit quantised values, row
+  // partials and per-stage column sums (folded into the 64-bit column sums at stage ends);
+  // else 64-bit throughout.  The warp's row total goes through warp_sum_u64 either way.
+  using qint = typename std::conditional<Q32, unsigned, unsigned long long>::type;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned long long bars[kMaxNS];
   __shared__ double red[32];
@@ -699,32 +725,44 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
   if (tid == 0)
     for (int s = 0; s < nst && s < g.ns; ++s) marg_issue(ring, bars, g, X, rb, re, s);
   double inner = 0.0, sq = 0.0;
-  long long xa[QPT][4];   // x1 column sums of the thread's quads
+  unsigned long long xa[QPT][4];   // x1 column sums of the thread's quads
+  qint xs[QPT][4];                 // this stage's column sums (Q32: folded into xa per stage)
 #pragma unroll
   for (int u = 0; u < QPT; ++u)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) xa[u][e] = 0;
-  long long x3run = 0;    // lane 0: the warp's running x3 sum of slice x3k
+    for (int e = 0; e < 4; ++e) { xa[u][e] = 0; xs[u][e] = 0; }
+  unsigned long long x3run = 0;    // lane 0: the warp's running x3 sum of slice x3k
   int64_t x3k = -1;
-  // the warp's row total: butterfly, then lane 0 adds it to x2[j] and to the running x3 sum
-  auto row_done = [&](long long rs, int j, int64_t k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+  // the warp's row total (exact): lane 0 adds it to x2[j] and to the running x3 sum
+  auto row_done = [&](qint rs, int j, int64_t k) {
+    const unsigned long long t = Q32 ? warp_sum_u64<2>(rs) : warp_sum_u64<3>(rs);
     if (lane == 0) {
-      if (rs) atomicAdd(&x2[j], (unsigned long long)rs);
+      if (t) atomicAdd(&x2[j], t);
       if (k != x3k) {
-        if (x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
+        if (x3run) atomicAdd(&x3[x3k], x3run);
         x3k = k;
         x3run = 0;
       }
-      x3run += rs;
+      x3run += t;
     }
   };
-  auto quad_marg = [&](const float4& v, long long (&xq)[4]) -> long long {
-    const long long q0 = quant<MOI>(v.x, scf, scd), q1 = quant<MOI>(v.y, scf, scd);
-    const long long q2 = quant<MOI>(v.z, scf, scd), q3 = quant<MOI>(v.w, scf, scd);
+  auto quad_marg = [&](const float4& v, qint (&xq)[4]) -> qint {
+    qint q0, q1, q2, q3;
+    if constexpr (Q32) {
+      q0 = quant32<MOI>(v.x, scf, scd); q1 = quant32<MOI>(v.y, scf, scd);
+      q2 = quant32<MOI>(v.z, scf, scd); q3 = quant32<MOI>(v.w, scf, scd);
+    } else {
+      q0 = (qint)quant<MOI>(v.x, scf, scd); q1 = (qint)quant<MOI>(v.y, scf, scd);
+      q2 = (qint)quant<MOI>(v.z, scf, scd); q3 = (qint)quant<MOI>(v.w, scf, scd);
+    }
     xq[0] += q0; xq[1] += q1; xq[2] += q2; xq[3] += q3;
     return (q0 + q1) + (q2 + q3);   // padding columns are zero in the store: q = 0
+  };
+  auto fold_x1 = [&]() {   // stage-end fold of the stage's column sums
+#pragma unroll
+    for (int u = 0; u < QPT; ++u)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) { xa[u][e] += xs[u][e]; xs[u][e] = 0; }
   };
   auto wrow = [&](const float* wr, float (&w)[RB]) {
     if constexpr (RB % 4 == 0) {
@@ -793,7 +831,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
 #pragma unroll 1
           for (int r = ra + ((grp - ra) % g.ng + g.ng) % g.ng; r < ra + seg; r += g.ng) {
             const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
-            long long rs = 0;
+            qint rs = 0;
             if (qok) {
               float w[RB];
               wrow(wr, w);
@@ -806,7 +844,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
                 acc[3][f] = fmaf(v.w, w[f], acc[3][f]);
               }
               fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
-              rs = quad_marg(v, xa[0]);
+              rs = quad_marg(v, xs[0]);
             }
             row_done(rs, j + r - ra, k);
             ++run;
@@ -817,6 +855,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
         }
         if (run >= kFoldRows) fold(kc);
         sq += (double)fs;
+        fold_x1();
       }
       if (!BRES && s + 1 < nst) store_w(s + 1);
       __syncthreads();
@@ -873,7 +912,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
             const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
             float w[RB];
             wrow(wr, w);
-            long long rs = 0;
+            qint rs = 0;
 #pragma unroll
             for (int u = 0; u < QPT; ++u) {
               const int q = tq + u * g.tpg;
@@ -889,7 +928,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
                 }
                 fi = fmaf(v.x, m0, fmaf(v.y, m1, fmaf(v.z, m2, fmaf(v.w, m3, fi))));
                 fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
-                rs += quad_marg(v, xa[u]);
+                rs += quad_marg(v, xs[u]);
               }
             }
             row_done(rs, j + r - ra, k);
@@ -900,6 +939,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
         }
         inner += (double)fi;
         sq += (double)fs;
+        fold_x1();
       }
       if (!BRES && s + 1 < nst) store_w(s + 1);
       __syncthreads();
@@ -911,7 +951,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
       js = jn;
     }
   }
-  if (lane == 0 && x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
+  if (lane == 0 && x3run) atomicAdd(&x3[x3k], x3run);
   inner = block_sum_d(inner, red);
   sq = block_sum_d(sq, red);
   if (tid == 0) {
@@ -920,7 +960,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
   }
   // x1: the groups' column sums through the (idle) ring, summed per column in group order
   __syncthreads();
-  long long* xg = reinterpret_cast<long long*>(smem);   // [ng][pitch]
+  unsigned long long* xg = reinterpret_cast<unsigned long long*>(smem);   // [ng][pitch]
   if (active)
 #pragma unroll
     for (int u = 0; u < QPT; ++u)
@@ -931,9 +971,9 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
       }
   __syncthreads();
   for (int c = tid; c < g.ncol; c += nthr) {
-    long long t = 0;
+    unsigned long long t = 0;
     for (int gi = 0; gi < g.ng; ++gi) t += xg[(size_t)gi * g.pitch + c];
-    if (t) atomicAdd(&x1[c], (unsigned long long)t);
+    if (t) atomicAdd(&x1[c], t);
   }
 }
 
@@ -1084,7 +1124,7 @@ __global__ void sum_pairs_kernel(const double* part, int nb, double* out2) {
 
 // ---- a1 + lag-1 fit: one pass over slices [0, nk) ----------------------------------------------
 template <int RB, int MOI>
-static cudaError_t margfit_rb(const DenseView& X, int64_t nk, int S, const float* lam, const float* A,
+static cudaError_t margfit_rb(const DenseView& X, int64_t nk, int S, int qb, const float* lam, const float* A,
                               const float* B, const float* C, int R, const int32_t* kmap, int64_t* x1,
                               int64_t* x2, int64_t* x3, double* ws, double* out2, cudaStream_t st) {
   int gx, nt;
@@ -1103,13 +1143,18 @@ static cudaError_t margfit_rb(const DenseView& X, int64_t nk, int S, const float
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<gx, nt, smem, st>>>(X.base, g, (int)X.J, R, scf, scd, lam, A, B, C, part, u1, u2, u3, kmap);
   };
+  // 32-bit marginal arithmetic when every q <= 2^qb keeps a lane's row partial (4 QPT values)
+  // and its per-stage column sums (<= ceil(tr / ng) rows) below 2^32
+  int rows_bits = 0;
+  while ((1 << rows_bits) < (g.tr + g.ng - 1) / g.ng) ++rows_bits;
+  const bool q32 = qb + std::max(g.qpt == 2 ? 3 : 2, rows_bits) <= 31 && (MOI == 0 || qb <= 31);
   if (g.qpt == 1) {
-    if (g.bres) go(margfit_stream_kernel<MOI, RB, 1, true>);
-    else go(margfit_stream_kernel<MOI, RB, 1, false>);
+    if (q32) { if (g.bres) go(margfit_stream_kernel<MOI, RB, 1, true, true>); else go(margfit_stream_kernel<MOI, RB, 1, false, true>); }
+    else { if (g.bres) go(margfit_stream_kernel<MOI, RB, 1, true, false>); else go(margfit_stream_kernel<MOI, RB, 1, false, false>); }
   } else {
     if constexpr (RB <= 12) {
-      if (g.bres) go(margfit_stream_kernel<MOI, RB, 2, true>);
-      else go(margfit_stream_kernel<MOI, RB, 2, false>);
+      if (q32) { if (g.bres) go(margfit_stream_kernel<MOI, RB, 2, true, true>); else go(margfit_stream_kernel<MOI, RB, 2, false, true>); }
+      else { if (g.bres) go(margfit_stream_kernel<MOI, RB, 2, true, false>); else go(margfit_stream_kernel<MOI, RB, 2, false, false>); }
     } else {
       return cudaErrorInvalidValue;   // excluded by fit_stream_supported
     }
@@ -1118,14 +1163,14 @@ static cudaError_t margfit_rb(const DenseView& X, int64_t nk, int S, const float
   return cudaGetLastError();
 }
 
-cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, const float* lam,
+cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, int qb, const float* lam,
                                    const float* A, const float* B, const float* C, int R, const int32_t* kmap,
                                    int64_t* x1, int64_t* x2, int64_t* x3, double* ws, double* out2,
                                    cudaStream_t st) {
   if (nk <= 0 || !fit_stream_supported(X, R)) return cudaErrorInvalidValue;
 #define SBT_MF(RBV)                                                                                       \
-  return moi == 0 ? margfit_rb<RBV, 0>(X, nk, S, lam, A, B, C, R, kmap, x1, x2, x3, ws, out2, st)         \
-                  : margfit_rb<RBV, 1>(X, nk, S, lam, A, B, C, R, kmap, x1, x2, x3, ws, out2, st)
+  return moi == 0 ? margfit_rb<RBV, 0>(X, nk, S, qb, lam, A, B, C, R, kmap, x1, x2, x3, ws, out2, st)     \
+                  : margfit_rb<RBV, 1>(X, nk, S, qb, lam, A, B, C, R, kmap, x1, x2, x3, ws, out2, st)
   if (R <= 4) { SBT_MF(4); }
   if (R <= 8) { SBT_MF(8); }
   if (R <= 10) { SBT_MF(10); }

@@ -22,7 +22,9 @@ I, J, K, R, K0, bs = 64, 48, 40, 4, 30, 5
 T, truth = planted_dense(I, J, K, R, noise=0.01, seed=3)
 T0, batches = split_dense(T, K0, bs)
 model = [np.ascontiguousarray(np.asarray(x, np.float32)) for x in (truth[0], truth[1], truth[2], truth[3][:K0])]
-opts = L.default_opts(als_max_iters=15, als_tol=0.0, capacity=K, full_fit=1)
+import os
+opts = L.default_opts(als_max_iters=15, als_tol=0.0, capacity=K, full_fit=int(os.environ.get("SBT_T_FF", "1")),
+                      warm_start=int(os.environ.get("SBT_T_WARM", "0")))
 dist = L.make_dist(0, 1, L.sambaten_dist_unique_id(), 0, K0)
 hd = L.sambaten_init_factors_dist(L.dense(torch.from_numpy(T0).cuda()), dist, R, 2, 4, 9,
                                   model[1], model[2], model[3], model[0], opts)
@@ -37,21 +39,27 @@ for b in batches:
         A = np.empty((I, R), np.float32); B = np.empty((J, R), np.float32)
         C = np.empty((Kt, R), np.float32); lam = np.empty(R, np.float32)
         info = L.sambaten_update(h, L.dense(torch.from_numpy(b).cuda()), A, B, C, lam)
-        out.append((A, B, C, lam, info.fit_full, info.reps_rejected_mask))
+        out.append((A, B, C, lam, info.fit_full, info.reps_rejected_mask, info.fit_full_prev))
     for x, y in zip(out[0][:4], out[1][:4]):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
-    assert out[0][4] == out[1][4] and out[0][5] == out[1][5]
+    assert out[0][4] == out[1][4] and out[0][5] == out[1][5] and out[0][6] == out[1][6], (out[0][4:], out[1][4:])
+    if opts.full_fit == 2:
+        assert out[0][4] == -1.0 and 0.9 < out[0][6] <= 1.0
 L.sambaten_destroy(hd); L.sambaten_destroy(hs)
 print("DIST_OK")
 '''
 
 
-@pytest.mark.parametrize("loopback", [False, True])
-def test_world1_dist_handle_matches_single_gpu_bitwise(loopback):
+@pytest.mark.parametrize("loopback,ff,warm", [(False, 1, 0), (True, 1, 0), (False, 2, 0), (True, 2, 1)])
+def test_world1_dist_handle_matches_single_gpu_bitwise(loopback, ff, warm):
+    """full_fit = 2 (lag-1 fit in the a1 pass, SURVEY 8(f) NEXT #1) and the warm start (R34)
+    on the sharded handle: bit-identical to the single-GPU handle with the same options."""
     env = dict(os.environ)
     env.pop("SAMBATEN_DIST_LOOPBACK", None)
     if loopback:
         env["SAMBATEN_DIST_LOOPBACK"] = "1"
+    env["SBT_T_FF"] = str(ff)
+    env["SBT_T_WARM"] = str(warm)
     r = subprocess.run([sys.executable, "-c", "ROOT = %r\n" % ROOT + SCRIPT], env=env, capture_output=True,
                        text=True, timeout=600)
     assert "DIST_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]

@@ -88,13 +88,22 @@ def test_c4_full_size_marginals_sampling_gather():
     batch = store[w.K0:Kt].clone()
     model = [np.ones(w.R, np.float32), A.astype(np.float32), B.astype(np.float32),
              np.ascontiguousarray(Cf[:w.K0].astype(np.float32))]
-    opts = L().default_opts(als_max_iters=2, als_tol=0.0, capacity=Kt, full_fit=0, accept_tau=0.0,
+    # full_fit = 2: the bench's launch configuration -- the marginals of the old slices come from
+    # the fused marginal + lag-1 fit kernel (32-bit arithmetic at this scale, q <= 2^27)
+    opts = L().default_opts(als_max_iters=2, als_tol=0.0, capacity=Kt, full_fit=2, accept_tau=0.0,
                             borrow_store=1)
     h = L().sambaten_init_factors(L().dense(store[:w.K0]), w.R, w.s, w.r, w.seed, model[1], model[2],
                                   model[3], model[0], opts)
     try:
         info = L().sambaten_update(h, L().dense(batch))
         del batch
+        # the lag-1 fit (the initial model over X0) equals the separate fit kernel's value
+        rel = torch.zeros(1, dtype=torch.float64, device="cuda")
+        dm = [dev(v) for v in model]
+        L().sambaten_fit(L().dense(store[:w.K0]), dm[0], dm[1], dm[2], dm[3], w.R, rel)
+        torch.cuda.synchronize()
+        assert info.fit_full == -1.0
+        assert abs(info.fit_full_prev - (1.0 - float(rel[0]))) <= 1e-6, (info.fit_full_prev, 1.0 - float(rel[0]))
         x = [torch.zeros(n, dtype=torch.int64, device="cuda") for n in (w.I, w.J, Kt)]
         mx = max(float(store[k0:min(k0 + 100, w.K0)].abs().max()) for k0 in range(0, w.K0, 100))
         S = O.fixed_point_scale(w.I * w.J * Kt, mx)
