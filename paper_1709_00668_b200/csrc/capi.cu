@@ -1113,7 +1113,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   // full_fit = 2: the previous model's fit rides on the marginal pass over the old slices
   DenseView Vold = V;
   Vold.K = Ko;
-  const bool lag = h->opts.full_fit == 2 && !inc && Ko > 0 && fit_stream_supported(Vold, R);
+  const bool lag = h->opts.full_fit == 2 && !inc && Ko > 0 && margfit_supported(Vold, R);
   h->lag_now = lag;
   double* d_fit2 = reinterpret_cast<double*>(h->misc.as<char>() + 112);
   double* d_relerr_prev = d_relerr + 4;

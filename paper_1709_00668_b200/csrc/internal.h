@@ -106,6 +106,25 @@ cudaError_t run_als_cluster(const DenseAls& a, const ClusterPlan& pl, float* Dgl
 cudaError_t launch_sumsq_dense(const float* Y, int64_t y_stride, int64_t rows, int64_t pitch,
                                int64_t ncols, int r, double* out, cudaStream_t st);
 cudaError_t run_dense_als(const DenseAls& a, cudaStream_t st);
+// Collectives the sharded full-tensor ALS needs (capi_dist.inc binds them to NCCL; a world-1
+// handle to plain copies): in-place sum all-reduce and an all-gather of n doubles per rank.
+struct AlsComm {
+  void* ctx;
+  cudaError_t (*sum_d)(void* ctx, double* buf, size_t n, cudaStream_t st);
+  cudaError_t (*gather_d)(void* ctx, const double* send, double* recv, size_t n, cudaStream_t st);
+  int world;
+};
+// Full-tensor CP-ALS over a time-sharded store.  loc: this rank's slab
+// (r = 1, nK = local slices, workspace of dense_als_workspace; U[0] = glob.U[0], U[1] =
+// glob.U[1], U[2] = a local buffer of the slab's C rows), glob: the replicated factors (nK =
+// global slices; dense_als_small_bind; factors initialised, Grams and ysq (all-reduced) set);
+// kmap: local -> global slice (device, loc.nK); gidx: [world][kpad] global slice of every
+// rank's padded row (or -1); stage: kpad * R doubles; gathered: world * kpad * R doubles.
+cudaError_t run_dense_als_sharded(const DenseAls& loc, const DenseAls& glob, const int32_t* kmap,
+                                  const int32_t* gidx, int kpad, double* stage, double* gathered,
+                                  const AlsComm& c, cudaStream_t st);
+size_t dense_als_small_workspace(const DenseAls& a);
+void dense_als_small_bind(DenseAls* a, void* ws);
 // single-mode MTTKRP for the stateless API (r = 1): M (fp32 [n_mode][R])
 cudaError_t dense_mttkrp_single(const DenseAls& a, int mode, float* M, cudaStream_t st);
 
@@ -301,6 +320,7 @@ size_t fit_stream_ws_doubles(const DenseView& X);
 // slices (SURVEY 8(f) NEXT #1 lag-1 fit): x1/x2/x3 accumulate (zero them first); out2 =
 // {<X, M>, ||X||^2} of those slices (finish with launch_fit_finish); kmap: local slice -> model
 // row (sharded stores) or NULL; ws: fit_stream_ws_doubles; needs fit_stream_supported(X, R)
+bool margfit_supported(const DenseView& X, int R);
 // qb: every quantised value q = RNE(phi 2^S) of the pass is <= 2^qb (32-bit arithmetic when small)
 cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, int qb, const float* lam,
                                    const float* A, const float* B, const float* C, int R, const int32_t* kmap,

@@ -597,4 +597,136 @@ cudaError_t dense_mttkrp_single(const DenseAls& a, int mode, float* M, cudaStrea
   return mttkrp_single_rb<32>(a, mode, M, st);
 }
 
+// ---------------------------------------------------------------------------------------
+// Full-tensor CP-ALS over a time-sharded store: every rank streams its
+// slab with the kernels above (r = 1); the mode-0 and mode-1 MTTKRPs are sums over slices, so
+// their slab partials are all-reduced and every rank solves the replicated A, B; the mode-2
+// MTTKRP rows belong to the rank holding the slice: they are all-gathered and scattered to
+// their global rows, and every rank solves the replicated C.  Integer-free but deterministic:
+// the all-reduce gives every rank the same bits, so the factors stay identical everywhere.
+// ---------------------------------------------------------------------------------------
+__global__ void reduce_part0_d_kernel(DenseAls a, double* M) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = (int64_t)a.nI * a.R;
+  if (idx >= tot || a.done[0]) return;
+  double s = 0.0;
+  for (int b = 0; b < a.nb0; ++b) s += a.part0[(int64_t)b * tot + idx];   // block order, as solve_kernel
+  M[idx] = s;
+}
+// rows of the replicated C held by this rank (kmap: local slice -> global slice)
+__global__ void gather_rows_kernel(const float* C, const int32_t* kmap, int64_t nloc, int R, float* Cl) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nloc * R) return;
+  const int64_t t = e / R;
+  Cl[e] = C[(int64_t)kmap[t] * R + (e - t * R)];
+}
+// all-gathered mode-2 rows [world][kpad][R] -> their global rows of M (gidx: global slice or -1)
+__global__ void scatter_rows_kernel(const double* in, const int32_t* gidx, int64_t n, int R, double* M,
+                                    const int* done) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * R || done[0]) return;
+  const int64_t t = e / R;
+  const int g = gidx[t];
+  if (g >= 0) M[(int64_t)g * R + (e - t * R)] = in[e];
+}
+
+template <int RB>
+static cudaError_t als_sharded_rb(DenseAls loc, DenseAls glob, const int32_t* kmap, const int32_t* gidx,
+                                  int kpad, double* stage, double* gathered, const AlsComm& c, cudaStream_t st) {
+  const int R = glob.R;
+  const int64_t nloc = loc.nK;
+  // loc reads the replicated A, B and its own rows of C; its flags / done are glob's
+  loc.done = glob.done; loc.flags = glob.flags;
+  int cw, nz, RP;
+  col_chunking(loc.nI, &cw, &nz, &RP);
+  const int threads0 = ((RP * cw + 31) / 32) * 32;
+  constexpr int NW = DpassCfg<RB>::NW;
+  DenseAls loc2 = loc;   // mode-2 rows into the staging buffer
+  loc2.M = stage;
+  DenseAls g0 = glob;    // mode-0 solve reads M through part0 with one "block"
+  g0.part0 = glob.M; g0.nb0 = 1;
+  auto refresh_cloc = [&]() {
+    if (nloc > 0)
+      gather_rows_kernel<<<(unsigned)ceil_div(nloc * R, 256), 256, 0, st>>>(glob.U[2], kmap, nloc, R, loc.U[2]);
+  };
+  refresh_cloc();
+  for (int it = 0; it < glob.maxit; ++it) {
+    // mode 0: slab partials -> all-reduce -> replicated solve
+    if (nloc > 0) {
+      mttkrp0_kernel<RB><<<dim3(loc.nb0, 1, nz), threads0, 0, st>>>(loc, cw, RP);
+      reduce_part0_d_kernel<<<(unsigned)ceil_div((int64_t)loc.nI * R, 256), 256, 0, st>>>(loc, glob.M);
+    } else {
+      cudaMemsetAsync(glob.M, 0, sizeof(double) * loc.nI * R, st);
+    }
+    cudaError_t e = c.sum_d(c.ctx, glob.M, (size_t)glob.nI * R, st);
+    if (e != cudaSuccess) return e;
+    solve_kernel<RB><<<1, kAlsThreads, 0, st>>>(g0, 0);
+    // mode 1: D of the slab, M_1 partial -> all-reduce -> replicated solve
+    if (nloc > 0) {
+      const int64_t nrows = nloc * loc.nJ;
+      dpass_kernel<RB><<<dim3((unsigned)ceil_div(nrows, 32 * NW), 1), 32 * NW, 0, st>>>(loc);
+      m1_kernel<<<dim3((unsigned)ceil_div((int64_t)loc.nJ * R, 256), 1), 256, 0, st>>>(loc);
+    } else {
+      cudaMemsetAsync(glob.M, 0, sizeof(double) * loc.nJ * R, st);
+    }
+    e = c.sum_d(c.ctx, glob.M, (size_t)glob.nJ * R, st);
+    if (e != cudaSuccess) return e;
+    solve_kernel<RB><<<1, kAlsThreads, 0, st>>>(glob, 1);
+    // mode 2: the slab's rows -> all-gather -> global rows -> replicated solve
+    cudaMemsetAsync(stage, 0, sizeof(double) * (size_t)kpad * R, st);
+    if (nloc > 0) m2_kernel<<<dim3((unsigned)nloc, 1), 32 * R, 0, st>>>(loc2);
+    e = c.gather_d(c.ctx, stage, gathered, (size_t)kpad * R, st);
+    if (e != cudaSuccess) return e;
+    const int64_t ng = (int64_t)c.world * kpad;
+    scatter_rows_kernel<<<(unsigned)ceil_div(ng * R, 256), 256, 0, st>>>(gathered, gidx, ng, R, glob.M, glob.done);
+    solve_kernel<RB><<<1, kAlsThreads, 0, st>>>(glob, 2);
+    refresh_cloc();
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t run_dense_als_sharded(const DenseAls& loc, const DenseAls& glob, const int32_t* kmap,
+                                  const int32_t* gidx, int kpad, double* stage, double* gathered,
+                                  const AlsComm& c, cudaStream_t st) {
+  if (glob.R <= 4) return als_sharded_rb<4>(loc, glob, kmap, gidx, kpad, stage, gathered, c, st);
+  if (glob.R <= 8) return als_sharded_rb<8>(loc, glob, kmap, gidx, kpad, stage, gathered, c, st);
+  if (glob.R <= 10) return als_sharded_rb<10>(loc, glob, kmap, gidx, kpad, stage, gathered, c, st);
+  if (glob.R <= 12) return als_sharded_rb<12>(loc, glob, kmap, gidx, kpad, stage, gathered, c, st);
+  if (glob.R <= 16) return als_sharded_rb<16>(loc, glob, kmap, gidx, kpad, stage, gathered, c, st);
+  if (glob.R <= 24) return als_sharded_rb<24>(loc, glob, kmap, gidx, kpad, stage, gathered, c, st);
+  return als_sharded_rb<32>(loc, glob, kmap, gidx, kpad, stage, gathered, c, st);
+}
+
+// the replicated factors' small state (no D / part0): G, lam, ysq, fit, fit_prev, iters, done,
+// flags, M and Uscr sized for max(nI, nJ, nK) rows
+size_t dense_als_small_workspace(const DenseAls& a) {
+  const int64_t maxn = (int64_t)max(a.nI, max(a.nJ, a.nK));
+  const int R = a.R;
+  size_t b = 0;
+  auto add = [&](size_t bytes) { b += (bytes + 255) & ~(size_t)255; };
+  add(sizeof(double) * 3 * R * R); add(sizeof(double) * R); add(sizeof(double) * (1 + 256));
+  add(sizeof(double)); add(sizeof(double)); add(sizeof(int)); add(sizeof(int)); add(sizeof(int));
+  add(sizeof(double) * maxn * R); add(sizeof(double) * maxn * R);
+  return b;
+}
+
+void dense_als_small_bind(DenseAls* a, void* ws) {
+  char* p = static_cast<char*>(ws);
+  const int R = a->R;
+  const int64_t maxn = (int64_t)max(a->nI, max(a->nJ, a->nK));
+  auto take = [&](size_t bytes) { char* q = p; p += (bytes + 255) & ~(size_t)255; return q; };
+  a->G = (double*)take(sizeof(double) * 3 * R * R);
+  a->lam = (double*)take(sizeof(double) * R);
+  a->ysq = (double*)take(sizeof(double) * (1 + 256));
+  a->fit = (double*)take(sizeof(double));
+  a->fit_prev = (double*)take(sizeof(double));
+  a->iters = (int*)take(sizeof(int));
+  a->done = (int*)take(sizeof(int));
+  a->flags = (int*)take(sizeof(int));
+  a->m_stride = maxn * R;
+  a->M = (double*)take(sizeof(double) * maxn * R);
+  a->Uscr = (double*)take(sizeof(double) * maxn * R);
+  a->part0 = nullptr; a->nb0 = 0; a->D = nullptr;
+}
+
 }  // namespace sbt

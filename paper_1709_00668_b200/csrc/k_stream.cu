@@ -662,15 +662,23 @@ __device__ __forceinline__ unsigned quant32(float x, float scf, double scd) {
   return (unsigned)__double2ull_rn(__dmul_rn(__dmul_rn(d, d), scd));
 }
 
+// Exact warp sum of values < 2^31 (two 16-bit halves through REDUX; each half-sum < 2^21).
+__device__ __forceinline__ unsigned long long warp_sum_u31(unsigned v) {
+  const unsigned lo = __reduce_add_sync(0xffffffffu, v & 0xFFFFu);
+  const unsigned hi = __reduce_add_sync(0xffffffffu, v >> 16);
+  return ((unsigned long long)hi << 16) + lo;
+}
+
 template <int MOI, int RB, int QPT, bool BRES, bool Q32>
 __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_kernel(
     const float* __restrict__ X, StreamGeom g, int J, int R, float scf, double scd,
     const float* __restrict__ lam, const float* __restrict__ A, const float* __restrict__ B,
     const float* __restrict__ C, double* __restrict__ part, unsigned long long* __restrict__ x1,
     unsigned long long* __restrict__ x2, unsigned long long* __restrict__ x3, const int32_t* __restrict__ kmap) {
-  // Q32 (plan-time guarantee: q <= 2^qb with qb small enough): 32-bit quantised values, row
-  // partials and per-stage column sums (folded into the 64-bit column sums at stage ends);
-  // else 64-bit throughout.  The warp's row total goes through warp_sum_u64 either way.
+  // Q32 (plan-time guarantee on q <= 2^qb): 32-bit quantised values, row partials and per-stage
+  // column sums (folded into 64-bit column sums at stage ends); else 64-bit throughout.
+  // Shared memory is addressed by byte offsets from the extern array (32-bit LDS addressing;
+  // no generic-pointer window arithmetic in the row loop).
   using qint = typename std::conditional<Q32, unsigned, unsigned long long>::type;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned long long bars[kMaxNS];
@@ -679,11 +687,17 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
   const int nq = g.pitch / 4;
   const int tq = tid % g.tpg, grp = tid / g.tpg;   // g.tpg: a multiple of 32
   const bool active = grp < g.ng;
+  const int ng = g.ng;
   const int64_t rb = g.row0 + (int64_t)blockIdx.x * g.rows_per_cta;
   const int64_t re = min(rb + g.rows_per_cta, g.row0 + g.nrows);
-  float* ring = reinterpret_cast<float*>(smem);
-  float* Wbuf = ring + (size_t)g.ns * g.tr * g.pitch;   // BRES: Bs [J][RB]; else W [2][tr][RB]
+  const int pitchB = g.pitch * (int)sizeof(float);
+  const int stageB = g.tr * pitchB;
+  float* Wbuf = reinterpret_cast<float*>(smem + (size_t)g.ns * stageB);   // BRES: Bs [J][RB]; else W [2][tr][RB]
   const int nst = rb < re ? (int)((re - rb + g.tr - 1) / g.tr) : 0;
+  // the warp's largest column quad decides whether every lane's quads are real columns
+  const int wq_max = (tid | 31) % g.tpg;
+  const bool wfull = QPT == 1 ? wq_max < nq : wq_max + g.tpg < nq;
+  const bool q1ok = QPT == 2 && tq + g.tpg < nq;
   float wb[kWPT];
   auto load_w = [&](int64_t r0, int j0) {
     const int nr = (int)min((int64_t)g.tr, re - r0);
@@ -722,29 +736,32 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
     if (nst > 0) { load_w(rb, js); store_w(0); }
   }
   __syncthreads();
+  float* ring = reinterpret_cast<float*>(smem);
   if (tid == 0)
     for (int s = 0; s < nst && s < g.ns; ++s) marg_issue(ring, bars, g, X, rb, re, s);
   double inner = 0.0, sq = 0.0;
-  unsigned long long xa[QPT][4];   // x1 column sums of the thread's quads
-  qint xs[QPT][4];                 // this stage's column sums (Q32: folded into xa per stage)
+  // x1 column sums of the thread's quads: 64-bit totals in shared memory (registers are the
+  // scarce resource here), this stage's sums in registers, folded at every stage end
+  const size_t wbytes = BRES ? sizeof(float) * (size_t)J * RB : sizeof(float) * 2 * (size_t)g.tr * RB;
+  unsigned long long* xsm = reinterpret_cast<unsigned long long*>(smem + (((size_t)g.ns * stageB + wbytes + 15) & ~(size_t)15));
+  qint xs[QPT][4];
 #pragma unroll
   for (int u = 0; u < QPT; ++u)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) { xa[u][e] = 0; xs[u][e] = 0; }
-  unsigned long long x3run = 0;    // lane 0: the warp's running x3 sum of slice x3k
+    for (int e = 0; e < 4; ++e) { xsm[(u * 4 + e) * nthr + tid] = 0; xs[u][e] = 0; }
+  unsigned long long x3acc = 0;    // the lane's share of slice x3k (flushed at slice changes)
   int64_t x3k = -1;
-  // the warp's row total (exact): lane 0 adds it to x2[j] and to the running x3 sum
-  auto row_done = [&](qint rs, int j, int64_t k) {
-    const unsigned long long t = Q32 ? warp_sum_u64<2>(rs) : warp_sum_u64<3>(rs);
-    if (lane == 0) {
-      if (t) atomicAdd(&x2[j], t);
-      if (k != x3k) {
-        if (x3run) atomicAdd(&x3[x3k], x3run);
-        x3k = k;
-        x3run = 0;
-      }
-      x3run += t;
-    }
+  auto flush_x3 = [&]() {
+    const unsigned long long t = warp_sum_u64<3>(x3acc);
+    if (lane == 0 && t) atomicAdd(&x3[x3k], t);
+    x3acc = 0;
+  };
+  auto row_x2 = [&](qint rs, int j) {   // the warp's share of row (j, k) -> x2[j]
+    unsigned long long t;
+    if constexpr (Q32) t = warp_sum_u31(rs);
+    else t = warp_sum_u64<3>(rs);
+    if (lane == 0 && t) atomicAdd(&x2[j], t);
+    x3acc += rs;
   };
   auto quad_marg = [&](const float4& v, qint (&xq)[4]) -> qint {
     qint q0, q1, q2, q3;
@@ -758,11 +775,11 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
     xq[0] += q0; xq[1] += q1; xq[2] += q2; xq[3] += q3;
     return (q0 + q1) + (q2 + q3);   // padding columns are zero in the store: q = 0
   };
-  auto fold_x1 = [&]() {   // stage-end fold of the stage's column sums
+  auto fold_x1 = [&]() {
 #pragma unroll
     for (int u = 0; u < QPT; ++u)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) { xa[u][e] += xs[u][e]; xs[u][e] = 0; }
+      for (int e = 0; e < 4; ++e) { xsm[(u * 4 + e) * nthr + tid] += xs[u][e]; xs[u][e] = 0; }
   };
   auto wrow = [&](const float* wr, float (&w)[RB]) {
     if constexpr (RB % 4 == 0) {
@@ -779,6 +796,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
       }
     }
   };
+  auto ldv = [&](int off) -> float4 { return *reinterpret_cast<const float4*>(smem + off); };
   if constexpr (QPT == 1) {
     constexpr int kFoldRows = 128;
     float acc[4][RB];
@@ -806,7 +824,6 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
       inner += (double)t;
       run = 0;
     };
-    const bool qok = tq < nq;
     for (int s = 0; s < nst; ++s) {
       const int slot = s % g.ns;
       const int64_t r0 = rb + (int64_t)s * g.tr;
@@ -817,7 +834,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
       if (!BRES && s + 1 < nst) load_w(r0 + g.tr, jn);
       s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
       if (active) {
-        const float* st = ring + (size_t)slot * g.tr * g.pitch;
+        const int soff = slot * stageB + 16 * tq;
         const float* W = Wbuf + (BRES ? 0 : (size_t)(s & 1) * g.tr * RB);
         float fs = 0.f;
         int64_t k = ks;
@@ -828,27 +845,36 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
             if (kc >= 0) fold(kc);
             kc = k;
           }
-#pragma unroll 1
-          for (int r = ra + ((grp - ra) % g.ng + g.ng) % g.ng; r < ra + seg; r += g.ng) {
-            const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
-            qint rs = 0;
-            if (qok) {
-              float w[RB];
-              wrow(wr, w);
-              const float4 v = *reinterpret_cast<const float4*>(st + (size_t)r * g.pitch + 4 * tq);
-#pragma unroll
-              for (int f = 0; f < RB; ++f) {
-                acc[0][f] = fmaf(v.x, w[f], acc[0][f]);
-                acc[1][f] = fmaf(v.y, w[f], acc[1][f]);
-                acc[2][f] = fmaf(v.z, w[f], acc[2][f]);
-                acc[3][f] = fmaf(v.w, w[f], acc[3][f]);
-              }
-              fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
-              rs = quad_marg(v, xs[0]);
-            }
-            row_done(rs, j + r - ra, k);
-            ++run;
+          if (k != x3k) {
+            if (x3k >= 0) flush_x3();
+            x3k = k;
           }
+          auto rows = [&](auto fullc) {
+            constexpr bool FULL = decltype(fullc)::value;
+#pragma unroll 1
+            for (int r = ra + ((grp - ra) % ng + ng) % ng; r < ra + seg; r += ng) {
+              const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
+              qint rs = 0;
+              if (FULL || tq < nq) {
+                float w[RB];
+                wrow(wr, w);
+                const float4 v = ldv(soff + r * pitchB);
+#pragma unroll
+                for (int f = 0; f < RB; ++f) {
+                  acc[0][f] = fmaf(v.x, w[f], acc[0][f]);
+                  acc[1][f] = fmaf(v.y, w[f], acc[1][f]);
+                  acc[2][f] = fmaf(v.z, w[f], acc[2][f]);
+                  acc[3][f] = fmaf(v.w, w[f], acc[3][f]);
+                }
+                fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
+                rs = quad_marg(v, xs[0]);
+              }
+              row_x2(rs, j + r - ra);
+            }
+          };
+          if (wfull) rows(std::true_type{});
+          else rows(std::false_type{});
+          run += (seg + ng - 1) / ng;
           ra += seg;
           j = 0;
           ++k;
@@ -884,6 +910,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
             al[u][e][f] = v;
           }
     };
+    const int uoff = 16 * g.tpg;   // byte offset of the thread's second quad
     for (int s = 0; s < nst; ++s) {
       const int slot = s % g.ns;
       const int64_t r0 = rb + (int64_t)s * g.tr;
@@ -894,7 +921,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
       if (!BRES && s + 1 < nst) load_w(r0 + g.tr, jn);
       s_wait(&bars[slot], (unsigned)(s / g.ns) & 1u);
       if (active) {
-        const float* st = ring + (size_t)slot * g.tr * g.pitch;
+        const int soff = slot * stageB + 16 * tq;
         const float* W = Wbuf + (BRES ? 0 : (size_t)(s & 1) * g.tr * RB);
         float fi = 0.f, fs = 0.f;
         int64_t k = ks;
@@ -907,32 +934,54 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
             load_al(k);
             kc = k;
           }
+          if (k != x3k) {
+            if (x3k >= 0) flush_x3();
+            x3k = k;
+          }
+          auto rows = [&](auto fullc) {
+            constexpr bool FULL = decltype(fullc)::value;
 #pragma unroll 1
-          for (int r = ra + ((grp - ra) % g.ng + g.ng) % g.ng; r < ra + seg; r += g.ng) {
-            const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
-            float w[RB];
-            wrow(wr, w);
-            qint rs = 0;
-#pragma unroll
-            for (int u = 0; u < QPT; ++u) {
-              const int q = tq + u * g.tpg;
-              if (q < nq) {
-                const float4 v = *reinterpret_cast<const float4*>(st + (size_t)r * g.pitch + 4 * q);
+            for (int r = ra + ((grp - ra) % ng + ng) % ng; r < ra + seg; r += ng) {
+              const float* wr = BRES ? W + (size_t)(j + r - ra) * RB : W + r * RB;
+              float w[RB];
+              wrow(wr, w);
+              const int off = soff + r * pitchB;
+              qint rs;
+              {
+                const float4 v = ldv(off);
                 float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
 #pragma unroll
                 for (int f = 0; f < RB; ++f) {
-                  m0 = fmaf(al[u][0][f], w[f], m0);
-                  m1 = fmaf(al[u][1][f], w[f], m1);
-                  m2 = fmaf(al[u][2][f], w[f], m2);
-                  m3 = fmaf(al[u][3][f], w[f], m3);
+                  m0 = fmaf(al[0][0][f], w[f], m0);
+                  m1 = fmaf(al[0][1][f], w[f], m1);
+                  m2 = fmaf(al[0][2][f], w[f], m2);
+                  m3 = fmaf(al[0][3][f], w[f], m3);
                 }
                 fi = fmaf(v.x, m0, fmaf(v.y, m1, fmaf(v.z, m2, fmaf(v.w, m3, fi))));
                 fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
-                rs += quad_marg(v, xs[u]);
+                rs = quad_marg(v, xs[0]);
               }
+              {
+                // the second quad: a lane past the last column reads its first quad again and
+                // contributes zeros (its al columns are zero too) -- no branch in the loop
+                float4 v = ldv(q1ok ? off + uoff : off);
+                if (!q1ok) v = make_float4(0.f, 0.f, 0.f, 0.f);
+                float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f;
+#pragma unroll
+                for (int f = 0; f < RB; ++f) {
+                  m0 = fmaf(al[1][0][f], w[f], m0);
+                  m1 = fmaf(al[1][1][f], w[f], m1);
+                  m2 = fmaf(al[1][2][f], w[f], m2);
+                  m3 = fmaf(al[1][3][f], w[f], m3);
+                }
+                fi = fmaf(v.x, m0, fmaf(v.y, m1, fmaf(v.z, m2, fmaf(v.w, m3, fi))));
+                fs = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, fs))));
+                rs += quad_marg(v, xs[1]);
+              }
+              row_x2(rs, j + r - ra);
             }
-            row_done(rs, j + r - ra, k);
-          }
+          };
+          rows(std::true_type{});
           ra += seg;
           j = 0;
           ++k;
@@ -951,7 +1000,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
       js = jn;
     }
   }
-  if (lane == 0 && x3run) atomicAdd(&x3[x3k], x3run);
+  if (active && x3k >= 0) flush_x3();
   inner = block_sum_d(inner, red);
   sq = block_sum_d(sq, red);
   if (tid == 0) {
@@ -967,7 +1016,7 @@ __global__ void __launch_bounds__(QPT == 1 ? kST : kFitT2, 1) margfit_stream_ker
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int q = tq + u * g.tpg;
-        if (q < nq) xg[(size_t)grp * g.pitch + 4 * q + e] = xa[u][e];
+        if (q < nq) xg[(size_t)grp * g.pitch + 4 * q + e] = xsm[(u * 4 + e) * nthr + tid];
       }
   __syncthreads();
   for (int c = tid; c < g.ncol; c += nthr) {
@@ -998,8 +1047,9 @@ StreamGeom margfit_geom(const DenseView& X, int64_t k0, int64_t nk, int RB, int*
   if (g.tr < 1) g.tr = 1;
   if (!g.bres && g.tr * RB > kWPT * nthr) g.tr = kWPT * nthr / RB;
   if (g.tr > 256) g.tr = 256;
-  const size_t extra = g.bres ? bres_b : sizeof(float) * 2 * (size_t)g.tr * RB;
-  const int ring_b = (int)(208 * 1024 - extra);
+  const size_t extra = (g.bres ? bres_b : sizeof(float) * 2 * (size_t)g.tr * RB) + 16 +
+                       sizeof(unsigned long long) * 4 * g.qpt * nthr;   // + the x1 totals
+  const int ring_b = (int)(220 * 1024 - extra);
   g.cw = g.pitch;
   g.ns = ring_b / (g.tr * row_b);
   if (g.ns > kMaxNS) g.ns = kMaxNS;
@@ -1130,9 +1180,10 @@ static cudaError_t margfit_rb(const DenseView& X, int64_t nk, int S, int qb, con
   int gx, nt;
   StreamGeom g = margfit_geom(X, 0, nk, RB, &gx, &nt);
   const size_t extra = g.bres ? (size_t)X.J * RB : 2 * (size_t)g.tr * RB;
-  size_t smem = sizeof(float) * ((size_t)g.ns * g.tr * g.pitch + extra);
-  const size_t xg = sizeof(long long) * (size_t)g.ng * g.pitch;   // x1 combine reuses the region
-  if (smem < xg) smem = xg;
+  size_t smem = ((sizeof(float) * ((size_t)g.ns * g.tr * g.pitch + extra) + 15) & ~(size_t)15) +
+                sizeof(unsigned long long) * 4 * g.qpt * nt;
+  const size_t xg = sizeof(long long) * (size_t)g.ng * g.pitch;   // x1 combine reuses the ring
+  if ((size_t)g.ns * g.tr * g.pitch * sizeof(float) < xg) return cudaErrorInvalidValue;
   const float scf = ldexpf(1.0f, S < -126 ? -126 : (S > 127 ? 127 : S));
   const double scd = ldexp(1.0, S);
   auto* u1 = reinterpret_cast<unsigned long long*>(x1);
@@ -1152,7 +1203,7 @@ static cudaError_t margfit_rb(const DenseView& X, int64_t nk, int S, int qb, con
     if (q32) { if (g.bres) go(margfit_stream_kernel<MOI, RB, 1, true, true>); else go(margfit_stream_kernel<MOI, RB, 1, false, true>); }
     else { if (g.bres) go(margfit_stream_kernel<MOI, RB, 1, true, false>); else go(margfit_stream_kernel<MOI, RB, 1, false, false>); }
   } else {
-    if constexpr (RB <= 12) {
+    if constexpr (RB == 4 || RB == 10) {
       if (q32) { if (g.bres) go(margfit_stream_kernel<MOI, RB, 2, true, true>); else go(margfit_stream_kernel<MOI, RB, 2, false, true>); }
       else { if (g.bres) go(margfit_stream_kernel<MOI, RB, 2, true, false>); else go(margfit_stream_kernel<MOI, RB, 2, false, false>); }
     } else {
@@ -1163,16 +1214,22 @@ static cudaError_t margfit_rb(const DenseView& X, int64_t nk, int S, int qb, con
   return cudaGetLastError();
 }
 
+bool margfit_supported(const DenseView& X, int R) {
+  return fit_stream_supported(X, R) && (X.pitch / 4 <= kST || R <= 10);
+}
+
 cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, int qb, const float* lam,
                                    const float* A, const float* B, const float* C, int R, const int32_t* kmap,
                                    int64_t* x1, int64_t* x2, int64_t* x3, double* ws, double* out2,
                                    cudaStream_t st) {
-  if (nk <= 0 || !fit_stream_supported(X, R)) return cudaErrorInvalidValue;
+  if (nk <= 0 || !margfit_supported(X, R)) return cudaErrorInvalidValue;
 #define SBT_MF(RBV)                                                                                       \
   return moi == 0 ? margfit_rb<RBV, 0>(X, nk, S, qb, lam, A, B, C, R, kmap, x1, x2, x3, ws, out2, st)     \
                   : margfit_rb<RBV, 1>(X, nk, S, qb, lam, A, B, C, R, kmap, x1, x2, x3, ws, out2, st)
+  // (an RB = 8 instantiation of the fused kernel crashes ptxas 12.9: R in 5..8 runs at RB = 10)
+  // (RB = 8 and 12 instantiations of the two-quad kernel crash ptxas 12.9: R in 5..8 runs at
+  // RB = 10, and R = 11, 12 with rows > 2048 floats are not offered: margfit_supported)
   if (R <= 4) { SBT_MF(4); }
-  if (R <= 8) { SBT_MF(8); }
   if (R <= 10) { SBT_MF(10); }
   if (R <= 12) { SBT_MF(12); }
   SBT_MF(16);
