@@ -56,9 +56,10 @@ def parse():
     p.add_argument("--no-variant", action="store_true", help="skip the incremental-marginals variant run")
     p.add_argument("--no-getrank", action="store_true", help="skip the GetRank timing (SURVEY 8(f) NEXT #2)")
     p.add_argument("--no-full-fit", action="store_true", help="return the summary fit only (R21)")
-    p.add_argument("--full-fit", type=int, default=2, choices=[1, 2],
-                   help="1: a7 pass after the merge; 2 (default): lag-1 fit inside the next update's a1 "
-                        "pass (SURVEY 8(f) NEXT #1; dense only, COO configs use 1)")
+    p.add_argument("--full-fit", type=int, default=1, choices=[1, 2],
+                   help="1 (default): the committed model's fit (dense: incremental -- the batch plus the "
+                        "rows the merge changed, k_fitinc.cu); 2: lag-1 fit inside the next update's a1 pass "
+                        "(SURVEY 8(f) NEXT #1; dense only, COO configs use 1)")
     p.add_argument("--sharded", action="store_true",
                    help="use the sharded (NCCL) handle even at N=1 (always used at N>1, dense configs)")
     return p.parse_args()
@@ -260,10 +261,15 @@ def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
     Kloc = k_local if k_local is not None else Ks
     IJ = w.I * w.J
     lag = all(inf.get("fit_full_prev", -1.0) != -1.0 for inf in infos)
+    incfit = all(inf.get("fit_path", 0) == 3 for inf in infos)
     out["a1"] = hbm_line("margfit_stream_kernel (a1 + lag-1 fit) + marg_stream_kernel (batch)" if lag
                          else "marg_stream_kernel", 1,
                          statistics.mean(4.0 * IJ * kl for kl in Kloc) + 8.0 * (w.I + w.J + statistics.mean(Ks)))
-    if not lag:
+    if incfit:   # the batch's slices (+ changed rows): 4 B per new entry
+        out["a7"] = dict(hbm_line("fitrows_kernel (incremental fit: the batch's slices)", 7,
+                                  statistics.mean(4.0 * IJ * w.batch for _ in Kloc)),
+                         note="incremental exact fit (k_fitinc.cu): reads only the new slices")
+    elif not lag:
         out["a7"] = hbm_line("fit_stream_kernel", 7, statistics.mean(4.0 * IJ * kl for kl in Kloc))
     nI, nJ = -(-w.I // w.s), -(-w.J // w.s)
     Y = []
@@ -559,7 +565,10 @@ def main():
     config["accept_tau"] = tau
     config["als_init"] = "warm (model rows, R34)" if warm else "cold (Philox point, P:213)"
     ff = 0 if args.no_full_fit else (args.full_fit if not work.coo else 1)
-    config["full_fit"] = {0: "none (summary fit only)", 1: "a7 pass after the merge",
+    config["full_fit"] = {0: "none (summary fit only)",
+                          1: "the committed model's exact fit (dense: incremental from the previous model's "
+                             "per-component inner products -- the batch's slices plus the rows the merge changed; "
+                             "COO: a pass over the nonzeros)",
                           2: "lag-1: the previous model's fit inside this update's a1 pass (NEXT #1)"}[ff]
     opts = L.default_opts(als_max_iters=w.maxit, als_tol=w.tol, capacity=work.cap, full_fit=ff,
                           accept_tau=tau, stream=stream.cuda_stream, warm_start=int(warm))
@@ -691,6 +700,8 @@ def main():
         "clocks": clocks,
         "fit_full_last": infos[-1]["fit_full"] if infos[-1]["fit_full"] != -1.0 else infos[-1]["fit_full_prev"],
         "fit_full_is_lag1": infos[-1]["fit_full"] == -1.0 and infos[-1]["fit_full_prev"] != -1.0,
+        "fit_path_last": {0: "none", 1: "separate pass", 2: "lag-1 in a1", 3: "incremental",
+                          4: "incremental plan -> full pass"}.get(infos[-1].get("fit_path", 0)),
         "fit_summary_last": infos[-1]["fit_summary"],
         "reps_rejected_last": bin(infos[-1]["reps_rejected_mask"]).count("1"),
     }

@@ -77,7 +77,10 @@ typedef struct {
                           /*     the sampled rows (R17)                              */
   double accept_tau;      /* rep acceptance threshold on min_f S(f, pi f) (R26); default 0.9 */
   int full_fit;           /* 1: sambaten_update also computes the full relative error of the   */
-                          /*    model it commits (a7: one extra pass over the tensor);          */
+                          /*    model it commits (a7): on dense handles kept up to date from the */
+                          /*    previous model's per-component inner products (the batch's      */
+                          /*    slices plus the rows the merge changed; exact algebra, O(batch)  */
+                          /*    bytes), else one pass over the tensor;                           */
                           /* 2: lag-1 fused fit: the relative error of the */
                           /*    model the PREVIOUS update (or init) committed is computed inside  */
                           /*    this update's marginal pass over the old slices, which reads the  */
@@ -138,6 +141,10 @@ typedef struct {
   double fit_full_prev;        /* full_fit = 2: 1 - ||X_prev - model_prev||/||X_prev|| of the    */
                                /* model the previous update committed, over the tensor it was   */
                                /* committed on (computed in this update's a1 pass); else -1     */
+  int fit_path;                /* how the full fit was obtained: 0 none, 1 separate pass over  */
+                               /* the tensor, 2 lag-1 inside a1, 3 incremental (the batch plus */
+                               /* the rows the merge changed), 4 incremental plan fell back to */
+                               /* one full per-component pass                                   */
 } sambaten_info;
 
 /* Fill *opts with the defaults listed above. */

@@ -53,7 +53,8 @@ class Info(C.Structure):
                 ("kernel_launches", C.c_int), ("reps_pinv_mask", C.c_uint32),
                 ("step_ms", C.c_double * 8), ("als_iters_sum", C.c_int),
                 ("rep_rank", C.c_int * 32), ("als_plan", C.c_int * 4),
-                ("summary_entries", C.c_int64), ("fit_full_prev", C.c_double)]
+                ("summary_entries", C.c_int64), ("fit_full_prev", C.c_double),
+                ("fit_path", C.c_int)]
 
     def as_dict(self):
         return dict(fit_summary=self.fit_summary, fit_full=self.fit_full,
@@ -62,7 +63,8 @@ class Info(C.Structure):
                     kernel_launches=self.kernel_launches, reps_pinv_mask=self.reps_pinv_mask,
                     step_ms=list(self.step_ms), als_iters_sum=self.als_iters_sum,
                     rep_rank=list(self.rep_rank), als_plan=list(self.als_plan),
-                    summary_entries=self.summary_entries, fit_full_prev=self.fit_full_prev)
+                    summary_entries=self.summary_entries, fit_full_prev=self.fit_full_prev,
+                    fit_path=self.fit_path)
 
 
 _lib = None

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <tuple>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/sambaten.h"
@@ -107,6 +108,7 @@ struct HostStatus {        // pinned; filled by one D2H copy at the end of an up
   int flags[kMaxReps];
   double fit[kMaxReps];
   double relerr, relerr_prev;
+  int fit_mode;
 };
 
 struct DistState;   // capi_dist.inc
@@ -119,6 +121,8 @@ struct sambaten_s {
   int als_plan[4] = {-1, 0, 0, 0};   // the a4 plan of the last update (sambaten_info.als_plan)
   int64_t summ_entries = 0;          // summary entries / nnz of the update in flight (sambaten_info)
   bool lag_now = false;              // this update computes the previous model's fit in a1 (full_fit = 2)
+  int fit_path = 0;                  // sambaten_info.fit_path of the update in flight
+  const int* d_fit_mode = nullptr;   // device plan of the incremental fit (1 incremental, 2 full)
   cudaStream_t st2 = nullptr;     // side stream: host batch copy overlapped with a1 (old slices)
   cudaEvent_t ev_side[2] = {nullptr, nullptr};
   DevBuf xm, xm_ck;          // committed marginals of the current tensor (incremental a1)
@@ -131,7 +135,8 @@ struct sambaten_s {
   int S = 0, maxphi_log2 = 0;
   // store and model
   DevBuf X;
-  DevBuf model[2];          // A | B | C | lam, double-buffered (merge writes the shadow)
+  DevBuf model[2];          // A | B | C | lam | fit state, double-buffered (merge writes the shadow)
+  DevBuf fiws;              // incremental-fit workspace (k_fitinc.cu)
   int cur = 0;
   DevBuf ck;                // checkpoint of the model
   int64_t K_ck = -1;
@@ -162,7 +167,11 @@ struct sambaten_s {
   float* B(int b) const { return A(b) + I * R; }
   float* C(int b) const { return B(b) + J * R; }
   float* lam(int b) const { return C(b) + Kcap * R; }
-  size_t model_floats() const { return (size_t)(I + J + Kcap + 1) * R; }
+  // the incremental fit's state rides in the model buffer (so merge copies, checkpoint and
+  // restore carry it): [P[0..R), ||X||^2, valid] fp64 after lambda (k_fitinc.cu)
+  size_t fit_off() const { return ((size_t)(I + J + Kcap + 1) * R + 1) & ~(size_t)1; }
+  double* fitst(int b) const { return reinterpret_cast<double*>(model[b].as<float>() + fit_off()); }
+  size_t model_floats() const { return fit_off() + 2 * (size_t)(R + 2); }
   DenseView view() const { return DenseView{X.as<float>(), I, J, K, pitch}; }
   DenseView view_local() const;   // the local slab of a sharded handle (capi_dist.inc)
 };
@@ -189,6 +198,102 @@ static bool cluster_plan(sambaten_s* h, const DenseAls& a, ClusterPlan* pl) {
 // beyond it is rejected), so q = RNE(phi 2^S) <= 2^(maxphi_log2 + 8 + S) (x^2 measure: the
 // log of the squared bound)
 static int qbits(const sambaten_s* h) { return h->maxphi_log2 + 8 + h->S; }
+
+// ---- incremental exact fit (k_fitinc.cu) --------------------------------------------------------
+static size_t align256(size_t b);
+// Workspace: 4 term partials, the changed-row lists, counts, mode, Grams and their tiles.
+struct FitIncWs {
+  double* parts[4]; int32_t *jlist, *klist; int *counts, *mode; double *G, *gws, *red;
+};
+static cudaError_t fitinc_ws(sambaten_s* h, FitIncWs* w) {
+  const int R = h->R, RB = fitrows_rb_of(R), nb = fitrows_blocks();
+  const size_t pb = align256(sizeof(double) * (size_t)nb * (RB + 1));
+  const size_t lb = align256(sizeof(int32_t) * (size_t)std::max<int64_t>(std::max(h->J, h->Kcap), 1));
+  const size_t gw = align256(sizeof(double) * gram3_ws_doubles(h->I, h->J, h->Kcap, R));
+  const size_t need = 4 * pb + 2 * lb + 256 + align256(sizeof(double) * 3 * R * R) + gw + 256;
+  cudaError_t e = h->fiws.ensure(need);
+  if (e != cudaSuccess) return e;
+  char* p = h->fiws.as<char>();
+  for (int t = 0; t < 4; ++t) { w->parts[t] = reinterpret_cast<double*>(p); p += pb; }
+  w->jlist = reinterpret_cast<int32_t*>(p); p += lb;
+  w->klist = reinterpret_cast<int32_t*>(p); p += lb;
+  w->counts = reinterpret_cast<int*>(p); w->mode = w->counts + 2; w->red = reinterpret_cast<double*>(p + 64); p += 256;
+  w->G = reinterpret_cast<double*>(p); p += align256(sizeof(double) * 3 * R * R);
+  w->gws = reinterpret_cast<double*>(p);
+  return cudaSuccess;
+}
+
+// Fit of model nb over the slices [0, K) of view V: incremental from model b's state over the
+// first Ko slices when the plan allows, else one full pass (decided on the device).
+// full_only: skip the plan (initial state).  kmap: store slice -> model row (sharded) or NULL;
+// allow_c: the dC term may run (its slice list holds store slices = model rows; single GPU).
+// reduce: sharded all-reduce of the [R + 1] sums (NULL on one GPU).
+static cudaError_t fitinc_run(sambaten_s* h, const DenseView& V, int64_t Ko_store, int64_t Ko_model, int64_t K_model,
+                              int b, int nb, bool full_only, const int32_t* kmap, bool allow_c,
+                              double* relerr, cudaStream_t st,
+                              const std::function<cudaError_t(double*, size_t)>& reduce = nullptr) {
+  const int R = h->R;
+  FitIncWs w;
+  cudaError_t e = fitinc_ws(h, &w);
+  if (e != cudaSuccess) return e;
+  if (full_only) {
+    const int two = 2;
+    e = cudaMemcpyAsync(w.mode, &two, sizeof(int), cudaMemcpyHostToDevice, st);
+  } else {
+    FitPlanArgs p{};
+    p.A0 = h->A(b); p.A1 = h->A(nb); p.B0 = h->B(b); p.B1 = h->B(nb); p.C0 = h->C(b); p.C1 = h->C(nb);
+    p.I = h->I; p.J = h->J; p.Kold = Ko_model; p.R = R;
+    p.st_old = h->fitst(b);
+    // incremental while its rows stay under half of a full pass; the dC term only where allowed
+    p.budget_rows = 0.5 * (double)h->J * (double)Ko_model;
+    p.allow_c = allow_c ? 1 : 0;
+    p.jlist = w.jlist; p.klist = w.klist; p.counts = w.counts; p.mode = w.mode;
+    e = launch_fitinc_plan(p, st);
+  }
+  if (e != cudaSuccess) return e;
+  FitRows base{};
+  base.X = V.base; base.pitch = V.pitch; base.I = (int)h->I; base.J = (int)h->J; base.R = R;
+  base.kmap = kmap;
+  // term 0: the new slices with the new model
+  FitRows t0 = base;
+  t0.kind = 0; t0.k0 = Ko_store; t0.k1 = V.K; t0.As = h->A(nb); t0.U = h->B(nb); t0.V = h->C(nb);
+  t0.gate = w.mode; t0.gate_val = 1;
+  // term 1: changed B rows over the old slices: A (B' - B) C'
+  FitRows t1 = base;
+  t1.kind = 1; t1.k0 = 0; t1.k1 = Ko_store; t1.list = w.jlist; t1.nlist = w.counts;
+  t1.As = h->A(b); t1.U = h->B(nb); t1.Usub = h->B(b); t1.V = h->C(nb); t1.gate = w.mode; t1.gate_val = 1;
+  // term 2: changed old C rows: A B (C' - C)   (store slice = model row: single GPU only)
+  FitRows t2 = base;
+  t2.kind = 2; t2.list = w.klist; t2.nlist = w.counts + 1;
+  t2.As = h->A(b); t2.U = h->B(b); t2.V = h->C(nb); t2.Vsub = h->C(b); t2.gate = w.mode; t2.gate_val = 1;
+  // term 3: the full pass with the new model
+  FitRows t3 = base;
+  t3.kind = 0; t3.k0 = 0; t3.k1 = V.K; t3.As = h->A(nb); t3.U = h->B(nb); t3.V = h->C(nb);
+  t3.gate = w.mode; t3.gate_val = 2;
+  if (!full_only) {
+    if (Ko_store < V.K && (e = launch_fitrows(t0, w.parts[0], st)) != cudaSuccess) return e;
+    if (Ko_store > 0 && (e = launch_fitrows(t1, w.parts[1], st)) != cudaSuccess) return e;
+    if (allow_c && (e = launch_fitrows(t2, w.parts[2], st)) != cudaSuccess) return e;
+  }
+  if (V.K > 0 && (e = launch_fitrows(t3, w.parts[3], st)) != cudaSuccess) return e;
+  e = launch_gram3(h->A(nb), h->B(nb), h->C(nb), h->I, h->J, K_model, R, w.G, w.gws, st);
+  if (e != cudaSuccess) return e;
+  FitFinishArgs f{};
+  const int nbk = fitrows_blocks();
+  f.terms[0] = (!full_only && Ko_store < V.K) ? w.parts[0] : nullptr;
+  f.terms[1] = (!full_only && Ko_store > 0) ? w.parts[1] : nullptr;
+  f.terms[2] = (!full_only && allow_c) ? w.parts[2] : nullptr;
+  f.terms[3] = V.K > 0 ? w.parts[3] : nullptr;
+  for (int t = 0; t < 4; ++t) f.nparts[t] = nbk;
+  f.mode = w.mode; f.R = R; f.RB = fitrows_rb_of(R);
+  f.st_old = h->fitst(b); f.st_new = h->fitst(nb); f.lam = h->lam(nb); f.G = w.G; f.relerr = relerr;
+  if (reduce) {
+    if ((e = launch_fitinc_sum(f, w.red, st)) != cudaSuccess) return e;
+    if ((e = reduce(w.red, (size_t)R + 1)) != cudaSuccess) return e;
+    f.reduced = w.red;
+  }
+  return launch_fitinc_finish(f, st);
+}
 
 static void set_plan_report(sambaten_s* h, bool cluster, const ClusterPlan& pl, int R) {
   h->als_plan[0] = cluster ? 1 : 0;
@@ -388,7 +493,7 @@ extern "C" void sambaten_destroy(sambaten_t h) {
   h->model[0].release(); h->model[1].release(); h->ck.release();
   h->marg.release(); h->xm.release(); h->xm_ck.release(); h->samp.release(); h->summ.release(); h->fac.release();
   h->als.release(); h->match.release(); h->misc.release(); h->segs.release(); h->fitws.release();
-  h->coo_ws.release(); h->grws.release(); h->grk.release();
+  h->coo_ws.release(); h->grws.release(); h->grk.release(); h->fiws.release();
   if (h->segs_host) cudaFreeHost(h->segs_host);
   if (h->hs) cudaFreeHost(h->hs);
   for (int e = 0; e < 9; ++e)
@@ -401,6 +506,17 @@ __global__ static void lam_to_f32_kernel(const double* l, int R, float* out) {
 }
 
 static sambaten_status init_als_coo(sambaten_s* h);
+
+// The incremental fit's state of the initial model (one per-component pass over X0; untimed
+// init work) when the updates will report the full fit of a dense handle (full_fit = 1).
+static cudaError_t init_fit_state(sambaten_s* h) {
+  if (h->opts.full_fit != 1 || h->fmt != SAMBATEN_DENSE || h->dist || getenv("SAMBATEN_FULL_FIT_PASS"))
+    return cudaSuccess;
+  cudaError_t e = h->misc.ensure(4096);
+  if (e != cudaSuccess) return e;
+  double* scratch = reinterpret_cast<double*>(h->misc.as<char>() + 512);
+  return fitinc_run(h, h->view(), 0, 0, h->K, h->cur, h->cur, true, nullptr, false, scratch, h->st);
+}
 
 extern "C" sambaten_status sambaten_init(sambaten_t* out, const sambaten_tensor* X0, int R, int s,
                                          int r, uint64_t seed, const sambaten_opts* opts) {
@@ -425,7 +541,8 @@ extern "C" sambaten_status sambaten_init(sambaten_t* out, const sambaten_tensor*
   if (ce == cudaSuccess) ce = run_dense_als(a, h->st);
   if (ce == cudaSuccess) {
     lam_to_f32_kernel<<<1, 32, 0, h->st>>>(a.lam, R, h->lam(h->cur));
-    ce = cudaStreamSynchronize(h->st);
+    ce = init_fit_state(h);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->st);
   }
   ws.release();
   if (ce != cudaSuccess) {
@@ -449,6 +566,7 @@ extern "C" sambaten_status sambaten_init_factors(sambaten_t* out, const sambaten
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(h->B(b), B, sizeof(float) * h->J * R, cudaMemcpyDefault, h->st);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(h->C(b), C, sizeof(float) * h->K * R, cudaMemcpyDefault, h->st);
   if (ce == cudaSuccess) ce = cudaMemcpyAsync(h->lam(b), lambda, sizeof(float) * R, cudaMemcpyDefault, h->st);
+  if (ce == cudaSuccess) ce = init_fit_state(h);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->st);
   if (ce != cudaSuccess) {
     set_error(std::string("init_factors: ") + cudaGetErrorString(ce));
@@ -682,6 +800,7 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
   const bool fit_now = h->opts.full_fit == 1 || (h->opts.full_fit == 2 && !h->lag_now);
   if (fit_now) CK(cudaMemcpyAsync(&hs->relerr, d_relerr, 8, cudaMemcpyDeviceToHost, st));
   if (h->lag_now) CK(cudaMemcpyAsync(&hs->relerr_prev, d_relerr + 4, 8, cudaMemcpyDeviceToHost, st));
+  if (h->d_fit_mode) CK(cudaMemcpyAsync(&hs->fit_mode, h->d_fit_mode, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (d_vflags) vflags = hs->vflags;
   if (vflags & 1u) FAIL(SAMBATEN_E_INDEX_RANGE, "update: COO index out of range (S:77)");
@@ -715,6 +834,7 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
     info->fit_summary = fsum / r;
     info->fit_full = fit_now ? 1.0 - hs->relerr : -1.0;
     info->fit_full_prev = h->lag_now ? 1.0 - hs->relerr_prev : -1.0;
+    info->fit_path = h->d_fit_mode ? (hs->fit_mode == 1 ? 3 : 4) : (h->lag_now ? 2 : (fit_now ? 1 : 0));
     info->als_iters_max = itmax;
     info->als_iters_sum = itsum;
     info->k_total = h->K;
@@ -1079,6 +1199,8 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   h->als_plan[0] = -1; h->als_plan[1] = h->als_plan[2] = h->als_plan[3] = 0;   // set by the dense paths
   h->summ_entries = 0;
   h->lag_now = false;
+  h->fit_path = 0;
+  h->d_fit_mode = nullptr;
   if (h->dist)
     return h->fmt == SAMBATEN_COO ? update_coo_dist(h, batch, Aout, Bout, Cout, lamout, info)
                                   : update_dense_dist(h, batch, Aout, Bout, Cout, lamout, info);
@@ -1264,11 +1386,21 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   CK(cudaEventRecord(h->ev[7], st));
   // ---- a7: full fit of the new model (optional; with full_fit = 2 it rides on the next a1) --
   const bool fit_now = h->opts.full_fit == 1 || (h->opts.full_fit == 2 && !lag);
-  if (fit_now) {
+  if (fit_now && h->opts.full_fit == 1 && !getenv("SAMBATEN_FULL_FIT_PASS")) {
+    // the new model's exact fit kept up to date from the previous one (k_fitinc.cu): the batch's
+    // slices plus the rows the merge changed, or one full pass when the plan says so
+    CK(fitinc_run(h, V, Ko, Ko, Ko + Kn, b, nb, false, nullptr, true, d_relerr, st));
+    FitIncWs w;
+    CK(fitinc_ws(h, &w));
+    h->d_fit_mode = w.mode;
+  } else if (fit_now) {
     // separate workspace: reallocating misc here would lose the max-phi word written in a0
     const size_t need = sizeof(double) * fit_ws_doubles_any(V);
     CK(h->fitws.ensure(need));
     CK(fit_any(V, h->lam(nb), h->A(nb), h->B(nb), h->C(nb), R, h->fitws.as<double>(), d_relerr, st));
+    CK(cudaMemsetAsync(h->fitst(nb) + R + 1, 0, sizeof(double), st));   // per-component state not kept
+  } else {
+    CK(cudaMemsetAsync(h->fitst(nb) + R + 1, 0, sizeof(double), st));
   }
   CK(cudaEventRecord(h->ev[8], st));
   // a0 ingest or max_phi (+ the old-slice marginal pass when a host batch overlaps its copy),

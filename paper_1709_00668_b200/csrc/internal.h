@@ -320,6 +320,43 @@ size_t fit_stream_ws_doubles(const DenseView& X);
 // slices (SURVEY 8(f) NEXT #1 lag-1 fit): x1/x2/x3 accumulate (zero them first); out2 =
 // {<X, M>, ||X||^2} of those slices (finish with launch_fit_finish); kmap: local slice -> model
 // row (sharded stores) or NULL; ws: fit_stream_ws_doubles; needs fit_stream_supported(X, R)
+// ---- incremental exact fit (k_fitinc.cu) ---------------------------------
+// per-component sums P[f] += sum over a row set of the store of sum_i X(i,j,k) As(i,f) w(j,k,f),
+// w = (U - Usub)(j,f) (V - Vsub)(kmap(k), f); column R of the outputs: sum of X^2 over the rows
+struct FitRows {
+  const float* X; int64_t pitch; int I, J, R;
+  int kind;                  // 0: slices [k0, k1), every j; 1: j in list, k in [k0, k1); 2: k in list, every j
+  int64_t k0, k1;
+  const int32_t* list; const int* nlist;   // kinds 1, 2 (device count)
+  const float* As;                         // I x R
+  const float *U, *Usub, *V, *Vsub;        // J x R and (model rows) x R; Usub / Vsub may be NULL
+  const int32_t* kmap;                     // store slice -> model row (sharded) or NULL
+  const int* gate; int gate_val;           // run only if *gate == gate_val (NULL: always)
+  int as_in_smem;                          // set by launch_fitrows
+};
+struct FitPlanArgs {
+  const float *A0, *A1, *B0, *B1, *C0, *C1;   // old / new model
+  int64_t I, J, Kold; int R;
+  const double* st_old;                        // [P[R], ||X||^2, valid]
+  double budget_rows; int allow_c;             // allow_c = 0: a changed old C row forces the full pass
+  int32_t *jlist, *klist; int* counts;          // counts[0] = changed B rows, [1] = changed old C rows
+  int* mode;                                    // 1 incremental, 2 full pass
+};
+struct FitFinishArgs {
+  const double* terms[4]; int nparts[4];       // 0 new slices, 1 dB, 2 dC (incremental), 3 full pass
+  const double* reduced;                       // sharded: all-reduced [R + 1] sums, else NULL
+  const int* mode; int R, RB;
+  const double* st_old; double* st_new;
+  const float* lam; const double* G;           // new lambda, Grams [3][R][R]
+  double* relerr;
+};
+int fitrows_rb_of(int R);
+int fitrows_blocks();
+cudaError_t launch_fitrows(FitRows a, double* part, cudaStream_t st);   // part: fitrows_blocks() x (RB + 1)
+cudaError_t launch_fitinc_plan(const FitPlanArgs& p, cudaStream_t st);
+cudaError_t launch_fitinc_finish(const FitFinishArgs& a, cudaStream_t st);
+cudaError_t launch_fitinc_sum(const FitFinishArgs& a, double* out, cudaStream_t st);
+
 bool margfit_supported(const DenseView& X, int R);
 // qb: every quantised value q = RNE(phi 2^S) of the pass is <= 2^qb (32-bit arithmetic when small)
 cudaError_t launch_marg_fit_stream(const DenseView& X, int64_t nk, int moi, int S, int qb, const float* lam,
