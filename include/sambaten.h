@@ -309,6 +309,38 @@ SAMBATEN_API sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, fl
  * G = X x1 pinv(A) x2 pinv(B) x3 pinv(C) and cc = 100 (1 - sum (G - T)^2 / F), T the
  * superdiagonal unit core.  A, B, C: device float32 [dims][F] row-major; lambda: device
  * float64[F]; cc: host or device float64[1].  fp64 throughout; E_INVALID on bad arguments. */
+/* ---------------------------------------------------------------------------------------
+ * Full-tensor CP-ALS: the evaluation's CP_ALS baseline and relative
+ * fitness, and the distributed initial decomposition.
+ * ------------------------------------------------------------------------------------- */
+
+/* The CP_ALS baseline of the paper's evaluation ("re-compute CP using CP_ALS every time
+ * a new batch update arrives"; P:232 ALS): full CP-ALS at the handle's rank of its CURRENT
+ * tensor (all stored slices), from the Philox U(0,1) point with counter update_id = the
+ * handle's update count and repetition 255 (reading R35), at most max_iters iterations, stop
+ * when |fit - fit_prev| < tol (R11).  Sharded dense handles: collective, the slabs' MTTKRP
+ * partials all-reduced (NCCL), every rank gets the same factors.  The handle's model is not
+ * touched.  A [I][R], B [J][R], C [K][R], lambda [R] (host or device, NULL = not copied);
+ * relerr: 1 - the final ALS fit = relative error of that model; iters: the count.
+ * Errors: E_INVALID (NULL handle, max_iters < 1, sharded COO), E_OOM, E_CUDA. */
+SAMBATEN_API sambaten_status sambaten_recompute(sambaten_t h, int max_iters, double tol, float* A, float* B,
+                                                float* C, float* lambda, double* relerr, int* iters);
+
+/* Relative fitness = ||X - X_SamBaTen|| / ||X - X_CPALS|| of the handle's committed
+ * model against sambaten_recompute's; also returns both relative errors (NULL = not
+ * returned).  Lower is better; 1 = as good as recomputing.  Collective on sharded handles. */
+SAMBATEN_API sambaten_status sambaten_relative_fitness(sambaten_t h, int max_iters, double tol, double* rf,
+                                                       double* relerr_sambaten, double* relerr_baseline);
+
+/* The sharded handle initialised by the DISTRIBUTED full CP-ALS of X0 ("10% as
+ * existing"; R10 Philox init, update_id 0, rep 0; opts->init_max_iters / init_tol): every rank
+ * passes its slab [dist->k0, dist->k0 + dims[2]) of X0; the slabs' MTTKRP partials are
+ * all-reduced and the mode-2 rows all-gathered (NCCL) so every rank holds the same model.
+ * Dense tensors only.  Errors as sambaten_init_factors_dist. */
+SAMBATEN_API sambaten_status sambaten_init_dist(sambaten_t* h, const sambaten_tensor* X0_local,
+                                                const sambaten_dist* dist, int R, int s, int r, uint64_t seed,
+                                                const sambaten_opts* opts);
+
 /* The a4 plan (sambaten_info.als_plan layout) the library would pick for r dense summaries of
  * shape nI x nJ x nK at rank R on the current device (no handle; host call that queries the
  * device's cluster occupancy).  Lets a test assert that a small problem runs the same kernel

@@ -491,6 +491,28 @@ def init_als(X0, cfg, cap_entries, maxit=1000, tol=1e-6):
     return st
 
 
+RECOMPUTE_REP = 255   # reading R35: the CP_ALS baseline's Philox repetition index
+
+
+def recompute(X, R, seed, update_id, maxit, tol):
+    """The paper's CP_ALS baseline ("re-compute CP using CP_ALS every time a new batch
+    update arrives"): full CP-ALS of the whole current tensor X from the Philox point
+    als_init(..., update_id, rep = 255) (reading R35).  Returns (lambda, [A, B, C], fit, iters)."""
+    if isinstance(X, Coo):
+        Y, rows = X, X.dims
+    else:
+        Y = view_ijk(X)
+        rows = Y.shape
+    U0 = als_init(rows, R, seed, update_id, RECOMPUTE_REP)
+    lam, U, fit, it, _ = cp_als(Y, U0, maxit, tol)
+    return lam, U, fit, it
+
+
+def relative_fitness(X, model_s, model_b):
+    """Relative Fitness = ||X - X_SamBaTen|| / ||X - X_BaseLine||: lower is better."""
+    return relative_error(X, *model_s) / relative_error(X, *model_b)
+
+
 class FixedPointRange(Exception):
     pass
 

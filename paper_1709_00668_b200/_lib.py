@@ -110,6 +110,9 @@ def lib():
         "sambaten_corcondia": (i32, [T, ip, vp, vp, vp, vp, vp, vp]),
         "sambaten_getrank": (i32, [T, ip, ip, u64, ip, d, d, C.POINTER(ip), vp, vp]),
         "sambaten_als_plan": (i32, [ip, ip, ip, ip, ip, vp]),
+        "sambaten_recompute": (i32, [vp, ip, d, vp, vp, vp, vp, C.POINTER(d), C.POINTER(ip)]),
+        "sambaten_relative_fitness": (i32, [vp, ip, d, C.POINTER(d), C.POINTER(d), C.POINTER(d)]),
+        "sambaten_init_dist": (i32, [C.POINTER(vp), T, C.POINTER(Dist), ip, ip, ip, u64, O]),
         "sambaten_last_error": (C.c_char_p, []),
         "sambaten_version": (C.c_char_p, []),
     }
@@ -128,6 +131,7 @@ EXPORTED = ["sambaten_default_opts", "sambaten_init", "sambaten_init_factors", "
             "sambaten_mttkrp", "sambaten_cp_als", "sambaten_fit", "sambaten_philox", "sambaten_detlog",
             "sambaten_dist_unique_id", "sambaten_init_factors_dist", "sambaten_batch_partition",
             "sambaten_dist_plan", "sambaten_corcondia", "sambaten_getrank", "sambaten_als_plan",
+            "sambaten_recompute", "sambaten_relative_fitness", "sambaten_init_dist",
             "sambaten_last_error", "sambaten_version"]
 
 
@@ -288,6 +292,28 @@ def sambaten_last_samples(h, Is=None, Js=None, Ks=None):
     n = (C.c_int64 * 3)()
     check(lib().sambaten_last_samples(h, ptr(Is), ptr(Js), ptr(Ks), n))
     return tuple(n)
+
+
+def sambaten_recompute(h, max_iters, tol, A=None, B=None, Cm=None, lam=None):
+    """CP_ALS baseline: full CP-ALS of the handle's current tensor; returns
+    (relative error, iterations); factors copied into the given arrays when not None."""
+    e, it = C.c_double(), C.c_int()
+    check(lib().sambaten_recompute(h, max_iters, tol, ptr(A), ptr(B), ptr(Cm), ptr(lam), C.byref(e), C.byref(it)))
+    return e.value, it.value
+
+
+def sambaten_relative_fitness(h, max_iters, tol):
+    """Relative fitness: (rf, relerr_sambaten, relerr_cp_als)."""
+    rf, es, eb = C.c_double(), C.c_double(), C.c_double()
+    check(lib().sambaten_relative_fitness(h, max_iters, tol, C.byref(rf), C.byref(es), C.byref(eb)))
+    return rf.value, es.value, eb.value
+
+
+def sambaten_init_dist(X0_local, dist, R, s, r, seed, opts=None):
+    h = C.c_void_p()
+    check(lib().sambaten_init_dist(C.byref(h), C.byref(X0_local), C.byref(dist), R, s, r, seed,
+                                   C.byref(opts) if opts else None))
+    return h
 
 
 def sambaten_relative_error(h):

@@ -510,7 +510,8 @@ static sambaten_status init_als_coo(sambaten_s* h);
 // The incremental fit's state of the initial model (one per-component pass over X0; untimed
 // init work) when the updates will report the full fit of a dense handle (full_fit = 1).
 static cudaError_t init_fit_state(sambaten_s* h) {
-  if (h->opts.full_fit != 1 || h->fmt != SAMBATEN_DENSE || h->dist || getenv("SAMBATEN_FULL_FIT_PASS"))
+  if (h->opts.full_fit != 1 || h->fmt != SAMBATEN_DENSE || h->dist || getenv("SAMBATEN_FULL_FIT_PASS") ||
+      !fitrows_supported(h->pitch, h->R))
     return cudaSuccess;
   cudaError_t e = h->misc.ensure(4096);
   if (e != cudaSuccess) return e;
@@ -1386,7 +1387,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   CK(cudaEventRecord(h->ev[7], st));
   // ---- a7: full fit of the new model (optional; with full_fit = 2 it rides on the next a1) --
   const bool fit_now = h->opts.full_fit == 1 || (h->opts.full_fit == 2 && !lag);
-  if (fit_now && h->opts.full_fit == 1 && !getenv("SAMBATEN_FULL_FIT_PASS")) {
+  if (fit_now && h->opts.full_fit == 1 && !getenv("SAMBATEN_FULL_FIT_PASS") && fitrows_supported(h->pitch, R)) {
     // the new model's exact fit kept up to date from the previous one (k_fitinc.cu): the batch's
     // slices plus the rows the merge changed, or one full pass when the plan says so
     CK(fitinc_run(h, V, Ko, Ko, Ko + Kn, b, nb, false, nullptr, true, d_relerr, st));

@@ -332,7 +332,6 @@ struct FitRows {
   const float *U, *Usub, *V, *Vsub;        // J x R and (model rows) x R; Usub / Vsub may be NULL
   const int32_t* kmap;                     // store slice -> model row (sharded) or NULL
   const int* gate; int gate_val;           // run only if *gate == gate_val (NULL: always)
-  int as_in_smem;                          // set by launch_fitrows
 };
 struct FitPlanArgs {
   const float *A0, *A1, *B0, *B1, *C0, *C1;   // old / new model
@@ -351,6 +350,7 @@ struct FitFinishArgs {
   double* relerr;
 };
 int fitrows_rb_of(int R);
+bool fitrows_supported(int64_t pitch, int R);   // pitch % 4 == 0 and the transposed As fits in shared memory
 int fitrows_blocks();
 cudaError_t launch_fitrows(FitRows a, double* part, cudaStream_t st);   // part: fitrows_blocks() x (RB + 1)
 cudaError_t launch_fitinc_plan(const FitPlanArgs& p, cudaStream_t st);

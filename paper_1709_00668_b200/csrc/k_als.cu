@@ -635,8 +635,9 @@ static cudaError_t als_sharded_rb(DenseAls loc, DenseAls glob, const int32_t* km
                                   int kpad, double* stage, double* gathered, const AlsComm& c, cudaStream_t st) {
   const int R = glob.R;
   const int64_t nloc = loc.nK;
-  // loc reads the replicated A, B and its own rows of C; its flags / done are glob's
-  loc.done = glob.done; loc.flags = glob.flags;
+  // loc reads the replicated A, B and its own rows of C; its flags / done are glob's, and its
+  // mode-1 MTTKRP partial lands in glob's M (all-reduced in place there)
+  loc.done = glob.done; loc.flags = glob.flags; loc.M = glob.M;
   int cw, nz, RP;
   col_chunking(loc.nI, &cw, &nz, &RP);
   const int threads0 = ((RP * cw + 31) / 32) * 32;

@@ -25,35 +25,38 @@ namespace sbt {
 
 namespace {
 
-constexpr int kFT = 256;            // threads per block
+constexpr int kFT = 512;            // threads per block (one block per SM: As fills the shared memory)
 constexpr int kFW = kFT / 32;
 
-// One row (j, k) of the store per warp; lane l takes the columns l, l + 32, ... of the row.
-// acc[f] += (sum over the lane's columns of X(i,j,k) As(i,f)) * w(j,k,f): the row weight
-// multiplies the lane partial (linearity), so no reduction per row is needed.  As (I x R)
-// is staged in shared memory when it fits, else read through L1.
+// One row (j, k) of the store per warp; lane l takes the column quads l, l + 32, ... of the
+// row (float4 loads; the store's padding columns are zero).  acc[f] += (sum over the lane's
+// columns of X(i,j,k) As(i,f)) * w(j,k,f): the row weight multiplies the lane partial
+// (linearity), so no reduction per row is needed.  As is staged transposed in shared memory,
+// As_s[f][i] (padded to the pitch with zeros), so a lane reads its four columns of component f
+// with one conflict-free 16-byte load.
 template <int RB>
 __global__ void __launch_bounds__(kFT) fitrows_kernel(FitRows a, double* __restrict__ part) {
   extern __shared__ __align__(16) float As_s[];
   const int R = a.R;
-  if (a.gate && *a.gate != a.gate_val) {   // device-side plan (no host round trip)
+  int64_t nrows;
+  if (a.gate && *a.gate != a.gate_val) nrows = 0;   // device-side plan (no host round trip)
+  else if (a.kind == 0) nrows = (a.k1 - a.k0) * a.J;
+  else {
+    const int nl = *a.nlist;
+    nrows = a.kind == 1 ? (int64_t)nl * (a.k1 - a.k0) : (int64_t)nl * a.J;
+  }
+  if (nrows <= (int64_t)blockIdx.x * kFW) {   // no row for this block: zero partials
     if (threadIdx.x < RB + 1) part[(int64_t)blockIdx.x * (RB + 1) + threadIdx.x] = 0.0;
     return;
   }
-  const bool smem_as = a.as_in_smem;
-  if (smem_as) {
-    for (int e = threadIdx.x; e < a.I * R; e += blockDim.x) As_s[e] = a.As[e];
-    __syncthreads();
+  const int P = (int)a.pitch;
+  for (int e = threadIdx.x; e < R * P; e += blockDim.x) {
+    const int f = e / P, i = e - f * P;
+    As_s[e] = i < a.I ? a.As[(int64_t)i * R + f] : 0.f;
   }
-  const float* As = smem_as ? As_s : a.As;
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int64_t nrows;
-  int nl = 0;
-  if (a.kind == 0) nrows = (a.k1 - a.k0) * a.J;
-  else {
-    nl = *a.nlist;
-    nrows = a.kind == 1 ? (int64_t)nl * (a.k1 - a.k0) : (int64_t)nl * a.J;
-  }
+  const int nq = P / 4;
   double acc[RB + 1];
 #pragma unroll
   for (int f = 0; f <= RB; ++f) acc[f] = 0.0;
@@ -62,21 +65,33 @@ __global__ void __launch_bounds__(kFT) fitrows_kernel(FitRows a, double* __restr
     if (a.kind == 0) { k = a.k0 + row / a.J; j = row - (k - a.k0) * a.J; }
     else if (a.kind == 1) { const int64_t t = row / (a.k1 - a.k0); j = a.list[t]; k = a.k0 + (row - t * (a.k1 - a.k0)); }
     else { const int64_t t = row / a.J; j = row - t * a.J; k = a.list[t]; }
-    // k is a slice of the store: local (sharded) -> model row through kmap; kind 2 lists hold
-    // store slices too (the caller maps)
-    const int64_t kg = a.kmap ? a.kmap[k] : k;
-    const float* x = a.X + (k * a.J + j) * a.pitch;
+    const int64_t kg = a.kmap ? a.kmap[k] : k;   // store slice -> model row (sharded)
+    const float4* x = reinterpret_cast<const float4*>(a.X + (k * a.J + j) * a.pitch);
     float d[RB];
 #pragma unroll
     for (int f = 0; f < RB; ++f) d[f] = 0.f;
     float ss = 0.f;
-    for (int i = lane; i < a.I; i += 32) {
-      const float v = x[i];
-      ss = fmaf(v, v, ss);
-      const float* ar = As + (int64_t)i * R;
+    // four quads per step: four 16-byte loads in flight per lane before the arithmetic
+    for (int q0 = lane; q0 < nq; q0 += 128) {
+      float4 v[4];
 #pragma unroll
-      for (int f = 0; f < RB; ++f)
-        if (f < R) d[f] = fmaf(v, ar[f], d[f]);
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + 32 * u;
+        v[u] = q < nq ? __ldg(x + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + 32 * u;
+        if (q >= nq) break;
+        ss = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, fmaf(v[u].w, v[u].w, ss))));
+#pragma unroll
+        for (int f = 0; f < RB; ++f) {
+          if (f < R) {
+            const float4 w = reinterpret_cast<const float4*>(As_s + f * P)[q];
+            d[f] = fmaf(v[u].x, w.x, fmaf(v[u].y, w.y, fmaf(v[u].z, w.z, fmaf(v[u].w, w.w, d[f]))));
+          }
+        }
+      }
     }
 #pragma unroll
     for (int f = 0; f < RB; ++f) {
@@ -89,7 +104,7 @@ __global__ void __launch_bounds__(kFT) fitrows_kernel(FitRows a, double* __restr
     }
     acc[RB] += (double)ss;
   }
-  // block reduction (fixed order): warp butterflies, then warp 0 over the warps
+  // block reduction (fixed order): warp butterflies, then over the warps
   __shared__ double red[kFW][RB + 1];
 #pragma unroll
   for (int f = 0; f <= RB; ++f) {
@@ -157,29 +172,39 @@ __global__ void fitinc_plan_kernel(FitPlanArgs p) {
   }
 }
 
-// P' (incremental: P + the three term partials; full: the full pass's partials), ||X'||^2,
-// the relative error from lam' and the Grams; writes the new state (valid).
+// Sum of the block partials of the terms the plan selected (terms 0..2: incremental; term 3:
+// the full pass) into out[R + 1]: thread t < R + 1 sums column t over the terms and blocks in a
+// fixed order with four independent chains (deterministic; no serial chain of 4 x blocks).
+__device__ void fitinc_terms_sum(const FitFinishArgs& a, bool incr, double* out) {
+  const int R = a.R, RB = a.RB, t = threadIdx.x;
+  if (t > R) return;
+  const int col = t < R ? t : RB;   // column RB holds the sums of squares
+  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int tm = 0; tm < 4; ++tm) {
+    const double* pt = a.terms[tm];
+    if (!pt || incr != (tm < 3)) continue;
+    if (t == R && (tm == 1 || tm == 2)) continue;   // ||X||^2 grows by the new slices only
+    for (int b = 0; b < a.nparts[tm]; ++b) s4[b & 3] += pt[(int64_t)b * (RB + 1) + col];
+  }
+  out[t] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+}
+
+// P' (incremental: P + the selected terms; full: the full pass), ||X'||^2, the relative
+// error from lam' and the Grams; writes the new state (valid).
 __global__ void fitinc_finish_kernel(FitFinishArgs a) {
-  if (threadIdx.x != 0) return;
-  const int R = a.R, RB = a.RB;
+  __shared__ double sums[kMaxR + 1];
+  const int R = a.R;
   const bool incr = *a.mode == 1;
+  if (a.reduced) {
+    if (threadIdx.x <= R) sums[threadIdx.x] = a.reduced[threadIdx.x];
+  } else {
+    fitinc_terms_sum(a, incr, sums);
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
   double P[kMaxR];
-  double xsq;
-  for (int f = 0; f < R; ++f) P[f] = incr ? a.st_old[f] : 0.0;
-  xsq = incr ? a.st_old[R] : 0.0;
-  for (int t = 0; t < 4; ++t) {
-    const double* pt = a.terms[t];
-    if (!pt) continue;
-    if (incr != (t < 3)) continue;   // terms 0..2: incremental; term 3: full pass
-    for (int b = 0; b < a.nparts[t]; ++b) {
-      for (int f = 0; f < R; ++f) P[f] += pt[(int64_t)b * (RB + 1) + f];
-      if (t == 0 || t == 3) xsq += pt[(int64_t)b * (RB + 1) + RB];   // ||batch||^2 / ||X'||^2
-    }
-  }
-  if (a.reduced) {   // sharded: the per-rank sums were all-reduced into reduced[R + 1]
-    for (int f = 0; f < R; ++f) P[f] = (incr ? a.st_old[f] : 0.0) + a.reduced[f];
-    xsq = (incr ? a.st_old[R] : 0.0) + a.reduced[R];
-  }
+  for (int f = 0; f < R; ++f) P[f] = (incr ? a.st_old[f] : 0.0) + sums[f];
+  const double xsq = (incr ? a.st_old[R] : 0.0) + sums[R];
   double inner = 0.0, mn = 0.0;
   for (int f = 0; f < R; ++f) inner += (double)a.lam[f] * P[f];
   for (int f = 0; f < R; ++f)
@@ -192,25 +217,14 @@ __global__ void fitinc_finish_kernel(FitFinishArgs a) {
   a.st_new[R + 1] = 1.0;
 }
 
-// sum of the block partials of every term into out[R + 1] (sharded: before the all-reduce)
+// the selected terms' sums into out[R + 1] (sharded: before the all-reduce)
 __global__ void fitinc_sum_kernel(FitFinishArgs a, double* out) {
-  if (threadIdx.x != 0) return;
-  const int R = a.R, RB = a.RB;
-  const bool incr = *a.mode == 1;
-  for (int f = 0; f <= R; ++f) out[f] = 0.0;
-  for (int t = 0; t < 4; ++t) {
-    const double* pt = a.terms[t];
-    if (!pt || incr != (t < 3)) continue;
-    for (int b = 0; b < a.nparts[t]; ++b) {
-      for (int f = 0; f < R; ++f) out[f] += pt[(int64_t)b * (RB + 1) + f];
-      if (t == 0 || t == 3) out[R] += pt[(int64_t)b * (RB + 1) + RB];
-    }
-  }
+  fitinc_terms_sum(a, *a.mode == 1, out);
 }
 
 template <int RB>
 cudaError_t fitrows_rb(const FitRows& a, double* part, int nblocks, cudaStream_t st) {
-  size_t smem = a.as_in_smem ? sizeof(float) * (size_t)a.I * a.R : 0;
+  const size_t smem = sizeof(float) * (size_t)a.pitch * a.R;
   cudaFuncSetAttribute(fitrows_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fitrows_kernel<RB><<<nblocks, kFT, smem, st>>>(a, part);
   return cudaGetLastError();
@@ -220,10 +234,14 @@ cudaError_t fitrows_rb(const FitRows& a, double* part, int nblocks, cudaStream_t
 
 int fitrows_rb_of(int R) { return R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : 32; }
 
-int fitrows_blocks() { return kNumSMs * 4; }
+int fitrows_blocks() { return kNumSMs * 2; }
+
+bool fitrows_supported(int64_t pitch, int R) {
+  return pitch % 4 == 0 && (size_t)pitch * R * sizeof(float) <= 200 * 1024;
+}
 
 cudaError_t launch_fitrows(FitRows a, double* part, cudaStream_t st) {
-  a.as_in_smem = (size_t)a.I * a.R * sizeof(float) <= 160 * 1024;
+  if (!fitrows_supported(a.pitch, a.R)) return cudaErrorInvalidValue;
   const int nb = fitrows_blocks();
   switch (fitrows_rb_of(a.R)) {
     case 4: return fitrows_rb<4>(a, part, nb, st);
@@ -240,12 +258,12 @@ cudaError_t launch_fitinc_plan(const FitPlanArgs& p, cudaStream_t st) {
 }
 
 cudaError_t launch_fitinc_finish(const FitFinishArgs& a, cudaStream_t st) {
-  fitinc_finish_kernel<<<1, 32, 0, st>>>(a);
+  fitinc_finish_kernel<<<1, 64, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fitinc_sum(const FitFinishArgs& a, double* out, cudaStream_t st) {
-  fitinc_sum_kernel<<<1, 32, 0, st>>>(a, out);
+  fitinc_sum_kernel<<<1, 64, 0, st>>>(a, out);
   return cudaGetLastError();
 }
 

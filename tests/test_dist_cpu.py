@@ -234,3 +234,47 @@ def test_sharded_coo_summaries_equal_full_gather(world, tmp_path):
     out = tmp_path / "done"
     _run(world, _coo_worker, str(out))
     assert out.read_text() == "ok"
+
+
+# --------------------------------------------------------------------------- 3. full-tensor ALS
+def _full_als_worker(rank, world, iters):
+    """The sharded full-tensor CP-ALS (run_dense_als_sharded) written with
+    the oracle's building blocks: slab MTTKRP partials of modes 0 and 1 all-reduced, mode-2
+    rows all-gathered, replicated solves -- must reproduce the single-process oracle CP-ALS."""
+    T, truth = planted_dense(18, 15, 23, 3, noise=0.01, seed=62)
+    K = T.shape[0]
+    k0, kn = partition(K, world, rank)
+    slab = O.view_ijk(T[k0:k0 + kn]).astype(np.float64)
+    U = O.als_init(O.view_ijk(T).shape, 3, 9, 0, 0)
+    U_ref = [u.copy() for u in U]
+    R = 3
+    for _ in range(iters):
+        for m in range(3):
+            V = np.ones((R, R))
+            for n in range(3):
+                if n != m:
+                    V *= U[n].T @ U[n]
+            loc = [U[0], U[1], U[2][k0:k0 + kn]]
+            M = O.mttkrp(slab, loc, m)
+            if m < 2:
+                t = torch.from_numpy(M.copy())
+                dist.all_reduce(t)
+                M = t.numpy()
+            else:
+                parts = [None] * world
+                dist.all_gather_object(parts, (k0, M))
+                M = np.zeros((K, R))
+                for b0, Mp in parts:
+                    M[b0:b0 + Mp.shape[0]] = Mp
+            Um, _ = O.solve_normal(M, V)
+            lam = np.sqrt(np.sum(Um * Um, axis=0))
+            U[m] = Um / np.where(lam > 0, lam, 1.0)
+    lam_ref, U_ref, fit_ref, it_ref, _ = O.cp_als(O.view_ijk(T), U_ref, iters, 0.0)
+    for a, b in zip(U, U_ref):
+        assert np.allclose(a, b, rtol=1e-9, atol=1e-12)
+    assert np.allclose(lam, lam_ref, rtol=1e-9)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_full_als_decomposition(world):
+    _run(world, _full_als_worker, 6)

@@ -42,7 +42,9 @@ for b in batches:
         out.append((A, B, C, lam, info.fit_full, info.reps_rejected_mask, info.fit_full_prev))
     for x, y in zip(out[0][:4], out[1][:4]):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
-    assert out[0][4] == out[1][4] and out[0][5] == out[1][5] and out[0][6] == out[1][6], (out[0][4:], out[1][4:])
+    # the single-GPU handle keeps its full fit incrementally (k_fitinc.cu), the sharded one by a
+    # pass over the slabs: the same quantity in two summation orders
+    assert abs(out[0][4] - out[1][4]) <= 1e-6 and out[0][5] == out[1][5] and out[0][6] == out[1][6], (out[0][4:], out[1][4:])
     if opts.full_fit == 2:
         assert out[0][4] == -1.0 and 0.9 < out[0][6] <= 1.0
 L.sambaten_destroy(hd); L.sambaten_destroy(hs)

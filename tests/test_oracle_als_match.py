@@ -179,3 +179,33 @@ def test_fms_properties():
     assert O.fms(other, orth) == 0.0
     m2 = _model(10, 9, 8, 4, 10)
     assert O.fms(m, m2) == pytest.approx(O.fms(m2, m), abs=1e-12)
+
+
+def test_recompute_is_cp_als_from_the_r35_point():
+    """R35: the CP_ALS baseline starts from Philox repetition 255 of the current update id; on a
+    noiseless planted tensor it converges to the planted model (fit > 0.999 at 500 iterations,
+    R27) and the relative fitness of the planted truth against it is ~1 (both exact)."""
+    from synth import planted_dense
+    T, truth = planted_dense(30, 28, 26, 3, noise=0.0, seed=61)
+    lam, U, fit, it = O.recompute(T, 3, seed=4, update_id=2, maxit=500, tol=1e-12)
+    assert fit > 0.999
+    U0 = O.als_init(O.view_ijk(T).shape, 3, 4, 2, 255)
+    lam2, U2, fit2, it2, _ = O.cp_als(O.view_ijk(T), U0, 500, 1e-12)
+    assert fit == fit2 and all(np.array_equal(a, b) for a, b in zip(U, U2))
+    # a different repetition index starts elsewhere (the stream is keyed by rep)
+    assert not np.array_equal(U0[0], O.als_init(O.view_ijk(T).shape, 3, 4, 2, 0)[0])
+
+
+def test_relative_fitness_definition_pins():
+    """RF(X, M, M) = 1; a model with twice the baseline's residual has RF = 2 (the
+    residual of lam * M scales linearly when X = 0 outside the model's span: here X = M_b + E
+    with E orthogonal to both models' span is built by an exact rank-1 construction)."""
+    rng = np.random.default_rng(3)
+    a, b, c = (rng.random(n) for n in (5, 4, 3))
+    X = np.einsum("i,j,k->kji", a, b, c).astype(np.float32)
+    m = (np.ones(1), a[:, None], b[:, None], c[:, None])
+    assert O.relative_fitness(X, m, m) == 1.0
+    # scaled models: residual |1 - s| * ||X|| -> RF = |1 - s1| / |1 - s2|
+    m1 = (np.array([0.8]), a[:, None], b[:, None], c[:, None])
+    m2 = (np.array([0.9]), a[:, None], b[:, None], c[:, None])
+    assert abs(O.relative_fitness(X, m1, m2) - 2.0) < 1e-6
