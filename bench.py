@@ -60,6 +60,8 @@ def parse():
                    help="1 (default): the committed model's fit (dense: incremental -- the batch plus the "
                         "rows the merge changed, k_fitinc.cu); 2: lag-1 fit inside the next update's a1 pass "
                         "(SURVEY 8(f) NEXT #1; dense only, COO configs use 1)")
+    p.add_argument("--no-recompute", action="store_true", help="skip the CP_ALS recompute / relative fitness report")
+    p.add_argument("--recompute-iters", type=int, default=60, help="CP_ALS baseline iteration cap (P:441 uses 1000)")
     p.add_argument("--sharded", action="store_true",
                    help="use the sharded (NCCL) handle even at N=1 (always used at N>1, dense configs)")
     return p.parse_args()
@@ -713,6 +715,24 @@ def main():
                        "ms_per_step": 1000.0 * e2e_tot / len(e2e_times),
                        "step_ms": {f"a{k}": statistics.mean(inf["step_ms"][k] for inf in e2e_infos)
                                    for k in range(8)}}
+    if not args.no_recompute and not work.coo:
+        # the paper's evaluation: CP_ALS recomputed on the current tensor (the
+        # baseline arm; P:441 tol 1e-5, capped iterations) and Relative Fitness of the committed
+        # model against it; device time of the recompute next to the update's
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        rf, es, eb = L.sambaten_relative_fitness(h, args.recompute_iters, 1e-5)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_rc = e0.elapsed_time(e1)
+        line["relative_fitness"] = {
+            "value": rf, "relerr_sambaten": es, "relerr_cp_als": eb, "cp_als_max_iters": args.recompute_iters,
+            "cp_als_tol": 1e-5, "recompute_plus_fit_ms": t_rc,
+            "update_ms": 1000.0 * tot / args.steps,
+            "speedup_vs_recompute": t_rc / (1000.0 * tot / args.steps),
+            "note": "P:417-421 Relative Fitness = ||X - X_SamBaTen|| / ||X - X_CP_ALS||; CP_ALS = full CP-ALS of "
+                    "the current tensor from the R35 Philox point (sambaten_recompute; SURVEY 8(f) NEXT #3)"}
     line["als_iters_per_rep"] = statistics.mean(inf["als_iters_sum"] for inf in infos) / (w.r / (world if sharded else 1))
     line["als_plan_last"] = infos[-1]["als_plan"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -132,7 +132,9 @@ typedef struct {
                                /* opts.getrank reduced it, R33); entries >= r are 0           */
   int als_plan[4];             /* the a4 launch plan this update ran (dense handles):         */
                                /* [0] kind: 0 multi-kernel ALS, 1 cluster ALS (one thread-    */
-                               /* block cluster per repetition), -1 none (COO / GetRank);     */
+                               /* block cluster per repetition), 2 grid ALS (CTA groups of one */
+                               /* cooperative grid, global-memory exchange), -1 none (COO /   */
+                               /* GetRank);                                                   */
                                /* [1] CTAs per repetition, [2] RB (padded rank width),        */
                                /* [3] 1 if D lives in shared memory, 0 if in global memory     */
   int64_t summary_entries;     /* entries (dense) or nonzeros (COO) of the summaries this      */

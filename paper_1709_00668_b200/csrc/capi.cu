@@ -296,7 +296,7 @@ static cudaError_t fitinc_run(sambaten_s* h, const DenseView& V, int64_t Ko_stor
 }
 
 static void set_plan_report(sambaten_s* h, bool cluster, const ClusterPlan& pl, int R) {
-  h->als_plan[0] = cluster ? 1 : 0;
+  h->als_plan[0] = cluster ? (pl.grid ? 2 : 1) : 0;
   h->als_plan[1] = cluster ? pl.CS : 1;
   h->als_plan[2] = cluster ? pl.RB : R;
   h->als_plan[3] = cluster ? pl.dsh : 0;
@@ -1815,7 +1815,7 @@ extern "C" sambaten_status sambaten_als_plan(int nI, int nJ, int nK, int R, int 
   ClusterPlan pl{};
   const bool ok = r >= 2 && !getenv("SAMBATEN_NO_CLUSTER_ALS") && plan_als_cluster(a, &pl);
   cudaGetLastError();
-  plan[0] = ok ? 1 : 0;
+  plan[0] = ok ? (pl.grid ? 2 : 1) : 0;
   plan[1] = ok ? pl.CS : 1;
   plan[2] = ok ? pl.RB : R;
   plan[3] = ok ? pl.dsh : 0;

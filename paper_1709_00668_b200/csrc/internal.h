@@ -96,7 +96,10 @@ cudaError_t launch_als_init(const DenseAls& a, uint64_t seed, uint32_t update_id
 cudaError_t launch_als_init_factors(const DenseAls& a, uint64_t seed, uint32_t update_id,
                                     uint32_t rep0, cudaStream_t st, uint32_t rep_stride = 1);
 // cluster-per-repetition ALS (k_als_cluster.cu): all iterations in one launch
-struct ClusterPlan { int CS = 0; size_t smem = 0; int act = 0; int RB = 0; int stage_fl = 0; int dsh = 0; };
+struct ClusterPlan {
+  int CS = 0; size_t smem = 0; int act = 0; int RB = 0; int stage_fl = 0; int dsh = 0;
+  int grid = 0;   // 1: CS plain CTAs per repetition in one cooperative grid (global-memory comm)
+};
 // row pitch (floats) of the summary layouts Y[u][q][p] / Yt[u][p][q] the cluster path reads
 int cluster_pitch(int n);
 bool plan_als_cluster(const DenseAls& a, ClusterPlan* pl);

@@ -711,13 +711,72 @@ __device__ __forceinline__ int team_stages(int team, int nu, int NT, int nrow, i
   return nsl * nch;
 }
 
-template <int RB>
+// Grid communication (GRID = true): the CS CTAs of a repetition are ordinary CTAs of one
+// co-resident (cooperative) grid instead of a thread-block cluster, so a repetition can span
+// more SMs than a cluster slot allows (148 / r of them).  What the cluster path reads from its
+// peers' shared memory (partial MTTKRPs P, partial Grams Gp, scalars sc) each CTA also exports
+// to its slot of a global buffer; solved rows are pushed to a global copy of U_m; the cluster
+// barrier becomes a per-repetition arrival counter (release / acquire at gpu scope).  Peer
+// data is read with ld.global.cg (L2; L1 is not coherent across SMs).
+struct GridComm {
+  double* x;          // [r][CS][xstride] exported P | Gp | sc
+  float* u;           // [r][2][max(nI, nJ) * US] pushed rows of U_0, U_1
+  unsigned* bar;      // [r] arrival counters (zeroed before the launch)
+  int xstride;        // doubles per CTA slot
+  int offP, offG, offS;
+  int ustride;        // floats per (rep, mode) row block
+};
+
+__device__ __forceinline__ void grid_rep_sync(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int RB, bool GRID>
 __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS, float* Dglob,
-                                                             int stage_fl, int dshw) {
+                                                             int stage_fl, int dshw, GridComm gc) {
   // dshw: bit 0 = D in shared memory (plan), bit 1 = narrow pass A (SAMBATEN_ALS_NARROW_A)
   const int dsh = dshw & 1;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
+  const int rank = GRID ? (int)(blockIdx.x % CS) : (int)cg::this_cluster().block_rank();
+  unsigned bar_target = 0;
+  auto csync = [&]() {
+    if constexpr (GRID) {
+      bar_target += (unsigned)CS;
+      grid_rep_sync(gc.bar + blockIdx.x / CS, bar_target);
+    } else {
+      cg::this_cluster().sync();
+    }
+  };
+  double* gx_me = GRID ? gc.x + ((int64_t)(blockIdx.x / CS) * CS + rank) * gc.xstride : nullptr;
+  double* gx_rep = GRID ? gc.x + (int64_t)(blockIdx.x / CS) * CS * gc.xstride : nullptr;
+  // sum over the repetition's CTAs (fixed rank order) of element idx of an exported array
+  auto csum = [&](double* local, int goff, int idx) -> double {
+    if constexpr (GRID) {
+      double v[16];
+      double s = 0.0;
+      int c = 0;
+      for (; c + 16 <= CS; c += 16) {
+#pragma unroll
+        for (int t = 0; t < 16; ++t) v[t] = __ldcg(gx_rep + (int64_t)(c + t) * gc.xstride + goff + idx);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) s += v[t];
+      }
+      for (; c < CS; ++c) s += __ldcg(gx_rep + (int64_t)c * gc.xstride + goff + idx);
+      return s;
+    } else {
+      (void)goff;
+      return cluster_sum(local, idx, CS);
+    }
+  };
   const int rep = blockIdx.x / CS;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int R = a.R, nI = a.nI, nJ = a.nJ, nK = a.nK;
@@ -805,10 +864,10 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       s += v * v;
     }
     s = block_sum_d(s, s_red);
-    if (tid == 0) sc[0] = s;
+    if (tid == 0) { sc[0] = s; if (GRID) gx_me[gc.offS + 0] = s; }
   }
-  cluster.sync();
-  const double ysq = cluster_sum(sc, 0, CS);
+  csync();
+  const double ysq = csum(sc, gc.offS, 0);
   PH(0);
 
   double fit = 0.0, fit_prev = 0.0;
@@ -858,7 +917,11 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         }
         PH(6);
       }
-      cluster.sync();   // S1: partials of every CTA complete
+      if constexpr (GRID) {   // export the partial MTTKRP
+        const int np = (m == 0 ? nI : nJ) * RB;
+        for (int e = tid; e < np; e += kCT) gx_me[gc.offP + e] = P[e];
+      }
+      csync();   // S1: partials of every CTA complete
       PH(m == 0 ? 2 : 8);
       // ---- rows [c0, c1) of this mode: sum the CS partials, solve, partial Gram ----
       const int c0 = min(n, rank * ch), c1 = min(n, c0 + ch);
@@ -866,7 +929,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
 #pragma unroll 1
       for (int e = tid; e < nr * R; e += kCT) {
         const int pl = e / R, f = e - pl * R;
-        Msh[pl * RB + f] = cluster_sum(P, (c0 + pl) * RB + f, CS);
+        Msh[pl * RB + f] = csum(P, gc.offP, (c0 + pl) * RB + f);
       }
       __syncthreads();
       float* Us = m == 0 ? U0s : U1s;
@@ -879,7 +942,12 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         // push the solved row (unnormalised, fp32) into every CTA's copy of U_m: no CTA reads
         // U_m between S1 and S2 (pass A reads U1/U2, pass B U0/U2), and S2 publishes the stores
         const float xf = __double2float_rn(s);
-        for (int c = 0; c < CS; ++c) cluster.map_shared_rank(Us, c)[(c0 + pl) * US + f] = xf;
+        if constexpr (GRID) {
+          gc.u[((int64_t)(blockIdx.x / CS) * 2 + m) * gc.ustride + (c0 + pl) * US + f] = xf;
+        } else {
+          cg::cluster_group cluster = cg::this_cluster();
+          for (int c = 0; c < CS; ++c) cluster.map_shared_rank(Us, c)[(c0 + pl) * US + f] = xf;
+        }
       }
       __syncthreads();
 #pragma unroll 1
@@ -888,12 +956,20 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         double s = 0.0;
         for (int pl = 0; pl < nr; ++pl) s += Xun[pl * RB + f] * Xun[pl * RB + g];
         Gp[m * RB * RB + pr] = s;
+        if (GRID) gx_me[gc.offG + m * RB * RB + pr] = s;
       }
       PH(m == 0 ? 3 : 9);
-      cluster.sync();   // S2: solved rows and partial Grams of every CTA complete
+      csync();   // S2: solved rows and partial Grams of every CTA complete
       PH(m == 0 ? 4 : 10);
+      if constexpr (GRID) {   // pull every CTA's solved rows into the local copy of U_m
+        const float* src = gc.u + ((int64_t)(blockIdx.x / CS) * 2 + m) * gc.ustride;
+        for (int e = tid; e < n * US; e += kCT) {
+          const int p = e / US, f = e - p * US;
+          if (f < R) Us[e] = __ldcg(src + e);
+        }
+      }
 #pragma unroll 1
-      for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = cluster_sum(Gp, m * RB * RB + pr, CS);
+      for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = csum(Gp, gc.offG, m * RB * RB + pr);
       __syncthreads();
       if (tid < R) {
         lam[tid] = sqrt(Gs[tid * R + tid]);
@@ -989,7 +1065,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         inner += Xun2[ul * RB + f] * Msh[ul * RB + f];
       }
       inner = block_sum_d(inner, s_red);
-      if (tid == 0) sc[1] = inner;
+      if (tid == 0) { sc[1] = inner; if (GRID) gx_me[gc.offS + 1] = inner; }
     }
 #pragma unroll 1
     for (int pr = tid; pr < RR; pr += kCT) {
@@ -997,13 +1073,14 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       double s = 0.0;
       for (int ul = 0; ul < nu; ++ul) s += Xun2[ul * RB + f] * Xun2[ul * RB + g];
       Gp[2 * RB * RB + pr] = s;
+      if (GRID) gx_me[gc.offG + 2 * RB * RB + pr] = s;
     }
     PH(13);
-    cluster.sync();   // S3
+    csync();   // S3
     PH(14);
 #pragma unroll 1
-    for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = cluster_sum(Gp, 2 * RB * RB + pr, CS);
-    if (tid == kCT - 1) s_inner = cluster_sum(sc, 1, CS);   // the fit's <Y, M>, fetched alongside
+    for (int pr = tid; pr < RR; pr += kCT) Gs[pr] = csum(Gp, gc.offG, 2 * RB * RB + pr);
+    if (tid == kCT - 1) s_inner = csum(sc, gc.offS, 1);   // the fit's <Y, M>, fetched alongside
     __syncthreads();
     if (tid < R) {
       lam[tid] = sqrt(Gs[tid * R + tid]);
@@ -1078,7 +1155,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
       a.ysq[rep] = ysq; a.done[rep] = 1;
     }
   }
-  cluster.sync();   // keep every CTA's shared memory alive until all remote reads are done
+  if constexpr (!GRID) cg::this_cluster().sync();   // keep every CTA's shared memory alive until all remote reads are done
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1090,90 +1167,138 @@ static int rb_of(int R) {
   return R <= 4 ? 4 : R <= 8 ? 8 : R <= 10 ? 10 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
 }
 
-template <int RB>
+template <int RB, bool GRID>
 static cudaError_t cluster_setup(int CS, size_t smem) {
-  auto k = als_cluster_kernel<RB>;
+  auto k = als_cluster_kernel<RB, GRID>;
   (void)smem;   // always allow the cap: plans of several shapes share the kernel
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemCap);
   if (e != cudaSuccess) return e;
-  if (CS > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (!GRID && CS > 8) e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return e;
 }
 
+// cluster launch (one cluster of CS CTAs per repetition) or grid launch (cooperative: every CTA
+// co-resident, CS consecutive CTAs per repetition)
 static void fill_cfg(cudaLaunchConfig_t* cfg, cudaLaunchAttribute* attr, int CS, int nclusters,
-                     size_t smem, cudaStream_t st) {
+                     size_t smem, cudaStream_t st, bool grid = false) {
   *cfg = cudaLaunchConfig_t{};
   cfg->gridDim = dim3((unsigned)(CS * nclusters), 1, 1);
   cfg->blockDim = dim3(kCT, 1, 1);
   cfg->dynamicSmemBytes = smem;
   cfg->stream = st;
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
+  if (grid) {
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+  } else {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  }
   cfg->attrs = attr;
   cfg->numAttrs = 1;
 }
 
+// shared-memory layout of a plan with CS CTAs per repetition (D in shared memory when the
+// rings keep stages of >= 4 rows of the wider layout); false if nothing fits
+template <int RB>
+static bool plan_layout(const DenseAls& a, int CS, ClLayout* out, int* dsh_out) {
+  const int rowmax = pitch4(a.nI > a.nJ ? a.nI : a.nJ);
+  const int slice_fl = rowmax * (a.nI > a.nJ ? a.nJ : a.nI);
+  int dsh = -1;
+  for (int d = getenv("SAMBATEN_ALS_GLOBAL_D") ? 0 : 1; d >= 0 && dsh < 0; --d) {
+    const ClLayout L0 = cl_layout(a.nI, a.nJ, a.nK, RB, CS, 4, d);
+    const size_t fixed = L0.stage;   // the rings are the last region of the layout
+    if (fixed + sizeof(float) * 4 * RB * kCT > kSmemCap) continue;
+    int sfl = (int)((kSmemCap - fixed) / (sizeof(float) * kTS * L0.NT)) & ~3;
+    if (sfl > ((slice_fl + 3) & ~3)) sfl = (slice_fl + 3) & ~3;
+    if (sfl > 12288) sfl = 12288;
+    if (d == 1 && sfl < 4 * rowmax) continue;
+    const ClLayout L = cl_layout(a.nI, a.nJ, a.nK, RB, CS, sfl, d);
+    if (L.total <= kSmemCap) { dsh = d; *out = L; }
+  }
+  *dsh_out = dsh;
+  return dsh >= 0;
+}
+
+// cost model: a team (warp group) streams whole slices; ~8 busy warps saturate an SM's issue
+// slots, so a CTA's pass time ~ nu / min(busy teams * warps per team, 8) * warps per team
+static double plan_cost(const ClLayout& L, int nK, int CS, double waves) {
+  const int nu = (nK + CS - 1) / CS;
+  const int wpt = L.T / 32;
+  const int busy = nu < L.NT ? nu : L.NT;
+  const double rate = (double)(busy * wpt < 8 ? busy * wpt : 8) / wpt;   // slices in parallel
+  return waves * (double)nu / rate + 1e-3 * waves + 1e-5 * CS;
+}
 
 template <int RB>
 static bool plan_rb(const DenseAls& a, ClusterPlan* pl) {
   if (a.nI > 2 * kCT || a.nJ > 2 * kCT) return false;
-  // the stage size: what is left of the smem budget, split over kNS stages, capped at one
-  // slice of the larger layout and at 48 KB
   double best = 1e300;
   bool found = false;
-  for (int CS = 16; CS >= 1; --CS) {
+  const char* force = getenv("SAMBATEN_ALS_GRID");   // "0": clusters only, "1": grid only
+  const bool try_cluster = !force || force[0] != '1';
+  const bool try_grid = !force || force[0] != '0';
+  for (int CS = 16; CS >= 1 && try_cluster; --CS) {
     if (CS > a.nK) continue;
-    // D in shared memory when the rings keep stages of >= 4 rows of the wider layout
-    const int rowmax = pitch4(a.nI > a.nJ ? a.nI : a.nJ);
-    const int slice_fl = rowmax * (a.nI > a.nJ ? a.nJ : a.nI);
     ClLayout L{};
     int dsh = -1;
-    for (int d = getenv("SAMBATEN_ALS_GLOBAL_D") ? 0 : 1; d >= 0 && dsh < 0; --d) {
-      const ClLayout L0 = cl_layout(a.nI, a.nJ, a.nK, RB, CS, 4, d);
-      const size_t fixed = L0.stage;   // the rings are the last region of the layout
-      if (fixed + sizeof(float) * 4 * RB * kCT > kSmemCap) continue;
-      int sfl = (int)((kSmemCap - fixed) / (sizeof(float) * kTS * L0.NT)) & ~3;
-      if (sfl > ((slice_fl + 3) & ~3)) sfl = (slice_fl + 3) & ~3;
-      if (sfl > 12288) sfl = 12288;
-      if (d == 1 && sfl < 4 * rowmax) continue;
-      L = cl_layout(a.nI, a.nJ, a.nK, RB, CS, sfl, d);
-      if (L.total <= kSmemCap) dsh = d;
-    }
-    if (dsh < 0) continue;
-    if (cluster_setup<RB>(CS, L.total) != cudaSuccess) { cudaGetLastError(); continue; }
+    if (!plan_layout<RB>(a, CS, &L, &dsh)) continue;
+    if (cluster_setup<RB, false>(CS, L.total) != cudaSuccess) { cudaGetLastError(); continue; }
     cudaLaunchConfig_t cfg;
     cudaLaunchAttribute attr[1];
     fill_cfg(&cfg, attr, CS, 1, L.total, nullptr);
     int act = 0;
-    if (cudaOccupancyMaxActiveClusters(&act, als_cluster_kernel<RB>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&act, als_cluster_kernel<RB, false>, &cfg) != cudaSuccess) {
       cudaGetLastError();
       act = 0;
     }
     if (act < 1) continue;
-    // time ~ waves * slices per team
-    const double waves = (double)((a.r + act - 1) / act);
-    const int nu = (a.nK + CS - 1) / CS;
-    // model: a team (warp group) streams whole slices; ~8 busy warps saturate an SM's issue
-    // slots, so a CTA's pass time ~ nu / min(busy teams * warps per team, 8) * warps per
-    // team.  Ties: fewer waves, then the smaller cluster (cheaper DSMEM reductions).
-    const int wpt = L.T / 32;
-    const int busy = nu < L.NT ? nu : L.NT;
-    const double rate = (double)(busy * wpt < 8 ? busy * wpt : 8) / wpt;   // slices in parallel
-    const double t = waves * (double)nu / rate + 1e-3 * waves + 1e-5 * CS;
+    const double t = plan_cost(L, a.nK, CS, (double)((a.r + act - 1) / act));
     if (getenv("SAMBATEN_DEBUG"))
-      fprintf(stderr, "[sambaten]   plan candidate CS=%d act=%d nu=%d NT=%d T=%d smem=%zu dsh=%d sfl=%d t=%.3f\n",
-              CS, act, nu, L.NT, L.T, L.total, dsh, L.stage_fl, t);
+      fprintf(stderr, "[sambaten]   plan candidate cluster CS=%d act=%d NT=%d T=%d smem=%zu dsh=%d sfl=%d t=%.3f\n",
+              CS, act, L.NT, L.T, L.total, dsh, L.stage_fl, t);
     if (t < best) {
       best = t;
       found = true;
-      pl->CS = CS;
-      pl->smem = L.total;
-      pl->act = act;
-      pl->RB = RB;
-      pl->stage_fl = L.stage_fl;
-      pl->dsh = dsh;
+      *pl = ClusterPlan{};
+      pl->CS = CS; pl->smem = L.total; pl->act = act; pl->RB = RB; pl->stage_fl = L.stage_fl; pl->dsh = dsh;
+    }
+  }
+  if (try_grid) {
+    // one co-resident grid, CS = (SMs that hold a CTA) / r CTAs per repetition
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int CS = nsm / a.r;
+    if (CS > a.nK) CS = a.nK;
+    ClLayout L{};
+    int dsh = -1;
+    for (; CS >= 2; --CS)
+      if (plan_layout<RB>(a, CS, &L, &dsh)) break;
+    if (CS >= 2 && cluster_setup<RB, true>(CS, L.total) == cudaSuccess) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_cluster_kernel<RB, true>, kCT, L.total);
+      cudaGetLastError();
+      if (per_sm >= 1 && CS * a.r <= per_sm * nsm) {
+        // the per-repetition barriers go through L2 (~1-2 us each, five per iteration): charge
+        // them as a fraction of a slice's pass time
+        const double t = plan_cost(L, a.nK, CS, 1.0) * 1.03 + 0.15;
+        if (getenv("SAMBATEN_DEBUG"))
+          fprintf(stderr, "[sambaten]   plan candidate grid CS=%d NT=%d T=%d smem=%zu dsh=%d sfl=%d t=%.3f\n",
+                  CS, L.NT, L.T, L.total, dsh, L.stage_fl, t);
+        if (t < best || (force && force[0] == '1')) {
+          best = t;
+          found = true;
+          *pl = ClusterPlan{};
+          pl->CS = CS; pl->smem = L.total; pl->act = a.r; pl->RB = RB; pl->stage_fl = L.stage_fl; pl->dsh = dsh;
+          pl->grid = 1;
+        }
+      } else {
+        cudaGetLastError();
+      }
+    } else {
+      cudaGetLastError();
     }
   }
   return found;
@@ -1192,8 +1317,36 @@ bool plan_als_cluster(const DenseAls& a, ClusterPlan* pl) {
   }
 }
 
+// grid communication buffers after the D scratch: exported P | Gp | sc per CTA, pushed rows,
+// barrier counters
+static GridComm grid_comm_layout(const DenseAls& a, const ClusterPlan& pl, char* base, size_t* bytes) {
+  GridComm g{};
+  const int nmax = a.nI > a.nJ ? a.nI : a.nJ;
+  g.offP = 0;
+  g.offG = nmax * pl.RB;
+  g.offS = g.offG + 3 * pl.RB * pl.RB;
+  g.xstride = (g.offS + 64 + 31) & ~31;
+  g.ustride = (nmax * wstride(pl.RB) + 63) & ~63;
+  const size_t xb = sizeof(double) * (size_t)a.r * pl.CS * g.xstride;
+  const size_t ub = sizeof(float) * (size_t)a.r * 2 * g.ustride;
+  const size_t bb = sizeof(unsigned) * 64 * ((a.r + 63) / 64);
+  if (bytes) *bytes = xb + ub + bb + 256;
+  if (base) {
+    g.x = reinterpret_cast<double*>(base);
+    g.u = reinterpret_cast<float*>(base + xb);
+    g.bar = reinterpret_cast<unsigned*>(base + xb + ub);
+  }
+  return g;
+}
+
+static size_t d_scratch_bytes(const DenseAls& a, const ClusterPlan& pl) {
+  return pl.dsh ? 256 : ((sizeof(float) * (size_t)a.r * ((size_t)a.nK + pl.CS) * a.nJ * pl.RB + 255) & ~(size_t)255);
+}
+
 size_t als_cluster_dscratch_bytes(const DenseAls& a, const ClusterPlan& pl) {
-  return pl.dsh ? 16 : sizeof(float) * (size_t)a.r * ((size_t)a.nK + pl.CS) * a.nJ * pl.RB;
+  size_t gb = 0;
+  if (pl.grid) grid_comm_layout(a, pl, nullptr, &gb);
+  return d_scratch_bytes(a, pl) + gb;
 }
 
 int cluster_pitch(int n) { return pitch4(n); }
@@ -1218,9 +1371,17 @@ static cudaError_t cluster_launch(const DenseAls& a, const ClusterPlan& pl, floa
                                   cudaStream_t st) {
   cudaLaunchConfig_t cfg;
   cudaLaunchAttribute attr[1];
+  const int narrow = getenv("SAMBATEN_ALS_NARROW_A") ? 2 : 0;
+  if (pl.grid) {
+    GridComm gc = grid_comm_layout(a, pl, reinterpret_cast<char*>(Dglob) + d_scratch_bytes(a, pl), nullptr);
+    cudaError_t e = cudaMemsetAsync(gc.bar, 0, sizeof(unsigned) * a.r, st);
+    if (e != cudaSuccess) return e;
+    fill_cfg(&cfg, attr, pl.CS, a.r, pl.smem, st, true);
+    return cudaLaunchKernelEx(&cfg, als_cluster_kernel<RB, true>, a, pl.CS, Dglob, pl.stage_fl, pl.dsh | narrow, gc);
+  }
   fill_cfg(&cfg, attr, pl.CS, a.r, pl.smem, st);
-  return cudaLaunchKernelEx(&cfg, als_cluster_kernel<RB>, a, pl.CS, Dglob, pl.stage_fl,
-                            pl.dsh | (getenv("SAMBATEN_ALS_NARROW_A") ? 2 : 0));
+  return cudaLaunchKernelEx(&cfg, als_cluster_kernel<RB, false>, a, pl.CS, Dglob, pl.stage_fl, pl.dsh | narrow,
+                            GridComm{});
 }
 
 cudaError_t run_als_cluster(const DenseAls& a, const ClusterPlan& pl, float* Dglob, cudaStream_t st) {
