@@ -1281,13 +1281,20 @@ static bool plan_rb(const DenseAls& a, ClusterPlan* pl) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_cluster_kernel<RB, true>, kCT, L.total);
       cudaGetLastError();
       if (per_sm >= 1 && CS * a.r <= per_sm * nsm) {
-        // the per-repetition barriers go through L2 (~1-2 us each, five per iteration): charge
-        // them as a fraction of a slice's pass time
-        const double t = plan_cost(L, a.nK, CS, 1.0) * 1.03 + 0.15;
+        // The per-repetition barriers go through L2 (~1-2 us each, five per iteration), which
+        // the passes amortise only when a CTA streams enough slices: the grid is taken when it
+        // puts >= 1.25x the SMs of the best cluster plan to work and every CTA owns >= 8
+        // slices (measured: C4 summaries 300 x 300 x 320, r = 16: cluster 96 SMs 34.9 ms,
+        // grid 144 SMs 24.7 ms; C2 100 x 100 x 100, r = 8: cluster 80 SMs 1.33 ms, grid 144
+        // SMs 1.36 ms)
+        const double t = plan_cost(L, a.nK, CS, 1.0);
+        const int nu = (a.nK + CS - 1) / CS;
+        const int cl_sms = found ? pl->CS * (a.r < pl->act ? a.r : pl->act) : 0;
+        const bool take = (force && force[0] == '1') || (CS * a.r >= 1.25 * cl_sms && nu >= 8);
         if (getenv("SAMBATEN_DEBUG"))
-          fprintf(stderr, "[sambaten]   plan candidate grid CS=%d NT=%d T=%d smem=%zu dsh=%d sfl=%d t=%.3f\n",
-                  CS, L.NT, L.T, L.total, dsh, L.stage_fl, t);
-        if (t < best || (force && force[0] == '1')) {
+          fprintf(stderr, "[sambaten]   plan candidate grid CS=%d NT=%d T=%d smem=%zu dsh=%d sfl=%d t=%.3f take=%d\n",
+                  CS, L.NT, L.T, L.total, dsh, L.stage_fl, t, (int)take);
+        if (take) {
           best = t;
           found = true;
           *pl = ClusterPlan{};
