@@ -784,6 +784,16 @@ def main():
             run_variant(args.steps, incremental_marginals=1),
             note="opts.incremental_marginals=1: a1 adds the batch's contribution to the committed int64 "
                  "marginals (bit-identical to the full pass; tests/test_gpu_incremental.py)")}
+        if not work.coo:
+            line["variants"]["pipelined"] = dict(
+                run_variant(args.steps, pipelined=1),
+                note="opts.pipelined=1 (SURVEY 8(f) NEXT #4, R36; P:173): samples from the marginals the previous "
+                     "update committed, so a1 runs on a side stream overlapped with a2..a7; "
+                     "tests/test_gpu_update.py::test_pipelined_parity")
+            line["variants"]["pipelined_incremental"] = dict(
+                run_variant(args.steps, pipelined=1, incremental_marginals=1),
+                note="pipelined + incremental marginals: no pass over the whole tensor (the batch's slices, the "
+                     "summaries and the incremental fit only)")
         if device_gen and warm:
             v = run_variant(args.steps, warm_start=0, accept_tau=0.0)
             v["roofline_a4"] = v.pop("kernels")["a4"]

@@ -113,6 +113,12 @@ typedef struct {
                           /* NEXT #4, reading R34) instead of the Philox point.  Dense        */
                           /* handles (single-GPU and sharded), not with getrank (else         */
                           /* SAMBATEN_E_INVALID).                                             */
+  int pipelined;          /* 1: update t+1 samples from the marginals update t committed (the  */
+                          /* tensor BEFORE its batch, reading R36),*/
+                          /* so sampling and gather do not wait for this update's marginal    */
+                          /* pass, which runs on a side stream overlapped with a2..a7 and is  */
+                          /* committed for the next update.  Dense single-GPU handles (else   */
+                          /* SAMBATEN_E_INVALID).  Default 0.                                 */
 } sambaten_opts;
 
 typedef struct {

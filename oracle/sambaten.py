@@ -437,6 +437,7 @@ class Config:
     getrank_trials: int = 1
     getrank_threshold: float = 90.0
     warm_start: bool = False # summary ALS started from the model's rows
+    pipelined: bool = False  # sample update t+1 from update t's marginals
 
 
 @dataclass
@@ -451,6 +452,7 @@ class State:
     max_phi_log2: int        # ceil(log2 max phi(X0)): the fixed-point range (reading R7)
     update_id: int = 0
     last: dict = field(default_factory=dict)
+    marg: tuple = None       # pipelined (R36): marginals of the stored tensor, kept for the next update
 
     @property
     def dense(self):
@@ -540,12 +542,20 @@ def update(st, batch, keep_reps=False):
     X = dense_append(st.X, batch) if dense else coo_append(st.X, batch)
     # a1: marginals over X_old U X_new (readings R2, R3)
     x1, x2, x3 = (marginals_dense(X, st.S, cfg.moi) if dense else marginals_coo(X, st.S, cfg.moi))
+    sx = (x1, x2, x3)
+    if cfg.pipelined:
+        # reading R36 ("X is the tensor prior to the update"): the
+        # samples come from the marginals of the tensor BEFORE this batch (kept from the
+        # previous update, or computed from the stored tensor after init), so the sampling and
+        # the gather need not wait for this update's marginal pass
+        sx = st.marg if st.marg is not None else (
+            marginals_dense(st.X, st.S, cfg.moi) if dense else marginals_coo(st.X, st.S, cfg.moi))
     reps = []
     for rho in range(cfg.r):
         # a2: sampling (K_s only from the old slices, reading R2 / S:302)
-        Is = sample_mode(x1, sample_size(I, cfg.s[0]), cfg.seed, uid, rho, 0)
-        Js = sample_mode(x2, sample_size(J, cfg.s[1]), cfg.seed, uid, rho, 1)
-        Ks = sample_mode(x3[:K_o], sample_size(K_o, cfg.s[2]), cfg.seed, uid, rho, 2)
+        Is = sample_mode(sx[0], sample_size(I, cfg.s[0]), cfg.seed, uid, rho, 0)
+        Js = sample_mode(sx[1], sample_size(J, cfg.s[1]), cfg.seed, uid, rho, 1)
+        Ks = sample_mode(sx[2][:K_o], sample_size(K_o, cfg.s[2]), cfg.seed, uid, rho, 2)
         Kp = k_prime(Ks, K_o, K_n)
         # a3: gather the summary
         Y = gather_dense(X, Is, Js, Kp) if dense else gather_coo(X, Is, Js, Kp)
@@ -602,6 +612,8 @@ def update(st, batch, keep_reps=False):
     # commit
     st.X, st.A, st.B, st.C, st.lam = X, A, B, np.vstack([C, C_new]), lam
     st.update_id = uid
+    if cfg.pipelined:
+        st.marg = (x1, x2, x3)
     st.last = dict(x=(x1, x2, x3), reps=reps, fit_summary=float(np.mean([rp["fit"] for rp in reps])),
                    rejected=[i for i, rp in enumerate(reps) if not rp["match"].accepted])
     return st.last

@@ -38,7 +38,8 @@ class Opts(C.Structure):
                 ("init_max_iters", C.c_int),
                 ("init_tol", C.c_double), ("stream", C.c_void_p), ("borrow_store", C.c_int),
                 ("incremental_marginals", C.c_int), ("getrank", C.c_int),
-                ("getrank_trials", C.c_int), ("getrank_threshold", C.c_double), ("warm_start", C.c_int)]
+                ("getrank_trials", C.c_int), ("getrank_threshold", C.c_double), ("warm_start", C.c_int),
+                ("pipelined", C.c_int)]
 
 
 class Dist(C.Structure):

@@ -121,10 +121,12 @@ struct sambaten_s {
   int als_plan[4] = {-1, 0, 0, 0};   // the a4 plan of the last update (sambaten_info.als_plan)
   int64_t summ_entries = 0;          // summary entries / nnz of the update in flight (sambaten_info)
   bool lag_now = false;              // this update computes the previous model's fit in a1 (full_fit = 2)
+  bool pipe_now = false;             // this update's a1 runs on the side stream (opts.pipelined, R36)
   int fit_path = 0;                  // sambaten_info.fit_path of the update in flight
   const int* d_fit_mode = nullptr;   // device plan of the incremental fit (1 incremental, 2 full)
   cudaStream_t st2 = nullptr;     // side stream: host batch copy overlapped with a1 (old slices)
   cudaEvent_t ev_side[2] = {nullptr, nullptr};
+  cudaEvent_t ev_pl[2] = {nullptr, nullptr};   // pipelined a1 on the side stream (timing)
   DevBuf xm, xm_ck;          // committed marginals of the current tensor (incremental a1)
   bool xm_valid = false, xm_ck_valid = false;
   int R = 0, r = 0, s[3] = {1, 1, 1};
@@ -391,6 +393,10 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
     delete h;
     FAIL(SAMBATEN_E_INVALID, "init: warm_start needs a dense tensor and no getrank (R34)");
   }
+  if (h->opts.pipelined && h->fmt != SAMBATEN_DENSE) {
+    delete h;
+    FAIL(SAMBATEN_E_INVALID, "init: pipelined needs a dense tensor (R36)");
+  }
   if (h->opts.getrank) {
     if (h->fmt != SAMBATEN_DENSE) { delete h; FAIL(SAMBATEN_E_INVALID, "init: getrank needs a dense tensor (R33)"); }
     if (h->opts.getrank_trials < 1 || h->opts.getrank_trials > kMaxReps) {
@@ -487,6 +493,7 @@ extern "C" void sambaten_destroy(sambaten_t h) {
     cudaStreamDestroy(h->st2);
     cudaEventDestroy(h->ev_side[0]);
     cudaEventDestroy(h->ev_side[1]);
+    if (h->ev_pl[0]) { cudaEventDestroy(h->ev_pl[0]); cudaEventDestroy(h->ev_pl[1]); }
   }
   if (h->X_borrowed) h->X.p = nullptr;   // the caller's buffer: not ours to free
   h->X.release();
@@ -506,6 +513,7 @@ __global__ static void lam_to_f32_kernel(const double* l, int R, float* out) {
 }
 
 static sambaten_status init_als_coo(sambaten_s* h);
+static cudaError_t compute_committed_marginals(sambaten_s* h);
 
 // The incremental fit's state of the initial model (one per-component pass over X0; untimed
 // init work) when the updates will report the full fit of a dense handle (full_fit = 1).
@@ -822,7 +830,7 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
   }
   if (nacc == 0) FAIL(SAMBATEN_E_BATCH_REJECTED, "update: every repetition was rejected (R26)");
   // commit
-  if (h->opts.incremental_marginals) {   // this update's marginals are the new committed ones
+  if (h->opts.incremental_marginals || h->opts.pipelined) {   // this update's marginals are the new committed ones
     std::swap(h->marg, h->xm);
     h->xm_valid = true;
   }
@@ -848,7 +856,8 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
     info->summary_entries = h->summ_entries;
     for (int e = 0; e < 8; ++e) {
       float ms = 0.f;
-      cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);
+      if (e == 1 && h->pipe_now) cudaEventElapsedTime(&ms, h->ev_pl[0], h->ev_pl[1]);   // a1 on the side stream
+      else cudaEventElapsedTime(&ms, h->ev[e], h->ev[e + 1]);
       info->step_ms[e] = ms;
     }
   }
@@ -1200,6 +1209,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   h->als_plan[0] = -1; h->als_plan[1] = h->als_plan[2] = h->als_plan[3] = 0;   // set by the dense paths
   h->summ_entries = 0;
   h->lag_now = false;
+  h->pipe_now = false;
   h->fit_path = 0;
   h->d_fit_mode = nullptr;
   if (h->dist)
@@ -1215,6 +1225,23 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   const uint32_t uid = h->update_id + 1;
   const int64_t nI = sample_n(h->I, h->s[0]), nJ = sample_n(h->J, h->s[1]);
   const int64_t nKs = sample_n(Ko, h->s[2]), nKp = nKs + Kn;
+  // R36 pipelined: sample from the committed marginals of X_old (the first update after init
+  // computes them once); this update's a1 runs on the side stream, off the critical path
+  const bool pipe = h->opts.pipelined;
+  if (pipe) {
+    CK(compute_committed_marginals(h));
+    if (!h->st2) {
+      CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&h->ev_side[0], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&h->ev_side[1], cudaEventDisableTiming));
+    }
+    if (!h->ev_pl[0]) {
+      CK(cudaEventCreate(&h->ev_pl[0]));
+      CK(cudaEventCreate(&h->ev_pl[1]));
+    }
+  }
+  h->pipe_now = pipe;
+  const cudaStream_t sa1 = pipe ? h->st2 : st;   // the stream a1 runs on
 
   CK(cudaEventRecord(h->ev[0], st));
   // ---- a0: ingest into the preallocated capacity (not visible until commit) --------------
@@ -1242,17 +1269,18 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   double* d_relerr_prev = d_relerr + 4;
   if (lag) CK(h->fitws.ensure(sizeof(double) * fit_ws_doubles_any(V)));
   auto old_pass = [&]() -> cudaError_t {   // a1 over [0, Ko), with the lag-1 fit when asked
-    if (!lag) return marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, st);
+    if (!lag) return marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, sa1);
     cudaError_t e = launch_marg_fit_stream(Vold, Ko, h->opts.moi, h->S, qbits(h), h->lam(h->cur), h->A(h->cur),
                                            h->B(h->cur), h->C(h->cur), R, nullptr, x1, x2, x3,
-                                           h->fitws.as<double>(), d_fit2, st);
+                                           h->fitws.as<double>(), d_fit2, sa1);
     if (e != cudaSuccess) return e;
     return launch_fit_finish(d_fit2, h->lam(h->cur), h->A(h->cur), h->B(h->cur), h->C(h->cur), h->I, h->J, Ko,
-                             R, h->fitws.as<double>(), d_relerr_prev, st);
+                             R, h->fitws.as<double>(), d_relerr_prev, sa1);
   };
   // A host batch crosses PCIe on a side stream while a1 reads the old slices (they do not
-  // depend on it); the batch's own marginals follow once it has landed.
-  const bool overlap = !dev_batch && !inc && Ko > 0;
+  // depend on it); the batch's own marginals follow once it has landed.  (Pipelined updates
+  // run the whole a1 on the side stream instead.)
+  const bool overlap = !dev_batch && !inc && Ko > 0 && !pipe;
   if (overlap) {
     if (!h->st2) {
       CK(cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking));
@@ -1279,26 +1307,39 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   }
   CK(cudaEventRecord(h->ev[1], st));
   // ---- a1: marginals over X_old U X_new (R2, R3) ----------------------------------------
+  if (pipe) {   // the side stream, after the ingest
+    CK(cudaEventRecord(h->ev_side[0], st));
+    CK(cudaStreamWaitEvent(sa1, h->ev_side[0], 0));
+    CK(cudaEventRecord(h->ev_pl[0], sa1));
+  }
   if (overlap) {
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, st));   // the batch's slices
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1));   // the batch's slices
   } else if (inc) {
     // committed marginals of X_old plus the batch's contribution (integer sums: bit-identical
     // to the full pass)
-    CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, st));
-    CK(cudaMemsetAsync(x3 + Ko, 0, sizeof(int64_t) * (h->Kcap - Ko), st));
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, st));
+    CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, sa1));
+    CK(cudaMemsetAsync(x3 + Ko, 0, sizeof(int64_t) * (h->Kcap - Ko), sa1));
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1));
   } else if (lag) {
-    CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
+    CK(cudaMemsetAsync(x1, 0, marg_bytes, sa1));
     CK(old_pass());
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, st));   // the batch's slices
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1));   // the batch's slices
   } else {
-    CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
-    CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, st));
+    CK(cudaMemsetAsync(x1, 0, marg_bytes, sa1));
+    CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, sa1));
+  }
+  if (pipe) {
+    CK(cudaEventRecord(h->ev_pl[1], sa1));
+    CK(cudaEventRecord(h->ev_side[1], sa1));   // joined before the commit
   }
   CK(cudaEventRecord(h->ev[2], st));
-  // ---- a2: sampling ---------------------------------------------------------------------
+  // ---- a2: sampling (pipelined: from the committed marginals of X_old, R36) ---------------
   int32_t *Is, *Js, *Kp, *locI, *locJ, *locK;
-  CK(run_sampling(h, x1, x2, x3, Ko, Kn, nI, nJ, nKs, nKp, uid, &Is, &Js, &Kp, &locI, &locJ, &locK));
+  {
+    const int64_t* sx1 = pipe ? h->xm.as<int64_t>() : x1;
+    CK(run_sampling(h, sx1, sx1 + h->I, sx1 + h->I + h->J, Ko, Kn, nI, nJ, nKs, nKp, uid, &Is, &Js, &Kp, &locI,
+                    &locJ, &locK));
+  }
   CK(cudaEventRecord(h->ev[3], st));
   // ---- a3: gather the r summaries ------------------------------------------------------
   int64_t y_stride = (nKp * nJ * nI + 3) & ~int64_t(3);
@@ -1409,6 +1450,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   // marginals), a2 sample, a3 gather, a4 ALS, a5 match partial + match, a6 merge, a7 fit + two
   // Gram kernels + combine
   const int launches = 1 + (overlap ? 1 : 0) + 1 + (lag ? 5 : 0) + 1 + 1 + als_launches + 2 + 1 + (fit_now ? 4 : 0);
+  if (pipe) CK(cudaStreamWaitEvent(st, h->ev_side[1], 0));   // this update's marginals, committed for the next
   return finish_update(h, a, accepted, d_maxphi, nullptr, d_relerr, Ko, Kn, nI, nJ, nKs, nKp, b, nb,
                        launches, 0, Aout, Bout, Cout, lamout, info);
 }
@@ -1488,7 +1530,7 @@ extern "C" sambaten_status sambaten_relative_error(sambaten_t h, double* relerr)
 // Committed marginals of the current tensor for the incremental a1 (one full pass; single-GPU
 // handles -- a sharded handle computes them in its first update).
 static cudaError_t compute_committed_marginals(sambaten_s* h) {
-  if (h->dist || h->xm_valid || !h->opts.incremental_marginals) return cudaSuccess;
+  if (h->dist || h->xm_valid || !(h->opts.incremental_marginals || h->opts.pipelined)) return cudaSuccess;
   const size_t xb = sizeof(int64_t) * (h->I + h->J + h->Kcap);
   cudaError_t e = h->xm.ensure(xb);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->xm.p, 0, xb, h->st);

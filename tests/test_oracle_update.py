@@ -267,3 +267,32 @@ def test_update_pinv_path_zero_model_column():
     assert all(rp["pinv"] for rp in info["reps"])
     assert st.lam[2] == lam0[2] / 2.0
     assert np.all(st.C[18:, 2] == 0.0)
+
+
+def test_pipelined_samples_from_the_previous_tensor():
+    """R36: the pipelined update samples from the marginals of the tensor
+    BEFORE its batch -- pinned against the plain update run on the old tensor's
+    marginals: the first pipelined update's samples equal the samples the oracle draws from
+    marginals_dense(X_old); the second's those of X_1 (the first batch included); a rejected
+    batch keeps the stored marginals."""
+    T, truth = planted_dense(30, 26, 34, 3, noise=0.01, seed=17)
+    T0, batches = split_dense(T, 24, 5)
+    cfg = O.Config(R=3, s=(2, 2, 2), r=3, seed=7, maxit=10, tol=0.0, tau=0.0, pipelined=True)
+    st = _state_from_truth(T0, truth, cfg, T.size)
+    X = T0
+    for b in batches:
+        x1, x2, x3 = O.marginals_dense(X, st.S)
+        info = O.update(st, b)
+        uid = st.update_id
+        for rho, rp in enumerate(info["reps"]):
+            assert np.array_equal(rp["Is"], O.sample_mode(x1, O.sample_size(30, 2), 7, uid, rho, 0))
+            assert np.array_equal(rp["Js"], O.sample_mode(x2, O.sample_size(26, 2), 7, uid, rho, 1))
+            assert np.array_equal(rp["Ks"], O.sample_mode(x3, O.sample_size(X.shape[0], 2), 7, uid, rho, 2))
+        X = np.concatenate([X, b])
+        for a, c in zip(st.marg, O.marginals_dense(X, st.S)):
+            assert np.array_equal(a, c)
+    marg = st.marg
+    st.cfg = O.Config(R=3, s=(2, 2, 2), r=3, seed=7, maxit=2, tol=0.0, tau=1.5, pipelined=True)
+    with pytest.raises(O.BatchRejected):
+        O.update(st, batches[0])
+    assert st.marg is marg
