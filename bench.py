@@ -61,7 +61,7 @@ def parse():
                         "rows the merge changed, k_fitinc.cu); 2: lag-1 fit inside the next update's a1 pass "
                         "(SURVEY 8(f) NEXT #1; dense only, COO configs use 1)")
     p.add_argument("--no-recompute", action="store_true", help="skip the CP_ALS recompute / relative fitness report")
-    p.add_argument("--recompute-iters", type=int, default=60, help="CP_ALS baseline iteration cap (P:441 uses 1000)")
+    p.add_argument("--recompute-iters", type=int, default=150, help="CP_ALS baseline iteration cap (P:441 uses 1000)")
     p.add_argument("--sharded", action="store_true",
                    help="use the sharded (NCCL) handle even at N=1 (always used at N>1, dense configs)")
     return p.parse_args()
