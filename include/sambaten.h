@@ -110,8 +110,8 @@ typedef struct {
   double getrank_threshold; /* CorConDia cut-off of R31; default 90                           */
   int warm_start;         /* 1: each summary ALS starts from the model's rows (A(I_s), B(J_s),  */
                           /* C(K_s) diag(lambda), zero rows for the new slices   */
-                          /* NEXT #4, reading R34) instead of the Philox point.  Dense        */
-                          /* handles (single-GPU and sharded), not with getrank (else         */
+                          /* NEXT #4, reading R34) instead of the Philox point.  Dense and    */
+                          /* COO handles, single-GPU and sharded; not with getrank (else      */
                           /* SAMBATEN_E_INVALID).                                             */
   int pipelined;          /* 1: update t+1 samples from the marginals update t committed (the  */
                           /* tensor BEFORE its batch, reading R36),*/

@@ -389,9 +389,9 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
     h->Kcap = h->opts.capacity_k > 0 ? h->opts.capacity_k : 2 * h->K + 1024;
     if (h->Kcap < h->K) { delete h; FAIL(SAMBATEN_E_INVALID, "init: capacity_k < K0"); }
   }
-  if (h->opts.warm_start && (h->fmt != SAMBATEN_DENSE || h->opts.getrank)) {
+  if (h->opts.warm_start && h->opts.getrank) {
     delete h;
-    FAIL(SAMBATEN_E_INVALID, "init: warm_start needs a dense tensor and no getrank (R34)");
+    FAIL(SAMBATEN_E_INVALID, "init: warm_start and getrank are exclusive (R34)");
   }
   if (h->opts.pipelined && h->fmt != SAMBATEN_DENSE) {
     delete h;
@@ -887,11 +887,19 @@ struct Bump {
 
 static int bits_for(int64_t n) { int b = 1; while (((int64_t)1 << b) < n) ++b; return b; }
 
+// the model rows a warm-started summary ALS begins from (R34): A(I_s), B(J_s), C(K_s) diag(lambda)
+struct WarmRows {
+  const float *A, *B, *C, *lam;
+  const int32_t *Is, *Js, *Kp;
+  int nKs;
+};
+
 static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int32_t* p, const int32_t* q,
                                const int32_t* u, const float* v, const int64_t* d_off, int64_t ntot,
                                int nI, int nJ, int nK, int r, float* U0, float* U1, float* U2,
                                uint64_t seed, uint32_t uid, int maxit, double tol, bool init_factors,
-                               DenseAls* d, int* launches, uint32_t rep0 = 0, uint32_t rep_stride = 1) {
+                               DenseAls* d, int* launches, uint32_t rep0 = 0, uint32_t rep_stride = 1,
+                               const WarmRows* warm = nullptr) {
   const int64_t maxn = std::max<int64_t>(nI, std::max<int64_t>(nJ, nK));
   const int kb0 = bits_for(nI), kb1 = bits_for(nJ), kb2 = bits_for(nK);
   const int64_t n = std::max<int64_t>(ntot, 1);
@@ -981,6 +989,9 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     const int64_t ups[3] = {(int64_t)nI * RBp, (int64_t)nJ * RBp, (int64_t)nK * RBp};
     for (int m = 0; m < 3; ++m) { a.Up[m] = Up3[m]; a.up_stride[m] = ups[m]; }
     if (e == cudaSuccess && init_factors) e = launch_als_init_factors(*d, seed, uid, rep0, st, rep_stride);
+    if (e == cudaSuccess && warm)   // R34: the model's rows replace the Philox point (before the Grams)
+      e = launch_warm_init(*d, warm->A, warm->B, warm->C, warm->lam, warm->Is, warm->Js, warm->Kp, warm->nKs, st,
+                           (int)rep0, (int)rep_stride);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(done, 0, sizeof(int) * r, st);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(iters, 0, sizeof(int) * r, st);
     if (e == cudaSuccess && !init_factors) e = cudaMemsetAsync(flags, 0, sizeof(int) * r, st);
@@ -1167,9 +1178,11 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
   // ---- a4: batched CP-ALS on the COO summaries ----------------------------------------------
   DenseAls a{};
   int als_launches = 0;
+  const WarmRows wr{h->A(h->cur), h->B(h->cur), h->C(h->cur), h->lam(h->cur), Is, Js, Kp, (int)nKs};
   if (sambaten_status e = coo_als(h->coo_ws, st, R, sp, sq, su, sv, d_off, nsum, (int)nI, (int)nJ,
                                   (int)nKp, r, U0, U1, U2, h->seed, uid, h->opts.als_max_iters,
-                                  h->opts.als_tol, true, &a, &als_launches))
+                                  h->opts.als_tol, true, &a, &als_launches, 0, 1,
+                                  h->opts.warm_start ? &wr : nullptr))
     return e;
   launches += als_launches;
   CK(cudaEventRecord(h->ev[5], st));

@@ -1,7 +1,7 @@
 // k_gather.cu -- a3 (dense): the summaries X_s = X(I_s, J_s, K_s U new).
 //
 // Y[rep][u][q][p] = X(Is[p], Js[q], Kp[u]) and, for the cluster ALS, its per-slice transpose
-// Yt[rep][u][p][q].  Block = (32-row q tile, slice u, rep); for each 32-column p tile the
+// Yt[rep][u][p][q].  Block = (32-row q tile, rep, slice u); for each 32-column p tile the
 // 8 warps gather 4 source rows each (lanes walk the sorted I_s list held in shared memory,
 // so neighbouring lanes share 32 B sectors of the source row), write the Y rows coalesced
 // and stage the 32 x 32 block in shared memory (padded, conflict-free) for the coalesced Yt
@@ -20,7 +20,9 @@ __global__ void __launch_bounds__(kGatherThreads) gather_dense_kernel(
     int64_t y_stride, int pI, int pJ) {
   extern __shared__ int32_t is_sh[];
   __shared__ float tile[2][32][33];
-  const int qt = blockIdx.x, u = blockIdx.y, rep = blockIdx.z;
+  // grid (q tile, rep, slice): the repetitions' blocks of one slice position run together, so
+  // the rows of a new slice (the same k in every repetition) are read from L2 after the first
+  const int qt = blockIdx.x, rep = blockIdx.y, u = blockIdx.z;
   const int32_t* is = Is + rep * sI;
   for (int p = threadIdx.x; p < nI; p += blockDim.x) is_sh[p] = is[p];
   __syncthreads();
@@ -79,7 +81,7 @@ cudaError_t launch_gather_dense(const DenseView& X, const int32_t* Is, const int
   if (nK <= 0 || nJ <= 0 || nI <= 0 || r <= 0) return cudaSuccess;
   if (pI < nI) pI = nI;
   if (pJ < nJ) pJ = nJ;
-  dim3 grid((unsigned)ceil_div(pJ, 32), (unsigned)nK, (unsigned)r);
+  dim3 grid((unsigned)ceil_div(pJ, 32), (unsigned)r, (unsigned)nK);
   gather_dense_kernel<<<grid, kGatherThreads, sizeof(int32_t) * nI, st>>>(
       X.base, X.J, X.pitch, Is, Js, Kp, nI, nJ, nK, sI, sJ, sK, Y, Yt, y_stride, pI, pJ);
   return cudaGetLastError();

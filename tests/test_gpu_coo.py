@@ -33,16 +33,16 @@ def _samples(h, r):
     return Is.reshape(r, -1), Js.reshape(r, -1), Ks.reshape(r, -1)
 
 
-def _run(X, truth, K0, batch, R, s, r, maxit, tol=0.0, seed=7, nb=None, tau=0.9):
+def _run(X, truth, K0, batch, R, s, r, maxit, tol=0.0, seed=7, nb=None, tau=0.9, warm=False):
     X0, batches = split_coo(X, K0, batch)
     if nb is not None:
         batches = batches[:nb]
     lam, A, B, C = truth
     model = [np.ascontiguousarray(np.asarray(x, np.float32)) for x in (lam, A, B, C[:K0])]
-    cfg = O.Config(R=R, s=(s, s, s), r=r, seed=seed, maxit=maxit, tol=tol, tau=tau)
+    cfg = O.Config(R=R, s=(s, s, s), r=r, seed=seed, maxit=maxit, tol=tol, tau=tau, warm_start=warm)
     st = O.init_factors(_oc(X0), cfg, *model, X.nnz)
     opts = L().default_opts(als_max_iters=maxit, als_tol=tol, accept_tau=tau, capacity=X.nnz,
-                            capacity_k=X.dims[2], full_fit=1)
+                            capacity_k=X.dims[2], full_fit=1, warm_start=int(warm))
     h = L().sambaten_init_factors(_gc(X0), R, s, r, seed, model[1], model[2], model[3], model[0], opts)
     out = []
     try:
@@ -79,6 +79,17 @@ def test_coo_update_parity_planted():
         assert fms >= 0.99, fms
         assert abs(rel_g - rel_o) <= 1e-3, (rel_g, rel_o)
         assert abs((1 - info.fit_full) - rel_g) <= 1e-5
+
+
+def test_coo_warm_start_parity():
+    """The warm-started summary ALS (R34) on COO summaries: the model's rows as the start; the
+    same bars as the plain COO update (samples bit-exact inside _run), over two batches."""
+    X, truth = zipf_planted_coo(400, 300, 60, 4, 30_000, alpha=1.2, seed=13)
+    res = _run(X, truth, 50, 5, R=4, s=2, r=4, maxit=8, nb=2, warm=True)
+    for fms, rel_g, rel_o, gr, orr, info in res:
+        assert gr == orr
+        assert fms >= 0.99, fms
+        assert abs(rel_g - rel_o) <= 1e-3, (rel_g, rel_o)
 
 
 def test_coo_update_parity_communities_ragged():

@@ -77,6 +77,31 @@ def test_marginals_coo_bit_exact(moi):
         assert np.array_equal(host(g), r)
 
 
+@pytest.mark.parametrize("moi,hot", [(0, True), (1, True), (0, False)])
+def test_marginals_coo_hashed_bit_exact(moi, hot):
+    """The block-aggregated COO marginals (shared-memory hash tables, flushed when half full)
+    on inputs large enough to take that path (>= 32K nnz, several flushes per block): Zipf-hot
+    indices (a few i / j carry most entries, the C3 / C5 hazard) and near-uniform ones; bit-exact
+    against the oracle."""
+    from synth import zipf_planted_coo
+    torch = torch_cuda()
+    if hot:
+        Xs, _ = zipf_planted_coo(60_000, 50_000, 400, 4, 600_000, alpha=1.3, seed=8)
+    else:
+        rng = np.random.default_rng(9)
+        n = 400_000
+        ii, jj, kk = rng.integers(0, 60_000, n), rng.integers(0, 50_000, n), rng.integers(0, 400, n)
+        Xs = O.coo_canonical(ii, jj, kk, rng.random(n).astype(np.float32) + 0.5, (60_000, 50_000, 400))
+    X = O.Coo(np.asarray(Xs.i, np.int64), np.asarray(Xs.j, np.int64), np.asarray(Xs.k, np.int64), Xs.v, Xs.dims)
+    assert X.nnz > 200_000
+    S = O.fixed_point_scale(X.nnz, float(O.phi(X.v, moi).max()))
+    x = [torch.zeros(n, dtype=torch.int64, device="cuda") for n in X.dims]
+    t = L().coo(dev(X.i.astype(np.int32)), dev(X.j.astype(np.int32)), dev(X.k.astype(np.int32)), dev(X.v), X.dims)
+    L().sambaten_marginals(t, moi, S, *x)
+    for g, r in zip(x, O.marginals_coo(X, S, moi)):
+        assert np.array_equal(host(g), r)
+
+
 # ----------------------------------------------------------------------------- sampling
 @pytest.mark.parametrize("n,ns", [(50, 25), (500, 100), (1, 1), (7, 7), (100_000, 5000), (65_536, 6554),
                                   (3000, 300), (33, 0)])
