@@ -31,10 +31,6 @@ cudaError_t launch_marginals_dense(const DenseView& X, int64_t k0, int64_t nk, i
 cudaError_t launch_marginals_coo(const int32_t* i, const int32_t* j, const int32_t* k,
                                  const float* v, int64_t nnz, int moi, int S, int64_t* x1,
                                  int64_t* x2, int64_t* x3, cudaStream_t st);
-// the per-entry global-atomic variant (small inputs; SAMBATEN_COO_MARG_ATOMIC forces it)
-cudaError_t launch_marginals_coo_atomic(const int32_t* i, const int32_t* j, const int32_t* k,
-                                 const float* v, int64_t nnz, int moi, int S, int64_t* x1,
-                                 int64_t* x2, int64_t* x3, cudaStream_t st);
 // max phi over a dense view (slices [k0,k0+nk)) or COO values; result as double bits in
 // *out (callers zero it; phi >= 0 so the bit pattern is monotone).
 // a0 fused copy + max |x| of a contiguous device batch (n floats, n % 4 == 0, 16 B aligned)

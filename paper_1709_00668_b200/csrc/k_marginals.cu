@@ -255,128 +255,9 @@ __global__ void marg_coo_kernel(const int32_t* __restrict__ ii, const int32_t* _
   }
 }
 
-// COO marginals with block-local aggregation (the Zipf-hot indices of C3/C5 would otherwise
-// serialise on their global atomics): each block keeps two open-addressing hash tables in
-// shared memory (i -> sum of q for x1, j -> sum of q for x2; 8192 slots each), inserts the
-// entries of one tile at a time (shared 64-bit atomics; a hot index collapses to one slot),
-// and flushes a table to the global marginals (one atomic per distinct index) only when it is
-// half full and at the end -- across tiles, so hot indices stay aggregated.  x3: the entries
-// are sorted by k, so a warp's equal-k run is summed (match_any) before one atomic.  Integer
-// sums: bit-identical to any order.
-constexpr int kHashSlots = 8192;
-constexpr int kHashT = 512;
-constexpr int kHashTile = 2048;   // entries per tile (4 per thread)
-
-__device__ __forceinline__ unsigned hash_slot(int key) {
-  return ((unsigned)key * 0x9E3779B1u) >> (32 - 13);   // 2^13 = kHashSlots
-}
-
-__device__ __forceinline__ void hash_add(volatile int* keys, unsigned long long* vals, int* used, int key,
-                                         unsigned long long q) {
-  unsigned h = hash_slot(key);
-  for (;;) {
-    const int k = keys[h];
-    if (k == key) { atomicAdd(&vals[h], q); return; }
-    if (k == -1) {
-      const int prev = atomicCAS(const_cast<int*>(keys) + h, -1, key);
-      if (prev == -1) { atomicAdd(&vals[h], q); atomicAdd(used, 1); return; }
-      if (prev == key) { atomicAdd(&vals[h], q); return; }
-    }
-    h = (h + 1) & (kHashSlots - 1);
-  }
-}
-
-__device__ __forceinline__ void hash_flush(volatile int* keys, unsigned long long* vals, unsigned long long* out) {
-  for (int s = threadIdx.x; s < kHashSlots; s += blockDim.x) {
-    const int k = keys[s];
-    if (k != -1) {
-      atomicAdd(&out[k], vals[s]);
-      keys[s] = -1;
-      vals[s] = 0;
-    }
-  }
-}
-
-template <int MOI>
-__global__ void __launch_bounds__(kHashT) marg_coo_hash_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
-                                                               const int32_t* __restrict__ kk, const float* __restrict__ vv,
-                                                               int64_t nnz, float scf, double scd, unsigned long long* x1,
-                                                               unsigned long long* x2, unsigned long long* x3) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  unsigned long long* v1 = reinterpret_cast<unsigned long long*>(smem);
-  unsigned long long* v2 = v1 + kHashSlots;
-  volatile int* k1 = reinterpret_cast<volatile int*>(v2 + kHashSlots);
-  volatile int* k2 = k1 + kHashSlots;
-  __shared__ int used[2];
-  const int lane = threadIdx.x & 31;
-  for (int s = threadIdx.x; s < kHashSlots; s += blockDim.x) { v1[s] = 0; v2[s] = 0; k1[s] = -1; k2[s] = -1; }
-  if (threadIdx.x < 2) used[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t ntile = (nnz + kHashTile - 1) / kHashTile;
-  for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
-    const int64_t base = t * kHashTile;
-#pragma unroll
-    for (int u = 0; u < kHashTile / kHashT; ++u) {
-      const int64_t n = base + u * kHashT + threadIdx.x;   // a warp takes 32 consecutive entries
-      long long q = 0;
-      int k = -1;
-      if (n < nnz) {
-        q = quant<MOI>(vv[n], scf, scd);
-        if (q) {
-          hash_add(k1, v1, &used[0], ii[n], (unsigned long long)q);
-          hash_add(k2, v2, &used[1], jj[n], (unsigned long long)q);
-        }
-        k = kk[n];
-      }
-      const unsigned same = __match_any_sync(0xffffffffu, k);
-      const int leader = __ffs(same) - 1;
-      long long s3 = 0;
-      for (unsigned m = same; m; m &= m - 1) s3 += __shfl_sync(same, q, __ffs(m) - 1);
-      if (lane == leader && k >= 0 && s3) atomicAdd(&x3[k], (unsigned long long)s3);
-    }
-    __syncthreads();
-    // half full: flush (the next tile adds at most kHashTile keys per table)
-    if (used[0] > kHashSlots / 2 || used[1] > kHashSlots / 2) {
-      hash_flush(k1, v1, x1);
-      hash_flush(k2, v2, x2);
-      __syncthreads();
-      if (threadIdx.x < 2) used[threadIdx.x] = 0;
-      __syncthreads();
-    }
-  }
-  __syncthreads();
-  hash_flush(k1, v1, x1);
-  hash_flush(k2, v2, x2);
-}
-
 cudaError_t launch_marginals_coo(const int32_t* i, const int32_t* j, const int32_t* k,
                                  const float* v, int64_t nnz, int moi, int S, int64_t* x1,
                                  int64_t* x2, int64_t* x3, cudaStream_t st) {
-  if (nnz >= (int64_t)kHashTile * 16 && !getenv("SAMBATEN_COO_MARG_ATOMIC")) {
-    if (nnz <= 0) return cudaSuccess;
-    const float scf = pow2f(S < -126 ? -126 : (S > 127 ? 127 : S));
-    const double scd = ldexp(1.0, S);
-    const size_t smem = (sizeof(unsigned long long) + sizeof(int)) * 2 * kHashSlots;
-    int64_t blocks = (nnz + kHashTile - 1) / kHashTile;
-    if (blocks > kNumSMs) blocks = kNumSMs;
-    auto* u1 = reinterpret_cast<unsigned long long*>(x1);
-    auto* u2 = reinterpret_cast<unsigned long long*>(x2);
-    auto* u3 = reinterpret_cast<unsigned long long*>(x3);
-    if (moi == 0) {
-      cudaFuncSetAttribute(marg_coo_hash_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      marg_coo_hash_kernel<0><<<(unsigned)blocks, kHashT, smem, st>>>(i, j, k, v, nnz, scf, scd, u1, u2, u3);
-    } else {
-      cudaFuncSetAttribute(marg_coo_hash_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      marg_coo_hash_kernel<1><<<(unsigned)blocks, kHashT, smem, st>>>(i, j, k, v, nnz, scf, scd, u1, u2, u3);
-    }
-    return cudaGetLastError();
-  }
-  return launch_marginals_coo_atomic(i, j, k, v, nnz, moi, S, x1, x2, x3, st);
-}
-
-cudaError_t launch_marginals_coo_atomic(const int32_t* i, const int32_t* j, const int32_t* k,
-                                        const float* v, int64_t nnz, int moi, int S, int64_t* x1,
-                                        int64_t* x2, int64_t* x3, cudaStream_t st) {
   if (nnz <= 0) return cudaSuccess;
   const float scf = pow2f(S < -126 ? -126 : (S > 127 ? 127 : S));
   const double scd = ldexp(1.0, S);

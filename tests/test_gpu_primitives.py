@@ -78,11 +78,9 @@ def test_marginals_coo_bit_exact(moi):
 
 
 @pytest.mark.parametrize("moi,hot", [(0, True), (1, True), (0, False)])
-def test_marginals_coo_hashed_bit_exact(moi, hot):
-    """The block-aggregated COO marginals (shared-memory hash tables, flushed when half full)
-    on inputs large enough to take that path (>= 32K nnz, several flushes per block): Zipf-hot
-    indices (a few i / j carry most entries, the C3 / C5 hazard) and near-uniform ones; bit-exact
-    against the oracle."""
+def test_marginals_coo_large_bit_exact(moi, hot):
+    """COO marginals on larger inputs: Zipf-hot indices (a few i / j carry most entries, the
+    C3 / C5 hazard) and near-uniform ones; bit-exact against the oracle."""
     from synth import zipf_planted_coo
     torch = torch_cuda()
     if hot:
