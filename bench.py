@@ -386,7 +386,7 @@ def method_settings(w, args):
     keeps converging (the cold 30-iteration start decays both); dense C1/C2: cold
     start + tau = 0.9 (R26); C3: cold start, paper-literal tau = 0 (no planted model; its
     30-iteration summaries would fail the test)."""
-    warm = w.name.startswith("C4") or w.name == "C5"
+    warm = w.name.startswith("C4") or w.name == "C5"   # C4s / C4p: C4's profiling stand-ins
     tau = 0.9 if w.fmt == "dense" else 0.0
     if args.als_init == "cold":
         warm, tau = False, (0.0 if w.name.startswith("C4") else tau)

@@ -39,6 +39,9 @@ CONFIGS = {
     # profiling stand-in for C4 (not a BASELINE config): the same 3000 x 3000 slices, K = 300,
     # small enough for ncu kernel replay
     "C4s": Workload("C4s", "dense", 3000, 3000, 300, 270, 5, 10, 10, 16, 30, 1e-6),
+    # profiling stand-in for C4's a4 grid plan (not a BASELINE config): 3000 x 3000 x 600 slices
+    # (K0 = 550 + 50), summaries 300 x 300 x 105 -> 12 slices per CTA of the 9-CTA grid plan
+    "C4p": Workload("C4p", "dense", 3000, 3000, 600, 550, 50, 10, 10, 16, 30, 1e-6),
     # configs[4]: 100K^3, ~100M nnz, planted rank 10 Zipf 1.2, 90K + batches of 1K, s=20, r=8
     "C5": Workload("C5", "coo", 100_000, 100_000, 100_000, 90_000, 1000, 10, 20, 8, 30, 1e-6,
                    nnz=100_000_000, alpha=1.2),
