@@ -311,12 +311,6 @@ SAMBATEN_API sambaten_status sambaten_cp_als(const sambaten_tensor* X, int R, fl
                                 float* U2, double* lambda_out, int max_iters, double tol,
                                 double* fit_out, int32_t* iters_out, void* stream);
 
-/* ---- GetRank quality control (Alg. 2, P:279-294; SURVEY 8(f) NEXT #2) ------------------------
- * Core consistency (CorConDia, P:266 [bro2003new]; reading R29) of the rank-F model
- * [[lambda; A, B, C]] of the DENSE tensor X: with lambda absorbed into A, the least-squares core
- * G = X x1 pinv(A) x2 pinv(B) x3 pinv(C) and cc = 100 (1 - sum (G - T)^2 / F), T the
- * superdiagonal unit core.  A, B, C: device float32 [dims][F] row-major; lambda: device
- * float64[F]; cc: host or device float64[1].  fp64 throughout; E_INVALID on bad arguments. */
 /* ---------------------------------------------------------------------------------------
  * Full-tensor CP-ALS: the evaluation's CP_ALS baseline and relative
  * fitness, and the distributed initial decomposition.
@@ -355,10 +349,19 @@ SAMBATEN_API sambaten_status sambaten_init_dist(sambaten_t* h, const sambaten_te
  * instantiation as a large one.  Errors: E_INVALID (bad sizes), E_CUDA. */
 SAMBATEN_API sambaten_status sambaten_als_plan(int nI, int nJ, int nK, int R, int r, int plan[4]);
 
+/* ---- GetRank quality control (Alg. 2, P:279-294; SURVEY 8(f) NEXT #2) ------------------------
+ * Core consistency (CorConDia, P:266 [bro2003new]; reading R29) of the rank-F model
+ * [[lambda; A, B, C]] of the tensor X: with lambda absorbed into A, the least-squares core
+ * G = X x1 pinv(A) x2 pinv(B) x3 pinv(C) and cc = 100 (1 - sum (G - T)^2 / F), T the
+ * superdiagonal unit core.  Dense X, or a canonical COO X in DEVICE memory (sorted by (k,j,i)):
+ * the core is then formed from the nonzeros fibre by fibre ("exploits sparsity").
+ * A, B, C: device float32 [dims][F] row-major; lambda: device float64[F]; cc: host or device
+ * float64[1].  fp64 throughout; E_INVALID on bad arguments. */
 SAMBATEN_API sambaten_status sambaten_corcondia(const sambaten_tensor* X, int F, const float* A, const float* B,
                                    const float* C, const double* lambda, double* cc, void* stream);
 
-/* Alg. 2 on the dense (summary) tensor X: for every candidate rank F = 1..R_max and trial
+/* Alg. 2 on the (summary) tensor X, dense or canonical COO in device memory (the COO ALS and
+ * the sparse CorConDia): for every candidate rank F = 1..R_max and trial
  * j < trials, CP-ALS (max_iters, tol as sambaten_cp_als) from the Philox initialisation with
  * update_id = 0x47520000 + F and repetition j (R30), rated by CorConDia; R_new = the largest F
  * whose best trial reaches `threshold` (R31; 90 is customary), else 1.  cc: host float64

@@ -23,7 +23,7 @@ R31  "sort p and get top 1 index" taken literally always returns ran
 """
 import numpy as np
 
-from .sambaten import als_init, cp_als
+from .sambaten import Coo, als_init, coo_to_dense, cp_als, view_ijk
 
 GETRANK_ID = 0x47520000   # "GR" << 16: Philox update_id base of the GetRank trials (R30)
 
@@ -43,19 +43,24 @@ def tucker_core(Y, lam, A, B, C):
 
 
 def corcondia(Y, lam, A, B, C):
-    """Core consistency (R29) of the model [[lam; A, B, C]] of the dense tensor Y[i, j, k]."""
+    """Core consistency (R29) of the model [[lam; A, B, C]] of the tensor Y: dense Y[i, j, k], or
+    a Coo (densified: the same core; the GPU forms it from the nonzeros)."""
+    if isinstance(Y, Coo):
+        Y = view_ijk(coo_to_dense(Y))
     F = np.asarray(A).shape[1]
     G = tucker_core(Y, lam, A, B, C)
     return 100.0 * (1.0 - float(np.sum((G - superdiagonal(F)) ** 2)) / F)
 
 
 def getrank(Y, Rmax, trials, seed, maxit, tol, threshold=90.0, rep_base=0):
-    """Alg. 2 (R30, R31): returns (R_new, cc[Rmax][trials])."""
-    Y = np.asarray(Y, np.float64)
+    """Alg. 2 (R30, R31): returns (R_new, cc[Rmax][trials]); Y dense [i, j, k] or a Coo."""
+    if not isinstance(Y, Coo):
+        Y = np.asarray(Y, np.float64)
+    shape = Y.dims if isinstance(Y, Coo) else Y.shape
     cc = np.zeros((Rmax, trials))
     for F in range(1, Rmax + 1):
         for j in range(trials):
-            U0 = als_init(Y.shape, F, seed, GETRANK_ID + F, rep_base + j)
+            U0 = als_init(shape, F, seed, GETRANK_ID + F, rep_base + j)
             lam, U, _, _, _ = cp_als(Y, U0, maxit, tol)
             cc[F - 1, j] = corcondia(Y, lam, *U)
     best = cc.max(axis=1)

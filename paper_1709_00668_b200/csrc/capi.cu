@@ -1877,13 +1877,70 @@ extern "C" sambaten_status sambaten_als_plan(int nI, int nJ, int nK, int R, int 
   return SAMBATEN_OK;
 }
 
+// GetRank on a canonical COO tensor (device arrays): each candidate rank F and trial j runs the
+// COO ALS (r = 1, Philox init R30) and the sparse CorConDia rates it; same selection as dense.
+static sambaten_status getrank_coo(const sambaten_tensor* X, int R_max, int trials, uint64_t seed, int max_iters,
+                                   double tol, double threshold, int* R_new, double* cc, cudaStream_t st) {
+  constexpr uint32_t kGetRankId = 0x47520000u;   // R30
+  const int I = (int)X->dims[0], J = (int)X->dims[1], K = (int)X->dims[2];
+  DevBuf ws, offb, fac, ccb;
+  CK(offb.ensure(2 * sizeof(int64_t)));
+  two_offsets_kernel<<<1, 32, 0, st>>>(offb.as<int64_t>(), X->nnz);
+  CK(fac.ensure(sizeof(float) * ((size_t)I + J + K) * R_max + 256));
+  CK(ccb.ensure(sizeof(double) * (corcondia_coo_ws_doubles(I, J, K, R_max, 1) + (size_t)R_max * trials + 8)));
+  double* ccws = ccb.as<double>();
+  double* ccd = ccws + corcondia_coo_ws_doubles(I, J, K, R_max, 1);
+  for (int F = 1; F <= R_max; ++F) {
+    float* U0 = fac.as<float>();
+    float* U1 = U0 + (size_t)I * F;
+    float* U2 = U1 + (size_t)J * F;
+    for (int j = 0; j < trials; ++j) {
+      DenseAls d{};
+      int nl = 0;
+      if (sambaten_status e = coo_als(ws, st, F, X->idx[0], X->idx[1], X->idx[2], X->vals, offb.as<int64_t>(), X->nnz,
+                                      I, J, K, 1, U0, U1, U2, seed, kGetRankId + (uint32_t)F, max_iters, tol, true,
+                                      &d, &nl, (uint32_t)j, 1))
+        return e;
+      const float* U[3] = {U0, U1, U2};
+      const int64_t us[3] = {0, 0, 0};
+      CK(launch_corcondia_coo(X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, I, J, K, F, 1, U, us, d.lam, ccws,
+                              ccd + (size_t)(F - 1) * trials + j, st));
+    }
+  }
+  std::vector<double> hc((size_t)R_max * trials);
+  CK(cudaMemcpyAsync(hc.data(), ccd, sizeof(double) * hc.size(), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int best = 1;
+  for (int F = 1; F <= R_max; ++F) {
+    double m = -1e300;
+    for (int j = 0; j < trials; ++j) {
+      m = std::max(m, hc[(size_t)(F - 1) * trials + j]);
+      if (cc) cc[(size_t)(F - 1) * trials + j] = hc[(size_t)(F - 1) * trials + j];
+    }
+    if (m >= threshold) best = F;
+  }
+  *R_new = best;
+  return SAMBATEN_OK;
+}
+
 extern "C" sambaten_status sambaten_corcondia(const sambaten_tensor* X, int F, const float* A, const float* B,
                                               const float* C, const double* lambda, double* cc, void* stream) {
   if (sambaten_status e = check_dense(X, "corcondia")) return e;
-  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "corcondia: dense tensors only");
   if (F < 1 || F > kMaxR || !A || !B || !C || !lambda || !cc) FAIL(SAMBATEN_E_INVALID, "corcondia: bad argument");
   cudaStream_t st = stream_of(stream);
   const int I = (int)X->dims[0], J = (int)X->dims[1], K = (int)X->dims[2];
+  if (X->fmt == SAMBATEN_COO) {   // sparse CorConDia: device arrays, canonical order
+    DevBuf ws;
+    CK(ws.ensure(sizeof(double) * (corcondia_coo_ws_doubles(I, J, K, F, 1) + 1)));
+    double* out = ws.as<double>() + corcondia_coo_ws_doubles(I, J, K, F, 1);
+    const float* U[3] = {A, B, C};
+    const int64_t us[3] = {0, 0, 0};
+    CK(launch_corcondia_coo(X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, I, J, K, F, 1, U, us, lambda,
+                            ws.as<double>(), out, st));
+    CK(cudaMemcpyAsync(cc, out, sizeof(double), cudaMemcpyDefault, st));
+    CK(cudaStreamSynchronize(st));
+    return SAMBATEN_OK;
+  }
   void* ws = nullptr;
   CK(cudaMallocAsync(&ws, sizeof(double) * (corcondia_ws_doubles(I, J, K, F, 1) + 1), st));
   double* out = static_cast<double*>(ws) + corcondia_ws_doubles(I, J, K, F, 1);
@@ -1900,9 +1957,10 @@ extern "C" sambaten_status sambaten_getrank(const sambaten_tensor* X, int R_max,
                                             int max_iters, double tol, double threshold, int* R_new, double* cc,
                                             void* stream) {
   if (sambaten_status e = check_dense(X, "getrank")) return e;
-  if (X->fmt != SAMBATEN_DENSE) FAIL(SAMBATEN_E_INVALID, "getrank: dense tensors only");
   if (R_max < 1 || R_max > kMaxR || trials < 1 || trials > kMaxReps || max_iters < 1 || !R_new)
     FAIL(SAMBATEN_E_INVALID, "getrank: bad argument");
+  if (X->fmt == SAMBATEN_COO)
+    return getrank_coo(X, R_max, trials, seed, max_iters, tol, threshold, R_new, cc, stream_of(stream));
   DevBuf ws;
   const cudaError_t e = getrank_batch(X->vals, 0, X->dims[0], (int)X->dims[0], (int)X->dims[1], (int)X->dims[2],
                                       1, R_max, trials, seed, max_iters, tol, threshold, ws, stream_of(stream),

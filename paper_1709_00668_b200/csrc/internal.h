@@ -136,6 +136,13 @@ size_t corcondia_ws_doubles(int I, int J, int K, int F, int nm);
 cudaError_t launch_corcondia(const float* X, int64_t x_stride, int64_t pitch, int I, int J, int K, int F,
                              int nm, const float* const U[3], const int64_t u_stride[3], const double* lam,
                              double* ws, double* cc, cudaStream_t st);
+// the same for a canonical COO tensor (sorted by (k, j, i)): T1 / T2 from the nonzeros (sparse
+// CorConDia); ws: corcondia_coo_ws_doubles
+size_t corcondia_coo_ws_doubles(int I, int J, int K, int F, int nm);
+cudaError_t launch_corcondia_coo(const int32_t* ci, const int32_t* cj, const int32_t* ck, const float* cv,
+                                 int64_t nnz, int I, int J, int K, int F, int nm, const float* const U[3],
+                                 const int64_t u_stride[3], const double* lam, double* ws, double* cc,
+                                 cudaStream_t st);
 // Warm start (R34): U0 = A(I_s), U1 = B(J_s), U2 = [fp32(C(K_s) lambda); 0] per repetition
 // (Is [r][nI], Js [r][nJ], Kp [r][nK] with the first nKs entries the old slices K_s)
 cudaError_t launch_warm_init(const DenseAls& a, const float* A, const float* B, const float* C, const float* lam,

@@ -484,91 +484,6 @@ __global__ void coo_mttkrp_piece_kernel(CooAls a, int mode, int64_t npiece_max) 
   (void)npiece_max;
 }
 
-// The same piece MTTKRP with one of the two gathered factors staged in shared memory: a block
-// works on the pieces of ONE repetition (blocks_per_rep blocks each), so that repetition's
-// factor U_s (rows x R fp32, <= ~200 KB) is loaded once per block and its rows are read from
-// shared memory instead of L2 -- half the gather traffic that bounds this kernel.  The other
-// factor comes from the padded copies as before.  Same arithmetic and order as
-// coo_mttkrp_piece_kernel (lane runs in fp32, fp64 butterfly): identical results.
-template <int RB>
-__global__ void __launch_bounds__(512, 1) coo_mttkrp_smem_kernel(CooAls a, int mode, int smode, int bpr) {
-  extern __shared__ __align__(16) float Us[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const CooModePlan& pl = a.plan[mode];
-  const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
-  const int R = a.R;
-  const int RS = (R + 1) & ~1;   // staged row stride (float2 loads)
-  const int oa = mode == 0 ? 1 : 0, ob = mode == 2 ? 1 : 2;
-  const int gmode = smode == oa ? ob : oa;   // the factor still read from global memory
-  const bool staged_is_a = smode == oa;
-  const int rep = blockIdx.x / bpr, blk = blockIdx.x - rep * bpr;
-  if (rep >= a.r || a.done[rep]) return;
-  const int srows = smode == 0 ? a.nI : smode == 1 ? a.nJ : a.nK;
-  const float* src = a.Up[smode] + rep * a.up_stride[smode];
-  for (int e = threadIdx.x; e < srows * RS; e += blockDim.x) {
-    const int row = e / RS, f = e - row * RS;
-    Us[e] = f < R ? src[(int64_t)row * RB + f] : 0.f;
-  }
-  __syncthreads();
-  const float4* Ug = reinterpret_cast<const float4*>(a.Up[gmode] + rep * a.up_stride[gmode]);
-  const int64_t p0 = pl.pstart[(int64_t)rep * rows], p1 = pl.pstart[(int64_t)(rep + 1) * rows];
-  for (int64_t piece = p0 + (int64_t)blk * nw + warp; piece < p1; piece += (int64_t)bpr * nw) {
-    const int x = pl.prow[piece];
-    const int row = x - rep * rows;
-    const int64_t b = pl.pb[piece];
-    const int64_t e = min(b + kPiece, pl.ptr[x + 1]);
-    float ac[RB];
-#pragma unroll
-    for (int f = 0; f < RB; ++f) ac[f] = 0.f;
-#pragma unroll 2
-    for (int64_t t = b + lane; t < e; t += 32) {
-      const float v = pl.sv[t];
-      const int ia = pl.sa[t], ib = pl.sb[t];
-      const int is = staged_is_a ? ia : ib, ig = staged_is_a ? ib : ia;
-      const float4* rg = Ug + (int64_t)ig * (RB / 4);
-      const float2* rs = reinterpret_cast<const float2*>(Us + (int64_t)is * RS);
-      float xs[RB], xg[RB];
-#pragma unroll
-      for (int f4 = 0; f4 < RB / 4; ++f4) {
-        const float4 y = __ldg(rg + f4);
-        xg[4 * f4] = y.x; xg[4 * f4 + 1] = y.y; xg[4 * f4 + 2] = y.z; xg[4 * f4 + 3] = y.w;
-      }
-#pragma unroll
-      for (int f2 = 0; f2 < RB / 2; ++f2) {
-        if (2 * f2 < RS) {
-          const float2 y = rs[f2];
-          xs[2 * f2] = y.x; xs[2 * f2 + 1] = y.y;
-        } else {
-          xs[2 * f2] = 0.f; xs[2 * f2 + 1] = 0.f;
-        }
-      }
-      // the kernel above forms (v * U_a) * U_b: keep that association
-#pragma unroll
-      for (int f = 0; f < RB; ++f) {
-        const float xa = staged_is_a ? xs[f] : xg[f], xb = staged_is_a ? xg[f] : xs[f];
-        ac[f] = fmaf(v * xa, xb, ac[f]);
-      }
-    }
-    double acc[RB];
-#pragma unroll
-    for (int f = 0; f < RB; ++f) {
-      double s2 = (double)ac[f];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-      acc[f] = s2;
-    }
-    const bool single = pl.pstart[x + 1] - pl.pstart[x] == 1;
-    double* out = single ? a.M[mode] + (int64_t)rep * a.m_stride[mode] + (int64_t)row * R : pl.partial + piece * R;
-    if (lane < R) {
-      double v = 0.0;
-#pragma unroll
-      for (int f = 0; f < RB; ++f)
-        if (f == lane) v = acc[f];
-      out[lane] = v;
-    }
-  }
-}
-
 // rows with several pieces: sum the piece partials in order
 __global__ void coo_piece_fixup_kernel(CooAls a, int mode) {
   const CooModePlan& pl = a.plan[mode];
@@ -815,40 +730,9 @@ cudaError_t coo_build_plan(CooModePlan& pl, const int32_t* perm, const int32_t* 
   return cudaGetLastError();
 }
 
-template <int RB>
-static bool coo_mttkrp_smem_try(const CooAls& a, int mode, cudaStream_t st) {
-  // stage the smaller of the two other factors when its rows fit ~200 KB of shared memory
-  const int oa = mode == 0 ? 1 : 0, ob = mode == 2 ? 1 : 2;
-  const int n_of[3] = {a.nI, a.nJ, a.nK};
-  const int sm = n_of[oa] <= n_of[ob] ? oa : ob;
-  const size_t smem = sizeof(float) * (size_t)n_of[sm] * ((a.R + 1) & ~1);
-  if (!a.Up[0] || smem > 200 * 1024 || getenv("SAMBATEN_COO_MTTKRP_L2")) return false;
-  // enough pieces per block to amortise the factor load
-  int bpr = kNumSMs / a.r;
-  if (bpr < 1) bpr = 1;
-  cudaFuncSetAttribute(coo_mttkrp_smem_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  coo_mttkrp_smem_kernel<RB><<<(unsigned)(bpr * a.r), 512, smem, st>>>(a, mode, sm, bpr);
-  return true;
-}
-
 cudaError_t launch_coo_mttkrp(const CooAls& a, int mode, cudaStream_t st) {
   const CooModePlan& pl = a.plan[mode];
   const int64_t pmax = (int64_t)coo_plan_elems(pl.nrow, pl.n);
-  // large summaries: the shared-memory staged variant (R <= 16: padded copies exist)
-  if (pl.n >= (int64_t)1 << 20) {
-    bool done = false;
-    switch (a.RB) {
-      case 4: done = coo_mttkrp_smem_try<4>(a, mode, st); break;
-      case 8: done = coo_mttkrp_smem_try<8>(a, mode, st); break;
-      case 12: done = coo_mttkrp_smem_try<12>(a, mode, st); break;
-      case 16: done = coo_mttkrp_smem_try<16>(a, mode, st); break;
-      default: break;
-    }
-    if (done) {
-      coo_piece_fixup_kernel<<<grid_for(pl.nrow * a.R), kCT, 0, st>>>(a, mode);
-      return cudaGetLastError();
-    }
-  }
   int64_t blocks = ceil_div(pmax * 32, kCT);
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
   switch (a.RB) {

@@ -133,7 +133,82 @@ __global__ void corcondia_core_kernel(CcArgs a) {
   if (threadIdx.x == 0) a.cc[mdl] = 100.0 * (1.0 - dev / F);
 }
 
+// Sparse CorConDia ("exploits sparsity"): T1 and T2 are formed from the canonical COO
+// (sorted by (k, j, i)) without densifying -- T1(f, j, k) = sum over the fibre (j, k) of
+// P_0(f, i) x, T2(f, g, k) = sum_j P_1(g, j) T1(f, j, k) -- by one block per (model, slice k)
+// that walks the slice's fibres in order (deterministic): nnz * F + fibres * F^2 work instead
+// of I J K F.  The core kernel is the dense one.
+struct CcCoo {
+  const int32_t *ci, *cj, *ck; const float* cv; int64_t nnz;
+};
+
+__global__ void corcondia_t2_coo_kernel(CcArgs a, CcCoo x) {
+  extern __shared__ double t1[];   // [F]
+  const int k = blockIdx.x % a.K, mdl = blockIdx.x / a.K;
+  const int F = a.F;
+  // the slice's entry range by binary search on the sorted k
+  auto lower = [&](int key) {
+    int64_t lo = 0, hi = x.nnz;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (x.ck[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  __shared__ int64_t s_b, s_e;
+  if (threadIdx.x == 0) { s_b = lower(k); s_e = lower(k + 1); }
+  __syncthreads();
+  const int64_t b = s_b, e = s_e;
+  const double* P0 = a.P + ((int64_t)mdl * 3 + 0) * F * a.nmax;
+  const double* P1 = a.P + ((int64_t)mdl * 3 + 1) * F * a.nmax;
+  const int f = threadIdx.x / F, g = threadIdx.x - (threadIdx.x / F) * F;   // T2 cell of this thread
+  const bool cell = threadIdx.x < F * F;
+  double acc = 0.0;
+  for (int64_t t = b; t < e;) {
+    const int j = x.cj[t];
+    int64_t t2 = t;
+    while (t2 < e && x.cj[t2] == j) ++t2;   // the fibre (j, k): [t, t2)
+    if (threadIdx.x < F) {
+      double s = 0.0;
+      for (int64_t u = t; u < t2; ++u) s += P0[(int64_t)threadIdx.x * a.nmax + x.ci[u]] * (double)x.cv[u];
+      t1[threadIdx.x] = s;
+    }
+    __syncthreads();
+    if (cell) acc += P1[(int64_t)g * a.nmax + j] * t1[f];
+    __syncthreads();
+    t = t2;
+  }
+  if (cell) a.T2[(((int64_t)mdl * F + f) * F + g) * a.K + k] = acc;
+}
+
 }  // namespace
+
+cudaError_t launch_corcondia_coo(const int32_t* ci, const int32_t* cj, const int32_t* ck, const float* cv,
+                                 int64_t nnz, int I, int J, int K, int F, int nm, const float* const U[3],
+                                 const int64_t u_stride[3], const double* lam, double* ws, double* cc,
+                                 cudaStream_t st) {
+  CcArgs a{};
+  a.X = nullptr; a.x_stride = 0; a.pitch = 0; a.I = I; a.J = J; a.K = K; a.F = F; a.nm = nm;
+  for (int m = 0; m < 3; ++m) { a.U[m] = U[m]; a.u_stride[m] = u_stride[m]; }
+  a.lam = lam;
+  a.nmax = max(I, max(J, K));
+  a.P = ws;
+  a.T1 = nullptr;   // not formed: the fibres feed T2 directly
+  a.T2 = a.P + (size_t)nm * 3 * F * a.nmax;
+  a.W = a.T2 + (size_t)nm * F * F * K;
+  a.cc = cc;
+  CcCoo x{ci, cj, ck, cv, nnz};
+  corcondia_pinv_kernel<<<nm * 3, kGT, 0, st>>>(a);
+  const int threads = ((F * F + 31) / 32) * 32;
+  corcondia_t2_coo_kernel<<<nm * K, threads < 64 ? 64 : threads, sizeof(double) * F, st>>>(a, x);
+  corcondia_core_kernel<<<nm, kGT, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+size_t corcondia_coo_ws_doubles(int I, int J, int K, int F, int nm) {
+  const int nmax = max(I, max(J, K));
+  return (size_t)nm * (3 * (size_t)F * nmax + (size_t)F * F * K + 12 * (size_t)F * F + 1);
+}
 
 size_t corcondia_ws_doubles(int I, int J, int K, int F, int nm) {
   const int nmax = max(I, max(J, K));

@@ -9,6 +9,7 @@
 // thread), so each SM keeps ~100-190 KB of loads in flight with no register cost (a plain
 // ring read of this kind measured 5.7 TB/s on the B200, tools/micro/bw.cu).
 #include <algorithm>
+#include <stdlib.h>
 #include <type_traits>
 
 #include "common.cuh"
@@ -572,10 +573,13 @@ StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* g
   if (g.wpc < 1) g.wpc = 1;
   const int unit = kRPW * g.wpc;
   const int row_b = g.pitch * (int)sizeof(float);
-  int m = (96 * 1024) / (unit * row_b);   // ~96 KB stages: two in the ring (fewer barriers)
+  // stage / ring sizes (SBT_MARG_STAGE_KB / SBT_MARG_RING_KB: tuning experiments)
+  static const int stage_kb = getenv("SBT_MARG_STAGE_KB") ? atoi(getenv("SBT_MARG_STAGE_KB")) : 96;
+  static const int ring_kb = getenv("SBT_MARG_RING_KB") ? atoi(getenv("SBT_MARG_RING_KB")) : 192;
+  int m = (stage_kb * 1024) / (unit * row_b);   // ~96 KB stages: two in the ring (fewer barriers)
   if (m < 1) m = 1;
   g.tr = unit * m;
-  g.ns = kRingBytes / (g.tr * row_b);
+  g.ns = ring_kb * 1024 / (g.tr * row_b);
   if (g.ns > kMaxNS) g.ns = kMaxNS;
   if (g.ns < 2) { g.ns = 2; }
   int64_t nx = (int64_t)kNumSMs * kMargCTAs;

@@ -211,51 +211,3 @@ def test_fit_coo_and_cp_als_coo():
     assert abs(float(host(fit)[0]) - fo) <= 1e-3
     g = (host(lamd), *[host(u).astype(np.float64) for u in Ud])
     assert O.fms(g, (lo, *Uo)) >= 0.99
-
-
-SCRIPT_SMEM = r"""
-import sys, hashlib, numpy as np, torch
-sys.path.insert(0, ROOT)
-from paper_1709_00668_b200 import _lib as L
-from synth import zipf_planted_coo, split_coo
-X, truth = zipf_planted_coo(12000, 10000, 300, 6, 2_500_000, alpha=1.2, seed=21)
-X0, batches = split_coo(X, 280, 10)
-model = [np.ascontiguousarray(np.asarray(x, np.float32)) for x in (truth[0], truth[1], truth[2], truth[3][:280])]
-def coo(x):
-    return L.coo(*[torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (x.i, x.j, x.k, x.v)], x.dims)
-opts = L.default_opts(als_max_iters=6, als_tol=0.0, accept_tau=0.0, capacity=X.nnz, capacity_k=300, full_fit=1)
-h = L.sambaten_init_factors(coo(X0), 6, 2, 4, 3, model[1], model[2], model[3], model[0], opts)
-dig = hashlib.sha256()
-Kt = 280
-for b in batches[:2]:
-    Kt += b.dims[2]
-    info = L.sambaten_update(h, coo(b))
-    assert info.summary_entries > (1 << 20), info.summary_entries
-    m = [np.empty((12000, 6), np.float32), np.empty((10000, 6), np.float32), np.empty((Kt, 6), np.float32), np.empty(6, np.float32)]
-    L.sambaten_copy_factors(h, *m)
-    for a in m:
-        dig.update(a.tobytes())
-L.sambaten_destroy(h)
-print("DIGEST", dig.hexdigest())
-"""
-
-
-def test_coo_mttkrp_shared_memory_variant_bit_identical():
-    """Large COO summaries (> 2^20 nonzeros) run the piece MTTKRP with one factor staged in
-    shared memory; the same arithmetic in the same order as the L2-gather variant (forced with
-    SAMBATEN_COO_MTTKRP_L2, parity-tested against the oracle above): bit-identical models."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    digs = []
-    for force_l2 in (False, True):
-        env = dict(os.environ)
-        env.pop("SAMBATEN_COO_MTTKRP_L2", None)
-        if force_l2:
-            env["SAMBATEN_COO_MTTKRP_L2"] = "1"
-        r = subprocess.run([sys.executable, "-c", "ROOT = %r\n" % root + SCRIPT_SMEM], env=env,
-                           capture_output=True, text=True, timeout=900)
-        assert "DIGEST" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
-        digs.append(r.stdout.split("DIGEST")[1].strip())
-    assert digs[0] == digs[1]

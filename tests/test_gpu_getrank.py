@@ -132,3 +132,44 @@ def test_update_getrank_rank_deficient_matches_oracle():
     assert np.all(C[-Kn:, 2] == 0.0)
     for g, o in zip((lam, A, B, C), (st.lam, st.A, st.B, st.C)):
         assert np.allclose(g, o, rtol=1e-3, atol=1e-5), np.abs(g - o).max()
+
+
+# ---- sparse CorConDia / GetRank ("exploits sparsity") ----------------------------------
+def _coo_of(Y, keep):
+    """oracle Coo + device COO of Y[i, j, k] restricted to the mask `keep`."""
+    from oracle import sambaten as O
+    ii, jj, kk = np.nonzero(keep)
+    X = O.coo_canonical(ii, jj, kk, Y[ii, jj, kk].astype(np.float32), Y.shape)
+    t = L().coo(dev(X.i.astype(np.int32)), dev(X.j.astype(np.int32)), dev(X.k.astype(np.int32)), dev(X.v), X.dims)
+    return X, t
+
+
+@pytest.mark.parametrize("F,seed,density", [(2, 0, 0.3), (4, 1, 0.1), (6, 2, 0.5)])
+def test_corcondia_coo_matches_oracle(F, seed, density):
+    """The sparse CorConDia (T1 / T2 from the nonzeros, fibre by fibre) against the oracle's
+    dense core of the same tensor: |dcc| <= 1e-6 max(1, |cc|)."""
+    rng = np.random.default_rng(seed)
+    I, J, K = 34, 27, 23
+    A, B, C = rng.random((I, F)), rng.random((J, F)), rng.random((K, F))
+    Y = np.einsum("if,jf,kf->ijk", A, B, C) + 0.05 * rng.standard_normal((I, J, K))
+    X, t = _coo_of(Y, rng.random(Y.shape) < density)
+    lam = rng.random(F) + 0.5
+    A32, B32, C32 = (x.astype(np.float32) for x in (A, B, C))
+    got = L().sambaten_corcondia(t, F, dev(A32), dev(B32), dev(C32), dev(lam))
+    want = GR.corcondia(X, lam, A32.astype(np.float64), B32.astype(np.float64), C32.astype(np.float64))
+    assert abs(got - want) <= 1e-6 * max(1.0, abs(want)), (got, want)
+
+
+@pytest.mark.parametrize("F,seed", [(2, 0), (3, 1)])
+def test_getrank_coo_matches_oracle(F, seed):
+    """GetRank on a COO tensor (every entry of a planted low-rank tensor stored; the COO ALS of
+    each candidate rank and trial from the R30 point, rated by the sparse CorConDia): the same
+    R_new as the oracle, ratings within 0.05 up to the planted rank."""
+    rng = np.random.default_rng(seed)
+    A, B, C = rng.random((12, F)), rng.random((11, F)), rng.random((10, F))
+    Y = np.einsum("if,jf,kf->ijk", A, B, C).astype(np.float32).astype(np.float64)
+    X, t = _coo_of(Y, np.ones(Y.shape, bool))
+    rn_o, cc_o = GR.getrank(X, 4, 2, 7, 300, 0.0)
+    rn_g, cc_g = L().sambaten_getrank(t, 4, 2, 7, 300, 0.0)
+    assert rn_g == rn_o == F, (cc_g, cc_o)
+    assert np.all(np.abs(cc_g[:F] - cc_o[:F]) <= 0.05), (cc_g, cc_o)

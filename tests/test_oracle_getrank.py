@@ -121,3 +121,17 @@ def test_update_with_getrank_matches_only_the_present_components():
     rng = np.random.default_rng(1)
     _, _, Ct = rng.random((40, 3)), rng.random((36, 3)), rng.random((30, 3))
     assert np.allclose(st.C[-Kn:, :2], Ct[-Kn:, :2], rtol=1e-3, atol=1e-6)
+
+
+def test_corcondia_of_a_coo_tensor_is_that_of_its_densification():
+    """The oracle rates a Coo through its densification: equal to the dense call on the same
+    entries (pins the Coo branch), and an exact CP tensor stored as COO rates 100."""
+    from oracle import sambaten as O
+    rng = np.random.default_rng(5)
+    A, B, C = rng.random((9, 2)), rng.random((8, 2)), rng.random((7, 2))
+    Y = np.einsum("if,jf,kf->ijk", A, B, C).astype(np.float32).astype(np.float64)
+    ii, jj, kk = np.nonzero(Y > -1)
+    X = O.coo_canonical(ii, jj, kk, Y[ii, jj, kk].astype(np.float32), Y.shape)
+    lam = np.ones(2)
+    assert GR.corcondia(X, lam, A, B, C) == GR.corcondia(Y, lam, A, B, C)
+    assert abs(GR.corcondia(X, lam, A, B, C) - 100.0) < 1e-4
