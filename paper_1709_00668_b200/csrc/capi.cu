@@ -139,6 +139,7 @@ struct sambaten_s {
   DevBuf X;
   DevBuf model[2];          // A | B | C | lam | fit state, double-buffered (merge writes the shadow)
   DevBuf fiws;              // incremental-fit workspace (k_fitinc.cu)
+  DevBuf gord;              // the gather's (rep, slice) pairs in source-slice order
   int cur = 0;
   DevBuf ck;                // checkpoint of the model
   int64_t K_ck = -1;
@@ -500,7 +501,7 @@ extern "C" void sambaten_destroy(sambaten_t h) {
   h->model[0].release(); h->model[1].release(); h->ck.release();
   h->marg.release(); h->xm.release(); h->xm_ck.release(); h->samp.release(); h->summ.release(); h->fac.release();
   h->als.release(); h->match.release(); h->misc.release(); h->segs.release(); h->fitws.release();
-  h->coo_ws.release(); h->grws.release(); h->grk.release(); h->fiws.release();
+  h->coo_ws.release(); h->grws.release(); h->grk.release(); h->fiws.release(); h->gord.release();
   if (h->segs_host) cudaFreeHost(h->segs_host);
   if (h->hs) cudaFreeHost(h->hs);
   for (int e = 0; e < 9; ++e)
@@ -1382,8 +1383,9 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   float* Yt = use_cluster ? Y + r * y_stride : nullptr;
   a.Y = Y;
   a.Yt = Yt;
+  CK(h->gord.ensure(sizeof(int32_t) * r * nKp));
   CK(launch_gather_dense(V, Is, Js, Kp, (int)nI, (int)nJ, (int)nKp, r, nI, nJ, nKp, Y, y_stride, st,
-                         Yt, pI, pJ));
+                         Yt, pI, pJ, h->gord.as<int32_t>()));
   CK(cudaEventRecord(h->ev[4], st));
   // ---- a4: batched CP-ALS ---------------------------------------------------------------
   const size_t ws_als = align256(dense_als_workspace(&a));

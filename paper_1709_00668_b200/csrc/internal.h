@@ -64,7 +64,7 @@ cudaError_t launch_gather_dense(const DenseView& X, const int32_t* Is, const int
                                 const int32_t* Kp, int nI, int nJ, int nK, int r,
                                 int64_t idx_stride_I, int64_t idx_stride_J, int64_t idx_stride_K,
                                 float* Y, int64_t y_stride, cudaStream_t st, float* Yt = nullptr,
-                                int pI = 0, int pJ = 0);
+                                int pI = 0, int pJ = 0, int32_t* order_ws = nullptr);
 
 // ---- dense batched CP-ALS -------------------------------------------------------------
 struct DenseAls {

@@ -1,7 +1,7 @@
 // k_gather.cu -- a3 (dense): the summaries X_s = X(I_s, J_s, K_s U new).
 //
 // Y[rep][u][q][p] = X(Is[p], Js[q], Kp[u]) and, for the cluster ALS, its per-slice transpose
-// Yt[rep][u][p][q].  Block = (32-row q tile, rep, slice u); for each 32-column p tile the
+// Yt[rep][u][p][q].  Block = (32-row q tile, (rep, slice u) pair); for each 32-column p tile the
 // 8 warps gather 4 source rows each (lanes walk the sorted I_s list held in shared memory,
 // so neighbouring lanes share 32 B sectors of the source row), write the Y rows coalesced
 // and stage the 32 x 32 block in shared memory (padded, conflict-free) for the coalesced Yt
@@ -13,16 +13,52 @@ namespace sbt {
 
 constexpr int kGatherThreads = 256;
 
+// The (rep, u) pairs of all summaries ordered by their source slice K'[rep][u] (stable, one
+// block, bitonic in shared memory): the gather's blocks then walk the store slice by slice, so
+// the 16 repetitions' reads of a new slice hit L2 after the first and the address translations
+// stay within a few slices of the 108 GB store (random slice order missed the TLB).
+constexpr int kOrderMax = 8192;
+__global__ void __launch_bounds__(1024) gather_order_kernel(const int32_t* __restrict__ Kp, int nK, int r,
+                                                            int64_t sK, int32_t* __restrict__ order) {
+  extern __shared__ unsigned long long key[];   // [m], m = the power of two >= n
+  const int n = nK * r;
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int e = threadIdx.x; e < m; e += blockDim.x) {
+    if (e < n) {
+      const int rep = e / nK, u = e - rep * nK;
+      key[e] = ((unsigned long long)(unsigned)Kp[rep * sK + u] << 32) | (unsigned)e;   // (k, pair): stable
+    } else {
+      key[e] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (int kk = 2; kk <= m; kk <<= 1)
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (int e = threadIdx.x; e < m; e += blockDim.x) {
+        const int p = e ^ jj;
+        if (p > e) {
+          const bool up = (e & kk) == 0;
+          const unsigned long long a = key[e], b = key[p];
+          if ((a > b) == up) { key[e] = b; key[p] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  for (int e = threadIdx.x; e < n; e += blockDim.x) order[e] = (int32_t)(key[e] & 0xffffffffu);
+}
+
 __global__ void __launch_bounds__(kGatherThreads) gather_dense_kernel(
     const float* __restrict__ X, int64_t J, int64_t pitch, const int32_t* __restrict__ Is,
     const int32_t* __restrict__ Js, const int32_t* __restrict__ Kp, int nI, int nJ, int nK,
     int64_t sI, int64_t sJ, int64_t sK, float* __restrict__ Y, float* __restrict__ Yt,
-    int64_t y_stride, int pI, int pJ) {
+    int64_t y_stride, int pI, int pJ, const int32_t* __restrict__ order) {
   extern __shared__ int32_t is_sh[];
   __shared__ float tile[2][32][33];
-  // grid (q tile, rep, slice): the repetitions' blocks of one slice position run together, so
-  // the rows of a new slice (the same k in every repetition) are read from L2 after the first
-  const int qt = blockIdx.x, rep = blockIdx.y, u = blockIdx.z;
+  // grid (q tile, pair): pairs in source-slice order when `order` is given, else (rep, slice)
+  const int qt = blockIdx.x;
+  const int pr = order ? order[blockIdx.y] : (int)blockIdx.y;
+  const int rep = pr / nK, u = pr - rep * nK;
   const int32_t* is = Is + rep * sI;
   for (int p = threadIdx.x; p < nI; p += blockDim.x) is_sh[p] = is[p];
   __syncthreads();
@@ -77,13 +113,24 @@ __global__ void __launch_bounds__(kGatherThreads) gather_dense_kernel(
 cudaError_t launch_gather_dense(const DenseView& X, const int32_t* Is, const int32_t* Js,
                                 const int32_t* Kp, int nI, int nJ, int nK, int r,
                                 int64_t sI, int64_t sJ, int64_t sK, float* Y, int64_t y_stride,
-                                cudaStream_t st, float* Yt, int pI, int pJ) {
+                                cudaStream_t st, float* Yt, int pI, int pJ, int32_t* order_ws) {
   if (nK <= 0 || nJ <= 0 || nI <= 0 || r <= 0) return cudaSuccess;
   if (pI < nI) pI = nI;
   if (pJ < nJ) pJ = nJ;
-  dim3 grid((unsigned)ceil_div(pJ, 32), (unsigned)r, (unsigned)nK);
+  const int npair = nK * r;
+  if (npair > 65535) return cudaErrorInvalidConfiguration;   // grid.y limit
+  const int32_t* order = nullptr;
+  if (order_ws && npair <= kOrderMax && r > 1) {
+    int m = 1;
+    while (m < npair) m <<= 1;
+    cudaFuncSetAttribute(gather_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(unsigned long long) * kOrderMax));
+    gather_order_kernel<<<1, 1024, sizeof(unsigned long long) * m, st>>>(Kp, nK, r, sK, order_ws);
+    order = order_ws;
+  }
+  dim3 grid((unsigned)ceil_div(pJ, 32), (unsigned)npair, 1);
   gather_dense_kernel<<<grid, kGatherThreads, sizeof(int32_t) * nI, st>>>(
-      X.base, X.J, X.pitch, Is, Js, Kp, nI, nJ, nK, sI, sJ, sK, Y, Yt, y_stride, pI, pJ);
+      X.base, X.J, X.pitch, Is, Js, Kp, nI, nJ, nK, sI, sJ, sK, Y, Yt, y_stride, pI, pJ, order);
   return cudaGetLastError();
 }
 

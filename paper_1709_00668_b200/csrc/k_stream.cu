@@ -54,6 +54,7 @@ struct StreamGeom {
   int tr;                   // rows per stage
   int ns;                   // stages in the ring (<= kMaxNS)
   int nch = 1, wpc = 1;     // marginals: column chunks per row and warps per chunk in a CTA
+  int pc = 0;               // marginals: producer-consumer stage release (a producer warp)
   int qpt = 1, tpg = 1, ng = 1;   // fit: quads per thread, threads per row group, row groups
   bool bres = false;              // fit: B resident in shared memory (J x kMaxR floats)
 };
@@ -102,8 +103,14 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
                                                              unsigned long long* __restrict__ x3) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ unsigned long long bars[kMaxNS];
+  __shared__ unsigned long long empty[kMaxNS];   // producer-consumer mode: stage released
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
+  const int ncons = g.nch * g.wpc;                // consumer warps
+  // producer-consumer mode (g.pc): a dedicated producer warp refills a stage as soon as every
+  // consumer warp has released it (an "empty" mbarrier per stage) -- no CTA-wide barrier per
+  // stage, so a warp that finishes a stage early moves on to the next loaded one
+  const bool producer = g.pc && warp == ncons;
   // stages hold whole rows; warp w works on column chunk w % nch of the rows w / nch,
   // w / nch + wpc, ... (kRPW at a time)
   const int chunk = warp % g.nch, wslot = warp / g.nch;
@@ -115,12 +122,20 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
   float* ring = reinterpret_cast<float*>(smem);
   const int nst = (int)((re - rb + g.tr - 1) / g.tr);
   if (tid == 0) {
-    for (int s = 0; s < g.ns; ++s) s_mbar_init(&bars[s], 1);
+    for (int s = 0; s < g.ns; ++s) { s_mbar_init(&bars[s], 1); s_mbar_init(&empty[s], ncons); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0)
-    for (int s = 0; s < nst && s < g.ns; ++s) marg_issue(ring, bars, g, X, rb, re, s);
+  if (tid == 0 || (producer && lane == 0)) {
+    if (tid == 0)
+      for (int s = 0; s < nst && s < g.ns; ++s) marg_issue(ring, bars, g, X, rb, re, s);
+    if (producer)
+      for (int s = g.ns; s < nst; ++s) {   // refill stage s's slot once stage s - ns is released
+        s_wait(&empty[s % g.ns], (unsigned)((s / g.ns) - 1) & 1u);
+        s_fence_async();
+        marg_issue(ring, bars, g, X, rb, re, s);
+      }
+  }
   long long acc[kMQ][4];
 #pragma unroll
   for (int m = 0; m < kMQ; ++m)
@@ -128,7 +143,7 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
     for (int e = 0; e < 4; ++e) acc[m][e] = 0;
   long long x3run = 0;   // lane 0: running sum of slice x3k
   int64_t x3k = -1;
-  for (int s = 0; s < nst; ++s) {
+  for (int s = 0; s < nst && !producer; ++s) {
     const int64_t r0 = rb + (int64_t)s * g.tr;
     const int nr = (int)min((int64_t)g.tr, re - r0);
     const int slot = s % g.ns;
@@ -205,14 +220,20 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
         }
       }
     }
-    __syncthreads();   // stage consumed by every warp
-    if (tid == 0 && s + g.ns < nst) {
-      s_fence_async();
-      marg_issue(ring, bars, g, X, rb, re, s + g.ns);
+    if (g.pc) {
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(&empty[slot])) : "memory");
+    } else {
+      __syncthreads();   // stage consumed by every warp
+      if (tid == 0 && s + g.ns < nst) {
+        s_fence_async();
+        marg_issue(ring, bars, g, X, rb, re, s + g.ns);
+      }
     }
   }
   if (lane == 0 && x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
   // x1: the warps' column sums through the (now idle) ring, summed per column in warp order
+  // (every stage has been consumed, so no copy is in flight)
   __syncthreads();
   long long* xw = reinterpret_cast<long long*>(smem);   // [kNW][cw]
 #pragma unroll
@@ -588,7 +609,9 @@ StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* g
   g.rows_per_cta = ceil_div(g.nrows, nx);
   *gx = (int)ceil_div(g.nrows, g.rows_per_cta);
   *gy = 1;
-  *threads = 32 * g.nch * g.wpc;
+  static const int pc = getenv("SBT_MARG_PC") ? atoi(getenv("SBT_MARG_PC")) : 0;
+  g.pc = pc && g.nch * g.wpc < kNW;   // room for the producer warp
+  *threads = 32 * (g.nch * g.wpc + (g.pc ? 1 : 0));
   return g;
 }
 // Fit pass: stages of whole rows (one bulk copy); thread (group grp, lane tq) owns the column
