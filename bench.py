@@ -655,8 +655,13 @@ def main():
     clk = ClockSampler(local)
     clk.start()
     times, infos, ents, kts = [], [], [], []
-    for _ in range(args.steps):
+    prof_step = os.environ.get("SBT_PROFILE_STEP")   # ncu --profile-from-start off: one timed step
+    for si in range(args.steps):
+        if prof_step is not None and si == int(prof_step):
+            torch.cuda.cudart().cudaProfilerStart()
         ms, info, ne, bi = step()
+        if prof_step is not None and si == int(prof_step):
+            torch.cuda.cudart().cudaProfilerStop()
         times.append(ms)
         infos.append(info.as_dict())
         ents.append(ne)

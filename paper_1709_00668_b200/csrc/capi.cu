@@ -139,6 +139,7 @@ struct sambaten_s {
   DevBuf X;
   DevBuf model[2];          // A | B | C | lam | fit state, double-buffered (merge writes the shadow)
   DevBuf fiws;              // incremental-fit workspace (k_fitinc.cu)
+  DevBuf mrep;              // replicated COO marginals (k_marginals.cu)
   DevBuf gord;              // the gather's (rep, slice) pairs in source-slice order
   int cur = 0;
   DevBuf ck;                // checkpoint of the model
@@ -202,18 +203,33 @@ static bool cluster_plan(sambaten_s* h, const DenseAls& a, ClusterPlan* pl) {
 // log of the squared bound)
 static int qbits(const sambaten_s* h) { return h->maxphi_log2 + 8 + h->S; }
 
+// a1 over the COO store entries [n0, n1), added to x1 / x2 / x3 (replicated kernel when large)
+static cudaError_t coo_marginals(sambaten_s* h, int64_t n0, int64_t n1, int64_t* x1, int64_t* x2, int64_t* x3,
+                                 cudaStream_t st) {
+  const int nrep = marg_coo_replicas(n1 - n0, h->I, h->J);
+  if (nrep >= 2) {
+    cudaError_t e = h->mrep.ensure(sizeof(int64_t) * (size_t)nrep * (h->I + h->J));
+    if (e != cudaSuccess) return e;
+  }
+  return launch_marginals_coo(h->ci() + n0, h->cj() + n0, h->ck_() + n0, h->cv() + n0, n1 - n0, h->opts.moi,
+                              h->S, x1, x2, x3, st, h->I, h->J, nrep >= 2 ? h->mrep.as<int64_t>() : nullptr, nrep);
+}
+
 // ---- incremental exact fit (k_fitinc.cu) --------------------------------------------------------
 static size_t align256(size_t b);
 // Workspace: 4 term partials, the changed-row lists, counts, mode, Grams and their tiles.
 struct FitIncWs {
   double* parts[4]; int32_t *jlist, *klist; int *counts, *mode; double *G, *gws, *red;
+  uint32_t* bits; int64_t wA, wB, wC;   // COO: changed-row bitmaps of A, B, C (words) + the any flag
 };
 static cudaError_t fitinc_ws(sambaten_s* h, FitIncWs* w) {
   const int R = h->R, RB = fitrows_rb_of(R), nb = fitrows_blocks();
   const size_t pb = align256(sizeof(double) * (size_t)nb * (RB + 1));
   const size_t lb = align256(sizeof(int32_t) * (size_t)std::max<int64_t>(std::max(h->J, h->Kcap), 1));
   const size_t gw = align256(sizeof(double) * gram3_ws_doubles(h->I, h->J, h->Kcap, R));
-  const size_t need = 4 * pb + 2 * lb + 256 + align256(sizeof(double) * 3 * R * R) + gw + 256;
+  w->wA = (h->I + 31) / 32; w->wB = (h->J + 31) / 32; w->wC = (h->Kcap + 31) / 32;
+  const size_t bb = align256(sizeof(uint32_t) * (size_t)(w->wA + w->wB + w->wC + 1));
+  const size_t need = 4 * pb + 2 * lb + 256 + align256(sizeof(double) * 3 * R * R) + gw + 256 + bb;
   cudaError_t e = h->fiws.ensure(need);
   if (e != cudaSuccess) return e;
   char* p = h->fiws.as<char>();
@@ -222,7 +238,8 @@ static cudaError_t fitinc_ws(sambaten_s* h, FitIncWs* w) {
   w->klist = reinterpret_cast<int32_t*>(p); p += lb;
   w->counts = reinterpret_cast<int*>(p); w->mode = w->counts + 2; w->red = reinterpret_cast<double*>(p + 64); p += 256;
   w->G = reinterpret_cast<double*>(p); p += align256(sizeof(double) * 3 * R * R);
-  w->gws = reinterpret_cast<double*>(p);
+  w->gws = reinterpret_cast<double*>(p); p += gw;
+  w->bits = reinterpret_cast<uint32_t*>(p);
   return cudaSuccess;
 }
 
@@ -295,6 +312,55 @@ static cudaError_t fitinc_run(sambaten_s* h, const DenseView& V, int64_t Ko_stor
     if ((e = reduce(w.red, (size_t)R + 1)) != cudaSuccess) return e;
     f.reduced = w.red;
   }
+  return launch_fitinc_finish(f, st);
+}
+
+// The same for a COO store.  Term 0: the entries appended after n_old (the batch's new slices)
+// with the new model.  Term 1: the old entries with a changed A, B or old C row (bitmaps), each
+// adding v (A'B'C' - ABC)_f -- the telescoped difference in one product, since the store has no
+// per-row index; it reads the old entries' indices only when some row changed.  The full pass
+// over [0, n_tot) only when the old state is not valid.
+static cudaError_t fitinc_run_coo(sambaten_s* h, int64_t n_old, int64_t n_tot, int64_t Ko_model, int64_t K_model,
+                                  int b, int nb, bool full_only, double* relerr, cudaStream_t st) {
+  const int R = h->R;
+  FitIncWs w;
+  cudaError_t e = fitinc_ws(h, &w);
+  if (e != cudaSuccess) return e;
+  uint32_t *bA = w.bits, *bB = bA + w.wA, *bC = bB + w.wB;
+  int* any = reinterpret_cast<int*>(bC + w.wC);
+  if (full_only) {
+    const int two = 2;
+    e = cudaMemcpyAsync(w.mode, &two, sizeof(int), cudaMemcpyHostToDevice, st);
+  } else {
+    e = cudaMemsetAsync(w.bits, 0, sizeof(uint32_t) * (size_t)(w.wA + w.wB + w.wC + 1), st);
+    CooFitFlags p{};
+    p.A0 = h->A(b); p.A1 = h->A(nb); p.B0 = h->B(b); p.B1 = h->B(nb); p.C0 = h->C(b); p.C1 = h->C(nb);
+    p.I = h->I; p.J = h->J; p.Kold = Ko_model; p.R = R;
+    p.bA = bA; p.bB = bB; p.bC = bC; p.any = any; p.st_old = h->fitst(b); p.mode = w.mode;
+    if (e == cudaSuccess) e = launch_coo_fit_flags(p, st);
+  }
+  if (e != cudaSuccess) return e;
+  CooFitRows base{};
+  base.i = h->ci(); base.j = h->cj(); base.k = h->ck_(); base.v = h->cv(); base.R = R;
+  base.A = h->A(nb); base.B = h->B(nb); base.C = h->C(nb); base.gate = w.mode;
+  CooFitRows t0 = base, t1 = base, t3 = base;
+  t0.n0 = n_old; t0.n1 = n_tot; t0.gate_val = 1;
+  t1.n0 = 0; t1.n1 = n_old; t1.gate_val = 1;
+  t1.A0 = h->A(b); t1.B0 = h->B(b); t1.C0 = h->C(b); t1.bA = bA; t1.bB = bB; t1.bC = bC; t1.any = any;
+  t3.n0 = 0; t3.n1 = n_tot; t3.gate_val = 2;
+  const bool term0 = !full_only && n_old < n_tot, term1 = !full_only && n_old > 0;
+  if (term0 && (e = launch_coo_fitrows(t0, w.parts[0], st)) != cudaSuccess) return e;
+  if (term1 && (e = launch_coo_fitrows(t1, w.parts[1], st)) != cudaSuccess) return e;
+  if ((e = launch_coo_fitrows(t3, w.parts[3], st)) != cudaSuccess) return e;
+  e = launch_gram3(h->A(nb), h->B(nb), h->C(nb), h->I, h->J, K_model, R, w.G, w.gws, st);
+  if (e != cudaSuccess) return e;
+  FitFinishArgs f{};
+  f.terms[0] = term0 ? w.parts[0] : nullptr;
+  f.terms[1] = term1 ? w.parts[1] : nullptr;
+  f.terms[3] = w.parts[3];
+  for (int t = 0; t < 4; ++t) f.nparts[t] = fitrows_blocks();
+  f.mode = w.mode; f.R = R; f.RB = fitrows_rb_of(R);
+  f.st_old = h->fitst(b); f.st_new = h->fitst(nb); f.lam = h->lam(nb); f.G = w.G; f.relerr = relerr;
   return launch_fitinc_finish(f, st);
 }
 
@@ -519,12 +585,14 @@ static cudaError_t compute_committed_marginals(sambaten_s* h);
 // The incremental fit's state of the initial model (one per-component pass over X0; untimed
 // init work) when the updates will report the full fit of a dense handle (full_fit = 1).
 static cudaError_t init_fit_state(sambaten_s* h) {
-  if (h->opts.full_fit != 1 || h->fmt != SAMBATEN_DENSE || h->dist || getenv("SAMBATEN_FULL_FIT_PASS") ||
-      !fitrows_supported(h->pitch, h->R))
+  if (h->opts.full_fit != 1 || h->dist || getenv("SAMBATEN_FULL_FIT_PASS") ||
+      (h->fmt == SAMBATEN_DENSE && !fitrows_supported(h->pitch, h->R)))
     return cudaSuccess;
   cudaError_t e = h->misc.ensure(4096);
   if (e != cudaSuccess) return e;
   double* scratch = reinterpret_cast<double*>(h->misc.as<char>() + 512);
+  if (h->fmt == SAMBATEN_COO)
+    return fitinc_run_coo(h, 0, h->nnz, 0, h->K, h->cur, h->cur, true, scratch, h->st);
   return fitinc_run(h, h->view(), 0, 0, h->K, h->cur, h->cur, true, nullptr, false, scratch, h->st);
 }
 
@@ -535,6 +603,12 @@ extern "C" sambaten_status sambaten_init(sambaten_t* out, const sambaten_tensor*
   if (sambaten_status e = alloc_store_and_model(h, X0)) { sambaten_destroy(h); *out = nullptr; return e; }
   if (h->fmt == SAMBATEN_COO) {
     if (sambaten_status e = init_als_coo(h)) { sambaten_destroy(h); *out = nullptr; return e; }
+    const cudaError_t ce = init_fit_state(h);
+    if (ce != cudaSuccess || cudaStreamSynchronize(h->st) != cudaSuccess) {
+      set_error(std::string("init fit state: ") + cudaGetErrorString(ce));
+      sambaten_destroy(h); *out = nullptr;
+      return SAMBATEN_E_CUDA;
+    }
     return SAMBATEN_OK;
   }
   // full CP-ALS on X0, r = 1, Philox init with update_id 0 (R10)
@@ -1119,11 +1193,10 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
   if (h->opts.incremental_marginals && h->xm_valid) {
     CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, st));
     CK(cudaMemsetAsync(x3 + Ko, 0, sizeof(int64_t) * (h->Kcap - Ko), st));
-    CK(launch_marginals_coo(h->ci() + h->nnz, h->cj() + h->nnz, h->ck_() + h->nnz, h->cv() + h->nnz,
-                            ntot - h->nnz, h->opts.moi, h->S, x1, x2, x3, st));
+    CK(coo_marginals(h, h->nnz, ntot, x1, x2, x3, st));
   } else {
     CK(cudaMemsetAsync(x1, 0, marg_bytes, st));
-    CK(launch_marginals_coo(h->ci(), h->cj(), h->ck_(), h->cv(), ntot, h->opts.moi, h->S, x1, x2, x3, st));
+    CK(coo_marginals(h, 0, ntot, x1, x2, x3, st));
   }
   launches += 1;
   CK(cudaEventRecord(h->ev[2], st));
@@ -1194,13 +1267,24 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
   launches += 1 + 4;
   CK(cudaEventRecord(h->ev[7], st));
   // ---- a7: full fit of the new model (optional) ----------------------------------------------
-  if (h->opts.full_fit) {
+  if (h->opts.full_fit && !getenv("SAMBATEN_FULL_FIT_PASS")) {
+    // the new model's exact fit from the previous one's per-component state: the batch's entries,
+    // or one full pass when an old row changed (decided on the device)
+    CK(fitinc_run_coo(h, h->nnz, ntot, Ko, Ko + Kn, b, nbuf, false, d_relerr, st));
+    FitIncWs w;
+    CK(fitinc_ws(h, &w));
+    h->d_fit_mode = w.mode;
+    launches += 6;
+  } else if (h->opts.full_fit) {
     CK(h->fitws.ensure(sizeof(double) * coo_fit_ws_doubles(h->I, h->J, h->Kcap)));
     CooView Xn = Xall;
     Xn.K = Ko + Kn;
     CK(launch_coo_fit(Xn, h->lam(nbuf), h->A(nbuf), h->B(nbuf), h->C(nbuf), R, h->fitws.as<double>(),
                       d_relerr, st));
+    CK(cudaMemsetAsync(h->fitst(nbuf) + R + 1, 0, sizeof(double), st));   // per-component state not kept
     launches += 3;
+  } else {
+    CK(cudaMemsetAsync(h->fitst(nbuf) + R + 1, 0, sizeof(double), st));
   }
   CK(cudaEventRecord(h->ev[8], st));
   return finish_update(h, a, accepted, d_maxphi, d_vflags, d_relerr, Ko, Kn, nI, nJ, nKs, nKp, b, nbuf,
@@ -1554,8 +1638,7 @@ static cudaError_t compute_committed_marginals(sambaten_s* h) {
     if (h->fmt == SAMBATEN_DENSE)
       e = marginals_any(h->view(), 0, h->K, h->opts.moi, h->S, x1, x1 + h->I, x1 + h->I + h->J, h->st);
     else
-      e = launch_marginals_coo(h->ci(), h->cj(), h->ck_(), h->cv(), h->nnz, h->opts.moi, h->S, x1, x1 + h->I,
-                               x1 + h->I + h->J, h->st);
+      e = coo_marginals(h, 0, h->nnz, x1, x1 + h->I, x1 + h->I + h->J, h->st);
   }
   if (e == cudaSuccess) h->xm_valid = true;
   return e;
@@ -1625,8 +1708,14 @@ extern "C" sambaten_status sambaten_marginals(const sambaten_tensor* X, int moi,
     if (X->dims[0] > 4096) FAIL(SAMBATEN_E_INVALID, "marginals: dense I > 4096 not supported");
     CK(marginals_any(user_view(X), 0, X->dims[2], moi, scale_exp, x1, x2, x3, st));
   } else {
-    CK(launch_marginals_coo(X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, moi, scale_exp, x1,
-                            x2, x3, st));
+    const int nrep = marg_coo_replicas(X->nnz, X->dims[0], X->dims[1]);
+    int64_t* rws = nullptr;
+    if (nrep >= 2) CK(cudaMallocAsync(reinterpret_cast<void**>(&rws), sizeof(int64_t) * (size_t)nrep *
+                                      (X->dims[0] + X->dims[1]), st));
+    const cudaError_t e = launch_marginals_coo(X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, moi, scale_exp,
+                                               x1, x2, x3, st, X->dims[0], X->dims[1], rws, nrep);
+    if (rws) CK(cudaFreeAsync(rws, st));
+    CK(e);
   }
   return SAMBATEN_OK;
 }

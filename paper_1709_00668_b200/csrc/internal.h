@@ -28,9 +28,14 @@ struct DenseView {
 // k) are accumulated with integer atomics (callers zero them first).
 cudaError_t launch_marginals_dense(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
                                    int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st);
+// x1/x2/x3 are added to.  rep_ws (nrep * (I + J) int64, nrep = marg_coo_replicas(...) >= 2):
+// the replicated kernel for large Zipf-hot stores; NULL: one global atomic per entry and mode.
+constexpr int kMargCooMaxRep = 16;
+int marg_coo_replicas(int64_t nnz, int64_t I, int64_t J);
 cudaError_t launch_marginals_coo(const int32_t* i, const int32_t* j, const int32_t* k,
                                  const float* v, int64_t nnz, int moi, int S, int64_t* x1,
-                                 int64_t* x2, int64_t* x3, cudaStream_t st);
+                                 int64_t* x2, int64_t* x3, cudaStream_t st, int64_t I = 0, int64_t J = 0,
+                                 int64_t* rep_ws = nullptr, int nrep = 0);
 // max phi over a dense view (slices [k0,k0+nk)) or COO values; result as double bits in
 // *out (callers zero it; phi >= 0 so the bit pattern is monotone).
 // a0 fused copy + max |x| of a contiguous device batch (n floats, n % 4 == 0, 16 B aligned)
@@ -359,6 +364,25 @@ struct FitFinishArgs {
   const float* lam; const double* G;           // new lambda, Grams [3][R][R]
   double* relerr;
 };
+// COO stores (k_fitinc.cu): per-component sums P[f] = sum_e v_e A(i_e,f) B(j_e,f) C(k_e,f) and
+// sum_e v_e^2 over the store entries [n0, n1), in fitrows' partial layout (the term of new slices,
+// entries appended after n0, or the full pass); gate as in FitRows
+struct CooFitRows {
+  const int32_t *i, *j, *k; const float* v; int64_t n0, n1;
+  const float *A, *B, *C; int R;
+  const int* gate; int gate_val;
+  // difference term (old entries): sum over entries with a changed row of v (A'B'C' - ABC)_f;
+  // A0 / B0 / C0 the previous model, changed-row bitmaps, *any == 0: nothing to do
+  const float *A0, *B0, *C0; const uint32_t *bA, *bB, *bC; const int* any;
+};
+// changed-row bitmaps of A, B and the old rows of C (zeroed by the caller, with *any) and the
+// plan mode (1: incremental when the old state is valid, else 2: the full pass)
+struct CooFitFlags {
+  const float *A0, *A1, *B0, *B1, *C0, *C1; int64_t I, J, Kold; int R;
+  uint32_t *bA, *bB, *bC; int* any; const double* st_old; int* mode;
+};
+cudaError_t launch_coo_fit_flags(const CooFitFlags& f, cudaStream_t st);
+cudaError_t launch_coo_fitrows(const CooFitRows& a, double* part, cudaStream_t st);   // part: fitrows_blocks() x (RB + 1)
 int fitrows_rb_of(int R);
 bool fitrows_supported(int64_t pitch, int R);   // pitch % 4 == 0 and the transposed As fits in shared memory
 int fitrows_blocks();

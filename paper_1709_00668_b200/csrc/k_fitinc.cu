@@ -18,6 +18,8 @@
 // (P, ||X||^2, valid) lives in the model buffer (checkpointed and restored with it).
 // Every sum here is exact algebra of the same quantity the full pass computes; only the
 // rounding order differs (fp32 runs of <= I / 32 products per lane, fp64 across).
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -222,6 +224,75 @@ __global__ void fitinc_sum_kernel(FitFinishArgs a, double* out) {
   fitinc_terms_sum(a, *a.mode == 1, out);
 }
 
+// COO: one thread per entry (grid-stride, fixed order per thread), the product of the three
+// factor entries in fp32 (as the summary fits), each component's sum in fp64; block sums in the
+// fixed tree order of block_sum_d
+template <int RB>
+__global__ void __launch_bounds__(256) coo_fitrows_kernel(CooFitRows a, double* __restrict__ part) {
+  __shared__ double red[32];
+  if (a.gate && *a.gate != a.gate_val) return;
+  const int R = a.R;
+  double acc[RB + 1];
+#pragma unroll
+  for (int f = 0; f <= RB; ++f) acc[f] = 0.0;
+  if (a.bA) {   // the difference term over the old entries
+    if (*a.any == 0) {   // no changed row: zero partials
+      if (threadIdx.x <= RB) part[(int64_t)blockIdx.x * (RB + 1) + threadIdx.x] = 0.0;
+      return;
+    }
+    for (int64_t e = a.n0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.n1;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const int i = a.i[e], j = a.j[e], k = a.k[e];
+      if (!(((a.bA[i >> 5] >> (i & 31)) | (a.bB[j >> 5] >> (j & 31)) | (a.bC[k >> 5] >> (k & 31))) & 1u)) continue;
+      const float v = a.v[e];
+      const float *ra = a.A + (int64_t)i * R, *rb = a.B + (int64_t)j * R, *rc = a.C + (int64_t)k * R;
+      const float *oa = a.A0 + (int64_t)i * R, *ob = a.B0 + (int64_t)j * R, *oc = a.C0 + (int64_t)k * R;
+#pragma unroll
+      for (int f = 0; f < RB; ++f)
+        if (f < R) acc[f] += (double)v * ((double)(ra[f] * rb[f] * rc[f]) - (double)(oa[f] * ob[f] * oc[f]));
+    }
+  } else {
+    for (int64_t e = a.n0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.n1;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const float v = a.v[e];
+      const float* ra = a.A + (int64_t)a.i[e] * R;
+      const float* rb = a.B + (int64_t)a.j[e] * R;
+      const float* rc = a.C + (int64_t)a.k[e] * R;
+#pragma unroll
+      for (int f = 0; f < RB; ++f)
+        if (f < R) acc[f] += (double)v * (double)(ra[f] * rb[f] * rc[f]);
+      acc[RB] += (double)v * (double)v;
+    }
+  }
+  for (int f = 0; f <= RB; ++f) {
+    if (f < R || f == RB) {
+      const double t = block_sum_d(acc[f], red);
+      if (threadIdx.x == 0) part[(int64_t)blockIdx.x * (RB + 1) + f] = t;
+    }
+  }
+}
+
+// one thread per model row of A, B and the old rows of C: a row differing in any entry sets
+// its bit (and *any); thread 0 writes the plan mode
+__global__ void coo_fit_flags_kernel(CooFitFlags p) {
+  const int64_t n = p.I + p.J + p.Kold;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *p.mode = p.st_old[p.R + 1] == 1.0 ? 1 : 2;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const float *x0, *x1;
+    uint32_t* bm;
+    int64_t r;
+    if (t < p.I) { r = t; x0 = p.A0; x1 = p.A1; bm = p.bA; }
+    else if (t < p.I + p.J) { r = t - p.I; x0 = p.B0; x1 = p.B1; bm = p.bB; }
+    else { r = t - p.I - p.J; x0 = p.C0; x1 = p.C1; bm = p.bC; }
+    bool ch = false;
+    for (int f = 0; f < p.R; ++f) ch |= x0[r * p.R + f] != x1[r * p.R + f];
+    if (ch) {
+      atomicOr(bm + (r >> 5), 1u << (r & 31));
+      atomicOr(p.any, 1);
+    }
+  }
+}
+
 template <int RB>
 cudaError_t fitrows_rb(const FitRows& a, double* part, int nblocks, cudaStream_t st) {
   const size_t smem = sizeof(float) * (size_t)a.pitch * a.R;
@@ -250,6 +321,25 @@ cudaError_t launch_fitrows(FitRows a, double* part, cudaStream_t st) {
     case 16: return fitrows_rb<16>(a, part, nb, st);
     default: return fitrows_rb<32>(a, part, nb, st);
   }
+}
+
+cudaError_t launch_coo_fitrows(const CooFitRows& a, double* part, cudaStream_t st) {
+  const int nb = fitrows_blocks();
+  switch (fitrows_rb_of(a.R)) {
+    case 4: coo_fitrows_kernel<4><<<nb, 256, 0, st>>>(a, part); break;
+    case 8: coo_fitrows_kernel<8><<<nb, 256, 0, st>>>(a, part); break;
+    case 12: coo_fitrows_kernel<12><<<nb, 256, 0, st>>>(a, part); break;
+    case 16: coo_fitrows_kernel<16><<<nb, 256, 0, st>>>(a, part); break;
+    default: coo_fitrows_kernel<32><<<nb, 256, 0, st>>>(a, part); break;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coo_fit_flags(const CooFitFlags& f, cudaStream_t st) {
+  const int64_t n = f.I + f.J + f.Kold;
+  const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), kNumSMs * 8));
+  coo_fit_flags_kernel<<<nb, 256, 0, st>>>(f);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fitinc_plan(const FitPlanArgs& p, cudaStream_t st) {

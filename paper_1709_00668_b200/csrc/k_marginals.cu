@@ -11,6 +11,8 @@
 // the pass is one coalesced sweep over HBM (4 B / entry algorithmic).
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -255,12 +257,131 @@ __global__ void marg_coo_kernel(const int32_t* __restrict__ ii, const int32_t* _
   }
 }
 
+// Replicated variant for large stores (C5: Zipf-hot indices).  The hottest index of a Zipf(1.2)
+// mode takes ~2 % of all entries; their int64 reds on one address serialise in its L2 slice
+// (~2 M of them at C5, ~2.5 ms).  Block b adds into replica b mod nrep of x1 and x2 (nrep
+// addresses per index in different slices), runs of equal j and k are combined first (entries
+// are sorted by (k, j, i)), and a second kernel adds the replicas into x1 / x2 (integer sums:
+// exact in any order).
+template <int MOI, bool VEC>
+__global__ void __launch_bounds__(256) marg_coo_rep_kernel(
+    const int32_t* __restrict__ ii, const int32_t* __restrict__ jj, const int32_t* __restrict__ kk,
+    const float* __restrict__ vv, int64_t nnz, float scf, double scd, unsigned long long* __restrict__ x1r,
+    unsigned long long* __restrict__ x2r, int64_t I, int64_t J, int nrep, unsigned long long* __restrict__ x3) {
+  const int lane = threadIdx.x & 31;
+  const int rp = blockIdx.x % nrep;
+  unsigned long long* x1 = x1r + (int64_t)rp * I;
+  unsigned long long* x2 = x2r + (int64_t)rp * J;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t base = ((int64_t)blockIdx.x * blockDim.x) * 4; base < nnz; base += step) {
+    const int64_t e0 = base + 4 * (int64_t)threadIdx.x;
+    int i[4], j[4], k[4];
+    long long q[4];
+    if (VEC && e0 + 3 < nnz) {
+      const int4 a = __ldcs(reinterpret_cast<const int4*>(ii + e0));
+      const int4 b = __ldcs(reinterpret_cast<const int4*>(jj + e0));
+      const int4 c = __ldcs(reinterpret_cast<const int4*>(kk + e0));
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(vv + e0));
+      i[0] = a.x; i[1] = a.y; i[2] = a.z; i[3] = a.w;
+      j[0] = b.x; j[1] = b.y; j[2] = b.z; j[3] = b.w;
+      k[0] = c.x; k[1] = c.y; k[2] = c.z; k[3] = c.w;
+      q[0] = quant<MOI>(v.x, scf, scd); q[1] = quant<MOI>(v.y, scf, scd);
+      q[2] = quant<MOI>(v.z, scf, scd); q[3] = quant<MOI>(v.w, scf, scd);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int64_t e = e0 + t;
+        const bool in = e < nnz;
+        i[t] = in ? __ldcs(ii + e) : 0;
+        j[t] = in ? __ldcs(jj + e) : (t ? j[t - 1] : 0);
+        k[t] = in ? __ldcs(kk + e) : (t ? k[t - 1] : -1);
+        q[t] = in ? quant<MOI>(__ldcs(vv + e), scf, scd) : 0;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (q[t]) atomicAdd(&x1[i[t]], (unsigned long long)q[t]);
+    // x2: runs of equal j among the thread's 4 entries
+    long long s = q[0];
+#pragma unroll
+    for (int t = 1; t < 4; ++t) {
+      if (j[t] != j[t - 1]) {
+        if (s) atomicAdd(&x2[j[t - 1]], (unsigned long long)s);
+        s = 0;
+      }
+      s += q[t];
+    }
+    if (s) atomicAdd(&x2[j[3]], (unsigned long long)s);
+    // x3: one slice for the thread and the warp -> one REDUX sum; else per-thread runs
+    const int k0 = __shfl_sync(0xffffffffu, k[0], 0);
+    const bool one = k[0] == k[3] && k[0] == k0 && k0 >= 0;
+    const long long st = q[0] + q[1] + q[2] + q[3];
+    if (__all_sync(0xffffffffu, one)) {
+      const unsigned long long u = (unsigned long long)st;   // < 2^63: 21 + 21 + 21 bit chunks
+      const unsigned c0 = __reduce_add_sync(0xffffffffu, (unsigned)(u & 0x1fffffu));
+      const unsigned c1 = __reduce_add_sync(0xffffffffu, (unsigned)((u >> 21) & 0x1fffffu));
+      const unsigned c2 = __reduce_add_sync(0xffffffffu, (unsigned)(u >> 42));
+      const unsigned long long tot = (unsigned long long)c0 + ((unsigned long long)c1 << 21) + ((unsigned long long)c2 << 42);
+      if (lane == 0 && tot) atomicAdd(&x3[k0], tot);
+    } else {
+      long long r3 = q[0];
+#pragma unroll
+      for (int t = 1; t < 4; ++t) {
+        if (k[t] != k[t - 1]) {
+          if (r3 && k[t - 1] >= 0) atomicAdd(&x3[k[t - 1]], (unsigned long long)r3);
+          r3 = 0;
+        }
+        r3 += q[t];
+      }
+      if (r3 && k[3] >= 0) atomicAdd(&x3[k[3]], (unsigned long long)r3);
+    }
+  }
+}
+
+__global__ void marg_rep_combine_kernel(const unsigned long long* __restrict__ rep, int64_t n, int nrep,
+                                        unsigned long long* __restrict__ out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    unsigned long long s = 0;
+    for (int t = 0; t < nrep; ++t) s += rep[(int64_t)t * n + e];
+    if (s) out[e] += s;
+  }
+}
+
+int marg_coo_replicas(int64_t nnz, int64_t I, int64_t J) {
+  if (getenv("SAMBATEN_COO_MARG_NOREP")) return 1;
+  if (const char* e = getenv("SBT_MARG_NREP")) return atoi(e);
+  const int64_t cap = nnz / (4 * std::max<int64_t>(I + J, 1));   // zeroing + combining <= 1/4 of the pass's entries
+  return (int)std::min<int64_t>(kMargCooMaxRep, cap);
+}
+
 cudaError_t launch_marginals_coo(const int32_t* i, const int32_t* j, const int32_t* k,
                                  const float* v, int64_t nnz, int moi, int S, int64_t* x1,
-                                 int64_t* x2, int64_t* x3, cudaStream_t st) {
+                                 int64_t* x2, int64_t* x3, cudaStream_t st, int64_t I, int64_t J,
+                                 int64_t* rep_ws, int nrep) {
   if (nnz <= 0) return cudaSuccess;
   const float scf = pow2f(S < -126 ? -126 : (S > 127 ? 127 : S));
   const double scd = ldexp(1.0, S);
+  if (rep_ws && nrep >= 2 && I > 0 && J > 0) {
+    auto* r1 = reinterpret_cast<unsigned long long*>(rep_ws);
+    auto* r2 = r1 + (int64_t)nrep * I;
+    cudaError_t e = cudaMemsetAsync(rep_ws, 0, sizeof(int64_t) * (size_t)nrep * (I + J), st);
+    if (e != cudaSuccess) return e;
+    const char* bps = getenv("SBT_MARG_BPS");
+    const int blocks = kNumSMs * (bps ? atoi(bps) : 16);   // 16 per SM measured best (C5 probe)
+    auto* u3 = reinterpret_cast<unsigned long long*>(x3);
+    const bool vec = ((uintptr_t)i | (uintptr_t)j | (uintptr_t)k | (uintptr_t)v) % 16 == 0;
+    if (moi == 0 && vec)
+      marg_coo_rep_kernel<0, true><<<blocks, 256, 0, st>>>(i, j, k, v, nnz, scf, scd, r1, r2, I, J, nrep, u3);
+    else if (moi == 0)
+      marg_coo_rep_kernel<0, false><<<blocks, 256, 0, st>>>(i, j, k, v, nnz, scf, scd, r1, r2, I, J, nrep, u3);
+    else if (vec)
+      marg_coo_rep_kernel<1, true><<<blocks, 256, 0, st>>>(i, j, k, v, nnz, scf, scd, r1, r2, I, J, nrep, u3);
+    else
+      marg_coo_rep_kernel<1, false><<<blocks, 256, 0, st>>>(i, j, k, v, nnz, scf, scd, r1, r2, I, J, nrep, u3);
+    marg_rep_combine_kernel<<<(unsigned)std::min<int64_t>(ceil_div(I, 256), kNumSMs * 4), 256, 0, st>>>(r1, I, nrep, reinterpret_cast<unsigned long long*>(x1));
+    marg_rep_combine_kernel<<<(unsigned)std::min<int64_t>(ceil_div(J, 256), kNumSMs * 4), 256, 0, st>>>(r2, J, nrep, reinterpret_cast<unsigned long long*>(x2));
+    return cudaGetLastError();
+  }
   const int threads = 256;
   int64_t blocks = ceil_div(nnz, threads);
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;

@@ -99,7 +99,8 @@ for rnd in range(2):
             out.append((A, B, C, lam, info.fit_full, info.reps_rejected_mask))
         for x, y in zip(out[0][:4], out[1][:4]):
             assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
-        assert out[0][4] == out[1][4] and out[0][5] == out[1][5]
+        # the single-GPU handle keeps its fit incrementally (k_fitinc.cu), the sharded one by a pass
+        assert abs(out[0][4] - out[1][4]) <= 1e-6 and out[0][5] == out[1][5]
     for h in (hd, hs):
         L.sambaten_restore(h)
 L.sambaten_destroy(hd); L.sambaten_destroy(hs)

@@ -74,6 +74,55 @@ def test_incremental_fit_matches_oracle(case):
         assert paths[0] == 4, paths                     # a changed A row: the full pass
 
 
+def _coo_stream(zero_A=None, R=4, seed=53):
+    from synth import zipf_planted_coo, split_coo
+    X, truth = zipf_planted_coo(300, 260, 60, R, 40_000, alpha=1.2, seed=seed)
+    K0, bs = 45, 5
+    X0, batches = split_coo(X, K0, bs)
+    lam, A, B, C = (np.ascontiguousarray(np.asarray(x, np.float32)) for x in truth)
+    C = np.ascontiguousarray(C[:K0])
+    if zero_A:
+        A[zero_A] = 0.0
+        B[list(range(1, 260, 11))] = 0.0
+        C[[3, 17, 30]] = 0.0
+    opts = L().default_opts(als_max_iters=12, als_tol=0.0, accept_tau=0.0, capacity=X.nnz,
+                            capacity_k=X.dims[2], full_fit=1)
+    gc = lambda Y: L().coo(dev(Y.i.astype(np.int32)), dev(Y.j.astype(np.int32)), dev(Y.k.astype(np.int32)),
+                           dev(Y.v), Y.dims)
+    h = L().sambaten_init_factors(gc(X0), R, 2, 4, 9, A, B, C, lam, opts)
+    oc = lambda Y: O.Coo(Y.i.astype(np.int64), Y.j.astype(np.int64), Y.k.astype(np.int64), Y.v, Y.dims)
+    return h, X0, batches, gc, oc
+
+
+@pytest.mark.parametrize("case", ["coo", "coo_zero_rows"])
+def test_incremental_fit_coo_matches_oracle(case):
+    """COO stores: the batch's entries with the new model plus, when the merge refilled zeroed
+    rows of A, B or old C, the old entries of those rows with the difference of the two
+    models (fit_path 3); fit_full vs the oracle's relative error of the GPU model over the whole
+    tensor <= 1e-6."""
+    from synth import CooArrays
+
+    def concat_coo(X, b):   # b's slices re-based to k = 0 follow X's
+        return CooArrays(np.concatenate([X.i, b.i]), np.concatenate([X.j, b.j]),
+                         np.concatenate([X.k, (b.k + X.dims[2]).astype(np.int32)]), np.concatenate([X.v, b.v]),
+                         (X.dims[0], X.dims[1], X.dims[2] + b.dims[2]))
+    zero = list(range(0, 300, 7)) if case == "coo_zero_rows" else None
+    h, X, batches, gc, oc = _coo_stream(zero_A=zero)
+    I, J, R = X.dims[0], X.dims[1], 4
+    paths = []
+    try:
+        for b in batches[:3]:
+            info = L().sambaten_update(h, gc(b))
+            X = concat_coo(X, b)
+            m = tuple(np.asarray(v, np.float64) for v in _model(h, I, J, X.dims[2], R))
+            rel_o = O.relative_error(oc(X), *m)
+            assert abs((1.0 - info.fit_full) - rel_o) <= 1e-6, (case, info.fit_full, 1 - rel_o, info.fit_path)
+            paths.append(info.fit_path)
+    finally:
+        L().sambaten_destroy(h)
+    assert all(p == 3 for p in paths), paths
+
+
 SCRIPT = r'''
 import os, sys, numpy as np, torch
 sys.path.insert(0, ROOT)

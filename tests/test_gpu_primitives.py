@@ -77,13 +77,17 @@ def test_marginals_coo_bit_exact(moi):
         assert np.array_equal(host(g), r)
 
 
-@pytest.mark.parametrize("moi,hot", [(0, True), (1, True), (0, False)])
+@pytest.mark.parametrize("moi,hot", [(0, True), (1, True), (0, False), (0, "rep"), (1, "rep")])
 def test_marginals_coo_large_bit_exact(moi, hot):
     """COO marginals on larger inputs: Zipf-hot indices (a few i / j carry most entries, the
-    C3 / C5 hazard) and near-uniform ones; bit-exact against the oracle."""
+    C3 / C5 hazard) and near-uniform ones; bit-exact against the oracle.  "rep": nnz >= 8 (I + J),
+    the replicated kernel (16 copies of x1 / x2, warp-combined j / k runs)."""
     from synth import zipf_planted_coo
     torch = torch_cuda()
-    if hot:
+    if hot == "rep":
+        Xs, _ = zipf_planted_coo(12_000, 9_000, 300, 4, 1_500_000, alpha=1.2, seed=10)
+        assert Xs.nnz >= 64 * (12_000 + 9_000)
+    elif hot:
         Xs, _ = zipf_planted_coo(60_000, 50_000, 400, 4, 600_000, alpha=1.3, seed=8)
     else:
         rng = np.random.default_rng(9)
