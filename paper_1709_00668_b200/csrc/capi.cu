@@ -960,6 +960,14 @@ struct Bump {
   }
 };
 
+// pinned host words for the COO ALS's done flags (kMaxReps; one per host thread)
+static int* pinned_done_flags() {
+  thread_local int* p = nullptr;
+  if (!p && cudaHostAlloc(reinterpret_cast<void**>(&p), sizeof(int) * kMaxReps, cudaHostAllocDefault) != cudaSuccess)
+    p = nullptr;
+  return p;
+}
+
 static int bits_for(int64_t n) { int b = 1; while (((int64_t)1 << b) < n) ++b; return b; }
 
 // the model rows a warm-started summary ALS begins from (R34): A(I_s), B(J_s), C(K_s) diag(lambda)
@@ -1093,14 +1101,27 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     if (e == cudaSuccess) e = launch_pad_factors(ra, st);
     const bool rows = R <= 16;
     if (e == cudaSuccess) e = cudaMemsetAsync(stop, 0, sizeof(int) * r, st);
-    for (int it = 0; it < maxit && e == cudaSuccess; ++it) {
+    // the stop test runs on the device; the host looks at the done flags after iterations 3,
+    // 6, 10, 15, ... (one small read each) and stops launching once every repetition is done
+    int nit = 0, next_check = 3, gap = 3;
+    for (int it = 0; it < maxit && e == cudaSuccess; ++it, ++nit) {
       if (rows && it > 0) e = launch_als_rows_commit(ra, st);
       for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
         e = launch_coo_mttkrp(a, m, st);
         if (e == cudaSuccess) e = rows ? launch_als_rows_mode(ra, m, st) : launch_als_solve(*d, m, st);
       }
+      int* hd = pinned_done_flags();
+      if (hd && rows && e == cudaSuccess && it + 1 == next_check && it + 1 < maxit) {
+        next_check += ++gap;
+        e = launch_als_rows_commit(ra, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hd, done, sizeof(int) * r, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        int nd = 0;
+        for (int t = 0; t < r; ++t) nd += hd[t] != 0;
+        if (nd == r) { ++nit; break; }
+      }
     }
-    *launches = 2 * 3 + 9 + 3 + 3 + 3 + (rows ? 16 : 6) * maxit;
+    *launches = 2 * 3 + 9 + 3 + 3 + 3 + (rows ? 16 : 6) * nit;
     if (e != cudaSuccess) {
       set_error(std::string("COO ALS: ") + cudaGetErrorString(e));
       d->nI = -1;

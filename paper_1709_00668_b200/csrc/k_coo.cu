@@ -161,37 +161,92 @@ __global__ void build_mask_kernel(const int32_t* __restrict__ loc, int64_t n, in
 }
 
 constexpr int kGTile = kCT * 8;   // entries per gather block
+constexpr int64_t kGatherSmemMax = 212 * 1024;
 
-// pass 1: counts[rho][block] of entries with bit rho set
-__global__ void coo_gather_count_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
-                                        const int32_t* __restrict__ kk, int64_t n,
-                                        const uint32_t* __restrict__ mI, const uint32_t* __restrict__ mJ,
-                                        const uint32_t* __restrict__ mK, int r, int64_t nblocks,
-                                        int64_t* __restrict__ counts) {
-  __shared__ int cnt[32];
-  if (threadIdx.x < 32) cnt[threadIdx.x] = 0;
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kGTile;
-  int local[32];
-  for (int rho = 0; rho < r; ++rho) local[rho] = 0;
-  for (int t = 0; t < kGTile / kCT; ++t) {
-    const int64_t e = base + (int64_t)t * kCT + threadIdx.x;
-    const uint32_t m = e < n ? (mI[ii[e]] & mJ[jj[e]] & mK[kk[e]]) : 0u;
-    const int lane = threadIdx.x & 31;
-    for (int rho = 0; rho < r; ++rho) {
-      const unsigned b = __ballot_sync(0xffffffffu, (m >> rho) & 1u);
-      if (lane == 0) local[rho] += __popc(b);
-    }
+// Membership of an entry: mI[i] & mJ[j] & mK[k] (bit rho: in repetition rho's summary).  SM: the
+// I and J masks (r <= 8: one byte per index) staged in shared memory once per persistent block
+// (C5: 200 KB; the uint32 masks in L2 cost one random sector read per entry and mode), mK read
+// from global memory (the entries are sorted by k: a slice's word stays in L1).
+template <bool SM>
+struct GatherMasks {
+  const uint32_t *mI, *mJ, *mK;
+  const uint8_t* sh;
+  int64_t I;
+  __device__ __forceinline__ uint32_t operator()(int i, int j, int k) const {
+    if (SM) return (uint32_t)(sh[i] & sh[I + j]) & mK[k];
+    return mI[i] & mJ[j] & mK[k];
   }
-  if ((threadIdx.x & 31) == 0)
-    for (int rho = 0; rho < r; ++rho)
-      if (local[rho]) atomicAdd(&cnt[rho], local[rho]);
+};
+
+template <bool SM>
+__device__ __forceinline__ void stage_masks(const uint32_t* mI, const uint32_t* mJ, int64_t I, int64_t J,
+                                            uint8_t* sh) {
+  if (!SM) return;
+  for (int64_t x = threadIdx.x; x < I + J; x += blockDim.x) sh[x] = (uint8_t)(x < I ? mI[x] : mJ[x - I]);
   __syncthreads();
-  if (threadIdx.x < r) counts[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
 }
 
-// pass 2: write the entries of every repetition in input order at offsets[rho][block]
-__global__ void coo_gather_write_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+// SM: 1024-thread blocks of four independent 256-thread groups (one tile each, named barrier
+// per group), so the persistent block keeps 32 warps in flight; else one group per block.
+template <bool SM>
+__device__ __forceinline__ void group_sync(int g) {
+  if (SM) asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kCT) : "memory");
+  else __syncthreads();
+}
+
+// pass 1: counts[rho][tile] of entries with bit rho set (persistent blocks over the tiles)
+template <bool SM>
+__global__ void __launch_bounds__(SM ? 4 * kCT : kCT) coo_gather_count_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
+                                        const int32_t* __restrict__ kk, int64_t n,
+                                        const uint32_t* __restrict__ mI, const uint32_t* __restrict__ mJ,
+                                        const uint32_t* __restrict__ mK, int64_t I, int64_t J, int r,
+                                        int64_t nblocks, int64_t* __restrict__ counts) {
+  constexpr int G = SM ? 4 : 1;
+  constexpr int RM = SM ? 8 : 32;   // repetitions held in registers (SM: r <= 8)
+  extern __shared__ uint8_t msh[];
+  __shared__ int cnt_all[G][32];
+  stage_masks<SM>(mI, mJ, I, J, msh);
+  const GatherMasks<SM> mask{mI, mJ, mK, msh, I};
+  const int g = threadIdx.x / kCT, tid = threadIdx.x - g * kCT, lane = tid & 31;
+  int* cnt = cnt_all[g];
+  for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < nblocks; tile += (int64_t)gridDim.x * G) {
+    if (tid < 32) cnt[tid] = 0;
+    group_sync<SM>(g);
+    const int64_t base = tile * kGTile;
+    constexpr int PER = kGTile / kCT;
+    int ei[PER], ej[PER], ek[PER];
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {   // all of the thread's loads in flight at once
+      const int64_t e = base + (int64_t)t * kCT + tid;
+      const bool in = e < n;
+      ei[t] = in ? __ldcs(ii + e) : -1;
+      ej[t] = in ? __ldcs(jj + e) : 0;
+      ek[t] = in ? __ldcs(kk + e) : 0;
+    }
+    int local[RM];
+#pragma unroll
+    for (int rho = 0; rho < RM; ++rho) local[rho] = 0;
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const uint32_t m = ei[t] >= 0 ? mask(ei[t], ej[t], ek[t]) : 0u;
+#pragma unroll
+      for (int rho = 0; rho < RM; ++rho) local[rho] += (int)((m >> rho) & 1u);
+    }
+#pragma unroll
+    for (int rho = 0; rho < RM; ++rho) {
+      if (rho >= r) break;
+      const int w = (int)__reduce_add_sync(0xffffffffu, (unsigned)local[rho]);
+      if (lane == 0 && w) atomicAdd(&cnt[rho], w);
+    }
+    group_sync<SM>(g);
+    if (tid < r) counts[(int64_t)tid * nblocks + tile] = cnt[tid];
+    group_sync<SM>(g);
+  }
+}
+
+// pass 2: write the entries of every repetition in input order at offsets[rho][tile]
+template <bool SM>
+__global__ void __launch_bounds__(SM ? 4 * kCT : kCT) coo_gather_write_kernel(const int32_t* __restrict__ ii, const int32_t* __restrict__ jj,
                                         const int32_t* __restrict__ kk, const float* __restrict__ vv,
                                         int64_t n, const uint32_t* __restrict__ mI,
                                         const uint32_t* __restrict__ mJ, const uint32_t* __restrict__ mK,
@@ -201,53 +256,83 @@ __global__ void coo_gather_write_kernel(const int32_t* __restrict__ ii, const in
                                         const int64_t* __restrict__ offsets, int32_t* __restrict__ op,
                                         int32_t* __restrict__ oq, int32_t* __restrict__ ou,
                                         float* __restrict__ ov) {
-  __shared__ int wcnt[kCT / 32][32];
-  __shared__ int64_t woff[kCT / 32][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int G = SM ? 4 : 1;
+  constexpr int RM = SM ? 8 : 32;
   constexpr int NW = kCT / 32;
   constexpr int PER = kGTile / kCT;
-  // each warp owns a contiguous sub-tile of kGTile / NW entries, processed in rounds of 32
-  const int64_t base = (int64_t)blockIdx.x * kGTile + (int64_t)warp * (kGTile / NW);
-  int c[32];
-  for (int rho = 0; rho < r; ++rho) c[rho] = 0;
-  for (int t = 0; t < PER; ++t) {
-    const int64_t e = base + (int64_t)t * 32 + lane;
-    const uint32_t m = e < n ? (mI[ii[e]] & mJ[jj[e]] & mK[kk[e]]) : 0u;
-    for (int rho = 0; rho < r; ++rho) c[rho] += __popc(__ballot_sync(0xffffffffu, (m >> rho) & 1u));
-  }
-  if (lane == 0)
-    for (int rho = 0; rho < r; ++rho) wcnt[warp][rho] = c[rho];
-  __syncthreads();
-  if (threadIdx.x < r) {   // warp offsets within the block, in warp order
-    int64_t run = offsets[(int64_t)threadIdx.x * nblocks + blockIdx.x];
-    for (int w = 0; w < NW; ++w) { woff[w][threadIdx.x] = run; run += wcnt[w][threadIdx.x]; }
-  }
-  __syncthreads();
-  int64_t pos[32];
-  for (int rho = 0; rho < r; ++rho) pos[rho] = woff[warp][rho];
+  extern __shared__ uint8_t msh[];
+  __shared__ int wcnt_all[G][NW][32];
+  __shared__ int64_t woff_all[G][NW][32];
+  stage_masks<SM>(mI, mJ, nIall, nJall, msh);
+  const GatherMasks<SM> mask{mI, mJ, mK, msh, nIall};
+  const int g = threadIdx.x / kCT, tid = threadIdx.x - g * kCT;
+  const int lane = tid & 31, warp = tid >> 5;
+  int (*wcnt)[32] = wcnt_all[g];
+  int64_t (*woff)[32] = woff_all[g];
   const unsigned lt = (1u << lane) - 1u;
-  for (int t = 0; t < PER; ++t) {
-    const int64_t e = base + (int64_t)t * 32 + lane;
-    uint32_t m = 0;
-    int32_t i = 0, j = 0, k = 0;
-    float v = 0.f;
-    if (e < n) {
-      i = ii[e]; j = jj[e]; k = kk[e];
-      m = mI[i] & mJ[j] & mK[k];
-      if (m) v = vv[e];
-    }
-    for (int rho = 0; rho < r; ++rho) {
-      const bool in = (m >> rho) & 1u;
-      const unsigned b = __ballot_sync(0xffffffffu, in);
-      if (in) {
-        const int64_t d = pos[rho] + __popc(b & lt);
-        op[d] = locI[(int64_t)rho * nIall + i];
-        oq[d] = locJ[(int64_t)rho * nJall + j];
-        ou[d] = k < Ko ? locK[(int64_t)rho * Ko + k] : nKs + (k - (int32_t)Ko);
-        ov[d] = v;
+  for (int64_t tile = (int64_t)blockIdx.x * G + g; tile < nblocks; tile += (int64_t)gridDim.x * G) {
+    // each warp owns a contiguous sub-tile of kGTile / NW entries, processed in rounds of 32
+    const int64_t base = tile * kGTile + (int64_t)warp * (kGTile / NW);
+    uint32_t mm[PER];
+    {
+      int ei[PER], ej[PER], ek[PER];
+#pragma unroll
+      for (int t = 0; t < PER; ++t) {   // all loads in flight, then the masks
+        const int64_t e = base + (int64_t)t * 32 + lane;
+        const bool in = e < n;
+        ei[t] = in ? ii[e] : -1;
+        ej[t] = in ? jj[e] : 0;
+        ek[t] = in ? kk[e] : 0;
       }
-      pos[rho] += __popc(b);
+#pragma unroll
+      for (int t = 0; t < PER; ++t) mm[t] = ei[t] >= 0 ? mask(ei[t], ej[t], ek[t]) : 0u;
     }
+    int c[RM];
+#pragma unroll
+    for (int rho = 0; rho < RM; ++rho) c[rho] = 0;
+#pragma unroll
+    for (int t = 0; t < PER; ++t)
+#pragma unroll
+      for (int rho = 0; rho < RM; ++rho) c[rho] += (int)((mm[t] >> rho) & 1u);
+#pragma unroll
+    for (int rho = 0; rho < RM; ++rho) {
+      if (rho >= r) break;
+      const int w = (int)__reduce_add_sync(0xffffffffu, (unsigned)c[rho]);
+      if (lane == 0) wcnt[warp][rho] = w;
+    }
+    group_sync<SM>(g);
+    if (tid < r) {   // warp offsets within the tile, in warp order
+      int64_t run = offsets[(int64_t)tid * nblocks + tile];
+      for (int w = 0; w < NW; ++w) { woff[w][tid] = run; run += wcnt[w][tid]; }
+    }
+    group_sync<SM>(g);
+    int64_t pos[RM];
+#pragma unroll
+    for (int rho = 0; rho < RM; ++rho) pos[rho] = rho < r ? woff[warp][rho] : 0;
+#pragma unroll
+    for (int t = 0; t < PER; ++t) {
+      const int64_t e = base + (int64_t)t * 32 + lane;
+      const uint32_t m = mm[t];
+      if (__ballot_sync(0xffffffffu, m != 0) == 0) continue;   // no member among these 32
+      int32_t i = 0, j = 0, k = 0;
+      float v = 0.f;
+      if (m) { i = ii[e]; j = jj[e]; k = kk[e]; v = vv[e]; }
+#pragma unroll
+      for (int rho = 0; rho < RM; ++rho) {
+        if (rho >= r) break;
+        const bool in = (m >> rho) & 1u;
+        const unsigned b = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const int64_t d = pos[rho] + __popc(b & lt);
+          op[d] = locI[(int64_t)rho * nIall + i];
+          oq[d] = locJ[(int64_t)rho * nJall + j];
+          ou[d] = k < Ko ? locK[(int64_t)rho * Ko + k] : nKs + (k - (int32_t)Ko);
+          ov[d] = v;
+        }
+        pos[rho] += __popc(b);
+      }
+    }
+    group_sync<SM>(g);   // woff / wcnt reused by the next tile
   }
 }
 
@@ -336,13 +421,16 @@ __global__ void make_keys_kernel(const int32_t* __restrict__ idx, const int64_t*
 
 // ptr[rho][x] = first position (in the sorted order) of the entries of rep rho with index x;
 // from the sorted composite keys: counts then scan.
-__global__ void key_count_kernel(const uint32_t* __restrict__ keys, int64_t n, int kb, int64_t rows,
-                                 int64_t* __restrict__ cnt /* [r*rows] */) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+// The keys are sorted, so ptr[x] for the rows x in (row(e-1), row(e)] is e: every row pointer
+// written once, no counting (the Zipf-hot rows made per-entry count atomics contend).
+__global__ void key_ptr_kernel(const uint32_t* __restrict__ keys, int64_t n, int kb, int64_t rows, int64_t m,
+                               int64_t* __restrict__ ptr /* [m = r*rows + 1] */) {
+  const uint32_t lo = (1u << kb) - 1u;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t k = keys[e];
-    const int64_t rho = k >> kb, x = k & ((1u << kb) - 1u);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[rho * rows + x]), 1ull);
+    const int64_t x = e < n ? (int64_t)(keys[e] >> kb) * rows + (keys[e] & lo) : m - 1;
+    const int64_t xp = e > 0 ? (int64_t)(keys[e - 1] >> kb) * rows + (keys[e - 1] & lo) : -1;
+    for (int64_t y = xp + 1; y <= x; ++y) ptr[y] = e;   // e == n: the trailing rows up to m - 1
   }
 }
 
@@ -356,6 +444,14 @@ __global__ void key_count_kernel(const uint32_t* __restrict__ keys, int64_t n, i
 // no float atomics.
 // ---------------------------------------------------------------------------------------
 constexpr int kPiece = 256;
+constexpr int kShortPiece = 16;   // pieces up to this many entries: lane per component
+
+// every repetition converged: a whole launch of the iteration has nothing to do (one warp vote;
+// r <= 32)
+__device__ __forceinline__ bool all_reps_done(const int* done, int r) {
+  const int lane = threadIdx.x & 31;
+  return __all_sync(0xffffffffu, lane >= r || done[lane] != 0);
+}
 
 __global__ void piece_count_kernel(const int64_t* __restrict__ ptr, int64_t nrow, int64_t* __restrict__ cnt) {
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= nrow;
@@ -411,6 +507,7 @@ __global__ void permute4_kernel(const int32_t* __restrict__ perm, const int32_t*
 template <int RB>
 __global__ void coo_mttkrp_piece_kernel(CooAls a, int mode, int64_t npiece_max) {
   const int lane = threadIdx.x & 31;
+  if (all_reps_done(a.done, a.r)) return;
   const CooModePlan& pl = a.plan[mode];
   const int64_t P = pl.pstart[pl.nrow];
   const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
@@ -423,6 +520,24 @@ __global__ void coo_mttkrp_piece_kernel(CooAls a, int mode, int64_t npiece_max) 
     if (a.done[rep]) continue;
     const int64_t b = pl.pb[piece];
     const int64_t e = min(b + kPiece, pl.ptr[x + 1]);
+    const bool single = pl.pstart[x + 1] - pl.pstart[x] == 1;
+    double* out = single ? a.M[mode] + (int64_t)rep * a.m_stride[mode] + (int64_t)row * R
+                         : pl.partial + piece * R;
+    if (e - b <= kShortPiece) {
+      // short piece (most rows of a sparse summary): lane f < R sums component f over the
+      // entries in order (fp32 products, fp64 sum) -- no butterfly of RB doubles
+      if (lane < R) {
+        const float* Ua = a.U[oa] + rep * a.u_stride[oa];
+        const float* Ub = a.U[ob] + rep * a.u_stride[ob];
+        double s = 0.0;
+        for (int64_t t = b; t < e; ++t) {
+          const float v = pl.sv[t];
+          s += (double)(v * Ua[(int64_t)pl.sa[t] * R + lane] * Ub[(int64_t)pl.sb[t] * R + lane]);
+        }
+        out[lane] = s;
+      }
+      continue;
+    }
     double acc[RB];
     if (a.Up[oa]) {
       // padded factor rows (16 B aligned): vector gathers; fp32 lane runs of <= kPiece / 32
@@ -470,9 +585,6 @@ __global__ void coo_mttkrp_piece_kernel(CooAls a, int mode, int64_t npiece_max) 
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       acc[f] = s;
     }
-    const bool single = pl.pstart[x + 1] - pl.pstart[x] == 1;
-    double* out = single ? a.M[mode] + (int64_t)rep * a.m_stride[mode] + (int64_t)row * R
-                         : pl.partial + piece * R;
     if (lane < R) {
       double v = 0.0;
 #pragma unroll
@@ -486,6 +598,7 @@ __global__ void coo_mttkrp_piece_kernel(CooAls a, int mode, int64_t npiece_max) 
 
 // rows with several pieces: sum the piece partials in order
 __global__ void coo_piece_fixup_kernel(CooAls a, int mode) {
+  if (all_reps_done(a.done, a.r)) return;
   const CooModePlan& pl = a.plan[mode];
   const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
   const int R = a.R;
@@ -618,10 +731,25 @@ cudaError_t launch_build_mask(const int32_t* loc, int64_t n, int r, uint32_t* ma
 
 int64_t coo_gather_blocks(int64_t nnz) { return ceil_div(nnz > 0 ? nnz : 1, kGTile); }
 
+// the shared-memory masks when r <= 8, I + J bytes fit and the store spans many tiles
+static bool gather_sm(const CooView& X, int r, int64_t nb) {
+  // staging reads 148 x 4 (I + J) B of masks: worth it when the entries' bytes dwarf that
+  return r <= 8 && X.I + X.J <= kGatherSmemMax && nb >= 4 * kNumSMs && X.nnz >= 100 * (X.I + X.J) &&
+         !getenv("SAMBATEN_COO_GATHER_GLOBAL");
+}
+
 cudaError_t launch_coo_gather_count(const CooView& X, const uint32_t* mI, const uint32_t* mJ,
                                     const uint32_t* mK, int r, int64_t* counts, cudaStream_t st) {
   const int64_t nb = coo_gather_blocks(X.nnz);
-  coo_gather_count_kernel<<<(unsigned)nb, kCT, 0, st>>>(X.i, X.j, X.k, X.nnz, mI, mJ, mK, r, nb, counts);
+  if (gather_sm(X, r, nb)) {
+    const int smem = (int)((X.I + X.J + 15) & ~15ll);
+    cudaFuncSetAttribute(coo_gather_count_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    coo_gather_count_kernel<true><<<kNumSMs, 4 * kCT, smem, st>>>(X.i, X.j, X.k, X.nnz, mI, mJ, mK, X.I, X.J, r, nb,
+                                                                counts);
+  } else {
+    coo_gather_count_kernel<false><<<(unsigned)nb, kCT, 0, st>>>(X.i, X.j, X.k, X.nnz, mI, mJ, mK, X.I, X.J, r, nb,
+                                                                   counts);
+  }
   return cudaGetLastError();
 }
 
@@ -631,9 +759,17 @@ cudaError_t launch_coo_gather_write(const CooView& X, const uint32_t* mI, const 
                                     const int64_t* offsets, int32_t* op, int32_t* oq, int32_t* ou,
                                     float* ov, cudaStream_t st) {
   const int64_t nb = coo_gather_blocks(X.nnz);
-  coo_gather_write_kernel<<<(unsigned)nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, mI, mJ, mK, locI,
-                                                        locJ, locK, X.I, X.J, Ko, nKs, r, nb, offsets,
-                                                        op, oq, ou, ov);
+  if (gather_sm(X, r, nb)) {
+    const int smem = (int)((X.I + X.J + 15) & ~15ll);
+    cudaFuncSetAttribute(coo_gather_write_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    coo_gather_write_kernel<true><<<kNumSMs, 4 * kCT, smem, st>>>(X.i, X.j, X.k, X.v, X.nnz, mI, mJ, mK, locI, locJ,
+                                                                locK, X.I, X.J, Ko, nKs, r, nb, offsets, op, oq,
+                                                                ou, ov);
+  } else {
+    coo_gather_write_kernel<false><<<(unsigned)nb, kCT, 0, st>>>(X.i, X.j, X.k, X.v, X.nnz, mI, mJ, mK, locI, locJ,
+                                                                   locK, X.I, X.J, Ko, nKs, r, nb, offsets, op, oq,
+                                                                   ou, ov);
+  }
   return cudaGetLastError();
 }
 
@@ -656,7 +792,9 @@ cudaError_t coo_sort_by_index(const int32_t* idx, const int64_t* off, int r, int
   if (n <= 0) return cudaSuccess;
   make_keys_kernel<<<grid_for(n), kCT, 0, st>>>(idx, off, r, kb, n, keys);
   iota_kernel<<<grid_for(n), kCT, 0, st>>>(perm, n);
-  const int bits = kb + 6;   // rep <= 32 needs 6 bits
+  int rb = 0;
+  while ((1 << rb) < r) ++rb;
+  const int bits = kb + rb;   // (rep, index) keys: 2 passes of 8 bits when they fit 16 bits
   const int64_t nb = ceil_div(n, kRTile);
   uint32_t* ka = keys; int32_t* va = perm;
   uint32_t* kb_ = ws_keys; int32_t* vb = ws_vals;
@@ -689,10 +827,9 @@ cudaError_t coo_make_keys(const int32_t* idx, const int64_t* off, int r, int kb,
 cudaError_t coo_row_pointers(const uint32_t* sorted_keys, int64_t n, int kb, int r, int64_t rows,
                              int64_t* cnt, int64_t* ptr, int64_t* sws, cudaStream_t st) {
   const int64_t m = (int64_t)r * rows + 1;
-  cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(int64_t) * m, st);
-  if (e != cudaSuccess) return e;
-  if (n > 0) key_count_kernel<<<grid_for(n), kCT, 0, st>>>(sorted_keys, n, kb, rows, cnt);
-  return exclusive_scan_i64(cnt, m, ptr, sws, st);
+  (void)cnt; (void)sws;
+  key_ptr_kernel<<<grid_for(n + 1), kCT, 0, st>>>(sorted_keys, n, kb, rows, m, ptr);
+  return cudaGetLastError();
 }
 
 __global__ void coo_max_phi_kernel(const float* __restrict__ v, int64_t n, int moi,

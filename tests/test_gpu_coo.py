@@ -155,10 +155,12 @@ def _rand_coo(dims, nnz, seed):
 
 
 @pytest.mark.parametrize("dims,ns", [((50, 40, 30), (25, 13, 7)), ((300, 200, 64), (30, 200, 64)),
-                                     ((7, 5, 3), (7, 5, 3))])
+                                     ((7, 5, 3), (7, 5, 3)), ((3000, 2000, 400), (700, 300, 120))])
 def test_gather_coo_bit_exact(dims, ns):
+    """The last case spans >= 4 x 148 tiles of 2048 entries: the persistent kernels with the I / J
+    membership masks in shared memory."""
     torch = torch_cuda()
-    X = _rand_coo(dims, 4000, 11)
+    X = _rand_coo(dims, 1_700_000 if dims[0] == 3000 else 4000, 11)
     rng = np.random.default_rng(3)
     idx = [np.sort(rng.choice(d, n, replace=False)).astype(np.int32) for d, n in zip(dims, ns)]
     cap = X.nnz
