@@ -43,8 +43,8 @@ using namespace sbt;
 // a1 / a7 dispatch: the TMA-ring streaming kernels when the view allows them (pitch % 4 == 0,
 // 16 B aligned; R <= 16 for the fit), else the tiled kernels.
 static cudaError_t marginals_any(const DenseView& V, int64_t k0, int64_t nk, int moi, int S,
-                                 int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st) {
-  if (stream_supported(V)) return launch_marginals_stream(V, k0, nk, moi, S, x1, x2, x3, st);
+                                 int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st, int qb = 64) {
+  if (stream_supported(V)) return launch_marginals_stream(V, k0, nk, moi, S, x1, x2, x3, st, qb);
   return launch_marginals_dense(V, k0, nk, moi, S, x1, x2, x3, st);
 }
 static size_t fit_ws_doubles_any(const DenseView& V) {
@@ -1388,7 +1388,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   double* d_relerr_prev = d_relerr + 4;
   if (lag) CK(h->fitws.ensure(sizeof(double) * fit_ws_doubles_any(V)));
   auto old_pass = [&]() -> cudaError_t {   // a1 over [0, Ko), with the lag-1 fit when asked
-    if (!lag) return marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, sa1);
+    if (!lag) return marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h));
     cudaError_t e = launch_marg_fit_stream(Vold, Ko, h->opts.moi, h->S, qbits(h), h->lam(h->cur), h->A(h->cur),
                                            h->B(h->cur), h->C(h->cur), R, nullptr, x1, x2, x3,
                                            h->fitws.as<double>(), d_fit2, sa1);
@@ -1432,20 +1432,20 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     CK(cudaEventRecord(h->ev_pl[0], sa1));
   }
   if (overlap) {
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1));   // the batch's slices
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h)));   // the batch's slices
   } else if (inc) {
     // committed marginals of X_old plus the batch's contribution (integer sums: bit-identical
     // to the full pass)
     CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, sa1));
     CK(cudaMemsetAsync(x3 + Ko, 0, sizeof(int64_t) * (h->Kcap - Ko), sa1));
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1));
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h)));
   } else if (lag) {
     CK(cudaMemsetAsync(x1, 0, marg_bytes, sa1));
     CK(old_pass());
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1));   // the batch's slices
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h)));   // the batch's slices
   } else {
     CK(cudaMemsetAsync(x1, 0, marg_bytes, sa1));
-    CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, sa1));
+    CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h)));
   }
   if (pipe) {
     CK(cudaEventRecord(h->ev_pl[1], sa1));
@@ -1657,7 +1657,7 @@ static cudaError_t compute_committed_marginals(sambaten_s* h) {
   int64_t* x1 = h->xm.as<int64_t>();
   if (e == cudaSuccess) {
     if (h->fmt == SAMBATEN_DENSE)
-      e = marginals_any(h->view(), 0, h->K, h->opts.moi, h->S, x1, x1 + h->I, x1 + h->I + h->J, h->st);
+      e = marginals_any(h->view(), 0, h->K, h->opts.moi, h->S, x1, x1 + h->I, x1 + h->I + h->J, h->st, qbits(h));
     else
       e = coo_marginals(h, 0, h->nnz, x1, x1 + h->I, x1 + h->I + h->J, h->st);
   }
@@ -1727,7 +1727,9 @@ extern "C" sambaten_status sambaten_marginals(const sambaten_tensor* X, int moi,
   CK(cudaMemsetAsync(x3, 0, sizeof(int64_t) * X->dims[2], st));
   if (X->fmt == SAMBATEN_DENSE) {
     if (X->dims[0] > 4096) FAIL(SAMBATEN_E_INVALID, "marginals: dense I > 4096 not supported");
-    CK(marginals_any(user_view(X), 0, X->dims[2], moi, scale_exp, x1, x2, x3, st));
+    // SAMBATEN_MARG_QB (test hook): the caller asserts every q <= 2^qb (qb <= 27: 32-bit kernel)
+    const char* qe = getenv("SAMBATEN_MARG_QB");
+    CK(marginals_any(user_view(X), 0, X->dims[2], moi, scale_exp, x1, x2, x3, st, qe ? atoi(qe) : 64));
   } else {
     const int nrep = marg_coo_replicas(X->nnz, X->dims[0], X->dims[1]);
     int64_t* rws = nullptr;

@@ -55,6 +55,8 @@ struct StreamGeom {
   int ns;                   // stages in the ring (<= kMaxNS)
   int nch = 1, wpc = 1;     // marginals: column chunks per row and warps per chunk in a CTA
   int pc = 0;               // marginals: producer-consumer stage release (a producer warp)
+  int dbg = 0;              // marginals: timing experiment (SBT_MARG_DBG; 1 no quantisation, 2 no work)
+  int spill = 0;            // marginals Q32: warp steps between folds of the 32-bit column sums
   int qpt = 1, tpg = 1, ng = 1;   // fit: quads per thread, threads per row group, row groups
   bool bres = false;              // fit: B resident in shared memory (J x kMaxR floats)
 };
@@ -83,6 +85,20 @@ __device__ __forceinline__ long long quant(float x, float scf, double scd) {
   }
 }
 
+template <int MOI>
+__device__ __forceinline__ unsigned quant32(float x, float scf, double scd) {
+  if (MOI == 0) return (unsigned)__float2uint_rn(fabsf(x) * scf);   // exact product; q < 2^31 (Q32 plan)
+  const double d = (double)x;
+  return (unsigned)__double2ull_rn(__dmul_rn(__dmul_rn(d, d), scd));
+}
+
+// Exact warp sum of values < 2^31 (two 16-bit halves through REDUX; each half-sum < 2^21).
+__device__ __forceinline__ unsigned long long warp_sum_u31(unsigned v) {
+  const unsigned lo = __reduce_add_sync(0xffffffffu, v & 0xFFFFu);
+  const unsigned hi = __reduce_add_sync(0xffffffffu, v >> 16);
+  return ((unsigned long long)hi << 16) + lo;
+}
+
 // ---------------------------------------------------------------------------------------
 // a1: marginals.  A warp handles kRPW consecutive rows of a stage at a time: lane l takes the
 // quads l, l+32, ... (<= kMQ) of the column chunk (<= 512 floats) and keeps their x1 column
@@ -95,7 +111,11 @@ constexpr int kMQ = 4;            // quads per lane: column chunk <= 32 * 4 * 4 
 constexpr int kRPW = 2;           // rows per warp per step
 constexpr int kMargCTAs = 1;      // CTAs per SM
 
-template <int MOI>
+// Q32 (the plan bound qb <= 27: every q <= 2^27): q as uint32 (F2I.U32), a lane's 16 values of
+// a row summed in 32 bits (<= 2^31), row totals by two 18-bit REDUX chunk sums, column sums in
+// 32-bit registers folded into the int64 sums every g.spill warp steps (2 g.spill 2^qb < 2^32):
+// about half the integer instructions per element of the 64-bit path, same exact sums.
+template <int MOI, bool Q32>
 __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float* __restrict__ X, StreamGeom g,
                                                              int J, float scf, double scd,
                                                              unsigned long long* __restrict__ x1,
@@ -137,10 +157,12 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
       }
   }
   long long acc[kMQ][4];
+  unsigned acc32[kMQ][4];
 #pragma unroll
   for (int m = 0; m < kMQ; ++m)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) acc[m][e] = 0;
+    for (int e = 0; e < 4; ++e) { acc[m][e] = 0; acc32[m][e] = 0u; }
+  int steps = 0;
   long long x3run = 0;   // lane 0: running sum of slice x3k
   int64_t x3k = -1;
   for (int s = 0; s < nst && !producer; ++s) {
@@ -162,19 +184,64 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
     };
     for (int rw = wslot * kRPW; rw < nr; rw += g.wpc * kRPW) {
       long long rs[kRPW];
+      if (Q32) {
+#pragma unroll
+        for (int v = 0; v < kRPW; ++v) {
+          unsigned r32 = 0u;
+          const int r = rw + v;
+          if (r < nr) {
+            const float* rowp = st + (size_t)r * g.pitch;
+#pragma unroll
+            for (int m = 0; m < kMQ; ++m) {
+              const int col = 4 * (lane + 32 * m);
+              if (col < cw_real) {
+                const float4 x = *reinterpret_cast<const float4*>(rowp + col);
+                unsigned q0 = quant32<MOI>(x.x, scf, scd), q1 = quant32<MOI>(x.y, scf, scd);
+                unsigned q2 = quant32<MOI>(x.z, scf, scd), q3 = quant32<MOI>(x.w, scf, scd);
+                if (col + 4 > cw_real) {
+                  if (col + 1 >= cw_real) q1 = 0u;
+                  if (col + 2 >= cw_real) q2 = 0u;
+                  if (col + 3 >= cw_real) q3 = 0u;
+                }
+                acc32[m][0] += q0; acc32[m][1] += q1; acc32[m][2] += q2; acc32[m][3] += q3;
+                r32 += (q0 + q1) + (q2 + q3);
+              }
+            }
+          }
+          // exact warp total of values <= 2^31: 18-bit chunks (sums < 2^23 and 2^19)
+          const unsigned lo = __reduce_add_sync(0xffffffffu, r32 & 0x3FFFFu);
+          const unsigned hi = __reduce_add_sync(0xffffffffu, r32 >> 18);
+          rs[v] = (long long)(((unsigned long long)hi << 18) + lo);
+        }
+        if (++steps == g.spill) {
+          steps = 0;
+#pragma unroll
+          for (int m = 0; m < kMQ; ++m)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) { acc[m][e] += acc32[m][e]; acc32[m][e] = 0u; }
+        }
+      }
 #pragma unroll
       for (int v = 0; v < kRPW; ++v) {
+        if (Q32) break;
         rs[v] = 0;
         const int r = rw + v;
         if (r < nr) {
           const float* rowp = st + (size_t)r * g.pitch;
+          if (g.dbg == 2) continue;
 #pragma unroll
           for (int m = 0; m < kMQ; ++m) {
             const int col = 4 * (lane + 32 * m);
             if (col < cw_real) {
               const float4 x = *reinterpret_cast<const float4*>(rowp + col);
-              long long q0 = quant<MOI>(x.x, scf, scd), q1 = quant<MOI>(x.y, scf, scd);
-              long long q2 = quant<MOI>(x.z, scf, scd), q3 = quant<MOI>(x.w, scf, scd);
+              long long q0, q1, q2, q3;
+              if (g.dbg == 1) {
+                q0 = __float_as_int(x.x) & 0xffff; q1 = __float_as_int(x.y) & 0xffff;
+                q2 = __float_as_int(x.z) & 0xffff; q3 = __float_as_int(x.w) & 0xffff;
+              } else {
+                q0 = quant<MOI>(x.x, scf, scd); q1 = quant<MOI>(x.y, scf, scd);
+                q2 = quant<MOI>(x.z, scf, scd); q3 = quant<MOI>(x.w, scf, scd);
+              }
               if (col + 1 >= cw_real) q1 = 0;
               if (col + 2 >= cw_real) q2 = 0;
               if (col + 3 >= cw_real) q3 = 0;
@@ -184,10 +251,11 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
           }
         }
       }
+      if (!Q32)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
+        for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int v = 0; v < kRPW; ++v) rs[v] += __shfl_xor_sync(0xffffffffu, rs[v], o);
+          for (int v = 0; v < kRPW; ++v) rs[v] += __shfl_xor_sync(0xffffffffu, rs[v], o);
       // every lane holds the kRPW row totals: lane v adds row v to x2; lane 0 folds them into
       // the warp's running x3 sum of slice x3k (flushed when the slice changes: one global
       // reduction per slice and warp instead of a contended shared 64-bit atomic per row)
@@ -232,6 +300,11 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
     }
   }
   if (lane == 0 && x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
+  if (Q32)
+#pragma unroll
+    for (int m = 0; m < kMQ; ++m)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[m][e] += acc32[m][e];
   // x1: the warps' column sums through the (now idle) ring, summed per column in warp order
   // (every stage has been consumed, so no copy is in flight)
   __syncthreads();
@@ -589,6 +662,11 @@ StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* g
   g.ncol = (int)X.I;
   const int maxcw = 4 * 32 * kMQ;
   g.nch = (g.pitch + maxcw - 1) / maxcw;
+  // chunks per row rounded up to a divisor of the CTA's warps, so every warp has a chunk (C4: 6 -> 8
+  // chunks of 376 floats, 16 warps; measured ~2 % faster than 12 warps on 500-float chunks)
+  while (g.nch < kNW && kNW % g.nch) ++g.nch;
+  static const int nch_env = getenv("SBT_MARG_NCH") ? atoi(getenv("SBT_MARG_NCH")) : 0;
+  if (nch_env > g.nch && nch_env <= kNW) g.nch = nch_env;   // narrower chunks (tuning experiment)
   g.cw = ((g.pitch + g.nch - 1) / g.nch + 3) & ~3;
   g.wpc = kNW / g.nch;
   if (g.wpc < 1) g.wpc = 1;
@@ -610,6 +688,8 @@ StreamGeom marg_geom(const DenseView& X, int64_t k0, int64_t nk, int* gx, int* g
   *gx = (int)ceil_div(g.nrows, g.rows_per_cta);
   *gy = 1;
   static const int pc = getenv("SBT_MARG_PC") ? atoi(getenv("SBT_MARG_PC")) : 0;
+  static const int dbg = getenv("SBT_MARG_DBG") ? atoi(getenv("SBT_MARG_DBG")) : 0;
+  g.dbg = dbg;
   g.pc = pc && g.nch * g.wpc < kNW;   // room for the producer warp
   *threads = 32 * (g.nch * g.wpc + (g.pc ? 1 : 0));
   return g;
@@ -680,20 +760,6 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
     t += (unsigned long long)__reduce_add_sync(0xffffffffu, part) << (21 * c);
   }
   return t;
-}
-
-template <int MOI>
-__device__ __forceinline__ unsigned quant32(float x, float scf, double scd) {
-  if (MOI == 0) return (unsigned)__float2uint_rn(fabsf(x) * scf);   // exact product; q < 2^31 (Q32 plan)
-  const double d = (double)x;
-  return (unsigned)__double2ull_rn(__dmul_rn(__dmul_rn(d, d), scd));
-}
-
-// Exact warp sum of values < 2^31 (two 16-bit halves through REDUX; each half-sum < 2^21).
-__device__ __forceinline__ unsigned long long warp_sum_u31(unsigned v) {
-  const unsigned lo = __reduce_add_sync(0xffffffffu, v & 0xFFFFu);
-  const unsigned hi = __reduce_add_sync(0xffffffffu, v >> 16);
-  return ((unsigned long long)hi << 16) + lo;
 }
 
 template <int MOI, int RB, int QPT, bool BRES, bool Q32>
@@ -1123,23 +1189,24 @@ bool stream_supported(const DenseView& X) {
 }
 
 cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
-                                    int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st) {
+                                    int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st, int qb) {
   if (nk <= 0) return cudaSuccess;
   int gx, gy, nthr;
   StreamGeom g = marg_geom(X, k0, nk, &gx, &gy, &nthr);
+  const bool q32 = qb <= 27 && !getenv("SAMBATEN_MARG_NO_Q32");
+  g.spill = q32 ? (int)(0xFFFFFFFFull / ((unsigned long long)kRPW << qb)) : 0;   // >= 15
   const float scf = ldexpf(1.0f, S < -126 ? -126 : (S > 127 ? 127 : S));
   const double scd = ldexp(1.0, S);
   const size_t smem = sizeof(float) * (size_t)g.ns * g.tr * g.pitch;
   auto* u1 = reinterpret_cast<unsigned long long*>(x1);
   auto* u2 = reinterpret_cast<unsigned long long*>(x2);
   auto* u3 = reinterpret_cast<unsigned long long*>(x3);
-  if (moi == 0) {
-    cudaFuncSetAttribute(marg_stream_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    marg_stream_kernel<0><<<dim3(gx, gy), nthr, smem, st>>>(X.base, g, (int)X.J, scf, scd, u1, u2, u3);
-  } else {
-    cudaFuncSetAttribute(marg_stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    marg_stream_kernel<1><<<dim3(gx, gy), nthr, smem, st>>>(X.base, g, (int)X.J, scf, scd, u1, u2, u3);
-  }
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<dim3(gx, gy), nthr, smem, st>>>(X.base, g, (int)X.J, scf, scd, u1, u2, u3);
+  };
+  if (moi == 0) q32 ? go(marg_stream_kernel<0, true>) : go(marg_stream_kernel<0, false>);
+  else q32 ? go(marg_stream_kernel<1, true>) : go(marg_stream_kernel<1, false>);
   return cudaGetLastError();
 }
 

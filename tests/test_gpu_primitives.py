@@ -61,6 +61,28 @@ def test_marginals_dense_bit_exact(shape, moi):
         assert np.array_equal(host(g), r)
 
 
+@pytest.mark.parametrize("shape", [(40, 30, 600), (9, 20, 3000), (5, 7, 1024), (3, 11, 2500)])
+@pytest.mark.parametrize("moi", [0, 1])
+def test_marginals_dense_q32_bit_exact(shape, moi, monkeypatch):
+    """The 32-bit stream kernel (every q <= 2^27, as at C4 where ceil log2 of the capacity is 35):
+    S chosen so that q = RNE(phi 2^S) <= 2^27 exactly at the maximum (phi <= 1 here), the bound
+    passed through the SAMBATEN_MARG_QB hook; bit-exact against the oracle (column sums folded
+    every 15 warp steps, row totals by 18-bit chunk sums)."""
+    torch = torch_cuda()
+    K, J, I = shape
+    rng = np.random.default_rng(sum(shape) + moi)
+    T = rng.random((K, J, I)).astype(np.float32)
+    T[0, 0, 0] = 1.0                        # q = 2^27 exactly
+    T[rng.random(T.shape) < 0.1] = 0.0
+    T[..., -1] = np.nextafter(np.float32(1.0), np.float32(0.0))   # a column of near-maximal values
+    S = 27
+    monkeypatch.setenv("SAMBATEN_MARG_QB", "27")
+    x = [torch.empty(n, dtype=torch.int64, device="cuda") for n in (I, J, K)]
+    L().sambaten_marginals(L().dense(dev(T)), moi, S, *x)
+    for g, r in zip(x, O.marginals_dense(T, S, moi)):
+        assert np.array_equal(host(g), r)
+
+
 @pytest.mark.parametrize("moi", [0, 1])
 def test_marginals_coo_bit_exact(moi):
     torch = torch_cuda()
