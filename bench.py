@@ -224,6 +224,11 @@ FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FP32 lanes x F
 L2_RESIDENT_BYTES = 100e6                           # summaries below this stay in the 126 MB L2
 
 
+# read-only HBM ceiling: tools/micro/read_bw.cu (40 GB, cp.async.bulk ring of 2-6 stages per SM, no
+# compute; LDG.128 streaming 7.41 TB/s) on this pool's B200 -> profiles/r02_read_ceiling.txt
+READ_CEILING_GBS = 7433.0
+
+
 def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
     """Per-step roofline of the dominant kernel of each streaming / ALS step, from the steps'
     CUDA-event times (info.step_ms, on the library's stream) and the algorithmic work of
@@ -245,8 +250,11 @@ def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
     def hbm_line(name, step, byts):
         t = ms(step)
         ach = byts / (t / 1e3) / 1e9
+        # MEASURED_PEAKS' hbm_gbs is a copy (read + write) figure; a read-only stream can exceed it:
+        # the read ceiling measured on this pool's B200 (TMA ring, no compute) is reported beside it
         return {"kernel": name, "bound": "hbm", "achieved": ach, "peak": hbm, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": ach / hbm, "traffic": traffic.get(f"a{step}"),
+                "read_ceiling": READ_CEILING_GBS, "frac_of_read_ceiling": ach / READ_CEILING_GBS,
                 "bytes_per_launch": byts, "ms_per_launch": t}
     Ks = [inf["k_total"] for inf in infos]
     if work.coo:

@@ -43,8 +43,9 @@ using namespace sbt;
 // a1 / a7 dispatch: the TMA-ring streaming kernels when the view allows them (pitch % 4 == 0,
 // 16 B aligned; R <= 16 for the fit), else the tiled kernels.
 static cudaError_t marginals_any(const DenseView& V, int64_t k0, int64_t nk, int moi, int S,
-                                 int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st, int qb = 64) {
-  if (stream_supported(V)) return launch_marginals_stream(V, k0, nk, moi, S, x1, x2, x3, st, qb);
+                                 int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st, int qb = 64,
+                                 double phimax = 1e300, const unsigned long long* d_phimax = nullptr) {
+  if (stream_supported(V)) return launch_marginals_stream(V, k0, nk, moi, S, x1, x2, x3, st, qb, phimax, d_phimax);
   return launch_marginals_dense(V, k0, nk, moi, S, x1, x2, x3, st);
 }
 static size_t fit_ws_doubles_any(const DenseView& V) {
@@ -135,6 +136,7 @@ struct sambaten_s {
   sambaten_opts opts;
   cudaStream_t st = nullptr;
   int S = 0, maxphi_log2 = 0;
+  double phimax_run = 1e300;   // upper bound on phi over the store (X0 and committed batches; restore keeps it)
   // store and model
   DevBuf X;
   DevBuf model[2];          // A | B | C | lam | fit state, double-buffered (merge writes the shadow)
@@ -545,6 +547,7 @@ static sambaten_status alloc_store_and_model(sambaten_s* h, const sambaten_tenso
   const int64_t cap_entries = h->fmt == SAMBATEN_DENSE ? h->I * h->J * h->Kcap : h->nnz_cap;
   h->S = sambaten_fixed_point_scale(cap_entries, maxphi);
   h->maxphi_log2 = ceil_log2_d(maxphi);
+  h->phimax_run = maxphi;
   return SAMBATEN_OK;
 }
 
@@ -893,6 +896,7 @@ static sambaten_status finish_update(sambaten_s* h, const DenseAls& a, const int
   memcpy(&maxphi, &hs->maxphi_bits, 8);
   if (maxphi > ldexp(1.0, h->maxphi_log2 + 8))
     FAIL(SAMBATEN_E_FIXEDPOINT_RANGE, "update: batch value outside the fixed-point range (R7)");
+  if (maxphi > h->phimax_run) h->phimax_run = maxphi;   // (a later failure only leaves it an upper bound)
   uint32_t rejected = 0, pm = 0;
   int nacc = 0, itmax = 0, itsum = 0;
   double fsum = 0.0;
@@ -1388,7 +1392,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   double* d_relerr_prev = d_relerr + 4;
   if (lag) CK(h->fitws.ensure(sizeof(double) * fit_ws_doubles_any(V)));
   auto old_pass = [&]() -> cudaError_t {   // a1 over [0, Ko), with the lag-1 fit when asked
-    if (!lag) return marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h));
+    if (!lag) return marginals_any(V, 0, Ko, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h), h->phimax_run);
     cudaError_t e = launch_marg_fit_stream(Vold, Ko, h->opts.moi, h->S, qbits(h), h->lam(h->cur), h->A(h->cur),
                                            h->B(h->cur), h->C(h->cur), R, nullptr, x1, x2, x3,
                                            h->fitws.as<double>(), d_fit2, sa1);
@@ -1432,20 +1436,20 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
     CK(cudaEventRecord(h->ev_pl[0], sa1));
   }
   if (overlap) {
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h)));   // the batch's slices
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h), 0.0, d_maxphi));   // the batch's slices
   } else if (inc) {
     // committed marginals of X_old plus the batch's contribution (integer sums: bit-identical
     // to the full pass)
     CK(cudaMemcpyAsync(x1, h->xm.p, sizeof(int64_t) * (h->I + h->J + Ko), cudaMemcpyDeviceToDevice, sa1));
     CK(cudaMemsetAsync(x3 + Ko, 0, sizeof(int64_t) * (h->Kcap - Ko), sa1));
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h)));
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h), 0.0, d_maxphi));
   } else if (lag) {
     CK(cudaMemsetAsync(x1, 0, marg_bytes, sa1));
     CK(old_pass());
-    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h)));   // the batch's slices
+    CK(marginals_any(V, Ko, Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h), 0.0, d_maxphi));   // the batch's slices
   } else {
     CK(cudaMemsetAsync(x1, 0, marg_bytes, sa1));
-    CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h)));
+    CK(marginals_any(V, 0, Ko + Kn, h->opts.moi, h->S, x1, x2, x3, sa1, qbits(h), h->phimax_run, d_maxphi));
   }
   if (pipe) {
     CK(cudaEventRecord(h->ev_pl[1], sa1));
@@ -1657,7 +1661,8 @@ static cudaError_t compute_committed_marginals(sambaten_s* h) {
   int64_t* x1 = h->xm.as<int64_t>();
   if (e == cudaSuccess) {
     if (h->fmt == SAMBATEN_DENSE)
-      e = marginals_any(h->view(), 0, h->K, h->opts.moi, h->S, x1, x1 + h->I, x1 + h->I + h->J, h->st, qbits(h));
+      e = marginals_any(h->view(), 0, h->K, h->opts.moi, h->S, x1, x1 + h->I, x1 + h->I + h->J, h->st, qbits(h),
+                        h->phimax_run);
     else
       e = coo_marginals(h, 0, h->nnz, x1, x1 + h->I, x1 + h->I + h->J, h->st);
   }
@@ -1728,8 +1733,11 @@ extern "C" sambaten_status sambaten_marginals(const sambaten_tensor* X, int moi,
   if (X->fmt == SAMBATEN_DENSE) {
     if (X->dims[0] > 4096) FAIL(SAMBATEN_E_INVALID, "marginals: dense I > 4096 not supported");
     // SAMBATEN_MARG_QB (test hook): the caller asserts every q <= 2^qb (qb <= 27: 32-bit kernel)
+    // SAMBATEN_MARG_PHIMAX (test hook): ... and every phi <= this bound (q < 2^22: FMA rounding)
     const char* qe = getenv("SAMBATEN_MARG_QB");
-    CK(marginals_any(user_view(X), 0, X->dims[2], moi, scale_exp, x1, x2, x3, st, qe ? atoi(qe) : 64));
+    const char* pe = getenv("SAMBATEN_MARG_PHIMAX");
+    CK(marginals_any(user_view(X), 0, X->dims[2], moi, scale_exp, x1, x2, x3, st, qe ? atoi(qe) : 64,
+                     pe ? atof(pe) : 1e300));
   } else {
     const int nrep = marg_coo_replicas(X->nnz, X->dims[0], X->dims[1]);
     int64_t* rws = nullptr;

@@ -329,8 +329,11 @@ cudaError_t launch_fit_finish(const double* in2, const float* lam, const float* 
 bool stream_supported(const DenseView& X);
 bool fit_stream_supported(const DenseView& X, int R);
 // qb: every q = RNE(phi 2^S) of the pass is <= 2^qb (64: unknown); qb <= 27 -> 32-bit arithmetic
+// phimax / d_phimax (device fp64 bits, may be NULL): upper bounds on phi of the pass's data (the
+// larger counts); a bound q < 2^22 selects the FMA rounding of the 32-bit kernel (MOI 0)
 cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
-                                    int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st, int qb = 64);
+                                    int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st, int qb = 64,
+                                    double phimax = 1e300, const unsigned long long* d_phimax = nullptr);
 size_t fit_stream_ws_doubles(const DenseView& X);
 // a1 over slices [0, nk) fused with the fit partials of the model (lam; A, B, C) over the same
 // slices (SURVEY 8(f) NEXT #1 lag-1 fit): x1/x2/x3 accumulate (zero them first); out2 =

@@ -57,6 +57,8 @@ struct StreamGeom {
   int pc = 0;               // marginals: producer-consumer stage release (a producer warp)
   int dbg = 0;              // marginals: timing experiment (SBT_MARG_DBG; 1 no quantisation, 2 no work)
   int spill = 0;            // marginals Q32: warp steps between folds of the 32-bit column sums
+  double qmax = 1e300;      // marginals: bound on q of the data in the pass (host part) ...
+  const unsigned long long* dphi = nullptr;   // ... and a device max phi (fp64 bits) folded in
   int qpt = 1, tpg = 1, ng = 1;   // fit: quads per thread, threads per row group, row groups
   bool bres = false;              // fit: B resident in shared memory (J x kMaxR floats)
 };
@@ -115,7 +117,7 @@ constexpr int kMargCTAs = 1;      // CTAs per SM
 // a row summed in 32 bits (<= 2^31), row totals by two 18-bit REDUX chunk sums, column sums in
 // 32-bit registers folded into the int64 sums every g.spill warp steps (2 g.spill 2^qb < 2^32):
 // about half the integer instructions per element of the 64-bit path, same exact sums.
-template <int MOI, bool Q32>
+template <int MOI, bool Q32, bool QT = true>
 __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float* __restrict__ X, StreamGeom g,
                                                              int J, float scf, double scd,
                                                              unsigned long long* __restrict__ x1,
@@ -163,6 +165,22 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
 #pragma unroll
     for (int e = 0; e < 4; ++e) { acc[m][e] = 0; acc32[m][e] = 0u; }
   int steps = 0;
+  // MOI 0 with every q of the pass < 2^22 (the store's running max phi and the batch's, read on
+  // the device): q = bits(fma(|x|, 2^S, 2^23)) - bits(2^23) exactly (one rounding of the exact
+  // value, ties to even), so the biased bits are summed and the bias removed per fold -- one
+  // FFMA per element instead of FMUL + F2I (the conversion pipe), mod-2^32 arithmetic exact
+  // because every true 32-bit sum is < 2^32
+  bool magic = false;
+  if (Q32 && MOI == 0) {
+    double qm = g.qmax;
+    if (g.dphi) qm = fmax(qm, __longlong_as_double((long long)*g.dphi) * scd);
+    magic = qm < 4194304.0;
+  }
+  constexpr unsigned kBias = 0x4B000000u;   // bits(2^23)
+  int nvq = 0;                               // this lane's column quads in its chunk
+#pragma unroll
+  for (int m = 0; m < kMQ; ++m) nvq += 4 * (lane + 32 * m) < cw_real ? 1 : 0;
+  const unsigned rbias = magic ? (unsigned)(4 * nvq) * kBias : 0u;   // per row total (mod 2^32)
   long long x3run = 0;   // lane 0: running sum of slice x3k
   int64_t x3k = -1;
   for (int s = 0; s < nst && !producer; ++s) {
@@ -185,40 +203,67 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
     for (int rw = wslot * kRPW; rw < nr; rw += g.wpc * kRPW) {
       long long rs[kRPW];
       if (Q32) {
+        // the two rows of the step together: one IADD3 per column for both rows' values
+        static_assert(kRPW == 2, "Q32 path pairs two rows");
+        unsigned r32a = 0u, r32b = 0u;
+        const bool two = rw + 1 < nr;
+        const float* rowa = st + (size_t)rw * g.pitch;
+        const float* rowb = rowa + g.pitch;
 #pragma unroll
-        for (int v = 0; v < kRPW; ++v) {
-          unsigned r32 = 0u;
-          const int r = rw + v;
-          if (r < nr) {
-            const float* rowp = st + (size_t)r * g.pitch;
-#pragma unroll
-            for (int m = 0; m < kMQ; ++m) {
-              const int col = 4 * (lane + 32 * m);
-              if (col < cw_real) {
-                const float4 x = *reinterpret_cast<const float4*>(rowp + col);
-                unsigned q0 = quant32<MOI>(x.x, scf, scd), q1 = quant32<MOI>(x.y, scf, scd);
-                unsigned q2 = quant32<MOI>(x.z, scf, scd), q3 = quant32<MOI>(x.w, scf, scd);
-                if (col + 4 > cw_real) {
-                  if (col + 1 >= cw_real) q1 = 0u;
-                  if (col + 2 >= cw_real) q2 = 0u;
-                  if (col + 3 >= cw_real) q3 = 0u;
-                }
-                acc32[m][0] += q0; acc32[m][1] += q1; acc32[m][2] += q2; acc32[m][3] += q3;
-                r32 += (q0 + q1) + (q2 + q3);
-              }
+        for (int m = 0; m < kMQ; ++m) {
+          const int col = 4 * (lane + 32 * m);
+          if (col < cw_real) {
+            const float4 xa = *reinterpret_cast<const float4*>(rowa + col);
+            const float4 xb = two ? *reinterpret_cast<const float4*>(rowb + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+            unsigned a0, a1, a2, a3, b0, b1, b2, b3;
+            if (magic) {   // biased: kBias + q
+              a0 = __float_as_uint(fmaf(fabsf(xa.x), scf, 8388608.0f));
+              a1 = __float_as_uint(fmaf(fabsf(xa.y), scf, 8388608.0f));
+              a2 = __float_as_uint(fmaf(fabsf(xa.z), scf, 8388608.0f));
+              a3 = __float_as_uint(fmaf(fabsf(xa.w), scf, 8388608.0f));
+              b0 = __float_as_uint(fmaf(fabsf(xb.x), scf, 8388608.0f));
+              b1 = __float_as_uint(fmaf(fabsf(xb.y), scf, 8388608.0f));
+              b2 = __float_as_uint(fmaf(fabsf(xb.z), scf, 8388608.0f));
+              b3 = __float_as_uint(fmaf(fabsf(xb.w), scf, 8388608.0f));
+            } else {
+              a0 = quant32<MOI>(xa.x, scf, scd); a1 = quant32<MOI>(xa.y, scf, scd);
+              a2 = quant32<MOI>(xa.z, scf, scd); a3 = quant32<MOI>(xa.w, scf, scd);
+              b0 = quant32<MOI>(xb.x, scf, scd); b1 = quant32<MOI>(xb.y, scf, scd);
+              b2 = quant32<MOI>(xb.z, scf, scd); b3 = quant32<MOI>(xb.w, scf, scd);
             }
+            if (QT && col + 4 > cw_real) {   // QT: I % 4 != 0, a chunk may end inside a quad
+              const unsigned z = magic ? kBias : 0u;   // the value of q = 0
+              if (col + 1 >= cw_real) { a1 = z; b1 = z; }
+              if (col + 2 >= cw_real) { a2 = z; b2 = z; }
+              if (col + 3 >= cw_real) { a3 = z; b3 = z; }
+            }
+            acc32[m][0] += a0 + b0; acc32[m][1] += a1 + b1; acc32[m][2] += a2 + b2; acc32[m][3] += a3 + b3;
+            r32a += (a0 + a1) + (a2 + a3);
+            r32b += (b0 + b1) + (b2 + b3);
           }
-          // exact warp total of values <= 2^31: 18-bit chunks (sums < 2^23 and 2^19)
-          const unsigned lo = __reduce_add_sync(0xffffffffu, r32 & 0x3FFFFu);
-          const unsigned hi = __reduce_add_sync(0xffffffffu, r32 >> 18);
-          rs[v] = (long long)(((unsigned long long)hi << 18) + lo);
+        }
+        // exact warp totals of values <= 2^31: 18-bit chunks (sums < 2^23 and 2^19)
+        r32a -= rbias;   // a missing second row contributed q = 0 values (xb = 0: biased kBias)
+        r32b -= rbias;
+        {
+          const unsigned lo = __reduce_add_sync(0xffffffffu, r32a & 0x3FFFFu);
+          const unsigned hi = __reduce_add_sync(0xffffffffu, r32a >> 18);
+          rs[0] = (long long)(((unsigned long long)hi << 18) + lo);
+        }
+        {
+          const unsigned lo = __reduce_add_sync(0xffffffffu, r32b & 0x3FFFFu);
+          const unsigned hi = __reduce_add_sync(0xffffffffu, r32b >> 18);
+          rs[1] = (long long)(((unsigned long long)hi << 18) + lo);
         }
         if (++steps == g.spill) {
+          const unsigned cb = magic ? (unsigned)(2 * steps) * kBias : 0u;   // two biased values per step
           steps = 0;
 #pragma unroll
-          for (int m = 0; m < kMQ; ++m)
+          for (int m = 0; m < kMQ; ++m) {
+            const bool vq = 4 * (lane + 32 * m) < cw_real;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) { acc[m][e] += acc32[m][e]; acc32[m][e] = 0u; }
+            for (int e = 0; e < 4; ++e) { acc[m][e] += vq ? acc32[m][e] - cb : 0u; acc32[m][e] = 0u; }
+          }
         }
       }
 #pragma unroll
@@ -300,11 +345,15 @@ __global__ void __launch_bounds__(kST, kMargCTAs) marg_stream_kernel(const float
     }
   }
   if (lane == 0 && x3run) atomicAdd(&x3[x3k], (unsigned long long)x3run);
-  if (Q32)
+  if (Q32) {
+    const unsigned cb = magic ? (unsigned)(2 * steps) * kBias : 0u;
 #pragma unroll
-    for (int m = 0; m < kMQ; ++m)
+    for (int m = 0; m < kMQ; ++m) {
+      const bool vq = 4 * (lane + 32 * m) < cw_real;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[m][e] += acc32[m][e];
+      for (int e = 0; e < 4; ++e) acc[m][e] += vq ? acc32[m][e] - cb : 0u;
+    }
+  }
   // x1: the warps' column sums through the (now idle) ring, summed per column in warp order
   // (every stage has been consumed, so no copy is in flight)
   __syncthreads();
@@ -1189,12 +1238,19 @@ bool stream_supported(const DenseView& X) {
 }
 
 cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, int moi, int S,
-                                    int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st, int qb) {
+                                    int64_t* x1, int64_t* x2, int64_t* x3, cudaStream_t st, int qb,
+                                    double phimax, const unsigned long long* d_phimax) {
   if (nk <= 0) return cudaSuccess;
   int gx, gy, nthr;
   StreamGeom g = marg_geom(X, k0, nk, &gx, &gy, &nthr);
+  // SBT_MARG_FORCE_QB (profiling hook for the small C4 stand-ins, whose capacity bound is 29 bits
+  // but whose data stay far below 2^27): the kernel instantiation C4 runs
+  if (const char* f = getenv("SBT_MARG_FORCE_QB")) qb = atoi(f);
   const bool q32 = qb <= 27 && !getenv("SAMBATEN_MARG_NO_Q32");
   g.spill = q32 ? (int)(0xFFFFFFFFull / ((unsigned long long)kRPW << qb)) : 0;   // >= 15
+  g.qmax = phimax * ldexp(1.0, S);   // phimax: upper bound on phi of the pass (inf: unknown)
+  g.dphi = d_phimax;
+  if (getenv("SAMBATEN_MARG_NO_MAGIC")) g.qmax = 1e300, g.dphi = nullptr;
   const float scf = ldexpf(1.0f, S < -126 ? -126 : (S > 127 ? 127 : S));
   const double scd = ldexp(1.0, S);
   const size_t smem = sizeof(float) * (size_t)g.ns * g.tr * g.pitch;
@@ -1205,8 +1261,11 @@ cudaError_t launch_marginals_stream(const DenseView& X, int64_t k0, int64_t nk, 
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<dim3(gx, gy), nthr, smem, st>>>(X.base, g, (int)X.J, scf, scd, u1, u2, u3);
   };
-  if (moi == 0) q32 ? go(marg_stream_kernel<0, true>) : go(marg_stream_kernel<0, false>);
-  else q32 ? go(marg_stream_kernel<1, true>) : go(marg_stream_kernel<1, false>);
+  const bool qt = X.I % 4 != 0;   // chunks are multiples of 4 floats: only the last can end mid-quad
+  if (moi == 0) q32 ? (qt ? go(marg_stream_kernel<0, true, true>) : go(marg_stream_kernel<0, true, false>))
+                    : go(marg_stream_kernel<0, false>);
+  else q32 ? (qt ? go(marg_stream_kernel<1, true, true>) : go(marg_stream_kernel<1, true, false>))
+           : go(marg_stream_kernel<1, false>);
   return cudaGetLastError();
 }
 

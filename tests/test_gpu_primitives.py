@@ -61,13 +61,15 @@ def test_marginals_dense_bit_exact(shape, moi):
         assert np.array_equal(host(g), r)
 
 
-@pytest.mark.parametrize("shape", [(40, 30, 600), (9, 20, 3000), (5, 7, 1024), (3, 11, 2500)])
-@pytest.mark.parametrize("moi", [0, 1])
-def test_marginals_dense_q32_bit_exact(shape, moi, monkeypatch):
+@pytest.mark.parametrize("shape", [(40, 30, 600), (9, 20, 3000), (5, 7, 1024), (3, 11, 2500), (37, 3, 600)])
+@pytest.mark.parametrize("moi,magic", [(0, False), (1, False), (0, True)])
+def test_marginals_dense_q32_bit_exact(shape, moi, magic, monkeypatch):
     """The 32-bit stream kernel (every q <= 2^27, as at C4 where ceil log2 of the capacity is 35):
     S chosen so that q = RNE(phi 2^S) <= 2^27 exactly at the maximum (phi <= 1 here), the bound
     passed through the SAMBATEN_MARG_QB hook; bit-exact against the oracle (column sums folded
-    every 15 warp steps, row totals by 18-bit chunk sums)."""
+    every 15 warp steps, row totals by 18-bit chunk sums).  magic: the data bound q <= 2^21 also
+    passed (SAMBATEN_MARG_PHIMAX), the FMA rounding with biased sums C4's data take.  (37, 3, 600):
+    an odd row count per stage step."""
     torch = torch_cuda()
     K, J, I = shape
     rng = np.random.default_rng(sum(shape) + moi)
@@ -77,6 +79,9 @@ def test_marginals_dense_q32_bit_exact(shape, moi, monkeypatch):
     T[..., -1] = np.nextafter(np.float32(1.0), np.float32(0.0))   # a column of near-maximal values
     S = 27
     monkeypatch.setenv("SAMBATEN_MARG_QB", "27")
+    if magic:   # q <= 2^21 < 2^22: q = bits(fma(|x|, 2^S, 2^23)) - bits(2^23), biased 32-bit sums
+        S = 21
+        monkeypatch.setenv("SAMBATEN_MARG_PHIMAX", "1.0")
     x = [torch.empty(n, dtype=torch.int64, device="cuda") for n in (I, J, K)]
     L().sambaten_marginals(L().dense(dev(T)), moi, S, *x)
     for g, r in zip(x, O.marginals_dense(T, S, moi)):
