@@ -340,8 +340,13 @@ template <int RB, bool PASSB>
 __device__ __forceinline__ void team_pass(const float* __restrict__ region, int nu, int nrow, int ncol,
                                        int pitch, const float* Uw, const float* U2s, float* rings,
                                        int stage_fl, unsigned long long* bars, int T, int NT,
-                                       unsigned tseq, float* Dg, double* P) {
+                                       unsigned tseq, float* Dg, double* P, double* ss = nullptr,
+                                       double* s_red = nullptr) {
   const int tid = threadIdx.x;
+  // ss (pass B of the first iteration): ||Src||^2 of the CTA's slices on the way -- the four
+  // squares of a quad in fp32, widened once per quad; block sum into *ss (fixed order)
+  const bool want_ss = PASSB && ss != nullptr;
+  double ssd = 0.0;
 #ifdef SBT_ALS_PHASES
   const long long tp0 = clock64();
 #endif
@@ -392,6 +397,7 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
 #pragma unroll 2
       for (int row = 0; row < nr; ++row) {
         const float4 y = *reinterpret_cast<const float4*>(st + row * pitch);
+        if (want_ss) ssd += (double)fmaf(y.x, y.x, fmaf(y.y, y.y, fmaf(y.z, y.z, y.w * y.w)));
         float w[RB];
         ld_wrow<RB>(wr + row * ((RB + 3) & ~3), w);
         if (!PASSB) {
@@ -427,6 +433,10 @@ __device__ __forceinline__ void team_pass(const float* __restrict__ region, int 
 #ifdef SBT_ALS_PHASES
   if (tid == 0 && blockIdx.x == 0) atomicAdd(&g_als_phase[PASSB ? 19 : 18], (unsigned long long)(clock64() - tp0));
 #endif
+  if (want_ss) {
+    const double t = block_sum_d(ssd, s_red);
+    if (tid == 0) *ss = t;
+  }
   if (!PASSB) {
     __syncthreads();   // every team done: rings free (no copy in flight) -> reduction buffer
     float* red = rings;
@@ -855,19 +865,8 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
     if (m == 2) for (int u = 0; u < nK; ++u) s += (double)gU2[(int64_t)u * R + f] * (double)gU2[(int64_t)u * R + g];
     G[m * RB * RB + fg] = s;
   }
-  {
-    double s = 0.0;
-    const int tot = nu * nJ * nI;
-    for (int e = tid; e < tot; e += kCT) {
-      const int row = e / nI, p = e - row * nI;
-      const double v = regA[(int64_t)row * pI + p];
-      s += v * v;
-    }
-    s = block_sum_d(s, s_red);
-    if (tid == 0) { sc[0] = s; if (GRID) gx_me[gc.offS + 0] = s; }
-  }
   csync();
-  const double ysq = csum(sc, gc.offS, 0);
+  double ysq = 0.0;   // ||Y||^2: formed in the first iteration's pass B (mode 1)
   PH(0);
 
   double fit = 0.0, fit_prev = 0.0;
@@ -904,7 +903,8 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         PH(1);
       } else {
         team_pass<RB, true>(regB, nu, nI, nJ, pJ, U0s, U2s, ring, Ly.stage_fl, bars, Ly.T, Ly.NT,
-                            tseq, D, P);
+                            tseq, D, P, it == 0 ? sc : nullptr, s_red);
+        if (it == 0 && tid == 0 && GRID) gx_me[gc.offS + 0] = sc[0];
         if (myteam < Ly.NT) tseq += team_stages(myteam, nu, Ly.NT, nI, pJ, Ly.stage_fl);
         __syncthreads();   // D of the own slices complete (global, visible to the CTA)
         // P(q,f) = sum_{own u} U2(u,f) D(u,q,f)   (fixed order; an fp32 run of <= ceil(K'/CS)
@@ -922,6 +922,7 @@ __global__ void __launch_bounds__(kCT, 1) als_cluster_kernel(DenseAls a, int CS,
         for (int e = tid; e < np; e += kCT) gx_me[gc.offP + e] = P[e];
       }
       csync();   // S1: partials of every CTA complete
+      if (m == 1 && it == 0) ysq = csum(sc, gc.offS, 0);
       PH(m == 0 ? 2 : 8);
       // ---- rows [c0, c1) of this mode: sum the CS partials, solve, partial Gram ----
       const int c0 = min(n, rank * ch), c1 = min(n, c0 + ch);
