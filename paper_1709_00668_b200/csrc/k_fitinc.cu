@@ -18,6 +18,8 @@
 // (P, ||X||^2, valid) lives in the model buffer (checkpointed and restored with it).
 // Every sum here is exact algebra of the same quantity the full pass computes; only the
 // rounding order differs (fp32 runs of <= I / 32 products per lane, fp64 across).
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -178,17 +180,28 @@ __global__ void fitinc_plan_kernel(FitPlanArgs p) {
 // the full pass) into out[R + 1]: thread t < R + 1 sums column t over the terms and blocks in a
 // fixed order with four independent chains (deterministic; no serial chain of 4 x blocks).
 __device__ void fitinc_terms_sum(const FitFinishArgs& a, bool incr, double* out) {
-  const int R = a.R, RB = a.RB, t = threadIdx.x;
-  if (t > R) return;
-  const int col = t < R ? t : RB;   // column RB holds the sums of squares
-  double s4[4] = {0.0, 0.0, 0.0, 0.0};
+  // thread t sums the blocks b = t, t + nt, ... of every selected term (a fixed assignment), then
+  // each column is reduced across the threads by the fixed tree of block_sum_d: deterministic,
+  // and the partials' loads are spread over the whole block (one thread per column serialised
+  // ~1200 dependent L2 loads: ~100 us)
+  __shared__ double red[32];
+  const int R = a.R, RB = a.RB, t = threadIdx.x, nt = blockDim.x;
+  double s[kMaxR + 1];
+  for (int c = 0; c <= R; ++c) s[c] = 0.0;
   for (int tm = 0; tm < 4; ++tm) {
     const double* pt = a.terms[tm];
     if (!pt || incr != (tm < 3)) continue;
-    if (t == R && (tm == 1 || tm == 2)) continue;   // ||X||^2 grows by the new slices only
-    for (int b = 0; b < a.nparts[tm]; ++b) s4[b & 3] += pt[(int64_t)b * (RB + 1) + col];
+    const bool sq = !(tm == 1 || tm == 2);   // ||X||^2 grows by the new slices only
+    for (int b = t; b < a.nparts[tm]; b += nt) {
+      const double* row = pt + (int64_t)b * (RB + 1);
+      for (int c = 0; c < R; ++c) s[c] += row[c];
+      if (sq) s[R] += row[RB];
+    }
   }
-  out[t] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  for (int c = 0; c <= R; ++c) {
+    const double v = block_sum_d(s[c], red);
+    if (t == 0) out[c] = v;
+  }
 }
 
 // P' (incremental: P + the selected terms; full: the full pass), ||X'||^2, the relative
@@ -202,16 +215,20 @@ __global__ void fitinc_finish_kernel(FitFinishArgs a) {
   } else {
     fitinc_terms_sum(a, incr, sums);
   }
+  __shared__ double Gs[3 * kMaxR * kMaxR], ls[kMaxR], so[kMaxR + 2];
+  for (int e = threadIdx.x; e < 3 * R * R; e += blockDim.x) Gs[e] = a.G[e];   // staged: thread 0's
+  for (int e = threadIdx.x; e < R; e += blockDim.x) ls[e] = (double)a.lam[e];  // loops read shared
+  for (int e = threadIdx.x; e < R + 1; e += blockDim.x) so[e] = a.st_old[e];
   __syncthreads();
   if (threadIdx.x != 0) return;
   double P[kMaxR];
-  for (int f = 0; f < R; ++f) P[f] = (incr ? a.st_old[f] : 0.0) + sums[f];
-  const double xsq = (incr ? a.st_old[R] : 0.0) + sums[R];
+  for (int f = 0; f < R; ++f) P[f] = (incr ? so[f] : 0.0) + sums[f];
+  const double xsq = (incr ? so[R] : 0.0) + sums[R];
   double inner = 0.0, mn = 0.0;
-  for (int f = 0; f < R; ++f) inner += (double)a.lam[f] * P[f];
+  for (int f = 0; f < R; ++f) inner += ls[f] * P[f];
   for (int f = 0; f < R; ++f)
     for (int g = 0; g < R; ++g)
-      mn += (double)a.lam[f] * (double)a.lam[g] * a.G[f * R + g] * a.G[R * R + f * R + g] * a.G[2 * R * R + f * R + g];
+      mn += ls[f] * ls[g] * Gs[f * R + g] * Gs[R * R + f * R + g] * Gs[2 * R * R + f * R + g];
   const double res = fmax(0.0, xsq - 2.0 * inner + mn);
   *a.relerr = xsq > 0.0 ? sqrt(res / xsq) : 0.0;
   for (int f = 0; f < R; ++f) a.st_new[f] = P[f];
@@ -293,8 +310,115 @@ __global__ void coo_fit_flags_kernel(CooFitFlags p) {
   }
 }
 
+// Column-owner variant (RB <= 12): thread t of column block cb owns the column quad
+// cb * 256 + t of every row and keeps As for its 4 columns in registers (4 RB floats), so the
+// per-element work is R FFMAs with no shared-memory operand traffic; a block walks a contiguous
+// range of rows in chunks of kCR, whose store offsets and weights w_f = U(j,f) V(k,f) (with the
+// Usub / Vsub differences) are formed once per chunk in shared memory.  Row-chunk partials in
+// fp32 (<= 16 rows), fp64 across; grid = fitrows_blocks(): nrg row groups x ncb column blocks
+// (the blocks past ncb * nrg write zero partials).
+constexpr int kCT2 = 256, kCR = 64, kRF = 8;   // kRF: rows whose 16-byte loads are in flight
+template <int RB>
+__global__ void __launch_bounds__(kCT2, 2) fitcols_kernel(FitRows a, double* __restrict__ part) {
+  __shared__ float Wsh[kCR][RB];
+  __shared__ int64_t Xoff[kCR];
+  __shared__ double red[32];
+  const int R = a.R, tid = threadIdx.x;
+  const int nq = (int)(a.pitch / 4), ncb = (nq + kCT2 - 1) / kCT2;
+  const int nrg = (int)gridDim.x / ncb;
+  const int cb = blockIdx.x % ncb, rg = blockIdx.x / ncb;
+  int64_t nrows;
+  if (a.gate && *a.gate != a.gate_val) nrows = 0;
+  else if (a.kind == 0) nrows = (a.k1 - a.k0) * a.J;
+  else {
+    const int nl = *a.nlist;
+    nrows = a.kind == 1 ? (int64_t)nl * (a.k1 - a.k0) : (int64_t)nl * a.J;
+  }
+  const int64_t per = nrg > 0 ? (nrows + nrg - 1) / nrg : 0;
+  const int64_t r0 = (int64_t)rg * per, r1 = min(nrows, r0 + per);
+  if (rg >= nrg || r0 >= r1) {
+    if (tid <= RB) part[(int64_t)blockIdx.x * (RB + 1) + tid] = 0.0;
+    return;
+  }
+  const int q = cb * kCT2 + tid;
+  const bool valid = q < nq;
+  float av[RB][4];
+#pragma unroll
+  for (int f = 0; f < RB; ++f)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int i = 4 * q + e;
+      av[f][e] = (valid && f < R && i < a.I) ? a.As[(int64_t)i * R + f] : 0.f;
+    }
+  double acc[RB + 1];
+#pragma unroll
+  for (int f = 0; f <= RB; ++f) acc[f] = 0.0;
+  for (int64_t c0 = r0; c0 < r1; c0 += kCR) {
+    const int nrc = (int)min((int64_t)kCR, r1 - c0);
+    __syncthreads();   // the previous chunk's offsets / weights are consumed
+    if (tid < nrc) {
+      const int64_t row = c0 + tid;
+      int64_t j, k;
+      if (a.kind == 0) { k = a.k0 + row / a.J; j = row - (k - a.k0) * a.J; }
+      else if (a.kind == 1) { const int64_t t = row / (a.k1 - a.k0); j = a.list[t]; k = a.k0 + (row - t * (a.k1 - a.k0)); }
+      else { const int64_t t = row / a.J; j = row - t * a.J; k = a.list[t]; }
+      const int64_t kg = a.kmap ? a.kmap[k] : k;   // store slice -> model row (sharded)
+      Xoff[tid] = (k * a.J + j) * a.pitch;
+#pragma unroll
+      for (int f = 0; f < RB; ++f) {
+        float w = 0.f;
+        if (f < R) {
+          float u = a.U[j * R + f], v = a.V[kg * R + f];
+          if (a.Usub) u -= a.Usub[j * R + f];
+          if (a.Vsub) v -= a.Vsub[kg * R + f];
+          w = u * v;
+        }
+        Wsh[tid][f] = w;
+      }
+    }
+    __syncthreads();
+    if (!valid) continue;
+    for (int rb = 0; rb < nrc; rb += 16) {
+      float accf[RB];
+#pragma unroll
+      for (int f = 0; f < RB; ++f) accf[f] = 0.f;
+      float ss = 0.f;
+      const int re = min(nrc, rb + 16);
+      for (int rr = rb; rr < re; rr += kRF) {
+        float4 x[kRF];
+#pragma unroll
+        for (int u = 0; u < kRF; ++u)   // kRF rows' loads in flight
+          x[u] = rr + u < re ? __ldg(reinterpret_cast<const float4*>(a.X + Xoff[rr + u]) + q)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < kRF; ++u) {
+          if (rr + u >= re) break;
+          ss = fmaf(x[u].x, x[u].x, fmaf(x[u].y, x[u].y, fmaf(x[u].z, x[u].z, fmaf(x[u].w, x[u].w, ss))));
+#pragma unroll
+          for (int f = 0; f < RB; ++f) {
+            const float d = fmaf(x[u].x, av[f][0], fmaf(x[u].y, av[f][1], fmaf(x[u].z, av[f][2], x[u].w * av[f][3])));
+            accf[f] = fmaf(d, Wsh[rr + u][f], accf[f]);
+          }
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < RB; ++f) acc[f] += (double)accf[f];
+      acc[RB] += (double)ss;
+    }
+  }
+#pragma unroll
+  for (int f = 0; f <= RB; ++f) {
+    const double t = block_sum_d(acc[f], red);
+    if (tid == 0) part[(int64_t)blockIdx.x * (RB + 1) + f] = t;
+  }
+}
+
 template <int RB>
 cudaError_t fitrows_rb(const FitRows& a, double* part, int nblocks, cudaStream_t st) {
+  if (RB <= 12 && !getenv("SAMBATEN_FITROWS_SMEM")) {
+    fitcols_kernel<RB <= 12 ? RB : 12><<<nblocks, kCT2, 0, st>>>(a, part);
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(float) * (size_t)a.pitch * a.R;
   cudaFuncSetAttribute(fitrows_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fitrows_kernel<RB><<<nblocks, kFT, smem, st>>>(a, part);
@@ -303,7 +427,7 @@ cudaError_t fitrows_rb(const FitRows& a, double* part, int nblocks, cudaStream_t
 
 }  // namespace
 
-int fitrows_rb_of(int R) { return R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : 32; }
+int fitrows_rb_of(int R) { return R <= 4 ? 4 : R <= 8 ? 8 : R <= 10 ? 10 : R <= 12 ? 12 : R <= 16 ? 16 : 32; }
 
 int fitrows_blocks() { return kNumSMs * 2; }
 
@@ -317,6 +441,7 @@ cudaError_t launch_fitrows(FitRows a, double* part, cudaStream_t st) {
   switch (fitrows_rb_of(a.R)) {
     case 4: return fitrows_rb<4>(a, part, nb, st);
     case 8: return fitrows_rb<8>(a, part, nb, st);
+    case 10: return fitrows_rb<10>(a, part, nb, st);
     case 12: return fitrows_rb<12>(a, part, nb, st);
     case 16: return fitrows_rb<16>(a, part, nb, st);
     default: return fitrows_rb<32>(a, part, nb, st);
@@ -328,6 +453,7 @@ cudaError_t launch_coo_fitrows(const CooFitRows& a, double* part, cudaStream_t s
   switch (fitrows_rb_of(a.R)) {
     case 4: coo_fitrows_kernel<4><<<nb, 256, 0, st>>>(a, part); break;
     case 8: coo_fitrows_kernel<8><<<nb, 256, 0, st>>>(a, part); break;
+    case 10: coo_fitrows_kernel<10><<<nb, 256, 0, st>>>(a, part); break;
     case 12: coo_fitrows_kernel<12><<<nb, 256, 0, st>>>(a, part); break;
     case 16: coo_fitrows_kernel<16><<<nb, 256, 0, st>>>(a, part); break;
     default: coo_fitrows_kernel<32><<<nb, 256, 0, st>>>(a, part); break;
@@ -348,12 +474,12 @@ cudaError_t launch_fitinc_plan(const FitPlanArgs& p, cudaStream_t st) {
 }
 
 cudaError_t launch_fitinc_finish(const FitFinishArgs& a, cudaStream_t st) {
-  fitinc_finish_kernel<<<1, 64, 0, st>>>(a);
+  fitinc_finish_kernel<<<1, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fitinc_sum(const FitFinishArgs& a, double* out, cudaStream_t st) {
-  fitinc_sum_kernel<<<1, 64, 0, st>>>(a, out);
+  fitinc_sum_kernel<<<1, 256, 0, st>>>(a, out);
   return cudaGetLastError();
 }
 

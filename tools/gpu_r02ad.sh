@@ -1,0 +1,10 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_fitinc.py tests/test_gpu_dist.py tests/test_gpu_update.py tests/test_gpu_incremental.py -q -p no:cacheprovider -x > gpurun_out/ad.log 2>&1; echo "rc=$?" >> gpurun_out/ad.log
+tail -n 2 gpurun_out/ad.log
+for c in C4 C2; do
+timeout 900 python bench.py --config $c --steps 10 --warmup 3 --no-getrank --no-cpu-baseline --no-e2e --no-variant --no-recompute > gpurun_out/b.json 2> gpurun_out/b.err
+python -c "
+import json;d=json.load(open('gpurun_out/b.json'))
+print('$c', round(d['ms_per_step'],3), {k:round(v,3) for k,v in d['step_ms'].items()})"
+done
