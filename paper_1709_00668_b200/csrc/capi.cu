@@ -153,6 +153,7 @@ struct sambaten_s {
   int64_t nnz = 0, nnz_cap = 0, nnz_ck = 0;
   DevBuf coo_ws;            // gather / sort / ALS workspace of the COO path
   DevBuf grws, grk;         // GetRank in the update (R33): trial workspace, per-rep ranks [r]
+  DevBuf grc[4];            // COO GetRank in the update: ALS workspace, factors, CorConDia, offsets
   int rep_rank[kMaxReps] = {};   // rank each rep of the last update decomposed at
   int32_t* ci() const { return X.as<int32_t>(); }
   int32_t* cj() const { return ci() + nnz_cap; }
@@ -467,7 +468,8 @@ static sambaten_status create_common(sambaten_t* out, const sambaten_tensor* X0,
     FAIL(SAMBATEN_E_INVALID, "init: pipelined needs a dense tensor (R36)");
   }
   if (h->opts.getrank) {
-    if (h->fmt != SAMBATEN_DENSE) { delete h; FAIL(SAMBATEN_E_INVALID, "init: getrank needs a dense tensor (R33)"); }
+    // dense or COO (the sparse summaries are rated by the COO CorConDia); single-GPU
+    // (the sharded init refuses it)
     if (h->opts.getrank_trials < 1 || h->opts.getrank_trials > kMaxReps) {
       delete h; FAIL(SAMBATEN_E_INVALID, "init: getrank_trials must be in [1, 32]");
     }
@@ -1167,6 +1169,11 @@ __global__ static void rep_offsets_kernel(const int64_t* scan, int64_t nb, int r
   if (t <= r) off[t] = scan[(int64_t)t * nb];
 }
 
+static sambaten_status getrank_coo_one(DevBuf* ws, const int32_t* ti, const int32_t* tj, const int32_t* tk,
+                                       const float* tv, int64_t nnz, int I, int J, int K, int R_max, int trials,
+                                       uint32_t rep_base, uint64_t seed, int max_iters, double tol,
+                                       double threshold, int* R_new, double* cc, cudaStream_t st, int* launches);
+
 // The COO update (Alg. 1 with the sparse store): see the dense update for the step structure.
 static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, float* Aout,
                                   float* Bout, float* Cout, float* lamout, sambaten_info* info) {
@@ -1277,18 +1284,61 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
   // ---- a4: batched CP-ALS on the COO summaries ----------------------------------------------
   DenseAls a{};
   int als_launches = 0;
+  // GetRank on every sparse summary (Alg. 2; R33), rep numbering as the dense path
+  // (trial j of summary s is Philox rep s * trials + j)
+  const int* d_rnew = nullptr;
+  if (h->opts.getrank) {
+    bool deficient = false;
+    for (int s = 0; s < r; ++s) {
+      if (sambaten_status e = getrank_coo_one(h->grc, sp + h_off[s], sq + h_off[s], su + h_off[s], sv + h_off[s],
+                                              h_off[s + 1] - h_off[s], (int)nI, (int)nJ, (int)nKp, R,
+                                              h->opts.getrank_trials, (uint32_t)(s * h->opts.getrank_trials),
+                                              h->seed, h->opts.als_max_iters, h->opts.als_tol,
+                                              h->opts.getrank_threshold, &h->rep_rank[s], nullptr, st,
+                                              &als_launches))
+        return e;
+      deficient |= h->rep_rank[s] < R;
+    }
+    if (deficient) {
+      CK(h->grk.ensure(sizeof(int) * r));
+      CK(cudaMemcpyAsync(h->grk.p, h->rep_rank, sizeof(int) * r, cudaMemcpyHostToDevice, st));
+      d_rnew = h->grk.as<int>();
+    }
+  }
   const WarmRows wr{h->A(h->cur), h->B(h->cur), h->C(h->cur), h->lam(h->cur), Is, Js, Kp, (int)nKs};
   if (sambaten_status e = coo_als(h->coo_ws, st, R, sp, sq, su, sv, d_off, nsum, (int)nI, (int)nJ,
                                   (int)nKp, r, U0, U1, U2, h->seed, uid, h->opts.als_max_iters,
                                   h->opts.als_tol, true, &a, &als_launches, 0, 1,
                                   h->opts.warm_start ? &wr : nullptr))
     return e;
+  if (d_rnew) {
+    // the repetitions GetRank reduced: decomposed alone at R_new (Philox rep s, as in the batch)
+    // and written, zero-padded to R columns, over their batch result (R33)
+    CK(h->grws.ensure(sizeof(float) * (size_t)(nI + nJ + nKp) * R + 256));
+    for (int s = 0; s < r; ++s) {
+      if (h->rep_rank[s] >= R) continue;
+      const int F = h->rep_rank[s];
+      CK(h->grc[3].ensure(2 * sizeof(int64_t)));
+      two_offsets_kernel<<<1, 32, 0, st>>>(h->grc[3].as<int64_t>(), h_off[s + 1] - h_off[s]);
+      float* V0 = h->grws.as<float>();
+      float* V1 = V0 + (size_t)nI * F;
+      float* V2 = V1 + (size_t)nJ * F;
+      DenseAls b{};
+      if (sambaten_status e = coo_als(h->grc[0], st, F, sp + h_off[s], sq + h_off[s], su + h_off[s], sv + h_off[s],
+                                      h->grc[3].as<int64_t>(), h_off[s + 1] - h_off[s], (int)nI, (int)nJ, (int)nKp,
+                                      1, V0, V1, V2, h->seed, uid, h->opts.als_max_iters, h->opts.als_tol, true,
+                                      &b, &als_launches, (uint32_t)s, 1))
+        return e;
+      CK(launch_rank_pad(b, a, s, st));
+      ++als_launches;
+    }
+  }
   launches += als_launches;
   CK(cudaEventRecord(h->ev[5], st));
   // ---- a5 / a6: match and merge (format independent) -----------------------------------------
   const int b = h->cur, nbuf = 1 - h->cur;
   int* accepted = nullptr;
-  CK(run_match_merge(h, a, Is, Js, Kp, locI, locJ, locK, Ko, Kn, nI, nJ, nKs, nKp, &accepted));
+  CK(run_match_merge(h, a, Is, Js, Kp, locI, locJ, locK, Ko, Kn, nI, nJ, nKs, nKp, &accepted, d_rnew));
   launches += 1 + 4;
   CK(cudaEventRecord(h->ev[7], st));
   // ---- a7: full fit of the new model (optional) ----------------------------------------------
@@ -1999,34 +2049,39 @@ extern "C" sambaten_status sambaten_als_plan(int nI, int nJ, int nK, int R, int 
   return SAMBATEN_OK;
 }
 
-// GetRank on a canonical COO tensor (device arrays): each candidate rank F and trial j runs the
-// COO ALS (r = 1, Philox init R30) and the sparse CorConDia rates it; same selection as dense.
-static sambaten_status getrank_coo(const sambaten_tensor* X, int R_max, int trials, uint64_t seed, int max_iters,
-                                   double tol, double threshold, int* R_new, double* cc, cudaStream_t st) {
+// GetRank (Alg. 2; R29-R31) on one canonical COO tensor (device arrays; dims I x J x
+// K): each candidate rank F and trial j runs the COO ALS (r = 1, Philox update_id 0x47520000 + F,
+// rep rep_base + j: R30, the dense path's numbering) and the sparse CorConDia rates it;
+// R_new = the largest F whose best trial reaches `threshold` (R31), else 1.  Synchronises st.
+// ws: [0] ALS workspace, [1] factors, [2] CorConDia workspace + ratings, [3] offsets.
+static sambaten_status getrank_coo_one(DevBuf* ws, const int32_t* ti, const int32_t* tj, const int32_t* tk,
+                                       const float* tv, int64_t nnz, int I, int J, int K, int R_max, int trials,
+                                       uint32_t rep_base, uint64_t seed, int max_iters, double tol,
+                                       double threshold, int* R_new, double* cc, cudaStream_t st, int* launches) {
   constexpr uint32_t kGetRankId = 0x47520000u;   // R30
-  const int I = (int)X->dims[0], J = (int)X->dims[1], K = (int)X->dims[2];
-  DevBuf ws, offb, fac, ccb;
-  CK(offb.ensure(2 * sizeof(int64_t)));
-  two_offsets_kernel<<<1, 32, 0, st>>>(offb.as<int64_t>(), X->nnz);
-  CK(fac.ensure(sizeof(float) * ((size_t)I + J + K) * R_max + 256));
-  CK(ccb.ensure(sizeof(double) * (corcondia_coo_ws_doubles(I, J, K, R_max, 1) + (size_t)R_max * trials + 8)));
-  double* ccws = ccb.as<double>();
-  double* ccd = ccws + corcondia_coo_ws_doubles(I, J, K, R_max, 1);
+  CK(ws[3].ensure(2 * sizeof(int64_t)));
+  two_offsets_kernel<<<1, 32, 0, st>>>(ws[3].as<int64_t>(), nnz);
+  CK(ws[1].ensure(sizeof(float) * ((size_t)I + J + K) * R_max + 256));
+  const size_t ccn = corcondia_coo_ws_doubles(I, J, K, R_max, 1);
+  CK(ws[2].ensure(sizeof(double) * (ccn + (size_t)R_max * trials + 8)));
+  double* ccws = ws[2].as<double>();
+  double* ccd = ccws + ccn;
   for (int F = 1; F <= R_max; ++F) {
-    float* U0 = fac.as<float>();
+    float* U0 = ws[1].as<float>();
     float* U1 = U0 + (size_t)I * F;
     float* U2 = U1 + (size_t)J * F;
     for (int j = 0; j < trials; ++j) {
       DenseAls d{};
       int nl = 0;
-      if (sambaten_status e = coo_als(ws, st, F, X->idx[0], X->idx[1], X->idx[2], X->vals, offb.as<int64_t>(), X->nnz,
-                                      I, J, K, 1, U0, U1, U2, seed, kGetRankId + (uint32_t)F, max_iters, tol, true,
-                                      &d, &nl, (uint32_t)j, 1))
+      if (sambaten_status e = coo_als(ws[0], st, F, ti, tj, tk, tv, ws[3].as<int64_t>(), nnz, I, J, K, 1, U0, U1,
+                                      U2, seed, kGetRankId + (uint32_t)F, max_iters, tol, true, &d, &nl,
+                                      rep_base + (uint32_t)j, 1))
         return e;
       const float* U[3] = {U0, U1, U2};
       const int64_t us[3] = {0, 0, 0};
-      CK(launch_corcondia_coo(X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, I, J, K, F, 1, U, us, d.lam, ccws,
+      CK(launch_corcondia_coo(ti, tj, tk, tv, nnz, I, J, K, F, 1, U, us, d.lam, ccws,
                               ccd + (size_t)(F - 1) * trials + j, st));
+      if (launches) *launches += nl + 4;
     }
   }
   std::vector<double> hc((size_t)R_max * trials);
@@ -2043,6 +2098,13 @@ static sambaten_status getrank_coo(const sambaten_tensor* X, int R_max, int tria
   }
   *R_new = best;
   return SAMBATEN_OK;
+}
+
+static sambaten_status getrank_coo(const sambaten_tensor* X, int R_max, int trials, uint64_t seed, int max_iters,
+                                   double tol, double threshold, int* R_new, double* cc, cudaStream_t st) {
+  DevBuf ws[4];
+  return getrank_coo_one(ws, X->idx[0], X->idx[1], X->idx[2], X->vals, X->nnz, (int)X->dims[0], (int)X->dims[1],
+                         (int)X->dims[2], R_max, trials, 0, seed, max_iters, tol, threshold, R_new, cc, st, nullptr);
 }
 
 extern "C" sambaten_status sambaten_corcondia(const sambaten_tensor* X, int F, const float* A, const float* B,

@@ -173,3 +173,65 @@ def test_getrank_coo_matches_oracle(F, seed):
     rn_g, cc_g = L().sambaten_getrank(t, 4, 2, 7, 300, 0.0)
     assert rn_g == rn_o == F, (cc_g, cc_o)
     assert np.all(np.abs(cc_g[:F] - cc_o[:F]) <= 0.05), (cc_g, cc_o)
+
+
+# ---- GetRank inside the COO update (sparse summaries rated by the COO CorConDia) -------
+def _coo_stream(T):
+    """The same tensor stored as a canonical COO (every entry of the planted tensor, sorted by
+    (k, j, i)): oracle Coo and device arrays."""
+    from oracle import sambaten as O
+    kk, jj, ii = np.nonzero(T != 0.0)
+    X = O.coo_canonical(ii, jj, kk, T[kk, jj, ii].astype(np.float32), (T.shape[2], T.shape[1], T.shape[0]))
+    t = L().coo(dev(X.i.astype(np.int32)), dev(X.j.astype(np.int32)), dev(X.k.astype(np.int32)), dev(X.v), X.dims)
+    return X, t
+
+
+def _run_gpu_coo(T0, batch, model, R, seed, maxit, tol, getrank):
+    lam, A, B, C = model
+    X0, t0 = _coo_stream(T0)
+    Xb, tb = _coo_stream(batch)
+    opts = L().default_opts(als_max_iters=maxit, als_tol=tol, accept_tau=0.0, capacity=X0.nnz + Xb.nnz,
+                            capacity_k=T0.shape[0] + batch.shape[0], full_fit=1, getrank=getrank)
+    h = L().sambaten_init_factors(t0, R, 2, 3, seed, A, B, C, lam, opts)
+    try:
+        K = T0.shape[0] + batch.shape[0]
+        I, J = T0.shape[2], T0.shape[1]
+        out = [np.empty(R, np.float32), np.empty((I, R), np.float32), np.empty((J, R), np.float32),
+               np.empty((K, R), np.float32)]
+        info = L().sambaten_update(h, tb, out[1], out[2], out[3], out[0])
+    finally:
+        L().sambaten_destroy(h)
+    return out, info
+
+
+def test_update_getrank_coo_full_rank_is_the_plain_update():
+    """COO handle: GetRank finds the universal rank on every sparse summary -> bit-identical to
+    the plain COO update."""
+    T0, batch, model = _stream(3, 3, 0)
+    plain, _ = _run_gpu_coo(T0, batch, model, 3, 4, 300, 1e-12, 0)
+    gr, info = _run_gpu_coo(T0, batch, model, 3, 4, 300, 1e-12, 1)
+    assert list(info.rep_rank[:3]) == [3, 3, 3]
+    for x, y in zip(plain, gr):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
+def test_update_getrank_coo_rank_deficient_matches_oracle():
+    """COO handle, rank-deficient batch (R33 with the sparse CorConDia): per-rep ranks equal the
+    oracle's on the same COO stream; the third component keeps its lambda bit for bit and gets
+    exact-zero new time rows; the merged model agrees with the oracle's (1e-3 relative)."""
+    from oracle import sambaten as O
+    T0, batch, model = _stream(2, 3, 1)
+    X0, _ = _coo_stream(T0)
+    Xb, _ = _coo_stream(batch)
+    cfg = O.Config(R=3, s=(2, 2, 2), r=3, seed=6, maxit=400, tol=1e-12, tau=0.0, getrank=True)
+    st = O.init_factors(X0, cfg, *[np.asarray(x, np.float64) for x in model], X0.nnz + Xb.nnz)
+    last = O.update(st, Xb)
+    got, info = _run_gpu_coo(T0, batch, model, 3, 6, 400, 1e-12, 1)
+    assert list(info.rep_rank[:3]) == [rp["rank"] for rp in last["reps"]] == [2, 2, 2]
+    assert info.reps_rejected_mask == 0
+    lam, A, B, C = got
+    assert lam[2] == model[0][2]
+    Kn = batch.shape[0]
+    assert np.all(C[-Kn:, 2] == 0.0)
+    for g, o in zip((lam, A, B, C), (st.lam, st.A, st.B, st.C)):
+        assert np.allclose(g, o, rtol=1e-3, atol=1e-5), np.abs(g - o).max()

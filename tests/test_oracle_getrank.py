@@ -135,3 +135,24 @@ def test_corcondia_of_a_coo_tensor_is_that_of_its_densification():
     lam = np.ones(2)
     assert GR.corcondia(X, lam, A, B, C) == GR.corcondia(Y, lam, A, B, C)
     assert abs(GR.corcondia(X, lam, A, B, C) - 100.0) < 1e-4
+
+
+def test_coo_update_with_getrank_equals_the_dense_one():
+    """The same stream stored as a COO tensor (every entry): GetRank on the sparse summaries
+    (cp_als on the Coo, CorConDia of the densified summary) gives the dense update's per-rep
+    ranks and, to rounding, its merged model -- the COO handle's parity target (R33)."""
+    T0, batch, model = _stream(2, 3, 1)
+
+    def coo(T):
+        kk, jj, ii = np.nonzero(T != 0.0)
+        return O.coo_canonical(ii, jj, kk, T[kk, jj, ii], (T.shape[2], T.shape[1], T.shape[0]))
+
+    cfg = O.Config(R=3, s=(2, 2, 2), r=3, seed=6, maxit=200, tol=1e-12, tau=0.0, getrank=True)
+    sd = O.init_factors(T0, cfg, *model, T0.size * 2)
+    ld = O.update(sd, batch)
+    X0, Xb = coo(T0), coo(batch)
+    sc = O.init_factors(X0, cfg, *model, (X0.nnz + Xb.nnz) * 2)
+    lc = O.update(sc, Xb)
+    assert [rp["rank"] for rp in lc["reps"]] == [rp["rank"] for rp in ld["reps"]] == [2, 2, 2]
+    for a, b in zip((sc.lam, sc.A, sc.B, sc.C), (sd.lam, sd.A, sd.B, sd.C)):
+        assert np.allclose(a, b, rtol=1e-8, atol=1e-10)
