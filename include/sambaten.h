@@ -104,8 +104,9 @@ typedef struct {
   int getrank;            /* 1: before each summary decomposition run GetRank (Alg. 2,        */
                           /* P:279-294) on the summary and decompose at the rank it returns;  */
                           /* only those components are matched and merged (P:264-266,        */
-                          /* readings R29-R33).  Dense and COO single-GPU handles (COO: the   */
-                          /* sparse CorConDia); a sharded init refuses it.  Default 0.        */
+                          /* readings R29-R33).  Dense and COO handles (COO: the sparse       */
+                          /* CorConDia), single-GPU and sharded (each rank rates its owned    */
+                          /* repetitions, the ranks are allgathered).  Default 0.             */
   int getrank_trials;     /* CP runs per candidate rank (Alg. 2 `it`); default 1              */
   double getrank_threshold; /* CorConDia cut-off of R31; default 90                           */
   int warm_start;         /* 1: each summary ALS starts from the model's rows (A(I_s), B(J_s),  */

@@ -731,7 +731,7 @@ static cudaError_t run_sampling(sambaten_s* h, const int64_t* x1, const int64_t*
 static cudaError_t getrank_batch(const float* Y, int64_t y_stride, int64_t pitch, int I, int J, int K,
                                  int nsum, int R_max, int trials, uint64_t seed, int max_iters, double tol,
                                  double threshold, DevBuf& ws, cudaStream_t st, int* R_new, double* cc,
-                                 int* launches) {
+                                 int* launches, uint32_t rep_base = 0) {
   constexpr uint32_t kGetRankId = 0x47520000u;   // R30
   // trials == 1: the nsum summaries are one batch of models (rep = s); else one batch of
   // `trials` models per summary (rep = s * trials + j)
@@ -761,7 +761,8 @@ static cudaError_t getrank_batch(const float* Y, int64_t y_stride, int64_t pitch
       a.u_stride[0] = (int64_t)I * F; a.u_stride[1] = (int64_t)J * F; a.u_stride[2] = (int64_t)K * F;
       dense_als_workspace(&a);
       if ((e = dense_als_bind_workspace(&a, base + ub)) != cudaSuccess) return e;
-      if ((e = launch_als_init(a, seed, kGetRankId + (uint32_t)F, (uint32_t)(g * trials), true, st)) != cudaSuccess)
+      if ((e = launch_als_init(a, seed, kGetRankId + (uint32_t)F, rep_base + (uint32_t)(g * trials), true, st)) !=
+          cudaSuccess)
         return e;
       if ((e = run_dense_als(a, st)) != cudaSuccess) return e;
       const float* U[3] = {a.U[0], a.U[1], a.U[2]};
@@ -796,7 +797,7 @@ static cudaError_t getrank_batch(const float* Y, int64_t y_stride, int64_t pitch
 // R_new[rho] (Philox rep rho, as the plain path) and is padded with zero columns into the
 // R-column candidate buffers of `a` (whose workspace is bound).
 static cudaError_t rank_als(sambaten_s* h, const DenseAls& a, const int* R_new, uint32_t uid,
-                            cudaStream_t st, int* launches) {
+                            cudaStream_t st, int* launches, uint32_t rep0 = 0, uint32_t rep_stride = 1) {
   DenseAls b{};
   b.y_stride = 0; b.pitch = a.pitch; b.nI = a.nI; b.nJ = a.nJ; b.nK = a.nK; b.r = 1;
   b.maxit = a.maxit; b.tol = a.tol;
@@ -813,7 +814,7 @@ static cudaError_t rank_als(sambaten_s* h, const DenseAls& a, const int* R_new, 
     b.u_stride[0] = (int64_t)a.nI * b.R; b.u_stride[1] = (int64_t)a.nJ * b.R; b.u_stride[2] = (int64_t)a.nK * b.R;
     dense_als_workspace(&b);
     if ((e = dense_als_bind_workspace(&b, h->grws.as<char>() + ub)) != cudaSuccess) return e;
-    if ((e = launch_als_init(b, h->seed, uid, (uint32_t)rho, true, st)) != cudaSuccess) return e;
+    if ((e = launch_als_init(b, h->seed, uid, rep0 + (uint32_t)rho * rep_stride, true, st)) != cudaSuccess) return e;
     if ((e = run_dense_als(b, st)) != cudaSuccess) return e;
     if ((e = launch_rank_pad(b, a, rho, st)) != cudaSuccess) return e;
     *launches += 4 + 7 * a.maxit + 1;

@@ -278,3 +278,52 @@ def _full_als_worker(rank, world, iters):
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_full_als_decomposition(world):
     _run(world, _full_als_worker, 6)
+
+
+# ------------------------------------------------- 5. GetRank in the sharded update (R33)
+def _getrank_worker(rank, world, out_path):
+    """Each rank rates its owned repetitions' summaries (rho = rank + t G, Philox reps
+    rho * trials + j as on one GPU); an allgather in rank-major order, read back as repetition
+    g + t G (capi_dist.inc dist_share_ranks), must give the single-process update's ranks."""
+    from oracle import getrank as GR
+    rng = np.random.default_rng(1)
+    I, J, K, K0, R, F_true = 40, 36, 30, 24, 3, 2
+    A, B, C = rng.random((I, R)), rng.random((J, R)), rng.random((K, R))
+    C[:, F_true:] = 0.0
+    T = np.ascontiguousarray(np.transpose(np.einsum("if,jf,kf->ijk", A, B, C), (2, 1, 0))).astype(np.float32)
+    T0, batch = T[:K0], T[K0:]
+    r, trials = 2 * world, 2
+    cfg = O.Config(R=R, s=(2, 2, 2), r=r, seed=6, maxit=60, tol=1e-9, tau=0.0, getrank=True, getrank_trials=trials)
+    ref = O.init_factors(T0, cfg, np.ones(R), A, B, C[:K0], T0.size * 2)
+    want = [rp["rank"] for rp in O.update(ref, batch)["reps"]]
+    st = O.init_factors(T0, cfg, np.ones(R), A, B, C[:K0], T0.size * 2)
+    X = np.concatenate([T0, batch])
+    x1, x2, x3 = O.marginals_dense(X, st.S, cfg.moi)
+    uid, Kn = 1, batch.shape[0]
+    own = []
+    for t in range(r // world):
+        rho = rank + t * world
+        Is = O.sample_mode(x1, O.sample_size(I, 2), cfg.seed, uid, rho, 0)
+        Js = O.sample_mode(x2, O.sample_size(J, 2), cfg.seed, uid, rho, 1)
+        Ks = O.sample_mode(x3[:K0], O.sample_size(K0, 2), cfg.seed, uid, rho, 2)
+        Y = O.gather_dense(X, Is, Js, O.k_prime(Ks, K0, Kn))
+        rn, _ = GR.getrank(Y, R, trials, cfg.seed, cfg.maxit, cfg.tol, cfg.getrank_threshold, rep_base=rho * trials)
+        own.append(rn)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, own)
+    flat = [x for g in gathered for x in g]          # rank-major, as the NCCL allgather
+    rloc = r // world
+    got = [0] * r
+    for g in range(world):
+        for t in range(rloc):
+            got[g + t * world] = flat[g * rloc + t]
+    assert got == want, (got, want)
+    if rank == 0:
+        open(out_path, "w").write("ok")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_getrank_ranks_equal_single_process(world, tmp_path):
+    out = tmp_path / "done"
+    _run(world, _getrank_worker, str(out))
+    assert out.read_text() == "ok"
