@@ -1545,7 +1545,7 @@ extern "C" sambaten_status sambaten_update(sambaten_t h, const sambaten_tensor* 
   a.Yt = Yt;
   CK(h->gord.ensure(sizeof(int32_t) * r * nKp));
   CK(launch_gather_dense(V, Is, Js, Kp, (int)nI, (int)nJ, (int)nKp, r, nI, nJ, nKp, Y, y_stride, st,
-                         Yt, pI, pJ, h->gord.as<int32_t>()));
+                         Yt, pI, pJ, h->gord.as<int32_t>(), Ko + Kn));
   CK(cudaEventRecord(h->ev[4], st));
   // ---- a4: batched CP-ALS ---------------------------------------------------------------
   const size_t ws_als = align256(dense_als_workspace(&a));

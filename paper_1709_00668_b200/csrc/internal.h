@@ -69,7 +69,9 @@ cudaError_t launch_gather_dense(const DenseView& X, const int32_t* Is, const int
                                 const int32_t* Kp, int nI, int nJ, int nK, int r,
                                 int64_t idx_stride_I, int64_t idx_stride_J, int64_t idx_stride_K,
                                 float* Y, int64_t y_stride, cudaStream_t st, float* Yt = nullptr,
-                                int pI = 0, int pJ = 0, int32_t* order_ws = nullptr);
+                                int pI = 0, int pJ = 0, int32_t* order_ws = nullptr, int64_t nslices = 0);
+// (order_ws: r * nK int32 scratch for the slice-ordered walk; nslices: slices of the store K'
+// indexes, <= 8192 for the ordering, else the plain (rep, slice) order)
 
 // ---- dense batched CP-ALS -------------------------------------------------------------
 struct DenseAls {

@@ -13,39 +13,43 @@ namespace sbt {
 
 constexpr int kGatherThreads = 256;
 
-// The (rep, u) pairs of all summaries ordered by their source slice K'[rep][u] (stable, one
-// block, bitonic in shared memory): the gather's blocks then walk the store slice by slice, so
-// the 16 repetitions' reads of a new slice hit L2 after the first and the address translations
-// stay within a few slices of the 108 GB store (random slice order missed the TLB).
-constexpr int kOrderMax = 8192;
+// The (rep, u) pairs of all summaries ordered by their source slice K'[rep][u] (ties by rep:
+// stable), so the gather's blocks walk the store slice by slice -- the 16 repetitions' reads of
+// a new slice hit L2 after the first and the address translations stay within a few slices of
+// the 108 GB store (random slice order missed the TLB).  One block: a bitmask per slice of the
+// repetitions that sampled it (a repetition's K' holds distinct slices), an exclusive scan of
+// the popcounts, and pair (rep, u) goes to start[k] + popc(mask[k] & ((1 << rep) - 1)).  Exact
+// integer work, independent of thread order.
+constexpr int kOrderSlices = 8192;   // slices of the store covered (2 x 32 KB of dynamic shared memory)
 __global__ void __launch_bounds__(1024) gather_order_kernel(const int32_t* __restrict__ Kp, int nK, int r,
-                                                            int64_t sK, int32_t* __restrict__ order) {
-  extern __shared__ unsigned long long key[];   // [m], m = the power of two >= n
-  const int n = nK * r;
-  int m = 1;
-  while (m < n) m <<= 1;
-  for (int e = threadIdx.x; e < m; e += blockDim.x) {
-    if (e < n) {
-      const int rep = e / nK, u = e - rep * nK;
-      key[e] = ((unsigned long long)(unsigned)Kp[rep * sK + u] << 32) | (unsigned)e;   // (k, pair): stable
-    } else {
-      key[e] = ~0ull;
-    }
+                                                            int64_t sK, int nslices, int32_t* __restrict__ order) {
+  extern __shared__ unsigned order_sm[];   // [nslices] masks | [nslices] starts
+  unsigned* mask = order_sm;
+  int* start = reinterpret_cast<int*>(order_sm + nslices);
+  __shared__ int sh[33];
+  __shared__ int carry;
+  for (int k = threadIdx.x; k < nslices; k += blockDim.x) mask[k] = 0u;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < nK * r; e += blockDim.x) {
+    const int rep = e / nK, u = e - rep * nK;
+    atomicOr(&mask[Kp[rep * sK + u]], 1u << rep);
   }
   __syncthreads();
-  for (int kk = 2; kk <= m; kk <<= 1)
-    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-      for (int e = threadIdx.x; e < m; e += blockDim.x) {
-        const int p = e ^ jj;
-        if (p > e) {
-          const bool up = (e & kk) == 0;
-          const unsigned long long a = key[e], b = key[p];
-          if ((a > b) == up) { key[e] = b; key[p] = a; }
-        }
-      }
-      __syncthreads();
-    }
-  for (int e = threadIdx.x; e < n; e += blockDim.x) order[e] = (int32_t)(key[e] & 0xffffffffu);
+  for (int k0 = 0; k0 < nslices; k0 += blockDim.x) {   // exclusive scan of the popcounts
+    const int k = k0 + threadIdx.x;
+    int tot;
+    const int ex = block_excl_scan(k < nslices ? __popc(mask[k]) : 0, sh, &tot);
+    if (k < nslices) start[k] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nK * r; e += blockDim.x) {
+    const int rep = e / nK, u = e - rep * nK;
+    const int k = Kp[rep * sK + u];
+    order[start[k] + __popc(mask[k] & ((1u << rep) - 1u))] = e;
+  }
 }
 
 __global__ void __launch_bounds__(kGatherThreads) gather_dense_kernel(
@@ -113,19 +117,17 @@ __global__ void __launch_bounds__(kGatherThreads) gather_dense_kernel(
 cudaError_t launch_gather_dense(const DenseView& X, const int32_t* Is, const int32_t* Js,
                                 const int32_t* Kp, int nI, int nJ, int nK, int r,
                                 int64_t sI, int64_t sJ, int64_t sK, float* Y, int64_t y_stride,
-                                cudaStream_t st, float* Yt, int pI, int pJ, int32_t* order_ws) {
+                                cudaStream_t st, float* Yt, int pI, int pJ, int32_t* order_ws, int64_t nslices) {
   if (nK <= 0 || nJ <= 0 || nI <= 0 || r <= 0) return cudaSuccess;
   if (pI < nI) pI = nI;
   if (pJ < nJ) pJ = nJ;
   const int npair = nK * r;
   if (npair > 65535) return cudaErrorInvalidConfiguration;   // grid.y limit
   const int32_t* order = nullptr;
-  if (order_ws && npair <= kOrderMax && r > 1) {
-    int m = 1;
-    while (m < npair) m <<= 1;
-    cudaFuncSetAttribute(gather_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(unsigned long long) * kOrderMax));
-    gather_order_kernel<<<1, 1024, sizeof(unsigned long long) * m, st>>>(Kp, nK, r, sK, order_ws);
+  if (order_ws && nslices > 0 && nslices <= kOrderSlices && r > 1 && r <= 32) {
+    const int smem = (int)(2 * sizeof(int) * nslices);
+    cudaFuncSetAttribute(gather_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * kOrderSlices);
+    gather_order_kernel<<<1, 1024, smem, st>>>(Kp, nK, r, sK, (int)nslices, order_ws);
     order = order_ws;
   }
   dim3 grid((unsigned)ceil_div(pJ, 32), (unsigned)npair, 1);
