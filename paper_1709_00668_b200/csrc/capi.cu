@@ -1023,6 +1023,7 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     double* Vi = b.take<double>((size_t)r * R * R);
     double* rpart = b.take<double>(als_rows_part_doubles((int)maxn, R, r));
     int* stop = b.take<int>(r);
+    unsigned* gbar = b.take<unsigned>(coo_als_persist_ctr_words(maxit));
     const int RBp = R <= 4 ? 4 : R <= 8 ? 8 : R <= 12 ? 12 : R <= 16 ? 16 : R <= 24 ? 24 : 32;
     const bool padded = R <= 16;   // the row-parallel solve keeps the padded copies in sync
     float* Upad = padded ? b.take<float>((size_t)r * ((int64_t)nI + nJ + nK) * RBp) : nullptr;
@@ -1037,6 +1038,8 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
       plan[m].pb = b.take<int64_t>(pe);
       plan[m].prow = b.take<int32_t>(pe);
       plan[m].partial = b.take<double>(pe * R);
+      plan[m].plist = b.take<int32_t>(pe);
+      plan[m].nlist = b.take<unsigned>(2);
       if (m < 2) {
         plan[m].sa = b.take<int32_t>(n); plan[m].sb = b.take<int32_t>(n); plan[m].sv = b.take<float>(n);
       }
@@ -1108,27 +1111,34 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
     if (e == cudaSuccess) e = launch_pad_factors(ra, st);
     const bool rows = R <= 16;
     if (e == cudaSuccess) e = cudaMemsetAsync(stop, 0, sizeof(int) * r, st);
-    // the stop test runs on the device; the host looks at the done flags after iterations 3,
-    // 6, 10, 15, ... (one small read each) and stops launching once every repetition is done
-    int nit = 0, next_check = 3, gap = 3;
-    for (int it = 0; it < maxit && e == cudaSuccess; ++it, ++nit) {
-      if (rows && it > 0) e = launch_als_rows_commit(ra, st);
-      for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
-        e = launch_coo_mttkrp(a, m, st);
-        if (e == cudaSuccess) e = rows ? launch_als_rows_mode(ra, m, st) : launch_als_solve(*d, m, st);
+    if (e == cudaSuccess && rows && coo_als_persist_supported(R)) {
+      // every iteration in one persistent cooperative kernel (k_coo_als.cu)
+      e = launch_coo_als_persist(a, ra, gbar, st);
+      *launches = 2 * 3 + 9 + 3 + 3 + 3 + 1;
+    } else {
+      // the per-mode pipeline: the stop test runs on the device; the host looks at the done
+      // flags after iterations 3, 6, 10, 15, ... (one small read each) and stops launching once
+      // every repetition is done
+      int nit = 0, next_check = 3, gap = 3;
+      for (int it = 0; it < maxit && e == cudaSuccess; ++it, ++nit) {
+        if (rows && it > 0) e = launch_als_rows_commit(ra, st);
+        for (int m = 0; m < 3 && e == cudaSuccess; ++m) {
+          e = launch_coo_mttkrp(a, m, st);
+          if (e == cudaSuccess) e = rows ? launch_als_rows_mode(ra, m, st) : launch_als_solve(*d, m, st);
+        }
+        int* hd = pinned_done_flags();
+        if (hd && rows && e == cudaSuccess && it + 1 == next_check && it + 1 < maxit) {
+          next_check += ++gap;
+          e = launch_als_rows_commit(ra, st);
+          if (e == cudaSuccess) e = cudaMemcpyAsync(hd, done, sizeof(int) * r, cudaMemcpyDeviceToHost, st);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+          int nd = 0;
+          for (int t = 0; t < r; ++t) nd += hd[t] != 0;
+          if (nd == r) { ++nit; break; }
+        }
       }
-      int* hd = pinned_done_flags();
-      if (hd && rows && e == cudaSuccess && it + 1 == next_check && it + 1 < maxit) {
-        next_check += ++gap;
-        e = launch_als_rows_commit(ra, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(hd, done, sizeof(int) * r, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        int nd = 0;
-        for (int t = 0; t < r; ++t) nd += hd[t] != 0;
-        if (nd == r) { ++nit; break; }
-      }
+      *launches = 2 * 3 + 9 + 3 + 3 + 3 + (rows ? 16 : 6) * nit;
     }
-    *launches = 2 * 3 + 9 + 3 + 3 + 3 + (rows ? 16 : 6) * nit;
     if (e != cudaSuccess) {
       set_error(std::string("COO ALS: ") + cudaGetErrorString(e));
       d->nI = -1;

@@ -218,6 +218,8 @@ struct CooModePlan {                   // per-mode MTTKRP layout (k_coo.cu)
   const int32_t *sa, *sb;              // other two indices in the mode's order
   const float* sv;                     // values in the mode's order
   double* partial;                     // [pieces][R] partial sums of multi-piece rows
+  int32_t* plist;                      // optional [pieces]: warp pieces at [0, nlist[0]), short
+  unsigned* nlist;                     //   pieces at plist[P - 1 - j], j < nlist[1] (any order)
 };
 struct CooAls {                        // the r COO summaries (concatenated) + ALS buffers
   int nI, nJ, nK, R, RB, r;
@@ -297,6 +299,11 @@ int gram_tiles_for(int n);
 cudaError_t launch_gram_tiles(const GramArgs& g, cudaStream_t st);
 cudaError_t launch_als_rows_commit(const RowsAls& a, cudaStream_t st);
 size_t als_rows_part_doubles(int maxn, int R, int r);
+// the whole batched COO ALS (every iteration and mode) in one cooperative launch (k_coo_als.cu);
+// R <= 16 with padded factors; bar: one zeroed-by-the-launch counter
+bool coo_als_persist_supported(int R);
+size_t coo_als_persist_ctr_words(int maxit);   // size of `bar` (barrier + work counters)
+cudaError_t launch_coo_als_persist(const CooAls& ca, const RowsAls& ra, unsigned* bar, cudaStream_t st);
 // ALS pieces shared with the COO path (k_als.cu)
 cudaError_t launch_als_solve(const DenseAls& a, int mode, cudaStream_t st);
 cudaError_t launch_als_gram(const DenseAls& a, cudaStream_t st);

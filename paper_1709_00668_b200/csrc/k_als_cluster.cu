@@ -742,11 +742,15 @@ __device__ __forceinline__ void grid_rep_sync(unsigned* ctr, unsigned target) {
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(ctr, 1u);
+    // spin on relaxed loads (an acquire load per poll would invalidate this SM's L1 each time,
+    // under the feet of the co-resident CTAs still working), then one acquire fence
     unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
-    } while (v < target);
-    __threadfence();
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    while (v < target) {
+      __nanosleep(20);
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }

@@ -19,39 +19,6 @@ namespace {
 
 constexpr int kRT = 128;   // rows per tile / threads per block
 
-// Gauss-Jordan in registers for R <= RB <= 16: lane c < 2R holds column c of [V | I].
-template <int RB>
-__device__ bool gj_reg(const double* V, double* Vi, int R) {
-  const int lane = threadIdx.x & 31;
-  double col[RB];
-#pragma unroll
-  for (int i = 0; i < RB; ++i) {
-    double v = 0.0;
-    if (i < R) v = lane < R ? V[i * R + lane] : (lane - R == i ? 1.0 : 0.0);
-    col[i] = v;
-  }
-  bool ok = true;
-#pragma unroll
-  for (int j = 0; j < RB; ++j) {
-    if (j < R) {
-      const double piv = __shfl_sync(0xffffffffu, col[j], j);
-      ok = ok && (piv > 0.0);
-      double fcol[RB];
-#pragma unroll
-      for (int i = 0; i < RB; ++i) fcol[i] = __shfl_sync(0xffffffffu, col[i], j);
-      col[j] = col[j] / piv;
-#pragma unroll
-      for (int i = 0; i < RB; ++i)
-        if (i < R && i != j) col[i] = fma(-fcol[i], col[j], col[i]);
-    }
-  }
-  if (ok && lane >= R && lane < 2 * R)
-#pragma unroll
-    for (int i = 0; i < RB; ++i)
-      if (i < R) Vi[i * R + (lane - R)] = col[i];
-  return ok;
-}
-
 __global__ void als_vinv_kernel(RowsAls a, int mode) {
   const int rep = blockIdx.x;
   if (a.done[rep]) return;

@@ -16,6 +16,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "coo_piece.cuh"
 #include "internal.h"
 
 namespace sbt {
@@ -443,8 +444,6 @@ __global__ void key_ptr_kernel(const uint32_t* __restrict__ keys, int64_t n, int
 // multi-piece rows write partials summed in piece order by a fix-up kernel -> deterministic,
 // no float atomics.
 // ---------------------------------------------------------------------------------------
-constexpr int kPiece = 256;
-constexpr int kShortPiece = 16;   // pieces up to this many entries: lane per component
 
 // every repetition converged: a whole launch of the iteration has nothing to do (one warp vote;
 // r <= 32)
@@ -471,6 +470,20 @@ __global__ void piece_fill_kernel(const int64_t* __restrict__ ptr, const int64_t
       pb[s + k] = ptr[x] + k * kPiece;
       prow[s + k] = (int32_t)x;
     }
+  }
+}
+
+// warp pieces (longer than kShortPiece) and short pieces in two lists (any order: every piece
+// writes its own output), so the persistent ALS can schedule the long ones first
+__global__ void piece_classify_kernel(const int64_t* __restrict__ ptr, const int64_t* __restrict__ pstart,
+                                      const int64_t* __restrict__ pb, const int32_t* __restrict__ prow,
+                                      int64_t nrow, int32_t* __restrict__ plist, unsigned* nlist) {
+  const int64_t P = pstart[nrow];
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const int x = prow[p];
+    const int64_t len = min(pb[p] + kPiece, ptr[x + 1]) - pb[p];
+    if (len > kShortPiece) plist[atomicAdd(nlist, 1u)] = (int32_t)p;
+    else plist[P - 1 - atomicAdd(nlist + 1, 1u)] = (int32_t)p;
   }
 }
 
@@ -501,97 +514,19 @@ __global__ void permute4_kernel(const int32_t* __restrict__ perm, const int32_t*
   }
 }
 
-// One warp per piece: lane l takes entries l, l+32, ... (fp32 products, fp64 per-lane sums),
-// then a fixed butterfly.  (A half-warp-per-entry variant with coalesced row gathers measured
-// slower on C3: fewer entries in flight per warp.)
+// One warp per piece (coo_piece.cuh): grid-stride over the pieces of the mode.
 template <int RB>
 __global__ void coo_mttkrp_piece_kernel(CooAls a, int mode, int64_t npiece_max) {
   const int lane = threadIdx.x & 31;
   if (all_reps_done(a.done, a.r)) return;
-  const CooModePlan& pl = a.plan[mode];
-  const int64_t P = pl.pstart[pl.nrow];
-  const int rows = mode == 0 ? a.nI : mode == 1 ? a.nJ : a.nK;
-  const int R = a.R;
-  const int oa = mode == 0 ? 1 : 0, ob = mode == 2 ? 1 : 2;
-  for (int64_t piece = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; piece < P;
-       piece += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int x = pl.prow[piece];
-    const int rep = x / rows, row = x - rep * rows;
-    if (a.done[rep]) continue;
-    const int64_t b = pl.pb[piece];
-    const int64_t e = min(b + kPiece, pl.ptr[x + 1]);
-    const bool single = pl.pstart[x + 1] - pl.pstart[x] == 1;
-    double* out = single ? a.M[mode] + (int64_t)rep * a.m_stride[mode] + (int64_t)row * R
-                         : pl.partial + piece * R;
-    if (e - b <= kShortPiece) {
-      // short piece (most rows of a sparse summary): lane f < R sums component f over the
-      // entries in order (fp32 products, fp64 sum) -- no butterfly of RB doubles
-      if (lane < R) {
-        const float* Ua = a.U[oa] + rep * a.u_stride[oa];
-        const float* Ub = a.U[ob] + rep * a.u_stride[ob];
-        double s = 0.0;
-        for (int64_t t = b; t < e; ++t) {
-          const float v = pl.sv[t];
-          s += (double)(v * Ua[(int64_t)pl.sa[t] * R + lane] * Ub[(int64_t)pl.sb[t] * R + lane]);
-        }
-        out[lane] = s;
-      }
-      continue;
-    }
-    double acc[RB];
-    if (a.Up[oa]) {
-      // padded factor rows (16 B aligned): vector gathers; fp32 lane runs of <= kPiece / 32
-      // products, fp64 across lanes
-      const float4* Ua = reinterpret_cast<const float4*>(a.Up[oa] + rep * a.up_stride[oa]);
-      const float4* Ub = reinterpret_cast<const float4*>(a.Up[ob] + rep * a.up_stride[ob]);
-      float ac[RB];
-#pragma unroll
-      for (int f = 0; f < RB; ++f) ac[f] = 0.f;
-#pragma unroll 2
-      for (int64_t t = b + lane; t < e; t += 32) {
-        const float v = pl.sv[t];
-        const float4* ra = Ua + (int64_t)pl.sa[t] * (RB / 4);
-        const float4* rb = Ub + (int64_t)pl.sb[t] * (RB / 4);
-#pragma unroll
-        for (int f4 = 0; f4 < RB / 4; ++f4) {
-          const float4 x = __ldg(ra + f4), y = __ldg(rb + f4);
-          ac[4 * f4 + 0] = fmaf(v * x.x, y.x, ac[4 * f4 + 0]);
-          ac[4 * f4 + 1] = fmaf(v * x.y, y.y, ac[4 * f4 + 1]);
-          ac[4 * f4 + 2] = fmaf(v * x.z, y.z, ac[4 * f4 + 2]);
-          ac[4 * f4 + 3] = fmaf(v * x.w, y.w, ac[4 * f4 + 3]);
-        }
-      }
-#pragma unroll
-      for (int f = 0; f < RB; ++f) acc[f] = (double)ac[f];
-    } else {
-      const float* Ua = a.U[oa] + rep * a.u_stride[oa];
-      const float* Ub = a.U[ob] + rep * a.u_stride[ob];
-#pragma unroll
-      for (int f = 0; f < RB; ++f) acc[f] = 0.0;
-#pragma unroll 2
-      for (int64_t t = b + lane; t < e; t += 32) {
-        const float v = pl.sv[t];
-        const float* ra = Ua + (int64_t)pl.sa[t] * R;
-        const float* rb = Ub + (int64_t)pl.sb[t] * R;
-#pragma unroll
-        for (int f = 0; f < RB; ++f)
-          if (f < R) acc[f] += (double)(v * ra[f] * rb[f]);
-      }
-    }
-#pragma unroll
-    for (int f = 0; f < RB; ++f) {
-      double s = acc[f];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      acc[f] = s;
-    }
-    if (lane < R) {
-      double v = 0.0;
-#pragma unroll
-      for (int f = 0; f < RB; ++f)
-        if (f == lane) v = acc[f];
-      out[lane] = v;
-    }
+  const unsigned dm = __ballot_sync(0xffffffffu, lane < a.r && a.done[lane] != 0);
+  const int64_t P = a.plan[mode].pstart[a.plan[mode].nrow];
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (RB <= 16) {   // short pieces two at a time (half-warps)
+    for (int64_t q = w0; 2 * q < P; q += nw) coo_pair_mttkrp<RB>(a, mode, q, P, lane, dm);
+  } else {
+    for (int64_t piece = w0; piece < P; piece += nw) coo_piece_mttkrp<RB>(a, mode, piece, lane, dm);
   }
   (void)npiece_max;
 }
@@ -861,6 +796,12 @@ cudaError_t coo_build_plan(CooModePlan& pl, const int32_t* perm, const int32_t* 
   cudaError_t e = exclusive_scan_i64(cnt, pl.nrow + 1, pl.pstart, sws, st);
   if (e != cudaSuccess) return e;
   piece_fill_kernel<<<grid_for(pl.nrow), kCT, 0, st>>>(pl.ptr, pl.pstart, pl.nrow, pl.pb, pl.prow);
+  if (pl.plist) {
+    e = cudaMemsetAsync(pl.nlist, 0, 2 * sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    piece_classify_kernel<<<grid_for(pl.nrow + pl.n / kPiece + 1), kCT, 0, st>>>(pl.ptr, pl.pstart, pl.pb, pl.prow,
+                                                                                 pl.nrow, pl.plist, pl.nlist);
+  }
   if (perm && n > 0)
     permute3_kernel<<<grid_for(n), kCT, 0, st>>>(perm, ia, ib, v, n, const_cast<int32_t*>(pl.sa),
                                                 const_cast<int32_t*>(pl.sb), const_cast<float*>(pl.sv));
