@@ -34,7 +34,7 @@ namespace {
 
 constexpr int kPT = 256;   // threads per block
 constexpr int kTile = 128; // rows per rows-phase tile (two threads per row)
-constexpr int kPairsPerGrab = 4;   // short-piece pairs a warp takes from the MTTKRP work counter
+constexpr int kPairsPerGrab = 8;   // short-piece pairs a warp takes from the MTTKRP work counter
 
 __device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned target) {
   __syncthreads();
@@ -270,13 +270,10 @@ __global__ void __launch_bounds__(kPT, 4) coo_als_persist_kernel(const __grid_co
         const int64_t P = __ldcg(pa.pstart + pa.nrow);
         const int64_t nlong = __ldcg(pa.nlist), nshort = __ldcg(pa.nlist + 1);
         unsigned* wq = bar + 1 + 6 * it + 2 * m;
-        for (;;) {
-          unsigned q0 = 0;
-          if (lane == 0) q0 = atomicAdd(wq, 1u);
-          q0 = __shfl_sync(0xffffffffu, q0, 0);
-          if ((int64_t)q0 >= nlong) break;
-          coo_piece_mttkrp<RB>(ca, m, pa.plist[q0], lane, done);
-        }
+        // warp pieces round-robin (similar costs, random order: no counter traffic), the short
+        // pieces from a counter in batches
+        const int64_t gw = ((int64_t)blockIdx.x * kPT + tid) >> 5, nw = ((int64_t)gridDim.x * kPT) >> 5;
+        for (int64_t q = gw; q < nlong; q += nw) coo_piece_mttkrp<RB>(ca, m, pa.plist[q], lane, done);
         const int64_t nsp = (nshort + 1) / 2;
         for (;;) {
           unsigned q0 = 0;
