@@ -264,7 +264,11 @@ def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
         # per ALS iteration, 3 mode passes of 16 B (i, j, k, v) per summary nonzero
         nz = statistics.mean(inf["summary_entries"] for inf in infos)
         it = statistics.mean(inf["als_iters_sum"] for inf in infos) / w.r
-        out["a4"] = dict(hbm_line("COO ALS (sort, piece MTTKRP, row solves)", 4, it * 3 * 16.0 * nz),
+        kinds = {inf["als_plan"][0] for inf in infos}
+        kname = ("coo_als_persist_kernel (all iterations, one cooperative launch; sort + piece plan before it)"
+                 if kinds == {3} else "COO ALS per-mode pipeline (piece MTTKRP, row solves)" if kinds == {4}
+                 else f"COO ALS (plan kinds {sorted(kinds)})")
+        out["a4"] = dict(hbm_line(kname, 4, it * 3 * 16.0 * nz),
                          note="algorithmic bytes: iterations x 3 mode passes x 16 B per summary nonzero "
                               "(SURVEY 8(d)); summaries smaller than L2 can exceed the HBM line")
         return out

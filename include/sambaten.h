@@ -137,11 +137,12 @@ typedef struct {
   int als_iters_sum;           /* ALS iterations summed over the repetitions (work accounting) */
   int rep_rank[32];            /* rank each repetition decomposed its summary at (R unless    */
                                /* opts.getrank reduced it, R33); entries >= r are 0           */
-  int als_plan[4];             /* the a4 launch plan this update ran (dense handles):         */
+  int als_plan[4];             /* the a4 launch plan this update ran:                          */
                                /* [0] kind: 0 multi-kernel ALS, 1 cluster ALS (one thread-    */
                                /* block cluster per repetition), 2 grid ALS (CTA groups of one */
-                               /* cooperative grid, global-memory exchange), -1 none (COO /   */
-                               /* GetRank);                                                   */
+                               /* cooperative grid, global-memory exchange), COO handles: 3   */
+                               /* persistent cooperative ALS (k_coo_als.cu), 4 per-mode kernel */
+                               /* pipeline (R > 16 / SAMBATEN_COO_ALS_MULTI); -1 none (GetRank)*/
                                /* [1] CTAs per repetition, [2] RB (padded rank width),        */
                                /* [3] 1 if D lives in shared memory, 0 if in global memory     */
   int64_t summary_entries;     /* entries (dense) or nonzeros (COO) of the summaries this      */

@@ -977,6 +977,9 @@ static int* pinned_done_flags() {
 
 static int bits_for(int64_t n) { int b = 1; while (((int64_t)1 << b) < n) ++b; return b; }
 
+// which batched COO ALS the last coo_als call ran (sambaten_info.als_plan[0]: 3 persistent, 4 per mode)
+static thread_local int g_coo_als_kind = -1;
+
 // the model rows a warm-started summary ALS begins from (R34): A(I_s), B(J_s), C(K_s) diag(lambda)
 struct WarmRows {
   const float *A, *B, *C, *lam;
@@ -1115,6 +1118,7 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
       // every iteration in one persistent cooperative kernel (k_coo_als.cu)
       e = launch_coo_als_persist(a, ra, gbar, st);
       *launches = 2 * 3 + 9 + 3 + 3 + 3 + 1;
+      g_coo_als_kind = 3;
     } else {
       // the per-mode pipeline: the stop test runs on the device; the host looks at the done
       // flags after iterations 3, 6, 10, 15, ... (one small read each) and stops launching once
@@ -1138,6 +1142,7 @@ static sambaten_status coo_als(DevBuf& wsbuf, cudaStream_t st, int R, const int3
         }
       }
       *launches = 2 * 3 + 9 + 3 + 3 + 3 + (rows ? 16 : 6) * nit;
+      g_coo_als_kind = 4;
     }
     if (e != cudaSuccess) {
       set_error(std::string("COO ALS: ") + cudaGetErrorString(e));
@@ -1322,6 +1327,7 @@ static sambaten_status update_coo(sambaten_t h, const sambaten_tensor* batch, fl
                                   h->opts.als_tol, true, &a, &als_launches, 0, 1,
                                   h->opts.warm_start ? &wr : nullptr))
     return e;
+  h->als_plan[0] = g_coo_als_kind; h->als_plan[1] = 0; h->als_plan[2] = R; h->als_plan[3] = 0;
   if (d_rnew) {
     // the repetitions GetRank reduced: decomposed alone at R_new (Philox rep s, as in the batch)
     // and written, zero-padded to R columns, over their batch result (R33)

@@ -472,7 +472,7 @@ size_t coo_als_persist_part_doubles(int maxn, int R, int r) {
 }
 
 bool coo_als_persist_supported(int R) {
-  static const bool off = getenv("SAMBATEN_COO_ALS_MULTI") != nullptr;   // the per-mode pipeline
+  const bool off = getenv("SAMBATEN_COO_ALS_MULTI") != nullptr;   // the per-mode pipeline (read per call)
   return !off && R <= 16;
 }
 

@@ -213,3 +213,20 @@ def test_fit_coo_and_cp_als_coo():
     assert abs(float(host(fit)[0]) - fo) <= 1e-3
     g = (host(lamd), *[host(u).astype(np.float64) for u in Ud])
     assert O.fms(g, (lo, *Uo)) >= 0.99
+
+
+def test_coo_update_persistent_als_matches_oracle_and_pipeline(monkeypatch):
+    """The persistent cooperative COO ALS (als_plan kind 3, k_coo_als.cu) against the oracle on a
+    Zipf-hot stream whose rows span several MTTKRP pieces (rows > 256 entries: multi-piece
+    partials), and against the per-mode kernel pipeline (kind 4) on the same input."""
+    X, truth = zipf_planted_coo(300, 250, 60, 6, 120_000, alpha=1.5, seed=11)
+    res = _run(X, truth, 50, 5, R=6, s=2, r=4, maxit=25, nb=2, tau=0.0)
+    for fms, rel_g, rel_o, gr, orr, info in res:
+        assert info.als_plan[0] == 3, list(info.als_plan)
+        assert fms >= 0.99, fms
+        assert abs(rel_g - rel_o) <= 1e-3, (rel_g, rel_o)
+    monkeypatch.setenv("SAMBATEN_COO_ALS_MULTI", "1")
+    res_m = _run(X, truth, 50, 5, R=6, s=2, r=4, maxit=25, nb=2, tau=0.0)
+    for (fms, rel_g, _, _, _, _), (fms_m, rel_m, _, _, _, info_m) in zip(res, res_m):
+        assert info_m.als_plan[0] == 4, list(info_m.als_plan)
+        assert abs(rel_g - rel_m) <= 1e-4, (rel_g, rel_m)
