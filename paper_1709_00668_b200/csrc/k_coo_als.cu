@@ -56,22 +56,31 @@ __device__ __forceinline__ void grid_sync(unsigned* ctr, unsigned target) {
 
 __device__ __forceinline__ int mode_rows(const RowsAls& ra, int m) { return m == 0 ? ra.nI : m == 1 ? ra.nJ : ra.nK; }
 
-// nitems sums over the ntile tile partials at addr(i) + t * stride: thread per item, tiles in
-// order, loads issued eight at a time (the sums are latency-bound chains of L2 reads).  Used for
-// both the leader's Gram and every block's lambda, so the two agree bit for bit.
+// nitems sums over the ntile tile partials at addr(i) + t * stride: two consecutive threads per
+// item, thread j summing its half of the tiles in order (loads issued 16 at a time: the sums
+// are latency-bound chains of L2 reads), the halves added by one shuffle (a + b on both lanes).
+// Used for both the leader's Gram and every block's lambda, so the two agree bit for bit.
 template <class Addr, class Out>
 __device__ __forceinline__ void tile_sums(int nitems, int ntile, int64_t stride, Addr addr, Out out) {
-  for (int i = threadIdx.x; i < nitems; i += blockDim.x) {
-    const double* p = addr(i);
+  const int half = (ntile + 1) / 2;
+  const int nrounds = (2 * nitems + blockDim.x - 1) / blockDim.x;
+  for (int rd = 0; rd < nrounds; ++rd) {   // uniform trip count: every lane reaches the shuffle
+    const int slot = rd * blockDim.x + threadIdx.x;
+    const int i = slot >> 1, j = slot & 1;
     double s = 0.0;
-    for (int t0 = 0; t0 < ntile; t0 += 8) {
-      double v[8];
+    if (i < nitems) {
+      const double* p = addr(i);
+      const int t1 = min(ntile, (j + 1) * half);
+      for (int t0 = j * half; t0 < t1; t0 += 16) {
+        double v[16];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = t0 + q < ntile ? __ldcg(p + (int64_t)(t0 + q) * stride) : 0.0;
+        for (int q = 0; q < 16; ++q) v[q] = t0 + q < t1 ? __ldcg(p + (int64_t)(t0 + q) * stride) : 0.0;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) s += v[q];
+        for (int q = 0; q < 16; ++q) s += v[q];
+      }
     }
-    out(i, s);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (i < nitems && j == 0) out(i, s);
   }
 }
 
@@ -183,6 +192,7 @@ __global__ void __launch_bounds__(kPT, 4) coo_als_persist_kernel(const __grid_co
   extern __shared__ __align__(16) double sh[];   // rows phase: xs[kPT][RB + 1]; leader scratch
   __shared__ double s_lam[kMaxReps * RB];
   __shared__ double s_vi[RB * RB];
+  __shared__ int64_t s_ps[kTile + 1];   // piece starts of a rows-phase tile
   __shared__ unsigned s_done;
   __shared__ CooAls ca;    // the parameter structs in shared memory: the mode index is dynamic
   __shared__ RowsAls ra;
@@ -212,6 +222,18 @@ __global__ void __launch_bounds__(kPT, 4) coo_als_persist_kernel(const __grid_co
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         atomicMax(prof + 16 + k, t - tstart);
         atomicMin(prof + 20 + k, t - tstart);
+      }
+    }
+  };
+  // B sub-steps (profiling): max over units of the time from the unit's start to each mark
+  unsigned long long tu = 0;
+  auto umark = [&](int k) {
+    if (prof) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (k < 0) tu = t; else atomicMax(prof + 24 + k, t - tu);
       }
     }
   };
@@ -306,28 +328,47 @@ __global__ void __launch_bounds__(kPT, 4) coo_als_persist_kernel(const __grid_co
         double* ms = sh;                       // [kTile][RB + 1]: m rows
         double* xs = sh + kTile * (RB + 1);    // [kTile][RB + 1]: x rows, then <x, m> in column RB
         // stage the tile's M rows, element-parallel (coalesced; a multi-piece row's piece
-        // partials summed in piece order)
-#pragma unroll 4
-        for (int e = tid; e < nr * R; e += kPT) {
-          const int rl = e / R, f = e - rl * R;
-          const int64_t xrow = (int64_t)rep * n + row0 + rl;
-          const int64_t ps = __ldg(pl.pstart + xrow), np = __ldg(pl.pstart + xrow + 1) - ps;
-          double v;
-          if (np == 1) {
-            v = __ldcg(ra.M[m] + rep * ra.m_stride[m] + (int64_t)(row0 + rl) * R + f);
-          } else {
-            v = 0.0;   // the piece partials in order, loads eight at a time
-            for (int64_t k0 = 0; k0 < np; k0 += 8) {
-              double w[8];
+        // partials summed in piece order): the rows' piece starts first, then every element's
+        // load at once
+        umark(-1);
+        for (int t = tid; t <= nr; t += kPT) s_ps[t] = __ldg(pl.pstart + (int64_t)rep * n + row0 + t);
+        __syncthreads();
+        {
+          constexpr int kEl = (kTile * RB + kPT - 1) / kPT;
+          const double* Mt = ra.M[m] + rep * ra.m_stride[m] + (int64_t)row0 * R;
+          double w[kEl];
 #pragma unroll
-              for (int q = 0; q < 8; ++q) w[q] = k0 + q < np ? __ldcg(pl.partial + (ps + k0 + q) * R + f) : 0.0;
-#pragma unroll
-              for (int q = 0; q < 8; ++q) v += w[q];
+          for (int q = 0; q < kEl; ++q) {
+            const int e = tid + q * kPT;
+            w[q] = 0.0;
+            if (e < nr * R) {
+              const int rl = e / R;
+              if (s_ps[rl + 1] - s_ps[rl] == 1) w[q] = __ldcg(Mt + e);
             }
           }
-          ms[rl * (RB + 1) + f] = v;
+#pragma unroll
+          for (int q = 0; q < kEl; ++q) {
+            const int e = tid + q * kPT;
+            if (e < nr * R) {
+              const int rl = e / R, f = e - rl * R;
+              const int64_t ps = s_ps[rl], np = s_ps[rl + 1] - ps;
+              double v = w[q];
+              if (np != 1) {
+                v = 0.0;   // the piece partials in order, loads eight at a time
+                for (int64_t k0 = 0; k0 < np; k0 += 8) {
+                  double wp[8];
+#pragma unroll
+                  for (int k = 0; k < 8; ++k) wp[k] = k0 + k < np ? __ldcg(pl.partial + (ps + k0 + k) * R + f) : 0.0;
+#pragma unroll
+                  for (int k = 0; k < 8; ++k) v += wp[k];
+                }
+              }
+              ms[rl * (RB + 1) + f] = v;
+            }
+          }
         }
         __syncthreads();
+        umark(0);
         // x = m Vi: two threads per row, each half of the components (g outer: RB / 2
         // independent chains, each in g order)
         {
@@ -362,6 +403,7 @@ __global__ void __launch_bounds__(kPT, 4) coo_als_persist_kernel(const __grid_co
           X[(int64_t)row0 * R + e] = xs[rl * (RB + 1) + f];
         }
         __syncthreads();
+        umark(1);
         double* part = ra.part + ((int64_t)rep * ntile + tile) * (npair + 1);
         for (int pr = tid; pr <= npair; pr += kPT) {
           double s = 0.0;
@@ -383,6 +425,7 @@ __global__ void __launch_bounds__(kPT, 4) coo_als_persist_kernel(const __grid_co
           part[pr] = s;
         }
         __syncthreads();
+        umark(2);
       }
       arrive(1);
       gsync();
@@ -482,10 +525,11 @@ cudaError_t launch_coo_als_persist(const CooAls& ca, const RowsAls& ra, unsigned
   int blocks = 0;
   static unsigned long long* prof = nullptr;
   static const bool want_prof = getenv("SAMBATEN_COO_ALS_PROFILE") != nullptr;
-  if (want_prof && !prof && cudaMalloc(&prof, 24 * sizeof(unsigned long long)) != cudaSuccess) prof = nullptr;
+  if (want_prof && !prof && cudaMalloc(&prof, 28 * sizeof(unsigned long long)) != cudaSuccess) prof = nullptr;
   if (prof) {
     cudaMemsetAsync(prof, 0, 20 * sizeof(unsigned long long), st);
     cudaMemsetAsync(prof + 20, 0xff, 4 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(prof + 24, 0, 4 * sizeof(unsigned long long), st);
   }
   cudaError_t e;
   switch (ca.RB) {
@@ -496,13 +540,15 @@ cudaError_t launch_coo_als_persist(const CooAls& ca, const RowsAls& ra, unsigned
     default: return cudaErrorInvalidValue;
   }
   if (prof && e == cudaSuccess) {
-    unsigned long long h[24];
+    unsigned long long h[28];
     e = cudaMemcpyAsync(h, prof, sizeof(h), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     fprintf(stderr, "[coo_als_persist] blocks %d  us: A(mttkrp) %.1f/%llu  B(rows) %.1f/%llu  C(reduce+scale) %.1f/%llu  prologue %.1f\n",
             blocks, h[0] * 1e-3, h[4], h[1] * 1e-3, h[5], h[2] * 1e-3, h[6], h[3] * 1e-3);
     fprintf(stderr, "[coo_als_persist] block arrival (sum over phases) us: A max %.1f min %.1f  B max %.1f min %.1f  C max %.1f min %.1f\n",
             h[8] * 1e-3, h[12] * 1e-3, h[9] * 1e-3, h[13] * 1e-3, h[10] * 1e-3, h[14] * 1e-3);
+    fprintf(stderr, "[coo_als_persist] rows unit (max over all units) us: staged %.1f  x %.1f  gram %.1f\n",
+            h[24] * 1e-3, h[25] * 1e-3, h[26] * 1e-3);
   }
   return e;
 }
