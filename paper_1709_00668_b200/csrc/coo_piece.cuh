@@ -43,8 +43,8 @@ __device__ __forceinline__ void coo_piece_mttkrp(const CooAls& a, int mode, int6
       const float* Ub = a.U[ob] + rep * a.u_stride[ob];
       double s = 0.0;
       for (int64_t t = b; t < e; ++t) {
-        const float v = pl.sv[t];
-        s += (double)(v * Ua[(int64_t)pl.sa[t] * R + lane] * Ub[(int64_t)pl.sb[t] * R + lane]);
+        const float v = __ldcs(pl.sv + t);
+        s += (double)(v * Ua[(int64_t)__ldcs(pl.sa + t) * R + lane] * Ub[(int64_t)__ldcs(pl.sb + t) * R + lane]);
       }
       out[lane] = s;
     }
@@ -60,9 +60,9 @@ __device__ __forceinline__ void coo_piece_mttkrp(const CooAls& a, int mode, int6
     for (int f = 0; f < RB; ++f) ac[f] = 0.f;
 #pragma unroll 2
     for (int64_t t = b + lane; t < e; t += 32) {
-      const float v = pl.sv[t];
-      const float4* ra = Ua + (int64_t)pl.sa[t] * (RB / 4);
-      const float4* rb = Ub + (int64_t)pl.sb[t] * (RB / 4);
+      const float v = __ldcs(pl.sv + t);
+      const float4* ra = Ua + (int64_t)__ldcs(pl.sa + t) * (RB / 4);
+      const float4* rb = Ub + (int64_t)__ldcs(pl.sb + t) * (RB / 4);
 #pragma unroll
       for (int f4 = 0; f4 < RB / 4; ++f4) {
         const float4 xa = ra[f4], yb = rb[f4];
@@ -91,9 +91,9 @@ __device__ __forceinline__ void coo_piece_mttkrp(const CooAls& a, int mode, int6
     for (int f = 0; f < RB; ++f) acc[f] = 0.0;
 #pragma unroll 2
     for (int64_t t = b + lane; t < e; t += 32) {
-      const float v = pl.sv[t];
-      const float* ra = Ua + (int64_t)pl.sa[t] * R;
-      const float* rb = Ub + (int64_t)pl.sb[t] * R;
+      const float v = __ldcs(pl.sv + t);
+      const float* ra = Ua + (int64_t)__ldcs(pl.sa + t) * R;
+      const float* rb = Ub + (int64_t)__ldcs(pl.sb + t) * R;
 #pragma unroll
       for (int f = 0; f < RB; ++f)
         if (f < R) acc[f] += (double)(v * ra[f] * rb[f]);
@@ -144,14 +144,14 @@ __device__ __forceinline__ void coo_short_half(const CooAls& a, int mode, int64_
     float v[4], ua[4], ub[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      v[q] = pl.sv[t + q];
-      ua[q] = Ua[(int64_t)pl.sa[t + q] * rs];
-      ub[q] = Ub[(int64_t)pl.sb[t + q] * rs];
+      v[q] = __ldcs(pl.sv + t + q);
+      ua[q] = Ua[(int64_t)__ldcs(pl.sa + t + q) * rs];
+      ub[q] = Ub[(int64_t)__ldcs(pl.sb + t + q) * rs];
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) s += (double)(v[q] * ua[q] * ub[q]);
   }
-  for (; t < e; ++t) s += (double)(pl.sv[t] * Ua[(int64_t)pl.sa[t] * rs] * Ub[(int64_t)pl.sb[t] * rs]);
+  for (; t < e; ++t) s += (double)(__ldcs(pl.sv + t) * Ua[(int64_t)__ldcs(pl.sa + t) * rs] * Ub[(int64_t)__ldcs(pl.sb + t) * rs]);
   out[hl] = s;
 }
 
