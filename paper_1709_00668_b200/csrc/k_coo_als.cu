@@ -187,7 +187,7 @@ __device__ void leader_reduce(const RowsAls& ra, int rep, int m, double* sh, boo
 }
 
 template <int RB>
-__global__ void __launch_bounds__(kPT, 4) coo_als_persist_kernel(const __grid_constant__ CooAls ca_p, const __grid_constant__ RowsAls ra_p, unsigned* bar,
+__global__ void __launch_bounds__(kPT, 3) coo_als_persist_kernel(const __grid_constant__ CooAls ca_p, const __grid_constant__ RowsAls ra_p, unsigned* bar,
                                                                 unsigned long long* prof) {
   extern __shared__ __align__(16) double sh[];   // rows phase: xs[kPT][RB + 1]; leader scratch
   __shared__ double s_lam[kMaxReps * RB];
@@ -484,7 +484,7 @@ cudaError_t launch_rb(const CooAls& ca, const RowsAls& ra, unsigned* bar, cudaSt
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_als_persist_kernel<RB>, kPT, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  static const int cap = [] { const char* v = getenv("SAMBATEN_COO_ALS_BPS"); return v ? atoi(v) : 4; }();
+  static const int cap = [] { const char* v = getenv("SAMBATEN_COO_ALS_BPS"); return v ? atoi(v) : 3; }();
   per_sm = std::min(per_sm, std::max(cap, 1));
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
