@@ -296,16 +296,21 @@ def kernel_rooflines(w, work, infos, peaks, peak_kind, G, k_local, args):
     out["a3"] = hbm_line("gather_dense_kernel", 3, 8.0 * rl * Ymean)
     it = statistics.mean(inf["als_iters_sum"] for inf in infos) / G
     t4 = ms(4)
+    kinds = {inf["als_plan"][0] for inf in infos}
+    a4name = {frozenset({1}): "als_cluster_kernel (cluster plan: one thread-block cluster per repetition)",
+              frozenset({2}): "als_cluster_kernel (grid plan: CTA groups of one cooperative grid)",
+              frozenset({0}): "multi-kernel ALS (mttkrp0 / dpass / solve kernels)"}.get(
+                  frozenset(kinds), f"dense ALS (plan kinds {sorted(kinds)})")
     if rl * Ymean * 8.0 <= L2_RESIDENT_BYTES:     # Y and its transpose stay in L2: fp32 FMA bound
         fl = it * 2 * Ymean * 2 * w.R
         ach = fl / (t4 / 1e3) / 1e12
-        out["a4"] = {"kernel": "als_cluster_kernel", "bound": "alu", "achieved": ach,
+        out["a4"] = {"kernel": a4name, "bound": "alu", "achieved": ach,
                      "peak": FP32_PEAK_TFLOPS, "peak_kind": "derived (148 SMs x 128 FP32 lanes x 2 x 1.965 GHz)",
                      "unit": "TFLOP/s", "frac": ach / FP32_PEAK_TFLOPS, "traffic": traffic.get("a4"),
                      "flops_per_launch": fl, "ms_per_launch": t4,
                      "note": "summaries L2-resident (SURVEY 8(d)): HBM fraction not meaningful"}
     else:
-        out["a4"] = hbm_line("als_cluster_kernel", 4, it * 2 * Ymean * 4.0)
+        out["a4"] = hbm_line(a4name, 4, it * 2 * Ymean * 4.0)
     return out
 
 
@@ -605,9 +610,14 @@ def main():
             L.sambaten_destroy(init_single(L, work, w, opts, config))
         k0b, k0n = partition(w.K0, world, rank)
         if device_gen:
-            x0buf = torch.empty((k0n, w.J, w.I), dtype=torch.float32, device="cuda")
-            work.gen(x0buf, k0b, k0n)
-            X0 = L.dense(x0buf)
+            # the slab generated in place in a buffer with room for this rank's share of the
+            # stream (Kcap_local slices), used as the local store (opts.borrow_store, no copy)
+            kcap_local = k0n + -(-(w.K - w.K0) // world) + 1
+            work.x0buf = torch.empty((kcap_local, w.J, w.I), dtype=torch.float32, device="cuda")
+            work.gen(work.x0buf[:k0n], k0b, k0n)
+            X0 = L.dense(work.x0buf[:k0n])
+            opts.borrow_store = 1
+            config["store"] = "caller buffer (opts.borrow_store), the rank's slab generated in place on the device"
         else:
             X0 = work.tensor(L, slab_of(work.X0, k0b, k0n, work.coo), device=True)
         dd = L.make_dist(rank, world, nid, k0b, w.K0)

@@ -93,10 +93,12 @@ typedef struct {
   int init_max_iters;     /* sambaten_init: ALS iterations on X0 (default 1000)       */
   double init_tol;        /* sambaten_init: tolerance (default 1e-6)                         */
   void* stream;           /* cudaStream_t for all work of this handle; NULL = default       */
-  int borrow_store;       /* dense, single-GPU init only: X0->vals is a DEVICE buffer with    */
-                          /* room for `capacity` slices (I % 4 == 0); the handle uses it as   */
-                          /* its tensor store in place (no copy of X0).  The caller keeps it  */
-                          /* alive and unmodified until sambaten_destroy.  Default 0 (copy).  */
+  int borrow_store;       /* dense init only: X0->vals is a DEVICE buffer with room for       */
+                          /* `capacity` slices (I % 4 == 0); the handle uses it as its tensor */
+                          /* store in place (no copy of X0).  sambaten_init_factors_dist: the */
+                          /* rank's slab buffer holds Kcap_local = K0_local + ceil((capacity -*/
+                          /* K0_global) / world) + 1 slices.  The caller keeps it alive and   */
+                          /* unmodified until sambaten_destroy.  Default 0 (copy).            */
   int incremental_marginals; /* 1: a1 adds the batch's contribution to the marginals kept from */
                           /* the previous update instead of re-reading the whole tensor --    */
                           /* bit-identical (integer sums); the first     */

@@ -33,7 +33,7 @@ def _samples(h, r):
     return Is.reshape(r, -1), Js.reshape(r, -1), Ks.reshape(r, -1)
 
 
-def _run(X, truth, K0, batch, R, s, r, maxit, tol=0.0, seed=7, nb=None, tau=0.9, warm=False):
+def _run(X, truth, K0, batch, R, s, r, maxit, tol=0.0, seed=7, nb=None, tau=0.9, warm=False, models=None):
     X0, batches = split_coo(X, K0, batch)
     if nb is not None:
         batches = batches[:nb]
@@ -64,6 +64,8 @@ def _run(X, truth, K0, batch, R, s, r, maxit, tol=0.0, seed=7, nb=None, tau=0.9,
             rel_g = O.relative_error(st.X, *g64)
             gpu_rej = [i for i in range(r) if info.reps_rejected_mask >> i & 1]
             out.append((fms, rel_g, rel_o, gpu_rej, oinfo["rejected"], info))
+            if models is not None:
+                models.append((gl.copy(), gA.copy(), gB.copy(), gC.copy()))
             # continue both sides from the GPU model
             st.lam, st.A, st.B, st.C = g64
     finally:
@@ -230,3 +232,22 @@ def test_coo_update_persistent_als_matches_oracle_and_pipeline(monkeypatch):
     for (fms, rel_g, _, _, _, _), (fms_m, rel_m, _, _, _, info_m) in zip(res, res_m):
         assert info_m.als_plan[0] == 4, list(info_m.als_plan)
         assert abs(rel_g - rel_m) <= 1e-4, (rel_g, rel_m)
+
+
+def test_coo_radix_scatter_tile_local_bit_identical(monkeypatch):
+    """The summaries' stable radix sort (k_coo.cu) with the tile ordered by digit in shared memory
+    before its runs are written (SAMBATEN_RADIX_LOCAL) gives the same permutation as the default
+    per-element scatter: the updated models are bit-identical, at a size whose summaries span
+    many 4096-entry tiles with a ragged last tile (two 8-bit passes of the (rep, index) keys)."""
+    X, truth = zipf_planted_coo(3000, 700, 60, 5, 300_001, alpha=1.3, seed=5)
+    ma, mb = [], []
+    ra = _run(X, truth, 50, 5, R=5, s=2, r=4, maxit=6, nb=2, tau=0.0, models=ma)
+    monkeypatch.setenv("SAMBATEN_RADIX_LOCAL", "1")
+    rb = _run(X, truth, 50, 5, R=5, s=2, r=4, maxit=6, nb=2, tau=0.0, models=mb)
+    assert len(ma) == len(mb) == 2
+    for x, y in zip(ma, mb):
+        for u, v in zip(x, y):
+            assert np.array_equal(u, v)
+    for (fms, rel_g, rel_o, _, _, _) in ra:
+        assert fms >= 0.99, fms
+        assert abs(rel_g - rel_o) <= 1e-3, (rel_g, rel_o)

@@ -26,8 +26,19 @@ import os
 opts = L.default_opts(als_max_iters=15, als_tol=0.0, capacity=K, full_fit=int(os.environ.get("SBT_T_FF", "1")),
                       warm_start=int(os.environ.get("SBT_T_WARM", "0")), getrank=int(os.environ.get("SBT_T_GR", "0")))
 dist = L.make_dist(0, 1, L.sambaten_dist_unique_id(), 0, K0)
-hd = L.sambaten_init_factors_dist(L.dense(torch.from_numpy(T0).cuda()), dist, R, 2, 4, 9,
-                                  model[1], model[2], model[3], model[0], opts)
+if os.environ.get("SBT_T_BORROW") == "1":
+    # opts.borrow_store on the sharded handle: the slab in place in a caller buffer of Kcap_local =
+    # K0 + ceil((capacity - K0) / world) + 1 slices whose unused slices hold NaN (never read)
+    od = L.default_opts(als_max_iters=15, als_tol=0.0, capacity=K, full_fit=int(os.environ.get("SBT_T_FF", "1")),
+                        warm_start=int(os.environ.get("SBT_T_WARM", "0")), getrank=int(os.environ.get("SBT_T_GR", "0")),
+                        borrow_store=1)
+    xbuf = torch.full((K0 + (K - K0) + 1, J, I), float("nan"), device="cuda")
+    xbuf[:K0] = torch.from_numpy(T0).cuda()
+    hd = L.sambaten_init_factors_dist(L.dense(xbuf[:K0]), dist, R, 2, 4, 9, model[1], model[2], model[3],
+                                      model[0], od)
+else:
+    hd = L.sambaten_init_factors_dist(L.dense(torch.from_numpy(T0).cuda()), dist, R, 2, 4, 9,
+                                      model[1], model[2], model[3], model[0], opts)
 hs = L.sambaten_init_factors(L.dense(torch.from_numpy(T0).cuda()), R, 2, 4, 9,
                              model[1], model[2], model[3], model[0], opts)
 Kt = K0
@@ -53,12 +64,15 @@ print("DIST_OK")
 '''
 
 
-@pytest.mark.parametrize("loopback,ff,warm,gr", [(False, 1, 0, 0), (True, 1, 0, 0), (False, 2, 0, 0), (True, 2, 1, 0),
-                                                  (True, 1, 0, 1)])
-def test_world1_dist_handle_matches_single_gpu_bitwise(loopback, ff, warm, gr):
-    """full_fit = 2 (lag-1 fit in the a1 pass) and the warm start (R34)
-    on the sharded handle: bit-identical to the single-GPU handle with the same options."""
+@pytest.mark.parametrize("loopback,ff,warm,gr,borrow", [(False, 1, 0, 0, 0), (True, 1, 0, 0, 0), (False, 2, 0, 0, 0),
+                                                         (True, 2, 1, 0, 0), (True, 1, 0, 1, 0), (False, 1, 1, 0, 1),
+                                                         (True, 2, 0, 0, 1)])
+def test_world1_dist_handle_matches_single_gpu_bitwise(loopback, ff, warm, gr, borrow):
+    """full_fit = 2 (lag-1 fit in the a1 pass), the warm start (R34) and
+    opts.borrow_store (the slab used in place) on the sharded handle: bit-identical to the
+    single-GPU handle with the same options."""
     env = dict(os.environ)
+    env["SBT_T_BORROW"] = str(borrow)
     env.pop("SAMBATEN_DIST_LOOPBACK", None)
     if loopback:
         env["SAMBATEN_DIST_LOOPBACK"] = "1"
