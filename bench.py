@@ -56,10 +56,12 @@ def parse():
     p.add_argument("--no-variant", action="store_true", help="skip the incremental-marginals variant run")
     p.add_argument("--no-getrank", action="store_true", help="skip the GetRank timing (SURVEY 8(f) NEXT #2)")
     p.add_argument("--no-full-fit", action="store_true", help="return the summary fit only (R21)")
-    p.add_argument("--full-fit", type=int, default=1, choices=[1, 2],
-                   help="1 (default): the committed model's fit (dense: incremental -- the batch plus the "
-                        "rows the merge changed, k_fitinc.cu); 2: lag-1 fit inside the next update's a1 pass "
-                        "(SURVEY 8(f) NEXT #1; dense only, COO configs use 1)")
+    p.add_argument("--full-fit", type=int, default=None, choices=[1, 2],
+                   help="1 (single-GPU default): the committed model's fit (dense: incremental -- the batch "
+                        "plus the rows the merge changed, k_fitinc.cu); 2 (sharded dense default: the sharded "
+                        "handle has no incremental fit, so its exact fit would be a second pass over the slab): "
+                        "lag-1 fit inside the next update's a1 pass (SURVEY 8(f) NEXT #1; dense only, COO "
+                        "configs use 1)")
     p.add_argument("--no-recompute", action="store_true", help="skip the CP_ALS recompute / relative fitness report")
     p.add_argument("--recompute-iters", type=int, default=150, help="CP_ALS baseline iteration cap (P:441 uses 1000)")
     p.add_argument("--sharded", action="store_true",
@@ -586,7 +588,8 @@ def main():
     warm, tau = method_settings(w, args)
     config["accept_tau"] = tau
     config["als_init"] = "warm (model rows, R34)" if warm else "cold (Philox point, P:213)"
-    ff = 0 if args.no_full_fit else (args.full_fit if not work.coo else 1)
+    ff_default = 2 if sharded else 1
+    ff = 0 if args.no_full_fit else ((args.full_fit or ff_default) if not work.coo else 1)
     config["full_fit"] = {0: "none (summary fit only)",
                           1: "the committed model's exact fit (dense: incremental from the previous model's "
                              "per-component inner products -- the batch's slices plus the rows the merge changed; "
